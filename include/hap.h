@@ -1,0 +1,165 @@
+/*
+ * hap.h — C ABI of libhap.so, the B200 (sm_100a) implementation of the hot path of the
+ * Householder-aligned permutation test (Kato et al., arXiv 2605.08048).
+ *
+ * Citations: "PAPER.md:L" = line L of the paper's LaTeX source (section / equation /
+ * algorithm named alongside); "DESIGN.md Rk" = reading k recorded in DESIGN.md where the
+ * paper is silent.
+ *
+ * Conventions (all entry points):
+ *  - Plain C types only.  `stream` is a cudaStream_t passed as void* (NULL = legacy
+ *    default stream).  Every call validates its arguments on the host, enqueues its work
+ *    on `stream` and returns without synchronising.
+ *  - Pointers marked [device] must be device (or managed) memory, [host] host memory,
+ *    [any] either (host memory is copied in on `stream` by the library).  The caller owns
+ *    every pointer it passes; the library owns only its context workspace.
+ *  - Errors: argument / shape errors are returned synchronously as hap_status; data
+ *    errors found on the device (ZeroVector, DegenerateMean) are written to the device
+ *    hap_align_info.status, make every later kernel of that test a no-op, and are
+ *    returned by hap_sync().  No C++ exception crosses the ABI.  hap_last_error() gives
+ *    a message for the last non-OK status of a context.
+ *  - A context is bound to one device and is not thread-safe; use one per host thread.
+ *  - Requires sm_100 (B200).  There is no CPU fallback: hap_create fails with
+ *    HAP_E_UNSUPPORTED_ARCH elsewhere.
+ */
+#ifndef HAP_H
+#define HAP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HAP_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define HAP_API __attribute__((visibility("default")))
+#else
+#define HAP_API
+#endif
+
+typedef struct hap_ctx_s* hap_ctx;
+
+typedef enum {
+    HAP_OK = 0,
+    HAP_E_INVALID_ARG = 1,
+    HAP_E_DIM_MISMATCH = 2,
+    HAP_E_ZERO_VECTOR = 3,      /* a raw row has ||h|| < 1e-12 (R3) */
+    HAP_E_DEGENERATE_MEAN = 4,  /* ||xbar|| or ||ybar|| < 1e-12 (R3) */
+    HAP_E_MIXED_SHAPES = 5,
+    HAP_E_OOM = 6,
+    HAP_E_CUDA = 7,
+    HAP_E_UNSUPPORTED_ARCH = 8, /* device is not sm_100 */
+    HAP_E_NOT_ALIGNED = 9       /* hap_permtest before any successful hap_align */
+} hap_status;
+
+typedef enum {
+    HAP_ALIGN_HOUSEHOLDER = 0, /* x' = x - 2u(u^T x) on X */
+    HAP_ALIGN_NONE = 1         /* naive baseline: pool the normalised clouds unreflected */
+} hap_align_mode;
+
+/* Result of hap_align, written to DEVICE memory (sizeof(hap_align_info) bytes, 8-byte
+ * aligned) so that hap_permtest can consume it without a host round trip. */
+typedef struct {
+    int64_t n_x, n_y, d;      /* n, m, d of PAPER.md:121-128 */
+    int64_t n_pad, d_pad;     /* padded GEMM extents (K = n_pad rows, d_pad columns) */
+    int32_t is_identity;      /* 1 if ||mu_x - mu_y|| < 1e-9 (no reflection; R3) or mode NONE */
+    int32_t status;           /* hap_status of the device-side data checks */
+    int64_t bad_row;          /* pooled row index of a ZeroVector error, else -1 */
+    double norm_xbar;         /* ||xbar|| = r(X) = r(X') in fp64 (Eq. 8) */
+    double norm_ybar;         /* ||ybar|| = r(Y) */
+    double r_x, r_y;          /* MRLs of the observed split through the mask-GEMM path (D7) */
+    double logk_x, logk_y;    /* L(r) = log kappa-hat(r) = -log v (Eq. 9; R1) */
+    double t_obs;             /* T_obs = log v(X') - log v(Y) = logk_y - logk_x (Eq. 10) */
+} hap_align_info;
+
+/* One test's permutation configuration (PERM-SPEC v1, R6). */
+typedef struct {
+    uint64_t seed;      /* Philox key = (lo32(seed), hi32(seed)) */
+    uint64_t B;         /* permutations of the whole test (informational; p uses it) */
+    uint64_t b_begin;   /* this call's shard [b_begin, b_end) of [0, B); b < 2^32 */
+    uint64_t b_end;
+    uint32_t stream_id; /* s: third Philox counter word (pair id by default) */
+    uint32_t block;     /* B0 permutations per generator/GEMM block; perf only, 0 = auto */
+    double tie_rel;     /* tie band tau = tie_rel * (|logk_x| + |logk_y|) (R8); <= 0 -> 1e-6 */
+    uint32_t flags;     /* reserved, 0 */
+    uint32_t reserved;
+} hap_perm_cfg;
+
+/* Exceedance counters of one test, DEVICE memory, ADDED into (caller zeroes them), so
+ * shards and resumed ranges compose by summation (Eq. pvalue). */
+typedef struct {
+    uint64_t exceed_ge;  /* #[T_b >= T_obs]      one-sided "greater" */
+    uint64_t exceed_abs; /* #[|T_b| >= |T_obs|]  two-sided (R5) */
+    uint64_t flagged;    /* #[|T_b - T_obs| <= tau] near-ties (R8) */
+} hap_counts;
+
+/* ---- context ------------------------------------------------------------------- */
+HAP_API int hap_abi_version(void);
+/* Create a context on CUDA device `device` (fails unless it is sm_100). */
+HAP_API hap_status hap_create(int device, hap_ctx* out);
+HAP_API hap_status hap_destroy(hap_ctx ctx);
+/* Synchronise the context's last stream; returns the first deferred error (CUDA error or
+ * the device status of the last hap_align). */
+HAP_API hap_status hap_sync(hap_ctx ctx);
+HAP_API const char* hap_last_error(hap_ctx ctx);
+
+/* ---- S1-S6: normalise, means, Householder axis, reflect, pool, T_obs ------------ */
+/* PAPER.md §3.1 (lines 115-180) and Alg. 1 steps 1-4.
+ *   X [any]  n_x*d fp32 row-major raw embeddings h (unnormalised)
+ *   Y [any]  n_y*d fp32 row-major
+ *   info [device] hap_align_info, written.
+ * Builds, in the context workspace, the pooled aligned cloud Z = [X'; Y]
+ * as the transposed bf16 hi/lo planes Zt_hi, Zt_lo (d_pad x n_pad, K contiguous) with
+ * hi = bf16(z), lo = bf16(z - hi) (PAPER.md:258 precision note; R9), the total
+ * t = 1^T Z (Eq. gemm), then evaluates T_obs on the observed split
+ * through the same mask-GEMM + epilogue path as the permutations (D7).
+ * Constraints: 1 <= n_x, n_y; n_x + n_y <= 65535; 2 <= d <= 16384. */
+HAP_API hap_status hap_align(hap_ctx ctx, const float* X, int64_t n_x, const float* Y, int64_t n_y,
+                     int64_t d, hap_align_mode mode, hap_align_info* info, void* stream);
+
+/* ---- S7-S9: permutation masks, mask-GEMM, statistic, exceedance counts ----------- */
+/* PAPER.md §3.2 (lines 201-243), Alg. 2: for each b in
+ * [cfg->b_begin, cfg->b_end) draws the PERM-SPEC v1 group-1 set G_b, forms sigma1 =
+ * sum_{i in G_b} z_i with the tcgen05 mask-GEMM, sigma2 = t - sigma1,
+ * r1 = ||sigma1||/n_x, r2 = ||sigma2||/n_y, T_b = L(r2) - L(r1) and ADDS
+ * the three comparisons against info->t_obs into *counts.  Uses the Z from the last
+ * hap_align on this context; `info` must be that call's info.
+ *   counts [device] hap_counts, added into.
+ *   stats  [device] optional (NULL = none): (b_end-b_begin)*3 doubles {r1, r2, T_b}. */
+HAP_API hap_status hap_permtest(hap_ctx ctx, const hap_align_info* info, const hap_perm_cfg* cfg,
+                        hap_counts* counts, double* stats, void* stream);
+
+/* ---- many word pairs ------------------------------------------------------------ */
+/* Varlen batch of P independent tests (configs 4/5): pair p has X rows
+ * X_packed[cu_nx[p] .. cu_nx[p+1]) and Y rows Y_packed[cu_ny[p] .. cu_ny[p+1]).
+ *   X_packed, Y_packed [device]; cu_nx, cu_ny [host] int64[P+1] prefix offsets.
+ *   pair_sel [host] optional list of the pairs this call handles (NULL = all P); the
+ *            others' infos/counts are left untouched (used for multi-GPU sharding).
+ *   cfg->stream_id is the base s; pair p uses s = stream_id + p.
+ *   infos [device] P hap_align_info; counts [device] P hap_counts (added into).
+ * A pair with a data error has its own infos[p].status set; the batch continues. */
+HAP_API hap_status hap_permtest_batch(hap_ctx ctx, int64_t P, const float* X_packed, const int64_t* cu_nx,
+                              const float* Y_packed, const int64_t* cu_ny, int64_t d,
+                              hap_align_mode mode, const hap_perm_cfg* cfg,
+                              const int64_t* pair_sel, int64_t n_sel, hap_align_info* infos,
+                              hap_counts* counts, void* stream);
+
+/* p = (1 + c)/(B + 1)  (Eq. pvalue). */
+HAP_API double hap_pvalue(uint64_t exceed, uint64_t B);
+
+/* ---- introspection for parity tests (same kernels as the hot path) -------------- */
+/* PERM-SPEC v1 sets for b in [b_begin, b_begin+count): out [device] count*N uint8
+ * membership (1 = group 1), produced by the product's generator kernel. */
+HAP_API hap_status hap_perm_sets(hap_ctx ctx, uint64_t seed, uint32_t stream_id, uint64_t b_begin,
+                         int64_t count, int64_t N, int64_t n_x, uint8_t* out, void* stream);
+/* Copy out the pooled workspace of the last hap_align: zhi, zlo [device] d_pad*n_pad
+ * uint16, the transposed bf16 planes Zt (row c holds column c of Z over the n_pad pooled
+ * rows, zero padded); t [device] d_pad fp64 column sums of (hi + lo). */
+HAP_API hap_status hap_export_pooled(hap_ctx ctx, uint16_t* zhi, uint16_t* zlo, double* t, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HAP_H */

@@ -1,0 +1,251 @@
+"""paper_2605_08048_b200 — thin Python binding of libhap.so (include/hap.h).
+
+The functions below have the same names as the C ABI and only marshal arguments
+(torch tensors -> raw device pointers, torch streams -> cudaStream_t).  Every step of
+the hot path runs in the library's sm_100a kernels; there is no CPU fallback: if the
+extension is missing or the device is not a B200, the calls raise.
+
+PyTorch is used only for device memory, streams and (in parallel.py) process groups.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libhap.so")
+
+HAP_OK = 0
+STATUS_NAMES = {0: "OK", 1: "INVALID_ARG", 2: "DIM_MISMATCH", 3: "ZERO_VECTOR",
+                4: "DEGENERATE_MEAN", 5: "MIXED_SHAPES", 6: "OOM", 7: "CUDA",
+                8: "UNSUPPORTED_ARCH", 9: "NOT_ALIGNED"}
+HAP_ALIGN_HOUSEHOLDER, HAP_ALIGN_NONE = 0, 1
+
+
+class HapError(RuntimeError):
+    def __init__(self, status: int, msg: str = ""):
+        super().__init__(f"hap status {status} ({STATUS_NAMES.get(status, '?')}): {msg}")
+        self.status = status
+
+
+class hap_align_info(ctypes.Structure):
+    _fields_ = [("n_x", ctypes.c_int64), ("n_y", ctypes.c_int64), ("d", ctypes.c_int64),
+                ("n_pad", ctypes.c_int64), ("d_pad", ctypes.c_int64),
+                ("is_identity", ctypes.c_int32), ("status", ctypes.c_int32),
+                ("bad_row", ctypes.c_int64), ("norm_xbar", ctypes.c_double),
+                ("norm_ybar", ctypes.c_double), ("r_x", ctypes.c_double),
+                ("r_y", ctypes.c_double), ("logk_x", ctypes.c_double),
+                ("logk_y", ctypes.c_double), ("t_obs", ctypes.c_double)]
+
+
+class hap_perm_cfg(ctypes.Structure):
+    _fields_ = [("seed", ctypes.c_uint64), ("B", ctypes.c_uint64), ("b_begin", ctypes.c_uint64),
+                ("b_end", ctypes.c_uint64), ("stream_id", ctypes.c_uint32),
+                ("block", ctypes.c_uint32), ("tie_rel", ctypes.c_double),
+                ("flags", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
+
+
+class hap_counts(ctypes.Structure):
+    _fields_ = [("exceed_ge", ctypes.c_uint64), ("exceed_abs", ctypes.c_uint64),
+                ("flagged", ctypes.c_uint64)]
+
+
+INFO_BYTES = ctypes.sizeof(hap_align_info)
+COUNTS_WORDS = 3
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libhap.so (fails loudly if it was not built: there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: run `python -m paper_2605_08048_b200.build` "
+                          "(or __graft_entry__.build()); there is no CPU fallback")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i64, u64, u32, i32, f64 = (ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint64,
+                                   ctypes.c_uint32, ctypes.c_int, ctypes.c_double)
+    P = ctypes.POINTER
+    sig = {
+        "hap_abi_version": ([], i32),
+        "hap_create": ([i32, P(vp)], i32),
+        "hap_destroy": ([vp], i32),
+        "hap_sync": ([vp], i32),
+        "hap_last_error": ([vp], ctypes.c_char_p),
+        "hap_align": ([vp, vp, i64, vp, i64, i64, i32, vp, vp], i32),
+        "hap_permtest": ([vp, vp, P(hap_perm_cfg), vp, vp, vp], i32),
+        "hap_permtest_batch": ([vp, i64, vp, P(i64), vp, P(i64), i64, i32, P(hap_perm_cfg),
+                                P(i64), i64, vp, vp, vp], i32),
+        "hap_pvalue": ([u64, u64], f64),
+        "hap_perm_sets": ([vp, u64, u32, u64, i64, i64, i64, vp, vp], i32),
+        "hap_export_pooled": ([vp, vp, vp, vp, vp], i32),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = L
+    return L
+
+
+def _ptr(t) -> int | None:
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def _stream(stream) -> int | None:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    return getattr(stream, "cuda_stream", stream)
+
+
+def _check(ctx, st: int) -> None:
+    if st != HAP_OK:
+        msg = lib().hap_last_error(ctx).decode() if ctx else ""
+        raise HapError(st, msg)
+
+
+# ----------------------------------------------------------------- C ABI, same names
+def hap_abi_version() -> int:
+    return lib().hap_abi_version()
+
+
+def hap_create(device: int = 0) -> int:
+    h = ctypes.c_void_p()
+    st = lib().hap_create(int(device), ctypes.byref(h))
+    if st != HAP_OK:
+        raise HapError(st, "hap_create")
+    return h.value
+
+
+def hap_destroy(ctx) -> None:
+    _check(None, lib().hap_destroy(ctx))
+
+
+def hap_sync(ctx) -> int:
+    return lib().hap_sync(ctx)
+
+
+def hap_last_error(ctx) -> str:
+    return lib().hap_last_error(ctx).decode()
+
+
+def hap_align(ctx, X, Y, mode: int, info, stream=None) -> None:
+    """X, Y: float32 [n, d] tensors (CUDA or pinned/plain CPU); info: CUDA uint8 tensor
+    of INFO_BYTES bytes (written)."""
+    n_x, d = X.shape
+    n_y, d2 = Y.shape
+    if d != d2:
+        raise HapError(2, "X and Y dims differ")
+    _check(ctx, lib().hap_align(ctx, _ptr(X), n_x, _ptr(Y), n_y, d, int(mode), _ptr(info),
+                                _stream(stream)))
+
+
+def make_cfg(seed: int, B: int, b_begin: int = 0, b_end: int | None = None, stream_id: int = 0,
+             block: int = 0, tie_rel: float = 1e-6) -> hap_perm_cfg:
+    return hap_perm_cfg(seed=seed, B=B, b_begin=b_begin, b_end=B if b_end is None else b_end,
+                        stream_id=stream_id, block=block, tie_rel=tie_rel, flags=0, reserved=0)
+
+
+def hap_permtest(ctx, info, cfg: hap_perm_cfg, counts, stats=None, stream=None) -> None:
+    """counts: CUDA uint64/int64 tensor [3] (added into); stats: optional CUDA float64
+    [b_end-b_begin, 3]."""
+    _check(ctx, lib().hap_permtest(ctx, _ptr(info), ctypes.byref(cfg), _ptr(counts), _ptr(stats),
+                                   _stream(stream)))
+
+
+def hap_permtest_batch(ctx, X_packed, cu_nx, Y_packed, cu_ny, mode: int, cfg: hap_perm_cfg,
+                       infos, counts, pair_sel=None, stream=None) -> None:
+    P = len(cu_nx) - 1
+    d = X_packed.shape[1]
+    cnx = np.ascontiguousarray(cu_nx, dtype=np.int64)
+    cny = np.ascontiguousarray(cu_ny, dtype=np.int64)
+    I64P = ctypes.POINTER(ctypes.c_int64)
+    sel = None
+    n_sel = 0
+    if pair_sel is not None:
+        sel = np.ascontiguousarray(pair_sel, dtype=np.int64)
+        n_sel = sel.size
+    _check(ctx, lib().hap_permtest_batch(
+        ctx, P, _ptr(X_packed), cnx.ctypes.data_as(I64P), _ptr(Y_packed),
+        cny.ctypes.data_as(I64P), d, int(mode), ctypes.byref(cfg),
+        sel.ctypes.data_as(I64P) if sel is not None else None, n_sel, _ptr(infos), _ptr(counts),
+        _stream(stream)))
+
+
+def hap_pvalue(exceed: int, B: int) -> float:
+    return lib().hap_pvalue(int(exceed), int(B))
+
+
+def hap_perm_sets(ctx, seed: int, stream_id: int, b_begin: int, count: int, N: int, n_x: int,
+                  out, stream=None) -> None:
+    _check(ctx, lib().hap_perm_sets(ctx, seed, stream_id, b_begin, count, N, n_x, _ptr(out),
+                                    _stream(stream)))
+
+
+def hap_export_pooled(ctx, zhi, zlo, t, stream=None) -> None:
+    _check(ctx, lib().hap_export_pooled(ctx, _ptr(zhi), _ptr(zlo), _ptr(t), _stream(stream)))
+
+
+# ----------------------------------------------------------------- conveniences
+def decode_info(info_tensor) -> hap_align_info:
+    """Copy a device hap_align_info back to the host (synchronises)."""
+    raw = bytes(info_tensor.cpu().numpy().tobytes())
+    return hap_align_info.from_buffer_copy(raw[:INFO_BYTES])
+
+
+class Context:
+    """Owns a hap_ctx plus the small device buffers of one test."""
+
+    def __init__(self, device: int = 0):
+        import torch
+        self.torch = torch
+        self.device = torch.device("cuda", device)
+        self.h = hap_create(device)
+        self.info = torch.zeros(INFO_BYTES, dtype=torch.uint8, device=self.device)
+        self.counts = torch.zeros(COUNTS_WORDS, dtype=torch.int64, device=self.device)
+
+    def close(self):
+        if self.h:
+            hap_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def permtest_pair(self, X, Y, B: int, seed: int, stream_id: int = 0, mode: int = 0,
+                      b_begin: int = 0, b_end: int | None = None, tie_rel: float = 1e-6,
+                      block: int = 0, want_stats: bool = False, sync: bool = True):
+        """One word-pair test end to end: hap_align + hap_permtest (+ p-value)."""
+        torch = self.torch
+        b_end = B if b_end is None else b_end
+        self.counts.zero_()
+        hap_align(self.h, X, Y, mode, self.info)
+        stats = (torch.empty((b_end - b_begin, 3), dtype=torch.float64, device=self.device)
+                 if want_stats else None)
+        cfg = make_cfg(seed, B, b_begin, b_end, stream_id, block, tie_rel)
+        hap_permtest(self.h, self.info, cfg, self.counts, stats)
+        if not sync:
+            return None
+        st = hap_sync(self.h)
+        info = decode_info(self.info)
+        if st != HAP_OK:
+            raise HapError(st, hap_last_error(self.h))
+        c = self.counts.cpu().tolist()
+        out = dict(t_obs=info.t_obs, r_x=info.r_x, r_y=info.r_y, logk_x=info.logk_x,
+                   logk_y=info.logk_y, norm_xbar=info.norm_xbar, norm_ybar=info.norm_ybar,
+                   is_identity=bool(info.is_identity), exceed_ge=c[0], exceed_abs=c[1],
+                   flagged=c[2], B=B, p_value=hap_pvalue(c[0], B),
+                   p_two_sided=hap_pvalue(c[1], B))
+        if want_stats:
+            out["stats"] = stats
+        return out

@@ -1,0 +1,396 @@
+// hap_api.cu — host side of the C ABI declared in include/hap.h: context, workspace,
+// TMA tensor maps, argument validation and the launch sequence of the hot path.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "hap_internal.h"
+
+using namespace hap;
+
+struct hap_ctx_s {
+    int device = 0;
+    int sm_count = 0;
+    std::string err;
+    cudaStream_t last_stream = nullptr;
+    const hap_align_info* last_info = nullptr;
+    // ---- workspace (grow-only)
+    void* buf[16] = {};
+    size_t cap[16] = {};
+    // ---- state of the last successful hap_align
+    bool aligned = false;
+    int64_t n_x = 0, n_y = 0, d = 0, n_pad = 0, d_pad = 0;
+    // ---- TMA descriptors (valid for the current buffers/shape)
+    CUtensorMap tmA{}, tmBhi{}, tmBlo{};
+    const void* tm_key[3] = {};
+    int64_t tm_shape[3] = {};
+};
+
+namespace {
+
+enum Buf {
+    kX = 0, kY, kNrm, kCoef, kPart, kXbar, kYbar, kU, kZhi, kZlo, kTpart, kT64, kT32, kMask,
+    kDummyInfo, kNumBufs
+};
+
+hap_status fail(hap_ctx c, hap_status s, const std::string& msg) {
+    if (c) c->err = msg;
+    return s;
+}
+
+hap_status cuda_fail(hap_ctx c, cudaError_t e, const char* what) {
+    return fail(c, HAP_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// grow-only device buffer
+hap_status ensure(hap_ctx c, int which, size_t bytes) {
+    bytes = std::max<size_t>(bytes, 256);
+    if (c->cap[which] >= bytes) return HAP_OK;
+    if (c->buf[which]) {
+        if (c->last_stream) cudaStreamSynchronize(c->last_stream);
+        cudaFree(c->buf[which]);
+        c->buf[which] = nullptr;
+        c->cap[which] = 0;
+    }
+    size_t alloc = bytes + bytes / 4;
+    cudaError_t e = cudaMalloc(&c->buf[which], alloc);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(c, HAP_E_OOM, std::string("cudaMalloc failed: ") + cudaGetErrorString(e));
+    }
+    c->cap[which] = alloc;
+    return HAP_OK;
+}
+
+template <typename T>
+T* B(hap_ctx c, int which) { return static_cast<T*>(c->buf[which]); }
+
+bool is_device_ptr(const void* p) {
+    cudaPointerAttributes at{};
+    cudaError_t e = cudaPointerGetAttributes(&at, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q{};
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// 2-D bf16 tensor map: inner dim `inner` (contiguous), `rows` rows, box {64, box_rows},
+// 128-byte swizzle, out-of-bounds elements read as zero.
+bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows, uint32_t box_rows) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {inner, rows};
+    cuuint64_t strides[1] = {inner * 2};
+    cuuint32_t box[2] = {64, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+int64_t mask_rows_cap(hap_ctx c) { return (int64_t)(c->cap[kMask] / (size_t)(c->n_pad * 2)); }
+
+hap_status refresh_maps(hap_ctx c) {
+    const void* keys[3] = {c->buf[kMask], c->buf[kZhi], c->buf[kZlo]};
+    const int64_t shape[3] = {c->n_pad, c->d_pad, mask_rows_cap(c)};
+    if (std::equal(keys, keys + 3, c->tm_key) && std::equal(shape, shape + 3, c->tm_shape))
+        return HAP_OK;
+    const uint32_t box_n = (uint32_t)std::min<int64_t>(kChunkN, c->d_pad);
+    if (!make_map(&c->tmA, c->buf[kMask], (uint64_t)c->n_pad, (uint64_t)mask_rows_cap(c), kTileM) ||
+        !make_map(&c->tmBhi, c->buf[kZhi], (uint64_t)c->n_pad, (uint64_t)c->d_pad, box_n) ||
+        !make_map(&c->tmBlo, c->buf[kZlo], (uint64_t)c->n_pad, (uint64_t)c->d_pad, box_n))
+        return fail(c, HAP_E_CUDA, "cuTensorMapEncodeTiled failed");
+    std::copy(keys, keys + 3, c->tm_key);
+    std::copy(shape, shape + 3, c->tm_shape);
+    return HAP_OK;
+}
+
+GemmArgs gemm_args(hap_ctx c, hap_align_info* info) {
+    GemmArgs g{};
+    g.n_pad = (int)c->n_pad;
+    g.d_pad = (int)c->d_pad;
+    g.n_x = (int)c->n_x;
+    g.n_y = (int)c->n_y;
+    g.d = (int)c->d;
+    g.box_n = (int)std::min<int64_t>(kChunkN, c->d_pad);
+    g.info = info;
+    g.t32 = B<float>(c, kT32);
+    g.tie_rel = 1e-6;
+    return g;
+}
+
+constexpr int64_t kDefaultBlock = 8192;
+
+}  // namespace
+
+extern "C" {
+
+int hap_abi_version(void) { return HAP_ABI_VERSION; }
+
+hap_status hap_create(int device, hap_ctx* out) {
+    if (!out) return HAP_E_INVALID_ARG;
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n) {
+        cudaGetLastError();
+        return HAP_E_INVALID_ARG;
+    }
+    cudaDeviceProp prop{};
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return HAP_E_CUDA;
+    if (prop.major != 10 || prop.minor != 0) return HAP_E_UNSUPPORTED_ARCH;
+    hap_ctx c = new (std::nothrow) hap_ctx_s();
+    if (!c) return HAP_E_OOM;
+    c->device = device;
+    c->sm_count = prop.multiProcessorCount;
+    cudaSetDevice(device);
+    *out = c;
+    return HAP_OK;
+}
+
+hap_status hap_destroy(hap_ctx c) {
+    if (!c) return HAP_E_INVALID_ARG;
+    cudaSetDevice(c->device);
+    if (c->last_stream) cudaStreamSynchronize(c->last_stream);
+    for (void* p : c->buf)
+        if (p) cudaFree(p);
+    delete c;
+    return HAP_OK;
+}
+
+const char* hap_last_error(hap_ctx c) { return c ? c->err.c_str() : "null context"; }
+
+hap_status hap_sync(hap_ctx c) {
+    if (!c) return HAP_E_INVALID_ARG;
+    cudaSetDevice(c->device);
+    cudaError_t e = c->last_stream ? cudaStreamSynchronize(c->last_stream) : cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(c, e, "hap_sync");
+    if (c->last_info) {
+        hap_align_info h{};
+        e = cudaMemcpy(&h, c->last_info, sizeof(h), cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) return cuda_fail(c, e, "hap_sync info");
+        if (h.status != HAP_OK) {
+            char msg[160];
+            snprintf(msg, sizeof msg, "data error %d (bad_row %lld)", h.status, (long long)h.bad_row);
+            return fail(c, (hap_status)h.status, msg);
+        }
+    }
+    return HAP_OK;
+}
+
+double hap_pvalue(uint64_t exceed, uint64_t Bn) { return (1.0 + (double)exceed) / ((double)Bn + 1.0); }
+
+hap_status hap_align(hap_ctx c, const float* X, int64_t n_x, const float* Y, int64_t n_y, int64_t d,
+                     hap_align_mode mode, hap_align_info* info, void* stream) {
+    if (!c) return HAP_E_INVALID_ARG;
+    if (!X || !Y || !info) return fail(c, HAP_E_INVALID_ARG, "null pointer");
+    if (n_x < 1 || n_y < 1 || n_x + n_y > 65535)
+        return fail(c, HAP_E_INVALID_ARG, "need 1 <= n_x, n_y and n_x + n_y <= 65535");
+    if (d < 2 || d > 16384) return fail(c, HAP_E_DIM_MISMATCH, "need 2 <= d <= 16384");
+    if (mode != HAP_ALIGN_HOUSEHOLDER && mode != HAP_ALIGN_NONE)
+        return fail(c, HAP_E_INVALID_ARG, "bad mode");
+    if (!is_device_ptr(info)) return fail(c, HAP_E_INVALID_ARG, "info must be device memory");
+    cudaSetDevice(c->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t N = n_x + n_y;
+    const int64_t n_pad = round_up(N, kKBlock);
+    const int64_t d_pad = round_up(d, 32);
+    const int nbx = (int)ceil_div(n_x, kRowBlock), nby = (int)ceil_div(n_y, kRowBlock);
+    hap_status s;
+    if ((s = ensure(c, kNrm, N * 8)) || (s = ensure(c, kCoef, N * 8)) ||
+        (s = ensure(c, kPart, (size_t)(nbx + nby) * d * 8)) || (s = ensure(c, kXbar, d * 8)) ||
+        (s = ensure(c, kYbar, d * 8)) || (s = ensure(c, kU, d * 8)) ||
+        (s = ensure(c, kZhi, (size_t)d_pad * n_pad * 2)) ||
+        (s = ensure(c, kZlo, (size_t)d_pad * n_pad * 2)) ||
+        (s = ensure(c, kTpart, (size_t)(n_pad / kRowTile) * d_pad * 8)) ||
+        (s = ensure(c, kT64, d_pad * 8)) || (s = ensure(c, kT32, d_pad * 4)) ||
+        (s = ensure(c, kMask, (size_t)std::max<int64_t>(kDefaultBlock, kTileM) * n_pad * 2)))
+        return s;
+    // host inputs are staged into the context (copied on `stream`)
+    const float* dX = X;
+    const float* dY = Y;
+    if (!is_device_ptr(X)) {
+        if ((s = ensure(c, kX, (size_t)n_x * d * 4))) return s;
+        cudaError_t e = cudaMemcpyAsync(c->buf[kX], X, (size_t)n_x * d * 4, cudaMemcpyHostToDevice, st);
+        if (e != cudaSuccess) return cuda_fail(c, e, "H2D X");
+        dX = B<float>(c, kX);
+    }
+    if (!is_device_ptr(Y)) {
+        if ((s = ensure(c, kY, (size_t)n_y * d * 4))) return s;
+        cudaError_t e = cudaMemcpyAsync(c->buf[kY], Y, (size_t)n_y * d * 4, cudaMemcpyHostToDevice, st);
+        if (e != cudaSuccess) return cuda_fail(c, e, "H2D Y");
+        dY = B<float>(c, kY);
+    }
+    c->n_x = n_x;
+    c->n_y = n_y;
+    c->d = d;
+    c->n_pad = n_pad;
+    c->d_pad = d_pad;
+    if ((s = refresh_maps(c))) return s;
+
+    AlignArgs a{};
+    a.X = dX;
+    a.Y = dY;
+    a.n_x = n_x;
+    a.n_y = n_y;
+    a.d = d;
+    a.n_pad = n_pad;
+    a.d_pad = d_pad;
+    a.mode = mode;
+    a.info = info;
+    a.nrm = B<double>(c, kNrm);
+    a.coef = B<double>(c, kCoef);
+    a.part = B<double>(c, kPart);
+    a.xbar = B<double>(c, kXbar);
+    a.ybar = B<double>(c, kYbar);
+    a.u = B<double>(c, kU);
+    a.zt_hi = B<uint16_t>(c, kZhi);
+    a.zt_lo = B<uint16_t>(c, kZlo);
+    a.tpart = B<double>(c, kTpart);
+    a.t64 = B<double>(c, kT64);
+    a.t32 = B<float>(c, kT32);
+    cudaError_t e = launch_align(a, st);
+    if (e != cudaSuccess) return cuda_fail(c, e, "align kernels");
+    // S6: T_obs through the same mask-GEMM + epilogue path (D7)
+    e = launch_observed_mask(B<uint16_t>(c, kMask), n_x, n_pad, st);
+    if (e != cudaSuccess) return cuda_fail(c, e, "observed mask");
+    GemmArgs g = gemm_args(c, info);
+    g.count = 1;
+    g.observed = 1;
+    e = launch_maskgemm(&c->tmA, &c->tmBhi, &c->tmBlo, g, st);
+    if (e != cudaSuccess) return cuda_fail(c, e, "observed mask-GEMM");
+    c->aligned = true;
+    c->last_stream = st;
+    c->last_info = info;
+    return HAP_OK;
+}
+
+hap_status hap_permtest(hap_ctx c, const hap_align_info* info, const hap_perm_cfg* cfg,
+                        hap_counts* counts, double* stats, void* stream) {
+    if (!c) return HAP_E_INVALID_ARG;
+    if (!c->aligned) return fail(c, HAP_E_NOT_ALIGNED, "hap_permtest before hap_align");
+    if (!info || !cfg || !counts) return fail(c, HAP_E_INVALID_ARG, "null pointer");
+    if (cfg->b_end < cfg->b_begin || cfg->b_end > (1ull << 32))
+        return fail(c, HAP_E_INVALID_ARG, "need b_begin <= b_end <= 2^32");
+    if (!is_device_ptr(counts) || (stats && !is_device_ptr(stats)))
+        return fail(c, HAP_E_INVALID_ARG, "counts/stats must be device memory");
+    cudaSetDevice(c->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t total = (int64_t)(cfg->b_end - cfg->b_begin);
+    int64_t blk = cfg->block ? (int64_t)cfg->block : kDefaultBlock;
+    blk = std::max<int64_t>(kTileM, round_up(blk, kTileM));
+    blk = std::min<int64_t>(blk, std::max<int64_t>(kTileM, round_up(total, kTileM)));
+    hap_status s;
+    if ((s = ensure(c, kMask, (size_t)blk * c->n_pad * 2))) return s;
+    if ((s = refresh_maps(c))) return s;
+    GemmArgs g = gemm_args(c, const_cast<hap_align_info*>(info));
+    g.counts = counts;
+    g.tie_rel = cfg->tie_rel > 0 ? cfg->tie_rel : 1e-6;
+    for (int64_t off = 0; off < total; off += blk) {
+        const int64_t cnt = std::min<int64_t>(blk, total - off);
+        PermArgs pa{};
+        pa.seed = cfg->seed;
+        pa.s = cfg->stream_id;
+        pa.b_begin = cfg->b_begin + (uint64_t)off;
+        pa.count = cnt;
+        pa.N = c->n_x + c->n_y;
+        pa.n_x = c->n_x;
+        pa.n_pad = c->n_pad;
+        pa.out = c->buf[kMask];
+        pa.out_kind = kMaskBf16Row;
+        pa.info = info;
+        cudaError_t e = launch_perm(pa, c->sm_count, st);
+        if (e != cudaSuccess) return cuda_fail(c, e, "perm generator");
+        g.count = (int)cnt;
+        g.observed = 0;
+        g.stats = stats ? stats + 3 * off : nullptr;
+        e = launch_maskgemm(&c->tmA, &c->tmBhi, &c->tmBlo, g, st);
+        if (e != cudaSuccess) return cuda_fail(c, e, "mask-GEMM");
+    }
+    c->last_stream = st;
+    return HAP_OK;
+}
+
+hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const int64_t* cu_nx,
+                              const float* Y_packed, const int64_t* cu_ny, int64_t d,
+                              hap_align_mode mode, const hap_perm_cfg* cfg, const int64_t* pair_sel,
+                              int64_t n_sel, hap_align_info* infos, hap_counts* counts, void* stream) {
+    if (!c) return HAP_E_INVALID_ARG;
+    if (P < 0 || !X_packed || !Y_packed || !cu_nx || !cu_ny || !cfg || !infos || !counts)
+        return fail(c, HAP_E_INVALID_ARG, "null pointer / negative P");
+    const int64_t n = pair_sel ? n_sel : P;
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t p = pair_sel ? pair_sel[i] : i;
+        if (p < 0 || p >= P) return fail(c, HAP_E_INVALID_ARG, "pair_sel out of range");
+        const int64_t nx = cu_nx[p + 1] - cu_nx[p], ny = cu_ny[p + 1] - cu_ny[p];
+        hap_status s = hap_align(c, X_packed + cu_nx[p] * d, nx, Y_packed + cu_ny[p] * d, ny, d, mode,
+                                 infos + p, stream);
+        if (s) return s;
+        hap_perm_cfg pc = *cfg;
+        pc.stream_id = cfg->stream_id + (uint32_t)p;
+        s = hap_permtest(c, infos + p, &pc, counts + p, nullptr, stream);
+        if (s) return s;
+    }
+    return HAP_OK;
+}
+
+hap_status hap_perm_sets(hap_ctx c, uint64_t seed, uint32_t stream_id, uint64_t b_begin, int64_t count,
+                         int64_t N, int64_t n_x, uint8_t* out, void* stream) {
+    if (!c) return HAP_E_INVALID_ARG;
+    if (!out || count < 0 || N < 1 || N > 65535 || n_x < 0 || n_x > N)
+        return fail(c, HAP_E_INVALID_ARG, "bad perm_sets arguments");
+    if (b_begin + (uint64_t)count > (1ull << 32)) return fail(c, HAP_E_INVALID_ARG, "b >= 2^32");
+    cudaSetDevice(c->device);
+    PermArgs pa{};
+    pa.seed = seed;
+    pa.s = stream_id;
+    pa.b_begin = b_begin;
+    pa.count = count;
+    pa.N = N;
+    pa.n_x = n_x;
+    pa.n_pad = round_up(N, kKBlock);
+    pa.out = out;
+    pa.out_kind = kMaskU8Set;
+    pa.info = nullptr;
+    cudaError_t e = launch_perm(pa, c->sm_count, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(c, e, "perm generator");
+    return HAP_OK;
+}
+
+hap_status hap_export_pooled(hap_ctx c, uint16_t* zhi, uint16_t* zlo, double* t, void* stream) {
+    if (!c) return HAP_E_INVALID_ARG;
+    if (!c->aligned) return fail(c, HAP_E_NOT_ALIGNED, "no pooled cloud yet");
+    if (!zhi || !zlo || !t) return fail(c, HAP_E_INVALID_ARG, "null pointer");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // transpose back with 2-D copies: Zt [d_pad][n_pad] -> Z [n_pad][d_pad] is done by
+    // the caller-side view; here we copy the transposed planes verbatim.
+    const size_t bytes = (size_t)c->d_pad * c->n_pad * 2;
+    cudaError_t e = cudaMemcpyAsync(zhi, c->buf[kZhi], bytes, cudaMemcpyDeviceToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(zlo, c->buf[kZlo], bytes, cudaMemcpyDeviceToDevice, st);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(t, c->buf[kT64], (size_t)c->d_pad * 8, cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(c, e, "export");
+    return HAP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,73 @@
+// hap_internal.h — declarations shared by the libhap translation units (host side).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/hap.h"
+
+namespace hap {
+
+constexpr int kKBlock = 64;     // GEMM K-block: 64 bf16 = one 128-byte swizzle atom
+constexpr int kTileM = 128;     // permutations per CTA tile (TMEM lanes)
+constexpr int kChunkN = 256;    // d-columns per accumulator chunk (UMMA N <= 256)
+constexpr int kRowBlock = 32;   // rows per column-partial block in K1b
+constexpr int kRowTile = 64;    // pooled rows per reflect/split tile in K1d
+
+inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+inline int64_t ceil_div(int64_t x, int64_t m) { return (x + m - 1) / m; }
+
+// ---- K1: alignment (k_align.cu) ----------------------------------------------------
+struct AlignArgs {
+    const float* X;
+    const float* Y;
+    int64_t n_x, n_y, d, n_pad, d_pad;
+    int mode;                // hap_align_mode
+    hap_align_info* info;    // device
+    double* nrm;             // [N]    row norms ||h_i||
+    double* coef;            // [N]    2 u^T x_i  (0 for Y rows / identity)
+    double* part;            // [nblk_x + nblk_y][d] fp64 column partials
+    double* xbar;            // [d]
+    double* ybar;            // [d]
+    double* u;               // [d]    Householder axis (fp64)
+    uint16_t* zt_hi;         // [d_pad][n_pad] bf16 bits
+    uint16_t* zt_lo;         // [d_pad][n_pad]
+    double* tpart;           // [n_pad/kRowTile][d_pad] fp64 partials of t
+    double* t64;             // [d_pad]
+    float* t32;              // [d_pad]
+};
+cudaError_t launch_align(const AlignArgs& a, cudaStream_t st);
+
+// ---- K2: PERM-SPEC v1 generator (k_perm.cu) ----------------------------------------
+enum MaskOut { kMaskBf16Row = 0, kMaskU8Set = 1 };
+struct PermArgs {
+    uint64_t seed;
+    uint32_t s;
+    uint64_t b_begin;
+    int64_t count;
+    int64_t N, n_x, n_pad;
+    void* out;               // bf16 rows [count][n_pad] or uint8 [count][N]
+    int out_kind;            // MaskOut
+    const hap_align_info* info;  // optional: skip if info->status != 0
+};
+cudaError_t launch_perm(const PermArgs& a, int sm_count, cudaStream_t st);
+cudaError_t launch_observed_mask(uint16_t* mask_row, int64_t n_x, int64_t n_pad, cudaStream_t st);
+
+// ---- K3: tcgen05 mask-GEMM + statistic epilogue (k_maskgemm.cu) --------------------
+struct GemmArgs {
+    int n_pad, d_pad, n_x, n_y, d;
+    int box_n;               // B tile rows = min(256, d_pad)
+    int count;               // valid permutation rows in this launch
+    int observed;            // 1: write T_obs etc. into info (row 0), 0: count
+    double tie_rel;
+    hap_align_info* info;
+    hap_counts* counts;
+    double* stats;           // optional, [count][3]
+    const float* t32;
+};
+cudaError_t launch_maskgemm(const CUtensorMap* tmA, const CUtensorMap* tmBhi,
+                            const CUtensorMap* tmBlo, const GemmArgs& g, cudaStream_t st);
+size_t maskgemm_smem_bytes();
+
+}  // namespace hap

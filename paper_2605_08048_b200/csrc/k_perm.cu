@@ -1,0 +1,170 @@
+// k_perm.cu — K2: PERM-SPEC v1 permutation generator (DESIGN.md "Kernels" K2, R6).
+//
+// "Randomly partition Z into (X^(b), Y^(b)) with sizes (n, m)" (Alg. 1);
+// "S_blk <- random {+1,-1}^{B0 x N} with exactly n entries +1 per row" (Alg. 2,
+// PAPER.md:710).  PERM-SPEC v1 fixes the law as the partial forward Fisher-Yates
+// shuffle over n_x steps with Philox4x32-10 words and Lemire bounded draws:
+//     a = [0..N-1]; for k < n_x: j_k = k + U(N-k); swap(a[k], a[j_k]);  G_b = a[0..n_x).
+//
+// GPU formulation (one warp per permutation, no serial swap chain).  With
+//   LT[q] = 1 + max{k : j_k = q, k != q}  (0 if no such step)       "last writer of q",
+// the final contents satisfy (K2 derivation):
+//   * a high position p >= n_x keeps value p unless written; if written, its final value
+//     is the value position k* = LT[p]-1 held just before step k*, i.e. chain(k*) with
+//     chain(k) = LT[k] ? chain(LT[k]-1) : k;
+//   * hence G_b = ([0, n_x) \ E) U {p >= n_x : LT[p] != 0},  E = {chain(LT[p]-1)}.
+// Phase A draws all j_k in parallel (lanes own Philox blocks) and scatters LT with
+// last-writer-wins in step order; phase B follows the (short, disjoint) chains; phase C
+// emits the exact 0/1 mask row.  Bit-exact against oracle/orc_perm_set (tests).
+#include <cuda_bf16.h>
+
+#include "hap_device.cuh"
+#include "hap_internal.h"
+
+namespace hap {
+namespace {
+
+constexpr int kPermWarps = 4;
+constexpr uint16_t kExiled = 0xFFFF;
+
+// U(N-k) for step k: Lemire on the main-stream word x; rejected words are replaced by
+// the side stream (counter (q', b, s, 1+k)) in order.
+__device__ __forceinline__ uint32_t fy_target(uint32_t x, uint32_t k, uint32_t N, uint32_t b,
+                                              uint32_t s, uint32_t k0, uint32_t k1) {
+    const uint32_t bound = N - k;
+    uint64_t m = (uint64_t)x * bound;
+    uint32_t lo = (uint32_t)m;
+    if (lo < bound) {
+        const uint32_t t = (0u - bound) % bound;
+        uint32_t side = 0;
+        while (lo < t) {
+            const u32x4 w = philox4x32_10(u32x4{side >> 2, b, s, 1u + k}, k0, k1);
+            x = u32x4_get(w, side & 3u);
+            ++side;
+            m = (uint64_t)x * bound;
+            lo = (uint32_t)m;
+        }
+    }
+    return k + (uint32_t)(m >> 32);
+}
+
+__global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy(PermArgs a, int lt_pitch) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    if (a.info && a.info->status != HAP_OK) return;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    uint16_t* LT = reinterpret_cast<uint16_t*>(smem) + (size_t)w * (lt_pitch + 128);
+    uint16_t* stage = LT + lt_pitch;
+    const uint32_t N = (uint32_t)a.N, nx = (uint32_t)a.n_x, s = a.s;
+    const uint32_t key0 = (uint32_t)(a.seed & 0xFFFFFFFFu), key1 = (uint32_t)(a.seed >> 32);
+    const int64_t wstride = (int64_t)gridDim.x * kPermWarps;
+    for (int64_t pi = (int64_t)blockIdx.x * kPermWarps + w; pi < a.count; pi += wstride) {
+        const uint32_t b = (uint32_t)(a.b_begin + (uint64_t)pi);
+        uint4* LT4 = reinterpret_cast<uint4*>(LT);
+        for (int q = l; q < lt_pitch / 8; q += 32) LT4[q] = make_uint4(0, 0, 0, 0);
+        __syncwarp();
+        // ---- phase A: draws + last-writer scatter, 128 steps per round
+        for (uint32_t k0 = 0; k0 < nx; k0 += 128) {
+            const uint32_t q = (k0 >> 2) + (uint32_t)l;
+            if (k0 + 4u * l < nx) {
+                const u32x4 wd = philox4x32_10(u32x4{q, b, s, 0u}, key0, key1);
+#pragma unroll
+                for (uint32_t e = 0; e < 4; ++e) {
+                    const uint32_t k = k0 + 4u * l + e;
+                    if (k < nx) stage[4 * l + e] = (uint16_t)fy_target(u32x4_get(wd, e), k, N, b, s,
+                                                                       key0, key1);
+                }
+            }
+            __syncwarp();
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const uint32_t idx = 32u * r + l, k = k0 + idx;
+                const bool valid = k < nx;
+                const uint32_t j = valid ? stage[idx] : 0u;
+                bool pending = valid && j != k;  // self-targets never move a value
+                // last writer (largest k) wins: lanes are in step order within the round
+                while (__any_sync(0xffffffffu, pending)) {
+                    if (pending) LT[j] = (uint16_t)(k + 1);
+                    __syncwarp();
+                    if (pending && LT[j] >= k + 1) pending = false;
+                    __syncwarp();
+                }
+            }
+        }
+        __syncwarp();
+        // ---- phase B: each written high position exiles the end of its chain
+        for (uint32_t p = nx + l; p < N; p += 32) {
+            const uint16_t v = LT[p];
+            if (v) {
+                uint32_t kk = v - 1u;
+                uint16_t t;
+                while ((t = LT[kk]) != 0 && t != kExiled) kk = t - 1u;
+                LT[kk] = kExiled;
+            }
+        }
+        __syncwarp();
+        // ---- phase C: exact 0/1 row
+        if (a.out_kind == kMaskBf16Row) {
+            uint4* row = reinterpret_cast<uint4*>(static_cast<uint16_t*>(a.out) + pi * a.n_pad);
+            for (int64_t v8 = l; v8 < a.n_pad / 8; v8 += 32) {
+                uint32_t wds[4];
+#pragma unroll
+                for (int e2 = 0; e2 < 4; ++e2) {
+                    uint32_t pack = 0;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const uint32_t v = (uint32_t)(8 * v8 + 2 * e2 + h);
+                        bool sel = false;
+                        if (v < N) {
+                            const uint16_t t = LT[v];
+                            sel = (v < nx) ? (t != kExiled) : (t != 0);
+                        }
+                        pack |= (sel ? 0x3F80u : 0u) << (16 * h);
+                    }
+                    wds[e2] = pack;
+                }
+                row[v8] = make_uint4(wds[0], wds[1], wds[2], wds[3]);
+            }
+        } else {
+            uint8_t* row = static_cast<uint8_t*>(a.out) + pi * a.N;
+            for (uint32_t v = l; v < N; v += 32) {
+                const uint16_t t = LT[v];
+                row[v] = (v < nx) ? (t != kExiled) : (t != 0);
+            }
+        }
+        __syncwarp();
+    }
+}
+
+__global__ void k2_observed_mask(uint16_t* row, int64_t n_x, int64_t n_pad) {
+    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < n_pad) row[v] = v < n_x ? (uint16_t)0x3F80 : (uint16_t)0;  // bf16(1), bf16(0)
+}
+
+}  // namespace
+
+cudaError_t launch_perm(const PermArgs& a, int sm_count, cudaStream_t st) {
+    if (a.count <= 0) return cudaSuccess;
+    const int lt_pitch = (int)round_up(a.N, 64);  // uint16 entries, 128-byte multiple
+    const size_t smem = (size_t)kPermWarps * (lt_pitch + 128) * sizeof(uint16_t);
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+        cudaError_t e = cudaFuncSetAttribute(k2_perm_fy, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        configured = smem;
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_perm_fy, kPermWarps * 32, smem);
+    if (per_sm < 1) per_sm = 1;
+    const int64_t need = ceil_div(a.count, kPermWarps);
+    const int grid = (int)std::min<int64_t>(need, (int64_t)sm_count * per_sm);
+    k2_perm_fy<<<grid, kPermWarps * 32, smem, st>>>(a, lt_pitch);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_observed_mask(uint16_t* mask_row, int64_t n_x, int64_t n_pad, cudaStream_t st) {
+    k2_observed_mask<<<(unsigned)ceil_div(n_pad, 256), 256, 0, st>>>(mask_row, n_x, n_pad);
+    return cudaGetLastError();
+}
+
+}  // namespace hap

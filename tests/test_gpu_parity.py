@@ -1,0 +1,242 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle, element by element
+on the same seeded inputs.  Bars:
+  * permutation index sets: bit-exact;
+  * r1, r2 (and r_X, r_Y): relative 1e-5; L: relative 1e-5;
+  * T: |dT| <= 1e-5 (|L1| + |L2|)  (T is a near-zero difference, D6);
+  * counts: every permutation outside the tie band tau decides identically, so
+    |c_gpu - c_oracle| <= flagged (tie band tau = 1e-6 (|L_X| + |L_Y|), R8).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import hap_inputs as HI
+
+pytestmark = pytest.mark.gpu
+
+SEED = HI.PERM_SEED
+
+
+@pytest.fixture(scope="module")
+def hap():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2605_08048_b200 import build
+    build.build()
+    import paper_2605_08048_b200 as h
+    return h
+
+
+@pytest.fixture(scope="module")
+def ctx(hap):
+    c = hap.Context(0)
+    yield c
+    c.close()
+
+
+def _cuda(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def check_pair(ctx, orc, X, Y, B, s=0, mode=0, block=0, b_begin=0, b_end=None, n_stats=None):
+    """Run both sides with stats; assert the parity bars; return (gpu, ref)."""
+    b_end = B if b_end is None else b_end
+    g = ctx.permtest_pair(_cuda(X), _cuda(Y), B, SEED, stream_id=s, mode=mode, block=block,
+                          b_begin=b_begin, b_end=b_end, want_stats=True)
+    ref = orc.run_pair(X, Y, B, SEED, s=s, mode=mode, b_begin=b_begin, b_end=b_end,
+                       want_stats=True)
+    Ls = abs(ref["L_x"]) + abs(ref["L_y"])
+    assert math.isclose(g["r_x"], ref["r_x"], rel_tol=1e-5)
+    assert math.isclose(g["r_y"], ref["r_y"], rel_tol=1e-5)
+    assert math.isclose(g["logk_x"], ref["L_x"], rel_tol=1e-5, abs_tol=1e-9)
+    assert math.isclose(g["logk_y"], ref["L_y"], rel_tol=1e-5, abs_tol=1e-9)
+    assert abs(g["t_obs"] - ref["t_obs"]) <= 1e-5 * Ls
+    gs = g["stats"].cpu().numpy()
+    rs = ref["stats"]
+    assert np.allclose(gs[:, 0], rs[:, 0], rtol=1e-5, atol=0)
+    assert np.allclose(gs[:, 1], rs[:, 1], rtol=1e-5, atol=0)
+    assert np.all(np.abs(gs[:, 2] - rs[:, 2]) <= 1e-5 * Ls)
+    # decisions identical outside the tie band
+    tau = ref["tau"]
+    out = np.abs(rs[:, 2] - ref["t_obs"]) > tau
+    assert np.array_equal(gs[out, 2] >= g["t_obs"], rs[out, 2] >= ref["t_obs"])
+    assert np.array_equal(np.abs(gs[out, 2]) >= abs(g["t_obs"]),
+                          np.abs(rs[out, 2]) >= abs(ref["t_obs"]))
+    for k in ("exceed_ge", "exceed_abs"):
+        assert abs(g[k] - ref[k]) <= ref["flagged"], (k, g[k], ref[k], ref["flagged"])
+    return g, ref
+
+
+# ------------------------------------------------------------------ K2 (index sets)
+@pytest.mark.parametrize("N,n_x", [(2, 1), (10, 4), (8, 4), (128, 64), (100, 37), (2000, 1000),
+                                   (2000, 1), (2000, 1999), (4097, 2500), (65535, 32767)])
+def test_perm_sets_bit_exact(hap, ctx, orc, N, n_x):
+    import torch
+    count = 64 if N < 10000 else 6
+    for s, b0 in [(0, 0), (5, 123456), (0xFFFFFFFF, 2**32 - count)]:
+        out = torch.empty((count, N), dtype=torch.uint8, device="cuda")
+        hap.hap_perm_sets(ctx.h, SEED, s, b0, count, N, n_x, out)
+        got = out.cpu().numpy()
+        for i in range(count):
+            want = orc.perm_set(SEED, s, b0 + i, N, n_x)
+            assert np.array_equal(got[i], want), (N, n_x, s, b0 + i)
+
+
+def test_perm_sets_golden(hap, ctx):
+    """The product generator reproduces the SURVEY golden sets directly."""
+    import torch
+    from conftest import read_golden
+    for row in read_golden("permspec_v1.txt"):
+        lhs, rhs = row.split(":")
+        seed, s, b, N, n = lhs.split()
+        out = torch.empty((1, int(N)), dtype=torch.uint8, device="cuda")
+        hap.hap_perm_sets(ctx.h, int(seed, 16), int(s), int(b), 1, int(N), int(n), out)
+        assert np.nonzero(out.cpu().numpy()[0])[0].tolist() == [int(x) for x in rhs.split()]
+
+
+# ------------------------------------------------------------------ K1 (pooled planes)
+@pytest.mark.parametrize("n_x,n_y,d,mode", [(64, 64, 768, 0), (37, 50, 100, 0), (1000, 1000, 768, 0),
+                                            (300, 200, 64, 1), (5, 3, 3, 0)])
+def test_pooled_planes(hap, ctx, orc, n_x, n_y, d, mode):
+    import torch
+    X, Y = HI.make_pair(HI.PairSpec(n_x, n_y, d, 40.0, 40.0, 50.0, seed=d + n_x))
+    ctx.permtest_pair(_cuda(X), _cuda(Y), 128, SEED, mode=mode)
+    n_pad = -(-(n_x + n_y) // 64) * 64
+    d_pad = -(-d // 32) * 32
+    zh = torch.empty((d_pad, n_pad), dtype=torch.int16, device="cuda")
+    zl = torch.empty_like(zh)
+    t = torch.empty(d_pad, dtype=torch.float64, device="cuda")
+    hap.hap_export_pooled(ctx.h, zh, zl, t)
+    torch.cuda.synchronize()
+    hi = zh.view(torch.bfloat16).float().double().cpu().numpy().T
+    lo = zl.view(torch.bfloat16).float().double().cpu().numpy().T
+    ref = orc.align(X, Y, mode)
+    N = n_x + n_y
+    z = hi[:N, :d] + lo[:N, :d]
+    assert np.all(np.abs(z - ref.Z) <= 2.0 ** -16 * np.abs(ref.Z) + 1e-12)
+    assert np.all(hi[N:] == 0) and np.all(lo[N:] == 0)
+    assert np.all(hi[:, d:] == 0) and np.all(lo[:, d:] == 0)
+    tt = t.cpu().numpy()
+    assert np.allclose(tt[:d], (hi + lo)[:, :d].sum(0), rtol=1e-12, atol=1e-12)
+    assert np.allclose(tt[:d], ref.Z.sum(0), rtol=1e-5, atol=1e-5)
+
+
+# ------------------------------------------------------------------ K3 + end to end
+def test_config1_full(ctx, orc):
+    """C1: n_x=n_y=64, d=768, B=1000, every permutation compared."""
+    X, Y = HI.config_pair("C1")
+    check_pair(ctx, orc, X, Y, 1000, s=1)
+
+
+@pytest.mark.parametrize("n_x,n_y,d,B,block", [(37, 50, 100, 300, 128), (1, 70, 48, 257, 0),
+                                               (70, 1, 40, 129, 0), (200, 300, 300, 1000, 256),
+                                               (5, 3, 3, 200, 0)])
+def test_ragged_shapes(ctx, orc, n_x, n_y, d, B, block):
+    """Ragged N (not a multiple of 64), d not a multiple of 32, several tiles with a
+    ragged tail, multi-block launches, single-row groups."""
+    X, Y = HI.make_pair(HI.PairSpec(n_x, n_y, d, 30.0, 60.0, 40.0, seed=n_x * 7 + d))
+    check_pair(ctx, orc, X, Y, B, s=3, block=block)
+
+
+def test_naive_mode(ctx, orc):
+    X, Y = HI.make_pair(HI.PairSpec(120, 90, 256, 100.0, 100.0, 90.0, seed=4))
+    g, ref = check_pair(ctx, orc, X, Y, 500, mode=1)
+    assert g["is_identity"]
+
+
+def test_config2_full(ctx, orc):
+    """C2 (the metric's configuration): n_x=n_y=1000, d=768, B=10^4, all b compared."""
+    X, Y = HI.config_pair("C2")
+    check_pair(ctx, orc, X, Y, 10000, s=2)
+
+
+def test_config3_sampled(ctx, orc):
+    """C3 shape (n_x=n_y=5000, d=4096): a b-range shard far from 0, every b of it
+    compared (full B=10^5 runs in test_sharding / bench)."""
+    X, Y = HI.config_pair("C3")
+    check_pair(ctx, orc, X, Y, 100000, s=3, b_begin=77000, b_end=77300)
+
+
+def test_worked_example_counts_exact(ctx, orc):
+    """SURVEY worked example (d=3): T values are >= 0.0155 apart, so the counts must be
+    identical, and the MC p approaches the exhaustive 12/70."""
+    from conftest import read_golden
+    rows = read_golden("worked_example.txt")
+    X = np.array([[float(v) for v in r.split()[1:]] for r in rows if r.startswith("X ")], np.float32)
+    Y = np.array([[float(v) for v in r.split()[1:]] for r in rows if r.startswith("Y ")], np.float32)
+    g, ref = check_pair(ctx, orc, X, Y, 20000)
+    assert g["exceed_ge"] == ref["exceed_ge"] and g["exceed_abs"] == ref["exceed_abs"]
+    assert abs(g["exceed_ge"] / 20000 - 12 / 70) < 4 * math.sqrt(12 / 70 * 58 / 70 / 20000)
+
+
+def test_dyadic_exact(ctx, orc):
+    """Dyadic unit rows in naive mode: every sum is exact on both sides, so r1, r2 are
+    bit-identical to the oracle."""
+    rng = np.random.default_rng(0)
+    X, Y = HI.dyadic_pair(rng, 7, 9, 64)
+    g, ref = check_pair(ctx, orc, X, Y, 512, mode=1)
+    gs = g["stats"].cpu().numpy()
+    assert np.array_equal(gs[:, 0], ref["stats"][:, 0])
+    assert np.array_equal(gs[:, 1], ref["stats"][:, 1])
+
+
+def test_duplicate_sets_tie_bit_exactly(ctx, orc):
+    """N=4, n=2: only 6 distinct splits, so many b repeat the observed split; those T
+    must equal T_obs bit-exactly (same GEMM + epilogue path, D7) and count as >=."""
+    X = np.array([[1, 0.2, 0], [0.3, 1, 0]], np.float32)
+    Y = np.array([[0, 0.1, 1], [1, 1, 1]], np.float32)
+    g, ref = check_pair(ctx, orc, X, Y, 600)
+    gs = g["stats"].cpu().numpy()
+    sets = [tuple(np.nonzero(orc.perm_set(SEED, 0, b, 4, 2))[0]) for b in range(600)]
+    obs = [i for i, s in enumerate(sets) if s == (0, 1)]
+    assert len(obs) > 50
+    assert np.all(gs[obs, 2] == g["t_obs"])
+    assert g["exceed_ge"] == ref["exceed_ge"]
+
+
+def test_errors_are_reported(hap, ctx):
+    import torch
+    X = np.ones((4, 8), np.float32)
+    Y = np.ones((4, 8), np.float32)
+    X[2] = 0
+    with pytest.raises(hap.HapError) as e:
+        ctx.permtest_pair(_cuda(X), _cuda(Y), 100, SEED)
+    assert e.value.status == 3
+    assert hap.decode_info(ctx.info).bad_row == 2
+    X = np.array([[1, 0], [-1, 0]], np.float32)
+    with pytest.raises(hap.HapError) as e:
+        ctx.permtest_pair(_cuda(X), _cuda(np.array([[0, 1.0]], np.float32)), 100, SEED)
+    assert e.value.status == 4
+    # identity: coincident mean directions
+    X, Y = HI.make_pair(HI.PairSpec(50, 50, 32, 20.0, 20.0, 0.0, seed=1))
+    g = ctx.permtest_pair(_cuda(X), _cuda(X), 100, SEED)
+    assert g["is_identity"]
+    with pytest.raises(hap.HapError):
+        ctx.permtest_pair(_cuda(X), _cuda(Y[:, :16].copy()), 100, SEED)
+
+
+def test_sharding_is_additive_and_deterministic(ctx):
+    """Counts over [0,B) equal the sum over shards; two runs are bitwise identical."""
+    X, Y = HI.config_pair("C2")
+    full = ctx.permtest_pair(_cuda(X), _cuda(Y), 10000, SEED, want_stats=True)
+    again = ctx.permtest_pair(_cuda(X), _cuda(Y), 10000, SEED, want_stats=True)
+    assert np.array_equal(full["stats"].cpu().numpy(), again["stats"].cpu().numpy())
+    tot = np.zeros(3, np.int64)
+    for b0, b1 in [(0, 1234), (1234, 5000), (5000, 10000)]:
+        r = ctx.permtest_pair(_cuda(X), _cuda(Y), 10000, SEED, b_begin=b0, b_end=b1)
+        tot += [r["exceed_ge"], r["exceed_abs"], r["flagged"]]
+    assert tot.tolist() == [full["exceed_ge"], full["exceed_abs"], full["flagged"]]
+
+
+def test_host_inputs_match_device_inputs(ctx):
+    """hap_align accepts host buffers (copied in on the stream): same result."""
+    import torch
+    X, Y = HI.config_pair("C1")
+    a = ctx.permtest_pair(_cuda(X), _cuda(Y), 1000, SEED, want_stats=True)
+    b = ctx.permtest_pair(torch.from_numpy(X).pin_memory(), torch.from_numpy(Y), 1000, SEED,
+                          want_stats=True)
+    assert np.array_equal(a["stats"].cpu().numpy(), b["stats"].cpu().numpy())
+    assert a["exceed_ge"] == b["exceed_ge"]
