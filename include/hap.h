@@ -155,9 +155,12 @@ HAP_API double hap_pvalue(uint64_t exceed, uint64_t B);
 HAP_API hap_status hap_perm_sets(hap_ctx ctx, uint64_t seed, uint32_t stream_id, uint64_t b_begin,
                          int64_t count, int64_t N, int64_t n_x, uint8_t* out, void* stream);
 /* Copy out the pooled workspace of the last hap_align: zhi, zlo [device] d_pad*n_pad
- * uint16, the transposed bf16 planes Zt (row c holds column c of Z over the n_pad pooled
- * rows, zero padded); t [device] d_pad fp64 column sums of (hi + lo). */
-HAP_API hap_status hap_export_pooled(hap_ctx ctx, uint16_t* zhi, uint16_t* zlo, double* t, void* stream);
+ * uint16, the transposed bf16 planes Zt of the CENTRED cloud (row c holds column c of
+ * Z - 1 m^T over the n_pad pooled rows, zero padded), so z[i][c] ~ hi + lo + m[c];
+ * t [device] d_pad fp64 = N m + column sums of (hi + lo);  m [device] d_pad fp64 centre
+ * (DESIGN.md "Numerics"). */
+HAP_API hap_status hap_export_pooled(hap_ctx ctx, uint16_t* zhi, uint16_t* zlo, double* t, double* m,
+                                     void* stream);
 
 #ifdef __cplusplus
 }

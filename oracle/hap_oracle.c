@@ -207,11 +207,15 @@ void orc_group_stats(const double* Z, int64_t N, int64_t d, int64_t n_x, const u
 }
 
 /* one comparison against the observed value (Eq. pvalue uses >=, PAPER.md:189;
- * two-sided |T_b| >= |T_obs| and the tie flag are DESIGN.md R5, R8). */
+ * two-sided |T_b| >= |T_obs| is DESIGN.md R5).  The near-tie flag (R8) marks a
+ * permutation within tau of either decision boundary: T_obs (one-sided) or |T_obs|
+ * (two-sided). */
 static void tally(double T, double t_obs, double tau, uint64_t* c) {
     if (T >= t_obs) c[0]++;
     if (fabs(T) >= fabs(t_obs)) c[1]++;
-    if (T == t_obs || fabs(T - t_obs) <= tau) c[2]++;
+    if (T == t_obs || fabs(T - t_obs) <= tau || fabs(T) == fabs(t_obs) ||
+        fabs(fabs(T) - fabs(t_obs)) <= tau)
+        c[2]++;
 }
 
 /* ------------------------------------------------------------------------- */

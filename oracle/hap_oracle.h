@@ -61,7 +61,8 @@ void orc_group_stats(const double* Z, int64_t N, int64_t d, int64_t n_x, const u
 
 /* Monte Carlo permutation loop, Alg. 1 step 5 with PERM-SPEC v1
  * sets for b in [b_begin, b_end), on nthreads host threads.  counts[3] +=
- * {#[T_b >= t_obs], #[|T_b| >= |t_obs|], #[|T_b - t_obs| <= tau]}.  stats
+ * {#[T_b >= t_obs], #[|T_b| >= |t_obs|], #[near-tie]} with near-tie =
+ * |T_b - t_obs| <= tau or ||T_b| - |t_obs|| <= tau (R8).  stats
  * (optional, may be NULL): (b_end-b_begin)*3 doubles {r1, r2, T}. */
 void orc_permtest(const double* Z, int64_t N, int64_t d, int64_t n_x, uint64_t seed, uint32_t s,
                   uint64_t b_begin, uint64_t b_end, double t_obs, double tau, int nthreads,

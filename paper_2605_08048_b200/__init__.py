@@ -82,7 +82,7 @@ def lib() -> ctypes.CDLL:
                                 P(i64), i64, vp, vp, vp], i32),
         "hap_pvalue": ([u64, u64], f64),
         "hap_perm_sets": ([vp, u64, u32, u64, i64, i64, i64, vp, vp], i32),
-        "hap_export_pooled": ([vp, vp, vp, vp, vp], i32),
+        "hap_export_pooled": ([vp, vp, vp, vp, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -189,8 +189,9 @@ def hap_perm_sets(ctx, seed: int, stream_id: int, b_begin: int, count: int, N: i
                                     _stream(stream)))
 
 
-def hap_export_pooled(ctx, zhi, zlo, t, stream=None) -> None:
-    _check(ctx, lib().hap_export_pooled(ctx, _ptr(zhi), _ptr(zlo), _ptr(t), _stream(stream)))
+def hap_export_pooled(ctx, zhi, zlo, t, m, stream=None) -> None:
+    _check(ctx, lib().hap_export_pooled(ctx, _ptr(zhi), _ptr(zlo), _ptr(t), _ptr(m),
+                                        _stream(stream)))
 
 
 # ----------------------------------------------------------------- conveniences

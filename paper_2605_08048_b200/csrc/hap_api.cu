@@ -21,8 +21,8 @@ struct hap_ctx_s {
     cudaStream_t last_stream = nullptr;
     const hap_align_info* last_info = nullptr;
     // ---- workspace (grow-only)
-    void* buf[16] = {};
-    size_t cap[16] = {};
+    void* buf[32] = {};
+    size_t cap[32] = {};
     // ---- state of the last successful hap_align
     bool aligned = false;
     int64_t n_x = 0, n_y = 0, d = 0, n_pad = 0, d_pad = 0;
@@ -35,8 +35,8 @@ struct hap_ctx_s {
 namespace {
 
 enum Buf {
-    kX = 0, kY, kNrm, kCoef, kPart, kXbar, kYbar, kU, kZhi, kZlo, kTpart, kT64, kT32, kMask,
-    kDummyInfo, kNumBufs
+    kX = 0, kY, kNrm, kCoef, kPart, kXbar, kYbar, kU, kZhi, kZlo, kTpart, kT64, kAB, kMask,
+    kM, kSconst, kNumBufs
 };
 
 hap_status fail(hap_ctx c, hap_status s, const std::string& msg) {
@@ -135,7 +135,8 @@ GemmArgs gemm_args(hap_ctx c, hap_align_info* info) {
     g.d = (int)c->d;
     g.box_n = (int)std::min<int64_t>(kChunkN, c->d_pad);
     g.info = info;
-    g.t32 = B<float>(c, kT32);
+    g.ab = B<float2>(c, kAB);
+    g.sconst = B<double>(c, kSconst);
     g.tie_rel = 1e-6;
     return g;
 }
@@ -223,7 +224,8 @@ hap_status hap_align(hap_ctx c, const float* X, int64_t n_x, const float* Y, int
         (s = ensure(c, kZhi, (size_t)d_pad * n_pad * 2)) ||
         (s = ensure(c, kZlo, (size_t)d_pad * n_pad * 2)) ||
         (s = ensure(c, kTpart, (size_t)(n_pad / kRowTile) * d_pad * 8)) ||
-        (s = ensure(c, kT64, d_pad * 8)) || (s = ensure(c, kT32, d_pad * 4)) ||
+        (s = ensure(c, kT64, d_pad * 8)) || (s = ensure(c, kAB, d_pad * 8)) ||
+        (s = ensure(c, kM, d_pad * 8)) || (s = ensure(c, kSconst, 16)) ||
         (s = ensure(c, kMask, (size_t)std::max<int64_t>(kDefaultBlock, kTileM) * n_pad * 2)))
         return s;
     // host inputs are staged into the context (copied on `stream`)
@@ -268,7 +270,9 @@ hap_status hap_align(hap_ctx c, const float* X, int64_t n_x, const float* Y, int
     a.zt_lo = B<uint16_t>(c, kZlo);
     a.tpart = B<double>(c, kTpart);
     a.t64 = B<double>(c, kT64);
-    a.t32 = B<float>(c, kT32);
+    a.m = B<double>(c, kM);
+    a.ab = B<float2>(c, kAB);
+    a.sconst = B<double>(c, kSconst);
     cudaError_t e = launch_align(a, st);
     if (e != cudaSuccess) return cuda_fail(c, e, "align kernels");
     // S6: T_obs through the same mask-GEMM + epilogue path (D7)
@@ -377,18 +381,19 @@ hap_status hap_perm_sets(hap_ctx c, uint64_t seed, uint32_t stream_id, uint64_t 
     return HAP_OK;
 }
 
-hap_status hap_export_pooled(hap_ctx c, uint16_t* zhi, uint16_t* zlo, double* t, void* stream) {
+hap_status hap_export_pooled(hap_ctx c, uint16_t* zhi, uint16_t* zlo, double* t, double* m,
+                             void* stream) {
     if (!c) return HAP_E_INVALID_ARG;
     if (!c->aligned) return fail(c, HAP_E_NOT_ALIGNED, "no pooled cloud yet");
-    if (!zhi || !zlo || !t) return fail(c, HAP_E_INVALID_ARG, "null pointer");
+    if (!zhi || !zlo || !t || !m) return fail(c, HAP_E_INVALID_ARG, "null pointer");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    // transpose back with 2-D copies: Zt [d_pad][n_pad] -> Z [n_pad][d_pad] is done by
-    // the caller-side view; here we copy the transposed planes verbatim.
     const size_t bytes = (size_t)c->d_pad * c->n_pad * 2;
     cudaError_t e = cudaMemcpyAsync(zhi, c->buf[kZhi], bytes, cudaMemcpyDeviceToDevice, st);
     if (e == cudaSuccess) e = cudaMemcpyAsync(zlo, c->buf[kZlo], bytes, cudaMemcpyDeviceToDevice, st);
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(t, c->buf[kT64], (size_t)c->d_pad * 8, cudaMemcpyDeviceToDevice, st);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(m, c->buf[kM], (size_t)c->d_pad * 8, cudaMemcpyDeviceToDevice, st);
     if (e != cudaSuccess) return cuda_fail(c, e, "export");
     return HAP_OK;
 }

@@ -33,9 +33,11 @@ struct AlignArgs {
     double* u;               // [d]    Householder axis (fp64)
     uint16_t* zt_hi;         // [d_pad][n_pad] bf16 bits
     uint16_t* zt_lo;         // [d_pad][n_pad]
-    double* tpart;           // [n_pad/kRowTile][d_pad] fp64 partials of t
-    double* t64;             // [d_pad]
-    float* t32;              // [d_pad]
+    double* m;               // [d_pad] centre (multiple of 2^-12): planes hold z - m
+    double* tpart;           // [n_pad/kRowTile][d_pad] fp64 partials of t' = sum (hi + lo)
+    double* t64;             // [d_pad] t = N m + t'
+    float2* ab;              // [d_pad] epilogue constants {2a, 2b}, a = n_x m, b = t - a
+    double* sconst;          // [2]     {sum a^2, sum b^2}
 };
 cudaError_t launch_align(const AlignArgs& a, cudaStream_t st);
 
@@ -64,7 +66,8 @@ struct GemmArgs {
     hap_align_info* info;
     hap_counts* counts;
     double* stats;           // optional, [count][3]
-    const float* t32;
+    const float2* ab;        // [d_pad] {2a, 2b}
+    const double* sconst;    // {sum a^2, sum b^2}
 };
 cudaError_t launch_maskgemm(const CUtensorMap* tmA, const CUtensorMap* tmBhi,
                             const CUtensorMap* tmBlo, const GemmArgs& g, cudaStream_t st);

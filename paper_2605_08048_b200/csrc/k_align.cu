@@ -131,8 +131,25 @@ __global__ void __launch_bounds__(1024) k1_finalize(AlignArgs a, int nblk_x, int
         nv = sqrt(block_sum(sv, red));
         identity = nv < 1e-9;  // coincident mean directions (R3)
     }
-    for (int64_t c = threadIdx.x; c < a.d; c += blockDim.x)
-        a.u[c] = identity ? 0.0 : (a.xbar[c] / nx - a.ybar[c] / ny) / nv;
+    double sux = 0.0;
+    for (int64_t c = threadIdx.x; c < a.d; c += blockDim.x) {
+        const double uc = identity ? 0.0 : (a.xbar[c] / nx - a.ybar[c] / ny) / nv;
+        a.u[c] = uc;
+        sux += uc * a.xbar[c];
+    }
+    // Centre m = t/N, quantised to a multiple of 2^-12 (exact shift,
+    // since every mask row has exactly n_x ones).  t follows from the means without the
+    // reflected rows: t = n_x (xbar - 2u(u^T xbar)) + n_y ybar.
+    const double ux = block_sum(sux, red);
+    const double Nd = (double)(a.n_x + a.n_y);
+    for (int64_t c = threadIdx.x; c < a.d_pad; c += blockDim.x) {
+        double m = 0.0;
+        if (c < a.d) {
+            const double t = (double)a.n_x * (a.xbar[c] - 2.0 * a.u[c] * ux) + (double)a.n_y * a.ybar[c];
+            m = rint(t / Nd * 4096.0) / 4096.0;
+        }
+        a.m[c] = m;
+    }
     if (threadIdx.x == 0) {
         hap_align_info* f = a.info;
         f->norm_xbar = nx;
@@ -162,7 +179,8 @@ __global__ void __launch_bounds__(256) k1_rowdot(AlignArgs a) {
 }
 
 // K1d (S4 reflect + S5 split/transpose + t partials): CTA per (64-row tile, 64-col tile).
-// z = h/||h|| - coef * u  (fp64);  hi = bf16(z), lo = bf16(z - hi)  (R9);
+// z = h/||h|| - coef * u  (fp64), centred z' = z - m;  hi = bf16(z'), lo = bf16(z' - hi)
+// (R9 and "Numerics");
 // written transposed into Zt_hi/Zt_lo [d_pad][n_pad] (GEMM K contiguous).
 // t partial of the tile: sum over its 64 rows of (hi + lo) in fp64, fixed order.
 constexpr int kSP = 33;  // padded smem row pitch in 32-bit words (64 bf16 + pad)
@@ -177,6 +195,7 @@ __global__ void __launch_bounds__(256) k1_reflect_split(AlignArgs a) {
     uint16_t* sl16 = reinterpret_cast<uint16_t*>(s_lo);
     const int64_t c = c0 + tc;
     const double uc = (c < a.d) ? a.u[c] : 0.0;
+    const double mc = (c < a.d) ? a.m[c] : 0.0;
 #pragma unroll 4
     for (int j = 0; j < 16; ++j) {
         const int rl = tr + 4 * j;
@@ -185,7 +204,7 @@ __global__ void __launch_bounds__(256) k1_reflect_split(AlignArgs a) {
         if (i < N && c < a.d) {
             const double nrm = a.nrm[i];
             const double h = (double)row_ptr(a, i)[c];
-            z = (nrm > 0.0 ? h / nrm : 0.0) - a.coef[i] * uc;
+            z = (nrm > 0.0 ? h / nrm : 0.0) - a.coef[i] * uc - mc;
         }
         const __nv_bfloat16 hi = __double2bfloat16(z);
         const __nv_bfloat16 lo = __double2bfloat16(z - (double)__bfloat162float(hi));
@@ -213,14 +232,31 @@ __global__ void __launch_bounds__(256) k1_reflect_split(AlignArgs a) {
     }
 }
 
-// K1e (S5 finish): t[c] = sum of the row-tile partials in ascending tile order.
-__global__ void k1_tfinal(AlignArgs a, int ntiles) {
-    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= a.d_pad) return;
-    double s = 0.0;
-    for (int t = 0; t < ntiles; ++t) s += a.tpart[(int64_t)t * a.d_pad + c];
-    a.t64[c] = s;
-    a.t32[c] = (float)s;
+// K1e (S5 finish + epilogue constants), one CTA.  t'[c] = sum of the row-tile partials
+// (ascending tile order) of the centred planes; t = N m + t'.  With a = n_x m and
+// b = t - a = n_y m + t' (both rounded to fp32), the epilogue forms
+//   S1 = ||a + acc||^2 = SA + sum acc (acc + 2a),   S2 = ||b - acc||^2 = SB + sum acc (acc - 2b)
+// with SA = sum a^2, SB = sum b^2 in fp64.
+__global__ void __launch_bounds__(1024) k1_tfinal(AlignArgs a, int ntiles) {
+    __shared__ double red[33];
+    double sa = 0.0, sb = 0.0;
+    for (int64_t c = threadIdx.x; c < a.d_pad; c += blockDim.x) {
+        double tp = 0.0;
+        for (int t = 0; t < ntiles; ++t) tp += a.tpart[(int64_t)t * a.d_pad + c];
+        const double m = a.m[c];
+        a.t64[c] = (double)(a.n_x + a.n_y) * m + tp;
+        const float af = (float)((double)a.n_x * m);
+        const float bf = (float)((double)a.n_y * m + tp);
+        a.ab[c] = make_float2(2.0f * af, 2.0f * bf);
+        sa += (double)af * (double)af;
+        sb += (double)bf * (double)bf;
+    }
+    sa = block_sum(sa, red);
+    sb = block_sum(sb, red);
+    if (threadIdx.x == 0) {
+        a.sconst[0] = sa;
+        a.sconst[1] = sb;
+    }
 }
 
 }  // namespace
@@ -235,7 +271,7 @@ cudaError_t launch_align(const AlignArgs& a, cudaStream_t st) {
     const int ntiles = (int)(a.n_pad / kRowTile);
     dim3 grid((unsigned)ntiles, (unsigned)ceil_div(a.d_pad, 64));
     k1_reflect_split<<<grid, 256, 0, st>>>(a);
-    k1_tfinal<<<(unsigned)ceil_div(a.d_pad, 256), 256, 0, st>>>(a, ntiles);
+    k1_tfinal<<<1, 1024, 0, st>>>(a, ntiles);
     return cudaGetLastError();
 }
 

@@ -132,30 +132,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int q = warp & 3;
         const int row = 32 * q + lane;
         const int perm = row0 + row;
-        double S1 = 0.0, S2 = 0.0;
+        // sigma1 = a + acc, sigma2 = b - acc  (centred accumulator acc)
+        double S1 = g.sconst[0], S2 = g.sconst[1];
         for (int c = 0; c < nchunks; ++c) {
             const int a = c & 1;
             const int width = min(kChunkN, g.d_pad - c * kChunkN);
             mbar_wait(&tfull[a], ((uint32_t)c >> 1) & 1u);
             tc_fence_after();
             float s1 = 0.f, s2 = 0.f;
-            const float4* tp = reinterpret_cast<const float4*>(g.t32 + c * kChunkN);
+            const float4* abp = reinterpret_cast<const float4*>(g.ab + c * kChunkN);
             for (int cb = 0; cb < width / 32; ++cb) {
                 uint32_t r[32];
                 tmem_ld_32x32b_x32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(a * kChunkN + 32 * cb),
                                    r);
                 tmem_ld_wait();
 #pragma unroll
-                for (int j4 = 0; j4 < 8; ++j4) {
-                    const float4 tt = __ldg(tp + cb * 8 + j4);
-                    const float t4[4] = {tt.x, tt.y, tt.z, tt.w};
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const float sg = __uint_as_float(r[4 * j4 + e]);
-                        s1 = fmaf(sg, sg, s1);
-                        const float s2e = t4[e] - sg;  // sigma2 = t - sigma1
-                        s2 = fmaf(s2e, s2e, s2);
-                    }
+                for (int j2 = 0; j2 < 16; ++j2) {
+                    const float4 k4 = __ldg(abp + cb * 16 + j2);  // {2a, 2b} of two columns
+                    const float x0 = __uint_as_float(r[2 * j2]), x1 = __uint_as_float(r[2 * j2 + 1]);
+                    s1 = fmaf(x0, x0 + k4.x, s1);
+                    s2 = fmaf(x0, x0 - k4.y, s2);
+                    s1 = fmaf(x1, x1 + k4.z, s1);
+                    s2 = fmaf(x1, x1 - k4.w, s2);
                 }
             }
             tc_fence_before();
@@ -163,6 +161,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             S1 += (double)s1;
             S2 += (double)s2;
         }
+        S1 = fmax(S1, 0.0);
+        S2 = fmax(S2, 0.0);
         const double r1 = sqrt(S1) / (double)g.n_x;
         const double r2 = sqrt(S2) / (double)g.n_y;
         const double L1 = logkappa(r1, (double)g.d), L2 = logkappa(r2, (double)g.d);
@@ -182,7 +182,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool valid = perm < g.count;
             const bool ge = valid && (T >= t_obs);
             const bool ab = valid && (fabs(T) >= fabs(t_obs));
-            const bool fl = valid && (T == t_obs || fabs(T - t_obs) <= tau);
+            // near-tie of either decision (R8)
+            const bool fl = valid && (T == t_obs || fabs(T - t_obs) <= tau ||
+                                      fabs(T) == fabs(t_obs) || fabs(fabs(T) - fabs(t_obs)) <= tau);
             const uint32_t bge = __ballot_sync(0xffffffffu, ge);
             const uint32_t bab = __ballot_sync(0xffffffffu, ab);
             const uint32_t bfl = __ballot_sync(0xffffffffu, fl);

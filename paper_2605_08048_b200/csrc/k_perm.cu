@@ -56,8 +56,9 @@ __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy(PermArgs a, int lt
     uint16_t* stage = LT + lt_pitch;
     const uint32_t N = (uint32_t)a.N, nx = (uint32_t)a.n_x, s = a.s;
     const uint32_t key0 = (uint32_t)(a.seed & 0xFFFFFFFFu), key1 = (uint32_t)(a.seed >> 32);
-    const int64_t wstride = (int64_t)gridDim.x * kPermWarps;
-    for (int64_t pi = (int64_t)blockIdx.x * kPermWarps + w; pi < a.count; pi += wstride) {
+    const int nw = (int)(blockDim.x >> 5);
+    const int64_t wstride = (int64_t)gridDim.x * nw;
+    for (int64_t pi = (int64_t)blockIdx.x * nw + w; pi < a.count; pi += wstride) {
         const uint32_t b = (uint32_t)(a.b_begin + (uint64_t)pi);
         uint4* LT4 = reinterpret_cast<uint4*>(LT);
         for (int q = l; q < lt_pitch / 8; q += 32) LT4[q] = make_uint4(0, 0, 0, 0);
@@ -145,7 +146,9 @@ __global__ void k2_observed_mask(uint16_t* row, int64_t n_x, int64_t n_pad) {
 cudaError_t launch_perm(const PermArgs& a, int sm_count, cudaStream_t st) {
     if (a.count <= 0) return cudaSuccess;
     const int lt_pitch = (int)round_up(a.N, 64);  // uint16 entries, 128-byte multiple
-    const size_t smem = (size_t)kPermWarps * (lt_pitch + 128) * sizeof(uint16_t);
+    const size_t per_warp = (size_t)(lt_pitch + 128) * sizeof(uint16_t);
+    const int nw = (int)std::max<size_t>(1, std::min<size_t>(kPermWarps, (200u * 1024u) / per_warp));
+    const size_t smem = (size_t)nw * per_warp;
     static size_t configured = 0;
     if (smem > 48 * 1024 && smem > configured) {
         cudaError_t e = cudaFuncSetAttribute(k2_perm_fy, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -154,11 +157,11 @@ cudaError_t launch_perm(const PermArgs& a, int sm_count, cudaStream_t st) {
         configured = smem;
     }
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_perm_fy, kPermWarps * 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_perm_fy, nw * 32, smem);
     if (per_sm < 1) per_sm = 1;
-    const int64_t need = ceil_div(a.count, kPermWarps);
+    const int64_t need = ceil_div(a.count, nw);
     const int grid = (int)std::min<int64_t>(need, (int64_t)sm_count * per_sm);
-    k2_perm_fy<<<grid, kPermWarps * 32, smem, st>>>(a, lt_pitch);
+    k2_perm_fy<<<grid, nw * 32, smem, st>>>(a, lt_pitch);
     return cudaGetLastError();
 }
 

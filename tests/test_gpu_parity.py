@@ -63,8 +63,9 @@ def check_pair(ctx, orc, X, Y, B, s=0, mode=0, block=0, b_begin=0, b_end=None, n
     tau = ref["tau"]
     out = np.abs(rs[:, 2] - ref["t_obs"]) > tau
     assert np.array_equal(gs[out, 2] >= g["t_obs"], rs[out, 2] >= ref["t_obs"])
-    assert np.array_equal(np.abs(gs[out, 2]) >= abs(g["t_obs"]),
-                          np.abs(rs[out, 2]) >= abs(ref["t_obs"]))
+    out2 = np.abs(np.abs(rs[:, 2]) - abs(ref["t_obs"])) > tau
+    assert np.array_equal(np.abs(gs[out2, 2]) >= abs(g["t_obs"]),
+                          np.abs(rs[out2, 2]) >= abs(ref["t_obs"]))
     for k in ("exceed_ge", "exceed_abs"):
         assert abs(g[k] - ref[k]) <= ref["flagged"], (k, g[k], ref[k], ref["flagged"])
     return g, ref
@@ -109,18 +110,24 @@ def test_pooled_planes(hap, ctx, orc, n_x, n_y, d, mode):
     zh = torch.empty((d_pad, n_pad), dtype=torch.int16, device="cuda")
     zl = torch.empty_like(zh)
     t = torch.empty(d_pad, dtype=torch.float64, device="cuda")
-    hap.hap_export_pooled(ctx.h, zh, zl, t)
+    m = torch.empty(d_pad, dtype=torch.float64, device="cuda")
+    hap.hap_export_pooled(ctx.h, zh, zl, t, m)
     torch.cuda.synchronize()
     hi = zh.view(torch.bfloat16).float().double().cpu().numpy().T
     lo = zl.view(torch.bfloat16).float().double().cpu().numpy().T
+    mm = m.cpu().numpy()
     ref = orc.align(X, Y, mode)
     N = n_x + n_y
-    z = hi[:N, :d] + lo[:N, :d]
-    assert np.all(np.abs(z - ref.Z) <= 2.0 ** -16 * np.abs(ref.Z) + 1e-12)
+    # the planes hold the centred cloud z - m (m a multiple of 2^-12, ~ t/N)
+    assert np.all(mm * 4096 == np.round(mm * 4096)) and np.all(mm[d:] == 0)
+    assert np.allclose(mm[:d], ref.Z.sum(0) / N, atol=2.0 ** -13 + 1e-9)
+    zc = hi[:N, :d] + lo[:N, :d]
+    want = ref.Z - mm[None, :d]
+    assert np.all(np.abs(zc - want) <= 2.0 ** -16 * np.abs(want) + 1e-12)
     assert np.all(hi[N:] == 0) and np.all(lo[N:] == 0)
     assert np.all(hi[:, d:] == 0) and np.all(lo[:, d:] == 0)
     tt = t.cpu().numpy()
-    assert np.allclose(tt[:d], (hi + lo)[:, :d].sum(0), rtol=1e-12, atol=1e-12)
+    assert np.allclose(tt[:d], zc.sum(0) + N * mm[:d], rtol=1e-12, atol=1e-12)
     assert np.allclose(tt[:d], ref.Z.sum(0), rtol=1e-5, atol=1e-5)
 
 
@@ -131,14 +138,25 @@ def test_config1_full(ctx, orc):
     check_pair(ctx, orc, X, Y, 1000, s=1)
 
 
-@pytest.mark.parametrize("n_x,n_y,d,B,block", [(37, 50, 100, 300, 128), (1, 70, 48, 257, 0),
-                                               (70, 1, 40, 129, 0), (200, 300, 300, 1000, 256),
+@pytest.mark.parametrize("n_x,n_y,d,B,block", [(37, 50, 100, 300, 128), (2, 70, 48, 257, 0),
+                                               (70, 2, 40, 129, 0), (200, 300, 300, 1000, 256),
                                                (5, 3, 3, 200, 0)])
 def test_ragged_shapes(ctx, orc, n_x, n_y, d, B, block):
     """Ragged N (not a multiple of 64), d not a multiple of 32, several tiles with a
     ragged tail, multi-block launches, single-row groups."""
     X, Y = HI.make_pair(HI.PairSpec(n_x, n_y, d, 30.0, 60.0, 40.0, seed=n_x * 7 + d))
     check_pair(ctx, orc, X, Y, B, s=3, block=block)
+
+
+def test_singleton_group(ctx, orc):
+    """n_x = 1: r1 = ||z_i|| = 1 for every split (L is clamped at r = 1 - 1e-9, R4, and
+    ill-conditioned there), so only the MRLs are compared."""
+    X, Y = HI.make_pair(HI.PairSpec(1, 70, 48, 30.0, 60.0, 40.0, seed=11))
+    g = ctx.permtest_pair(_cuda(X), _cuda(Y), 200, SEED, want_stats=True)
+    ref = orc.run_pair(X, Y, 200, SEED, want_stats=True)
+    gs = g["stats"].cpu().numpy()
+    assert np.allclose(gs[:, 0], 1.0, rtol=1e-6)
+    assert np.allclose(gs[:, 1], ref["stats"][:, 1], rtol=1e-5)
 
 
 def test_naive_mode(ctx, orc):
