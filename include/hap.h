@@ -149,6 +149,24 @@ HAP_API hap_status hap_permtest_batch(hap_ctx ctx, int64_t P, const float* X_pac
 /* p = (1 + c)/(B + 1)  (Eq. pvalue). */
 HAP_API double hap_pvalue(uint64_t exceed, uint64_t B);
 
+/* ---- live profiling (bench.py) ---------------------------------------------------- */
+/* Phases of the hot path, for per-kernel timing and launch counting. */
+typedef enum {
+    HAP_PHASE_ALIGN = 0,     /* K1 kernels (S1-S5) */
+    HAP_PHASE_OBSERVED = 1,  /* observed-split mask + mask-GEMM (S6) */
+    HAP_PHASE_PERMGEN = 2,   /* K2 permutation generator (S7) */
+    HAP_PHASE_MASKGEMM = 3,  /* K3 mask-GEMM + statistic epilogue (S8-S9) */
+    HAP_NUM_PHASES = 4
+} hap_phase;
+/* enable != 0: every later launch of the context is bracketed by CUDA events recorded on
+ * its own stream (adds host work; leave off when timing whole steps). */
+HAP_API hap_status hap_profile(hap_ctx ctx, int enable);
+/* Synchronises the recorded events and returns, per phase, the summed device time (ms,
+ * [host] double[HAP_NUM_PHASES]) of the launches timed since the last reset and the number
+ * of kernel launches issued ([host] int64_t[HAP_NUM_PHASES], counted whether or not timing
+ * is enabled).  reset != 0 clears both. */
+HAP_API hap_status hap_profile_read(hap_ctx ctx, double* ms, int64_t* launches, int reset);
+
 /* ---- introspection for parity tests (same kernels as the hot path) -------------- */
 /* PERM-SPEC v1 sets for b in [b_begin, b_begin+count): out [device] count*N uint8
  * membership (1 = group 1), produced by the product's generator kernel. */

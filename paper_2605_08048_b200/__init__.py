@@ -83,6 +83,8 @@ def lib() -> ctypes.CDLL:
         "hap_pvalue": ([u64, u64], f64),
         "hap_perm_sets": ([vp, u64, u32, u64, i64, i64, i64, vp, vp], i32),
         "hap_export_pooled": ([vp, vp, vp, vp, vp, vp], i32),
+        "hap_profile": ([vp, i32], i32),
+        "hap_profile_read": ([vp, P(f64), P(i64), i32], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -192,6 +194,21 @@ def hap_perm_sets(ctx, seed: int, stream_id: int, b_begin: int, count: int, N: i
 def hap_export_pooled(ctx, zhi, zlo, t, m, stream=None) -> None:
     _check(ctx, lib().hap_export_pooled(ctx, _ptr(zhi), _ptr(zlo), _ptr(t), _ptr(m),
                                         _stream(stream)))
+
+
+PHASES = ("align", "observed", "permgen", "maskgemm")
+
+
+def hap_profile(ctx, enable: bool) -> None:
+    _check(ctx, lib().hap_profile(ctx, 1 if enable else 0))
+
+
+def hap_profile_read(ctx, reset: bool = False):
+    """-> ({phase: ms}, {phase: launches}) (synchronises the recorded events)."""
+    ms = (ctypes.c_double * len(PHASES))()
+    n = (ctypes.c_int64 * len(PHASES))()
+    _check(ctx, lib().hap_profile_read(ctx, ms, n, 1 if reset else 0))
+    return dict(zip(PHASES, list(ms))), dict(zip(PHASES, list(n)))
 
 
 # ----------------------------------------------------------------- conveniences

@@ -9,6 +9,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <vector>
 
 #include "hap_internal.h"
 
@@ -30,6 +31,13 @@ struct hap_ctx_s {
     CUtensorMap tmA{}, tmBhi{}, tmBlo{};
     const void* tm_key[3] = {};
     int64_t tm_shape[3] = {};
+    // ---- profiling
+    bool prof = false;
+    struct Mark { cudaEvent_t a, b; int phase; };
+    std::vector<Mark> marks;
+    std::vector<cudaEvent_t> pool;
+    int64_t launches[HAP_NUM_PHASES] = {};
+    double ms[HAP_NUM_PHASES] = {};
 };
 
 namespace {
@@ -143,6 +151,42 @@ GemmArgs gemm_args(hap_ctx c, hap_align_info* info) {
 
 constexpr int64_t kDefaultBlock = 8192;
 
+cudaEvent_t take_event(hap_ctx c) {
+    if (!c->pool.empty()) {
+        cudaEvent_t e = c->pool.back();
+        c->pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// Brackets the launches issued in its scope: counts them and, when profiling is on,
+// records a start/stop event pair on the launching stream.
+struct PhaseScope {
+    hap_ctx c;
+    int phase;
+    int nlaunch;
+    cudaStream_t st;
+    cudaEvent_t a = nullptr;
+    PhaseScope(hap_ctx c_, int phase_, int nlaunch_, cudaStream_t st_)
+        : c(c_), phase(phase_), nlaunch(nlaunch_), st(st_) {
+        if (c->prof) {
+            a = take_event(c);
+            cudaEventRecord(a, st);
+        }
+    }
+    ~PhaseScope() {
+        c->launches[phase] += nlaunch;
+        if (a) {
+            cudaEvent_t b = take_event(c);
+            cudaEventRecord(b, st);
+            c->marks.push_back({a, b, phase});
+        }
+    }
+};
+
 }  // namespace
 
 extern "C" {
@@ -175,6 +219,11 @@ hap_status hap_destroy(hap_ctx c) {
     if (c->last_stream) cudaStreamSynchronize(c->last_stream);
     for (void* p : c->buf)
         if (p) cudaFree(p);
+    for (auto& m : c->marks) {
+        cudaEventDestroy(m.a);
+        cudaEventDestroy(m.b);
+    }
+    for (auto e : c->pool) cudaEventDestroy(e);
     delete c;
     return HAP_OK;
 }
@@ -273,15 +322,23 @@ hap_status hap_align(hap_ctx c, const float* X, int64_t n_x, const float* Y, int
     a.m = B<double>(c, kM);
     a.ab = B<float2>(c, kAB);
     a.sconst = B<double>(c, kSconst);
-    cudaError_t e = launch_align(a, st);
+    cudaError_t e;
+    {
+        PhaseScope ps(c, HAP_PHASE_ALIGN, kAlignLaunches, st);
+        e = launch_align(a, st);
+    }
     if (e != cudaSuccess) return cuda_fail(c, e, "align kernels");
     // S6: T_obs through the same mask-GEMM + epilogue path (D7)
-    e = launch_observed_mask(B<uint16_t>(c, kMask), n_x, n_pad, st);
-    if (e != cudaSuccess) return cuda_fail(c, e, "observed mask");
-    GemmArgs g = gemm_args(c, info);
-    g.count = 1;
-    g.observed = 1;
-    e = launch_maskgemm(&c->tmA, &c->tmBhi, &c->tmBlo, g, st);
+    {
+        PhaseScope ps(c, HAP_PHASE_OBSERVED, 2, st);
+        e = launch_observed_mask(B<uint16_t>(c, kMask), n_x, n_pad, st);
+        if (e == cudaSuccess) {
+            GemmArgs g = gemm_args(c, info);
+            g.count = 1;
+            g.observed = 1;
+            e = launch_maskgemm(&c->tmA, &c->tmBhi, &c->tmBlo, g, st);
+        }
+    }
     if (e != cudaSuccess) return cuda_fail(c, e, "observed mask-GEMM");
     c->aligned = true;
     c->last_stream = st;
@@ -323,12 +380,19 @@ hap_status hap_permtest(hap_ctx c, const hap_align_info* info, const hap_perm_cf
         pa.out = c->buf[kMask];
         pa.out_kind = kMaskBf16Row;
         pa.info = info;
-        cudaError_t e = launch_perm(pa, c->sm_count, st);
+        cudaError_t e;
+        {
+            PhaseScope ps(c, HAP_PHASE_PERMGEN, 1, st);
+            e = launch_perm(pa, c->sm_count, st);
+        }
         if (e != cudaSuccess) return cuda_fail(c, e, "perm generator");
         g.count = (int)cnt;
         g.observed = 0;
         g.stats = stats ? stats + 3 * off : nullptr;
-        e = launch_maskgemm(&c->tmA, &c->tmBhi, &c->tmBlo, g, st);
+        {
+            PhaseScope ps(c, HAP_PHASE_MASKGEMM, 1, st);
+            e = launch_maskgemm(&c->tmA, &c->tmBhi, &c->tmBlo, g, st);
+        }
         if (e != cudaSuccess) return cuda_fail(c, e, "mask-GEMM");
     }
     c->last_stream = st;
@@ -354,6 +418,36 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
         pc.stream_id = cfg->stream_id + (uint32_t)p;
         s = hap_permtest(c, infos + p, &pc, counts + p, nullptr, stream);
         if (s) return s;
+    }
+    return HAP_OK;
+}
+
+hap_status hap_profile(hap_ctx c, int enable) {
+    if (!c) return HAP_E_INVALID_ARG;
+    c->prof = enable != 0;
+    return HAP_OK;
+}
+
+hap_status hap_profile_read(hap_ctx c, double* ms, int64_t* launches, int reset) {
+    if (!c) return HAP_E_INVALID_ARG;
+    cudaSetDevice(c->device);
+    for (auto& m : c->marks) {
+        float t = 0.f;
+        cudaError_t e = cudaEventSynchronize(m.b);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&t, m.a, m.b);
+        if (e != cudaSuccess) return cuda_fail(c, e, "profile events");
+        c->ms[m.phase] += t;
+        c->pool.push_back(m.a);
+        c->pool.push_back(m.b);
+    }
+    c->marks.clear();
+    for (int p = 0; p < HAP_NUM_PHASES; ++p) {
+        if (ms) ms[p] = c->ms[p];
+        if (launches) launches[p] = c->launches[p];
+        if (reset) {
+            c->ms[p] = 0.0;
+            c->launches[p] = 0;
+        }
     }
     return HAP_OK;
 }

@@ -40,6 +40,7 @@ struct AlignArgs {
     double* sconst;          // [2]     {sum a^2, sum b^2}
 };
 cudaError_t launch_align(const AlignArgs& a, cudaStream_t st);
+constexpr int kAlignLaunches = 6;  // kernels issued by launch_align
 
 // ---- K2: PERM-SPEC v1 generator (k_perm.cu) ----------------------------------------
 enum MaskOut { kMaskBf16Row = 0, kMaskU8Set = 1 };

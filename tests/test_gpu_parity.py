@@ -179,14 +179,16 @@ def test_config3_sampled(ctx, orc):
 
 
 def test_worked_example_counts_exact(ctx, orc):
-    """SURVEY worked example (d=3): T values are >= 0.0155 apart, so the counts must be
-    identical, and the MC p approaches the exhaustive 12/70."""
+    """SURVEY worked example (d=3): T values are >= 0.0155 apart from T_obs, so the
+    one-sided count must be identical, and the MC p approaches the exhaustive 12/70.
+    (With n_x = n_y the complement split has T = -T_obs exactly: a true two-sided tie,
+    which the tie band flags, so the two-sided count is only checked within `flagged`.)"""
     from conftest import read_golden
     rows = read_golden("worked_example.txt")
     X = np.array([[float(v) for v in r.split()[1:]] for r in rows if r.startswith("X ")], np.float32)
     Y = np.array([[float(v) for v in r.split()[1:]] for r in rows if r.startswith("Y ")], np.float32)
     g, ref = check_pair(ctx, orc, X, Y, 20000)
-    assert g["exceed_ge"] == ref["exceed_ge"] and g["exceed_abs"] == ref["exceed_abs"]
+    assert g["exceed_ge"] == ref["exceed_ge"]
     assert abs(g["exceed_ge"] / 20000 - 12 / 70) < 4 * math.sqrt(12 / 70 * 58 / 70 / 20000)
 
 
