@@ -67,11 +67,14 @@ typedef struct {
     int32_t is_identity;      /* 1 if ||mu_x - mu_y|| < 1e-9 (no reflection; R3) or mode NONE */
     int32_t status;           /* hap_status of the device-side data checks */
     int64_t bad_row;          /* pooled row index of a ZeroVector error, else -1 */
-    double norm_xbar;         /* ||xbar|| = r(X) = r(X') in fp64 (Eq. 8) */
-    double norm_ybar;         /* ||ybar|| = r(Y) */
-    double r_x, r_y;          /* MRLs of the observed split through the mask-GEMM path (D7) */
-    double logk_x, logk_y;    /* L(r) = log kappa-hat(r) = -log v (Eq. 9; R1) */
-    double t_obs;             /* T_obs = log v(X') - log v(Y) = logk_y - logk_x (Eq. 10) */
+    double r_x, r_y;          /* MRLs ||xbar||, ||ybar|| in fp64 (Eq. 8; r(X') = r(X), :161) */
+    double logk_x, logk_y;    /* L(r) = log kappa-hat(r) = -log v (Eq. 9; R1, R4) */
+    double t_obs;             /* T_obs = log v(X') - log v(Y) = logk_y - logk_x (Eq. 10), fp64 */
+    /* the observed split evaluated through the mask-GEMM + epilogue path (row 0 of every
+     * tile, D7): the value hap_permtest compares each T_b against, so that a
+     * permutation that redraws the observed split ties it bit-exactly.  Written by
+     * hap_permtest (NaN until then). */
+    double gemm_r_x, gemm_r_y, gemm_t_obs;
 } hap_align_info;
 
 /* One test's permutation configuration (PERM-SPEC v1, R6). */
@@ -82,6 +85,8 @@ typedef struct {
     uint64_t b_end;
     uint32_t stream_id; /* s: third Philox counter word (pair id by default) */
     uint32_t block;     /* B0 permutations per generator/GEMM block; perf only, 0 = auto */
+    int32_t pair_mode;  /* K3 CTA grouping: 0 = auto (2), 1 = cta_group::1, 2 = cta_group::2 */
+    int32_t reserved0;
     double tie_rel;     /* tie band tau = tie_rel * (|logk_x| + |logk_y|) (R8); <= 0 -> 1e-6 */
     uint32_t flags;     /* reserved, 0 */
     uint32_t reserved;
@@ -113,8 +118,8 @@ HAP_API const char* hap_last_error(hap_ctx ctx);
  * Builds, in the context workspace, the pooled aligned cloud Z = [X'; Y]
  * as the transposed bf16 hi/lo planes Zt_hi, Zt_lo (d_pad x n_pad, K contiguous) with
  * hi = bf16(z), lo = bf16(z - hi) (PAPER.md:258 precision note; R9), the total
- * t = 1^T Z (Eq. gemm), then evaluates T_obs on the observed split
- * through the same mask-GEMM + epilogue path as the permutations (D7).
+ * t = 1^T Z (Eq. gemm) and the observed statistic r_x, r_y, logk_x,
+ * logk_y, t_obs in fp64 (Alg. 1 step 4).
  * Constraints: 1 <= n_x, n_y; n_x + n_y <= 65535; 2 <= d <= 16384. */
 HAP_API hap_status hap_align(hap_ctx ctx, const float* X, int64_t n_x, const float* Y, int64_t n_y,
                      int64_t d, hap_align_mode mode, hap_align_info* info, void* stream);
@@ -124,11 +129,12 @@ HAP_API hap_status hap_align(hap_ctx ctx, const float* X, int64_t n_x, const flo
  * [cfg->b_begin, cfg->b_end) draws the PERM-SPEC v1 group-1 set G_b, forms sigma1 =
  * sum_{i in G_b} z_i with the tcgen05 mask-GEMM, sigma2 = t - sigma1,
  * r1 = ||sigma1||/n_x, r2 = ||sigma2||/n_y, T_b = L(r2) - L(r1) and ADDS
- * the three comparisons against info->t_obs into *counts.  Uses the Z from the last
- * hap_align on this context; `info` must be that call's info.
+ * the three comparisons against T_obs into *counts, T_obs being evaluated through the
+ * same GEMM path on the observed split (written to info->gemm_*).  Uses the Z from the
+ * last hap_align on this context; `info` must be that call's info (device, updated).
  *   counts [device] hap_counts, added into.
  *   stats  [device] optional (NULL = none): (b_end-b_begin)*3 doubles {r1, r2, T_b}. */
-HAP_API hap_status hap_permtest(hap_ctx ctx, const hap_align_info* info, const hap_perm_cfg* cfg,
+HAP_API hap_status hap_permtest(hap_ctx ctx, hap_align_info* info, const hap_perm_cfg* cfg,
                         hap_counts* counts, double* stats, void* stream);
 
 /* ---- many word pairs ------------------------------------------------------------ */
@@ -153,7 +159,7 @@ HAP_API double hap_pvalue(uint64_t exceed, uint64_t B);
 /* Phases of the hot path, for per-kernel timing and launch counting. */
 typedef enum {
     HAP_PHASE_ALIGN = 0,     /* K1 kernels (S1-S5) */
-    HAP_PHASE_OBSERVED = 1,  /* observed-split mask + mask-GEMM (S6) */
+    HAP_PHASE_OBSERVED = 1,  /* reserved (S6 runs inside K1 and, through the GEMM, in K3) */
     HAP_PHASE_PERMGEN = 2,   /* K2 permutation generator (S7) */
     HAP_PHASE_MASKGEMM = 3,  /* K3 mask-GEMM + statistic epilogue (S8-S9) */
     HAP_NUM_PHASES = 4

@@ -34,16 +34,18 @@ class hap_align_info(ctypes.Structure):
     _fields_ = [("n_x", ctypes.c_int64), ("n_y", ctypes.c_int64), ("d", ctypes.c_int64),
                 ("n_pad", ctypes.c_int64), ("d_pad", ctypes.c_int64),
                 ("is_identity", ctypes.c_int32), ("status", ctypes.c_int32),
-                ("bad_row", ctypes.c_int64), ("norm_xbar", ctypes.c_double),
-                ("norm_ybar", ctypes.c_double), ("r_x", ctypes.c_double),
+                ("bad_row", ctypes.c_int64), ("r_x", ctypes.c_double),
                 ("r_y", ctypes.c_double), ("logk_x", ctypes.c_double),
-                ("logk_y", ctypes.c_double), ("t_obs", ctypes.c_double)]
+                ("logk_y", ctypes.c_double), ("t_obs", ctypes.c_double),
+                ("gemm_r_x", ctypes.c_double), ("gemm_r_y", ctypes.c_double),
+                ("gemm_t_obs", ctypes.c_double)]
 
 
 class hap_perm_cfg(ctypes.Structure):
     _fields_ = [("seed", ctypes.c_uint64), ("B", ctypes.c_uint64), ("b_begin", ctypes.c_uint64),
                 ("b_end", ctypes.c_uint64), ("stream_id", ctypes.c_uint32),
-                ("block", ctypes.c_uint32), ("tie_rel", ctypes.c_double),
+                ("block", ctypes.c_uint32), ("pair_mode", ctypes.c_int32),
+                ("reserved0", ctypes.c_int32), ("tie_rel", ctypes.c_double),
                 ("flags", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
 
 
@@ -150,9 +152,10 @@ def hap_align(ctx, X, Y, mode: int, info, stream=None) -> None:
 
 
 def make_cfg(seed: int, B: int, b_begin: int = 0, b_end: int | None = None, stream_id: int = 0,
-             block: int = 0, tie_rel: float = 1e-6) -> hap_perm_cfg:
+             block: int = 0, tie_rel: float = 1e-6, pair_mode: int = 0) -> hap_perm_cfg:
     return hap_perm_cfg(seed=seed, B=B, b_begin=b_begin, b_end=B if b_end is None else b_end,
-                        stream_id=stream_id, block=block, tie_rel=tie_rel, flags=0, reserved=0)
+                        stream_id=stream_id, block=block, pair_mode=pair_mode, reserved0=0,
+                        tie_rel=tie_rel, flags=0, reserved=0)
 
 
 def hap_permtest(ctx, info, cfg: hap_perm_cfg, counts, stats=None, stream=None) -> None:
@@ -242,7 +245,8 @@ class Context:
 
     def permtest_pair(self, X, Y, B: int, seed: int, stream_id: int = 0, mode: int = 0,
                       b_begin: int = 0, b_end: int | None = None, tie_rel: float = 1e-6,
-                      block: int = 0, want_stats: bool = False, sync: bool = True):
+                      block: int = 0, want_stats: bool = False, sync: bool = True,
+                      pair_mode: int = 0):
         """One word-pair test end to end: hap_align + hap_permtest (+ p-value)."""
         torch = self.torch
         b_end = B if b_end is None else b_end
@@ -250,7 +254,7 @@ class Context:
         hap_align(self.h, X, Y, mode, self.info)
         stats = (torch.empty((b_end - b_begin, 3), dtype=torch.float64, device=self.device)
                  if want_stats else None)
-        cfg = make_cfg(seed, B, b_begin, b_end, stream_id, block, tie_rel)
+        cfg = make_cfg(seed, B, b_begin, b_end, stream_id, block, tie_rel, pair_mode)
         hap_permtest(self.h, self.info, cfg, self.counts, stats)
         if not sync:
             return None
@@ -260,7 +264,8 @@ class Context:
             raise HapError(st, hap_last_error(self.h))
         c = self.counts.cpu().tolist()
         out = dict(t_obs=info.t_obs, r_x=info.r_x, r_y=info.r_y, logk_x=info.logk_x,
-                   logk_y=info.logk_y, norm_xbar=info.norm_xbar, norm_ybar=info.norm_ybar,
+                   logk_y=info.logk_y, gemm_t_obs=info.gemm_t_obs, gemm_r_x=info.gemm_r_x,
+                   gemm_r_y=info.gemm_r_y,
                    is_identity=bool(info.is_identity), exceed_ge=c[0], exceed_abs=c[1],
                    flagged=c[2], B=B, p_value=hap_pvalue(c[0], B),
                    p_two_sided=hap_pvalue(c[1], B))

@@ -30,7 +30,7 @@ struct hap_ctx_s {
     // ---- TMA descriptors (valid for the current buffers/shape)
     CUtensorMap tmA{}, tmBhi{}, tmBlo{};
     const void* tm_key[3] = {};
-    int64_t tm_shape[3] = {};
+    int64_t tm_shape[4] = {};
     // ---- profiling
     bool prof = false;
     struct Mark { cudaEvent_t a, b; int phase; };
@@ -44,7 +44,7 @@ namespace {
 
 enum Buf {
     kX = 0, kY, kNrm, kCoef, kPart, kXbar, kYbar, kU, kZhi, kZlo, kTpart, kT64, kAB, kMask,
-    kM, kSconst, kNumBufs
+    kM, kSconst, kGemmPart, kTileDone, kNumBufs
 };
 
 hap_status fail(hap_ctx c, hap_status s, const std::string& msg) {
@@ -72,6 +72,7 @@ hap_status ensure(hap_ctx c, int which, size_t bytes) {
         cudaGetLastError();
         return fail(c, HAP_E_OOM, std::string("cudaMalloc failed: ") + cudaGetErrorString(e));
     }
+    cudaMemset(c->buf[which], 0, alloc);
     c->cap[which] = alloc;
     return HAP_OK;
 }
@@ -118,19 +119,22 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows, u
 }
 
 int64_t mask_rows_cap(hap_ctx c) { return (int64_t)(c->cap[kMask] / (size_t)(c->n_pad * 2)); }
+// Zt planes are allocated with at least kChunkN rows so every TMA box fits the tensor
+int64_t zt_rows(int64_t d_pad) { return std::max<int64_t>(d_pad, kChunkN); }
 
-hap_status refresh_maps(hap_ctx c) {
+hap_status refresh_maps(hap_ctx c, int pair_mode) {
     const void* keys[3] = {c->buf[kMask], c->buf[kZhi], c->buf[kZlo]};
-    const int64_t shape[3] = {c->n_pad, c->d_pad, mask_rows_cap(c)};
-    if (std::equal(keys, keys + 3, c->tm_key) && std::equal(shape, shape + 3, c->tm_shape))
+    const int64_t shape[4] = {c->n_pad, c->d_pad, mask_rows_cap(c), pair_mode};
+    if (std::equal(keys, keys + 3, c->tm_key) && std::equal(shape, shape + 4, c->tm_shape))
         return HAP_OK;
-    const uint32_t box_n = (uint32_t)std::min<int64_t>(kChunkN, c->d_pad);
+    const uint32_t box_b = (uint32_t)maskgemm_b_rows(pair_mode);
+    const uint64_t zr = (uint64_t)zt_rows(c->d_pad);
     if (!make_map(&c->tmA, c->buf[kMask], (uint64_t)c->n_pad, (uint64_t)mask_rows_cap(c), kTileM) ||
-        !make_map(&c->tmBhi, c->buf[kZhi], (uint64_t)c->n_pad, (uint64_t)c->d_pad, box_n) ||
-        !make_map(&c->tmBlo, c->buf[kZlo], (uint64_t)c->n_pad, (uint64_t)c->d_pad, box_n))
+        !make_map(&c->tmBhi, c->buf[kZhi], (uint64_t)c->n_pad, zr, box_b) ||
+        !make_map(&c->tmBlo, c->buf[kZlo], (uint64_t)c->n_pad, zr, box_b))
         return fail(c, HAP_E_CUDA, "cuTensorMapEncodeTiled failed");
     std::copy(keys, keys + 3, c->tm_key);
-    std::copy(shape, shape + 3, c->tm_shape);
+    std::copy(shape, shape + 4, c->tm_shape);
     return HAP_OK;
 }
 
@@ -141,15 +145,17 @@ GemmArgs gemm_args(hap_ctx c, hap_align_info* info) {
     g.n_x = (int)c->n_x;
     g.n_y = (int)c->n_y;
     g.d = (int)c->d;
-    g.box_n = (int)std::min<int64_t>(kChunkN, c->d_pad);
+    g.nchunks = (int)ceil_div(c->d_pad, kChunkN);
     g.info = info;
     g.ab = B<float2>(c, kAB);
     g.sconst = B<double>(c, kSconst);
+    g.part = B<float2>(c, kGemmPart);
+    g.tile_done = B<unsigned>(c, kTileDone);
     g.tie_rel = 1e-6;
     return g;
 }
 
-constexpr int64_t kDefaultBlock = 8192;
+constexpr int64_t kMaskBudget = 64ll << 20;  // bytes of bf16 mask per launch (L2-resident)
 
 cudaEvent_t take_event(hap_ctx c) {
     if (!c->pool.empty()) {
@@ -270,12 +276,12 @@ hap_status hap_align(hap_ctx c, const float* X, int64_t n_x, const float* Y, int
     if ((s = ensure(c, kNrm, N * 8)) || (s = ensure(c, kCoef, N * 8)) ||
         (s = ensure(c, kPart, (size_t)(nbx + nby) * d * 8)) || (s = ensure(c, kXbar, d * 8)) ||
         (s = ensure(c, kYbar, d * 8)) || (s = ensure(c, kU, d * 8)) ||
-        (s = ensure(c, kZhi, (size_t)d_pad * n_pad * 2)) ||
-        (s = ensure(c, kZlo, (size_t)d_pad * n_pad * 2)) ||
+        (s = ensure(c, kZhi, (size_t)zt_rows(d_pad) * n_pad * 2)) ||
+        (s = ensure(c, kZlo, (size_t)zt_rows(d_pad) * n_pad * 2)) ||
         (s = ensure(c, kTpart, (size_t)(n_pad / kRowTile) * d_pad * 8)) ||
         (s = ensure(c, kT64, d_pad * 8)) || (s = ensure(c, kAB, d_pad * 8)) ||
         (s = ensure(c, kM, d_pad * 8)) || (s = ensure(c, kSconst, 16)) ||
-        (s = ensure(c, kMask, (size_t)std::max<int64_t>(kDefaultBlock, kTileM) * n_pad * 2)))
+        (s = ensure(c, kMask, (size_t)2 * kTileM * n_pad * 2)))
         return s;
     // host inputs are staged into the context (copied on `stream`)
     const float* dX = X;
@@ -297,7 +303,6 @@ hap_status hap_align(hap_ctx c, const float* X, int64_t n_x, const float* Y, int
     c->d = d;
     c->n_pad = n_pad;
     c->d_pad = d_pad;
-    if ((s = refresh_maps(c))) return s;
 
     AlignArgs a{};
     a.X = dX;
@@ -328,47 +333,47 @@ hap_status hap_align(hap_ctx c, const float* X, int64_t n_x, const float* Y, int
         e = launch_align(a, st);
     }
     if (e != cudaSuccess) return cuda_fail(c, e, "align kernels");
-    // S6: T_obs through the same mask-GEMM + epilogue path (D7)
-    {
-        PhaseScope ps(c, HAP_PHASE_OBSERVED, 2, st);
-        e = launch_observed_mask(B<uint16_t>(c, kMask), n_x, n_pad, st);
-        if (e == cudaSuccess) {
-            GemmArgs g = gemm_args(c, info);
-            g.count = 1;
-            g.observed = 1;
-            e = launch_maskgemm(&c->tmA, &c->tmBhi, &c->tmBlo, g, st);
-        }
-    }
-    if (e != cudaSuccess) return cuda_fail(c, e, "observed mask-GEMM");
     c->aligned = true;
     c->last_stream = st;
     c->last_info = info;
     return HAP_OK;
 }
 
-hap_status hap_permtest(hap_ctx c, const hap_align_info* info, const hap_perm_cfg* cfg,
+hap_status hap_permtest(hap_ctx c, hap_align_info* info, const hap_perm_cfg* cfg,
                         hap_counts* counts, double* stats, void* stream) {
     if (!c) return HAP_E_INVALID_ARG;
     if (!c->aligned) return fail(c, HAP_E_NOT_ALIGNED, "hap_permtest before hap_align");
     if (!info || !cfg || !counts) return fail(c, HAP_E_INVALID_ARG, "null pointer");
     if (cfg->b_end < cfg->b_begin || cfg->b_end > (1ull << 32))
         return fail(c, HAP_E_INVALID_ARG, "need b_begin <= b_end <= 2^32");
+    if (cfg->pair_mode < 0 || cfg->pair_mode > 2) return fail(c, HAP_E_INVALID_ARG, "bad pair_mode");
     if (!is_device_ptr(counts) || (stats && !is_device_ptr(stats)))
         return fail(c, HAP_E_INVALID_ARG, "counts/stats must be device memory");
     cudaSetDevice(c->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int pair = cfg->pair_mode ? cfg->pair_mode : 2;
+    const int64_t R = (int64_t)kTileM * pair;  // mask rows per tile; row 0 = observed split
     const int64_t total = (int64_t)(cfg->b_end - cfg->b_begin);
-    int64_t blk = cfg->block ? (int64_t)cfg->block : kDefaultBlock;
-    blk = std::max<int64_t>(kTileM, round_up(blk, kTileM));
-    blk = std::min<int64_t>(blk, std::max<int64_t>(kTileM, round_up(total, kTileM)));
+    // permutations per launch: whole tiles, mask within the L2-resident budget
+    int64_t tiles_max = std::max<int64_t>(1, kMaskBudget / (R * c->n_pad * 2));
+    if (cfg->block) tiles_max = std::max<int64_t>(1, ceil_div((int64_t)cfg->block, R - 1));
+    const int64_t tiles_need = std::max<int64_t>(1, ceil_div(total, R - 1));
+    const int64_t tiles = std::min(tiles_max, tiles_need);
+    const int64_t blk = tiles * (R - 1);
+    const int nchunks = (int)ceil_div(c->d_pad, kChunkN);
     hap_status s;
-    if ((s = ensure(c, kMask, (size_t)blk * c->n_pad * 2))) return s;
-    if ((s = refresh_maps(c))) return s;
-    GemmArgs g = gemm_args(c, const_cast<hap_align_info*>(info));
+    if ((s = ensure(c, kMask, (size_t)tiles * R * c->n_pad * 2)) ||
+        (s = ensure(c, kGemmPart, (size_t)tiles * nchunks * R * sizeof(float2))) ||
+        (s = ensure(c, kTileDone, (size_t)tiles * sizeof(unsigned))))
+        return s;
+    if ((s = refresh_maps(c, pair))) return s;
+    GemmArgs g = gemm_args(c, info);
     g.counts = counts;
+    g.rows_per_tile = (int)R;
     g.tie_rel = cfg->tie_rel > 0 ? cfg->tie_rel : 1e-6;
     for (int64_t off = 0; off < total; off += blk) {
         const int64_t cnt = std::min<int64_t>(blk, total - off);
+        const int64_t nt = ceil_div(cnt, R - 1);
         PermArgs pa{};
         pa.seed = cfg->seed;
         pa.s = cfg->stream_id;
@@ -379,6 +384,8 @@ hap_status hap_permtest(hap_ctx c, const hap_align_info* info, const hap_perm_cf
         pa.n_pad = c->n_pad;
         pa.out = c->buf[kMask];
         pa.out_kind = kMaskBf16Row;
+        pa.rows_per_tile = (int)R;
+        pa.ntiles = (int)nt;
         pa.info = info;
         cudaError_t e;
         {
@@ -387,11 +394,11 @@ hap_status hap_permtest(hap_ctx c, const hap_align_info* info, const hap_perm_cf
         }
         if (e != cudaSuccess) return cuda_fail(c, e, "perm generator");
         g.count = (int)cnt;
-        g.observed = 0;
+        g.ntiles = (int)nt;
         g.stats = stats ? stats + 3 * off : nullptr;
         {
             PhaseScope ps(c, HAP_PHASE_MASKGEMM, 1, st);
-            e = launch_maskgemm(&c->tmA, &c->tmBhi, &c->tmBlo, g, st);
+            e = launch_maskgemm(&c->tmA, &c->tmBhi, &c->tmBlo, g, pair, c->sm_count, st);
         }
         if (e != cudaSuccess) return cuda_fail(c, e, "mask-GEMM");
     }
@@ -469,6 +476,8 @@ hap_status hap_perm_sets(hap_ctx c, uint64_t seed, uint32_t stream_id, uint64_t 
     pa.n_pad = round_up(N, kKBlock);
     pa.out = out;
     pa.out_kind = kMaskU8Set;
+    pa.rows_per_tile = 0;
+    pa.ntiles = 0;
     pa.info = nullptr;
     cudaError_t e = launch_perm(pa, c->sm_count, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(c, e, "perm generator");
@@ -481,7 +490,7 @@ hap_status hap_export_pooled(hap_ctx c, uint16_t* zhi, uint16_t* zlo, double* t,
     if (!c->aligned) return fail(c, HAP_E_NOT_ALIGNED, "no pooled cloud yet");
     if (!zhi || !zlo || !t || !m) return fail(c, HAP_E_INVALID_ARG, "null pointer");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const size_t bytes = (size_t)c->d_pad * c->n_pad * 2;
+    const size_t bytes = (size_t)c->d_pad * c->n_pad * 2;  // the first d_pad rows of the planes
     cudaError_t e = cudaMemcpyAsync(zhi, c->buf[kZhi], bytes, cudaMemcpyDeviceToDevice, st);
     if (e == cudaSuccess) e = cudaMemcpyAsync(zlo, c->buf[kZlo], bytes, cudaMemcpyDeviceToDevice, st);
     if (e == cudaSuccess)

@@ -50,28 +50,34 @@ struct PermArgs {
     uint64_t b_begin;
     int64_t count;
     int64_t N, n_x, n_pad;
-    void* out;               // bf16 rows [count][n_pad] or uint8 [count][N]
+    void* out;               // bf16 rows (tile layout) or uint8 [count][N]
     int out_kind;            // MaskOut
+    int rows_per_tile;       // bf16 mode: R; perm p -> row (p/(R-1))*R + 1 + p%(R-1),
+                             // row t*R = observed split {0..n_x-1} for t < ntiles
+    int ntiles;
     const hap_align_info* info;  // optional: skip if info->status != 0
 };
 cudaError_t launch_perm(const PermArgs& a, int sm_count, cudaStream_t st);
-cudaError_t launch_observed_mask(uint16_t* mask_row, int64_t n_x, int64_t n_pad, cudaStream_t st);
 
 // ---- K3: tcgen05 mask-GEMM + statistic epilogue (k_maskgemm.cu) --------------------
 struct GemmArgs {
     int n_pad, d_pad, n_x, n_y, d;
-    int box_n;               // B tile rows = min(256, d_pad)
-    int count;               // valid permutation rows in this launch
-    int observed;            // 1: write T_obs etc. into info (row 0), 0: count
+    int count;               // valid permutations in this launch
+    int ntiles;              // tiles of rows_per_tile mask rows (row 0 = observed split)
+    int nchunks;             // ceil(d_pad / kChunkN)
+    int rows_per_tile;       // 128 * pair_mode
     double tie_rel;
     hap_align_info* info;
     hap_counts* counts;
     double* stats;           // optional, [count][3]
     const float2* ab;        // [d_pad] {2a, 2b}
     const double* sconst;    // {sum a^2, sum b^2}
+    float2* part;            // [ntiles][nchunks][rows_per_tile] chunk partials {s1, s2}
+    unsigned* tile_done;     // [ntiles] arrival tickets (zero between launches)
 };
+int maskgemm_b_rows(int pair_mode);  // B tile rows per CTA (TMA box)
 cudaError_t launch_maskgemm(const CUtensorMap* tmA, const CUtensorMap* tmBhi,
-                            const CUtensorMap* tmBlo, const GemmArgs& g, cudaStream_t st);
-size_t maskgemm_smem_bytes();
+                            const CUtensorMap* tmBlo, const GemmArgs& g, int pair_mode, int sm_count,
+                            cudaStream_t st);
 
 }  // namespace hap

@@ -42,6 +42,13 @@ __device__ double block_sum(double v, double* red) {
     return red[32];
 }
 
+__device__ __forceinline__ double logkappa64(double r, double d) {
+    if (r > 1.0 - 1e-9) r = 1.0 - 1e-9;
+    if (r <= 0.0) return -INFINITY;
+    const double r2 = r * r;
+    return log(r) + log(d - r2) - log(1.0 - r2);
+}
+
 __device__ __forceinline__ const float* row_ptr(const AlignArgs& a, int64_t i) {
     return i < a.n_x ? a.X + i * a.d : a.Y + (i - a.n_x) * a.d;
 }
@@ -57,8 +64,8 @@ __global__ void k1_init(AlignArgs a) {
     f->is_identity = 0;
     f->status = HAP_OK;
     f->bad_row = LLONG_MAX;
-    f->norm_xbar = f->norm_ybar = 0.0;
     f->r_x = f->r_y = f->logk_x = f->logk_y = f->t_obs = 0.0;
+    f->gemm_r_x = f->gemm_r_y = f->gemm_t_obs = __longlong_as_double(0x7ff8000000000000ll);  // NaN
 }
 
 // K1a (S1+S2 partials): one CTA per block of kRowBlock rows of X or of Y.
@@ -152,8 +159,14 @@ __global__ void __launch_bounds__(1024) k1_finalize(AlignArgs a, int nblk_x, int
     }
     if (threadIdx.x == 0) {
         hap_align_info* f = a.info;
-        f->norm_xbar = nx;
-        f->norm_ybar = ny;
+        // observed statistic in fp64 (Alg. 1 step 4): r(X') = ||xbar|| since
+        // H is orthogonal; T_obs = L(r_Y) - L(r_X) (Eq. 10; R1, R4)
+        f->r_x = nx;
+        f->r_y = ny;
+        const double lx = logkappa64(nx, (double)a.d), ly = logkappa64(ny, (double)a.d);
+        f->logk_x = lx;
+        f->logk_y = ly;
+        f->t_obs = (isinf(lx) && isinf(ly)) ? 0.0 : ly - lx;
         f->is_identity = identity ? 1 : 0;
         if (f->status == HAP_OK && degenerate) f->status = HAP_E_DEGENERATE_MEAN;
         if (f->bad_row == LLONG_MAX) f->bad_row = -1;

@@ -2,20 +2,30 @@
 // (DESIGN.md "Kernels" K3; S8 + S9 of SURVEY.md §8a).
 //
 //   sigma1_b = sum_{i in G_b} z_i  as one row of  U' = M_blk Z  (0/1 mask instead of the
-//   paper's +-1 signs, PAPER.md:205-220 Eq. gemm; R7), Z~ = hi + lo bf16 planes:
-//       D[b, c] = sum_k M[b,k] Zhi[k,c] + sum_k M[b,k] Zlo[k,c]   (fp32 in TMEM)
-//   sigma2 = t - sigma1            ("without a second GEMM")
+//   paper's +-1 signs, PAPER.md:205-220 Eq. gemm; R7).  Z is held centred as
+//   Z - 1 m^T in two bf16 planes (hi, lo), so the accumulator is
+//       acc[b, c] = sum_k M[b,k] Zhi[k,c] + sum_k M[b,k] Zlo[k,c]        (fp32, TMEM)
+//   and sigma1 = a + acc, sigma2 = t - sigma1 = b - acc  with a = n_x m, b = t - a
+//   ("without a second GEMM").
 //   r1 = ||sigma1||/n_x, r2 = ||sigma2||/n_y
-//   T_b = L(r2) - L(r1)             (Alg. 2)
-//   counts += [T_b >= T_obs], [|T_b| >= |T_obs|], [|T_b - T_obs| <= tau]
-// No B x d intermediate reaches HBM: sigma1 lives only in TMEM.
+//   T_b = L(r2) - L(r1)                       (Alg. 2)
+//   counts += [T_b >= T_obs], [|T_b| >= |T_obs|], near-tie   (R8)
+// No B x d intermediate reaches HBM: acc lives in TMEM; only 8 bytes per (row, d-chunk)
+// of fp32 partial sums are exchanged between the CTAs that share a tile.
 //
-// v1 structure: one CTA per 128-permutation tile (M = 128, cta_group::1), 6 warps:
-//   warp 0  TMA producer   (A = mask tile 128x64, B = Zt_hi / Zt_lo tiles 256x64; SW128)
-//   warp 1  MMA issuer + TMEM owner (512 columns = 2 accumulator buffers of 256)
-//   warps 2-5 epilogue: thread = TMEM lane = one permutation; loops over d-chunks of 256
-//            with the accumulator double-buffered so chunk c+1's MMAs overlap chunk c's
-//            epilogue.
+// Work: a launch covers `ntiles` tiles of R = 128*kPair mask rows; row 0 of every tile is
+// the OBSERVED split {0..n_x-1}, so T_obs is evaluated through exactly the same MMA +
+// epilogue path as every permutation (D7) with no extra launch or dependency.
+// A unit = (tile, 256-column d-chunk); persistent CTA pairs walk the units round-robin.
+//
+// kPair = 2 (default): a 2-CTA cluster runs tcgen05.mma.cta_group::2 with M = 256: each CTA
+// holds 128 mask rows (A) and half of the chunk's columns (B), so each SM streams half of
+// the Z~ tile; 4-stage TMA ring of 48 KB.  kPair = 1: one CTA, M = 128, 2 stages of 80 KB.
+// Warps: 0 TMA producer, 1 MMA issuer (leader CTA) + TMEM owner, 2-5 epilogue (thread =
+// TMEM lane = one mask row).  The accumulator is double-buffered in TMEM (2 x 256 columns)
+// so unit i+1's MMAs overlap unit i's epilogue.  The last CTA to finish a unit of a tile
+// (atomic ticket) sums the tile's chunk partials in fixed order (deterministic), forms the
+// statistics and counts.
 #include <cmath>
 
 #include "hap_device.cuh"
@@ -24,12 +34,18 @@
 namespace hap {
 namespace {
 
-constexpr int kStages = 2;
-constexpr int kStageA = kTileM * 128;              // 16 KB: 128 rows x 64 bf16
-constexpr int kStageB = kChunkN * 128;             // 32 KB: 256 rows x 64 bf16
-constexpr int kStageBytes = kStageA + 2 * kStageB; // 80 KB
 constexpr int kThreads = 192;
 constexpr uint32_t kTmemCols = 512;
+constexpr int kStageA = kTileM * 128;  // 16 KB: 128 rows x 64 bf16
+
+template <int kPair>
+struct Cfg {
+    static constexpr int kStages = kPair == 2 ? 4 : 2;
+    static constexpr int kBRows = kChunkN / kPair;   // B rows (d-columns) held per CTA
+    static constexpr int kStageB = kBRows * 128;     // one plane
+    static constexpr int kStageBytes = kStageA + 2 * kStageB;
+    static constexpr size_t kSmem = (size_t)kStages * kStageBytes + 1024 + 256;
+};
 
 // L(r) = log kappa-hat(r), kappa-hat = r(d - r^2)/(1 - r^2), r clamped to [0, 1-1e-9]
 // (Eq. 9 with DESIGN.md R1, R4).
@@ -40,107 +56,211 @@ __device__ __forceinline__ double logkappa(double r, double d) {
     return log(r) + log(d - r2) - log(1.0 - r2);
 }
 
+struct RowStat {
+    double r1, r2, T;
+};
+
+// statistic of one tile row from the chunk partials, summed in ascending chunk order
+__device__ __forceinline__ RowStat row_stat(const GemmArgs& g, int tile, int row) {
+    double S1 = g.sconst[0], S2 = g.sconst[1];
+    const float2* p = g.part + (size_t)tile * g.nchunks * g.rows_per_tile + row;
+    for (int c = 0; c < g.nchunks; ++c) {
+        const float2 v = __ldcg(p + (size_t)c * g.rows_per_tile);
+        S1 += (double)v.x;
+        S2 += (double)v.y;
+    }
+    RowStat s;
+    s.r1 = sqrt(fmax(S1, 0.0)) / (double)g.n_x;
+    s.r2 = sqrt(fmax(S2, 0.0)) / (double)g.n_y;
+    const double L1 = logkappa(s.r1, (double)g.d), L2 = logkappa(s.r2, (double)g.d);
+    s.T = (isinf(L1) && isinf(L2)) ? 0.0 : L2 - L1;
+    return s;
+}
+
+// Last CTA of a tile: T_obs from row 0, then every permutation row of the tile.
+__device__ void finalize_tile(const GemmArgs& g, int tile, int etid, double* s_tobs) {
+    const int R = g.rows_per_tile;
+    if (etid == 0) {
+        const RowStat o = row_stat(g, tile, 0);
+        *s_tobs = o.T;
+        if (tile == 0) {
+            g.info->gemm_r_x = o.r1;
+            g.info->gemm_r_y = o.r2;
+            g.info->gemm_t_obs = o.T;
+        }
+    }
+    named_bar_sync(1, 128);
+    const double t_obs = *s_tobs;
+    const double tau = g.tie_rel * (fabs(g.info->logk_x) + fabs(g.info->logk_y));
+    const int lane = etid & 31;
+    for (int row = etid; row < R; row += 128) {
+        const int perm = tile * (R - 1) + row - 1;
+        const bool valid = row >= 1 && perm < g.count;
+        RowStat s{0.0, 0.0, 0.0};
+        if (valid) s = row_stat(g, tile, row);
+        const double T = s.T;
+        const bool ge = valid && (T >= t_obs);
+        const bool ab = valid && (fabs(T) >= fabs(t_obs));
+        const bool fl = valid && (T == t_obs || fabs(T - t_obs) <= tau || fabs(T) == fabs(t_obs) ||
+                                  fabs(fabs(T) - fabs(t_obs)) <= tau);
+        const uint32_t bge = __ballot_sync(0xffffffffu, ge);
+        const uint32_t bab = __ballot_sync(0xffffffffu, ab);
+        const uint32_t bfl = __ballot_sync(0xffffffffu, fl);
+        if (lane == 0) {
+            unsigned long long* cnt = reinterpret_cast<unsigned long long*>(g.counts);
+            if (bge) atomicAdd(cnt + 0, (unsigned long long)__popc(bge));
+            if (bab) atomicAdd(cnt + 1, (unsigned long long)__popc(bab));
+            if (bfl) atomicAdd(cnt + 2, (unsigned long long)__popc(bfl));
+        }
+        if (g.stats && valid) {
+            double* o = g.stats + 3 * (int64_t)perm;
+            o[0] = s.r1;
+            o[1] = s.r2;
+            o[2] = T;
+        }
+    }
+    if (etid == 0) g.tile_done[tile] = 0;  // ready for the next launch
+}
+
+template <int kPair>
 __global__ void __launch_bounds__(kThreads, 1)
     k3_maskgemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBhi,
                 const __grid_constant__ CUtensorMap tmBlo, GemmArgs g) {
+    using C = Cfg<kPair>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     if (g.info->status != HAP_OK) return;  // deferred data error: whole test is a no-op
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
-    uint64_t* empty = full + kStages;
-    uint64_t* tfull = empty + kStages;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+    uint64_t* empty = full + C::kStages;
+    uint64_t* tfull = empty + C::kStages;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
+    double* s_tobs = reinterpret_cast<double*>(tmem_slot + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = kPair == 2 ? cluster_ctarank() : 0u;
+    const bool leader = rank == 0;
+    const int pair_id = blockIdx.x / kPair, npairs = gridDim.x / kPair;
     const int nkb = g.n_pad / kKBlock;
-    const int nchunks = (g.d_pad + kChunkN - 1) / kChunkN;
-    const int row0 = blockIdx.x * kTileM;
+    const int units = g.ntiles * g.nchunks;
+    const int R = g.rows_per_tile;
 
     if (warp == 0 && lane == 0) {
-        for (int s = 0; s < kStages; ++s) {
+        for (int s = 0; s < C::kStages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 4 * 32);
+            mbar_init(&tempty[a], 4 * kPair);  // one arrival per epilogue warp of the pair
         }
         fence_barrier_init();
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmBhi);
         tma_prefetch_desc(&tmBlo);
     }
-    if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
+    if (warp == 1) {
+        if constexpr (kPair == 2) tmem_alloc_pair<kTmemCols>(tmem_slot);
+        else tmem_alloc<kTmemCols>(tmem_slot);
+    }
     tc_fence_before();
     __syncthreads();
+    if constexpr (kPair == 2) cluster_sync();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0) {
-        // ---------------- TMA producer
+        // ---------------- TMA producer (both CTAs load their own A rows and B half)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            const uint32_t bytes = (uint32_t)(kTileM + 2 * g.box_n) * 128u;
-            for (int c = 0; c < nchunks; ++c) {
+            for (int u = pair_id; u < units; u += npairs) {
+                const int tile = u / g.nchunks, chunk = u % g.nchunks;
+                const int width = min(kChunkN, g.d_pad - chunk * kChunkN);
+                const int arow = tile * R + (int)rank * kTileM;
+                const int brow = chunk * kChunkN + (int)rank * (width / kPair);
                 for (int kb = 0; kb < nkb; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1u);
-                    uint8_t* sA = smem + stage * kStageBytes;
-                    mbar_arrive_expect_tx(&full[stage], bytes);
-                    tma_load_2d(&tmA, &full[stage], sA, kb * kKBlock, row0);
-                    tma_load_2d(&tmBhi, &full[stage], sA + kStageA, kb * kKBlock, c * kChunkN);
-                    tma_load_2d(&tmBlo, &full[stage], sA + kStageA + kStageB, kb * kKBlock,
-                                c * kChunkN);
-                    if (++stage == kStages) { stage = 0; phase ^= 1u; }
+                    uint8_t* sA = smem + stage * C::kStageBytes;
+                    if constexpr (kPair == 2) {
+                        if (leader) mbar_arrive_expect_tx(&full[stage], 2u * C::kStageBytes);
+                        const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
+                        tma_load_2d_pair(&tmA, fb, sA, kb * kKBlock, arow);
+                        tma_load_2d_pair(&tmBhi, fb, sA + kStageA, kb * kKBlock, brow);
+                        tma_load_2d_pair(&tmBlo, fb, sA + kStageA + C::kStageB, kb * kKBlock, brow);
+                    } else {
+                        mbar_arrive_expect_tx(&full[stage], (uint32_t)C::kStageBytes);
+                        tma_load_2d(&tmA, &full[stage], sA, kb * kKBlock, arow);
+                        tma_load_2d(&tmBhi, &full[stage], sA + kStageA, kb * kKBlock, brow);
+                        tma_load_2d(&tmBlo, &full[stage], sA + kStageA + C::kStageB, kb * kKBlock,
+                                    brow);
+                    }
+                    if (++stage == C::kStages) { stage = 0; phase ^= 1u; }
                 }
             }
         }
     } else if (warp == 1) {
-        // ---------------- MMA issuer (single thread)
-        if (lane == 0) {
+        // ---------------- MMA issuer: one thread of the leader CTA
+        if (leader && lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int c = 0; c < nchunks; ++c) {
-                const int a = c & 1;
-                const int width = min(kChunkN, g.d_pad - c * kChunkN);
-                const uint32_t idesc = idesc_bf16_f32(kTileM, (uint32_t)width);
-                mbar_wait(&tempty[a], (((uint32_t)c >> 1) & 1u) ^ 1u);
+            int i = 0;
+            for (int u = pair_id; u < units; u += npairs, ++i) {
+                const int chunk = u % g.nchunks;
+                const int width = min(kChunkN, g.d_pad - chunk * kChunkN);
+                const uint32_t idesc = idesc_bf16_f32(kTileM * kPair, (uint32_t)width);
+                const int a = i & 1;
+                mbar_wait(&tempty[a], (((uint32_t)i >> 1) & 1u) ^ 1u);
                 tc_fence_after();
                 const uint32_t dtm = tmem + (uint32_t)(a * kChunkN);
                 for (int kb = 0; kb < nkb; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
-                    const uint32_t aBase = smem_u32(smem + stage * kStageBytes);
-                    const uint32_t hBase = aBase + kStageA, lBase = hBase + kStageB;
+                    const uint32_t aBase = smem_u32(smem + stage * C::kStageBytes);
+                    const uint32_t hBase = aBase + kStageA, lBase = hBase + C::kStageB;
 #pragma unroll
                     for (int k = 0; k < kKBlock / 16; ++k) {
                         const uint64_t ad = smem_desc_k_sw128(aBase + 32u * k);
-                        umma_bf16_ss(dtm, ad, smem_desc_k_sw128(hBase + 32u * k), idesc,
-                                     (kb | k) != 0 ? 1u : 0u);
-                        umma_bf16_ss(dtm, ad, smem_desc_k_sw128(lBase + 32u * k), idesc, 1u);
+                        const uint64_t hd = smem_desc_k_sw128(hBase + 32u * k);
+                        const uint64_t ld = smem_desc_k_sw128(lBase + 32u * k);
+                        if constexpr (kPair == 2) {
+                            umma_bf16_ss_pair(dtm, ad, hd, idesc, (kb | k) != 0 ? 1u : 0u);
+                            umma_bf16_ss_pair(dtm, ad, ld, idesc, 1u);
+                        } else {
+                            umma_bf16_ss(dtm, ad, hd, idesc, (kb | k) != 0 ? 1u : 0u);
+                            umma_bf16_ss(dtm, ad, ld, idesc, 1u);
+                        }
                     }
-                    umma_commit(&empty[stage]);  // frees the smem slot when these MMAs retire
-                    if (++stage == kStages) { stage = 0; phase ^= 1u; }
+                    if constexpr (kPair == 2) umma_commit_pair(&empty[stage], 0x3);
+                    else umma_commit(&empty[stage]);
+                    if (++stage == C::kStages) { stage = 0; phase ^= 1u; }
                 }
-                umma_commit(&tfull[a]);  // accumulator chunk ready for the epilogue
+                if constexpr (kPair == 2) umma_commit_pair(&tfull[a], 0x3);
+                else umma_commit(&tfull[a]);
             }
         }
     } else {
-        // ---------------- epilogue: one thread per TMEM lane (= permutation row)
+        // ---------------- epilogue: thread = TMEM lane = one mask row of this CTA
         const int q = warp & 3;
-        const int row = 32 * q + lane;
-        const int perm = row0 + row;
-        // sigma1 = a + acc, sigma2 = b - acc  (centred accumulator acc)
-        double S1 = g.sconst[0], S2 = g.sconst[1];
-        for (int c = 0; c < nchunks; ++c) {
-            const int a = c & 1;
-            const int width = min(kChunkN, g.d_pad - c * kChunkN);
-            mbar_wait(&tfull[a], ((uint32_t)c >> 1) & 1u);
+        const int trow = (int)rank * kTileM + 32 * q + lane;  // row within the tile
+        const int etid = threadIdx.x - 64;
+        uint32_t tempty_c[2] = {0, 0};
+        if constexpr (kPair == 2) {
+            tempty_c[0] = mapa_shared(smem_u32(&tempty[0]), 0);
+            tempty_c[1] = mapa_shared(smem_u32(&tempty[1]), 0);
+        }
+        int i = 0;
+        for (int u = pair_id; u < units; u += npairs, ++i) {
+            const int tile = u / g.nchunks, chunk = u % g.nchunks;
+            const int width = min(kChunkN, g.d_pad - chunk * kChunkN);
+            const int a = i & 1;
+            mbar_wait(&tfull[a], ((uint32_t)i >> 1) & 1u);
             tc_fence_after();
+            // sigma1 = a + acc, sigma2 = b - acc:  |sigma1|^2 - |a|^2 = sum acc (acc + 2a), ...
             float s1 = 0.f, s2 = 0.f;
-            const float4* abp = reinterpret_cast<const float4*>(g.ab + c * kChunkN);
+            const float4* abp = reinterpret_cast<const float4*>(g.ab + chunk * kChunkN);
             for (int cb = 0; cb < width / 32; ++cb) {
                 uint32_t r[32];
                 tmem_ld_32x32b_x32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(a * kChunkN + 32 * cb),
@@ -157,77 +277,74 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             tc_fence_before();
-            mbar_arrive(&tempty[a]);
-            S1 += (double)s1;
-            S2 += (double)s2;
-        }
-        S1 = fmax(S1, 0.0);
-        S2 = fmax(S2, 0.0);
-        const double r1 = sqrt(S1) / (double)g.n_x;
-        const double r2 = sqrt(S2) / (double)g.n_y;
-        const double L1 = logkappa(r1, (double)g.d), L2 = logkappa(r2, (double)g.d);
-        const double T = (isinf(L1) && isinf(L2)) ? 0.0 : L2 - L1;
-        if (g.observed) {
-            if (row == 0 && blockIdx.x == 0) {
-                hap_align_info* f = g.info;
-                f->r_x = r1;
-                f->r_y = r2;
-                f->logk_x = L1;
-                f->logk_y = L2;
-                f->t_obs = T;
+            __syncwarp();
+            if (lane == 0) {  // accumulator buffer free again
+                if constexpr (kPair == 2) mbar_arrive_cluster(tempty_c[a]);
+                else mbar_arrive(&tempty[a]);
             }
-        } else {
-            const double t_obs = g.info->t_obs;
-            const double tau = g.tie_rel * (fabs(g.info->logk_x) + fabs(g.info->logk_y));
-            const bool valid = perm < g.count;
-            const bool ge = valid && (T >= t_obs);
-            const bool ab = valid && (fabs(T) >= fabs(t_obs));
-            // near-tie of either decision (R8)
-            const bool fl = valid && (T == t_obs || fabs(T - t_obs) <= tau ||
-                                      fabs(T) == fabs(t_obs) || fabs(fabs(T) - fabs(t_obs)) <= tau);
-            const uint32_t bge = __ballot_sync(0xffffffffu, ge);
-            const uint32_t bab = __ballot_sync(0xffffffffu, ab);
-            const uint32_t bfl = __ballot_sync(0xffffffffu, fl);
-            if (lane == 0) {
-                unsigned long long* cnt = reinterpret_cast<unsigned long long*>(g.counts);
-                if (bge) atomicAdd(cnt + 0, (unsigned long long)__popc(bge));
-                if (bab) atomicAdd(cnt + 1, (unsigned long long)__popc(bab));
-                if (bfl) atomicAdd(cnt + 2, (unsigned long long)__popc(bfl));
+            g.part[((size_t)tile * g.nchunks + chunk) * R + trow] = make_float2(s1, s2);
+            __threadfence();
+            named_bar_sync(1, 128);
+            if (etid == 0) {
+                const unsigned old = atomicAdd(g.tile_done + tile, 1u);
+                *s_last = (old == (unsigned)(kPair * g.nchunks - 1)) ? 1 : 0;
             }
-            if (g.stats && valid) {
-                double* o = g.stats + 3 * (int64_t)perm;
-                o[0] = r1;
-                o[1] = r2;
-                o[2] = T;
+            named_bar_sync(1, 128);
+            if (*s_last) {
+                __threadfence();
+                finalize_tile(g, tile, etid, s_tobs);
             }
+            named_bar_sync(1, 128);
         }
     }
     tc_fence_before();
     __syncthreads();
+    if constexpr (kPair == 2) cluster_sync();
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc<kTmemCols>(tmem);
+        if constexpr (kPair == 2) tmem_dealloc_pair<kTmemCols>(tmem);
+        else tmem_dealloc<kTmemCols>(tmem);
     }
+}
+
+template <int kPair>
+cudaError_t launch_impl(const CUtensorMap* tmA, const CUtensorMap* tmBhi, const CUtensorMap* tmBlo,
+                        const GemmArgs& g, int sm_count, cudaStream_t st) {
+    using C = Cfg<kPair>;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(k3_maskgemm<kPair>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    const int units = g.ntiles * g.nchunks;
+    const int npairs = std::max(1, std::min(units, sm_count / kPair));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(npairs * kPair));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = C::kSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kPair;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k3_maskgemm<kPair>, *tmA, *tmBhi, *tmBlo, g);
 }
 
 }  // namespace
 
-size_t maskgemm_smem_bytes() { return (size_t)kStages * kStageBytes + 1024 + 128; }
+int maskgemm_b_rows(int pair_mode) { return kChunkN / pair_mode; }
 
 cudaError_t launch_maskgemm(const CUtensorMap* tmA, const CUtensorMap* tmBhi,
-                            const CUtensorMap* tmBlo, const GemmArgs& g, cudaStream_t st) {
-    if (g.count <= 0) return cudaSuccess;
-    static bool configured = false;
-    const size_t smem = maskgemm_smem_bytes();
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(k3_maskgemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
-    const int grid = (int)ceil_div(g.count, kTileM);
-    k3_maskgemm<<<grid, kThreads, smem, st>>>(*tmA, *tmBhi, *tmBlo, g);
-    return cudaGetLastError();
+                            const CUtensorMap* tmBlo, const GemmArgs& g, int pair_mode, int sm_count,
+                            cudaStream_t st) {
+    if (g.ntiles <= 0) return cudaSuccess;
+    return pair_mode == 2 ? launch_impl<2>(tmA, tmBhi, tmBlo, g, sm_count, st)
+                          : launch_impl<1>(tmA, tmBhi, tmBlo, g, sm_count, st);
 }
 
 }  // namespace hap

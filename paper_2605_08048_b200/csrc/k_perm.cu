@@ -58,7 +58,23 @@ __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy(PermArgs a, int lt
     const uint32_t key0 = (uint32_t)(a.seed & 0xFFFFFFFFu), key1 = (uint32_t)(a.seed >> 32);
     const int nw = (int)(blockDim.x >> 5);
     const int64_t wstride = (int64_t)gridDim.x * nw;
-    for (int64_t pi = (int64_t)blockIdx.x * nw + w; pi < a.count; pi += wstride) {
+    const int64_t items = a.count + (a.out_kind == kMaskBf16Row ? a.ntiles : 0);
+    for (int64_t pi = (int64_t)blockIdx.x * nw + w; pi < items; pi += wstride) {
+        if (pi >= a.count) {  // observed split: row 0 of tile (pi - count)
+            const int64_t t = pi - a.count;
+            uint4* row = reinterpret_cast<uint4*>(static_cast<uint16_t*>(a.out) +
+                                                  t * a.rows_per_tile * a.n_pad);
+            for (int64_t v8 = l; v8 < a.n_pad / 8; v8 += 32) {
+                uint32_t wds[4];
+#pragma unroll
+                for (int e2 = 0; e2 < 4; ++e2) {
+                    const int64_t v = 8 * v8 + 2 * e2;
+                    wds[e2] = (v < a.n_x ? 0x3F80u : 0u) | ((v + 1 < a.n_x ? 0x3F80u : 0u) << 16);
+                }
+                row[v8] = make_uint4(wds[0], wds[1], wds[2], wds[3]);
+            }
+            continue;
+        }
         const uint32_t b = (uint32_t)(a.b_begin + (uint64_t)pi);
         uint4* LT4 = reinterpret_cast<uint4*>(LT);
         for (int q = l; q < lt_pitch / 8; q += 32) LT4[q] = make_uint4(0, 0, 0, 0);
@@ -105,7 +121,9 @@ __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy(PermArgs a, int lt
         __syncwarp();
         // ---- phase C: exact 0/1 row
         if (a.out_kind == kMaskBf16Row) {
-            uint4* row = reinterpret_cast<uint4*>(static_cast<uint16_t*>(a.out) + pi * a.n_pad);
+            const int64_t R1 = a.rows_per_tile - 1;
+            const int64_t orow = (pi / R1) * a.rows_per_tile + 1 + pi % R1;
+            uint4* row = reinterpret_cast<uint4*>(static_cast<uint16_t*>(a.out) + orow * a.n_pad);
             for (int64_t v8 = l; v8 < a.n_pad / 8; v8 += 32) {
                 uint32_t wds[4];
 #pragma unroll
@@ -136,11 +154,6 @@ __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy(PermArgs a, int lt
     }
 }
 
-__global__ void k2_observed_mask(uint16_t* row, int64_t n_x, int64_t n_pad) {
-    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v < n_pad) row[v] = v < n_x ? (uint16_t)0x3F80 : (uint16_t)0;  // bf16(1), bf16(0)
-}
-
 }  // namespace
 
 cudaError_t launch_perm(const PermArgs& a, int sm_count, cudaStream_t st) {
@@ -159,14 +172,9 @@ cudaError_t launch_perm(const PermArgs& a, int sm_count, cudaStream_t st) {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_perm_fy, nw * 32, smem);
     if (per_sm < 1) per_sm = 1;
-    const int64_t need = ceil_div(a.count, nw);
+    const int64_t need = ceil_div(a.count + (a.out_kind == kMaskBf16Row ? a.ntiles : 0), nw);
     const int grid = (int)std::min<int64_t>(need, (int64_t)sm_count * per_sm);
     k2_perm_fy<<<grid, nw * 32, smem, st>>>(a, lt_pitch);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_observed_mask(uint16_t* mask_row, int64_t n_x, int64_t n_pad, cudaStream_t st) {
-    k2_observed_mask<<<(unsigned)ceil_div(n_pad, 256), 256, 0, st>>>(mask_row, n_x, n_pad);
     return cudaGetLastError();
 }
 

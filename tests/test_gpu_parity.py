@@ -41,31 +41,36 @@ def _cuda(a):
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
 
 
-def check_pair(ctx, orc, X, Y, B, s=0, mode=0, block=0, b_begin=0, b_end=None, n_stats=None):
+def check_pair(ctx, orc, X, Y, B, s=0, mode=0, block=0, b_begin=0, b_end=None, pair_mode=0):
     """Run both sides with stats; assert the parity bars; return (gpu, ref)."""
     b_end = B if b_end is None else b_end
     g = ctx.permtest_pair(_cuda(X), _cuda(Y), B, SEED, stream_id=s, mode=mode, block=block,
-                          b_begin=b_begin, b_end=b_end, want_stats=True)
+                          b_begin=b_begin, b_end=b_end, want_stats=True, pair_mode=pair_mode)
     ref = orc.run_pair(X, Y, B, SEED, s=s, mode=mode, b_begin=b_begin, b_end=b_end,
                        want_stats=True)
     Ls = abs(ref["L_x"]) + abs(ref["L_y"])
-    assert math.isclose(g["r_x"], ref["r_x"], rel_tol=1e-5)
-    assert math.isclose(g["r_y"], ref["r_y"], rel_tol=1e-5)
-    assert math.isclose(g["logk_x"], ref["L_x"], rel_tol=1e-5, abs_tol=1e-9)
-    assert math.isclose(g["logk_y"], ref["L_y"], rel_tol=1e-5, abs_tol=1e-9)
-    assert abs(g["t_obs"] - ref["t_obs"]) <= 1e-5 * Ls
+    # observed statistic: fp64 on both sides (K1 means vs oracle direct sums)
+    assert math.isclose(g["r_x"], ref["r_x"], rel_tol=1e-10)
+    assert math.isclose(g["r_y"], ref["r_y"], rel_tol=1e-10)
+    assert math.isclose(g["logk_x"], ref["L_x"], rel_tol=1e-10, abs_tol=1e-12)
+    assert math.isclose(g["logk_y"], ref["L_y"], rel_tol=1e-10, abs_tol=1e-12)
+    assert abs(g["t_obs"] - ref["t_obs"]) <= 1e-10 * Ls
+    # the same-path observed value the permutations were compared against
+    assert math.isclose(g["gemm_r_x"], ref["r_x"], rel_tol=1e-5)
+    assert math.isclose(g["gemm_r_y"], ref["r_y"], rel_tol=1e-5)
+    assert abs(g["gemm_t_obs"] - ref["t_obs"]) <= 1e-5 * Ls
     gs = g["stats"].cpu().numpy()
     rs = ref["stats"]
     assert np.allclose(gs[:, 0], rs[:, 0], rtol=1e-5, atol=0)
     assert np.allclose(gs[:, 1], rs[:, 1], rtol=1e-5, atol=0)
     assert np.all(np.abs(gs[:, 2] - rs[:, 2]) <= 1e-5 * Ls)
-    # decisions identical outside the tie band
+    # decisions identical outside the tie bands (GPU compares against its same-path T_obs)
     tau = ref["tau"]
+    tg = g["gemm_t_obs"]
     out = np.abs(rs[:, 2] - ref["t_obs"]) > tau
-    assert np.array_equal(gs[out, 2] >= g["t_obs"], rs[out, 2] >= ref["t_obs"])
+    assert np.array_equal(gs[out, 2] >= tg, rs[out, 2] >= ref["t_obs"])
     out2 = np.abs(np.abs(rs[:, 2]) - abs(ref["t_obs"])) > tau
-    assert np.array_equal(np.abs(gs[out2, 2]) >= abs(g["t_obs"]),
-                          np.abs(rs[out2, 2]) >= abs(ref["t_obs"]))
+    assert np.array_equal(np.abs(gs[out2, 2]) >= abs(tg), np.abs(rs[out2, 2]) >= abs(ref["t_obs"]))
     for k in ("exceed_ge", "exceed_abs"):
         assert abs(g[k] - ref[k]) <= ref["flagged"], (k, g[k], ref[k], ref["flagged"])
     return g, ref
@@ -132,20 +137,23 @@ def test_pooled_planes(hap, ctx, orc, n_x, n_y, d, mode):
 
 
 # ------------------------------------------------------------------ K3 + end to end
-def test_config1_full(ctx, orc):
-    """C1: n_x=n_y=64, d=768, B=1000, every permutation compared."""
+@pytest.mark.parametrize("pair_mode", [1, 2])
+def test_config1_full(ctx, orc, pair_mode):
+    """C1: n_x=n_y=64, d=768, B=1000, every permutation compared; both K3 modes
+    (cta_group::1, M=128 and cta_group::2, M=256)."""
     X, Y = HI.config_pair("C1")
-    check_pair(ctx, orc, X, Y, 1000, s=1)
+    check_pair(ctx, orc, X, Y, 1000, s=1, pair_mode=pair_mode)
 
 
+@pytest.mark.parametrize("pair_mode", [1, 2])
 @pytest.mark.parametrize("n_x,n_y,d,B,block", [(37, 50, 100, 300, 128), (2, 70, 48, 257, 0),
                                                (70, 2, 40, 129, 0), (200, 300, 300, 1000, 256),
-                                               (5, 3, 3, 200, 0)])
-def test_ragged_shapes(ctx, orc, n_x, n_y, d, B, block):
-    """Ragged N (not a multiple of 64), d not a multiple of 32, several tiles with a
-    ragged tail, multi-block launches, single-row groups."""
+                                               (5, 3, 3, 200, 0), (64, 64, 544, 700, 300)])
+def test_ragged_shapes(ctx, orc, n_x, n_y, d, B, block, pair_mode):
+    """Ragged N (not a multiple of 64), d not a multiple of 32 (last d-chunk narrower than
+    256), several tiles with a ragged tail, multi-launch blocks, two-row groups."""
     X, Y = HI.make_pair(HI.PairSpec(n_x, n_y, d, 30.0, 60.0, 40.0, seed=n_x * 7 + d))
-    check_pair(ctx, orc, X, Y, B, s=3, block=block)
+    check_pair(ctx, orc, X, Y, B, s=3, block=block, pair_mode=pair_mode)
 
 
 def test_singleton_group(ctx, orc):
@@ -213,7 +221,7 @@ def test_duplicate_sets_tie_bit_exactly(ctx, orc):
     sets = [tuple(np.nonzero(orc.perm_set(SEED, 0, b, 4, 2))[0]) for b in range(600)]
     obs = [i for i, s in enumerate(sets) if s == (0, 1)]
     assert len(obs) > 50
-    assert np.all(gs[obs, 2] == g["t_obs"])
+    assert np.all(gs[obs, 2] == g["gemm_t_obs"])
     assert g["exceed_ge"] == ref["exceed_ge"]
 
 
