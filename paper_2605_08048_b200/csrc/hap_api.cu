@@ -27,10 +27,16 @@ struct hap_ctx_s {
     // ---- state of the last successful hap_align
     bool aligned = false;
     int64_t n_x = 0, n_y = 0, d = 0, n_pad = 0, d_pad = 0;
-    // ---- TMA descriptors (valid for the current buffers/shape)
-    CUtensorMap tmA{}, tmBhi{}, tmBlo{};
-    const void* tm_key[3] = {};
-    int64_t tm_shape[4] = {};
+    // ---- TMA descriptors (valid for the current buffers/shape); tmA per mask slot
+    CUtensorMap tmA[2]{}, tmBhi{}, tmBlo{};
+    const void* tm_key[4] = {};
+    int64_t tm_shape[5] = {};
+    // ---- generator side stream: K2 only depends on (seed, s, b, N, n_x), so it runs on
+    // `side`, forked from the caller's stream before K1, and joins back before K3
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_ready[2] = {}, ev_free[2] = {};
+    bool forked = false;
+    int slot = 0;
     // ---- profiling
     bool prof = false;
     struct Mark { cudaEvent_t a, b; int phase; };
@@ -43,8 +49,8 @@ struct hap_ctx_s {
 namespace {
 
 enum Buf {
-    kX = 0, kY, kNrm, kCoef, kPart, kXbar, kYbar, kU, kZhi, kZlo, kTpart, kT64, kAB, kMask,
-    kM, kSconst, kGemmPart, kTileDone, kNumBufs
+    kX = 0, kY, kNrm, kCoef, kPart, kXbar, kYbar, kUnused, kZhi, kZlo, kTpart, kT64, kAB, kMask,
+    kM, kSconst, kGemmPart, kTileDone, kScal, kSpart, kScratch, kMask1, kNumBufs
 };
 
 hap_status fail(hap_ctx c, hap_status s, const std::string& msg) {
@@ -62,6 +68,7 @@ hap_status ensure(hap_ctx c, int which, size_t bytes) {
     if (c->cap[which] >= bytes) return HAP_OK;
     if (c->buf[which]) {
         if (c->last_stream) cudaStreamSynchronize(c->last_stream);
+        if (c->side) cudaStreamSynchronize(c->side);
         cudaFree(c->buf[which]);
         c->buf[which] = nullptr;
         c->cap[which] = 0;
@@ -118,23 +125,27 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows, u
     return r == CUDA_SUCCESS;
 }
 
-int64_t mask_rows_cap(hap_ctx c) { return (int64_t)(c->cap[kMask] / (size_t)(c->n_pad * 2)); }
+int64_t mask_rows_cap(hap_ctx c) {
+    return (int64_t)(std::min(c->cap[kMask], c->cap[kMask1]) / (size_t)(c->n_pad * 2));
+}
 // Zt planes are allocated with at least kChunkN rows so every TMA box fits the tensor
 int64_t zt_rows(int64_t d_pad) { return std::max<int64_t>(d_pad, kChunkN); }
 
 hap_status refresh_maps(hap_ctx c, int pair_mode) {
-    const void* keys[3] = {c->buf[kMask], c->buf[kZhi], c->buf[kZlo]};
-    const int64_t shape[4] = {c->n_pad, c->d_pad, mask_rows_cap(c), pair_mode};
-    if (std::equal(keys, keys + 3, c->tm_key) && std::equal(shape, shape + 4, c->tm_shape))
+    const void* keys[4] = {c->buf[kMask], c->buf[kMask1], c->buf[kZhi], c->buf[kZlo]};
+    const int64_t shape[5] = {c->n_pad, c->d_pad, mask_rows_cap(c), pair_mode, 0};
+    if (std::equal(keys, keys + 4, c->tm_key) && std::equal(shape, shape + 5, c->tm_shape))
         return HAP_OK;
     const uint32_t box_b = (uint32_t)maskgemm_b_rows(pair_mode);
     const uint64_t zr = (uint64_t)zt_rows(c->d_pad);
-    if (!make_map(&c->tmA, c->buf[kMask], (uint64_t)c->n_pad, (uint64_t)mask_rows_cap(c), kTileM) ||
+    const uint64_t mr = (uint64_t)mask_rows_cap(c);
+    if (!make_map(&c->tmA[0], c->buf[kMask], (uint64_t)c->n_pad, mr, kTileM) ||
+        !make_map(&c->tmA[1], c->buf[kMask1], (uint64_t)c->n_pad, mr, kTileM) ||
         !make_map(&c->tmBhi, c->buf[kZhi], (uint64_t)c->n_pad, zr, box_b) ||
         !make_map(&c->tmBlo, c->buf[kZlo], (uint64_t)c->n_pad, zr, box_b))
         return fail(c, HAP_E_CUDA, "cuTensorMapEncodeTiled failed");
-    std::copy(keys, keys + 3, c->tm_key);
-    std::copy(shape, shape + 4, c->tm_shape);
+    std::copy(keys, keys + 4, c->tm_key);
+    std::copy(shape, shape + 5, c->tm_shape);
     return HAP_OK;
 }
 
@@ -215,6 +226,27 @@ hap_status hap_create(int device, hap_ctx* out) {
     c->device = device;
     c->sm_count = prop.multiProcessorCount;
     cudaSetDevice(device);
+    // K1 scratch words: no ZeroVector row seen yet, tickets at zero
+    if (ensure(c, kScratch, 64) != HAP_OK) {
+        delete c;
+        return HAP_E_OOM;
+    }
+    if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess) {
+        hap_destroy(c);
+        return HAP_E_CUDA;
+    }
+    for (int i = 0; i < 2; ++i)
+        if (cudaEventCreateWithFlags(&c->ev_ready[i], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->ev_free[i], cudaEventDisableTiming) != cudaSuccess) {
+            hap_destroy(c);
+            return HAP_E_CUDA;
+        }
+    const long long init[2] = {0x7fffffffffffffffll, 0};
+    if (cudaMemcpy(c->buf[kScratch], init, sizeof init, cudaMemcpyHostToDevice) != cudaSuccess) {
+        hap_destroy(c);
+        return HAP_E_CUDA;
+    }
     *out = c;
     return HAP_OK;
 }
@@ -230,6 +262,15 @@ hap_status hap_destroy(hap_ctx c) {
         cudaEventDestroy(m.b);
     }
     for (auto e : c->pool) cudaEventDestroy(e);
+    if (c->side) {
+        cudaStreamSynchronize(c->side);
+        cudaStreamDestroy(c->side);
+    }
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    for (int i = 0; i < 2; ++i) {
+        if (c->ev_ready[i]) cudaEventDestroy(c->ev_ready[i]);
+        if (c->ev_free[i]) cudaEventDestroy(c->ev_free[i]);
+    }
     delete c;
     return HAP_OK;
 }
@@ -275,7 +316,8 @@ hap_status hap_align(hap_ctx c, const float* X, int64_t n_x, const float* Y, int
     hap_status s;
     if ((s = ensure(c, kNrm, N * 8)) || (s = ensure(c, kCoef, N * 8)) ||
         (s = ensure(c, kPart, (size_t)(nbx + nby) * d * 8)) || (s = ensure(c, kXbar, d * 8)) ||
-        (s = ensure(c, kYbar, d * 8)) || (s = ensure(c, kU, d * 8)) ||
+        (s = ensure(c, kYbar, d * 8)) || (s = ensure(c, kScal, 64)) ||
+        (s = ensure(c, kSpart, (size_t)2 * ceil_div(d_pad, 256) * 8)) ||
         (s = ensure(c, kZhi, (size_t)zt_rows(d_pad) * n_pad * 2)) ||
         (s = ensure(c, kZlo, (size_t)zt_rows(d_pad) * n_pad * 2)) ||
         (s = ensure(c, kTpart, (size_t)(n_pad / kRowTile) * d_pad * 8)) ||
@@ -319,7 +361,9 @@ hap_status hap_align(hap_ctx c, const float* X, int64_t n_x, const float* Y, int
     a.part = B<double>(c, kPart);
     a.xbar = B<double>(c, kXbar);
     a.ybar = B<double>(c, kYbar);
-    a.u = B<double>(c, kU);
+    a.scal = B<double>(c, kScal);
+    a.spart = B<double>(c, kSpart);
+    a.scratch = B<long long>(c, kScratch);
     a.zt_hi = B<uint16_t>(c, kZhi);
     a.zt_lo = B<uint16_t>(c, kZlo);
     a.tpart = B<double>(c, kTpart);
@@ -327,7 +371,11 @@ hap_status hap_align(hap_ctx c, const float* X, int64_t n_x, const float* Y, int
     a.m = B<double>(c, kM);
     a.ab = B<float2>(c, kAB);
     a.sconst = B<double>(c, kSconst);
-    cudaError_t e;
+    // fork the generator stream here: K2 of the coming hap_permtest may run during K1
+    cudaError_t e = cudaEventRecord(c->ev_fork, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c->side, c->ev_fork, 0);
+    if (e != cudaSuccess) return cuda_fail(c, e, "fork");
+    c->forked = true;
     {
         PhaseScope ps(c, HAP_PHASE_ALIGN, kAlignLaunches, st);
         e = launch_align(a, st);
@@ -363,17 +411,26 @@ hap_status hap_permtest(hap_ctx c, hap_align_info* info, const hap_perm_cfg* cfg
     const int nchunks = (int)ceil_div(c->d_pad, kChunkN);
     hap_status s;
     if ((s = ensure(c, kMask, (size_t)tiles * R * c->n_pad * 2)) ||
+        (s = ensure(c, kMask1, (size_t)tiles * R * c->n_pad * 2)) ||
         (s = ensure(c, kGemmPart, (size_t)tiles * nchunks * R * sizeof(float2))) ||
         (s = ensure(c, kTileDone, (size_t)tiles * sizeof(unsigned))))
         return s;
     if ((s = refresh_maps(c, pair))) return s;
+    cudaError_t e;
+    if (!c->forked) {  // no hap_align since the last permtest: fork after all prior work
+        e = cudaEventRecord(c->ev_fork, st);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(c->side, c->ev_fork, 0);
+        if (e != cudaSuccess) return cuda_fail(c, e, "fork");
+    }
+    c->forked = false;
     GemmArgs g = gemm_args(c, info);
     g.counts = counts;
     g.rows_per_tile = (int)R;
     g.tie_rel = cfg->tie_rel > 0 ? cfg->tie_rel : 1e-6;
-    for (int64_t off = 0; off < total; off += blk) {
+    for (int64_t off = 0, blkno = 0; off < total; off += blk, ++blkno) {
         const int64_t cnt = std::min<int64_t>(blk, total - off);
         const int64_t nt = ceil_div(cnt, R - 1);
+        const int slot = (int)(blkno & 1);
         PermArgs pa{};
         pa.seed = cfg->seed;
         pa.s = cfg->stream_id;
@@ -382,24 +439,27 @@ hap_status hap_permtest(hap_ctx c, hap_align_info* info, const hap_perm_cfg* cfg
         pa.N = c->n_x + c->n_y;
         pa.n_x = c->n_x;
         pa.n_pad = c->n_pad;
-        pa.out = c->buf[kMask];
+        pa.out = c->buf[slot ? kMask1 : kMask];
         pa.out_kind = kMaskBf16Row;
         pa.rows_per_tile = (int)R;
         pa.ntiles = (int)nt;
-        pa.info = info;
-        cudaError_t e;
-        {
-            PhaseScope ps(c, HAP_PHASE_PERMGEN, 1, st);
-            e = launch_perm(pa, c->sm_count, st);
+        // K2 on the side stream; a slot is rewritten only after the K3 that read it
+        e = blkno >= 2 ? cudaStreamWaitEvent(c->side, c->ev_free[slot], 0) : cudaSuccess;
+        if (e == cudaSuccess) {
+            PhaseScope ps(c, HAP_PHASE_PERMGEN, 1, c->side);
+            e = launch_perm(pa, c->sm_count, c->side);
         }
+        if (e == cudaSuccess) e = cudaEventRecord(c->ev_ready[slot], c->side);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, c->ev_ready[slot], 0);  // join
         if (e != cudaSuccess) return cuda_fail(c, e, "perm generator");
         g.count = (int)cnt;
         g.ntiles = (int)nt;
         g.stats = stats ? stats + 3 * off : nullptr;
         {
             PhaseScope ps(c, HAP_PHASE_MASKGEMM, 1, st);
-            e = launch_maskgemm(&c->tmA, &c->tmBhi, &c->tmBlo, g, pair, c->sm_count, st);
+            e = launch_maskgemm(&c->tmA[slot], &c->tmBhi, &c->tmBlo, g, pair, c->sm_count, st);
         }
+        if (e == cudaSuccess) e = cudaEventRecord(c->ev_free[slot], st);
         if (e != cudaSuccess) return cuda_fail(c, e, "mask-GEMM");
     }
     c->last_stream = st;
@@ -478,7 +538,6 @@ hap_status hap_perm_sets(hap_ctx c, uint64_t seed, uint32_t stream_id, uint64_t 
     pa.out_kind = kMaskU8Set;
     pa.rows_per_tile = 0;
     pa.ntiles = 0;
-    pa.info = nullptr;
     cudaError_t e = launch_perm(pa, c->sm_count, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(c, e, "perm generator");
     return HAP_OK;

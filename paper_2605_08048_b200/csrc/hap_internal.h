@@ -26,13 +26,15 @@ struct AlignArgs {
     int mode;                // hap_align_mode
     hap_align_info* info;    // device
     double* nrm;             // [N]    row norms ||h_i||
-    double* coef;            // [N]    2 u^T x_i  (0 for Y rows / identity)
+    double* coef;            // [n_x]  2 u^T x_i (0 for the identity)
     double* part;            // [nblk_x + nblk_y][d] fp64 column partials
     double* xbar;            // [d]
     double* ybar;            // [d]
-    double* u;               // [d]    Householder axis (fp64)
-    uint16_t* zt_hi;         // [d_pad][n_pad] bf16 bits
-    uint16_t* zt_lo;         // [d_pad][n_pad]
+    double* scal;            // [8]    {||xbar||, ||ybar||, ||v||, u.xbar, identity}
+    double* spart;           // [2 * max grid] per-CTA scalar partials
+    long long* scratch;      // [0] min ZeroVector row (LLONG_MAX = none), [1] two tickets
+    uint16_t* zt_hi;         // [>=d_pad][n_pad] bf16 bits
+    uint16_t* zt_lo;         // [>=d_pad][n_pad]
     double* m;               // [d_pad] centre (multiple of 2^-12): planes hold z - m
     double* tpart;           // [n_pad/kRowTile][d_pad] fp64 partials of t' = sum (hi + lo)
     double* t64;             // [d_pad] t = N m + t'
@@ -40,7 +42,7 @@ struct AlignArgs {
     double* sconst;          // [2]     {sum a^2, sum b^2}
 };
 cudaError_t launch_align(const AlignArgs& a, cudaStream_t st);
-constexpr int kAlignLaunches = 6;  // kernels issued by launch_align
+constexpr int kAlignLaunches = 5;  // kernels issued by launch_align
 
 // ---- K2: PERM-SPEC v1 generator (k_perm.cu) ----------------------------------------
 enum MaskOut { kMaskBf16Row = 0, kMaskU8Set = 1 };
@@ -55,7 +57,6 @@ struct PermArgs {
     int rows_per_tile;       // bf16 mode: R; perm p -> row (p/(R-1))*R + 1 + p%(R-1),
                              // row t*R = observed split {0..n_x-1} for t < ntiles
     int ntiles;
-    const hap_align_info* info;  // optional: skip if info->status != 0
 };
 cudaError_t launch_perm(const PermArgs& a, int sm_count, cudaStream_t st);
 

@@ -1,14 +1,18 @@
-// k_align.cu — K1: S1-S5 of the hot path (DESIGN.md "Kernels" K1a-K1e).
+// k_align.cu — K1: S1-S6 of the hot path (DESIGN.md "Kernels" K1a-K1e).
 //
 //   S1 normalise   x = h/||h||               PAPER.md:115-118 (§3.1 Eq. 2)
 //   S2 means       xbar, ybar, mu_x, mu_y    PAPER.md:143-148; Alg. 1
 //   S3 axis        u = (mu_x-mu_y)/||.||     PAPER.md:149-156 (Eqs. 5-6); Alg. 1 :664
 //   S4 reflect     x' = x - 2u(u^T x)        PAPER.md:157-161, 245-255 (Eq. householder_fast)
-//   S5 pool+split  Z = [X';Y] -> bf16 hi/lo planes (transposed, K contiguous), t = 1^T Z
-//                                             PAPER.md:183, 215-218 (Eq. gemm), 258
+//   S5 pool+split  Z = [X';Y] -> centred bf16 hi/lo planes (transposed, K contiguous),
+//                  t = 1^T Z                 PAPER.md:183, 215-218 (Eq. gemm), 258
+//   S6 observed    r_X = ||xbar|| (= r(X')), r_Y, T_obs (Eq. 10), fp64
 //
-// All reductions are fixed-order (per-block fp64 partials summed in ascending block
-// order), so Z~ and t are bit-identical across runs and ranks.
+// Five grid-wide kernels, none single-CTA: per-row-block partials (K1a), per-column means
+// with a last-arriving-CTA scalar finalize (K1b), per-row reflection coefficients (K1c),
+// reflect/centre/split/transpose tiles (K1d), per-column totals with a last-CTA finalize of
+// the epilogue constants (K1e).  All reductions are fixed-order (partials summed in
+// ascending block order), so Z~ and t are bit-identical across runs and ranks.
 #include <cuda_bf16.h>
 
 #include <cfloat>
@@ -33,8 +37,8 @@ __device__ double block_sum(double v, double* red) {
     __syncthreads();
     if (l == 0) red[w] = v;
     __syncthreads();
-    double s = 0.0;
     if (threadIdx.x == 0) {
+        double s = 0.0;
         for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
         red[32] = s;
     }
@@ -42,6 +46,7 @@ __device__ double block_sum(double v, double* red) {
     return red[32];
 }
 
+// L(r) = log kappa-hat(r), r clamped to [0, 1-1e-9] (Eq. 9; R1, R4)
 __device__ __forceinline__ double logkappa64(double r, double d) {
     if (r > 1.0 - 1e-9) r = 1.0 - 1e-9;
     if (r <= 0.0) return -INFINITY;
@@ -53,151 +58,191 @@ __device__ __forceinline__ const float* row_ptr(const AlignArgs& a, int64_t i) {
     return i < a.n_x ? a.X + i * a.d : a.Y + (i - a.n_x) * a.d;
 }
 
-// K1 init: shape fields and a clean status
-__global__ void k1_init(AlignArgs a) {
-    hap_align_info* f = a.info;
-    f->n_x = a.n_x;
-    f->n_y = a.n_y;
-    f->d = a.d;
-    f->n_pad = a.n_pad;
-    f->d_pad = a.d_pad;
-    f->is_identity = 0;
-    f->status = HAP_OK;
-    f->bad_row = LLONG_MAX;
-    f->r_x = f->r_y = f->logk_x = f->logk_y = f->t_obs = 0.0;
-    f->gemm_r_x = f->gemm_r_y = f->gemm_t_obs = __longlong_as_double(0x7ff8000000000000ll);  // NaN
-}
-
-// K1a (S1+S2 partials): one CTA per block of kRowBlock rows of X or of Y.
+// ---------------------------------------------------------------------------------
+// K1a (S1 + S2 partials): one CTA per block of kRowBlock rows of X or of Y.
 // Phase 1: warp-per-row fp64 norms ||h_i|| (ZeroVector check).
 // Phase 2: fp64 column partial sums of the normalised rows h_i/||h_i||.
-__global__ void __launch_bounds__(256) k1_norm_colsum(AlignArgs a, int nblk_x) {
+__global__ void __launch_bounds__(256) k1a_norm_colsum(AlignArgs a, int nblk_x) {
     __shared__ double s_inv[kRowBlock];
     const bool isx = (int)blockIdx.x < nblk_x;
     const int64_t blk = isx ? blockIdx.x : blockIdx.x - nblk_x;
     const int64_t nrows = isx ? a.n_x : a.n_y;
     const int64_t r0 = blk * kRowBlock;
-    const int64_t rn = (nrows - r0 < kRowBlock) ? (nrows - r0) : (int64_t)kRowBlock;
+    const int rn = (int)((nrows - r0 < kRowBlock) ? (nrows - r0) : (int64_t)kRowBlock);
     const int64_t base = isx ? r0 : a.n_x + r0;  // pooled row index of local row 0
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const bool vec = (a.d & 3) == 0;
     for (int r = w; r < rn; r += 8) {
         const float* h = row_ptr(a, base + r);
         double s = 0.0;
-        for (int64_t c = l; c < a.d; c += 32) {
-            const double v = (double)h[c];
-            s += v * v;
+        if (vec) {
+            const float4* h4 = reinterpret_cast<const float4*>(h);
+            for (int64_t c = l; c < a.d / 4; c += 32) {
+                const float4 v = __ldg(h4 + c);
+                s += (double)v.x * v.x + (double)v.y * v.y + (double)v.z * v.z + (double)v.w * v.w;
+            }
+        } else {
+            for (int64_t c = l; c < a.d; c += 32) {
+                const double v = (double)h[c];
+                s += v * v;
+            }
         }
         s = warp_sum(s);
         if (l == 0) {
             const double nrm = sqrt(s);
             a.nrm[base + r] = nrm;
-            if (nrm < 1e-12) {
-                a.info->status = HAP_E_ZERO_VECTOR;
-                atomicMin(reinterpret_cast<long long*>(&a.info->bad_row), (long long)(base + r));
-                s_inv[r] = 0.0;
-            } else {
-                s_inv[r] = 1.0 / nrm;
-            }
+            if (nrm < 1e-12) atomicMin(reinterpret_cast<long long*>(a.scratch), (long long)(base + r));
+            s_inv[r] = nrm < 1e-12 ? 0.0 : 1.0 / nrm;
         }
     }
     __syncthreads();
     double* part = a.part + (int64_t)blockIdx.x * a.d;
-    for (int64_t c = threadIdx.x; c < a.d; c += blockDim.x) {
-        double acc = 0.0;
-        for (int r = 0; r < rn; ++r) acc += (double)row_ptr(a, base + r)[c] * s_inv[r];
-        part[c] = acc;
+    if (vec) {
+        for (int64_t c4 = threadIdx.x; c4 < a.d / 4; c4 += blockDim.x) {
+            double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+            for (int r = 0; r < rn; ++r) {
+                const float4 v = __ldg(reinterpret_cast<const float4*>(row_ptr(a, base + r)) + c4);
+                const double iv = s_inv[r];
+                s0 += (double)v.x * iv;
+                s1 += (double)v.y * iv;
+                s2 += (double)v.z * iv;
+                s3 += (double)v.w * iv;
+            }
+            part[4 * c4 + 0] = s0;
+            part[4 * c4 + 1] = s1;
+            part[4 * c4 + 2] = s2;
+            part[4 * c4 + 3] = s3;
+        }
+    } else {
+        for (int64_t c = threadIdx.x; c < a.d; c += blockDim.x) {
+            double acc = 0.0;
+            for (int r = 0; r < rn; ++r) acc += (double)row_ptr(a, base + r)[c] * s_inv[r];
+            part[c] = acc;
+        }
     }
 }
 
-// K1b (S2 finish + S3): one CTA.  xbar, ybar from the partials in ascending block order,
-// norms, DegenerateMean check, mean directions, Householder axis u (fp64).
-__global__ void __launch_bounds__(1024) k1_finalize(AlignArgs a, int nblk_x, int nblk_y) {
+// ---------------------------------------------------------------------------------
+// K1b (S2 finish + S3 + S6): CTA per 256 columns: xbar_c, ybar_c from the block partials
+// (ascending block order), per-CTA partial sums of ||xbar||^2, ||ybar||^2.  The last CTA
+// to finish (atomic ticket) finalises the scalars in fixed order: norms, DegenerateMean,
+// v = mu_x - mu_y (||v|| and v.xbar summed directly), identity test, r, L, T_obs, info.
+__global__ void __launch_bounds__(256) k1b_means(AlignArgs a, int nblk_x, int nblk_y) {
     __shared__ double red[33];
-    double sx = 0.0, sy = 0.0;
-    for (int64_t c = threadIdx.x; c < a.d; c += blockDim.x) {
+    __shared__ int s_last;
+    double sxx = 0.0, syy = 0.0;
+    for (int64_t c = (int64_t)blockIdx.x * 256 + threadIdx.x; c < a.d && threadIdx.x < 256;
+         c += (int64_t)gridDim.x * 256) {
         double xs = 0.0, ys = 0.0;
         for (int b = 0; b < nblk_x; ++b) xs += a.part[(int64_t)b * a.d + c];
         for (int b = 0; b < nblk_y; ++b) ys += a.part[(int64_t)(nblk_x + b) * a.d + c];
         const double xb = xs / (double)a.n_x, yb = ys / (double)a.n_y;
         a.xbar[c] = xb;
         a.ybar[c] = yb;
-        sx += xb * xb;
-        sy += yb * yb;
+        sxx += xb * xb;
+        syy += yb * yb;
     }
-    const double nx = sqrt(block_sum(sx, red));
-    const double ny = sqrt(block_sum(sy, red));
+    sxx = block_sum(sxx, red);
+    syy = block_sum(syy, red);
+    if (threadIdx.x == 0) {
+        a.spart[2 * blockIdx.x + 0] = sxx;
+        a.spart[2 * blockIdx.x + 1] = syy;
+        __threadfence();
+        const unsigned t = atomicAdd(reinterpret_cast<unsigned*>(a.scratch + 1), 1u);
+        s_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    // ---- last CTA: scalars
+    double SX = 0.0, SY = 0.0;
+    for (int b = 0; b < (int)gridDim.x; ++b) {
+        SX += __ldcg(a.spart + 2 * b);
+        SY += __ldcg(a.spart + 2 * b + 1);
+    }
+    const double nx = sqrt(SX), ny = sqrt(SY);
     const bool degenerate = nx < 1e-12 || ny < 1e-12;
     bool identity = (a.mode == HAP_ALIGN_NONE) || degenerate;
-    double nv = 0.0;
+    double nv = 0.0, vx = 0.0;
     if (!identity) {
-        double sv = 0.0;
+        double sv = 0.0, svx = 0.0;
         for (int64_t c = threadIdx.x; c < a.d; c += blockDim.x) {
-            const double v = a.xbar[c] / nx - a.ybar[c] / ny;
+            const double xb = __ldcg(a.xbar + c), yb = __ldcg(a.ybar + c);
+            const double v = xb / nx - yb / ny;
             sv += v * v;
+            svx += v * xb;
         }
         nv = sqrt(block_sum(sv, red));
+        vx = block_sum(svx, red);
         identity = nv < 1e-9;  // coincident mean directions (R3)
     }
-    double sux = 0.0;
-    for (int64_t c = threadIdx.x; c < a.d; c += blockDim.x) {
-        const double uc = identity ? 0.0 : (a.xbar[c] / nx - a.ybar[c] / ny) / nv;
-        a.u[c] = uc;
-        sux += uc * a.xbar[c];
-    }
-    // Centre m = t/N, quantised to a multiple of 2^-12 (exact shift,
-    // since every mask row has exactly n_x ones).  t follows from the means without the
-    // reflected rows: t = n_x (xbar - 2u(u^T xbar)) + n_y ybar.
-    const double ux = block_sum(sux, red);
-    const double Nd = (double)(a.n_x + a.n_y);
-    for (int64_t c = threadIdx.x; c < a.d_pad; c += blockDim.x) {
-        double m = 0.0;
-        if (c < a.d) {
-            const double t = (double)a.n_x * (a.xbar[c] - 2.0 * a.u[c] * ux) + (double)a.n_y * a.ybar[c];
-            m = rint(t / Nd * 4096.0) / 4096.0;
-        }
-        a.m[c] = m;
-    }
     if (threadIdx.x == 0) {
+        double* sc = a.scal;
+        sc[0] = nx;
+        sc[1] = ny;
+        sc[2] = identity ? 0.0 : nv;
+        sc[3] = identity ? 0.0 : vx / nv;  // u . xbar
+        sc[4] = identity ? 1.0 : 0.0;
         hap_align_info* f = a.info;
-        // observed statistic in fp64 (Alg. 1 step 4): r(X') = ||xbar|| since
-        // H is orthogonal; T_obs = L(r_Y) - L(r_X) (Eq. 10; R1, R4)
+        const long long bad = *reinterpret_cast<volatile long long*>(a.scratch);
+        f->n_x = a.n_x;
+        f->n_y = a.n_y;
+        f->d = a.d;
+        f->n_pad = a.n_pad;
+        f->d_pad = a.d_pad;
+        f->is_identity = identity ? 1 : 0;
+        f->status = bad < a.n_x + a.n_y ? HAP_E_ZERO_VECTOR
+                                        : (degenerate ? HAP_E_DEGENERATE_MEAN : HAP_OK);
+        f->bad_row = bad < a.n_x + a.n_y ? bad : -1;
+        // observed statistic in fp64 (Alg. 1 step 4): r(X') = ||xbar||
+        // since H is orthogonal; T_obs = L(r_Y) - L(r_X) (Eq. 10)
         f->r_x = nx;
         f->r_y = ny;
         const double lx = logkappa64(nx, (double)a.d), ly = logkappa64(ny, (double)a.d);
         f->logk_x = lx;
         f->logk_y = ly;
         f->t_obs = (isinf(lx) && isinf(ly)) ? 0.0 : ly - lx;
-        f->is_identity = identity ? 1 : 0;
-        if (f->status == HAP_OK && degenerate) f->status = HAP_E_DEGENERATE_MEAN;
-        if (f->bad_row == LLONG_MAX) f->bad_row = -1;
+        const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+        f->gemm_r_x = f->gemm_r_y = f->gemm_t_obs = qnan;
+        // reset the scratch words for the next call
+        a.scratch[0] = LLONG_MAX;
+        reinterpret_cast<unsigned*>(a.scratch + 1)[0] = 0u;
     }
 }
 
-// K1c (S4 coefficient): warp per pooled row, coef_i = 2 u^T x_i = 2 (u^T h_i)/||h_i||
-// for X rows (0 for Y rows and the identity).
-__global__ void __launch_bounds__(256) k1_rowdot(AlignArgs a) {
-    const int64_t N = a.n_x + a.n_y;
+__device__ __forceinline__ double axis_c(const AlignArgs& a, int64_t c) {  // u_c
+    const double nv = a.scal[2];
+    if (nv == 0.0 || c >= a.d) return 0.0;
+    return (a.xbar[c] / a.scal[0] - a.ybar[c] / a.scal[1]) / nv;
+}
+
+// ---------------------------------------------------------------------------------
+// K1c (S4 coefficient): warp per X row, coef_i = 2 u^T x_i = 2 (u^T h_i)/||h_i||.
+__global__ void __launch_bounds__(256) k1c_rowdot(AlignArgs a) {
     const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int l = threadIdx.x & 31;
-    if (i >= N) return;
-    if (i >= a.n_x || a.info->is_identity) {
+    if (i >= a.n_x) return;
+    if (a.scal[4] != 0.0) {
         if (l == 0) a.coef[i] = 0.0;
         return;
     }
+    const double nx = a.scal[0], ny = a.scal[1], nv = a.scal[2];
     const float* h = a.X + i * a.d;
     double s = 0.0;
-    for (int64_t c = l; c < a.d; c += 32) s += (double)h[c] * a.u[c];
+    for (int64_t c = l; c < a.d; c += 32)
+        s += (double)__ldg(h + c) * (__ldg(a.xbar + c) / nx - __ldg(a.ybar + c) / ny);
     s = warp_sum(s);
-    if (l == 0) a.coef[i] = a.nrm[i] > 0.0 ? 2.0 * s / a.nrm[i] : 0.0;
+    if (l == 0) a.coef[i] = a.nrm[i] > 0.0 ? 2.0 * (s / nv) / a.nrm[i] : 0.0;
 }
 
-// K1d (S4 reflect + S5 split/transpose + t partials): CTA per (64-row tile, 64-col tile).
-// z = h/||h|| - coef * u  (fp64), centred z' = z - m;  hi = bf16(z'), lo = bf16(z' - hi)
-// (R9 and "Numerics");
-// written transposed into Zt_hi/Zt_lo [d_pad][n_pad] (GEMM K contiguous).
-// t partial of the tile: sum over its 64 rows of (hi + lo) in fp64, fixed order.
+// ---------------------------------------------------------------------------------
+// K1d (S4 reflect + S5 centre/split/transpose + t partials): CTA per (64 rows, 64 cols).
+// z = h/||h|| - coef * u  (fp64), centred z' = z - m with m = t/N quantised to 2^-12, where
+// t = n_x (xbar - 2u(u^T xbar)) + n_y ybar follows from the means;
+// hi = bf16(z'), lo = bf16(z' - hi)  (R9, "Numerics"); written transposed into
+// Zt_hi/Zt_lo [d_pad][n_pad].  t partial of the tile: fixed-order fp64 sum of (hi + lo).
 constexpr int kSP = 33;  // padded smem row pitch in 32-bit words (64 bf16 + pad)
-__global__ void __launch_bounds__(256) k1_reflect_split(AlignArgs a) {
+__global__ void __launch_bounds__(256) k1d_reflect_split(AlignArgs a) {
     __shared__ uint32_t s_hi[64 * kSP];
     __shared__ uint32_t s_lo[64 * kSP];
     const int64_t N = a.n_x + a.n_y;
@@ -207,8 +252,13 @@ __global__ void __launch_bounds__(256) k1_reflect_split(AlignArgs a) {
     uint16_t* sh16 = reinterpret_cast<uint16_t*>(s_hi);
     uint16_t* sl16 = reinterpret_cast<uint16_t*>(s_lo);
     const int64_t c = c0 + tc;
-    const double uc = (c < a.d) ? a.u[c] : 0.0;
-    const double mc = (c < a.d) ? a.m[c] : 0.0;
+    const double uc = axis_c(a, c);
+    double mc = 0.0;
+    if (c < a.d) {
+        const double t = (double)a.n_x * (a.xbar[c] - 2.0 * uc * a.scal[3]) + (double)a.n_y * a.ybar[c];
+        mc = rint(t / (double)N * 4096.0) / 4096.0;
+    }
+    if (blockIdx.x == 0 && tr == 0 && c < a.d_pad) a.m[c] = mc;
 #pragma unroll 4
     for (int j = 0; j < 16; ++j) {
         const int rl = tr + 4 * j;
@@ -217,7 +267,8 @@ __global__ void __launch_bounds__(256) k1_reflect_split(AlignArgs a) {
         if (i < N && c < a.d) {
             const double nrm = a.nrm[i];
             const double h = (double)row_ptr(a, i)[c];
-            z = (nrm > 0.0 ? h / nrm : 0.0) - a.coef[i] * uc - mc;
+            const double cf = i < a.n_x ? a.coef[i] : 0.0;
+            z = (nrm > 0.0 ? h / nrm : 0.0) - cf * uc - mc;
         }
         const __nv_bfloat16 hi = __double2bfloat16(z);
         const __nv_bfloat16 lo = __double2bfloat16(z - (double)__bfloat162float(hi));
@@ -235,7 +286,6 @@ __global__ void __launch_bounds__(256) k1_reflect_split(AlignArgs a) {
         uint32_t* dl = reinterpret_cast<uint32_t*>(a.zt_lo + col * a.n_pad + r0);
         dh[l] = vh;
         dl[l] = vl;
-        // t partial for column `col` over these 64 rows (fixed order: pairs, then xor tree)
         const double v = (double)__bfloat162float(__ushort_as_bfloat16((uint16_t)(vh & 0xFFFF))) +
                          (double)__bfloat162float(__ushort_as_bfloat16((uint16_t)(vl & 0xFFFF))) +
                          (double)__bfloat162float(__ushort_as_bfloat16((uint16_t)(vh >> 16))) +
@@ -245,15 +295,17 @@ __global__ void __launch_bounds__(256) k1_reflect_split(AlignArgs a) {
     }
 }
 
-// K1e (S5 finish + epilogue constants), one CTA.  t'[c] = sum of the row-tile partials
-// (ascending tile order) of the centred planes; t = N m + t'.  With a = n_x m and
-// b = t - a = n_y m + t' (both rounded to fp32), the epilogue forms
-//   S1 = ||a + acc||^2 = SA + sum acc (acc + 2a),   S2 = ||b - acc||^2 = SB + sum acc (acc - 2b)
-// with SA = sum a^2, SB = sum b^2 in fp64.
-__global__ void __launch_bounds__(1024) k1_tfinal(AlignArgs a, int ntiles) {
+// ---------------------------------------------------------------------------------
+// K1e (S5 finish + epilogue constants): CTA per 256 columns.  t'[c] = sum of the row-tile
+// partials (ascending); t = N m + t'.  With a = n_x m and b = t - a = n_y m + t' (fp32),
+// the GEMM epilogue forms S1 = SA + sum acc (acc + 2a), S2 = SB + sum acc (acc - 2b) with
+// SA = sum a^2, SB = sum b^2 (fp64; last CTA sums the per-CTA partials in fixed order).
+__global__ void __launch_bounds__(256) k1e_tfinal(AlignArgs a, int ntiles) {
     __shared__ double red[33];
+    __shared__ int s_last;
     double sa = 0.0, sb = 0.0;
-    for (int64_t c = threadIdx.x; c < a.d_pad; c += blockDim.x) {
+    const int64_t c = (int64_t)blockIdx.x * 256 + threadIdx.x;
+    if (c < a.d_pad) {
         double tp = 0.0;
         for (int t = 0; t < ntiles; ++t) tp += a.tpart[(int64_t)t * a.d_pad + c];
         const double m = a.m[c];
@@ -261,15 +313,29 @@ __global__ void __launch_bounds__(1024) k1_tfinal(AlignArgs a, int ntiles) {
         const float af = (float)((double)a.n_x * m);
         const float bf = (float)((double)a.n_y * m + tp);
         a.ab[c] = make_float2(2.0f * af, 2.0f * bf);
-        sa += (double)af * (double)af;
-        sb += (double)bf * (double)bf;
+        sa = (double)af * (double)af;
+        sb = (double)bf * (double)bf;
     }
     sa = block_sum(sa, red);
     sb = block_sum(sb, red);
     if (threadIdx.x == 0) {
-        a.sconst[0] = sa;
-        a.sconst[1] = sb;
+        a.spart[2 * blockIdx.x + 0] = sa;
+        a.spart[2 * blockIdx.x + 1] = sb;
+        __threadfence();
+        const unsigned t = atomicAdd(reinterpret_cast<unsigned*>(a.scratch + 1) + 1, 1u);
+        s_last = (t == gridDim.x - 1);
     }
+    __syncthreads();
+    if (!s_last || threadIdx.x != 0) return;
+    __threadfence();
+    double SA = 0.0, SB = 0.0;
+    for (int b = 0; b < (int)gridDim.x; ++b) {
+        SA += __ldcg(a.spart + 2 * b);
+        SB += __ldcg(a.spart + 2 * b + 1);
+    }
+    a.sconst[0] = SA;
+    a.sconst[1] = SB;
+    reinterpret_cast<unsigned*>(a.scratch + 1)[1] = 0u;
 }
 
 }  // namespace
@@ -277,14 +343,14 @@ __global__ void __launch_bounds__(1024) k1_tfinal(AlignArgs a, int ntiles) {
 cudaError_t launch_align(const AlignArgs& a, cudaStream_t st) {
     const int64_t N = a.n_x + a.n_y;
     const int nbx = (int)ceil_div(a.n_x, kRowBlock), nby = (int)ceil_div(a.n_y, kRowBlock);
-    k1_init<<<1, 1, 0, st>>>(a);
-    k1_norm_colsum<<<nbx + nby, 256, 0, st>>>(a, nbx);
-    k1_finalize<<<1, 1024, 0, st>>>(a, nbx, nby);
-    k1_rowdot<<<(unsigned)ceil_div(N * 32, 256), 256, 0, st>>>(a);
+    k1a_norm_colsum<<<nbx + nby, 256, 0, st>>>(a, nbx);
+    k1b_means<<<(unsigned)ceil_div(a.d, 256), 256, 0, st>>>(a, nbx, nby);
+    k1c_rowdot<<<(unsigned)ceil_div(a.n_x * 32, 256), 256, 0, st>>>(a);
     const int ntiles = (int)(a.n_pad / kRowTile);
     dim3 grid((unsigned)ntiles, (unsigned)ceil_div(a.d_pad, 64));
-    k1_reflect_split<<<grid, 256, 0, st>>>(a);
-    k1_tfinal<<<1, 1024, 0, st>>>(a, ntiles);
+    k1d_reflect_split<<<grid, 256, 0, st>>>(a);
+    k1e_tfinal<<<(unsigned)ceil_div(a.d_pad, 256), 256, 0, st>>>(a, ntiles);
+    (void)N;
     return cudaGetLastError();
 }
 

@@ -50,7 +50,6 @@ __device__ __forceinline__ uint32_t fy_target(uint32_t x, uint32_t k, uint32_t N
 
 __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy(PermArgs a, int lt_pitch) {
     extern __shared__ __align__(16) uint8_t smem[];
-    if (a.info && a.info->status != HAP_OK) return;
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     uint16_t* LT = reinterpret_cast<uint16_t*>(smem) + (size_t)w * (lt_pitch + 128);
     uint16_t* stage = LT + lt_pitch;
@@ -81,41 +80,49 @@ __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy(PermArgs a, int lt
         __syncwarp();
         // ---- phase A: draws + last-writer scatter, 128 steps per round
         for (uint32_t k0 = 0; k0 < nx; k0 += 128) {
-            const uint32_t q = (k0 >> 2) + (uint32_t)l;
             if (k0 + 4u * l < nx) {
-                const u32x4 wd = philox4x32_10(u32x4{q, b, s, 0u}, key0, key1);
+                const u32x4 wd = philox4x32_10(u32x4{(k0 >> 2) + (uint32_t)l, b, s, 0u}, key0, key1);
+                uint32_t j[4];
 #pragma unroll
                 for (uint32_t e = 0; e < 4; ++e) {
                     const uint32_t k = k0 + 4u * l + e;
-                    if (k < nx) stage[4 * l + e] = (uint16_t)fy_target(u32x4_get(wd, e), k, N, b, s,
-                                                                       key0, key1);
+                    j[e] = k < nx ? fy_target(u32x4_get(wd, e), k, N, b, s, key0, key1) : 0u;
                 }
+                *reinterpret_cast<uint2*>(stage + 4 * l) =
+                    make_uint2(j[0] | (j[1] << 16), j[2] | (j[3] << 16));
             }
             __syncwarp();
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
                 const uint32_t idx = 32u * r + l, k = k0 + idx;
-                const bool valid = k < nx;
-                const uint32_t j = valid ? stage[idx] : 0u;
-                bool pending = valid && j != k;  // self-targets never move a value
-                // last writer (largest k) wins: lanes are in step order within the round
-                while (__any_sync(0xffffffffu, pending)) {
-                    if (pending) LT[j] = (uint16_t)(k + 1);
-                    __syncwarp();
-                    if (pending && LT[j] >= k + 1) pending = false;
-                    __syncwarp();
-                }
+                const uint32_t j = k < nx ? stage[idx] : 0u;
+                // self-targets never move a value and are not "writers" (k != q in LT)
+                const bool writes = k < nx && j != k;
+                // last writer (largest k = highest lane) of each target wins
+                const uint32_t peers = __match_any_sync(0xffffffffu, writes ? j : 0x10000u + l);
+                if (writes && (31 - __clz(peers)) == l) LT[j] = (uint16_t)(k + 1);
+                __syncwarp();  // order this round's stores before the next (larger k) round
             }
         }
-        __syncwarp();
-        // ---- phase B: each written high position exiles the end of its chain
-        for (uint32_t p = nx + l; p < N; p += 32) {
-            const uint16_t v = LT[p];
-            if (v) {
-                uint32_t kk = v - 1u;
-                uint16_t t;
-                while ((t = LT[kk]) != 0 && t != kExiled) kk = t - 1u;
-                LT[kk] = kExiled;
+        // ---- phase B: each written high position exiles the end of its chain; lanes
+        // walk chains one step per iteration and pick up new positions when free
+        {
+            uint32_t p = nx + l;
+            int kk = -1;
+            while (__any_sync(0xffffffffu, p < N || kk >= 0)) {
+                if (kk >= 0) {
+                    const uint16_t t = LT[kk];
+                    if (t != 0 && t != kExiled) {
+                        kk = (int)t - 1;
+                    } else {
+                        LT[kk] = kExiled;
+                        kk = -1;
+                    }
+                } else if (p < N) {
+                    const uint16_t v = LT[p];
+                    p += 32;
+                    if (v) kk = (int)v - 1;
+                }
             }
         }
         __syncwarp();
@@ -124,24 +131,33 @@ __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy(PermArgs a, int lt
             const int64_t R1 = a.rows_per_tile - 1;
             const int64_t orow = (pi / R1) * a.rows_per_tile + 1 + pi % R1;
             uint4* row = reinterpret_cast<uint4*>(static_cast<uint16_t*>(a.out) + orow * a.n_pad);
+            const uint4* L4 = reinterpret_cast<const uint4*>(LT);
             for (int64_t v8 = l; v8 < a.n_pad / 8; v8 += 32) {
-                uint32_t wds[4];
+                const uint4 q = L4[v8];
+                const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+                uint32_t o[4];
+                const int64_t v0 = 8 * v8;
+                if (v0 + 8 <= (int64_t)nx) {  // low block: selected unless exiled
 #pragma unroll
-                for (int e2 = 0; e2 < 4; ++e2) {
-                    uint32_t pack = 0;
+                    for (int e = 0; e < 4; ++e) o[e] = ~__vcmpeq2(w[e], 0xFFFFFFFFu) & 0x3F803F80u;
+                } else if (v0 >= (int64_t)nx) {  // high block: selected iff written
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const uint32_t v = (uint32_t)(8 * v8 + 2 * e2 + h);
-                        bool sel = false;
-                        if (v < N) {
-                            const uint16_t t = LT[v];
-                            sel = (v < nx) ? (t != kExiled) : (t != 0);
+                    for (int e = 0; e < 4; ++e) o[e] = __vcmpne2(w[e], 0u) & 0x3F803F80u;
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        uint32_t pack = 0;
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int64_t v = v0 + 2 * e + h;
+                            const uint32_t t = (w[e] >> (16 * h)) & 0xFFFFu;
+                            const bool sel = v < (int64_t)nx ? (t != kExiled) : (t != 0);
+                            pack |= (sel ? 0x3F80u : 0u) << (16 * h);
                         }
-                        pack |= (sel ? 0x3F80u : 0u) << (16 * h);
+                        o[e] = pack;
                     }
-                    wds[e2] = pack;
                 }
-                row[v8] = make_uint4(wds[0], wds[1], wds[2], wds[3]);
+                row[v8] = make_uint4(o[0], o[1], o[2], o[3]);
             }
         } else {
             uint8_t* row = static_cast<uint8_t*>(a.out) + pi * a.N;
