@@ -246,7 +246,7 @@ def run_hap(args):
 
     # ---------------- pass 2: per-kernel device time (CUDA events on the launching stream)
     Kp = min(K, 400)
-    hap.hap_profile(ctx.h, True)
+    hap.hap_profile(ctx.h, 2)  # serialised phases so the per-kernel times do not overlap
     for k in range(Kp):
         step(k)
     phase_ms, phase_n = hap.hap_profile_read(ctx.h, reset=True)

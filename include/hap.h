@@ -165,7 +165,8 @@ typedef enum {
     HAP_NUM_PHASES = 4
 } hap_phase;
 /* enable != 0: every later launch of the context is bracketed by CUDA events recorded on
- * its own stream (adds host work; leave off when timing whole steps). */
+ * its own stream (adds host work; leave off when timing whole steps).  enable >= 2 also
+ * serialises the generator onto the caller's stream so the phase times do not overlap. */
 HAP_API hap_status hap_profile(hap_ctx ctx, int enable);
 /* Synchronises the recorded events and returns, per phase, the summed device time (ms,
  * [host] double[HAP_NUM_PHASES]) of the launches timed since the last reset and the number

@@ -202,8 +202,9 @@ def hap_export_pooled(ctx, zhi, zlo, t, m, stream=None) -> None:
 PHASES = ("align", "observed", "permgen", "maskgemm")
 
 
-def hap_profile(ctx, enable: bool) -> None:
-    _check(ctx, lib().hap_profile(ctx, 1 if enable else 0))
+def hap_profile(ctx, enable) -> None:
+    """enable: 0 off, 1 per-phase events, 2 events + serialised phases."""
+    _check(ctx, lib().hap_profile(ctx, int(enable)))
 
 
 def hap_profile_read(ctx, reset: bool = False):

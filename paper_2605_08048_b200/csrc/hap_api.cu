@@ -39,6 +39,7 @@ struct hap_ctx_s {
     int slot = 0;
     // ---- profiling
     bool prof = false;
+    bool serial = false;  // profiling level 2: generator on the caller's stream
     struct Mark { cudaEvent_t a, b; int phase; };
     std::vector<Mark> marks;
     std::vector<cudaEvent_t> pool;
@@ -49,8 +50,8 @@ struct hap_ctx_s {
 namespace {
 
 enum Buf {
-    kX = 0, kY, kNrm, kCoef, kPart, kXbar, kYbar, kUnused, kZhi, kZlo, kTpart, kT64, kAB, kMask,
-    kM, kSconst, kGemmPart, kTileDone, kScal, kSpart, kScratch, kMask1, kNumBufs
+    kX = 0, kY, kNrm, kCoef, kPart, kXbar, kYbar, kU, kZhi, kZlo, kTpart, kT64, kAB, kMask,
+    kM, kSconst, kGemmPart, kTileDone, kScal, kSpart, kScratch, kMask1, kInv, kNumBufs
 };
 
 hap_status fail(hap_ctx c, hap_status s, const std::string& msg) {
@@ -317,7 +318,8 @@ hap_status hap_align(hap_ctx c, const float* X, int64_t n_x, const float* Y, int
     if ((s = ensure(c, kNrm, N * 8)) || (s = ensure(c, kCoef, N * 8)) ||
         (s = ensure(c, kPart, (size_t)(nbx + nby) * d * 8)) || (s = ensure(c, kXbar, d * 8)) ||
         (s = ensure(c, kYbar, d * 8)) || (s = ensure(c, kScal, 64)) ||
-        (s = ensure(c, kSpart, (size_t)2 * ceil_div(d_pad, 256) * 8)) ||
+        (s = ensure(c, kSpart, (size_t)2 * ceil_div(d_pad, 32) * 8)) ||
+        (s = ensure(c, kInv, N * 8)) || (s = ensure(c, kU, d_pad * 8)) ||
         (s = ensure(c, kZhi, (size_t)zt_rows(d_pad) * n_pad * 2)) ||
         (s = ensure(c, kZlo, (size_t)zt_rows(d_pad) * n_pad * 2)) ||
         (s = ensure(c, kTpart, (size_t)(n_pad / kRowTile) * d_pad * 8)) ||
@@ -362,6 +364,8 @@ hap_status hap_align(hap_ctx c, const float* X, int64_t n_x, const float* Y, int
     a.xbar = B<double>(c, kXbar);
     a.ybar = B<double>(c, kYbar);
     a.scal = B<double>(c, kScal);
+    a.inv = B<double>(c, kInv);
+    a.u = B<double>(c, kU);
     a.spart = B<double>(c, kSpart);
     a.scratch = B<long long>(c, kScratch);
     a.zt_hi = B<uint16_t>(c, kZhi);
@@ -444,12 +448,13 @@ hap_status hap_permtest(hap_ctx c, hap_align_info* info, const hap_perm_cfg* cfg
         pa.rows_per_tile = (int)R;
         pa.ntiles = (int)nt;
         // K2 on the side stream; a slot is rewritten only after the K3 that read it
-        e = blkno >= 2 ? cudaStreamWaitEvent(c->side, c->ev_free[slot], 0) : cudaSuccess;
+        cudaStream_t gs = c->serial ? st : c->side;
+        e = (blkno >= 2 && !c->serial) ? cudaStreamWaitEvent(gs, c->ev_free[slot], 0) : cudaSuccess;
         if (e == cudaSuccess) {
-            PhaseScope ps(c, HAP_PHASE_PERMGEN, 1, c->side);
-            e = launch_perm(pa, c->sm_count, c->side);
+            PhaseScope ps(c, HAP_PHASE_PERMGEN, 1, gs);
+            e = launch_perm(pa, c->sm_count, gs);
         }
-        if (e == cudaSuccess) e = cudaEventRecord(c->ev_ready[slot], c->side);
+        if (e == cudaSuccess) e = cudaEventRecord(c->ev_ready[slot], gs);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(st, c->ev_ready[slot], 0);  // join
         if (e != cudaSuccess) return cuda_fail(c, e, "perm generator");
         g.count = (int)cnt;
@@ -492,6 +497,7 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
 hap_status hap_profile(hap_ctx c, int enable) {
     if (!c) return HAP_E_INVALID_ARG;
     c->prof = enable != 0;
+    c->serial = enable >= 2;
     return HAP_OK;
 }
 

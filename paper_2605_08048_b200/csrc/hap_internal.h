@@ -26,6 +26,8 @@ struct AlignArgs {
     int mode;                // hap_align_mode
     hap_align_info* info;    // device
     double* nrm;             // [N]    row norms ||h_i||
+    double* inv;             // [N]    1/||h_i|| (0 for a zero row)
+    double* u;               // [d_pad] Householder axis (0 for the identity)
     double* coef;            // [n_x]  2 u^T x_i (0 for the identity)
     double* part;            // [nblk_x + nblk_y][d] fp64 column partials
     double* xbar;            // [d]

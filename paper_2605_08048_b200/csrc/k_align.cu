@@ -91,6 +91,7 @@ __global__ void __launch_bounds__(256) k1a_norm_colsum(AlignArgs a, int nblk_x) 
         if (l == 0) {
             const double nrm = sqrt(s);
             a.nrm[base + r] = nrm;
+            a.inv[base + r] = nrm < 1e-12 ? 0.0 : 1.0 / nrm;
             if (nrm < 1e-12) atomicMin(reinterpret_cast<long long*>(a.scratch), (long long)(base + r));
             s_inv[r] = nrm < 1e-12 ? 0.0 : 1.0 / nrm;
         }
@@ -127,20 +128,25 @@ __global__ void __launch_bounds__(256) k1a_norm_colsum(AlignArgs a, int nblk_x) 
 // (ascending block order), per-CTA partial sums of ||xbar||^2, ||ybar||^2.  The last CTA
 // to finish (atomic ticket) finalises the scalars in fixed order: norms, DegenerateMean,
 // v = mu_x - mu_y (||v|| and v.xbar summed directly), identity test, r, L, T_obs, info.
-__global__ void __launch_bounds__(256) k1b_means(AlignArgs a, int nblk_x, int nblk_y) {
+constexpr int kMeanCols = 64;
+__global__ void __launch_bounds__(kMeanCols) k1b_means(AlignArgs a, int nblk_x, int nblk_y) {
     __shared__ double red[33];
     __shared__ int s_last;
     double sxx = 0.0, syy = 0.0;
-    for (int64_t c = (int64_t)blockIdx.x * 256 + threadIdx.x; c < a.d && threadIdx.x < 256;
-         c += (int64_t)gridDim.x * 256) {
+    const int64_t c = (int64_t)blockIdx.x * kMeanCols + threadIdx.x;
+    if (c < a.d) {
         double xs = 0.0, ys = 0.0;
-        for (int b = 0; b < nblk_x; ++b) xs += a.part[(int64_t)b * a.d + c];
-        for (int b = 0; b < nblk_y; ++b) ys += a.part[(int64_t)(nblk_x + b) * a.d + c];
+        const double* px = a.part + c;
+#pragma unroll 8
+        for (int b = 0; b < nblk_x; ++b) xs += __ldcg(px + (int64_t)b * a.d);
+        const double* py = a.part + (int64_t)nblk_x * a.d + c;
+#pragma unroll 8
+        for (int b = 0; b < nblk_y; ++b) ys += __ldcg(py + (int64_t)b * a.d);
         const double xb = xs / (double)a.n_x, yb = ys / (double)a.n_y;
         a.xbar[c] = xb;
         a.ybar[c] = yb;
-        sxx += xb * xb;
-        syy += yb * yb;
+        sxx = xb * xb;
+        syy = yb * yb;
     }
     sxx = block_sum(sxx, red);
     syy = block_sum(syy, red);
@@ -154,7 +160,7 @@ __global__ void __launch_bounds__(256) k1b_means(AlignArgs a, int nblk_x, int nb
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    // ---- last CTA: scalars
+    // ---- last CTA: scalars (fixed order), then u (S3)
     double SX = 0.0, SY = 0.0;
     for (int b = 0; b < (int)gridDim.x; ++b) {
         SX += __ldcg(a.spart + 2 * b);
@@ -166,8 +172,8 @@ __global__ void __launch_bounds__(256) k1b_means(AlignArgs a, int nblk_x, int nb
     double nv = 0.0, vx = 0.0;
     if (!identity) {
         double sv = 0.0, svx = 0.0;
-        for (int64_t c = threadIdx.x; c < a.d; c += blockDim.x) {
-            const double xb = __ldcg(a.xbar + c), yb = __ldcg(a.ybar + c);
+        for (int64_t cc = threadIdx.x; cc < a.d; cc += blockDim.x) {
+            const double xb = __ldcg(a.xbar + cc), yb = __ldcg(a.ybar + cc);
             const double v = xb / nx - yb / ny;
             sv += v * v;
             svx += v * xb;
@@ -176,12 +182,26 @@ __global__ void __launch_bounds__(256) k1b_means(AlignArgs a, int nblk_x, int nb
         vx = block_sum(svx, red);
         identity = nv < 1e-9;  // coincident mean directions (R3)
     }
+    const double ux = identity ? 0.0 : vx / nv;  // u . xbar
+    const double dN = (double)(a.n_x + a.n_y);
+    for (int64_t cc = threadIdx.x; cc < a.d_pad; cc += blockDim.x) {
+        double u = 0.0, m = 0.0;
+        if (cc < a.d) {
+            const double xb = __ldcg(a.xbar + cc), yb = __ldcg(a.ybar + cc);
+            u = identity ? 0.0 : (xb / nx - yb / ny) / nv;
+            // centre m = t/N quantised to 2^-12 with t = n_x (xbar - 2u(u.xbar)) + n_y ybar
+            const double t = (double)a.n_x * (xb - 2.0 * u * ux) + (double)a.n_y * yb;
+            m = rint(t / dN * 4096.0) / 4096.0;
+        }
+        a.u[cc] = u;
+        a.m[cc] = m;
+    }
     if (threadIdx.x == 0) {
         double* sc = a.scal;
         sc[0] = nx;
         sc[1] = ny;
         sc[2] = identity ? 0.0 : nv;
-        sc[3] = identity ? 0.0 : vx / nv;  // u . xbar
+        sc[3] = ux;
         sc[4] = identity ? 1.0 : 0.0;
         hap_align_info* f = a.info;
         const long long bad = *reinterpret_cast<volatile long long*>(a.scratch);
@@ -210,12 +230,6 @@ __global__ void __launch_bounds__(256) k1b_means(AlignArgs a, int nblk_x, int nb
     }
 }
 
-__device__ __forceinline__ double axis_c(const AlignArgs& a, int64_t c) {  // u_c
-    const double nv = a.scal[2];
-    if (nv == 0.0 || c >= a.d) return 0.0;
-    return (a.xbar[c] / a.scal[0] - a.ybar[c] / a.scal[1]) / nv;
-}
-
 // ---------------------------------------------------------------------------------
 // K1c (S4 coefficient): warp per X row, coef_i = 2 u^T x_i = 2 (u^T h_i)/||h_i||.
 __global__ void __launch_bounds__(256) k1c_rowdot(AlignArgs a) {
@@ -226,13 +240,22 @@ __global__ void __launch_bounds__(256) k1c_rowdot(AlignArgs a) {
         if (l == 0) a.coef[i] = 0.0;
         return;
     }
-    const double nx = a.scal[0], ny = a.scal[1], nv = a.scal[2];
     const float* h = a.X + i * a.d;
     double s = 0.0;
-    for (int64_t c = l; c < a.d; c += 32)
-        s += (double)__ldg(h + c) * (__ldg(a.xbar + c) / nx - __ldg(a.ybar + c) / ny);
+    if ((a.d & 3) == 0) {
+        const float4* h4 = reinterpret_cast<const float4*>(h);
+        const double2* u2 = reinterpret_cast<const double2*>(a.u);
+#pragma unroll 2
+        for (int64_t c = l; c < a.d / 4; c += 32) {
+            const float4 v = __ldg(h4 + c);
+            const double2 u0 = __ldg(u2 + 2 * c), u1 = __ldg(u2 + 2 * c + 1);
+            s += (double)v.x * u0.x + (double)v.y * u0.y + (double)v.z * u1.x + (double)v.w * u1.y;
+        }
+    } else {
+        for (int64_t c = l; c < a.d; c += 32) s += (double)__ldg(h + c) * __ldg(a.u + c);
+    }
     s = warp_sum(s);
-    if (l == 0) a.coef[i] = a.nrm[i] > 0.0 ? 2.0 * (s / nv) / a.nrm[i] : 0.0;
+    if (l == 0) a.coef[i] = 2.0 * s * a.inv[i];
 }
 
 // ---------------------------------------------------------------------------------
@@ -252,23 +275,17 @@ __global__ void __launch_bounds__(256) k1d_reflect_split(AlignArgs a) {
     uint16_t* sh16 = reinterpret_cast<uint16_t*>(s_hi);
     uint16_t* sl16 = reinterpret_cast<uint16_t*>(s_lo);
     const int64_t c = c0 + tc;
-    const double uc = axis_c(a, c);
-    double mc = 0.0;
-    if (c < a.d) {
-        const double t = (double)a.n_x * (a.xbar[c] - 2.0 * uc * a.scal[3]) + (double)a.n_y * a.ybar[c];
-        mc = rint(t / (double)N * 4096.0) / 4096.0;
-    }
-    if (blockIdx.x == 0 && tr == 0 && c < a.d_pad) a.m[c] = mc;
+    const double uc = c < a.d_pad ? a.u[c] : 0.0;
+    const double mc = c < a.d_pad ? a.m[c] : 0.0;
 #pragma unroll 4
     for (int j = 0; j < 16; ++j) {
         const int rl = tr + 4 * j;
         const int64_t i = r0 + rl;
         double z = 0.0;
         if (i < N && c < a.d) {
-            const double nrm = a.nrm[i];
-            const double h = (double)row_ptr(a, i)[c];
+            const double h = (double)__ldg(row_ptr(a, i) + c);
             const double cf = i < a.n_x ? a.coef[i] : 0.0;
-            z = (nrm > 0.0 ? h / nrm : 0.0) - cf * uc - mc;
+            z = h * a.inv[i] - cf * uc - mc;
         }
         const __nv_bfloat16 hi = __double2bfloat16(z);
         const __nv_bfloat16 lo = __double2bfloat16(z - (double)__bfloat162float(hi));
@@ -300,14 +317,15 @@ __global__ void __launch_bounds__(256) k1d_reflect_split(AlignArgs a) {
 // partials (ascending); t = N m + t'.  With a = n_x m and b = t - a = n_y m + t' (fp32),
 // the GEMM epilogue forms S1 = SA + sum acc (acc + 2a), S2 = SB + sum acc (acc - 2b) with
 // SA = sum a^2, SB = sum b^2 (fp64; last CTA sums the per-CTA partials in fixed order).
-__global__ void __launch_bounds__(256) k1e_tfinal(AlignArgs a, int ntiles) {
+__global__ void __launch_bounds__(kMeanCols) k1e_tfinal(AlignArgs a, int ntiles) {
     __shared__ double red[33];
     __shared__ int s_last;
     double sa = 0.0, sb = 0.0;
-    const int64_t c = (int64_t)blockIdx.x * 256 + threadIdx.x;
+    const int64_t c = (int64_t)blockIdx.x * kMeanCols + threadIdx.x;
     if (c < a.d_pad) {
         double tp = 0.0;
-        for (int t = 0; t < ntiles; ++t) tp += a.tpart[(int64_t)t * a.d_pad + c];
+#pragma unroll 8
+        for (int t = 0; t < ntiles; ++t) tp += __ldcg(a.tpart + (int64_t)t * a.d_pad + c);
         const double m = a.m[c];
         a.t64[c] = (double)(a.n_x + a.n_y) * m + tp;
         const float af = (float)((double)a.n_x * m);
@@ -344,12 +362,12 @@ cudaError_t launch_align(const AlignArgs& a, cudaStream_t st) {
     const int64_t N = a.n_x + a.n_y;
     const int nbx = (int)ceil_div(a.n_x, kRowBlock), nby = (int)ceil_div(a.n_y, kRowBlock);
     k1a_norm_colsum<<<nbx + nby, 256, 0, st>>>(a, nbx);
-    k1b_means<<<(unsigned)ceil_div(a.d, 256), 256, 0, st>>>(a, nbx, nby);
+    k1b_means<<<(unsigned)ceil_div(a.d, kMeanCols), kMeanCols, 0, st>>>(a, nbx, nby);
     k1c_rowdot<<<(unsigned)ceil_div(a.n_x * 32, 256), 256, 0, st>>>(a);
     const int ntiles = (int)(a.n_pad / kRowTile);
     dim3 grid((unsigned)ntiles, (unsigned)ceil_div(a.d_pad, 64));
     k1d_reflect_split<<<grid, 256, 0, st>>>(a);
-    k1e_tfinal<<<(unsigned)ceil_div(a.d_pad, 256), 256, 0, st>>>(a, ntiles);
+    k1e_tfinal<<<(unsigned)ceil_div(a.d_pad, kMeanCols), kMeanCols, 0, st>>>(a, ntiles);
     (void)N;
     return cudaGetLastError();
 }
