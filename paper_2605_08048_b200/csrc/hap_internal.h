@@ -12,7 +12,7 @@ namespace hap {
 constexpr int kKBlock = 64;     // GEMM K-block: 64 bf16 = one 128-byte swizzle atom
 constexpr int kTileM = 128;     // permutations per CTA tile (TMEM lanes)
 constexpr int kChunkN = 256;    // d-columns per accumulator chunk (UMMA N <= 256)
-constexpr int kRowBlock = 32;   // rows per column-partial block in K1b
+constexpr int kRowBlock = 16;   // rows per column-partial block in K1a
 constexpr int kRowTile = 64;    // pooled rows per reflect/split tile in K1d
 
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }

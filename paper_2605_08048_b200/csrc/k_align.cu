@@ -128,20 +128,36 @@ __global__ void __launch_bounds__(256) k1a_norm_colsum(AlignArgs a, int nblk_x) 
 // (ascending block order), per-CTA partial sums of ||xbar||^2, ||ybar||^2.  The last CTA
 // to finish (atomic ticket) finalises the scalars in fixed order: norms, DegenerateMean,
 // v = mu_x - mu_y (||v|| and v.xbar summed directly), identity test, r, L, T_obs, info.
-constexpr int kMeanCols = 64;
-__global__ void __launch_bounds__(kMeanCols) k1b_means(AlignArgs a, int nblk_x, int nblk_y) {
+constexpr int kMeanCols = 64;   // columns per CTA in K1b / K1e
+constexpr int kMeanGroups = 4;  // threads per column, each summing a contiguous block range
+__device__ __forceinline__ double grouped_colsum(const double* base, int64_t stride, int nblk,
+                                                int g, double* s_grp, int col) {
+    // fixed order: group g sums blocks [g*q, (g+1)*q) ascending; groups combined 0..3
+    const int q = (nblk + kMeanGroups - 1) / kMeanGroups;
+    const int b0 = g * q, b1 = min(nblk, b0 + q);
+    double acc = 0.0;
+#pragma unroll 8
+    for (int b = b0; b < b1; ++b) acc += __ldcg(base + (int64_t)b * stride);
+    s_grp[g * kMeanCols + col] = acc;
+    __syncthreads();
+    double tot = 0.0;
+#pragma unroll
+    for (int gg = 0; gg < kMeanGroups; ++gg) tot += s_grp[gg * kMeanCols + col];
+    __syncthreads();
+    return tot;
+}
+
+__global__ void __launch_bounds__(kMeanCols * kMeanGroups) k1b_means(AlignArgs a, int nblk_x, int nblk_y) {
     __shared__ double red[33];
+    __shared__ double s_grp[kMeanGroups * kMeanCols];
     __shared__ int s_last;
+    const int col = threadIdx.x % kMeanCols, g = threadIdx.x / kMeanCols;
+    const int64_t c = (int64_t)blockIdx.x * kMeanCols + col;
+    const int64_t cc0 = c < a.d ? c : 0;
+    const double xs = grouped_colsum(a.part + cc0, a.d, nblk_x, g, s_grp, col);
+    const double ys = grouped_colsum(a.part + (int64_t)nblk_x * a.d + cc0, a.d, nblk_y, g, s_grp, col);
     double sxx = 0.0, syy = 0.0;
-    const int64_t c = (int64_t)blockIdx.x * kMeanCols + threadIdx.x;
-    if (c < a.d) {
-        double xs = 0.0, ys = 0.0;
-        const double* px = a.part + c;
-#pragma unroll 8
-        for (int b = 0; b < nblk_x; ++b) xs += __ldcg(px + (int64_t)b * a.d);
-        const double* py = a.part + (int64_t)nblk_x * a.d + c;
-#pragma unroll 8
-        for (int b = 0; b < nblk_y; ++b) ys += __ldcg(py + (int64_t)b * a.d);
+    if (c < a.d && g == 0) {
         const double xb = xs / (double)a.n_x, yb = ys / (double)a.n_y;
         a.xbar[c] = xb;
         a.ybar[c] = yb;
@@ -162,19 +178,22 @@ __global__ void __launch_bounds__(kMeanCols) k1b_means(AlignArgs a, int nblk_x, 
     __threadfence();
     // ---- last CTA: scalars (fixed order), then u (S3)
     double SX = 0.0, SY = 0.0;
-    for (int b = 0; b < (int)gridDim.x; ++b) {
-        SX += __ldcg(a.spart + 2 * b);
-        SY += __ldcg(a.spart + 2 * b + 1);
+    if (threadIdx.x < gridDim.x) {
+        SX = __ldcg(a.spart + 2 * threadIdx.x);
+        SY = __ldcg(a.spart + 2 * threadIdx.x + 1);
     }
+    SX = block_sum(SX, red);
+    SY = block_sum(SY, red);
     const double nx = sqrt(SX), ny = sqrt(SY);
     const bool degenerate = nx < 1e-12 || ny < 1e-12;
     bool identity = (a.mode == HAP_ALIGN_NONE) || degenerate;
     double nv = 0.0, vx = 0.0;
+    const double rnx = degenerate ? 0.0 : 1.0 / nx, rny = degenerate ? 0.0 : 1.0 / ny;
     if (!identity) {
         double sv = 0.0, svx = 0.0;
         for (int64_t cc = threadIdx.x; cc < a.d; cc += blockDim.x) {
             const double xb = __ldcg(a.xbar + cc), yb = __ldcg(a.ybar + cc);
-            const double v = xb / nx - yb / ny;
+            const double v = xb * rnx - yb * rny;
             sv += v * v;
             svx += v * xb;
         }
@@ -182,16 +201,17 @@ __global__ void __launch_bounds__(kMeanCols) k1b_means(AlignArgs a, int nblk_x, 
         vx = block_sum(svx, red);
         identity = nv < 1e-9;  // coincident mean directions (R3)
     }
-    const double ux = identity ? 0.0 : vx / nv;  // u . xbar
-    const double dN = (double)(a.n_x + a.n_y);
+    const double rnv = identity ? 0.0 : 1.0 / nv;
+    const double ux = vx * rnv;  // u . xbar
+    const double rN = 4096.0 / (double)(a.n_x + a.n_y);
     for (int64_t cc = threadIdx.x; cc < a.d_pad; cc += blockDim.x) {
         double u = 0.0, m = 0.0;
         if (cc < a.d) {
             const double xb = __ldcg(a.xbar + cc), yb = __ldcg(a.ybar + cc);
-            u = identity ? 0.0 : (xb / nx - yb / ny) / nv;
+            u = (xb * rnx - yb * rny) * rnv;
             // centre m = t/N quantised to 2^-12 with t = n_x (xbar - 2u(u.xbar)) + n_y ybar
             const double t = (double)a.n_x * (xb - 2.0 * u * ux) + (double)a.n_y * yb;
-            m = rint(t / dN * 4096.0) / 4096.0;
+            m = rint(t * rN) * (1.0 / 4096.0);
         }
         a.u[cc] = u;
         a.m[cc] = m;
@@ -275,20 +295,21 @@ __global__ void __launch_bounds__(256) k1d_reflect_split(AlignArgs a) {
     uint16_t* sh16 = reinterpret_cast<uint16_t*>(s_hi);
     uint16_t* sl16 = reinterpret_cast<uint16_t*>(s_lo);
     const int64_t c = c0 + tc;
-    const double uc = c < a.d_pad ? a.u[c] : 0.0;
-    const double mc = c < a.d_pad ? a.m[c] : 0.0;
+    // fp32 is ample here: the value is then represented with 16 mantissa bits (hi + lo)
+    const float uc = c < a.d_pad ? (float)a.u[c] : 0.f;
+    const float mc = c < a.d_pad ? (float)a.m[c] : 0.f;
 #pragma unroll 4
     for (int j = 0; j < 16; ++j) {
         const int rl = tr + 4 * j;
         const int64_t i = r0 + rl;
-        double z = 0.0;
+        float z = 0.f;
         if (i < N && c < a.d) {
-            const double h = (double)__ldg(row_ptr(a, i) + c);
-            const double cf = i < a.n_x ? a.coef[i] : 0.0;
-            z = h * a.inv[i] - cf * uc - mc;
+            const float h = __ldg(row_ptr(a, i) + c);
+            const float cf = i < a.n_x ? (float)a.coef[i] : 0.f;
+            z = fmaf(-cf, uc, h * (float)a.inv[i]) - mc;
         }
-        const __nv_bfloat16 hi = __double2bfloat16(z);
-        const __nv_bfloat16 lo = __double2bfloat16(z - (double)__bfloat162float(hi));
+        const __nv_bfloat16 hi = __float2bfloat16_rn(z);
+        const __nv_bfloat16 lo = __float2bfloat16_rn(z - __bfloat162float(hi));
         sh16[tc * (2 * kSP) + rl] = __bfloat16_as_ushort(hi);
         sl16[tc * (2 * kSP) + rl] = __bfloat16_as_ushort(lo);
     }
@@ -317,15 +338,15 @@ __global__ void __launch_bounds__(256) k1d_reflect_split(AlignArgs a) {
 // partials (ascending); t = N m + t'.  With a = n_x m and b = t - a = n_y m + t' (fp32),
 // the GEMM epilogue forms S1 = SA + sum acc (acc + 2a), S2 = SB + sum acc (acc - 2b) with
 // SA = sum a^2, SB = sum b^2 (fp64; last CTA sums the per-CTA partials in fixed order).
-__global__ void __launch_bounds__(kMeanCols) k1e_tfinal(AlignArgs a, int ntiles) {
+__global__ void __launch_bounds__(kMeanCols * kMeanGroups) k1e_tfinal(AlignArgs a, int ntiles) {
     __shared__ double red[33];
+    __shared__ double s_grp[kMeanGroups * kMeanCols];
     __shared__ int s_last;
+    const int col = threadIdx.x % kMeanCols, g = threadIdx.x / kMeanCols;
+    const int64_t c = (int64_t)blockIdx.x * kMeanCols + col;
+    const double tp = grouped_colsum(a.tpart + (c < a.d_pad ? c : 0), a.d_pad, ntiles, g, s_grp, col);
     double sa = 0.0, sb = 0.0;
-    const int64_t c = (int64_t)blockIdx.x * kMeanCols + threadIdx.x;
-    if (c < a.d_pad) {
-        double tp = 0.0;
-#pragma unroll 8
-        for (int t = 0; t < ntiles; ++t) tp += __ldcg(a.tpart + (int64_t)t * a.d_pad + c);
+    if (c < a.d_pad && g == 0) {
         const double m = a.m[c];
         a.t64[c] = (double)(a.n_x + a.n_y) * m + tp;
         const float af = (float)((double)a.n_x * m);
@@ -344,16 +365,20 @@ __global__ void __launch_bounds__(kMeanCols) k1e_tfinal(AlignArgs a, int ntiles)
         s_last = (t == gridDim.x - 1);
     }
     __syncthreads();
-    if (!s_last || threadIdx.x != 0) return;
+    if (!s_last) return;
     __threadfence();
     double SA = 0.0, SB = 0.0;
-    for (int b = 0; b < (int)gridDim.x; ++b) {
-        SA += __ldcg(a.spart + 2 * b);
-        SB += __ldcg(a.spart + 2 * b + 1);
+    if (threadIdx.x < gridDim.x) {
+        SA = __ldcg(a.spart + 2 * threadIdx.x);
+        SB = __ldcg(a.spart + 2 * threadIdx.x + 1);
     }
-    a.sconst[0] = SA;
-    a.sconst[1] = SB;
-    reinterpret_cast<unsigned*>(a.scratch + 1)[1] = 0u;
+    SA = block_sum(SA, red);
+    SB = block_sum(SB, red);
+    if (threadIdx.x == 0) {
+        a.sconst[0] = SA;
+        a.sconst[1] = SB;
+        reinterpret_cast<unsigned*>(a.scratch + 1)[1] = 0u;
+    }
 }
 
 }  // namespace
@@ -362,12 +387,12 @@ cudaError_t launch_align(const AlignArgs& a, cudaStream_t st) {
     const int64_t N = a.n_x + a.n_y;
     const int nbx = (int)ceil_div(a.n_x, kRowBlock), nby = (int)ceil_div(a.n_y, kRowBlock);
     k1a_norm_colsum<<<nbx + nby, 256, 0, st>>>(a, nbx);
-    k1b_means<<<(unsigned)ceil_div(a.d, kMeanCols), kMeanCols, 0, st>>>(a, nbx, nby);
+    k1b_means<<<(unsigned)ceil_div(a.d, kMeanCols), kMeanCols * kMeanGroups, 0, st>>>(a, nbx, nby);
     k1c_rowdot<<<(unsigned)ceil_div(a.n_x * 32, 256), 256, 0, st>>>(a);
     const int ntiles = (int)(a.n_pad / kRowTile);
     dim3 grid((unsigned)ntiles, (unsigned)ceil_div(a.d_pad, 64));
     k1d_reflect_split<<<grid, 256, 0, st>>>(a);
-    k1e_tfinal<<<(unsigned)ceil_div(a.d_pad, kMeanCols), kMeanCols, 0, st>>>(a, ntiles);
+    k1e_tfinal<<<(unsigned)ceil_div(a.d_pad, kMeanCols), kMeanCols * kMeanGroups, 0, st>>>(a, ntiles);
     (void)N;
     return cudaGetLastError();
 }

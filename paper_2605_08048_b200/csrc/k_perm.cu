@@ -92,37 +92,56 @@ __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy(PermArgs a, int lt
                     make_uint2(j[0] | (j[1] << 16), j[2] | (j[3] << 16));
             }
             __syncwarp();
+            // scatter in 4 rounds of 32 consecutive steps (round r has larger k than r-1,
+            // so rounds resolve in step order); a collision inside a round is fixed below
+            uint32_t jr[4];
+            bool wr[4];
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
-                const uint32_t idx = 32u * r + l, k = k0 + idx;
-                const uint32_t j = k < nx ? stage[idx] : 0u;
-                // self-targets never move a value and are not "writers" (k != q in LT)
-                const bool writes = k < nx && j != k;
-                // last writer (largest k = highest lane) of each target wins
-                const uint32_t peers = __match_any_sync(0xffffffffu, writes ? j : 0x10000u + l);
-                if (writes && (31 - __clz(peers)) == l) LT[j] = (uint16_t)(k + 1);
-                __syncwarp();  // order this round's stores before the next (larger k) round
+                const uint32_t k = k0 + 32u * r + l;
+                jr[r] = k < nx ? stage[32 * r + l] : 0u;
+                wr[r] = k < nx && jr[r] != k;  // self-targets never move a value (k != q)
+                if (wr[r]) LT[jr[r]] = (uint16_t)(k + 1);
+                __syncwarp();
+            }
+            // last writer (largest k) must win: a step that lost a same-round collision to
+            // a smaller k rewrites; repeat until no step is short-changed (rarely > 1 pass)
+            bool lost = false;
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const uint32_t k = k0 + 32u * r + l;
+                if (wr[r] && LT[jr[r]] < k + 1) lost = true;
+            }
+            while (__any_sync(0xffffffffu, lost)) {
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const uint32_t k = k0 + 32u * r + l;
+                    if (lost && wr[r] && LT[jr[r]] < k + 1) LT[jr[r]] = (uint16_t)(k + 1);
+                    __syncwarp();
+                }
+                lost = false;
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const uint32_t k = k0 + 32u * r + l;
+                    if (wr[r] && LT[jr[r]] < k + 1) lost = true;
+                }
             }
         }
         // ---- phase B: each written high position exiles the end of its chain; lanes
         // walk chains one step per iteration and pick up new positions when free
         {
             uint32_t p = nx + l;
-            int kk = -1;
-            while (__any_sync(0xffffffffu, p < N || kk >= 0)) {
-                if (kk >= 0) {
-                    const uint16_t t = LT[kk];
-                    if (t != 0 && t != kExiled) {
-                        kk = (int)t - 1;
-                    } else {
-                        LT[kk] = kExiled;
-                        kk = -1;
-                    }
-                } else if (p < N) {
-                    const uint16_t v = LT[p];
-                    p += 32;
-                    if (v) kk = (int)v - 1;
-                }
+            uint32_t kk = 0xFFFFFFFFu;  // current chain node, or none
+            for (;;) {
+                const bool in_chain = kk != 0xFFFFFFFFu;
+                const bool scanning = !in_chain && p < N;
+                if (!__any_sync(0xffffffffu, in_chain || scanning)) break;
+                const uint32_t addr = in_chain ? kk : (scanning ? p : 0u);
+                const uint32_t t = LT[addr];
+                const bool end = in_chain && (t == 0u || t == kExiled);
+                if (end) LT[kk] = kExiled;
+                p += scanning ? 32u : 0u;
+                kk = end ? 0xFFFFFFFFu : ((in_chain || (scanning && t != 0u)) ? t - 1u : kk);
             }
         }
         __syncwarp();

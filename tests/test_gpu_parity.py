@@ -128,7 +128,8 @@ def test_pooled_planes(hap, ctx, orc, n_x, n_y, d, mode):
     assert np.allclose(mm[:d], ref.Z.sum(0) / N, atol=2.0 ** -13 + 1e-9)
     zc = hi[:N, :d] + lo[:N, :d]
     want = ref.Z - mm[None, :d]
-    assert np.all(np.abs(zc - want) <= 2.0 ** -16 * np.abs(want) + 1e-12)
+    # bf16 hi+lo keeps 16 mantissa bits of z - m, computed in fp32 (abs. error < 2^-22)
+    assert np.all(np.abs(zc - want) <= 2.0 ** -16 * np.abs(want) + 2.0 ** -22)
     assert np.all(hi[N:] == 0) and np.all(lo[N:] == 0)
     assert np.all(hi[:, d:] == 0) and np.all(lo[:, d:] == 0)
     tt = t.cpu().numpy()
