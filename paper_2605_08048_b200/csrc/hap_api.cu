@@ -32,11 +32,12 @@ struct hap_ctx_s {
     const void* tm_key[4] = {};
     int64_t tm_shape[5] = {};
     // ---- generator side stream: K2 only depends on (seed, s, b, N, n_x), so it runs on
-    // `side`, forked from the caller's stream before K1, and joins back before K3
+    // `side` with no dependency on the caller's stream except the mask-GEMM that last read
+    // the mask slot it overwrites; K3 joins it with an event wait
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_ready[2] = {}, ev_free[2] = {};
-    bool forked = false;
     int slot = 0;
+    bool used[2] = {false, false};
     // ---- profiling
     bool prof = false;
     bool serial = false;  // profiling level 2: generator on the caller's stream
@@ -375,11 +376,7 @@ hap_status hap_align(hap_ctx c, const float* X, int64_t n_x, const float* Y, int
     a.m = B<double>(c, kM);
     a.ab = B<float2>(c, kAB);
     a.sconst = B<double>(c, kSconst);
-    // fork the generator stream here: K2 of the coming hap_permtest may run during K1
-    cudaError_t e = cudaEventRecord(c->ev_fork, st);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(c->side, c->ev_fork, 0);
-    if (e != cudaSuccess) return cuda_fail(c, e, "fork");
-    c->forked = true;
+    cudaError_t e;
     {
         PhaseScope ps(c, HAP_PHASE_ALIGN, kAlignLaunches, st);
         e = launch_align(a, st);
@@ -421,20 +418,18 @@ hap_status hap_permtest(hap_ctx c, hap_align_info* info, const hap_perm_cfg* cfg
         return s;
     if ((s = refresh_maps(c, pair))) return s;
     cudaError_t e;
-    if (!c->forked) {  // no hap_align since the last permtest: fork after all prior work
-        e = cudaEventRecord(c->ev_fork, st);
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(c->side, c->ev_fork, 0);
-        if (e != cudaSuccess) return cuda_fail(c, e, "fork");
-    }
-    c->forked = false;
     GemmArgs g = gemm_args(c, info);
     g.counts = counts;
     g.rows_per_tile = (int)R;
     g.tie_rel = cfg->tie_rel > 0 ? cfg->tie_rel : 1e-6;
-    for (int64_t off = 0, blkno = 0; off < total; off += blk, ++blkno) {
+    for (int64_t off = 0; off < total; off += blk) {
         const int64_t cnt = std::min<int64_t>(blk, total - off);
         const int64_t nt = ceil_div(cnt, R - 1);
-        const int slot = (int)(blkno & 1);
+        // mask slots alternate over all launches of the context: the generator of this
+        // block only waits for the mask-GEMM that last read its slot, so it can run
+        // concurrently with the previous block's (or previous test's) mask-GEMM and K1
+        const int slot = c->slot;
+        c->slot ^= 1;
         PermArgs pa{};
         pa.seed = cfg->seed;
         pa.s = cfg->stream_id;
@@ -447,9 +442,10 @@ hap_status hap_permtest(hap_ctx c, hap_align_info* info, const hap_perm_cfg* cfg
         pa.out_kind = kMaskBf16Row;
         pa.rows_per_tile = (int)R;
         pa.ntiles = (int)nt;
+        pa.max_ctas_per_sm = 4;
         // K2 on the side stream; a slot is rewritten only after the K3 that read it
         cudaStream_t gs = c->serial ? st : c->side;
-        e = (blkno >= 2 && !c->serial) ? cudaStreamWaitEvent(gs, c->ev_free[slot], 0) : cudaSuccess;
+        e = (c->used[slot] && !c->serial) ? cudaStreamWaitEvent(gs, c->ev_free[slot], 0) : cudaSuccess;
         if (e == cudaSuccess) {
             PhaseScope ps(c, HAP_PHASE_PERMGEN, 1, gs);
             e = launch_perm(pa, c->sm_count, gs);
@@ -466,6 +462,7 @@ hap_status hap_permtest(hap_ctx c, hap_align_info* info, const hap_perm_cfg* cfg
         }
         if (e == cudaSuccess) e = cudaEventRecord(c->ev_free[slot], st);
         if (e != cudaSuccess) return cuda_fail(c, e, "mask-GEMM");
+        c->used[slot] = true;
     }
     c->last_stream = st;
     return HAP_OK;

@@ -59,6 +59,7 @@ struct PermArgs {
     int rows_per_tile;       // bf16 mode: R; perm p -> row (p/(R-1))*R + 1 + p%(R-1),
                              // row t*R = observed split {0..n_x-1} for t < ntiles
     int ntiles;
+    int max_ctas_per_sm;     // 0 = occupancy limit
 };
 cudaError_t launch_perm(const PermArgs& a, int sm_count, cudaStream_t st);
 

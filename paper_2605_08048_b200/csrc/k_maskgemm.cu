@@ -20,7 +20,7 @@
 //
 // kPair = 2 (default): a 2-CTA cluster runs tcgen05.mma.cta_group::2 with M = 256: each CTA
 // holds 128 mask rows (A) and half of the chunk's columns (B), so each SM streams half of
-// the Z~ tile; 4-stage TMA ring of 48 KB.  kPair = 1: one CTA, M = 128, 2 stages of 80 KB.
+// the Z~ tile; 3-stage TMA ring of 48 KB (the rest of the SM's smem is left to K2).  kPair = 1: one CTA, M = 128, 2 stages of 80 KB.
 // Warps: 0 TMA producer, 1 MMA issuer (leader CTA) + TMEM owner, 2-5 epilogue (thread =
 // TMEM lane = one mask row).  The accumulator is double-buffered in TMEM (2 x 256 columns)
 // so unit i+1's MMAs overlap unit i's epilogue.  The last CTA to finish a unit of a tile
@@ -40,7 +40,8 @@ constexpr int kStageA = kTileM * 128;  // 16 KB: 128 rows x 64 bf16
 
 template <int kPair>
 struct Cfg {
-    static constexpr int kStages = kPair == 2 ? 4 : 2;
+    // 3 x 48 KB leaves room for the generator (K2) CTAs to co-reside on every SM
+    static constexpr int kStages = kPair == 2 ? 3 : 2;
     static constexpr int kBRows = kChunkN / kPair;   // B rows (d-columns) held per CTA
     static constexpr int kStageB = kBRows * 128;     // one plane
     static constexpr int kStageBytes = kStageA + 2 * kStageB;

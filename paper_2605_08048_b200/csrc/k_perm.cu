@@ -206,7 +206,9 @@ cudaError_t launch_perm(const PermArgs& a, int sm_count, cudaStream_t st) {
     }
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_perm_fy, nw * 32, smem);
-    if (per_sm < 1) per_sm = 1;
+    // at most 4 resident CTAs per SM: the generator for the next block runs beside the
+    // persistent mask-GEMM, which keeps one CTA per SM
+    per_sm = std::max(1, std::min(per_sm, a.max_ctas_per_sm > 0 ? a.max_ctas_per_sm : per_sm));
     const int64_t need = ceil_div(a.count + (a.out_kind == kMaskBf16Row ? a.ntiles : 0), nw);
     const int grid = (int)std::min<int64_t>(need, (int64_t)sm_count * per_sm);
     k2_perm_fy<<<grid, nw * 32, smem, st>>>(a, lt_pitch);
