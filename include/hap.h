@@ -174,6 +174,11 @@ HAP_API hap_status hap_profile(hap_ctx ctx, int enable);
  * is enabled).  reset != 0 clears both. */
 HAP_API hap_status hap_profile_read(hap_ctx ctx, double* ms, int64_t* launches, int reset);
 
+/* Timeline of the launches timed since the last read/reset (profiling on): out [host]
+ * max_n * 3 doubles {phase, start_us, end_us} relative to the first recorded launch, in
+ * record order; *n receives the count.  Consumes the records (like hap_profile_read). */
+HAP_API hap_status hap_profile_timeline(hap_ctx ctx, double* out, int64_t max_n, int64_t* n);
+
 /* ---- introspection for parity tests (same kernels as the hot path) -------------- */
 /* PERM-SPEC v1 sets for b in [b_begin, b_begin+count): out [device] count*N uint8
  * membership (1 = group 1), produced by the product's generator kernel. */

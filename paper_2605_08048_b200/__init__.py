@@ -87,6 +87,7 @@ def lib() -> ctypes.CDLL:
         "hap_export_pooled": ([vp, vp, vp, vp, vp, vp], i32),
         "hap_profile": ([vp, i32], i32),
         "hap_profile_read": ([vp, P(f64), P(i64), i32], i32),
+        "hap_profile_timeline": ([vp, P(f64), i64, P(i64)], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -213,6 +214,15 @@ def hap_profile_read(ctx, reset: bool = False):
     n = (ctypes.c_int64 * len(PHASES))()
     _check(ctx, lib().hap_profile_read(ctx, ms, n, 1 if reset else 0))
     return dict(zip(PHASES, list(ms))), dict(zip(PHASES, list(n)))
+
+
+def hap_profile_timeline(ctx, max_n: int = 100000):
+    """-> list of (phase_name, start_us, end_us) of the timed launches since the last read."""
+    buf = (ctypes.c_double * (3 * max_n))()
+    n = ctypes.c_int64()
+    _check(ctx, lib().hap_profile_timeline(ctx, buf, max_n, ctypes.byref(n)))
+    return [(PHASES[int(buf[3 * i])], buf[3 * i + 1], buf[3 * i + 2])
+            for i in range(min(n.value, max_n))]
 
 
 # ----------------------------------------------------------------- conveniences

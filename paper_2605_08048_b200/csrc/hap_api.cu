@@ -442,7 +442,7 @@ hap_status hap_permtest(hap_ctx c, hap_align_info* info, const hap_perm_cfg* cfg
         pa.out_kind = kMaskBf16Row;
         pa.rows_per_tile = (int)R;
         pa.ntiles = (int)nt;
-        pa.max_ctas_per_sm = 4;
+        pa.max_ctas_per_sm = 0;
         // K2 on the side stream; a slot is rewritten only after the K3 that read it
         cudaStream_t gs = c->serial ? st : c->side;
         e = (c->used[slot] && !c->serial) ? cudaStreamWaitEvent(gs, c->ev_free[slot], 0) : cudaSuccess;
@@ -519,6 +519,34 @@ hap_status hap_profile_read(hap_ctx c, double* ms, int64_t* launches, int reset)
             c->launches[p] = 0;
         }
     }
+    return HAP_OK;
+}
+
+hap_status hap_profile_timeline(hap_ctx c, double* out, int64_t max_n, int64_t* n) {
+    if (!c || !n) return HAP_E_INVALID_ARG;
+    cudaSetDevice(c->device);
+    int64_t k = 0;
+    cudaEvent_t t0 = c->marks.empty() ? nullptr : c->marks.front().a;
+    for (auto& m : c->marks) {
+        float ta = 0.f, tb = 0.f;
+        cudaError_t e = cudaEventSynchronize(m.b);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&ta, t0, m.a);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&tb, t0, m.b);
+        if (e != cudaSuccess) return cuda_fail(c, e, "profile timeline");
+        if (out && k < max_n) {
+            out[3 * k + 0] = m.phase;
+            out[3 * k + 1] = 1e3 * ta;
+            out[3 * k + 2] = 1e3 * tb;
+        }
+        ++k;
+        c->ms[m.phase] += tb - ta;
+    }
+    for (auto& m : c->marks) {
+        c->pool.push_back(m.a);
+        c->pool.push_back(m.b);
+    }
+    c->marks.clear();
+    *n = k;
     return HAP_OK;
 }
 

@@ -94,54 +94,51 @@ __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy(PermArgs a, int lt
             __syncwarp();
             // scatter in 4 rounds of 32 consecutive steps (round r has larger k than r-1,
             // so rounds resolve in step order); a collision inside a round is fixed below
-            uint32_t jr[4];
-            bool wr[4];
+            uint32_t jr[4], kr[4];
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
                 const uint32_t k = k0 + 32u * r + l;
-                jr[r] = k < nx ? stage[32 * r + l] : 0u;
-                wr[r] = k < nx && jr[r] != k;  // self-targets never move a value (k != q)
-                if (wr[r]) LT[jr[r]] = (uint16_t)(k + 1);
+                const uint32_t j = k < nx ? (uint32_t)stage[32 * r + l] : k;
+                // self-targets never move a value (k != q in LT); idle lanes act as such
+                jr[r] = j;
+                kr[r] = (j != k) ? k + 1u : 0u;  // value to store, 0 = no write
+                if (kr[r]) LT[j] = (uint16_t)kr[r];
                 __syncwarp();
             }
             // last writer (largest k) must win: a step that lost a same-round collision to
             // a smaller k rewrites; repeat until no step is short-changed (rarely > 1 pass)
-            bool lost = false;
+            for (;;) {
+                uint32_t lost = 0u;
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                const uint32_t k = k0 + 32u * r + l;
-                if (wr[r] && LT[jr[r]] < k + 1) lost = true;
-            }
-            while (__any_sync(0xffffffffu, lost)) {
+                for (int r = 0; r < 4; ++r) lost |= (uint32_t)(LT[jr[r]] < kr[r]) << r;
+                if (!__any_sync(0xffffffffu, lost)) break;
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
-                    const uint32_t k = k0 + 32u * r + l;
-                    if (lost && wr[r] && LT[jr[r]] < k + 1) LT[jr[r]] = (uint16_t)(k + 1);
+                    if ((lost >> r) & 1u) LT[jr[r]] = (uint16_t)kr[r];
                     __syncwarp();
-                }
-                lost = false;
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    const uint32_t k = k0 + 32u * r + l;
-                    if (wr[r] && LT[jr[r]] < k + 1) lost = true;
                 }
             }
         }
-        // ---- phase B: each written high position exiles the end of its chain; lanes
-        // walk chains one step per iteration and pick up new positions when free
+        // ---- phase B: each written high position exiles the end of its chain.  Per lane a
+        // two-state machine (scan the lane's high positions / walk a chain), one LDS per
+        // iteration, so lanes with short chains keep scanning while others walk.  In both
+        // states the step ends on t == 0 (unwritten position / chain end); high positions
+        // are never marked, chain nodes never exiled, so one test serves both states.
         {
-            uint32_t p = nx + l;
-            uint32_t kk = 0xFFFFFFFFu;  // current chain node, or none
-            for (;;) {
-                const bool in_chain = kk != 0xFFFFFFFFu;
-                const bool scanning = !in_chain && p < N;
-                if (!__any_sync(0xffffffffu, in_chain || scanning)) break;
-                const uint32_t addr = in_chain ? kk : (scanning ? p : 0u);
-                const uint32_t t = LT[addr];
-                const bool end = in_chain && (t == 0u || t == kExiled);
-                if (end) LT[kk] = kExiled;
-                p += scanning ? 32u : 0u;
-                kk = end ? 0xFFFFFFFFu : ((in_chain || (scanning && t != 0u)) ? t - 1u : kk);
+            const uint32_t Nm1 = N - 1u;
+            uint32_t pn = nx + l;          // next high position of this lane to scan
+            uint32_t cur = min(pn, Nm1);   // LT index read this iteration
+            uint32_t walking = 0u;
+            while (__any_sync(0xffffffffu, pn < N)) {
+#pragma unroll
+                for (int rep = 0; rep < 2; ++rep) {  // dead lanes only read (store is gated)
+                    const uint32_t t = LT[cur];
+                    const uint32_t stop = (t == 0u) | (t == (uint32_t)kExiled);
+                    if (walking & stop & (pn < N)) LT[cur] = kExiled;  // chain end: exiled
+                    pn += stop ? 32u : 0u;
+                    cur = stop ? min(pn, Nm1) : t - 1u;
+                    walking = stop ^ 1u;
+                }
             }
         }
         __syncwarp();
