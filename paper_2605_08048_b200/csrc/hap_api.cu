@@ -314,12 +314,12 @@ hap_status hap_align(hap_ctx c, const float* X, int64_t n_x, const float* Y, int
     const int64_t N = n_x + n_y;
     const int64_t n_pad = round_up(N, kKBlock);
     const int64_t d_pad = round_up(d, 32);
-    const int nbx = (int)ceil_div(n_x, kRowBlock), nby = (int)ceil_div(n_y, kRowBlock);
+    const int grid = c->sm_count;  // K1: one cooperative CTA per SM
     hap_status s;
     if ((s = ensure(c, kNrm, N * 8)) || (s = ensure(c, kCoef, N * 8)) ||
-        (s = ensure(c, kPart, (size_t)(nbx + nby) * d * 8)) || (s = ensure(c, kXbar, d * 8)) ||
+        (s = ensure(c, kPart, (size_t)2 * grid * d * 8)) || (s = ensure(c, kXbar, d * 8)) ||
         (s = ensure(c, kYbar, d * 8)) || (s = ensure(c, kScal, 64)) ||
-        (s = ensure(c, kSpart, (size_t)2 * ceil_div(d_pad, 32) * 8)) ||
+        (s = ensure(c, kSpart, (size_t)8 * grid * 8)) ||
         (s = ensure(c, kInv, N * 8)) || (s = ensure(c, kU, d_pad * 8)) ||
         (s = ensure(c, kZhi, (size_t)zt_rows(d_pad) * n_pad * 2)) ||
         (s = ensure(c, kZlo, (size_t)zt_rows(d_pad) * n_pad * 2)) ||
@@ -379,7 +379,7 @@ hap_status hap_align(hap_ctx c, const float* X, int64_t n_x, const float* Y, int
     cudaError_t e;
     {
         PhaseScope ps(c, HAP_PHASE_ALIGN, kAlignLaunches, st);
-        e = launch_align(a, st);
+        e = launch_align(a, grid, st);
     }
     if (e != cudaSuccess) return cuda_fail(c, e, "align kernels");
     c->aligned = true;

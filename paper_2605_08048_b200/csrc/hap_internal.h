@@ -29,12 +29,12 @@ struct AlignArgs {
     double* inv;             // [N]    1/||h_i|| (0 for a zero row)
     double* u;               // [d_pad] Householder axis (0 for the identity)
     double* coef;            // [n_x]  2 u^T x_i (0 for the identity)
-    double* part;            // [nblk_x + nblk_y][d] fp64 column partials
+    double* part;            // [2 * grid][d] fp64 per-CTA column partials (X, Y)
     double* xbar;            // [d]
     double* ybar;            // [d]
     double* scal;            // [8]    {||xbar||, ||ybar||, ||v||, u.xbar, identity}
-    double* spart;           // [2 * max grid] per-CTA scalar partials
-    long long* scratch;      // [0] min ZeroVector row (LLONG_MAX = none), [1] two tickets
+    double* spart;           // [8 * grid] per-CTA scalar partials
+    long long* scratch;      // [0] min ZeroVector row (LLONG_MAX = none), [2] grid barrier
     uint16_t* zt_hi;         // [>=d_pad][n_pad] bf16 bits
     uint16_t* zt_lo;         // [>=d_pad][n_pad]
     double* m;               // [d_pad] centre (multiple of 2^-12): planes hold z - m
@@ -43,8 +43,9 @@ struct AlignArgs {
     float2* ab;              // [d_pad] epilogue constants {2a, 2b}, a = n_x m, b = t - a
     double* sconst;          // [2]     {sum a^2, sum b^2}
 };
-cudaError_t launch_align(const AlignArgs& a, cudaStream_t st);
-constexpr int kAlignLaunches = 5;  // kernels issued by launch_align
+// one cooperative kernel of `grid` CTAs (one per SM); scratch[2] holds its grid barrier
+cudaError_t launch_align(const AlignArgs& a, int grid, cudaStream_t st);
+constexpr int kAlignLaunches = 1;  // kernels issued by launch_align
 
 // ---- K2: PERM-SPEC v1 generator (k_perm.cu) ----------------------------------------
 enum MaskOut { kMaskBf16Row = 0, kMaskU8Set = 1 };
