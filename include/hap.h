@@ -174,6 +174,9 @@ HAP_API hap_status hap_profile(hap_ctx ctx, int enable);
  * is enabled).  reset != 0 clears both. */
 HAP_API hap_status hap_profile_read(hap_ctx ctx, double* ms, int64_t* launches, int reset);
 
+/* enable >= 3: K1 records a timestamp after each of its 7 phases; this returns the phase
+ * durations (us, [host] double[7]) of the last hap_align (synchronises the device). */
+HAP_API hap_status hap_profile_k1_phases(hap_ctx ctx, double* us);
 /* Timeline of the launches timed since the last read/reset (profiling on): out [host]
  * max_n * 3 doubles {phase, start_us, end_us} relative to the first recorded launch, in
  * record order; *n receives the count.  Consumes the records (like hap_profile_read). */

@@ -88,6 +88,7 @@ def lib() -> ctypes.CDLL:
         "hap_profile": ([vp, i32], i32),
         "hap_profile_read": ([vp, P(f64), P(i64), i32], i32),
         "hap_profile_timeline": ([vp, P(f64), i64, P(i64)], i32),
+        "hap_profile_k1_phases": ([vp, P(f64)], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -214,6 +215,12 @@ def hap_profile_read(ctx, reset: bool = False):
     n = (ctypes.c_int64 * len(PHASES))()
     _check(ctx, lib().hap_profile_read(ctx, ms, n, 1 if reset else 0))
     return dict(zip(PHASES, list(ms))), dict(zip(PHASES, list(n)))
+
+
+def hap_profile_k1_phases(ctx):
+    us = (ctypes.c_double * 7)()
+    _check(ctx, lib().hap_profile_k1_phases(ctx, us))
+    return list(us)
 
 
 def hap_profile_timeline(ctx, max_n: int = 100000):

@@ -41,6 +41,7 @@ struct hap_ctx_s {
     // ---- profiling
     bool prof = false;
     bool serial = false;  // profiling level 2: generator on the caller's stream
+    bool stamp_k1 = false;  // profiling level 3: K1 phase timestamps
     struct Mark { cudaEvent_t a, b; int phase; };
     std::vector<Mark> marks;
     std::vector<cudaEvent_t> pool;
@@ -52,7 +53,7 @@ namespace {
 
 enum Buf {
     kX = 0, kY, kNrm, kCoef, kPart, kXbar, kYbar, kU, kZhi, kZlo, kTpart, kT64, kAB, kMask,
-    kM, kSconst, kGemmPart, kTileDone, kScal, kSpart, kScratch, kMask1, kInv, kNumBufs
+    kM, kSconst, kGemmPart, kTileDone, kScal, kSpart, kScratch, kMask1, kInv, kStamps, kNumBufs
 };
 
 hap_status fail(hap_ctx c, hap_status s, const std::string& msg) {
@@ -369,6 +370,8 @@ hap_status hap_align(hap_ctx c, const float* X, int64_t n_x, const float* Y, int
     a.u = B<double>(c, kU);
     a.spart = B<double>(c, kSpart);
     a.scratch = B<long long>(c, kScratch);
+    a.stamps = nullptr;
+    if (c->stamp_k1 && ensure(c, kStamps, 64) == HAP_OK) a.stamps = B<long long>(c, kStamps);
     a.zt_hi = B<uint16_t>(c, kZhi);
     a.zt_lo = B<uint16_t>(c, kZlo);
     a.tpart = B<double>(c, kTpart);
@@ -495,6 +498,19 @@ hap_status hap_profile(hap_ctx c, int enable) {
     if (!c) return HAP_E_INVALID_ARG;
     c->prof = enable != 0;
     c->serial = enable >= 2;
+    c->stamp_k1 = enable >= 3;
+    return HAP_OK;
+}
+
+hap_status hap_profile_k1_phases(hap_ctx c, double* us) {
+    if (!c || !us) return HAP_E_INVALID_ARG;
+    if (!c->buf[kStamps]) return fail(c, HAP_E_INVALID_ARG, "K1 stamps not enabled (hap_profile 3)");
+    long long t[8];
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaMemcpy(t, c->buf[kStamps], sizeof t, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(c, e, "k1 phases");
+    for (int k = 0; k < 5; ++k) us[k] = 1e-3 * (double)(t[k + 1] - t[k]);
+    us[5] = us[6] = 0.0;
     return HAP_OK;
 }
 

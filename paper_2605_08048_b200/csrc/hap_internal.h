@@ -13,7 +13,7 @@ constexpr int kKBlock = 64;     // GEMM K-block: 64 bf16 = one 128-byte swizzle 
 constexpr int kTileM = 128;     // permutations per CTA tile (TMEM lanes)
 constexpr int kChunkN = 256;    // d-columns per accumulator chunk (UMMA N <= 256)
 constexpr int kRowBlock = 16;   // rows per column-partial block in K1a
-constexpr int kRowTile = 64;    // pooled rows per reflect/split tile in K1d
+constexpr int kRowTile = 32;    // pooled rows per reflect/split tile in K1 (P4)
 
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 inline int64_t ceil_div(int64_t x, int64_t m) { return (x + m - 1) / m; }
@@ -42,6 +42,7 @@ struct AlignArgs {
     double* t64;             // [d_pad] t = N m + t'
     float2* ab;              // [d_pad] epilogue constants {2a, 2b}, a = n_x m, b = t - a
     double* sconst;          // [2]     {sum a^2, sum b^2}
+    long long* stamps;       // optional [8] globaltimer after each K1 phase (profiling)
 };
 // one cooperative kernel of `grid` CTAs (one per SM); scratch[2] holds its grid barrier
 cudaError_t launch_align(const AlignArgs& a, int grid, cudaStream_t st);

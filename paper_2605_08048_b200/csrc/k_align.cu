@@ -9,18 +9,17 @@
 //   S6 observed    r_X = ||xbar|| (= r(X')), r_Y, T_obs (Eq. 10), fp64
 //
 // The problem is small (C2: 6 MB) and a chain of dependent reductions, so the cost is
-// latency, not bandwidth: one persistent cooperative grid (one CTA per SM) runs the seven
-// phases below separated by software grid barriers.  Every reduction is fixed-order
+// latency, not bandwidth: one persistent cooperative grid (one CTA per SM) runs the five
+// phases below separated by four software grid barriers.  Every reduction is fixed-order
 // (per-CTA partials combined in ascending CTA order by a warp xor-tree or a block tree), so
 // Z~ and t are bit-identical across runs and ranks; scalars needed by every CTA are reduced
 // redundantly by every CTA from the same partials (identical results, no broadcast).
 //   P1 rows   : norms (ZeroVector check) + per-CTA fp64 column partials of X and of Y
 //   P2 columns: xbar, ybar (warp per column over the CTA partials); partials of |xbar|^2..
 //   P3 columns: ||xbar||, ||ybar||; partials of ||v||^2, v.xbar  (v = mu_x - mu_y)
-//   P4        : identity / degenerate, info; u, centre m per column; coef_i = 2 u^T x_i
-//   P5 tiles  : 64x64 reflect, centre, bf16 hi/lo split, transpose, t partials per tile
-//   P6 columns: t, epilogue constants {2a, 2b}; partials of sum a^2, sum b^2
-//   P7 CTA 0  : {sum a^2, sum b^2}; scratch reset
+//   P4 tiles  : info; per 32-row tile (self-contained CTA): coef_i = 2 u^T x_i, axis u and
+//               centre m per column, reflect, centre, bf16 hi/lo split, transpose, t partials
+//   P5 columns: t, epilogue constants {2a, 2b}; the last CTA (ticket) forms sum a^2, sum b^2
 #include <cuda_bf16.h>
 
 #include <cfloat>
@@ -64,6 +63,14 @@ __device__ double cta_partials_sum(const double* spart, int k, double* red) {
     for (int p = threadIdx.x; p < (int)gridDim.x; p += kThreads)
         v += __ldcg(spart + (size_t)p * kSpartStride + k);
     return block_sum(v, red);
+}
+
+__device__ __forceinline__ void stamp(const AlignArgs& a, int k) {
+    if (a.stamps && blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        a.stamps[k] = (long long)t;
+    }
 }
 
 // Software grid barrier (all CTAs are co-resident: cooperative launch).  bar[0] counts
@@ -111,6 +118,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_align_fused(AlignArgs a) {
     const int64_t N = a.n_x + a.n_y;
     const bool vec = (a.d & 3) == 0;
     unsigned* bar = reinterpret_cast<unsigned*>(a.scratch + 2);
+    stamp(a, 0);
 
     // ---------------- P1: norms + per-CTA column partials (X slice and Y slice)
     for (int q = 0; q < 2; ++q) {
@@ -122,6 +130,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_align_fused(AlignArgs a) {
             double s = 0.0;
             if (vec) {
                 const float4* h4 = reinterpret_cast<const float4*>(h);
+#pragma unroll 4
                 for (int64_t c = lane; c < a.d / 4; c += 32) {
                     const float4 v = __ldg(h4 + c);
                     s += (double)v.x * v.x + (double)v.y * v.y + (double)v.z * v.z +
@@ -149,6 +158,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_align_fused(AlignArgs a) {
         if (vec) {
             for (int64_t c4 = tid; c4 < a.d / 4; c4 += kThreads) {
                 double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+#pragma unroll 8
                 for (int r = 0; r < nr; ++r) {
                     const float4 v =
                         __ldg(reinterpret_cast<const float4*>(row_ptr(a, base + r0 + r)) + c4);
@@ -174,6 +184,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_align_fused(AlignArgs a) {
         __syncthreads();
     }
     grid_sync(bar);
+    stamp(a, 1);
 
     // ---------------- P2: xbar_c, ybar_c = (sum over CTA partials, lane-strided + xor tree)/n
     {
@@ -182,6 +193,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_align_fused(AlignArgs a) {
             const int q = (int)(it / a.d);
             const int64_t c = it % a.d;
             double v = 0.0;
+#pragma unroll 8
             for (int p = lane; p < G; p += 32) v += __ldcg(a.part + (size_t)(2 * p + q) * a.d + c);
             v = warp_sum(v) / (double)(q ? a.n_y : a.n_x);
             if (lane == 0) {
@@ -198,6 +210,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_align_fused(AlignArgs a) {
         }
     }
     grid_sync(bar);
+    stamp(a, 2);
 
     // ---------------- P3: norms; partials of ||v||^2 and v.xbar
     const double nx = sqrt(cta_partials_sum(a.spart, 0, red));
@@ -220,8 +233,12 @@ __global__ void __launch_bounds__(kThreads, 1) k1_align_fused(AlignArgs a) {
         }
     }
     grid_sync(bar);
+    stamp(a, 3);
 
-    // ---------------- P4: identity, info; u and m per column; coef_i = 2 u^T x_i
+    // ---------------- P4: identity, info; then 32-row tiles, each CTA self-contained:
+    // coefficients coef_i = 2 u^T x_i of its rows, axis u_c and centre m_c per column (both
+    // from the means), z' = h/||h|| - coef u - m (fp32 is ample: the value is then kept to
+    // 16 significant bits), hi/lo split, transpose, fixed-order t partial per column
     const double nv0 = sqrt(cta_partials_sum(a.spart, 2, red));
     const double vx = cta_partials_sum(a.spart, 3, red);
     const bool identity = (a.mode == HAP_ALIGN_NONE) || degenerate || nv0 < 1e-9;  // R3
@@ -250,85 +267,97 @@ __global__ void __launch_bounds__(kThreads, 1) k1_align_fused(AlignArgs a) {
         const double qnan = __longlong_as_double(0x7ff8000000000000ll);
         f->gemm_r_x = f->gemm_r_y = f->gemm_t_obs = qnan;
     }
-    for (int64_t c = (int64_t)cta * kThreads + tid; c < a.d_pad; c += (int64_t)G * kThreads) {
-        double u = 0.0, m = 0.0;
-        if (c < a.d) {
-            const double xb = __ldcg(a.xbar + c), yb = __ldcg(a.ybar + c);
-            u = (xb * rnx - yb * rny) * rnv;
-            // centre m = t/N quantised to 2^-12, t = n_x (xbar - 2u(u.xbar)) + n_y ybar
-            const double t = (double)a.n_x * (xb - 2.0 * u * ux) + (double)a.n_y * yb;
-            m = rint(t * rN) * (1.0 / 4096.0);
-        }
-        a.u[c] = u;
-        a.m[c] = m;
-    }
-    if (!identity) {
-        for (int64_t i = (int64_t)cta * kWarps + warp; i < a.n_x; i += (int64_t)G * kWarps) {
-            const float* h = a.X + i * a.d;
-            double s = 0.0;
-            for (int64_t c = lane; c < a.d; c += 32)
-                s += (double)__ldg(h + c) * (__ldcg(a.xbar + c) * rnx - __ldcg(a.ybar + c) * rny);
-            s = warp_sum(s);
-            if (lane == 0) a.coef[i] = 2.0 * s * rnv * __ldcg(a.inv + i);
-        }
-    }
-    grid_sync(bar);
-
-    // ---------------- P5: 64x64 tiles: z' = h/||h|| - coef u - m (fp32 is ample: the value
-    // is then kept to 16 significant bits), hi/lo split, transpose, t partials
     {
+        double* s_coef = s_inv;  // reuse: 32 rows
         uint16_t* sh16 = reinterpret_cast<uint16_t*>(s_hi);
         uint16_t* sl16 = reinterpret_cast<uint16_t*>(s_lo);
-        const int64_t ntr = a.n_pad / kRowTile, ntc = (a.d_pad + 63) / 64;
-        for (int64_t tile = cta; tile < ntr * ntc; tile += G) {
-            const int64_t rt = tile / ntc, ct = tile % ntc;
-            const int64_t r0 = rt * kRowTile, c0 = ct * 64;
-            const int tc = tid & 63, tr = tid >> 6;
-            const int64_t c = c0 + tc;
-            const float uc = c < a.d_pad ? (float)__ldcg(a.u + c) : 0.f;
-            const float mc = c < a.d_pad ? (float)__ldcg(a.m + c) : 0.f;
-#pragma unroll 4
-            for (int j = 0; j < 16; ++j) {
-                const int rl = tr + 4 * j;
+        const int64_t ntr = a.n_pad / kRowTile;
+        for (int64_t rt = cta; rt < ntr; rt += G) {
+            const int64_t r0 = rt * kRowTile;
+            // coefficients of the tile's rows (warp per row)
+            for (int rl = warp; rl < kRowTile; rl += kWarps) {
                 const int64_t i = r0 + rl;
-                float z = 0.f;
-                if (i < N && c < a.d) {
-                    const float h = __ldg(row_ptr(a, i) + c);
-                    const float cf = (i < a.n_x && !identity) ? (float)__ldcg(a.coef + i) : 0.f;
-                    z = fmaf(-cf, uc, h * (float)__ldcg(a.inv + i)) - mc;
+                double sdot = 0.0;
+                if (i < a.n_x && !identity) {
+                    const float* h = a.X + i * a.d;
+#pragma unroll 8
+                    for (int64_t c = lane; c < a.d; c += 32)
+                        sdot += (double)__ldg(h + c) * (__ldcg(a.xbar + c) * rnx - __ldcg(a.ybar + c) * rny);
+                    sdot = warp_sum(sdot);
                 }
-                const __nv_bfloat16 hi = __float2bfloat16_rn(z);
-                const __nv_bfloat16 lo = __float2bfloat16_rn(z - __bfloat162float(hi));
-                sh16[tc * (2 * kSP) + rl] = __bfloat16_as_ushort(hi);
-                sl16[tc * (2 * kSP) + rl] = __bfloat16_as_ushort(lo);
+                if (lane == 0) s_coef[rl] = (i < a.n_x && !identity) ? 2.0 * sdot * rnv * __ldcg(a.inv + i) : 0.0;
             }
             __syncthreads();
-            for (int cc = warp; cc < 64; cc += kWarps) {
-                const int64_t col = c0 + cc;
-                if (col >= a.d_pad) break;
-                const uint32_t vh = s_hi[cc * kSP + lane], vl = s_lo[cc * kSP + lane];
-                reinterpret_cast<uint32_t*>(a.zt_hi + col * a.n_pad + r0)[lane] = vh;
-                reinterpret_cast<uint32_t*>(a.zt_lo + col * a.n_pad + r0)[lane] = vl;
-                const double v =
-                    (double)__bfloat162float(__ushort_as_bfloat16((uint16_t)(vh & 0xFFFF))) +
-                    (double)__bfloat162float(__ushort_as_bfloat16((uint16_t)(vl & 0xFFFF))) +
-                    (double)__bfloat162float(__ushort_as_bfloat16((uint16_t)(vh >> 16))) +
-                    (double)__bfloat162float(__ushort_as_bfloat16((uint16_t)(vl >> 16)));
-                const double s = warp_sum(v);
-                if (lane == 0) a.tpart[rt * a.d_pad + col] = s;
+            for (int64_t c0 = 0; c0 < a.d_pad; c0 += 64) {
+                const int tc = tid & 63, tr = tid >> 6;  // 64 columns x 4 row groups
+                const int64_t c = c0 + tc;
+                double ud = 0.0, md = 0.0;
+                if (c < a.d) {
+                    const double xb = __ldcg(a.xbar + c), yb = __ldcg(a.ybar + c);
+                    ud = (xb * rnx - yb * rny) * rnv;
+                    // centre m = t/N quantised to 2^-12, t = n_x (xbar - 2u(u.xbar)) + n_y ybar
+                    const double t = (double)a.n_x * (xb - 2.0 * ud * ux) + (double)a.n_y * yb;
+                    md = rint(t * rN) * (1.0 / 4096.0);
+                }
+                if (rt == 0 && tr == 0 && c < a.d_pad) {  // export copies
+                    a.u[c] = ud;
+                    a.m[c] = md;
+                }
+                const float uc = (float)ud, mc = (float)md;
+                float hv[kRowTile / 4];
+#pragma unroll
+                for (int j = 0; j < kRowTile / 4; ++j) {  // issue all loads first
+                    const int64_t i = r0 + tr + 4 * j;
+                    hv[j] = (i < N && c < a.d) ? __ldg(row_ptr(a, i) + c) : 0.f;
+                }
+#pragma unroll
+                for (int j = 0; j < kRowTile / 4; ++j) {
+                    const int rl = tr + 4 * j;
+                    const int64_t i = r0 + rl;
+                    float z = 0.f;
+                    if (i < N && c < a.d)
+                        z = fmaf(-(float)s_coef[rl], uc, hv[j] * (float)__ldcg(a.inv + i)) - mc;
+                    const __nv_bfloat16 hi = __float2bfloat16_rn(z);
+                    const __nv_bfloat16 lo = __float2bfloat16_rn(z - __bfloat162float(hi));
+                    sh16[tc * (2 * kSP) + rl] = __bfloat16_as_ushort(hi);
+                    sl16[tc * (2 * kSP) + rl] = __bfloat16_as_ushort(lo);
+                }
+                __syncthreads();
+                // 32 rows = 16 words per column: half-warps write one column each
+                const int hw = lane >> 4, hl = lane & 15;
+                for (int cc = 2 * warp + hw; cc < 64; cc += 2 * kWarps) {
+                    const int64_t col = c0 + cc;
+                    double v = 0.0;
+                    if (col < a.d_pad) {
+                        const uint32_t vh = s_hi[cc * kSP + hl], vl = s_lo[cc * kSP + hl];
+                        reinterpret_cast<uint32_t*>(a.zt_hi + col * a.n_pad + r0)[hl] = vh;
+                        reinterpret_cast<uint32_t*>(a.zt_lo + col * a.n_pad + r0)[hl] = vl;
+                        v = (double)__bfloat162float(__ushort_as_bfloat16((uint16_t)(vh & 0xFFFF))) +
+                            (double)__bfloat162float(__ushort_as_bfloat16((uint16_t)(vl & 0xFFFF))) +
+                            (double)__bfloat162float(__ushort_as_bfloat16((uint16_t)(vh >> 16))) +
+                            (double)__bfloat162float(__ushort_as_bfloat16((uint16_t)(vl >> 16)));
+                    }
+#pragma unroll
+                    for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                    if (hl == 0 && col < a.d_pad) a.tpart[rt * a.d_pad + col] = v;
+                }
+                __syncthreads();
             }
-            __syncthreads();
         }
     }
     grid_sync(bar);
+    stamp(a, 4);
 
-    // ---------------- P6: t = N m + sum of tile partials (lane-strided + xor tree);
-    // a = n_x m, b = t - a (fp32) for the GEMM epilogue; partials of sum a^2, sum b^2
+    // ---------------- P5: t = N m + sum of tile partials (lane-strided + xor tree);
+    // a = n_x m, b = t - a (fp32) for the GEMM epilogue; partials of sum a^2, sum b^2;
+    // the last CTA to finish (ticket) forms {sum a^2, sum b^2} in fixed order
     {
+        __shared__ int s_last;
         const int64_t ntr = a.n_pad / kRowTile;
         double sa = 0.0, sb = 0.0;
         for (int64_t c = (int64_t)cta * kWarps + warp; c < a.d_pad; c += (int64_t)G * kWarps) {
             double tp = 0.0;
+#pragma unroll 4
             for (int64_t t = lane; t < ntr; t += 32) tp += __ldcg(a.tpart + t * a.d_pad + c);
             tp = warp_sum(tp);
             if (lane == 0) {
@@ -346,20 +375,24 @@ __global__ void __launch_bounds__(kThreads, 1) k1_align_fused(AlignArgs a) {
         if (tid == 0) {
             a.spart[(size_t)cta * kSpartStride + 4] = sa;
             a.spart[(size_t)cta * kSpartStride + 5] = sb;
+            __threadfence();
+            unsigned* ticket = reinterpret_cast<unsigned*>(a.scratch + 1);
+            s_last = atomicAdd(ticket, 1u) == (unsigned)G - 1;
+        }
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            const double SA = cta_partials_sum(a.spart, 4, red);
+            const double SB = cta_partials_sum(a.spart, 5, red);
+            if (tid == 0) {
+                a.sconst[0] = SA;
+                a.sconst[1] = SB;
+                a.scratch[0] = LLONG_MAX;  // reset the ZeroVector word and the ticket
+                reinterpret_cast<unsigned*>(a.scratch + 1)[0] = 0u;
+            }
         }
     }
-    grid_sync(bar);
-
-    // ---------------- P7: epilogue constants; reset the ZeroVector scratch word
-    if (cta == 0) {
-        const double SA = cta_partials_sum(a.spart, 4, red);
-        const double SB = cta_partials_sum(a.spart, 5, red);
-        if (tid == 0) {
-            a.sconst[0] = SA;
-            a.sconst[1] = SB;
-            a.scratch[0] = LLONG_MAX;
-        }
-    }
+    stamp(a, 5);
 }
 
 }  // namespace
