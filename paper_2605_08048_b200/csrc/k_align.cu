@@ -16,9 +16,10 @@
 // redundantly by every CTA from the same partials (identical results, no broadcast).
 //   P1 rows   : norms (ZeroVector check) + per-CTA fp64 column partials of X and of Y
 //   P2 columns: xbar, ybar (warp per column over the CTA partials); partials of |xbar|^2..
-//   P3 columns: ||xbar||, ||ybar||; partials of ||v||^2, v.xbar  (v = mu_x - mu_y)
-//   P4 tiles  : info; per 32-row tile (self-contained CTA): coef_i = 2 u^T x_i, axis u and
-//               centre m per column, reflect, centre, bf16 hi/lo split, transpose, t partials
+//   P3 columns: ||xbar||, ||ybar||; partials of ||v||^2, v.xbar (v = mu_x - mu_y); rows:
+//               xbar.h_i, ybar.h_i for the reflection coefficients
+//   P4 tiles  : info; 32x64 tiles: axis u and centre m per column, coef from the P3 dots,
+//               reflect, centre, bf16 hi/lo split, transpose, t partials
 //   P5 columns: t, epilogue constants {2a, 2b}; the last CTA (ticket) forms sum a^2, sum b^2
 #include <cuda_bf16.h>
 
@@ -231,6 +232,23 @@ __global__ void __launch_bounds__(kThreads, 1) k1_align_fused(AlignArgs a) {
             a.spart[(size_t)cta * kSpartStride + 2] = sv;
             a.spart[(size_t)cta * kSpartStride + 3] = svx;
         }
+        // row dots for the reflection coefficients (they do not need ||v||):
+        // coef_i = 2 u^T x_i = 2 (xbar.h_i / ||xbar|| - ybar.h_i / ||ybar||) / (||v|| ||h_i||)
+        if (a.mode != HAP_ALIGN_NONE && !degenerate) {
+            for (int64_t i = (int64_t)cta * kWarps + warp; i < a.n_x; i += (int64_t)G * kWarps) {
+                const float* h = a.X + i * a.d;
+                double dx = 0.0, dy = 0.0;
+#pragma unroll 8
+                for (int64_t c = lane; c < a.d; c += 32) {
+                    const double hv = (double)__ldg(h + c);
+                    dx += hv * __ldcg(a.xbar + c);
+                    dy += hv * __ldcg(a.ybar + c);
+                }
+                dx = warp_sum(dx);
+                dy = warp_sum(dy);
+                if (lane == 0) a.coef[i] = (dx * rnx - dy * rny) * __ldcg(a.inv + i);
+            }
+        }
     }
     grid_sync(bar);
     stamp(a, 3);
@@ -268,81 +286,73 @@ __global__ void __launch_bounds__(kThreads, 1) k1_align_fused(AlignArgs a) {
         f->gemm_r_x = f->gemm_r_y = f->gemm_t_obs = qnan;
     }
     {
-        double* s_coef = s_inv;  // reuse: 32 rows
+        // 2-D tiles (32 rows x 64 columns); P3 stored (u^T x_i) * ||v|| in coef[i]
+        double* s_cf = s_inv;         // [32] 2 u^T x_i of the tile rows
+        double* s_iv = s_inv + 64;    // [32] 1/||h_i||
         uint16_t* sh16 = reinterpret_cast<uint16_t*>(s_hi);
         uint16_t* sl16 = reinterpret_cast<uint16_t*>(s_lo);
-        const int64_t ntr = a.n_pad / kRowTile;
-        for (int64_t rt = cta; rt < ntr; rt += G) {
+        const int64_t ntr = a.n_pad / kRowTile, ntc = (a.d_pad + 63) / 64;
+        for (int64_t tile = cta; tile < ntr * ntc; tile += G) {
+            const int64_t rt = tile / ntc, c0 = (tile % ntc) * 64;
             const int64_t r0 = rt * kRowTile;
-            // coefficients of the tile's rows (warp per row)
-            for (int rl = warp; rl < kRowTile; rl += kWarps) {
-                const int64_t i = r0 + rl;
-                double sdot = 0.0;
-                if (i < a.n_x && !identity) {
-                    const float* h = a.X + i * a.d;
-#pragma unroll 8
-                    for (int64_t c = lane; c < a.d; c += 32)
-                        sdot += (double)__ldg(h + c) * (__ldcg(a.xbar + c) * rnx - __ldcg(a.ybar + c) * rny);
-                    sdot = warp_sum(sdot);
-                }
-                if (lane == 0) s_coef[rl] = (i < a.n_x && !identity) ? 2.0 * sdot * rnv * __ldcg(a.inv + i) : 0.0;
+            if (tid < kRowTile) {
+                const int64_t i = r0 + tid;
+                s_cf[tid] = (i < a.n_x && !identity) ? 2.0 * __ldcg(a.coef + i) * rnv : 0.0;
+                s_iv[tid] = i < N ? __ldcg(a.inv + i) : 0.0;
+            }
+            const int tc = tid & 63, tr = tid >> 6;  // 64 columns x 4 row groups of 8
+            const int64_t c = c0 + tc;
+            float hv[kRowTile / 4];
+#pragma unroll
+            for (int j = 0; j < kRowTile / 4; ++j) {  // issue all loads first
+                const int64_t i = r0 + tr + 4 * j;
+                hv[j] = (i < N && c < a.d) ? __ldg(row_ptr(a, i) + c) : 0.f;
+            }
+            double ud = 0.0, md = 0.0;
+            if (c < a.d) {
+                const double xb = __ldcg(a.xbar + c), yb = __ldcg(a.ybar + c);
+                ud = (xb * rnx - yb * rny) * rnv;
+                // centre m = t/N quantised to 2^-12, t = n_x (xbar - 2u(u.xbar)) + n_y ybar
+                const double t = (double)a.n_x * (xb - 2.0 * ud * ux) + (double)a.n_y * yb;
+                md = rint(t * rN) * (1.0 / 4096.0);
+            }
+            if (rt == 0 && tr == 0 && c < a.d_pad) {  // export copies (read in P5)
+                a.u[c] = ud;
+                a.m[c] = md;
             }
             __syncthreads();
-            for (int64_t c0 = 0; c0 < a.d_pad; c0 += 64) {
-                const int tc = tid & 63, tr = tid >> 6;  // 64 columns x 4 row groups
-                const int64_t c = c0 + tc;
-                double ud = 0.0, md = 0.0;
-                if (c < a.d) {
-                    const double xb = __ldcg(a.xbar + c), yb = __ldcg(a.ybar + c);
-                    ud = (xb * rnx - yb * rny) * rnv;
-                    // centre m = t/N quantised to 2^-12, t = n_x (xbar - 2u(u.xbar)) + n_y ybar
-                    const double t = (double)a.n_x * (xb - 2.0 * ud * ux) + (double)a.n_y * yb;
-                    md = rint(t * rN) * (1.0 / 4096.0);
-                }
-                if (rt == 0 && tr == 0 && c < a.d_pad) {  // export copies
-                    a.u[c] = ud;
-                    a.m[c] = md;
-                }
-                const float uc = (float)ud, mc = (float)md;
-                float hv[kRowTile / 4];
+            const float uc = (float)ud, mc = (float)md;
 #pragma unroll
-                for (int j = 0; j < kRowTile / 4; ++j) {  // issue all loads first
-                    const int64_t i = r0 + tr + 4 * j;
-                    hv[j] = (i < N && c < a.d) ? __ldg(row_ptr(a, i) + c) : 0.f;
-                }
-#pragma unroll
-                for (int j = 0; j < kRowTile / 4; ++j) {
-                    const int rl = tr + 4 * j;
-                    const int64_t i = r0 + rl;
-                    float z = 0.f;
-                    if (i < N && c < a.d)
-                        z = fmaf(-(float)s_coef[rl], uc, hv[j] * (float)__ldcg(a.inv + i)) - mc;
-                    const __nv_bfloat16 hi = __float2bfloat16_rn(z);
-                    const __nv_bfloat16 lo = __float2bfloat16_rn(z - __bfloat162float(hi));
-                    sh16[tc * (2 * kSP) + rl] = __bfloat16_as_ushort(hi);
-                    sl16[tc * (2 * kSP) + rl] = __bfloat16_as_ushort(lo);
-                }
-                __syncthreads();
-                // 32 rows = 16 words per column: half-warps write one column each
-                const int hw = lane >> 4, hl = lane & 15;
-                for (int cc = 2 * warp + hw; cc < 64; cc += 2 * kWarps) {
-                    const int64_t col = c0 + cc;
-                    double v = 0.0;
-                    if (col < a.d_pad) {
-                        const uint32_t vh = s_hi[cc * kSP + hl], vl = s_lo[cc * kSP + hl];
-                        reinterpret_cast<uint32_t*>(a.zt_hi + col * a.n_pad + r0)[hl] = vh;
-                        reinterpret_cast<uint32_t*>(a.zt_lo + col * a.n_pad + r0)[hl] = vl;
-                        v = (double)__bfloat162float(__ushort_as_bfloat16((uint16_t)(vh & 0xFFFF))) +
-                            (double)__bfloat162float(__ushort_as_bfloat16((uint16_t)(vl & 0xFFFF))) +
-                            (double)__bfloat162float(__ushort_as_bfloat16((uint16_t)(vh >> 16))) +
-                            (double)__bfloat162float(__ushort_as_bfloat16((uint16_t)(vl >> 16)));
-                    }
-#pragma unroll
-                    for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-                    if (hl == 0 && col < a.d_pad) a.tpart[rt * a.d_pad + col] = v;
-                }
-                __syncthreads();
+            for (int j = 0; j < kRowTile / 4; ++j) {
+                const int rl = tr + 4 * j;
+                const float z = (r0 + rl < N && c < a.d)
+                                    ? fmaf(-(float)s_cf[rl], uc, hv[j] * (float)s_iv[rl]) - mc
+                                    : 0.f;
+                const __nv_bfloat16 hi = __float2bfloat16_rn(z);
+                const __nv_bfloat16 lo = __float2bfloat16_rn(z - __bfloat162float(hi));
+                sh16[tc * (2 * kSP) + rl] = __bfloat16_as_ushort(hi);
+                sl16[tc * (2 * kSP) + rl] = __bfloat16_as_ushort(lo);
             }
+            __syncthreads();
+            // 32 rows = 16 words per column: half-warps write one column each
+            const int hw = lane >> 4, hl = lane & 15;
+            for (int cc = 2 * warp + hw; cc < 64; cc += 2 * kWarps) {
+                const int64_t col = c0 + cc;
+                double v = 0.0;
+                if (col < a.d_pad) {
+                    const uint32_t vh = s_hi[cc * kSP + hl], vl = s_lo[cc * kSP + hl];
+                    reinterpret_cast<uint32_t*>(a.zt_hi + col * a.n_pad + r0)[hl] = vh;
+                    reinterpret_cast<uint32_t*>(a.zt_lo + col * a.n_pad + r0)[hl] = vl;
+                    v = (double)__bfloat162float(__ushort_as_bfloat16((uint16_t)(vh & 0xFFFF))) +
+                        (double)__bfloat162float(__ushort_as_bfloat16((uint16_t)(vl & 0xFFFF))) +
+                        (double)__bfloat162float(__ushort_as_bfloat16((uint16_t)(vh >> 16))) +
+                        (double)__bfloat162float(__ushort_as_bfloat16((uint16_t)(vl >> 16)));
+                }
+#pragma unroll
+                for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (hl == 0 && col < a.d_pad) a.tpart[rt * a.d_pad + col] = v;
+            }
+            __syncthreads();
         }
     }
     grid_sync(bar);
