@@ -177,6 +177,9 @@ HAP_API hap_status hap_profile_read(hap_ctx ctx, double* ms, int64_t* launches, 
 /* enable >= 3: K1 records a timestamp after each of its 7 phases; this returns the phase
  * durations (us, [host] double[7]) of the last hap_align (synchronises the device). */
 HAP_API hap_status hap_profile_k1_phases(hap_ctx ctx, double* us);
+/* Development aid: with HAP_K3_EXPERIMENT bit 16 set in the environment, K3 records
+ * globaltimer stamps [sm_count][8 units][8 events]; copies up to n int64 into out [host]. */
+HAP_API hap_status hap_debug_k3_stamps(hap_ctx ctx, long long* out, int64_t n);
 /* Timeline of the launches timed since the last read/reset (profiling on): out [host]
  * max_n * 3 doubles {phase, start_us, end_us} relative to the first recorded launch, in
  * record order; *n receives the count.  Consumes the records (like hap_profile_read). */

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -53,7 +54,8 @@ namespace {
 
 enum Buf {
     kX = 0, kY, kNrm, kCoef, kPart, kXbar, kYbar, kU, kZhi, kZlo, kTpart, kT64, kAB, kMask,
-    kM, kSconst, kGemmPart, kTileDone, kScal, kSpart, kScratch, kMask1, kInv, kStamps, kNumBufs
+    kM, kSconst, kGemmPart, kTileDone, kScal, kSpart, kScratch, kMask1, kInv, kStamps, kK3Stamps,
+    kNumBufs
 };
 
 hap_status fail(hap_ctx c, hap_status s, const std::string& msg) {
@@ -166,6 +168,11 @@ GemmArgs gemm_args(hap_ctx c, hap_align_info* info) {
     g.part = B<float2>(c, kGemmPart);
     g.tile_done = B<unsigned>(c, kTileDone);
     g.tie_rel = 1e-6;
+    const char* ex = getenv("HAP_K3_EXPERIMENT");
+    g.exp = ex ? atoi(ex) : 0;
+    g.stamps = nullptr;
+    if ((g.exp & 16) && ensure(c, kK3Stamps, (size_t)c->sm_count * 64 * 8) == HAP_OK)
+        g.stamps = B<long long>(c, kK3Stamps);
     return g;
 }
 
@@ -499,6 +506,15 @@ hap_status hap_profile(hap_ctx c, int enable) {
     c->prof = enable != 0;
     c->serial = enable >= 2;
     c->stamp_k1 = enable >= 3;
+    return HAP_OK;
+}
+
+hap_status hap_debug_k3_stamps(hap_ctx c, long long* out, int64_t n) {
+    if (!c || !out || !c->buf[kK3Stamps]) return HAP_E_INVALID_ARG;
+    cudaDeviceSynchronize();
+    const size_t bytes = std::min<size_t>((size_t)n * 8, (size_t)c->sm_count * 64 * 8);
+    if (cudaMemcpy(out, c->buf[kK3Stamps], bytes, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return HAP_E_CUDA;
     return HAP_OK;
 }
 

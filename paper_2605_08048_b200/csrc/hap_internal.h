@@ -80,6 +80,8 @@ struct GemmArgs {
     const double* sconst;    // {sum a^2, sum b^2}
     float2* part;            // [ntiles][nchunks][rows_per_tile] chunk partials {s1, s2}
     unsigned* tile_done;     // [ntiles] arrival tickets (zero between launches)
+    int exp;                 // timing experiments only (HAP_K3_EXPERIMENT), 0 in production
+    long long* stamps;       // exp bit 16: [grid][8 units][8 events] globaltimer
 };
 int maskgemm_b_rows(int pair_mode);  // B tile rows per CTA (TMA box)
 cudaError_t launch_maskgemm(const CUtensorMap* tmA, const CUtensorMap* tmBhi,

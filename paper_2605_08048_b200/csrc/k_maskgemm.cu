@@ -57,6 +57,18 @@ __device__ __forceinline__ double logkappa(double r, double d) {
     return log(r) + log(d - r2) - log(1.0 - r2);
 }
 
+__device__ __forceinline__ long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return (long long)t;
+}
+// EXPERIMENT (exp bit 16): per (CTA, local unit i, event) timestamps
+#define K3_STAMP(i, ev)                                                                      \
+    do {                                                                                     \
+        if ((g.exp & 16) && g.stamps && (i) < 8)                                             \
+            g.stamps[((size_t)blockIdx.x * 8 + (i)) * 8 + (ev)] = gtimer();                  \
+    } while (0)
+
 struct RowStat {
     double r1, r2, T;
 };
@@ -182,15 +194,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int width = min(kChunkN, g.d_pad - chunk * kChunkN);
                 const int arow = tile * R + (int)rank * kTileM;
                 const int brow = chunk * kChunkN + (int)rank * (width / kPair);
+                const int ui = (u - pair_id) / npairs;
                 for (int kb = 0; kb < nkb; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1u);
+                    if (kb == 0) K3_STAMP(ui, 0);
+                    if (kb == nkb - 1) K3_STAMP(ui, 1);
                     uint8_t* sA = smem + stage * C::kStageBytes;
                     if constexpr (kPair == 2) {
-                        if (leader) mbar_arrive_expect_tx(&full[stage], 2u * C::kStageBytes);
+                        // EXPERIMENT (timing only): bit0 skips A loads, bit1 skips B lo loads
+                        const uint32_t bytes = (uint32_t)C::kStageBytes - ((g.exp & 1) ? kStageA : 0) -
+                                               ((g.exp & 2) ? C::kStageB : 0);
+                        if (leader) mbar_arrive_expect_tx(&full[stage], 2u * bytes);
                         const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
-                        tma_load_2d_pair(&tmA, fb, sA, kb * kKBlock, arow);
+                        if (!(g.exp & 1)) tma_load_2d_pair(&tmA, fb, sA, kb * kKBlock, arow);
                         tma_load_2d_pair(&tmBhi, fb, sA + kStageA, kb * kKBlock, brow);
-                        tma_load_2d_pair(&tmBlo, fb, sA + kStageA + C::kStageB, kb * kKBlock, brow);
+                        if (!(g.exp & 2))
+                            tma_load_2d_pair(&tmBlo, fb, sA + kStageA + C::kStageB, kb * kKBlock, brow);
                     } else {
                         mbar_arrive_expect_tx(&full[stage], (uint32_t)C::kStageBytes);
                         tma_load_2d(&tmA, &full[stage], sA, kb * kKBlock, arow);
@@ -215,6 +234,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int a = i & 1;
                 mbar_wait(&tempty[a], (((uint32_t)i >> 1) & 1u) ^ 1u);
                 tc_fence_after();
+                K3_STAMP(i, 2);
                 const uint32_t dtm = tmem + (uint32_t)(a * kChunkN);
                 for (int kb = 0; kb < nkb; ++kb) {
                     mbar_wait(&full[stage], phase);
@@ -228,7 +248,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const uint64_t ld = smem_desc_k_sw128(lBase + 32u * k);
                         if constexpr (kPair == 2) {
                             umma_bf16_ss_pair(dtm, ad, hd, idesc, (kb | k) != 0 ? 1u : 0u);
-                            umma_bf16_ss_pair(dtm, ad, ld, idesc, 1u);
+                            if (!(g.exp & 4)) umma_bf16_ss_pair(dtm, ad, ld, idesc, 1u);
                         } else {
                             umma_bf16_ss(dtm, ad, hd, idesc, (kb | k) != 0 ? 1u : 0u);
                             umma_bf16_ss(dtm, ad, ld, idesc, 1u);
@@ -240,6 +260,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 if constexpr (kPair == 2) umma_commit_pair(&tfull[a], 0x3);
                 else umma_commit(&tfull[a]);
+                K3_STAMP(i, 3);
             }
         }
     } else {
@@ -259,10 +280,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int a = i & 1;
             mbar_wait(&tfull[a], ((uint32_t)i >> 1) & 1u);
             tc_fence_after();
+            if (etid == 0) K3_STAMP(i, 4);
             // sigma1 = a + acc, sigma2 = b - acc:  |sigma1|^2 - |a|^2 = sum acc (acc + 2a), ...
             float s1 = 0.f, s2 = 0.f;
             const float4* abp = reinterpret_cast<const float4*>(g.ab + chunk * kChunkN);
-            for (int cb = 0; cb < width / 32; ++cb) {
+            for (int cb = 0; cb < ((g.exp & 8) ? 0 : width / 32); ++cb) {
                 uint32_t r[32];
                 tmem_ld_32x32b_x32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(a * kChunkN + 32 * cb),
                                    r);
@@ -283,6 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if constexpr (kPair == 2) mbar_arrive_cluster(tempty_c[a]);
                 else mbar_arrive(&tempty[a]);
             }
+            if (etid == 0) K3_STAMP(i, 5);
             g.part[((size_t)tile * g.nchunks + chunk) * R + trow] = make_float2(s1, s2);
             __threadfence();
             named_bar_sync(1, 128);
@@ -293,7 +316,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             named_bar_sync(1, 128);
             if (*s_last) {
                 __threadfence();
+                if (etid == 0) K3_STAMP(i, 6);
                 finalize_tile(g, tile, etid, s_tobs);
+                if (etid == 0) K3_STAMP(i, 7);
             }
             named_bar_sync(1, 128);
         }
