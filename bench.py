@@ -193,18 +193,36 @@ def run_hap(args):
     pool_np = make_pool(args.pool, rank)
     pool = [(torch.from_numpy(X).to(dev), torch.from_numpy(Y).to(dev)) for X, Y in pool_np]
     in_bytes = sum(x.numel() * 4 + y.numel() * 4 for x, y in pool)
-    ctx = hap.Context(local)
+    # consecutive tests are independent: a pipeline of `depth` contexts, each on its own
+    # stream, lets test k+1's alignment/generator overlap test k's mask-GEMM
+    depth = max(1, args.depth)
+    ctxs = [hap.Context(local) for _ in range(depth)]
+    streams = [torch.cuda.Stream(device=dev) for _ in range(depth)]
+    ctx = ctxs[0]
     st = torch.cuda.current_stream()
     K, W = args.steps, args.warmup
     counts = torch.zeros((max(K, 1) * world, 3), dtype=torch.int64, device=dev)
-    cfg = hap.make_cfg(HI.PERM_SEED, B)
+    cfgs = [hap.make_cfg(HI.PERM_SEED, B) for _ in range(depth)]
 
     def step(k, slot=None):
         X, Y = pool[k % len(pool)]
-        hap.hap_align(ctx.h, X, Y, hap.HAP_ALIGN_HOUSEHOLDER, ctx.info, st)
-        c = counts[slot] if slot is not None else ctx.counts
-        cfg.stream_id = (rank * 1_000_003 + k) & 0xFFFFFFFF
-        hap.hap_permtest(ctx.h, ctx.info, cfg, c, None, st)
+        c, s_, cf = ctxs[k % depth], streams[k % depth], cfgs[k % depth]
+        hap.hap_align(c.h, X, Y, hap.HAP_ALIGN_HOUSEHOLDER, c.info, s_)
+        out = counts[slot] if slot is not None else c.counts
+        cf.stream_id = (rank * 1_000_003 + k) & 0xFFFFFFFF
+        hap.hap_permtest(c.h, c.info, cf, out, None, s_)
+
+    def fork():  # all pipeline streams start after the work already on `st`
+        ev = torch.cuda.Event()
+        ev.record(st)
+        for s_ in streams:
+            s_.wait_event(ev)
+
+    def join():  # `st` waits for every pipeline stream
+        for s_ in streams:
+            ev = torch.cuda.Event()
+            ev.record(s_)
+            st.wait_event(ev)
 
     gpu_id = None
     try:
@@ -219,15 +237,18 @@ def run_hap(args):
     for k in range(W):
         step(k)
     torch.cuda.synchronize()
-    hap.hap_profile_read(ctx.h, reset=True)
+    for c in ctxs:
+        hap.hap_profile_read(c.h, reset=True)
     counts.zero_()
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     tw0 = time.time()
     e0.record(st)
+    fork()
     for k in range(K):
         step(k, slot=rank * K + k)
+    join()
     if world > 1:
         dist.all_reduce(counts)  # the one combine of the integer counts
     e1.record(st)
@@ -235,7 +256,10 @@ def run_hap(args):
     tw1 = time.time()
     barrier()
     ms = e0.elapsed_time(e1)
-    _, launches = hap.hap_profile_read(ctx.h, reset=True)
+    launches = {}
+    for c in ctxs:
+        for kname, v in hap.hap_profile_read(c.h, reset=True)[1].items():
+            launches[kname] = launches.get(kname, 0) + v
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -248,7 +272,10 @@ def run_hap(args):
     Kp = min(K, 400)
     hap.hap_profile(ctx.h, 2)  # serialised phases so the per-kernel times do not overlap
     for k in range(Kp):
-        step(k)
+        X, Y = pool[k % len(pool)]
+        hap.hap_align(ctx.h, X, Y, hap.HAP_ALIGN_HOUSEHOLDER, ctx.info, st)
+        cfgs[0].stream_id = k
+        hap.hap_permtest(ctx.h, ctx.info, cfgs[0], ctx.counts, None, st)
     phase_ms, phase_n = hap.hap_profile_read(ctx.h, reset=True)
     hap.hap_profile(ctx.h, False)
     peaks, peak_src = load_peaks()
@@ -310,6 +337,7 @@ def run_hap(args):
                                 f"({in_bytes / 1e6:.0f} MB > 126 MB L2)",
                           "parallelism": f"pairs sharded over {world} rank(s); 1 test per "
                                          "rank per step; counts combined by one all_reduce",
+                          "pipeline_depth": depth,
                           "arith": "bf16 hi/lo split operands, fp32 TMEM accumulation, "
                                    "fp64 statistic"},
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
@@ -317,7 +345,8 @@ def run_hap(args):
                "gpu_launches_by_phase": launches, "phase_ms_per_step": phases_per_step,
                "last_test": {"t_obs": res["t_obs"], "p_value": res["p_value"]}}
         print(json.dumps(out), flush=True)
-    ctx.close()
+    for c in ctxs:
+        c.close()
     if world > 1:
         dist.destroy_process_group()
 
@@ -330,6 +359,8 @@ def main():
     ap.add_argument("--impl", default="hap", choices=["hap", "reference"])
     ap.add_argument("--pool", type=int, default=24, help="distinct input pairs per rank")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--depth", type=int, default=2,
+                    help="independent tests in flight (contexts/streams)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

@@ -54,7 +54,7 @@ __device__ __forceinline__ double logkappa(double r, double d) {
     if (r > 1.0 - 1e-9) r = 1.0 - 1e-9;
     if (r <= 0.0) return -INFINITY;
     const double r2 = r * r;
-    return log(r) + log(d - r2) - log(1.0 - r2);
+    return log(r * (d - r2) / (1.0 - r2));  // one log (the oracle sums three: same value)
 }
 
 __device__ __forceinline__ long long gtimer() {
