@@ -39,6 +39,10 @@ struct hap_ctx_s {
     cudaEvent_t ev_fork = nullptr, ev_ready[2] = {}, ev_free[2] = {};
     int slot = 0;
     bool used[2] = {false, false};
+    // cached K3 schedules: key {ntiles, d_pad, npairs} -> offset (ints) in buf[kSched]
+    struct Sched { int64_t nt, d_pad, np; int64_t off; int max_slots; };
+    std::vector<Sched> sched;
+    int64_t sched_used = 0;
     // ---- profiling
     bool prof = false;
     bool serial = false;  // profiling level 2: generator on the caller's stream
@@ -55,7 +59,7 @@ namespace {
 enum Buf {
     kX = 0, kY, kNrm, kCoef, kPart, kXbar, kYbar, kU, kZhi, kZlo, kTpart, kT64, kAB, kMask,
     kM, kSconst, kGemmPart, kTileDone, kScal, kSpart, kScratch, kMask1, kInv, kStamps, kK3Stamps,
-    kNumBufs
+    kSched, kNumBufs
 };
 
 hap_status fail(hap_ctx c, hap_status s, const std::string& msg) {
@@ -161,7 +165,6 @@ GemmArgs gemm_args(hap_ctx c, hap_align_info* info) {
     g.n_x = (int)c->n_x;
     g.n_y = (int)c->n_y;
     g.d = (int)c->d;
-    g.nchunks = (int)ceil_div(c->d_pad, kChunkN);
     g.info = info;
     g.ab = B<float2>(c, kAB);
     g.sconst = B<double>(c, kSconst);
@@ -174,6 +177,98 @@ GemmArgs gemm_args(hap_ctx c, hap_align_info* info) {
     if ((g.exp & 16) && ensure(c, kK3Stamps, (size_t)c->sm_count * 64 * 8) == HAP_OK)
         g.stamps = B<long long>(c, kK3Stamps);
     return g;
+}
+
+// Balanced K3 schedule (see k_maskgemm.cu): every pair gets an equal contiguous range of
+// the tile-major column space (multiples of 32), cut into pieces at tile boundaries and at
+// 256 columns; slot = index of the piece within its tile.  Cached per shape; the device
+// copy is stream-ordered after earlier launches on the same stream.
+// A piece's K loop cannot run faster than the stage round trip (TMA + barrier latency over
+// the 3-stage ring): measured ~0.49 us per stage, i.e. the MMA time of a ~196-column piece
+// (K3 piece durations on B200: 15.7 us for widths 32..128, 20.5 us for 256).
+constexpr double kPieceFloor = 4.0 * 196.0;
+
+hap_status get_schedule(hap_ctx c, int64_t nt, int np, cudaStream_t st, GemmArgs& g) {
+    for (auto& e : c->sched)
+        if (e.nt == nt && e.d_pad == c->d_pad && e.np == np) {
+            const int* base = B<int>(c, kSched) + e.off;
+            g.piece_off = base;
+            g.tile_npieces = base + (np + 1);
+            g.pieces = reinterpret_cast<const int4*>(base + round_up(np + 1 + nt, 4));
+            g.max_slots = e.max_slots;
+            return HAP_OK;
+        }
+    // Piece cost model (cycles per K-stage, measured on B200): tensor-bound 4w (8 MMAs of
+    // 128 x w/256 cycles), but never below the stage round-trip floor.  The 256-column chunks of every tile, in tile-major order, are cut into np
+    // consecutive parts of cost <= M (a chunk is split at a multiple of 32 columns only where
+    // a part ends inside it); M is the smallest feasible makespan (binary search).
+    auto cost = [](int64_t w) { return std::max(4.0 * (double)w, kPieceFloor); };
+    std::vector<int64_t> chunks;  // widths, tile-major
+    for (int64_t t = 0; t < nt; ++t)
+        for (int64_t c0 = 0; c0 < c->d_pad; c0 += kChunkN)
+            chunks.push_back(std::min<int64_t>(kChunkN, c->d_pad - c0));
+    auto fill = [&](double M, std::vector<int>* out_pcs, std::vector<int>* out_off,
+                    std::vector<int>* out_npc) {
+        size_t ci = 0;
+        int64_t done = 0, t = 0, c0 = 0;
+        for (int p = 0; p < np; ++p) {
+            if (out_off) (*out_off)[p] = (int)(out_pcs->size() / 4);
+            double used = 0.0;
+            while (ci < chunks.size()) {
+                const int64_t left = chunks[ci] - done;
+                int64_t w = left;
+                if (used + cost(left) > M) {
+                    w = 0;
+                    for (int64_t cand = 32; cand < left; cand += 32)
+                        if (used + cost(cand) <= M) w = cand;
+                    if (w == 0) break;
+                }
+                if (out_pcs) out_pcs->insert(out_pcs->end(), {(int)t, (int)c0, (int)w, (*out_npc)[t]++});
+                used += cost(w);
+                c0 += w;
+                done += w;
+                if (done == chunks[ci]) {
+                    ++ci;
+                    done = 0;
+                    if (c0 >= c->d_pad) { ++t; c0 = 0; }
+                }
+            }
+        }
+        return ci == chunks.size();
+    };
+    double lo = cost(32), hi = 0.0;
+    for (int64_t w : chunks) hi += cost(w);
+    hi += 1.0;
+    for (int it = 0; it < 40; ++it) {
+        const double mid = 0.5 * (lo + hi);
+        if (fill(mid, nullptr, nullptr, nullptr)) hi = mid;
+        else lo = mid;
+    }
+    std::vector<int> off(np + 1, 0), npc(nt, 0), pcs;
+    fill(hi, &pcs, &off, &npc);
+    off[np] = (int)(pcs.size() / 4);
+    int max_slots = 1;
+    for (int v : npc) max_slots = std::max(max_slots, v);
+    std::vector<int> blob(round_up(np + 1 + nt, 4), 0);
+    std::copy(off.begin(), off.end(), blob.begin());
+    std::copy(npc.begin(), npc.end(), blob.begin() + (np + 1));
+    blob.insert(blob.end(), pcs.begin(), pcs.end());
+    const int64_t need = (c->sched_used + (int64_t)blob.size()) * (int64_t)sizeof(int);
+    if (need > (int64_t)c->cap[kSched]) {  // start over in a bigger buffer
+        if (c->last_stream) cudaStreamSynchronize(c->last_stream);
+        c->sched.clear();
+        c->sched_used = 0;
+        hap_status s = ensure(c, kSched, std::max<int64_t>(need, 1 << 20));
+        if (s) return s;
+    }
+    const int64_t at = c->sched_used;
+    cudaError_t e = cudaMemcpyAsync(B<int>(c, kSched) + at, blob.data(), blob.size() * sizeof(int),
+                                    cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // blob is a local vector
+    if (e != cudaSuccess) return cuda_fail(c, e, "schedule upload");
+    c->sched.push_back({nt, c->d_pad, np, at, max_slots});
+    c->sched_used = at + round_up((int64_t)blob.size(), 4);
+    return get_schedule(c, nt, np, st, g);
 }
 
 constexpr int64_t kMaskBudget = 64ll << 20;  // bytes of bf16 mask per launch (L2-resident)
@@ -419,11 +514,12 @@ hap_status hap_permtest(hap_ctx c, hap_align_info* info, const hap_perm_cfg* cfg
     const int64_t tiles_need = std::max<int64_t>(1, ceil_div(total, R - 1));
     const int64_t tiles = std::min(tiles_max, tiles_need);
     const int64_t blk = tiles * (R - 1);
-    const int nchunks = (int)ceil_div(c->d_pad, kChunkN);
+    const int npairs = c->sm_count / pair;
     hap_status s;
     if ((s = ensure(c, kMask, (size_t)tiles * R * c->n_pad * 2)) ||
         (s = ensure(c, kMask1, (size_t)tiles * R * c->n_pad * 2)) ||
-        (s = ensure(c, kGemmPart, (size_t)tiles * nchunks * R * sizeof(float2))) ||
+        (s = ensure(c, kGemmPart, (size_t)tiles * std::max<int64_t>(1, ceil_div(c->d_pad, 32)) * R *
+                                      sizeof(float2))) ||
         (s = ensure(c, kTileDone, (size_t)tiles * sizeof(unsigned))))
         return s;
     if ((s = refresh_maps(c, pair))) return s;
@@ -465,6 +561,8 @@ hap_status hap_permtest(hap_ctx c, hap_align_info* info, const hap_perm_cfg* cfg
         if (e != cudaSuccess) return cuda_fail(c, e, "perm generator");
         g.count = (int)cnt;
         g.ntiles = (int)nt;
+        g.npairs = npairs;
+        if ((s = get_schedule(c, nt, npairs, st, g))) return s;
         g.stats = stats ? stats + 3 * off : nullptr;
         {
             PhaseScope ps(c, HAP_PHASE_MASKGEMM, 1, st);

@@ -70,7 +70,11 @@ struct GemmArgs {
     int n_pad, d_pad, n_x, n_y, d;
     int count;               // valid permutations in this launch
     int ntiles;              // tiles of rows_per_tile mask rows (row 0 = observed split)
-    int nchunks;             // ceil(d_pad / kChunkN)
+    int npairs;              // CTA pairs (grid / pair_mode)
+    const int4* pieces;      // {tile, col0, width, slot} in (tile, col0) order
+    const int* piece_off;    // [npairs + 1] piece range of each pair
+    const int* tile_npieces; // [ntiles] pieces (= partial slots) per tile
+    int max_slots;           // partial slots per tile (stride)
     int rows_per_tile;       // 128 * pair_mode
     double tie_rel;
     hap_align_info* info;
@@ -78,7 +82,7 @@ struct GemmArgs {
     double* stats;           // optional, [count][3]
     const float2* ab;        // [d_pad] {2a, 2b}
     const double* sconst;    // {sum a^2, sum b^2}
-    float2* part;            // [ntiles][nchunks][rows_per_tile] chunk partials {s1, s2}
+    float2* part;            // [ntiles][max_slots][rows_per_tile] piece partials {s1, s2}
     unsigned* tile_done;     // [ntiles] arrival tickets (zero between launches)
     int exp;                 // timing experiments only (HAP_K3_EXPERIMENT), 0 in production
     long long* stamps;       // exp bit 16: [grid][8 units][8 events] globaltimer

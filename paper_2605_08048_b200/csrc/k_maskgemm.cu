@@ -16,7 +16,10 @@
 // Work: a launch covers `ntiles` tiles of R = 128*kPair mask rows; row 0 of every tile is
 // the OBSERVED split {0..n_x-1}, so T_obs is evaluated through exactly the same MMA +
 // epilogue path as every permutation (D7) with no extra launch or dependency.
-// A unit = (tile, 256-column d-chunk); persistent CTA pairs walk the units round-robin.
+// Schedule: the (tile, column) space is cut into one equal contiguous range per CTA pair
+// (multiples of 32 columns), each range into pieces at tile boundaries and at 256 columns
+// (the accumulator width); MMA time is proportional to the width, so the pairs finish
+// together.  A pair walks its pieces in order; every piece runs the full K loop.
 //
 // kPair = 2 (default): a 2-CTA cluster runs tcgen05.mma.cta_group::2 with M = 256: each CTA
 // holds 128 mask rows (A) and half of the chunk's columns (B), so each SM streams half of
@@ -24,7 +27,7 @@
 // Warps: 0 TMA producer, 1 MMA issuer (leader CTA) + TMEM owner, 2-5 epilogue (thread =
 // TMEM lane = one mask row).  The accumulator is double-buffered in TMEM (2 x 256 columns)
 // so unit i+1's MMAs overlap unit i's epilogue.  The last CTA to finish a unit of a tile
-// (atomic ticket) sums the tile's chunk partials in fixed order (deterministic), forms the
+// (atomic ticket) sums the tile's piece partials in column order (deterministic), forms the
 // statistics and counts.
 #include <cmath>
 
@@ -48,14 +51,6 @@ struct Cfg {
     static constexpr size_t kSmem = (size_t)kStages * kStageBytes + 1024 + 256;
 };
 
-// L(r) = log kappa-hat(r), kappa-hat = r(d - r^2)/(1 - r^2), r clamped to [0, 1-1e-9]
-// (Eq. 9 with DESIGN.md R1, R4).
-__device__ __forceinline__ double logkappa(double r, double d) {
-    if (r > 1.0 - 1e-9) r = 1.0 - 1e-9;
-    if (r <= 0.0) return -INFINITY;
-    const double r2 = r * r;
-    return log(r * (d - r2) / (1.0 - r2));  // one log (the oracle sums three: same value)
-}
 
 __device__ __forceinline__ long long gtimer() {
     unsigned long long t;
@@ -73,11 +68,21 @@ struct RowStat {
     double r1, r2, T;
 };
 
-// statistic of one tile row from the chunk partials, summed in ascending chunk order
+// q(r) = kappa-hat(r) = r (d - r^2)/(1 - r^2) with r clamped (R1, R4); L = log q
+__device__ __forceinline__ double kappa_hat(double r, double d) {
+    if (r > 1.0 - 1e-9) r = 1.0 - 1e-9;
+    if (r <= 0.0) return 0.0;
+    const double r2 = r * r;
+    return r * (d - r2) / (1.0 - r2);
+}
+
+// statistic of one tile row from the piece partials, summed in ascending column order;
+// T = L(r2) - L(r1) = log(q(r2)/q(r1)): one log (q = 0 gives the +-inf / both-zero cases)
 __device__ __forceinline__ RowStat row_stat(const GemmArgs& g, int tile, int row) {
     double S1 = g.sconst[0], S2 = g.sconst[1];
-    const float2* p = g.part + (size_t)tile * g.nchunks * g.rows_per_tile + row;
-    for (int c = 0; c < g.nchunks; ++c) {
+    const float2* p = g.part + (size_t)tile * g.max_slots * g.rows_per_tile + row;
+    const int np = g.tile_npieces[tile];
+    for (int c = 0; c < np; ++c) {
         const float2 v = __ldcg(p + (size_t)c * g.rows_per_tile);
         S1 += (double)v.x;
         S2 += (double)v.y;
@@ -85,33 +90,40 @@ __device__ __forceinline__ RowStat row_stat(const GemmArgs& g, int tile, int row
     RowStat s;
     s.r1 = sqrt(fmax(S1, 0.0)) / (double)g.n_x;
     s.r2 = sqrt(fmax(S2, 0.0)) / (double)g.n_y;
-    const double L1 = logkappa(s.r1, (double)g.d), L2 = logkappa(s.r2, (double)g.d);
-    s.T = (isinf(L1) && isinf(L2)) ? 0.0 : L2 - L1;
+    const double q1 = kappa_hat(s.r1, (double)g.d), q2 = kappa_hat(s.r2, (double)g.d);
+    s.T = (q1 == 0.0 && q2 == 0.0) ? 0.0 : (q1 == 0.0 ? INFINITY : log(q2 / q1));
     return s;
 }
 
-// Last CTA of a tile: T_obs from row 0, then every permutation row of the tile.
+// Last CTA of a tile: every thread evaluates the observed row (row 0, identical result in
+// all threads: same partials, same order) and its own permutation rows.
 __device__ void finalize_tile(const GemmArgs& g, int tile, int etid, double* s_tobs) {
     const int R = g.rows_per_tile;
-    if (etid == 0) {
-        const RowStat o = row_stat(g, tile, 0);
-        *s_tobs = o.T;
-        if (tile == 0) {
-            g.info->gemm_r_x = o.r1;
-            g.info->gemm_r_y = o.r2;
-            g.info->gemm_t_obs = o.T;
-        }
+    (void)s_tobs;
+    const RowStat o = row_stat(g, tile, 0);
+    if (tile == 0 && etid == 0) {
+        g.info->gemm_r_x = o.r1;
+        g.info->gemm_r_y = o.r2;
+        g.info->gemm_t_obs = o.T;
     }
-    named_bar_sync(1, 128);
-    const double t_obs = *s_tobs;
+    const double t_obs = o.T;
     const double tau = g.tie_rel * (fabs(g.info->logk_x) + fabs(g.info->logk_y));
     const int lane = etid & 31;
-    for (int row = etid; row < R; row += 128) {
+    constexpr int kRowsPerThread = 2;  // R <= 256 rows over 128 threads
+    RowStat st[kRowsPerThread];
+#pragma unroll
+    for (int j = 0; j < kRowsPerThread; ++j) {
+        const int row = etid + 128 * j;
         const int perm = tile * (R - 1) + row - 1;
-        const bool valid = row >= 1 && perm < g.count;
-        RowStat s{0.0, 0.0, 0.0};
-        if (valid) s = row_stat(g, tile, row);
-        const double T = s.T;
+        const bool valid = row >= 1 && row < R && perm < g.count;
+        st[j] = valid ? row_stat(g, tile, row) : RowStat{0.0, 0.0, 0.0};
+    }
+#pragma unroll
+    for (int j = 0; j < kRowsPerThread; ++j) {
+        const int row = etid + 128 * j;
+        const int perm = tile * (R - 1) + row - 1;
+        const bool valid = row >= 1 && row < R && perm < g.count;
+        const double T = st[j].T;
         const bool ge = valid && (T >= t_obs);
         const bool ab = valid && (fabs(T) >= fabs(t_obs));
         const bool fl = valid && (T == t_obs || fabs(T - t_obs) <= tau || fabs(T) == fabs(t_obs) ||
@@ -126,10 +138,10 @@ __device__ void finalize_tile(const GemmArgs& g, int tile, int etid, double* s_t
             if (bfl) atomicAdd(cnt + 2, (unsigned long long)__popc(bfl));
         }
         if (g.stats && valid) {
-            double* o = g.stats + 3 * (int64_t)perm;
-            o[0] = s.r1;
-            o[1] = s.r2;
-            o[2] = T;
+            double* out = g.stats + 3 * (int64_t)perm;
+            out[0] = st[j].r1;
+            out[1] = st[j].r2;
+            out[2] = T;
         }
     }
     if (etid == 0) g.tile_done[tile] = 0;  // ready for the next launch
@@ -153,12 +165,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     double* s_tobs = reinterpret_cast<double*>(tmem_slot + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) K3_STAMP(7, 0);  // kernel entry
     const uint32_t rank = kPair == 2 ? cluster_ctarank() : 0u;
     const bool leader = rank == 0;
-    const int pair_id = blockIdx.x / kPair, npairs = gridDim.x / kPair;
+    const int pair_id = blockIdx.x / kPair;
     const int nkb = g.n_pad / kKBlock;
-    const int units = g.ntiles * g.nchunks;
     const int R = g.rows_per_tile;
+    // this pair's pieces: a contiguous, equal-width range of the (tile, column) space
+    const int pc_begin = g.piece_off[pair_id], pc_end = g.piece_off[pair_id + 1];
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < C::kStages; ++s) {
@@ -183,18 +197,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     if constexpr (kPair == 2) cluster_sync();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    if (threadIdx.x == 0) K3_STAMP(7, 2);  // setup done
 
     if (warp == 0) {
         // ---------------- TMA producer (both CTAs load their own A rows and B half)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int u = pair_id; u < units; u += npairs) {
-                const int tile = u / g.nchunks, chunk = u % g.nchunks;
-                const int width = min(kChunkN, g.d_pad - chunk * kChunkN);
+            for (int pc = pc_begin; pc < pc_end; ++pc) {
+                const int4 pd = g.pieces[pc];  // {tile, col0, width, slot}
+                const int tile = pd.x, width = pd.z;
                 const int arow = tile * R + (int)rank * kTileM;
-                const int brow = chunk * kChunkN + (int)rank * (width / kPair);
-                const int ui = (u - pair_id) / npairs;
+                const int brow = pd.y + (int)rank * (width / kPair);
+                const int ui = pc - pc_begin;
                 for (int kb = 0; kb < nkb; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1u);
                     if (kb == 0) K3_STAMP(ui, 0);
@@ -227,9 +242,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             int stage = 0;
             uint32_t phase = 0;
             int i = 0;
-            for (int u = pair_id; u < units; u += npairs, ++i) {
-                const int chunk = u % g.nchunks;
-                const int width = min(kChunkN, g.d_pad - chunk * kChunkN);
+            for (int pc = pc_begin; pc < pc_end; ++pc, ++i) {
+                const int width = g.pieces[pc].z;
                 const uint32_t idesc = idesc_bf16_f32(kTileM * kPair, (uint32_t)width);
                 const int a = i & 1;
                 mbar_wait(&tempty[a], (((uint32_t)i >> 1) & 1u) ^ 1u);
@@ -274,16 +288,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             tempty_c[1] = mapa_shared(smem_u32(&tempty[1]), 0);
         }
         int i = 0;
-        for (int u = pair_id; u < units; u += npairs, ++i) {
-            const int tile = u / g.nchunks, chunk = u % g.nchunks;
-            const int width = min(kChunkN, g.d_pad - chunk * kChunkN);
+        for (int pc = pc_begin; pc < pc_end; ++pc, ++i) {
+            const int4 pd = g.pieces[pc];
+            const int tile = pd.x, width = pd.z;
             const int a = i & 1;
             mbar_wait(&tfull[a], ((uint32_t)i >> 1) & 1u);
             tc_fence_after();
             if (etid == 0) K3_STAMP(i, 4);
             // sigma1 = a + acc, sigma2 = b - acc:  |sigma1|^2 - |a|^2 = sum acc (acc + 2a), ...
             float s1 = 0.f, s2 = 0.f;
-            const float4* abp = reinterpret_cast<const float4*>(g.ab + chunk * kChunkN);
+            const float4* abp = reinterpret_cast<const float4*>(g.ab + pd.y);
             for (int cb = 0; cb < ((g.exp & 8) ? 0 : width / 32); ++cb) {
                 uint32_t r[32];
                 tmem_ld_32x32b_x32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(a * kChunkN + 32 * cb),
@@ -306,12 +320,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 else mbar_arrive(&tempty[a]);
             }
             if (etid == 0) K3_STAMP(i, 5);
-            g.part[((size_t)tile * g.nchunks + chunk) * R + trow] = make_float2(s1, s2);
+            g.part[((size_t)tile * g.max_slots + pd.w) * R + trow] = make_float2(s1, s2);
             __threadfence();
             named_bar_sync(1, 128);
             if (etid == 0) {
                 const unsigned old = atomicAdd(g.tile_done + tile, 1u);
-                *s_last = (old == (unsigned)(kPair * g.nchunks - 1)) ? 1 : 0;
+                *s_last = (old == (unsigned)(kPair * g.tile_npieces[tile] - 1)) ? 1 : 0;
             }
             named_bar_sync(1, 128);
             if (*s_last) {
@@ -326,6 +340,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_before();
     __syncthreads();
     if constexpr (kPair == 2) cluster_sync();
+    if (threadIdx.x == 0) K3_STAMP(7, 1);  // all roles done
     if (warp == 1) {
         tc_fence_after();
         if constexpr (kPair == 2) tmem_dealloc_pair<kTmemCols>(tmem);
@@ -344,8 +359,8 @@ cudaError_t launch_impl(const CUtensorMap* tmA, const CUtensorMap* tmBhi, const 
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    const int units = g.ntiles * g.nchunks;
-    const int npairs = std::max(1, std::min(units, sm_count / kPair));
+    const int npairs = g.npairs;
+    (void)sm_count;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)(npairs * kPair));
     cfg.blockDim = dim3(kThreads);
