@@ -151,3 +151,23 @@ def dyadic_pair(rng: np.random.Generator, n_x: int, n_y: int, d: int, ks=(1, 4, 
             m[i, cols] = rng.choice([-1.0, 1.0], size=k) / math.sqrt(k)
         return m
     return rows(n_x), rows(n_y)
+
+
+def varlen_batch(sizes, d: int = 768, seed: int = 1004, theta_deg: float = 30.0,
+                 ny_sizes=None):
+    """Packed varlen batch (C4 recipe): pair p is an independent vMF pair
+    with n_X = sizes[p], n_Y = ny_sizes[p] (default n_X), kappa(r=0.75) for d, mean
+    directions at theta_deg.  Returns (X_packed, cu_nx, Y_packed, cu_ny) with cu_* the
+    int64 prefix offsets [P+1] (FlashAttention-style)."""
+    sizes = [int(s) for s in sizes]
+    ny_sizes = sizes if ny_sizes is None else [int(s) for s in ny_sizes]
+    Xs, Ys = [], []
+    k = kappa_for(d)
+    for p, (nx, ny) in enumerate(zip(sizes, ny_sizes)):
+        X, Y = make_pair(PairSpec(nx, ny, d, k, k, theta_deg, seed=seed), rep=p)
+        Xs.append(X)
+        Ys.append(Y)
+    cu_nx = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    cu_ny = np.concatenate([[0], np.cumsum(ny_sizes)]).astype(np.int64)
+    return (np.ascontiguousarray(np.concatenate(Xs)), cu_nx,
+            np.ascontiguousarray(np.concatenate(Ys)), cu_ny)

@@ -140,6 +140,10 @@ HAP_API hap_status hap_permtest(hap_ctx ctx, hap_align_info* info, const hap_per
 /* ---- many word pairs ------------------------------------------------------------ */
 /* Varlen batch of P independent tests (configs 4/5): pair p has X rows
  * X_packed[cu_nx[p] .. cu_nx[p+1]) and Y rows Y_packed[cu_ny[p] .. cu_ny[p+1]).
+ * Consecutive selected pairs alternate between two internal lanes (own workspaces and
+ * streams, forked from and joined back to `stream`), so one pair's alignment and mask
+ * generation overlap the previous pair's mask-GEMM.  Shape errors of any selected pair
+ * are returned before anything is enqueued.
  *   X_packed, Y_packed [device]; cu_nx, cu_ny [host] int64[P+1] prefix offsets.
  *   pair_sel [host] optional list of the pairs this call handles (NULL = all P); the
  *            others' infos/counts are left untouched (used for multi-GPU sharding).

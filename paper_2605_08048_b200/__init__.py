@@ -290,3 +290,35 @@ class Context:
         if want_stats:
             out["stats"] = stats
         return out
+
+    def permtest_batch(self, X_packed, cu_nx, Y_packed, cu_ny, B: int, seed: int,
+                       stream_id: int = 0, mode: int = 0, tie_rel: float = 1e-6,
+                       pair_sel=None, pair_mode: int = 0, sync: bool = True):
+        """P independent tests of a varlen batch (hap_permtest_batch); pair p draws its
+        permutations from generator stream stream_id + p.  Returns one dict per pair
+        (None for pairs outside pair_sel); a pair whose data failed carries its status."""
+        torch = self.torch
+        P = len(cu_nx) - 1
+        infos = torch.zeros((P, INFO_BYTES), dtype=torch.uint8, device=self.device)
+        counts = torch.zeros((P, COUNTS_WORDS), dtype=torch.int64, device=self.device)
+        cfg = make_cfg(seed, B, 0, B, stream_id, 0, tie_rel, pair_mode)
+        hap_permtest_batch(self.h, X_packed, cu_nx, Y_packed, cu_ny, mode, cfg, infos, counts,
+                           pair_sel)
+        if not sync:
+            return infos, counts
+        hap_sync(self.h)
+        raw = infos.cpu().numpy()
+        cts = counts.cpu().tolist()
+        sel = set(range(P)) if pair_sel is None else set(int(p) for p in pair_sel)
+        out = []
+        for p in range(P):
+            if p not in sel:
+                out.append(None)
+                continue
+            info = hap_align_info.from_buffer_copy(bytes(raw[p].tobytes()))
+            c = cts[p]
+            out.append(dict(status=info.status, t_obs=info.t_obs, r_x=info.r_x, r_y=info.r_y,
+                            gemm_t_obs=info.gemm_t_obs, is_identity=bool(info.is_identity),
+                            exceed_ge=c[0], exceed_abs=c[1], flagged=c[2], B=B,
+                            p_value=hap_pvalue(c[0], B), p_two_sided=hap_pvalue(c[1], B)))
+        return out

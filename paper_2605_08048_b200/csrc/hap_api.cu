@@ -39,6 +39,11 @@ struct hap_ctx_s {
     cudaEvent_t ev_fork = nullptr, ev_ready[2] = {}, ev_free[2] = {};
     int slot = 0;
     bool used[2] = {false, false};
+    // batch pipeline: two sub-contexts (own workspaces + generator streams) on two
+    // internal streams forked from / joined to the caller's stream
+    hap_ctx sub[2] = {nullptr, nullptr};
+    cudaStream_t sub_stream[2] = {nullptr, nullptr};
+    cudaEvent_t ev_sub[2] = {nullptr, nullptr};
     // cached K3 schedules: key {ntiles, d_pad, npairs} -> offset (ints) in buf[kSched]
     struct Sched { int64_t nt, d_pad, np; int64_t off; int max_slots; };
     std::vector<Sched> sched;
@@ -371,6 +376,11 @@ hap_status hap_destroy(hap_ctx c) {
         cudaStreamSynchronize(c->side);
         cudaStreamDestroy(c->side);
     }
+    for (int i = 0; i < 2; ++i) {
+        if (c->sub[i]) hap_destroy(c->sub[i]);
+        if (c->sub_stream[i]) cudaStreamDestroy(c->sub_stream[i]);
+        if (c->ev_sub[i]) cudaEventDestroy(c->ev_sub[i]);
+    }
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     for (int i = 0; i < 2; ++i) {
         if (c->ev_ready[i]) cudaEventDestroy(c->ev_ready[i]);
@@ -583,20 +593,60 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
     if (!c) return HAP_E_INVALID_ARG;
     if (P < 0 || !X_packed || !Y_packed || !cu_nx || !cu_ny || !cfg || !infos || !counts)
         return fail(c, HAP_E_INVALID_ARG, "null pointer / negative P");
+    if (pair_sel && n_sel < 0) return fail(c, HAP_E_INVALID_ARG, "n_sel < 0");
+    if (!is_device_ptr(X_packed) || !is_device_ptr(Y_packed))
+        return fail(c, HAP_E_INVALID_ARG, "X_packed / Y_packed must be device memory");
     const int64_t n = pair_sel ? n_sel : P;
+    // shape checks are synchronous: validate every selected pair before enqueuing anything
     for (int64_t i = 0; i < n; ++i) {
         const int64_t p = pair_sel ? pair_sel[i] : i;
         if (p < 0 || p >= P) return fail(c, HAP_E_INVALID_ARG, "pair_sel out of range");
         const int64_t nx = cu_nx[p + 1] - cu_nx[p], ny = cu_ny[p + 1] - cu_ny[p];
-        hap_status s = hap_align(c, X_packed + cu_nx[p] * d, nx, Y_packed + cu_ny[p] * d, ny, d, mode,
-                                 infos + p, stream);
-        if (s) return s;
-        hap_perm_cfg pc = *cfg;
-        pc.stream_id = cfg->stream_id + (uint32_t)p;
-        s = hap_permtest(c, infos + p, &pc, counts + p, nullptr, stream);
-        if (s) return s;
+        if (nx < 1 || ny < 1 || nx + ny > 65535)
+            return fail(c, HAP_E_INVALID_ARG, "pair " + std::to_string(p) + ": bad n_x / n_y");
     }
-    return HAP_OK;
+    if (d < 2 || d > 16384) return fail(c, HAP_E_DIM_MISMATCH, "need 2 <= d <= 16384");
+    cudaSetDevice(c->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    for (int k = 0; k < 2; ++k) {
+        if (!c->sub[k]) {
+            hap_status s = hap_create(c->device, &c->sub[k]);
+            if (s) return fail(c, s, "sub-context");
+            c->sub[k]->prof = c->prof;
+            c->sub[k]->serial = c->serial;
+        }
+        if (!c->sub_stream[k] &&
+            (cudaStreamCreateWithFlags(&c->sub_stream[k], cudaStreamNonBlocking) != cudaSuccess ||
+             cudaEventCreateWithFlags(&c->ev_sub[k], cudaEventDisableTiming) != cudaSuccess))
+            return fail(c, HAP_E_CUDA, "batch streams");
+    }
+    // fork: the two lanes start after the work already on the caller's stream
+    cudaError_t e = cudaEventRecord(c->ev_fork, st);
+    for (int k = 0; k < 2 && e == cudaSuccess; ++k) e = cudaStreamWaitEvent(c->sub_stream[k], c->ev_fork, 0);
+    if (e != cudaSuccess) return cuda_fail(c, e, "batch fork");
+    hap_status s = HAP_OK;
+    for (int64_t i = 0; i < n && !s; ++i) {
+        const int64_t p = pair_sel ? pair_sel[i] : i;
+        const int k = (int)(i & 1);  // consecutive pairs alternate between the two lanes
+        hap_ctx w = c->sub[k];
+        const int64_t nx = cu_nx[p + 1] - cu_nx[p], ny = cu_ny[p + 1] - cu_ny[p];
+        s = hap_align(w, X_packed + cu_nx[p] * d, nx, Y_packed + cu_ny[p] * d, ny, d, mode, infos + p,
+                      c->sub_stream[k]);
+        if (!s) {
+            hap_perm_cfg pc = *cfg;
+            pc.stream_id = cfg->stream_id + (uint32_t)p;
+            s = hap_permtest(w, infos + p, &pc, counts + p, nullptr, c->sub_stream[k]);
+        }
+        if (s) c->err = "pair " + std::to_string(p) + ": " + w->err;
+    }
+    // join: the caller's stream waits for both lanes (also on error, to keep ordering sane)
+    for (int k = 0; k < 2; ++k) {
+        if (cudaEventRecord(c->ev_sub[k], c->sub_stream[k]) == cudaSuccess)
+            cudaStreamWaitEvent(st, c->ev_sub[k], 0);
+    }
+    c->last_stream = st;
+    c->last_info = nullptr;  // per-pair data errors are reported in infos[p].status
+    return s;
 }
 
 hap_status hap_profile(hap_ctx c, int enable) {
@@ -604,6 +654,8 @@ hap_status hap_profile(hap_ctx c, int enable) {
     c->prof = enable != 0;
     c->serial = enable >= 2;
     c->stamp_k1 = enable >= 3;
+    for (hap_ctx w : c->sub)
+        if (w) hap_profile(w, enable);
     return HAP_OK;
 }
 
@@ -641,9 +693,19 @@ hap_status hap_profile_read(hap_ctx c, double* ms, int64_t* launches, int reset)
         c->pool.push_back(m.b);
     }
     c->marks.clear();
+    double sub_ms[HAP_NUM_PHASES] = {}, sub_sum_ms[HAP_NUM_PHASES] = {};
+    int64_t sub_n[HAP_NUM_PHASES] = {}, sub_sum_n[HAP_NUM_PHASES] = {};
+    for (hap_ctx w : c->sub)
+        if (w) {
+            hap_profile_read(w, sub_ms, sub_n, reset);
+            for (int p = 0; p < HAP_NUM_PHASES; ++p) {
+                sub_sum_ms[p] += sub_ms[p];
+                sub_sum_n[p] += sub_n[p];
+            }
+        }
     for (int p = 0; p < HAP_NUM_PHASES; ++p) {
-        if (ms) ms[p] = c->ms[p];
-        if (launches) launches[p] = c->launches[p];
+        if (ms) ms[p] = c->ms[p] + sub_sum_ms[p];
+        if (launches) launches[p] = c->launches[p] + sub_sum_n[p];
         if (reset) {
             c->ms[p] = 0.0;
             c->launches[p] = 0;

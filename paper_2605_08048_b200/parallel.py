@@ -87,3 +87,40 @@ def gpu_range_runner(ctx, X, Y, B: int, seed: int, stream_id: int = 0, mode: int
         return ctx.counts.cpu().numpy()
     del torch
     return run
+
+
+def gpu_batch_sharded(ctx, X_packed, cu_nx, Y_packed, cu_ny, B: int, seed: int, rank: int,
+                      world: int, stream_id: int = 0, mode: int = 0, group=None,
+                      reduce: bool = True):
+    """Configs C4/C5 on the CUDA library: the pairs are LPT-assigned by cost N_p, each rank
+    runs its share with ONE hap_permtest_batch call (pair_sel), and one all_reduce(SUM) on
+    the device combines int64[P, INFO_WORDS + 3] = the bit-cast hap_align_info rows plus
+    the counts (every row is written by exactly one rank, the rest are zero, so the sum
+    reproduces the bits).  Returns (infos uint8[P, INFO_BYTES], counts int64[P, 3]) on the
+    device, identical on every rank and for every world size."""
+    import paper_2605_08048_b200 as hap
+    import torch
+
+    P = len(cu_nx) - 1
+    assert hap.INFO_BYTES % 8 == 0
+    iw = hap.INFO_BYTES // 8
+    cnx = np.asarray(cu_nx, dtype=np.int64)
+    cny = np.asarray(cu_ny, dtype=np.int64)
+    costs = (cnx[1:] - cnx[:-1]) + (cny[1:] - cny[:-1])
+    mine = lpt_assign(costs.tolist(), world)[rank]
+    buf = torch.zeros((P, iw + 3), dtype=torch.int64, device=ctx.device)
+    infos = buf[:, :iw]
+    counts = buf[:, iw:]
+    cfg = hap.make_cfg(seed, B, 0, B, stream_id)
+    if mine:
+        # infos / counts are row-strided views: the C ABI takes dense arrays, so stage them
+        inf_d = torch.zeros((P, hap.INFO_BYTES), dtype=torch.uint8, device=ctx.device)
+        cnt_d = torch.zeros((P, 3), dtype=torch.int64, device=ctx.device)
+        hap.hap_permtest_batch(ctx.h, X_packed, cnx, Y_packed, cny, mode, cfg, inf_d, cnt_d,
+                               pair_sel=mine, stream=torch.cuda.current_stream(ctx.device))
+        infos.copy_(inf_d.view(torch.int64))
+        counts.copy_(cnt_d)
+    if world > 1 and reduce:
+        import torch.distributed as dist
+        dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+    return buf[:, :iw].contiguous().view(torch.uint8), buf[:, iw:].contiguous()

@@ -269,3 +269,89 @@ def test_host_inputs_match_device_inputs(ctx):
                           want_stats=True)
     assert np.array_equal(a["stats"].cpu().numpy(), b["stats"].cpu().numpy())
     assert a["exceed_ge"] == b["exceed_ge"]
+
+
+# ------------------------------------------------------------------ varlen batch
+def _batch_vs_oracle(orc, res, Xp, cnx, Yp, cny, B, s0, sel):
+    for p in sel:
+        X = Xp[cnx[p]:cnx[p + 1]]
+        Y = Yp[cny[p]:cny[p + 1]]
+        ref = orc.run_pair(X, Y, B, SEED, s=s0 + p)
+        g = res[p]
+        assert g["status"] == 0
+        Ls = abs(ref["L_x"]) + abs(ref["L_y"])
+        assert abs(g["t_obs"] - ref["t_obs"]) <= 1e-10 * Ls
+        assert math.isclose(g["r_x"], ref["r_x"], rel_tol=1e-10)
+        assert abs(g["gemm_t_obs"] - ref["t_obs"]) <= 1e-5 * Ls
+        for k in ("exceed_ge", "exceed_abs"):
+            assert abs(g[k] - ref[k]) <= ref["flagged"], (p, k, g[k], ref[k])
+
+
+def test_batch_varlen_matches_oracle(ctx, orc):
+    """hap_permtest_batch over a ragged batch (C4 recipe, small B): every pair agrees
+    with the oracle run on generator stream stream_id + p, and is bitwise identical to
+    the same pair run alone through hap_permtest."""
+    sizes = [50, 300, 7, 129, 1000, 64, 2]
+    ny = [60, 250, 9, 128, 1000, 64, 3]
+    Xp, cnx, Yp, cny = HI.varlen_batch(sizes, d=96, ny_sizes=ny)
+    B, s0 = 700, 11
+    res = ctx.permtest_batch(_cuda(Xp), cnx, _cuda(Yp), cny, B, SEED, stream_id=s0)
+    _batch_vs_oracle(orc, res, Xp, cnx, Yp, cny, B, s0, range(len(sizes)))
+    for p in (1, 4):
+        one = ctx.permtest_pair(_cuda(Xp[cnx[p]:cnx[p + 1]]), _cuda(Yp[cny[p]:cny[p + 1]]), B,
+                                SEED, stream_id=s0 + p)
+        for k in ("t_obs", "gemm_t_obs", "exceed_ge", "exceed_abs", "flagged"):
+            assert one[k] == res[p][k], (p, k)
+
+
+def test_batch_config4_slice(ctx, orc):
+    """A slice of C4 at full size (d=768, B=10^4, log-uniform n): counts vs oracle."""
+    sizes = HI.c4_sizes(10000)[:4]
+    Xp, cnx, Yp, cny = HI.varlen_batch(sizes, d=768)
+    res = ctx.permtest_batch(_cuda(Xp), cnx, _cuda(Yp), cny, 10000, SEED, stream_id=0)
+    _batch_vs_oracle(orc, res, Xp, cnx, Yp, cny, 10000, 0, range(len(sizes)))
+
+
+def test_batch_pair_sel_and_data_errors(hap, ctx, orc):
+    """pair_sel runs only the selected pairs (others untouched); a pair with a zero row
+    reports its own status and the batch continues; shape errors are synchronous."""
+    import torch
+    sizes = [40, 33, 80, 20, 55]
+    Xp, cnx, Yp, cny = HI.varlen_batch(sizes, d=64)
+    Xp[cnx[2] + 5] = 0.0                       # pair 2: ZeroVector
+    sel = [4, 2, 0]
+    res = ctx.permtest_batch(_cuda(Xp), cnx, _cuda(Yp), cny, 300, SEED, stream_id=3,
+                             pair_sel=sel)
+    assert res[1] is None and res[3] is None
+    assert res[2]["status"] == 3 and res[2]["exceed_ge"] == 0
+    _batch_vs_oracle(orc, res, Xp, cnx, Yp, cny, 300, 3, [4, 0])
+    infos, counts = ctx.permtest_batch(_cuda(Xp), cnx, _cuda(Yp), cny, 300, SEED,
+                                       pair_sel=sel, sync=False)
+    hap.hap_sync(ctx.h)
+    assert counts[1].abs().sum().item() == 0 and counts[3].abs().sum().item() == 0
+    assert int(infos[1].to(torch.int64).sum()) == 0
+    bad = cnx.copy()
+    bad[3] = bad[2]                            # pair 2 gets n_x = 0
+    with pytest.raises(hap.HapError):
+        ctx.permtest_batch(_cuda(Xp), bad, _cuda(Yp), cny, 300, SEED)
+
+
+def test_gpu_batch_sharded_world_invariant(ctx):
+    """gpu_batch_sharded: the per-rank shares of a 3-way split (combined here by hand,
+    as the all_reduce would) equal the world-1 result bit for bit."""
+    import torch
+    from paper_2605_08048_b200 import parallel
+    sizes = [30, 200, 75, 12, 90, 140]
+    Xp, cnx, Yp, cny = HI.varlen_batch(sizes, d=128)
+    X, Y = _cuda(Xp), _cuda(Yp)
+    i1, c1 = parallel.gpu_batch_sharded(ctx, X, cnx, Y, cny, 500, SEED, 0, 1, stream_id=5)
+    acc_i = torch.zeros((len(sizes), i1.shape[1] // 8), dtype=torch.int64, device=X.device)
+    acc_c = torch.zeros_like(c1)
+    for r in range(3):
+        ir, cr = parallel.gpu_batch_sharded(ctx, X, cnx, Y, cny, 500, SEED, r, 3, stream_id=5,
+                                            reduce=False)
+        acc_i += ir.view(torch.int64)
+        acc_c += cr
+    torch.cuda.synchronize()
+    assert torch.equal(acc_c, c1)
+    assert torch.equal(acc_i.view(torch.uint8), i1)
