@@ -184,10 +184,25 @@ HAP_API hap_status hap_profile_k1_phases(hap_ctx ctx, double* us);
 /* Development aid: with HAP_K3_EXPERIMENT bit 16 set in the environment, K3 records
  * globaltimer stamps [sm_count][8 units][8 events]; copies up to n int64 into out [host]. */
 HAP_API hap_status hap_debug_k3_stamps(hap_ctx ctx, long long* out, int64_t n);
+/* Debug (profiling level 3): raw K1 timestamps, [8] kernel phases of CTA 0 then [grid][8]
+ * per-CTA events (entry, P1 done, barrier 1 passed, P2 done, P3 done, P4 coefficients done,
+ * P4 done, exit); out holds n int64 (at most 8 + 8 * SM count are written). */
+HAP_API hap_status hap_debug_k1_stamps(hap_ctx ctx, long long* out, int64_t n);
 /* Timeline of the launches timed since the last read/reset (profiling on): out [host]
  * max_n * 3 doubles {phase, start_us, end_us} relative to the first recorded launch, in
  * record order; *n receives the count.  Consumes the records (like hap_profile_read). */
 HAP_API hap_status hap_profile_timeline(hap_ctx ctx, double* out, int64_t max_n, int64_t* n);
+
+/* Kernel spans: with enable != 0 every kernel launched afterwards (by this context and its
+ * batch lanes) records {first CTA entry, last CTA exit} with the device's global timer, so
+ * concurrent launches on different streams can be laid on one timeline without the event
+ * records of hap_profile between them.  hap_profile_spans_read synchronises the device and
+ * writes, per launch in issue order, [host] out[3k] = phase + HAP_NUM_PHASES * lane (lane 0
+ * = this context, 1 and 2 = batch lanes), out[3k+1], out[3k+2] = start, end in us relative
+ * to the earliest start (-1 for a kernel that returned before the exit stamp); *n = number
+ * of launches recorded (at most 8192 per read), then resets. */
+HAP_API hap_status hap_profile_spans(hap_ctx ctx, int enable);
+HAP_API hap_status hap_profile_spans_read(hap_ctx ctx, double* out, int64_t max_n, int64_t* n);
 
 /* ---- introspection for parity tests (same kernels as the hot path) -------------- */
 /* PERM-SPEC v1 sets for b in [b_begin, b_begin+count): out [device] count*N uint8

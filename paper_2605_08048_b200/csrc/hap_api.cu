@@ -57,6 +57,9 @@ struct hap_ctx_s {
     std::vector<cudaEvent_t> pool;
     int64_t launches[HAP_NUM_PHASES] = {};
     double ms[HAP_NUM_PHASES] = {};
+    // kernel spans (hap_profile_spans): device {entry, exit} pairs, phase of each slot
+    bool spans = false;
+    std::vector<int> span_phase;
 };
 
 namespace {
@@ -64,7 +67,7 @@ namespace {
 enum Buf {
     kX = 0, kY, kNrm, kCoef, kPart, kXbar, kYbar, kU, kZhi, kZlo, kTpart, kT64, kAB, kMask,
     kM, kSconst, kGemmPart, kTileDone, kScal, kSpart, kScratch, kMask1, kInv, kStamps, kK3Stamps,
-    kSched, kNumBufs
+    kSched, kSpans, kNumBufs
 };
 
 hap_status fail(hap_ctx c, hap_status s, const std::string& msg) {
@@ -314,6 +317,29 @@ struct PhaseScope {
     }
 };
 
+constexpr int64_t kMaxSpans = 8192;
+
+hap_status reset_spans(hap_ctx c) {
+    hap_status s = ensure(c, kSpans, (size_t)kMaxSpans * 16);
+    if (s) return s;
+    std::vector<unsigned long long> init(2 * kMaxSpans);
+    for (int64_t i = 0; i < kMaxSpans; ++i) {
+        init[2 * i] = ~0ull;
+        init[2 * i + 1] = 0ull;
+    }
+    cudaError_t e = cudaMemcpy(c->buf[kSpans], init.data(), init.size() * 8, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(c, e, "span reset");
+    c->span_phase.clear();
+    return HAP_OK;
+}
+
+// device slot for the next launch of `phase` (nullptr when span profiling is off / full)
+unsigned long long* next_span(hap_ctx c, int phase) {
+    if (!c->spans || (int64_t)c->span_phase.size() >= kMaxSpans) return nullptr;
+    c->span_phase.push_back(phase);
+    return B<unsigned long long>(c, kSpans) + 2 * (c->span_phase.size() - 1);
+}
+
 }  // namespace
 
 extern "C" {
@@ -436,7 +462,7 @@ hap_status hap_align(hap_ctx c, const float* X, int64_t n_x, const float* Y, int
         (s = ensure(c, kInv, N * 8)) || (s = ensure(c, kU, d_pad * 8)) ||
         (s = ensure(c, kZhi, (size_t)zt_rows(d_pad) * n_pad * 2)) ||
         (s = ensure(c, kZlo, (size_t)zt_rows(d_pad) * n_pad * 2)) ||
-        (s = ensure(c, kTpart, (size_t)(n_pad / kRowTile) * d_pad * 8)) ||
+        (s = ensure(c, kTpart, (size_t)(2 * d + d_pad) * 8)) ||
         (s = ensure(c, kT64, d_pad * 8)) || (s = ensure(c, kAB, d_pad * 8)) ||
         (s = ensure(c, kM, d_pad * 8)) || (s = ensure(c, kSconst, 16)) ||
         (s = ensure(c, kMask, (size_t)2 * kTileM * n_pad * 2)))
@@ -483,14 +509,16 @@ hap_status hap_align(hap_ctx c, const float* X, int64_t n_x, const float* Y, int
     a.spart = B<double>(c, kSpart);
     a.scratch = B<long long>(c, kScratch);
     a.stamps = nullptr;
-    if (c->stamp_k1 && ensure(c, kStamps, 64) == HAP_OK) a.stamps = B<long long>(c, kStamps);
+    if (c->stamp_k1 && ensure(c, kStamps, (size_t)(8 + 8 * grid) * 8) == HAP_OK)
+        a.stamps = B<long long>(c, kStamps);
     a.zt_hi = B<uint16_t>(c, kZhi);
     a.zt_lo = B<uint16_t>(c, kZlo);
-    a.tpart = B<double>(c, kTpart);
+    a.acc = B<long long>(c, kTpart);
     a.t64 = B<double>(c, kT64);
     a.m = B<double>(c, kM);
     a.ab = B<float2>(c, kAB);
     a.sconst = B<double>(c, kSconst);
+    a.span = next_span(c, HAP_PHASE_ALIGN);
     cudaError_t e;
     {
         PhaseScope ps(c, HAP_PHASE_ALIGN, kAlignLaunches, st);
@@ -558,7 +586,11 @@ hap_status hap_permtest(hap_ctx c, hap_align_info* info, const hap_perm_cfg* cfg
         pa.out_kind = kMaskBf16Row;
         pa.rows_per_tile = (int)R;
         pa.ntiles = (int)nt;
-        pa.max_ctas_per_sm = 0;
+        {
+            static const char* cap = getenv("HAP_K2_MAX_CTAS");  // scheduling experiments
+            pa.max_ctas_per_sm = cap ? atoi(cap) : 0;
+        }
+        pa.span = next_span(c, HAP_PHASE_PERMGEN);
         // K2 on the side stream; a slot is rewritten only after the K3 that read it
         cudaStream_t gs = c->serial ? st : c->side;
         e = (c->used[slot] && !c->serial) ? cudaStreamWaitEvent(gs, c->ev_free[slot], 0) : cudaSuccess;
@@ -574,6 +606,7 @@ hap_status hap_permtest(hap_ctx c, hap_align_info* info, const hap_perm_cfg* cfg
         g.npairs = npairs;
         if ((s = get_schedule(c, nt, npairs, st, g))) return s;
         g.stats = stats ? stats + 3 * off : nullptr;
+        g.span = next_span(c, HAP_PHASE_MASKGEMM);
         {
             PhaseScope ps(c, HAP_PHASE_MASKGEMM, 1, st);
             e = launch_maskgemm(&c->tmA[slot], &c->tmBhi, &c->tmBlo, g, pair, c->sm_count, st);
@@ -649,6 +682,57 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
     return s;
 }
 
+hap_status hap_profile_spans(hap_ctx c, int enable) {
+    if (!c) return HAP_E_INVALID_ARG;
+    cudaSetDevice(c->device);
+    if (enable) {
+        hap_status s = reset_spans(c);
+        if (s) return s;
+    }
+    c->spans = enable != 0;
+    for (hap_ctx w : c->sub)
+        if (w) {
+            hap_status s = hap_profile_spans(w, enable);
+            if (s) return s;
+        }
+    return HAP_OK;
+}
+
+hap_status hap_profile_spans_read(hap_ctx c, double* out, int64_t max_n, int64_t* n) {
+    if (!c || !n) return HAP_E_INVALID_ARG;
+    cudaSetDevice(c->device);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(c, e, "span read");
+    hap_ctx lanes[3] = {c, c->sub[0], c->sub[1]};
+    struct Rec { int code; unsigned long long a, b; };
+    std::vector<Rec> recs;
+    for (int lane = 0; lane < 3; ++lane) {
+        hap_ctx w = lanes[lane];
+        if (!w || !w->spans || w->span_phase.empty()) continue;
+        std::vector<unsigned long long> h(2 * w->span_phase.size());
+        e = cudaMemcpy(h.data(), w->buf[kSpans], h.size() * 8, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) return cuda_fail(c, e, "span read");
+        for (size_t i = 0; i < w->span_phase.size(); ++i)
+            recs.push_back({w->span_phase[i] + HAP_NUM_PHASES * lane, h[2 * i], h[2 * i + 1]});
+        hap_status s = reset_spans(w);
+        if (s) return s;
+    }
+    unsigned long long t0 = ~0ull;
+    for (auto& r : recs)
+        if (r.b) t0 = std::min(t0, r.a);
+    int64_t k = 0;
+    for (auto& r : recs) {
+        if (out && k < max_n) {
+            out[3 * k + 0] = r.code;
+            out[3 * k + 1] = r.b ? 1e-3 * (double)(r.a - t0) : -1.0;  // -1: kernel exited early
+            out[3 * k + 2] = r.b ? 1e-3 * (double)(r.b - t0) : -1.0;
+        }
+        ++k;
+    }
+    *n = k;
+    return HAP_OK;
+}
+
 hap_status hap_profile(hap_ctx c, int enable) {
     if (!c) return HAP_E_INVALID_ARG;
     c->prof = enable != 0;
@@ -664,6 +748,15 @@ hap_status hap_debug_k3_stamps(hap_ctx c, long long* out, int64_t n) {
     cudaDeviceSynchronize();
     const size_t bytes = std::min<size_t>((size_t)n * 8, (size_t)c->sm_count * 64 * 8);
     if (cudaMemcpy(out, c->buf[kK3Stamps], bytes, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return HAP_E_CUDA;
+    return HAP_OK;
+}
+
+hap_status hap_debug_k1_stamps(hap_ctx c, long long* out, int64_t n) {
+    if (!c || !out || !c->buf[kStamps]) return HAP_E_INVALID_ARG;
+    cudaDeviceSynchronize();
+    const size_t bytes = std::min<size_t>((size_t)n * 8, (size_t)(8 + 8 * c->sm_count) * 8);
+    if (cudaMemcpy(out, c->buf[kStamps], bytes, cudaMemcpyDeviceToHost) != cudaSuccess)
         return HAP_E_CUDA;
     return HAP_OK;
 }
@@ -717,27 +810,42 @@ hap_status hap_profile_read(hap_ctx c, double* ms, int64_t* launches, int reset)
 hap_status hap_profile_timeline(hap_ctx c, double* out, int64_t max_n, int64_t* n) {
     if (!c || !n) return HAP_E_INVALID_ARG;
     cudaSetDevice(c->device);
+    // lane 0 = this context, lanes 1, 2 = the batch sub-contexts; one common time base
+    hap_ctx lanes[3] = {c, c->sub[0], c->sub[1]};
+    cudaEvent_t t0 = nullptr;
+    for (hap_ctx w : lanes)
+        if (w && !w->marks.empty() && !t0) t0 = w->marks.front().a;
     int64_t k = 0;
-    cudaEvent_t t0 = c->marks.empty() ? nullptr : c->marks.front().a;
-    for (auto& m : c->marks) {
-        float ta = 0.f, tb = 0.f;
-        cudaError_t e = cudaEventSynchronize(m.b);
-        if (e == cudaSuccess) e = cudaEventElapsedTime(&ta, t0, m.a);
-        if (e == cudaSuccess) e = cudaEventElapsedTime(&tb, t0, m.b);
-        if (e != cudaSuccess) return cuda_fail(c, e, "profile timeline");
-        if (out && k < max_n) {
-            out[3 * k + 0] = m.phase;
-            out[3 * k + 1] = 1e3 * ta;
-            out[3 * k + 2] = 1e3 * tb;
+    double tmin = 0.0;
+    for (int lane = 0; lane < 3; ++lane) {
+        hap_ctx w = lanes[lane];
+        if (!w) continue;
+        for (auto& m : w->marks) {
+            float ta = 0.f, tb = 0.f;
+            cudaError_t e = cudaEventSynchronize(m.b);
+            if (e == cudaSuccess) e = cudaEventElapsedTime(&ta, t0, m.a);
+            if (e == cudaSuccess) e = cudaEventElapsedTime(&tb, t0, m.b);
+            if (e != cudaSuccess) return cuda_fail(c, e, "profile timeline");
+            if (out && k < max_n) {
+                out[3 * k + 0] = m.phase + HAP_NUM_PHASES * lane;
+                out[3 * k + 1] = 1e3 * ta;
+                out[3 * k + 2] = 1e3 * tb;
+            }
+            tmin = std::min(tmin, 1e3 * (double)ta);
+            ++k;
+            w->ms[m.phase] += tb - ta;
         }
-        ++k;
-        c->ms[m.phase] += tb - ta;
+        for (auto& m : w->marks) {
+            w->pool.push_back(m.a);
+            w->pool.push_back(m.b);
+        }
+        w->marks.clear();
     }
-    for (auto& m : c->marks) {
-        c->pool.push_back(m.a);
-        c->pool.push_back(m.b);
-    }
-    c->marks.clear();
+    if (out)
+        for (int64_t i = 0; i < std::min(k, max_n); ++i) {
+            out[3 * i + 1] -= tmin;
+            out[3 * i + 2] -= tmin;
+        }
     *n = k;
     return HAP_OK;
 }

@@ -13,6 +13,20 @@ namespace hap {
 HAP_DEV uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+// kernel span profiling: {min entry, max exit} %globaltimer over CTAs (one clock for all
+// kernels and streams, so concurrent launches can be laid on one timeline)
+HAP_DEV unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+HAP_DEV void span_enter(unsigned long long* span) {
+    if (span) atomicMin(span, global_ns());
+}
+HAP_DEV void span_exit(unsigned long long* span) {
+    if (span) atomicMax(span + 1, global_ns());
+}
+
 HAP_DEV uint32_t lane_id() { return threadIdx.x & 31u; }
 HAP_DEV uint32_t warp_id() { return __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0); }
 HAP_DEV bool elect_one() {

@@ -12,8 +12,6 @@ namespace hap {
 constexpr int kKBlock = 64;     // GEMM K-block: 64 bf16 = one 128-byte swizzle atom
 constexpr int kTileM = 128;     // permutations per CTA tile (TMEM lanes)
 constexpr int kChunkN = 256;    // d-columns per accumulator chunk (UMMA N <= 256)
-constexpr int kRowBlock = 16;   // rows per column-partial block in K1a
-constexpr int kRowTile = 32;    // pooled rows per reflect/split tile in K1 (P4)
 
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 inline int64_t ceil_div(int64_t x, int64_t m) { return (x + m - 1) / m; }
@@ -38,12 +36,21 @@ struct AlignArgs {
     uint16_t* zt_hi;         // [>=d_pad][n_pad] bf16 bits
     uint16_t* zt_lo;         // [>=d_pad][n_pad]
     double* m;               // [d_pad] centre (multiple of 2^-12): planes hold z - m
-    double* tpart;           // [n_pad/kRowTile][d_pad] fp64 partials of t' = sum (hi + lo)
+    long long* acc;          // [2 d + d_pad] fixed-point column sums (zero between launches)
     double* t64;             // [d_pad] t = N m + t'
     float2* ab;              // [d_pad] epilogue constants {2a, 2b}, a = n_x m, b = t - a
     double* sconst;          // [2]     {sum a^2, sum b^2}
     long long* stamps;       // optional [8] globaltimer after each K1 phase (profiling)
+    unsigned long long* span;  // optional {first CTA entry, last CTA exit} globaltimer
 };
+// item geometry of K1: R pooled rows x all d columns as an fp32 smem tile of pitch P
+struct AlignGeom {
+    int rows, pitch;
+    bool stage_umc;    // per-column (u_c, m_c) staged in smem
+    bool stage_means;  // xbar, ybar also staged in smem
+    size_t smem;       // dynamic smem bytes
+};
+AlignGeom align_geometry(int64_t d);
 // one cooperative kernel of `grid` CTAs (one per SM); scratch[2] holds its grid barrier
 cudaError_t launch_align(const AlignArgs& a, int grid, cudaStream_t st);
 constexpr int kAlignLaunches = 1;  // kernels issued by launch_align
@@ -62,6 +69,7 @@ struct PermArgs {
                              // row t*R = observed split {0..n_x-1} for t < ntiles
     int ntiles;
     int max_ctas_per_sm;     // 0 = occupancy limit
+    unsigned long long* span;  // optional {first CTA entry, last CTA exit} globaltimer
 };
 cudaError_t launch_perm(const PermArgs& a, int sm_count, cudaStream_t st);
 
@@ -86,6 +94,7 @@ struct GemmArgs {
     unsigned* tile_done;     // [ntiles] arrival tickets (zero between launches)
     int exp;                 // timing experiments only (HAP_K3_EXPERIMENT), 0 in production
     long long* stamps;       // exp bit 16: [grid][8 units][8 events] globaltimer
+    unsigned long long* span;  // optional {first CTA entry, last CTA exit} globaltimer
 };
 int maskgemm_b_rows(int pair_mode);  // B tile rows per CTA (TMA box)
 cudaError_t launch_maskgemm(const CUtensorMap* tmA, const CUtensorMap* tmBhi,

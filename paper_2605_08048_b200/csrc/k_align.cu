@@ -9,22 +9,26 @@
 //   S6 observed    r_X = ||xbar|| (= r(X')), r_Y, T_obs (Eq. 10), fp64
 //
 // The problem is small (C2: 6 MB) and a chain of dependent reductions, so the cost is
-// latency, not bandwidth: one persistent cooperative grid (one CTA per SM) runs the five
-// phases below separated by four software grid barriers.  Every reduction is fixed-order
-// (per-CTA partials combined in ascending CTA order by a warp xor-tree or a block tree), so
-// Z~ and t are bit-identical across runs and ranks; scalars needed by every CTA are reduced
-// redundantly by every CTA from the same partials (identical results, no broadcast).
-//   P1 rows   : norms (ZeroVector check) + per-CTA fp64 column partials of X and of Y
-//   P2 columns: xbar, ybar (warp per column over the CTA partials); partials of |xbar|^2..
-//   P3 columns: ||xbar||, ||ybar||; partials of ||v||^2, v.xbar (v = mu_x - mu_y); rows:
-//               xbar.h_i, ybar.h_i for the reflection coefficients
-//   P4 tiles  : info; 32x64 tiles: axis u and centre m per column, coef from the P3 dots,
-//               reflect, centre, bf16 hi/lo split, transpose, t partials
-//   P5 columns: t, epilogue constants {2a, 2b}; the last CTA (ticket) forms sum a^2, sum b^2
+// latency, not bandwidth.  One persistent cooperative grid (one CTA of 512 threads per SM)
+// works on ITEMS of R consecutive pooled rows x all d columns, held as an fp32 tile in
+// shared memory, and needs ONE software grid barrier:
+//   P1 items  : load tile; row norms (ZeroVector check); column sums of x over the CTA's
+//               items, added as fixed-point int64 into global accumulators   | barrier
+//   P3 (local): every CTA forms xbar, ybar from the accumulators and reduces ||xbar||,
+//               ||ybar||, ||v||, v.xbar itself (same order in every CTA, so identical
+//               bits), CTA 0 writes info
+//   P4 items  : the tile of P1 is still resident: row dots -> reflection coefficients,
+//               z' = x - coef u - m, bf16 hi/lo split, transposed writes of both planes,
+//               fixed-point column sums of t' = sum (hi + lo)
+//   P5 (last CTA by ticket): t, epilogue constants {2a, 2b}, sum a^2, sum b^2; clears the
+//               accumulators
+// Cross-CTA sums are exact integer sums of per-CTA fixed-order partials, so Z~ and t are
+// bit-identical across runs and ranks.
 #include <cuda_bf16.h>
 
 #include <cfloat>
 #include <climits>
+#include <mutex>
 
 #include "hap_device.cuh"
 #include "hap_internal.h"
@@ -32,9 +36,10 @@
 namespace hap {
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
-constexpr int kSpartStride = 8;  // doubles per CTA in spart: P2 [0,1], P3 [2,3], P6 [4,5]
+constexpr int kMaxItemRows = 16;
+constexpr int kSpartStride = 8;  // doubles per CTA in spart: P5 [4,5]
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -42,20 +47,28 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-// block-wide fixed-order fp64 sum
-__device__ double block_sum(double v, double* red) {
-    v = warp_sum(v);
+// block-wide fixed-order fp64 sums of two values
+__device__ double2 block_sum2(double v0, double v1, double* red) {
+    v0 = warp_sum(v0);
+    v1 = warp_sum(v1);
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     __syncthreads();
-    if (l == 0) red[w] = v;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double s = 0.0;
-        for (int i = 0; i < kWarps; ++i) s += red[i];
-        red[32] = s;
+    if (l == 0) {
+        red[w] = v0;
+        red[kWarps + w] = v1;
     }
     __syncthreads();
-    return red[32];
+    if (threadIdx.x == 0) {
+        double s0 = 0.0, s1 = 0.0;
+        for (int i = 0; i < kWarps; ++i) {
+            s0 += red[i];
+            s1 += red[kWarps + i];
+        }
+        red[2 * kWarps] = s0;
+        red[2 * kWarps + 1] = s1;
+    }
+    __syncthreads();
+    return make_double2(red[2 * kWarps], red[2 * kWarps + 1]);
 }
 
 // sum over CTAs p of spart[p*kSpartStride + k], fixed order (same in every CTA)
@@ -63,7 +76,7 @@ __device__ double cta_partials_sum(const double* spart, int k, double* red) {
     double v = 0.0;
     for (int p = threadIdx.x; p < (int)gridDim.x; p += kThreads)
         v += __ldcg(spart + (size_t)p * kSpartStride + k);
-    return block_sum(v, red);
+    return block_sum2(v, 0.0, red).x;
 }
 
 __device__ __forceinline__ void stamp(const AlignArgs& a, int k) {
@@ -74,23 +87,27 @@ __device__ __forceinline__ void stamp(const AlignArgs& a, int k) {
     }
 }
 
-// Software grid barrier (all CTAs are co-resident: cooperative launch).  bar[0] counts
-// arrivals, bar[1] is the generation; the last arriver resets the count before bumping
-// the generation, so a CTA that sees the new generation also sees the reset.
+// per-CTA stamps (profiling level 3): stamps[8 + 8 cta + k]
+__device__ __forceinline__ void cstamp(const AlignArgs& a, int k) {
+    if (a.stamps && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        a.stamps[8 + 8 * blockIdx.x + k] = (long long)t;
+    }
+}
+
+// Software grid barrier (all CTAs are co-resident: cooperative launch): one release-add
+// per CTA on a counter that only grows within a launch, then acquire-polling until every
+// CTA has arrived.  The counter is cleared for the next launch by the last CTA of P5 (all
+// CTAs have passed the barrier by then).
 __device__ __forceinline__ void grid_sync(unsigned* bar) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        volatile unsigned* vb = bar;
-        const unsigned gen = vb[1];
-        __threadfence();
-        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-            vb[0] = 0u;
-            __threadfence();
-            atomicAdd(bar + 1, 1u);
-        } else {
-            while (vb[1] == gen) __nanosleep(32);
-        }
-        __threadfence();
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+        unsigned v = 0;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+        } while (v < gridDim.x);
     }
     __syncthreads();
 }
@@ -107,162 +124,212 @@ __device__ __forceinline__ const float* row_ptr(const AlignArgs& a, int64_t i) {
     return i < a.n_x ? a.X + i * a.d : a.Y + (i - a.n_x) * a.d;
 }
 
-constexpr int kSP = 33;  // padded smem pitch (32-bit words) of a 64-row bf16 column
+// raw rows [r0, r0 + R) -> tile[r * P + c] (zero rows beyond N); all loads in flight first
+__device__ __forceinline__ void load_tile(const AlignArgs& a, float* tile, int64_t r0, int R, int P) {
+    const int64_t N = a.n_x + a.n_y;
+    if ((a.d & 3) == 0) {
+        const int q = (int)(a.d >> 2);
+        const int total = R * q;
+        for (int b = threadIdx.x; b < total; b += 4 * kThreads) {
+            float4 v[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int idx = b + k * kThreads;
+                const int r = idx / q, c4 = idx - r * q;
+                v[k] = (idx < total && r0 + r < N)
+                           ? __ldg(reinterpret_cast<const float4*>(row_ptr(a, r0 + r)) + c4)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int idx = b + k * kThreads;
+                if (idx < total) {
+                    const int r = idx / q, c4 = idx - r * q;
+                    float2* t2 = reinterpret_cast<float2*>(tile + (size_t)r * P + 4 * c4);
+                    t2[0] = make_float2(v[k].x, v[k].y);
+                    t2[1] = make_float2(v[k].z, v[k].w);
+                }
+            }
+        }
+    } else {
+        const int d = (int)a.d;
+        for (int idx = threadIdx.x; idx < R * d; idx += kThreads) {
+            const int r = idx / d, c = idx - r * d;
+            tile[(size_t)r * P + c] = r0 + r < N ? __ldg(row_ptr(a, r0 + r) + c) : 0.f;
+        }
+    }
+}
 
-__global__ void __launch_bounds__(kThreads, 1) k1_align_fused(AlignArgs a) {
-    __shared__ double red[33];
-    __shared__ double s_inv[512];
-    __shared__ uint32_t s_hi[64 * kSP];
-    __shared__ uint32_t s_lo[64 * kSP];
+// Deterministic cross-CTA sums: every CTA adds its fixed-order fp64 partial, rounded to a
+// multiple of 2^-kFixS, into an int64 accumulator; integer addition is exact and commutes,
+// so the sum is the same bits in every run whatever the arrival order.  Column sums of x
+// are < 2^16 in magnitude (N <= 65535, |x_c| <= 1) and those of z' < 2^18, so 2^-44
+// resolution keeps them below 2^62; the rounding error (<= 2^-45 per CTA partial) is far
+// below the fp64 parity bar of the observed statistic (DESIGN.md D-K1).
+constexpr double kFixScale = 17592186044416.0;  // 2^44
+constexpr double kFixInv = 1.0 / 17592186044416.0;
+__device__ __forceinline__ void fix_add(long long* acc, double v) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(acc), (unsigned long long)__double2ll_rn(v * kFixScale));
+}
+__device__ __forceinline__ double fix_get(const long long* acc) {
+    return (double)__ldcg(acc) * kFixInv;
+}
+
+// dynamic smem: tile f32 [R][P] | (u_c, m_c) f32 [d_pad] (stage_umc) | xs, ys f64 [d]
+// (stage_means); R <= 16.
+// <= 64 registers/thread (launch bound 2): a K1 CTA then fits beside a mask-GEMM CTA on
+// one SM, so the next test's alignment overlaps the current test's GEMM.
+template <int R>
+__global__ void __launch_bounds__(kThreads, 2) k1_align_fused(AlignArgs a, int P, int stage_umc,
+                                                              int stage_means) {
+    constexpr int rp = R / 2;  // row pairs per column: rp consecutive lanes share a column
+    constexpr int lrp = rp >= 8 ? 3 : rp >= 4 ? 2 : rp >= 2 ? 1 : 0;
+    extern __shared__ __align__(16) uint8_t k1_smem[];
+    __shared__ double red[2 * kWarps + 2];
+    __shared__ double s_inv[kMaxItemRows];
+    __shared__ float s_invf[kMaxItemRows], s_cff[kMaxItemRows];
+    __shared__ int s_last;
+    float* tile = reinterpret_cast<float*>(k1_smem);
+    float2* umc = reinterpret_cast<float2*>(k1_smem + (size_t)R * P * 4);  // [d_pad] (u_c, m_c)
+    double* xs = reinterpret_cast<double*>(umc + (stage_umc ? a.d_pad : 0));
+    double* ys = xs + a.d;
+    double* s_t = stage_means ? ys + a.d : xs;  // [d_pad] t' partials (with stage_umc)
     const int G = gridDim.x, cta = blockIdx.x;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t N = a.n_x + a.n_y;
-    const bool vec = (a.d & 3) == 0;
+    const int d = (int)a.d;
+    const int64_t items = a.n_pad / R;
+    long long* acc_x = a.acc;  // [d] fixed-point column sums of x (X rows), then Y rows
+    long long* acc_y = a.acc + d;
+    long long* acc_t = a.acc + 2 * d;  // [d_pad] fixed-point sums of t' = sum (hi + lo)
     unsigned* bar = reinterpret_cast<unsigned*>(a.scratch + 2);
+    if (tid == 0) span_enter(a.span);
     stamp(a, 0);
+    cstamp(a, 0);
 
-    // ---------------- P1: norms + per-CTA column partials (X slice and Y slice)
-    for (int q = 0; q < 2; ++q) {
-        const int64_t n = q ? a.n_y : a.n_x;
-        const int64_t r0 = n * cta / G, r1 = n * (cta + 1) / G;  // <= 443 rows (N <= 65535)
-        const int64_t base = q ? a.n_x : 0;
-        for (int64_t r = r0 + warp; r < r1; r += kWarps) {
-            const float* h = row_ptr(a, base + r);
-            double s = 0.0;
-            if (vec) {
-                const float4* h4 = reinterpret_cast<const float4*>(h);
-#pragma unroll 4
-                for (int64_t c = lane; c < a.d / 4; c += 32) {
-                    const float4 v = __ldg(h4 + c);
-                    s += (double)v.x * v.x + (double)v.y * v.y + (double)v.z * v.z +
-                         (double)v.w * v.w;
-                }
-            } else {
-                for (int64_t c = lane; c < a.d; c += 32) {
-                    const double v = (double)__ldg(h + c);
+    // ---------------- P1: norms + column sums of x over this CTA's items -> accumulators
+    int64_t resident = -1;
+    {
+        double sx0 = 0.0, sy0 = 0.0, sx1 = 0.0, sy1 = 0.0;  // columns tid, tid + kThreads
+        for (int64_t item = cta; item < items; item += G) {
+            const int64_t r0 = item * R;
+            if (resident >= 0) __syncthreads();  // previous tile fully consumed
+            load_tile(a, tile, r0, R, P);
+            __syncthreads();
+            if (warp < R) {
+                const int64_t i = r0 + warp;
+                double s = 0.0;
+                for (int c = lane; c < d; c += 32) {
+                    const double v = (double)tile[(size_t)warp * P + c];
                     s += v * v;
                 }
-            }
-            s = warp_sum(s);
-            if (lane == 0) {
-                const double nrm = sqrt(s);
-                const double iv = nrm < 1e-12 ? 0.0 : 1.0 / nrm;
-                a.inv[base + r] = iv;
-                s_inv[r - r0] = iv;
-                if (nrm < 1e-12)
-                    atomicMin(reinterpret_cast<long long*>(a.scratch), (long long)(base + r));
-            }
-        }
-        __syncthreads();
-        double* part = a.part + (size_t)(2 * cta + q) * a.d;
-        const int nr = (int)(r1 - r0);
-        if (vec) {
-            for (int64_t c4 = tid; c4 < a.d / 4; c4 += kThreads) {
-                double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
-#pragma unroll 8
-                for (int r = 0; r < nr; ++r) {
-                    const float4 v =
-                        __ldg(reinterpret_cast<const float4*>(row_ptr(a, base + r0 + r)) + c4);
-                    const double iv = s_inv[r];
-                    s0 += (double)v.x * iv;
-                    s1 += (double)v.y * iv;
-                    s2 += (double)v.z * iv;
-                    s3 += (double)v.w * iv;
+                s = warp_sum(s);
+                if (lane == 0) {
+                    const double nrm = sqrt(s);
+                    const double iv = (i < N && nrm >= 1e-12) ? 1.0 / nrm : 0.0;
+                    s_inv[warp] = iv;
+                    if (i < N) {
+                        a.inv[i] = iv;
+                        if (nrm < 1e-12)
+                            atomicMin(reinterpret_cast<long long*>(a.scratch), (long long)i);
+                    }
                 }
-                part[4 * c4 + 0] = s0;
-                part[4 * c4 + 1] = s1;
-                part[4 * c4 + 2] = s2;
-                part[4 * c4 + 3] = s3;
             }
-        } else {
-            for (int64_t c = tid; c < a.d; c += kThreads) {
-                double acc = 0.0;
-                for (int r = 0; r < nr; ++r)
-                    acc += (double)__ldg(row_ptr(a, base + r0 + r) + c) * s_inv[r];
-                part[c] = acc;
+            __syncthreads();
+            const int64_t nxr64 = a.n_x - r0;  // X rows of the item
+            const int nxr = nxr64 <= 0 ? 0 : (nxr64 >= R ? R : (int)nxr64);
+            for (int c = tid, k = 0; c < d; c += kThreads, ++k) {
+                double px = 0.0, py = 0.0;
+                for (int r = 0; r < R; ++r) {
+                    const double v = (double)tile[(size_t)r * P + c] * s_inv[r];
+                    if (r < nxr) px += v;
+                    else py += v;
+                }
+                if (k == 0) {
+                    sx0 += px;
+                    sy0 += py;
+                } else if (k == 1) {
+                    sx1 += px;
+                    sy1 += py;
+                } else {  // d > 2 kThreads: straight to the accumulators
+                    fix_add(acc_x + c, px);
+                    fix_add(acc_y + c, py);
+                }
             }
+            resident = item;
         }
-        __syncthreads();
+        if (resident >= 0 && tid < d) {
+            fix_add(acc_x + tid, sx0);
+            fix_add(acc_y + tid, sy0);
+        }
+        if (resident >= 0 && tid + kThreads < d) {
+            fix_add(acc_x + tid + kThreads, sx1);
+            fix_add(acc_y + tid + kThreads, sy1);
+        }
     }
+    cstamp(a, 1);
     grid_sync(bar);
     stamp(a, 1);
-
-    // ---------------- P2: xbar_c, ybar_c = (sum over CTA partials, lane-strided + xor tree)/n
-    {
-        double sxx = 0.0, syy = 0.0;
-        for (int64_t it = (int64_t)cta * kWarps + warp; it < 2 * a.d; it += (int64_t)G * kWarps) {
-            const int q = (int)(it / a.d);
-            const int64_t c = it % a.d;
-            double v = 0.0;
-#pragma unroll 8
-            for (int p = lane; p < G; p += 32) v += __ldcg(a.part + (size_t)(2 * p + q) * a.d + c);
-            v = warp_sum(v) / (double)(q ? a.n_y : a.n_x);
-            if (lane == 0) {
-                (q ? a.ybar : a.xbar)[c] = v;
-                if (q) syy += v * v;
-                else sxx += v * v;
-            }
-        }
-        sxx = block_sum(sxx, red);
-        syy = block_sum(syy, red);
-        if (tid == 0) {
-            a.spart[(size_t)cta * kSpartStride + 0] = sxx;
-            a.spart[(size_t)cta * kSpartStride + 1] = syy;
-        }
-    }
-    grid_sync(bar);
+    cstamp(a, 2);
     stamp(a, 2);
+    cstamp(a, 3);
 
-    // ---------------- P3: norms; partials of ||v||^2 and v.xbar
-    const double nx = sqrt(cta_partials_sum(a.spart, 0, red));
-    const double ny = sqrt(cta_partials_sum(a.spart, 1, red));
+    // ---------------- P3 (CTA-local, identical in every CTA): means, their norms, axis
+    const double rnX = 1.0 / (double)a.n_x, rnY = 1.0 / (double)a.n_y;
+    double sxx = 0.0, syy = 0.0;
+    for (int c = tid; c < d; c += kThreads) {
+        const double xb = fix_get(acc_x + c) * rnX, yb = fix_get(acc_y + c) * rnY;
+        if (stage_means) {
+            xs[c] = xb;
+            ys[c] = yb;
+        }
+        if (cta == 0) {
+            a.xbar[c] = xb;
+            a.ybar[c] = yb;
+        }
+        sxx += xb * xb;
+        syy += yb * yb;
+    }
+    const double2 sq = block_sum2(sxx, syy, red);
+    const double nx = sqrt(sq.x), ny = sqrt(sq.y);
     const bool degenerate = nx < 1e-12 || ny < 1e-12;
     const double rnx = degenerate ? 0.0 : 1.0 / nx, rny = degenerate ? 0.0 : 1.0 / ny;
-    {
-        double sv = 0.0, svx = 0.0;
-        for (int64_t c = (int64_t)cta * kThreads + tid; c < a.d; c += (int64_t)G * kThreads) {
-            const double xb = __ldcg(a.xbar + c), yb = __ldcg(a.ybar + c);
-            const double v = xb * rnx - yb * rny;
-            sv += v * v;
-            svx += v * xb;
-        }
-        sv = block_sum(sv, red);
-        svx = block_sum(svx, red);
-        if (tid == 0) {
-            a.spart[(size_t)cta * kSpartStride + 2] = sv;
-            a.spart[(size_t)cta * kSpartStride + 3] = svx;
-        }
-        // row dots for the reflection coefficients (they do not need ||v||):
-        // coef_i = 2 u^T x_i = 2 (xbar.h_i / ||xbar|| - ybar.h_i / ||ybar||) / (||v|| ||h_i||)
-        if (a.mode != HAP_ALIGN_NONE && !degenerate) {
-            for (int64_t i = (int64_t)cta * kWarps + warp; i < a.n_x; i += (int64_t)G * kWarps) {
-                const float* h = a.X + i * a.d;
-                double dx = 0.0, dy = 0.0;
-#pragma unroll 8
-                for (int64_t c = lane; c < a.d; c += 32) {
-                    const double hv = (double)__ldg(h + c);
-                    dx += hv * __ldcg(a.xbar + c);
-                    dy += hv * __ldcg(a.ybar + c);
-                }
-                dx = warp_sum(dx);
-                dy = warp_sum(dy);
-                if (lane == 0) a.coef[i] = (dx * rnx - dy * rny) * __ldcg(a.inv + i);
-            }
-        }
+#define XB(c) (stage_means ? xs[c] : fix_get(acc_x + (c)) * rnX)
+#define YB(c) (stage_means ? ys[c] : fix_get(acc_y + (c)) * rnY)
+    double sv = 0.0, svx = 0.0;
+    for (int c = tid; c < d; c += kThreads) {
+        const double xb = XB(c), yb = YB(c);
+        const double v = xb * rnx - yb * rny;
+        sv += v * v;
+        svx += v * xb;
     }
-    grid_sync(bar);
-    stamp(a, 3);
-
-    // ---------------- P4: identity, info; then 32-row tiles, each CTA self-contained:
-    // coefficients coef_i = 2 u^T x_i of its rows, axis u_c and centre m_c per column (both
-    // from the means), z' = h/||h|| - coef u - m (fp32 is ample: the value is then kept to
-    // 16 significant bits), hi/lo split, transpose, fixed-order t partial per column
-    const double nv0 = sqrt(cta_partials_sum(a.spart, 2, red));
-    const double vx = cta_partials_sum(a.spart, 3, red);
+    const double2 vv = block_sum2(sv, svx, red);
+    const double nv0 = sqrt(vv.x);
     const bool identity = (a.mode == HAP_ALIGN_NONE) || degenerate || nv0 < 1e-9;  // R3
     const double rnv = identity ? 0.0 : 1.0 / nv0;
-    const double ux = vx * rnv;  // u . xbar
+    const double ux = vv.y * rnv;  // u . xbar
     const double rN = 4096.0 / (double)N;
+    // axis u_c and centre m_c = t_c/N quantised to 2^-12, t = n_x (xbar - 2u(u.xbar)) + n_y ybar
+    auto axis_centre = [&](int c, double& ud, double& md) {
+        ud = 0.0;
+        md = 0.0;
+        if (c < d) {
+            const double xb = XB(c), yb = YB(c);
+            ud = (xb * rnx - yb * rny) * rnv;
+            const double t = (double)a.n_x * (xb - 2.0 * ud * ux) + (double)a.n_y * yb;
+            md = rint(t * rN) * (1.0 / 4096.0);
+        }
+    };
+    if (stage_umc || cta == 0)
+        for (int c = tid; c < (int)a.d_pad; c += kThreads) {
+            double ud, md;
+            axis_centre(c, ud, md);
+            if (stage_umc) umc[c] = make_float2((float)ud, (float)md);
+            if (cta == 0) {  // export copies (read in P5 and by hap_export_pooled)
+                a.u[c] = ud;
+                a.m[c] = md;
+            }
+        }
     if (cta == 0 && tid == 0) {
         hap_align_info* f = a.info;
         const long long bad = *reinterpret_cast<volatile long long*>(a.scratch);
@@ -285,133 +352,191 @@ __global__ void __launch_bounds__(kThreads, 1) k1_align_fused(AlignArgs a) {
         const double qnan = __longlong_as_double(0x7ff8000000000000ll);
         f->gemm_r_x = f->gemm_r_y = f->gemm_t_obs = qnan;
     }
-    {
-        // 2-D tiles (32 rows x 64 columns); P3 stored (u^T x_i) * ||v|| in coef[i]
-        double* s_cf = s_inv;         // [32] 2 u^T x_i of the tile rows
-        double* s_iv = s_inv + 64;    // [32] 1/||h_i||
-        uint16_t* sh16 = reinterpret_cast<uint16_t*>(s_hi);
-        uint16_t* sl16 = reinterpret_cast<uint16_t*>(s_lo);
-        const int64_t ntr = a.n_pad / kRowTile, ntc = (a.d_pad + 63) / 64;
-        for (int64_t tile = cta; tile < ntr * ntc; tile += G) {
-            const int64_t rt = tile / ntc, c0 = (tile % ntc) * 64;
-            const int64_t r0 = rt * kRowTile;
-            if (tid < kRowTile) {
-                const int64_t i = r0 + tid;
-                s_cf[tid] = (i < a.n_x && !identity) ? 2.0 * __ldcg(a.coef + i) * rnv : 0.0;
-                s_iv[tid] = i < N ? __ldcg(a.inv + i) : 0.0;
+    stamp(a, 3);
+    cstamp(a, 4);
+
+    // ---------------- P4: items again, last one first (its tile is still resident)
+    const int units = rp * (int)a.d_pad;
+    if (stage_umc)
+        for (int c = tid; c < (int)a.d_pad; c += kThreads) s_t[c] = 0.0;
+    if (resident >= 0) {
+        const int64_t nmine = (resident - cta) / G + 1;
+        for (int64_t k = nmine - 1; k >= 0; --k) {
+            const int64_t item = cta + k * G;
+            const int64_t r0 = item * R;
+            if (item != resident) {
+                __syncthreads();
+                load_tile(a, tile, r0, R, P);
+                if (tid < R) s_inv[tid] = r0 + tid < N ? __ldcg(a.inv + r0 + tid) : 0.0;
+                __syncthreads();
             }
-            const int tc = tid & 63, tr = tid >> 6;  // 64 columns x 4 row groups of 8
-            const int64_t c = c0 + tc;
-            float hv[kRowTile / 4];
-#pragma unroll
-            for (int j = 0; j < kRowTile / 4; ++j) {  // issue all loads first
-                const int64_t i = r0 + tr + 4 * j;
-                hv[j] = (i < N && c < a.d) ? __ldg(row_ptr(a, i) + c) : 0.f;
-            }
-            double ud = 0.0, md = 0.0;
-            if (c < a.d) {
-                const double xb = __ldcg(a.xbar + c), yb = __ldcg(a.ybar + c);
-                ud = (xb * rnx - yb * rny) * rnv;
-                // centre m = t/N quantised to 2^-12, t = n_x (xbar - 2u(u.xbar)) + n_y ybar
-                const double t = (double)a.n_x * (xb - 2.0 * ud * ux) + (double)a.n_y * yb;
-                md = rint(t * rN) * (1.0 / 4096.0);
-            }
-            if (rt == 0 && tr == 0 && c < a.d_pad) {  // export copies (read in P5)
-                a.u[c] = ud;
-                a.m[c] = md;
-            }
-            __syncthreads();
-            const float uc = (float)ud, mc = (float)md;
-#pragma unroll
-            for (int j = 0; j < kRowTile / 4; ++j) {
-                const int rl = tr + 4 * j;
-                const float z = (r0 + rl < N && c < a.d)
-                                    ? fmaf(-(float)s_cf[rl], uc, hv[j] * (float)s_iv[rl]) - mc
-                                    : 0.f;
-                const __nv_bfloat16 hi = __float2bfloat16_rn(z);
-                const __nv_bfloat16 lo = __float2bfloat16_rn(z - __bfloat162float(hi));
-                sh16[tc * (2 * kSP) + rl] = __bfloat16_as_ushort(hi);
-                sl16[tc * (2 * kSP) + rl] = __bfloat16_as_ushort(lo);
-            }
-            __syncthreads();
-            // 32 rows = 16 words per column: half-warps write one column each
-            const int hw = lane >> 4, hl = lane & 15;
-            for (int cc = 2 * warp + hw; cc < 64; cc += 2 * kWarps) {
-                const int64_t col = c0 + cc;
-                double v = 0.0;
-                if (col < a.d_pad) {
-                    const uint32_t vh = s_hi[cc * kSP + hl], vl = s_lo[cc * kSP + hl];
-                    reinterpret_cast<uint32_t*>(a.zt_hi + col * a.n_pad + r0)[hl] = vh;
-                    reinterpret_cast<uint32_t*>(a.zt_lo + col * a.n_pad + r0)[hl] = vl;
-                    v = (double)__bfloat162float(__ushort_as_bfloat16((uint16_t)(vh & 0xFFFF))) +
-                        (double)__bfloat162float(__ushort_as_bfloat16((uint16_t)(vl & 0xFFFF))) +
-                        (double)__bfloat162float(__ushort_as_bfloat16((uint16_t)(vh >> 16))) +
-                        (double)__bfloat162float(__ushort_as_bfloat16((uint16_t)(vl >> 16)));
+            // reflection coefficients 2 u^T x_i = 2 (xbar.h_i/||xbar|| - ybar.h_i/||ybar||)
+            // / (||v|| ||h_i||) of the X rows (Y is not reflected)
+            if (warp < R) {
+                const int64_t i = r0 + warp;
+                double cf = 0.0;
+                if (i < a.n_x && !identity) {
+                    double dx = 0.0, dy = 0.0;
+                    for (int c = lane; c < d; c += 32) {
+                        const double hv = (double)tile[(size_t)warp * P + c];
+                        dx += hv * XB(c);
+                        dy += hv * YB(c);
+                    }
+                    dx = warp_sum(dx);
+                    dy = warp_sum(dy);
+                    cf = 2.0 * ((dx * rnx - dy * rny) * s_inv[warp]) * rnv;
                 }
-#pragma unroll
-                for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-                if (hl == 0 && col < a.d_pad) a.tpart[rt * a.d_pad + col] = v;
+                if (lane == 0) {
+                    s_cff[warp] = (float)cf;
+                    s_invf[warp] = (float)s_inv[warp];
+                }
             }
             __syncthreads();
+            if (k == nmine - 1) cstamp(a, 5);
+            // z' = x - coef u - m (fp32 is ample: the value is then kept to 16 significant
+            // bits), hi/lo split; thread = (column, row pair): rp lanes write one column's
+            // 2R contiguous bytes of each plane
+            {
+                // j is fixed per thread (kThreads is a multiple of rp): hoist the row terms
+                const int j = tid & (rp - 1);
+                const float cf0 = s_cff[2 * j], cf1 = s_cff[2 * j + 1];
+                const float iv0 = s_invf[2 * j], iv1 = s_invf[2 * j + 1];
+                const bool v0 = r0 + 2 * j < N, v1 = r0 + 2 * j + 1 < N;
+                uint32_t* zh = reinterpret_cast<uint32_t*>(a.zt_hi + r0) + j;
+                uint32_t* zl = reinterpret_cast<uint32_t*>(a.zt_lo + r0) + j;
+                const float* t0 = tile + (size_t)(2 * j) * P;
+                const float* t1 = t0 + P;
+                for (int uidx = tid; uidx < units; uidx += kThreads) {
+                    const int c = uidx >> lrp;
+                    float2 um;  // (0, 0) for pad columns
+                    if (stage_umc) {
+                        um = umc[c];
+                    } else {
+                        double ud, md;
+                        axis_centre(c, ud, md);
+                        um = make_float2((float)ud, (float)md);
+                    }
+                    // z' = x - coef u - m in fp32 (the value is then kept to 16 bits)
+                    const float z0 = v0 && c < d ? fmaf(-cf0, um.x, t0[c] * iv0) - um.y : 0.f;
+                    const float z1 = v1 && c < d ? fmaf(-cf1, um.x, t1[c] * iv1) - um.y : 0.f;
+                    const __nv_bfloat16 h0 = __float2bfloat16_rn(z0), h1 = __float2bfloat16_rn(z1);
+                    const float fh0 = __bfloat162float(h0), fh1 = __bfloat162float(h1);
+                    const __nv_bfloat16 l0 = __float2bfloat16_rn(z0 - fh0), l1 = __float2bfloat16_rn(z1 - fh1);
+                    const size_t off = (size_t)c * (size_t)(a.n_pad >> 1);
+                    zh[off] = (uint32_t)__bfloat16_as_ushort(h0) | ((uint32_t)__bfloat16_as_ushort(h1) << 16);
+                    zl[off] = (uint32_t)__bfloat16_as_ushort(l0) | ((uint32_t)__bfloat16_as_ushort(l1) << 16);
+                    // hi + lo is exact in fp32; the column's t' partial is summed in fp64
+                    double tv = (double)(fh0 + __bfloat162float(l0)) + (double)(fh1 + __bfloat162float(l1));
+#pragma unroll
+                    for (int o = 1; o < rp; o <<= 1) tv += __shfl_xor_sync(0xffffffffu, tv, o);
+                    if (j == 0) {  // the column's owner thread (the same for every item)
+                        if (stage_umc) s_t[c] += tv;
+                        else fix_add(acc_t + c, tv);
+                    }
+                }
+            }
+        }
+        if (stage_umc) {
+            __syncthreads();
+            for (int c = tid; c < (int)a.d_pad; c += kThreads) fix_add(acc_t + c, s_t[c]);
         }
     }
-    grid_sync(bar);
+#undef XB
+#undef YB
+    cstamp(a, 6);
     stamp(a, 4);
 
-    // ---------------- P5: t = N m + sum of tile partials (lane-strided + xor tree);
-    // a = n_x m, b = t - a (fp32) for the GEMM epilogue; partials of sum a^2, sum b^2;
-    // the last CTA to finish (ticket) forms {sum a^2, sum b^2} in fixed order
-    {
-        __shared__ int s_last;
-        const int64_t ntr = a.n_pad / kRowTile;
+    // ---------------- P5 (last CTA to finish, ticket): t = N m + t', a = n_x m, b = t - a
+    // (fp32) for the GEMM epilogue, {sum a^2, sum b^2} in fixed order; then the
+    // accumulators are cleared for the next launch
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+        unsigned* ticket = reinterpret_cast<unsigned*>(a.scratch + 1);
+        s_last = atomicAdd(ticket, 1u) == (unsigned)G - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
         double sa = 0.0, sb = 0.0;
-        for (int64_t c = (int64_t)cta * kWarps + warp; c < a.d_pad; c += (int64_t)G * kWarps) {
-            double tp = 0.0;
-#pragma unroll 4
-            for (int64_t t = lane; t < ntr; t += 32) tp += __ldcg(a.tpart + t * a.d_pad + c);
-            tp = warp_sum(tp);
-            if (lane == 0) {
-                const double m = __ldcg(a.m + c);
-                a.t64[c] = (double)N * m + tp;
-                const float af = (float)((double)a.n_x * m);
-                const float bf = (float)((double)a.n_y * m + tp);
-                a.ab[c] = make_float2(2.0f * af, 2.0f * bf);
-                sa += (double)af * (double)af;
-                sb += (double)bf * (double)bf;
-            }
+        for (int64_t c = tid; c < a.d_pad; c += kThreads) {
+            const double tsum = fix_get(acc_t + c);
+            const double m = __ldcg(a.m + c);
+            a.t64[c] = (double)N * m + tsum;
+            const float af = (float)((double)a.n_x * m);
+            const float bf = (float)((double)a.n_y * m + tsum);
+            a.ab[c] = make_float2(2.0f * af, 2.0f * bf);
+            sa += (double)af * (double)af;
+            sb += (double)bf * (double)bf;
         }
-        sa = block_sum(sa, red);
-        sb = block_sum(sb, red);
+        const double2 sab = block_sum2(sa, sb, red);
+        for (int64_t c = tid; c < 2 * (int64_t)d + a.d_pad; c += kThreads) a.acc[c] = 0;
         if (tid == 0) {
-            a.spart[(size_t)cta * kSpartStride + 4] = sa;
-            a.spart[(size_t)cta * kSpartStride + 5] = sb;
-            __threadfence();
-            unsigned* ticket = reinterpret_cast<unsigned*>(a.scratch + 1);
-            s_last = atomicAdd(ticket, 1u) == (unsigned)G - 1;
-        }
-        __syncthreads();
-        if (s_last) {
-            __threadfence();
-            const double SA = cta_partials_sum(a.spart, 4, red);
-            const double SB = cta_partials_sum(a.spart, 5, red);
-            if (tid == 0) {
-                a.sconst[0] = SA;
-                a.sconst[1] = SB;
-                a.scratch[0] = LLONG_MAX;  // reset the ZeroVector word and the ticket
-                reinterpret_cast<unsigned*>(a.scratch + 1)[0] = 0u;
-            }
+            a.sconst[0] = sab.x;
+            a.sconst[1] = sab.y;
+            a.scratch[0] = LLONG_MAX;  // reset the ZeroVector word, the ticket, the barrier
+            reinterpret_cast<unsigned*>(a.scratch + 1)[0] = 0u;
+            bar[0] = 0u;
         }
     }
     stamp(a, 5);
+    cstamp(a, 7);
+    __syncthreads();
+    if (tid == 0) span_exit(a.span);
 }
 
 }  // namespace
 
+AlignGeom align_geometry(int64_t d) {
+    AlignGeom g{};
+    g.pitch = (int)(round_up(d, 16) + 2);  // = 2 (mod 16): conflict-free (column, row-pair) reads
+    g.rows = kMaxItemRows;
+    while (g.rows > 2 && (size_t)g.rows * g.pitch * 4 + (size_t)8 * round_up(d, 32) > 200u * 1024u)
+        g.rows >>= 1;
+    const size_t tile = (size_t)g.rows * g.pitch * 4, umc = (size_t)8 * round_up(d, 32),
+                 means = (size_t)16 * d;
+    g.stage_umc = tile + 2 * umc <= 220u * 1024u;
+    g.stage_means = g.stage_umc && tile + 2 * umc + means <= 220u * 1024u;
+    g.smem = tile + (g.stage_umc ? 2 * umc : 0) + (g.stage_means ? means : 0);  // + t' partials
+    return g;
+}
+
+// Cooperative grids of different streams could each be partly resident and wait for each
+// other's SMs at their grid barriers; every K1 launch of the process is therefore ordered
+// after the previous one on the device (an event chain; K1 is latency-bound and short).
+static std::mutex g_k1_mu;
+static cudaEvent_t g_k1_last[64] = {};
+
 cudaError_t launch_align(const AlignArgs& a, int grid, cudaStream_t st) {
+    const AlignGeom g = align_geometry(a.d);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(g_k1_mu);
+    cudaEvent_t& last = g_k1_last[dev & 63];
+    if (!last) {
+        cudaError_t e = cudaEventCreateWithFlags(&last, cudaEventDisableTiming);
+        if (e != cudaSuccess) return e;
+    } else {
+        cudaError_t e = cudaStreamWaitEvent(st, last, 0);
+        if (e != cudaSuccess) return e;
+    }
+    const void* fn = g.rows == 16 ? (const void*)k1_align_fused<16>
+                     : g.rows == 8 ? (const void*)k1_align_fused<8>
+                     : g.rows == 4 ? (const void*)k1_align_fused<4>
+                                   : (const void*)k1_align_fused<2>;
+    static size_t configured[5] = {0, 0, 0, 0, 0};
+    const int fi = g.rows == 16 ? 4 : g.rows == 8 ? 3 : g.rows == 4 ? 2 : 1;
+    if (g.smem > 48 * 1024 && g.smem > configured[fi]) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
+        if (e != cudaSuccess) return e;
+        configured[fi] = g.smem;
+    }
     AlignArgs copy = a;
-    void* args[] = {&copy};
-    return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k1_align_fused), dim3(grid),
-                                       dim3(kThreads), args, 0, st);
+    int P = g.pitch, su = g.stage_umc ? 1 : 0, sm = g.stage_means ? 1 : 0;
+    void* args[] = {&copy, &P, &su, &sm};
+    cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, g.smem, st);
+    if (e != cudaSuccess) return e;
+    return cudaEventRecord(last, st);
 }
 
 }  // namespace hap

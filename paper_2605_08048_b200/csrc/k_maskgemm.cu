@@ -166,6 +166,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) K3_STAMP(7, 0);  // kernel entry
+    if (threadIdx.x == 0) span_enter(g.span);
     const uint32_t rank = kPair == 2 ? cluster_ctarank() : 0u;
     const bool leader = rank == 0;
     const int pair_id = blockIdx.x / kPair;
@@ -341,6 +342,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     if constexpr (kPair == 2) cluster_sync();
     if (threadIdx.x == 0) K3_STAMP(7, 1);  // all roles done
+    if (threadIdx.x == 0) span_exit(g.span);
     if (warp == 1) {
         tc_fence_after();
         if constexpr (kPair == 2) tmem_dealloc_pair<kTmemCols>(tmem);

@@ -58,6 +58,7 @@ __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy(PermArgs a, int lt
     const int nw = (int)(blockDim.x >> 5);
     const int64_t wstride = (int64_t)gridDim.x * nw;
     const int64_t items = a.count + (a.out_kind == kMaskBf16Row ? a.ntiles : 0);
+    if (l == 0) span_enter(a.span);
     for (int64_t pi = (int64_t)blockIdx.x * nw + w; pi < items; pi += wstride) {
         if (pi >= a.count) {  // observed split: row 0 of tile (pi - count)
             const int64_t t = pi - a.count;
@@ -184,31 +185,190 @@ __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy(PermArgs a, int lt
         }
         __syncwarp();
     }
+    if (l == 0) span_exit(a.span);
+}
+
+
+// ---------------------------------------------------------------------------------------
+// Wide-table variant (N <= kWideMaxN): LT as uint32 so the last-writer scatter is one
+// shared atomicMax per step (any order, no rounds / verification), and phase B first
+// compacts the chain starts of the written high positions into a per-warp list, then
+// walks the chains lane-balanced.  Same result bits as k2_perm_fy (tests).
+constexpr uint32_t kExiled32 = 0xFFFFFFFFu;
+
+__device__ __forceinline__ void emit_row_u32(const PermArgs& a, const uint32_t* LT, int64_t pi,
+                                             uint32_t nx, int l) {
+    const int64_t R1 = a.rows_per_tile - 1;
+    const int64_t orow = (pi / R1) * a.rows_per_tile + 1 + pi % R1;
+    uint4* row = reinterpret_cast<uint4*>(static_cast<uint16_t*>(a.out) + orow * a.n_pad);
+    uint4* L4 = reinterpret_cast<uint4*>(const_cast<uint32_t*>(LT));
+    const uint4 z = make_uint4(0, 0, 0, 0);
+    for (int v8 = l; v8 < (int)(a.n_pad >> 3); v8 += 32) {
+        const uint4 q0 = L4[2 * v8], q1 = L4[2 * v8 + 1];
+        L4[2 * v8] = z;  // leave the table zeroed for the next permutation
+        L4[2 * v8 + 1] = z;
+        const uint32_t t[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+        const uint32_t v0 = 8u * (uint32_t)v8;
+        uint32_t o[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            // low position: selected unless exiled (t + 1 != 0); high: iff written (t != 0)
+            const uint32_t va = v0 + 2 * e, vb = va + 1;
+            const bool sa = t[2 * e] + (va < nx ? 1u : 0u) != 0u;
+            const bool sb = t[2 * e + 1] + (vb < nx ? 1u : 0u) != 0u;
+            o[e] = (sa ? 0x3F80u : 0u) | (sb ? 0x3F800000u : 0u);
+        }
+        row[v8] = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+}
+
+__global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy32(PermArgs a, int lt_pitch) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    // per warp: LT u32[lt_pitch] | sink u32[32] | starts u16[lt_pitch / 2 + 16]
+    uint32_t* LT = reinterpret_cast<uint32_t*>(smem + (size_t)w * ((size_t)lt_pitch * 5u + 160u));
+    uint32_t* sink = LT + lt_pitch + l;  // per-lane target of the atomics of no-op steps
+    uint16_t* starts = reinterpret_cast<uint16_t*>(LT + lt_pitch + 32);
+    const uint32_t N = (uint32_t)a.N, nx = (uint32_t)a.n_x, s = a.s;
+    const uint32_t key0 = (uint32_t)(a.seed & 0xFFFFFFFFu), key1 = (uint32_t)(a.seed >> 32);
+    const int nw = (int)(blockDim.x >> 5);
+    const int64_t wstride = (int64_t)gridDim.x * nw;
+    const int64_t items = a.count + (a.out_kind == kMaskBf16Row ? a.ntiles : 0);
+    if (l == 0) span_enter(a.span);
+    {
+        uint4* L4 = reinterpret_cast<uint4*>(LT);
+        for (int q = l; q < lt_pitch / 4; q += 32) L4[q] = make_uint4(0, 0, 0, 0);
+    }
+    __syncwarp();
+    for (int64_t pi = (int64_t)blockIdx.x * nw + w; pi < items; pi += wstride) {
+        if (pi >= a.count) {  // observed split: row 0 of tile (pi - count)
+            const int64_t t = pi - a.count;
+            uint4* row = reinterpret_cast<uint4*>(static_cast<uint16_t*>(a.out) +
+                                                  t * a.rows_per_tile * a.n_pad);
+            for (int64_t v8 = l; v8 < a.n_pad / 8; v8 += 32) {
+                uint32_t wds[4];
+#pragma unroll
+                for (int e2 = 0; e2 < 4; ++e2) {
+                    const int64_t v = 8 * v8 + 2 * e2;
+                    wds[e2] = (v < a.n_x ? 0x3F80u : 0u) | ((v + 1 < a.n_x ? 0x3F80u : 0u) << 16);
+                }
+                row[v8] = make_uint4(wds[0], wds[1], wds[2], wds[3]);
+            }
+            continue;
+        }
+        const uint32_t b = (uint32_t)(a.b_begin + (uint64_t)pi);
+        // ---- phase A: draws + last-writer scatter (atomicMax = largest step wins)
+        for (uint32_t k0 = 4u * (uint32_t)l; k0 < nx; k0 += 128u) {
+            const u32x4 wd = philox4x32_10(u32x4{k0 >> 2, b, s, 0u}, key0, key1);
+            const uint32_t x[4] = {wd.x, wd.y, wd.z, wd.w};
+            uint32_t j[4];
+            bool slow = false;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {  // Lemire fast path; rejection needs lo < bound
+                const uint32_t k = k0 + e, bound = N - k;
+                const uint64_t m = (uint64_t)x[e] * bound;
+                slow |= (uint32_t)m < bound;
+                j[e] = k + (uint32_t)(m >> 32);
+            }
+            if (slow) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    if (k0 + e < nx) j[e] = fy_target(x[e], k0 + e, N, b, s, key0, key1);
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {  // unconditional: no-op steps hit the lane's sink
+                const uint32_t k = k0 + e;
+                atomicMax((k < nx && j[e] != k) ? LT + j[e] : sink, k + 1u);
+            }
+        }
+        __syncwarp();
+        // ---- phase B1: compact the chain starts LT[p]-1 of the written high positions
+        uint32_t nst = 0;
+        for (uint32_t p0 = (nx & ~3u) + 4u * (uint32_t)l; __any_sync(0xffffffffu, p0 < N);
+             p0 += 128u) {
+            uint4 q = make_uint4(0, 0, 0, 0);
+            if (p0 < N) q = *reinterpret_cast<const uint4*>(LT + p0);
+            // positions below n_x only occur in the first chunk; beyond N the table is 0
+            if (p0 < nx) {
+                q.x = p0 >= nx ? q.x : 0u;
+                q.y = p0 + 1 >= nx ? q.y : 0u;
+                q.z = p0 + 2 >= nx ? q.z : 0u;
+            }
+            const uint32_t c = (q.x != 0u) + (q.y != 0u) + (q.z != 0u) + (q.w != 0u);
+            uint32_t incl = c;  // inclusive warp prefix sum of the counts
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (l >= o) incl += v;
+            }
+            uint32_t at = nst + incl - c;
+            if (q.x) starts[at++] = (uint16_t)(q.x - 1u);
+            if (q.y) starts[at++] = (uint16_t)(q.y - 1u);
+            if (q.z) starts[at++] = (uint16_t)(q.z - 1u);
+            if (q.w) starts[at] = (uint16_t)(q.w - 1u);
+            nst += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        __syncwarp();
+        // ---- phase B2: walk each chain to its end (an unwritten low position) and exile it
+        {
+            uint32_t i = (uint32_t)l;
+            uint32_t cur = i < nst ? starts[i] : 0u;
+            while (__any_sync(0xffffffffu, i < nst)) {
+#pragma unroll
+                for (int rep = 0; rep < 2; ++rep) {
+                    const uint32_t t = LT[cur];  // inactive lanes re-read a harmless entry
+                    const bool end = (i < nst) & (t == 0u);
+                    if (end) LT[cur] = kExiled32;
+                    i += end ? 32u : 0u;
+                    const uint32_t nxt = starts[min(i, nst)];  // nst < lt_pitch/2: in bounds
+                    cur = end ? nxt : t - 1u;
+                    cur = i < nst ? cur : 0u;
+                }
+            }
+        }
+        __syncwarp();
+        // ---- phase C: exact 0/1 row (re-zeroes the table)
+        if (a.out_kind == kMaskBf16Row) {
+            emit_row_u32(a, LT, pi, nx, l);
+        } else {
+            uint8_t* row = static_cast<uint8_t*>(a.out) + pi * a.N;
+            for (uint32_t v = l; v < N; v += 32) {
+                const uint32_t t = LT[v];
+                LT[v] = 0u;
+                row[v] = (v < nx) ? (t != kExiled32) : (t != 0u);
+            }
+        }
+        __syncwarp();
+    }
+    if (l == 0) span_exit(a.span);
 }
 
 }  // namespace
 
 cudaError_t launch_perm(const PermArgs& a, int sm_count, cudaStream_t st) {
     if (a.count <= 0) return cudaSuccess;
-    const int lt_pitch = (int)round_up(a.N, 64);  // uint16 entries, 128-byte multiple
-    const size_t per_warp = (size_t)(lt_pitch + 128) * sizeof(uint16_t);
+    const int lt_pitch = (int)round_up(a.N, 64);  // entries, 128-byte multiple
+    // wide (uint32) table + start list when 4 warps fit in the budget, else uint16 table
+    const bool wide = (size_t)lt_pitch * 5u + 160u <= (200u * 1024u) / 4u;
+    const size_t per_warp = wide ? (size_t)lt_pitch * 5u + 160u : (size_t)(lt_pitch + 128) * sizeof(uint16_t);
     const int nw = (int)std::max<size_t>(1, std::min<size_t>(kPermWarps, (200u * 1024u) / per_warp));
     const size_t smem = (size_t)nw * per_warp;
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-        cudaError_t e = cudaFuncSetAttribute(k2_perm_fy, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
+    const void* fn = wide ? (const void*)k2_perm_fy32 : (const void*)k2_perm_fy;
+    static size_t configured[2] = {0, 0};
+    if (smem > 48 * 1024 && smem > configured[wide]) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        configured = smem;
+        configured[wide] = smem;
     }
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_perm_fy, nw * 32, smem);
-    // at most 4 resident CTAs per SM: the generator for the next block runs beside the
-    // persistent mask-GEMM, which keeps one CTA per SM
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nw * 32, smem);
     per_sm = std::max(1, std::min(per_sm, a.max_ctas_per_sm > 0 ? a.max_ctas_per_sm : per_sm));
     const int64_t need = ceil_div(a.count + (a.out_kind == kMaskBf16Row ? a.ntiles : 0), nw);
     const int grid = (int)std::min<int64_t>(need, (int64_t)sm_count * per_sm);
-    k2_perm_fy<<<grid, nw * 32, smem, st>>>(a, lt_pitch);
+    if (wide)
+        k2_perm_fy32<<<grid, nw * 32, smem, st>>>(a, lt_pitch);
+    else
+        k2_perm_fy<<<grid, nw * 32, smem, st>>>(a, lt_pitch);
     return cudaGetLastError();
 }
 

@@ -157,6 +157,14 @@ def test_ragged_shapes(ctx, orc, n_x, n_y, d, B, block, pair_mode):
     check_pair(ctx, orc, X, Y, B, s=3, block=block, pair_mode=pair_mode)
 
 
+@pytest.mark.parametrize("d", [4096, 9000, 16384])
+def test_wide_dimension(ctx, orc, d):
+    """K1 item geometry for wide rows: fewer rows per smem tile (8 / 4 / 2), per-column
+    axis/centre computed on the fly and t' partials straight to the accumulators."""
+    X, Y = HI.make_pair(HI.PairSpec(37, 41, d, HI.kappa_for(d), HI.kappa_for(d), 30.0, seed=9))
+    check_pair(ctx, orc, X, Y, 300, s=3)
+
+
 def test_singleton_group(ctx, orc):
     """n_x = 1: r1 = ||z_i|| = 1 for every split (L is clamped at r = 1 - 1e-9, R4, and
     ill-conditioned there), so only the MRLs are compared."""
