@@ -76,17 +76,9 @@ __device__ __forceinline__ double kappa_hat(double r, double d) {
     return r * (d - r2) / (1.0 - r2);
 }
 
-// statistic of one tile row from the piece partials, summed in ascending column order;
+// statistic of a tile row from its accumulated sums S1 = |sigma1|^2, S2 = |sigma2|^2;
 // T = L(r2) - L(r1) = log(q(r2)/q(r1)): one log (q = 0 gives the +-inf / both-zero cases)
-__device__ __forceinline__ RowStat row_stat(const GemmArgs& g, int tile, int row) {
-    double S1 = g.sconst[0], S2 = g.sconst[1];
-    const float2* p = g.part + (size_t)tile * g.max_slots * g.rows_per_tile + row;
-    const int np = g.tile_npieces[tile];
-    for (int c = 0; c < np; ++c) {
-        const float2 v = __ldcg(p + (size_t)c * g.rows_per_tile);
-        S1 += (double)v.x;
-        S2 += (double)v.y;
-    }
+__device__ __forceinline__ RowStat row_stat(const GemmArgs& g, double S1, double S2) {
     RowStat s;
     s.r1 = sqrt(fmax(S1, 0.0)) / (double)g.n_x;
     s.r2 = sqrt(fmax(S2, 0.0)) / (double)g.n_y;
@@ -96,34 +88,54 @@ __device__ __forceinline__ RowStat row_stat(const GemmArgs& g, int tile, int row
 }
 
 // Last CTA of a tile: every thread evaluates the observed row (row 0, identical result in
-// all threads: same partials, same order) and its own permutation rows.
-__device__ void finalize_tile(const GemmArgs& g, int tile, int etid, double* s_tobs) {
+// all threads: same partials, same order) and its own permutation rows etid, etid + 128.
+// All partial loads of the three rows are issued together (one L2 round trip per 8 pieces);
+// the piece partials are summed in ascending slot order (deterministic).
+__device__ void finalize_tile(const GemmArgs& g, int tile, int np, int etid, unsigned* s_cnt,
+                              double S1c, double S2c, double tau) {
     const int R = g.rows_per_tile;
-    (void)s_tobs;
-    const RowStat o = row_stat(g, tile, 0);
+    if (etid < 3) s_cnt[etid] = 0u;
+    constexpr int kRows = 3;  // row 0, etid, etid + 128 (R <= 256)
+    const int rows[kRows] = {0, etid, etid + 128};
+    double S1[kRows], S2[kRows];
+#pragma unroll
+    for (int k = 0; k < kRows; ++k) {
+        S1[k] = S1c;
+        S2[k] = S2c;
+    }
+    const float2* p = g.part + (size_t)tile * g.max_slots * R;
+    for (int c0 = 0; c0 < np; c0 += 8) {
+        float2 v[kRows][8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+#pragma unroll
+            for (int k = 0; k < kRows; ++k)
+                v[k][c] = (c0 + c < np && rows[k] < R) ? __ldcg(p + (size_t)(c0 + c) * R + rows[k])
+                                                        : make_float2(0.f, 0.f);
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+#pragma unroll
+            for (int k = 0; k < kRows; ++k) {
+                S1[k] += (double)v[k][c].x;
+                S2[k] += (double)v[k][c].y;
+            }
+    }
+    const RowStat o = row_stat(g, S1[0], S2[0]);
     if (tile == 0 && etid == 0) {
         g.info->gemm_r_x = o.r1;
         g.info->gemm_r_y = o.r2;
         g.info->gemm_t_obs = o.T;
     }
     const double t_obs = o.T;
-    const double tau = g.tie_rel * (fabs(g.info->logk_x) + fabs(g.info->logk_y));
     const int lane = etid & 31;
-    constexpr int kRowsPerThread = 2;  // R <= 256 rows over 128 threads
-    RowStat st[kRowsPerThread];
+    named_bar_sync(1, 128);  // s_cnt cleared
 #pragma unroll
-    for (int j = 0; j < kRowsPerThread; ++j) {
-        const int row = etid + 128 * j;
+    for (int j = 0; j < 2; ++j) {
+        const int row = rows[1 + j];
         const int perm = tile * (R - 1) + row - 1;
         const bool valid = row >= 1 && row < R && perm < g.count;
-        st[j] = valid ? row_stat(g, tile, row) : RowStat{0.0, 0.0, 0.0};
-    }
-#pragma unroll
-    for (int j = 0; j < kRowsPerThread; ++j) {
-        const int row = etid + 128 * j;
-        const int perm = tile * (R - 1) + row - 1;
-        const bool valid = row >= 1 && row < R && perm < g.count;
-        const double T = st[j].T;
+        const RowStat st = row_stat(g, S1[1 + j], S2[1 + j]);
+        const double T = st.T;
         const bool ge = valid && (T >= t_obs);
         const bool ab = valid && (fabs(T) >= fabs(t_obs));
         const bool fl = valid && (T == t_obs || fabs(T - t_obs) <= tau || fabs(T) == fabs(t_obs) ||
@@ -131,19 +143,21 @@ __device__ void finalize_tile(const GemmArgs& g, int tile, int etid, double* s_t
         const uint32_t bge = __ballot_sync(0xffffffffu, ge);
         const uint32_t bab = __ballot_sync(0xffffffffu, ab);
         const uint32_t bfl = __ballot_sync(0xffffffffu, fl);
-        if (lane == 0) {
-            unsigned long long* cnt = reinterpret_cast<unsigned long long*>(g.counts);
-            if (bge) atomicAdd(cnt + 0, (unsigned long long)__popc(bge));
-            if (bab) atomicAdd(cnt + 1, (unsigned long long)__popc(bab));
-            if (bfl) atomicAdd(cnt + 2, (unsigned long long)__popc(bfl));
+        if (lane == 0) {  // per-CTA totals first: 3 global atomics per tile
+            if (bge) atomicAdd(s_cnt + 0, (unsigned)__popc(bge));
+            if (bab) atomicAdd(s_cnt + 1, (unsigned)__popc(bab));
+            if (bfl) atomicAdd(s_cnt + 2, (unsigned)__popc(bfl));
         }
         if (g.stats && valid) {
             double* out = g.stats + 3 * (int64_t)perm;
-            out[0] = st[j].r1;
-            out[1] = st[j].r2;
+            out[0] = st.r1;
+            out[1] = st.r2;
             out[2] = T;
         }
     }
+    named_bar_sync(1, 128);
+    if (etid < 3 && s_cnt[etid])
+        atomicAdd(reinterpret_cast<unsigned long long*>(g.counts) + etid, (unsigned long long)s_cnt[etid]);
     if (etid == 0) g.tile_done[tile] = 0;  // ready for the next launch
 }
 
@@ -162,7 +176,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
     int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
-    double* s_tobs = reinterpret_cast<double*>(tmem_slot + 2);
+    unsigned* s_cnt = tmem_slot + 4;  // [3] per-tile counts of the finalize
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) K3_STAMP(7, 0);  // kernel entry
@@ -288,10 +302,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             tempty_c[0] = mapa_shared(smem_u32(&tempty[0]), 0);
             tempty_c[1] = mapa_shared(smem_u32(&tempty[1]), 0);
         }
+        // launch constants for the finalize, loaded while the first piece runs
+        const double S1c = g.sconst[0], S2c = g.sconst[1];
+        const double tau = g.tie_rel * (fabs(g.info->logk_x) + fabs(g.info->logk_y));
         int i = 0;
         for (int pc = pc_begin; pc < pc_end; ++pc, ++i) {
             const int4 pd = g.pieces[pc];
             const int tile = pd.x, width = pd.z;
+            const int np_tile = g.tile_npieces[tile];
             const int a = i & 1;
             mbar_wait(&tfull[a], ((uint32_t)i >> 1) & 1u);
             tc_fence_after();
@@ -299,19 +317,25 @@ __global__ void __launch_bounds__(kThreads, 1)
             // sigma1 = a + acc, sigma2 = b - acc:  |sigma1|^2 - |a|^2 = sum acc (acc + 2a), ...
             float s1 = 0.f, s2 = 0.f;
             const float4* abp = reinterpret_cast<const float4*>(g.ab + pd.y);
-            for (int cb = 0; cb < ((g.exp & 8) ? 0 : width / 32); ++cb) {
-                uint32_t r[32];
-                tmem_ld_32x32b_x32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(a * kChunkN + 32 * cb),
-                                   r);
+            const uint32_t tbase = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(a * kChunkN);
+            const int nblk = (g.exp & 8) ? 0 : width / 32;
+            for (int cb = 0; cb < nblk; cb += 2) {  // two 32-column loads in flight per wait
+                uint32_t r[2][32];
+                tmem_ld_32x32b_x32(tbase + (uint32_t)(32 * cb), r[0]);
+                if (cb + 1 < nblk) tmem_ld_32x32b_x32(tbase + (uint32_t)(32 * cb + 32), r[1]);
                 tmem_ld_wait();
 #pragma unroll
-                for (int j2 = 0; j2 < 16; ++j2) {
-                    const float4 k4 = __ldg(abp + cb * 16 + j2);  // {2a, 2b} of two columns
-                    const float x0 = __uint_as_float(r[2 * j2]), x1 = __uint_as_float(r[2 * j2 + 1]);
-                    s1 = fmaf(x0, x0 + k4.x, s1);
-                    s2 = fmaf(x0, x0 - k4.y, s2);
-                    s1 = fmaf(x1, x1 + k4.z, s1);
-                    s2 = fmaf(x1, x1 - k4.w, s2);
+                for (int h = 0; h < 2; ++h) {
+                    if (cb + h >= nblk) break;
+#pragma unroll
+                    for (int j2 = 0; j2 < 16; ++j2) {
+                        const float4 k4 = __ldg(abp + (cb + h) * 16 + j2);  // {2a, 2b} of two columns
+                        const float x0 = __uint_as_float(r[h][2 * j2]), x1 = __uint_as_float(r[h][2 * j2 + 1]);
+                        s1 = fmaf(x0, x0 + k4.x, s1);
+                        s2 = fmaf(x0, x0 - k4.y, s2);
+                        s1 = fmaf(x1, x1 + k4.z, s1);
+                        s2 = fmaf(x1, x1 - k4.w, s2);
+                    }
                 }
             }
             tc_fence_before();
@@ -326,13 +350,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             named_bar_sync(1, 128);
             if (etid == 0) {
                 const unsigned old = atomicAdd(g.tile_done + tile, 1u);
-                *s_last = (old == (unsigned)(kPair * g.tile_npieces[tile] - 1)) ? 1 : 0;
+                *s_last = (old == (unsigned)(kPair * np_tile - 1)) ? 1 : 0;
             }
             named_bar_sync(1, 128);
             if (*s_last) {
                 __threadfence();
                 if (etid == 0) K3_STAMP(i, 6);
-                finalize_tile(g, tile, etid, s_tobs);
+                finalize_tile(g, tile, np_tile, etid, s_cnt, S1c, S2c, tau);
                 if (etid == 0) K3_STAMP(i, 7);
             }
             named_bar_sync(1, 128);

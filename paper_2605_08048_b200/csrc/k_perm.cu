@@ -24,7 +24,7 @@
 namespace hap {
 namespace {
 
-constexpr int kPermWarps = 4;
+constexpr int kPermWarps = 1;
 constexpr uint16_t kExiled = 0xFFFF;
 
 // U(N-k) for step k: Lemire on the main-stream word x; rejected words are replaced by

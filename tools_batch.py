@@ -63,3 +63,8 @@ print(f"spans: total {span:.1f} us = {span / P:.1f} us/test; " +
       ", ".join(f"{k} med {np.median(v):.1f} us" for k, v in dur.items()))
 for ph, a, b in sorted(sp, key=lambda r: r[1])[:36]:
     print(f"   {ph:12s} {a:9.1f} {b:9.1f} {b - a:7.1f}")
+out = os.environ.get("HAP_SPANS_OUT")
+if out:
+    import json
+    with open(out, "w") as f:
+        json.dump(sp, f)
