@@ -162,7 +162,7 @@ __device__ void finalize_tile(const GemmArgs& g, int tile, int np, int etid, uns
 }
 
 template <int kPair>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __maxnreg__(168)
     k3_maskgemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBhi,
                 const __grid_constant__ CUtensorMap tmBlo, GemmArgs g) {
     using C = Cfg<kPair>;
