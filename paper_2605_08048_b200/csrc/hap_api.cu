@@ -39,15 +39,17 @@ struct hap_ctx_s {
     cudaEvent_t ev_fork = nullptr, ev_ready[2] = {}, ev_free[2] = {};
     int slot = 0;
     bool used[2] = {false, false};
-    // batch pipeline: two sub-contexts (own workspaces + generator streams) on two
-    // internal streams forked from / joined to the caller's stream
-    hap_ctx sub[2] = {nullptr, nullptr};
+    // batch pipeline: two lanes (internal streams forked from / joined to the caller's
+    // stream), each with kMaxWave sub-contexts (own workspaces + generator streams)
+    hap_ctx sub[2][kMaxWave] = {};
     cudaStream_t sub_stream[2] = {nullptr, nullptr};
     cudaEvent_t ev_sub[2] = {nullptr, nullptr};
-    // cached K3 schedules: key {ntiles, d_pad, npairs} -> offset (ints) in buf[kSched]
-    struct Sched { int64_t nt, d_pad, np; int64_t off; int max_slots; };
+    // cached K3 schedules: key {d_pad, npairs, (ntiles, n_pad) per test} -> offset (ints)
+    // in buf[kSched]; new ones are staged in pinned host memory and copied on the stream
+    struct Sched { std::vector<int64_t> key; int64_t off; int max_slots; };
     std::vector<Sched> sched;
     int64_t sched_used = 0;
+    int* sched_host = nullptr;  // pinned staging, same size as buf[kSched]
     // ---- profiling
     bool prof = false;
     bool serial = false;  // profiling level 2: generator on the caller's stream
@@ -166,18 +168,10 @@ hap_status refresh_maps(hap_ctx c, int pair_mode) {
     return HAP_OK;
 }
 
-GemmArgs gemm_args(hap_ctx c, hap_align_info* info) {
+GemmArgs gemm_args(hap_ctx c) {
     GemmArgs g{};
-    g.n_pad = (int)c->n_pad;
     g.d_pad = (int)c->d_pad;
-    g.n_x = (int)c->n_x;
-    g.n_y = (int)c->n_y;
     g.d = (int)c->d;
-    g.info = info;
-    g.ab = B<float2>(c, kAB);
-    g.sconst = B<double>(c, kSconst);
-    g.part = B<float2>(c, kGemmPart);
-    g.tile_done = B<unsigned>(c, kTileDone);
     g.tie_rel = 1e-6;
     const char* ex = getenv("HAP_K3_EXPERIMENT");
     g.exp = ex ? atoi(ex) : 0;
@@ -196,87 +190,107 @@ GemmArgs gemm_args(hap_ctx c, hap_align_info* info) {
 // (K3 piece durations on B200: 15.7 us for widths 32..128, 20.5 us for 256).
 constexpr double kPieceFloor = 4.0 * 196.0;
 
-hap_status get_schedule(hap_ctx c, int64_t nt, int np, cudaStream_t st, GemmArgs& g) {
+hap_status get_schedule(hap_ctx c, const GemmArgs& w, int np, cudaStream_t st, GemmArgs& g) {
+    std::vector<int64_t> key = {w.d_pad, np};
+    for (int k = 0; k < w.G; ++k) {
+        const int64_t nt = (k + 1 < w.G ? w.t[k + 1].tile0 : w.ntiles) - w.t[k].tile0;
+        key.push_back(nt);
+        key.push_back(w.t[k].n_pad);
+    }
+    const int64_t nt_all = w.ntiles;
     for (auto& e : c->sched)
-        if (e.nt == nt && e.d_pad == c->d_pad && e.np == np) {
+        if (e.key == key) {
             const int* base = B<int>(c, kSched) + e.off;
             g.piece_off = base;
             g.tile_npieces = base + (np + 1);
-            g.pieces = reinterpret_cast<const int4*>(base + round_up(np + 1 + nt, 4));
+            g.pieces = reinterpret_cast<const int4*>(base + round_up(np + 1 + nt_all, 4));
             g.max_slots = e.max_slots;
             return HAP_OK;
         }
-    // Piece cost model (cycles per K-stage, measured on B200): tensor-bound 4w (8 MMAs of
-    // 128 x w/256 cycles), but never below the stage round-trip floor.  The 256-column chunks of every tile, in tile-major order, are cut into np
-    // consecutive parts of cost <= M (a chunk is split at a multiple of 32 columns only where
-    // a part ends inside it); M is the smallest feasible makespan (binary search).
-    auto cost = [](int64_t w) { return std::max(4.0 * (double)w, kPieceFloor); };
-    std::vector<int64_t> chunks;  // widths, tile-major
-    for (int64_t t = 0; t < nt; ++t)
-        for (int64_t c0 = 0; c0 < c->d_pad; c0 += kChunkN)
-            chunks.push_back(std::min<int64_t>(kChunkN, c->d_pad - c0));
+    // Piece cost model (cycles, measured on B200): per K-stage tensor-bound 4w (8 MMAs of
+    // 128 x w/256 cycles) but never below the stage round-trip floor; a piece runs
+    // n_pad/64 stages.  The 256-column chunks of every tile (test-major, tile-major) are cut
+    // into np consecutive parts of cost <= M (a chunk is split at a multiple of 32 columns
+    // only where a part ends inside it); M is the smallest feasible makespan (binary search).
+    struct Chunk { int64_t width, nkb, tile, c0; };
+    std::vector<Chunk> chunks;
+    for (int k = 0; k < w.G; ++k) {
+        const int64_t nt = (k + 1 < w.G ? w.t[k + 1].tile0 : w.ntiles) - w.t[k].tile0;
+        for (int64_t t = 0; t < nt; ++t)
+            for (int64_t c0 = 0; c0 < w.d_pad; c0 += kChunkN)
+                chunks.push_back({std::min<int64_t>(kChunkN, w.d_pad - c0), w.t[k].n_pad / kKBlock,
+                                  w.t[k].tile0 + t, c0});
+    }
+    auto cost = [](int64_t wd, int64_t nkb) { return (double)nkb * std::max(4.0 * (double)wd, kPieceFloor); };
     auto fill = [&](double M, std::vector<int>* out_pcs, std::vector<int>* out_off,
                     std::vector<int>* out_npc) {
         size_t ci = 0;
-        int64_t done = 0, t = 0, c0 = 0;
+        int64_t done = 0;
         for (int p = 0; p < np; ++p) {
             if (out_off) (*out_off)[p] = (int)(out_pcs->size() / 4);
             double used = 0.0;
             while (ci < chunks.size()) {
-                const int64_t left = chunks[ci] - done;
-                int64_t w = left;
-                if (used + cost(left) > M) {
-                    w = 0;
+                const Chunk& ch = chunks[ci];
+                const int64_t left = ch.width - done;
+                int64_t wd = left;
+                if (used + cost(left, ch.nkb) > M) {
+                    wd = 0;
                     for (int64_t cand = 32; cand < left; cand += 32)
-                        if (used + cost(cand) <= M) w = cand;
-                    if (w == 0) break;
+                        if (used + cost(cand, ch.nkb) <= M) wd = cand;
+                    if (wd == 0) break;
                 }
-                if (out_pcs) out_pcs->insert(out_pcs->end(), {(int)t, (int)c0, (int)w, (*out_npc)[t]++});
-                used += cost(w);
-                c0 += w;
-                done += w;
-                if (done == chunks[ci]) {
+                if (out_pcs)
+                    out_pcs->insert(out_pcs->end(), {(int)ch.tile, (int)(ch.c0 + done), (int)wd,
+                                                     (*out_npc)[ch.tile]++});
+                used += cost(wd, ch.nkb);
+                done += wd;
+                if (done == ch.width) {
                     ++ci;
                     done = 0;
-                    if (c0 >= c->d_pad) { ++t; c0 = 0; }
                 }
             }
         }
         return ci == chunks.size();
     };
-    double lo = cost(32), hi = 0.0;
-    for (int64_t w : chunks) hi += cost(w);
-    hi += 1.0;
+    double lo = 0.0, hi = 1.0;
+    for (const Chunk& ch : chunks) hi += cost(ch.width, ch.nkb);
     for (int it = 0; it < 40; ++it) {
         const double mid = 0.5 * (lo + hi);
         if (fill(mid, nullptr, nullptr, nullptr)) hi = mid;
         else lo = mid;
     }
-    std::vector<int> off(np + 1, 0), npc(nt, 0), pcs;
+    std::vector<int> off(np + 1, 0), npc(nt_all, 0), pcs;
     fill(hi, &pcs, &off, &npc);
     off[np] = (int)(pcs.size() / 4);
     int max_slots = 1;
     for (int v : npc) max_slots = std::max(max_slots, v);
-    std::vector<int> blob(round_up(np + 1 + nt, 4), 0);
+    std::vector<int> blob(round_up(np + 1 + nt_all, 4), 0);
     std::copy(off.begin(), off.end(), blob.begin());
     std::copy(npc.begin(), npc.end(), blob.begin() + (np + 1));
     blob.insert(blob.end(), pcs.begin(), pcs.end());
-    const int64_t need = (c->sched_used + (int64_t)blob.size()) * (int64_t)sizeof(int);
-    if (need > (int64_t)c->cap[kSched]) {  // start over in a bigger buffer
+    const int64_t need = (int64_t)blob.size();
+    constexpr int64_t kSchedInts = 1 << 20;  // 4 MB ring (device + pinned host staging)
+    if (need > kSchedInts) return fail(c, HAP_E_INVALID_ARG, "K3 schedule too large");
+    if (!c->sched_host) {
+        hap_status s = ensure(c, kSched, (size_t)kSchedInts * sizeof(int));
+        if (s) return s;
+        if (cudaMallocHost(&c->sched_host, (size_t)kSchedInts * sizeof(int)) != cudaSuccess)
+            return fail(c, HAP_E_OOM, "pinned schedule staging");
+    }
+    if (c->sched_used + need > kSchedInts) {  // wrap: the ring's old copies must have run
         if (c->last_stream) cudaStreamSynchronize(c->last_stream);
+        cudaStreamSynchronize(st);
         c->sched.clear();
         c->sched_used = 0;
-        hap_status s = ensure(c, kSched, std::max<int64_t>(need, 1 << 20));
-        if (s) return s;
     }
     const int64_t at = c->sched_used;
-    cudaError_t e = cudaMemcpyAsync(B<int>(c, kSched) + at, blob.data(), blob.size() * sizeof(int),
+    std::copy(blob.begin(), blob.end(), c->sched_host + at);
+    cudaError_t e = cudaMemcpyAsync(B<int>(c, kSched) + at, c->sched_host + at, blob.size() * sizeof(int),
                                     cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // blob is a local vector
     if (e != cudaSuccess) return cuda_fail(c, e, "schedule upload");
-    c->sched.push_back({nt, c->d_pad, np, at, max_slots});
-    c->sched_used = at + round_up((int64_t)blob.size(), 4);
-    return get_schedule(c, nt, np, st, g);
+    c->sched.push_back({key, at, max_slots});
+    c->sched_used = at + round_up(need, 4);
+    return get_schedule(c, w, np, st, g);
 }
 
 constexpr int64_t kMaskBudget = 64ll << 20;  // bytes of bf16 mask per launch (L2-resident)
@@ -402,8 +416,10 @@ hap_status hap_destroy(hap_ctx c) {
         cudaStreamSynchronize(c->side);
         cudaStreamDestroy(c->side);
     }
+    if (c->sched_host) cudaFreeHost(c->sched_host);
     for (int i = 0; i < 2; ++i) {
-        if (c->sub[i]) hap_destroy(c->sub[i]);
+        for (int k = 0; k < kMaxWave; ++k)
+            if (c->sub[i][k]) hap_destroy(c->sub[i][k]);
         if (c->sub_stream[i]) cudaStreamDestroy(c->sub_stream[i]);
         if (c->ev_sub[i]) cudaEventDestroy(c->ev_sub[i]);
     }
@@ -531,89 +547,153 @@ hap_status hap_align(hap_ctx c, const float* X, int64_t n_x, const float* Y, int
     return HAP_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// One test's share of a wave: permutations [b_begin, b_begin + cnt) of an aligned workspace.
+struct WaveTest {
+    hap_ctx w;
+    hap_align_info* info;
+    const hap_perm_cfg* cfg;
+    hap_counts* counts;
+    double* stats;       // rows of this block (already offset), or null
+    uint64_t b_begin;
+    int64_t cnt;
+};
+
+// ONE generator launch (K2) and ONE mask-GEMM launch (K3) for G tests.  `owner` holds the
+// wave buffers (piece partials, tile tickets, schedule) and the generator side stream; each
+// test's masks go to the next mask slot of its own workspace, which K2 rewrites only after
+// the K3 that last read it (event), so K2 can overlap earlier work of other streams.
+hap_status run_wave(hap_ctx owner, int G, const WaveTest* T, int pair, cudaStream_t st) {
+    const int64_t R = (int64_t)kTileM * pair;  // mask rows per tile; row 0 = observed split
+    const int npairs = owner->sm_count / pair;
+    GemmArgs g = gemm_args(owner);
+    GemmMaps maps;
+    PermArgs pa{};
+    pa.G = G;
+    pa.out_kind = kMaskBf16Row;
+    pa.rows_per_tile = (int)R;
+    {
+        static const char* cap = getenv("HAP_K2_MAX_CTAS");  // scheduling experiments
+        pa.max_ctas_per_sm = cap ? atoi(cap) : 0;
+    }
+    g.G = G;
+    g.rows_per_tile = (int)R;
+    g.tie_rel = T[0].cfg->tie_rel > 0 ? T[0].cfg->tie_rel : 1e-6;
+    int slots[kMaxWave];
+    int64_t tiles = 0;
+    hap_status s;
+    for (int k = 0; k < G; ++k) {
+        hap_ctx w = T[k].w;
+        if (w->d_pad != owner->d_pad) return fail(owner, HAP_E_DIM_MISMATCH, "wave tests differ in d");
+        const int64_t nt = std::max<int64_t>(1, ceil_div(T[k].cnt, R - 1));
+        if ((s = ensure(w, kMask, (size_t)nt * R * w->n_pad * 2)) ||
+            (s = ensure(w, kMask1, (size_t)nt * R * w->n_pad * 2)) || (s = refresh_maps(w, pair)))
+            return s == HAP_OK ? s : fail(owner, s, w->err);
+        slots[k] = w->slot;
+        w->slot ^= 1;
+        PermTest& pt = pa.t[k];
+        pt.seed = T[k].cfg->seed;
+        pt.s = T[k].cfg->stream_id;
+        pt.b_begin = T[k].b_begin;
+        pt.count = T[k].cnt;
+        pt.N = w->n_x + w->n_y;
+        pt.n_x = w->n_x;
+        pt.n_pad = w->n_pad;
+        pt.out = w->buf[slots[k] ? kMask1 : kMask];
+        pt.ntiles = (int)nt;
+        GemmTest& gt = g.t[k];
+        gt.n_pad = (int)w->n_pad;
+        gt.n_x = (int)w->n_x;
+        gt.n_y = (int)w->n_y;
+        gt.count = (int)T[k].cnt;
+        gt.tile0 = (int)tiles;
+        gt.info = T[k].info;
+        gt.counts = T[k].counts;
+        gt.stats = T[k].stats;
+        gt.ab = B<float2>(w, kAB);
+        gt.sconst = B<double>(w, kSconst);
+        maps.a[k] = w->tmA[slots[k]];
+        maps.bhi[k] = w->tmBhi;
+        maps.blo[k] = w->tmBlo;
+        tiles += nt;
+    }
+    perm_items(pa);
+    g.ntiles = (int)tiles;
+    g.npairs = npairs;
+    if ((s = ensure(owner, kGemmPart, (size_t)tiles * std::max<int64_t>(1, ceil_div(owner->d_pad, 32)) * R *
+                                          sizeof(float2))) ||
+        (s = ensure(owner, kTileDone, (size_t)tiles * sizeof(unsigned))))
+        return s;
+    g.part = B<float2>(owner, kGemmPart);
+    g.tile_done = B<unsigned>(owner, kTileDone);
+    // K2 on the side stream: each test's slot is rewritten only after the K3 that read it
+    cudaStream_t gs = owner->serial ? st : owner->side;
+    cudaError_t e = cudaSuccess;
+    for (int k = 0; k < G && e == cudaSuccess && !owner->serial; ++k)
+        if (T[k].w->used[slots[k]]) e = cudaStreamWaitEvent(gs, T[k].w->ev_free[slots[k]], 0);
+    if (e == cudaSuccess) {
+        pa.span = next_span(owner, HAP_PHASE_PERMGEN);
+        PhaseScope ps(owner, HAP_PHASE_PERMGEN, 1, gs);
+        e = launch_perm(pa, owner->sm_count, gs);
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(owner->ev_ready[0], gs);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, owner->ev_ready[0], 0);  // join
+    if (e != cudaSuccess) return cuda_fail(owner, e, "perm generator");
+    if ((s = get_schedule(owner, g, npairs, st, g))) return s;
+    {
+        g.span = next_span(owner, HAP_PHASE_MASKGEMM);
+        PhaseScope ps(owner, HAP_PHASE_MASKGEMM, 1, st);
+        e = launch_maskgemm(maps, g, pair, st);
+    }
+    for (int k = 0; k < G && e == cudaSuccess; ++k) {
+        e = cudaEventRecord(T[k].w->ev_free[slots[k]], st);
+        T[k].w->used[slots[k]] = true;
+    }
+    if (e != cudaSuccess) return cuda_fail(owner, e, "mask-GEMM");
+    return HAP_OK;
+}
+
+hap_status check_cfg(hap_ctx c, const hap_perm_cfg* cfg) {
+    if (cfg->b_end < cfg->b_begin || cfg->b_end > (1ull << 32))
+        return fail(c, HAP_E_INVALID_ARG, "need b_begin <= b_end <= 2^32");
+    if (cfg->pair_mode < 0 || cfg->pair_mode > 2) return fail(c, HAP_E_INVALID_ARG, "bad pair_mode");
+    return HAP_OK;
+}
+
+// tiles of one launch for a test of n_pad pooled rows: the block's bf16 mask stays within
+// the L2-resident budget, or cfg->block permutations when set
+int64_t block_tiles(const hap_perm_cfg* cfg, int64_t n_pad, int64_t R) {
+    int64_t t = std::max<int64_t>(1, kMaskBudget / (R * n_pad * 2));
+    if (cfg->block) t = std::max<int64_t>(1, ceil_div((int64_t)cfg->block, R - 1));
+    return t;
+}
+
+}  // namespace
+
+extern "C" {
+
 hap_status hap_permtest(hap_ctx c, hap_align_info* info, const hap_perm_cfg* cfg,
                         hap_counts* counts, double* stats, void* stream) {
     if (!c) return HAP_E_INVALID_ARG;
     if (!c->aligned) return fail(c, HAP_E_NOT_ALIGNED, "hap_permtest before hap_align");
     if (!info || !cfg || !counts) return fail(c, HAP_E_INVALID_ARG, "null pointer");
-    if (cfg->b_end < cfg->b_begin || cfg->b_end > (1ull << 32))
-        return fail(c, HAP_E_INVALID_ARG, "need b_begin <= b_end <= 2^32");
-    if (cfg->pair_mode < 0 || cfg->pair_mode > 2) return fail(c, HAP_E_INVALID_ARG, "bad pair_mode");
+    hap_status s = check_cfg(c, cfg);
+    if (s) return s;
     if (!is_device_ptr(counts) || (stats && !is_device_ptr(stats)))
         return fail(c, HAP_E_INVALID_ARG, "counts/stats must be device memory");
     cudaSetDevice(c->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int pair = cfg->pair_mode ? cfg->pair_mode : 2;
-    const int64_t R = (int64_t)kTileM * pair;  // mask rows per tile; row 0 = observed split
+    const int64_t R = (int64_t)kTileM * pair;
     const int64_t total = (int64_t)(cfg->b_end - cfg->b_begin);
-    // permutations per launch: whole tiles, mask within the L2-resident budget
-    int64_t tiles_max = std::max<int64_t>(1, kMaskBudget / (R * c->n_pad * 2));
-    if (cfg->block) tiles_max = std::max<int64_t>(1, ceil_div((int64_t)cfg->block, R - 1));
-    const int64_t tiles_need = std::max<int64_t>(1, ceil_div(total, R - 1));
-    const int64_t tiles = std::min(tiles_max, tiles_need);
-    const int64_t blk = tiles * (R - 1);
-    const int npairs = c->sm_count / pair;
-    hap_status s;
-    if ((s = ensure(c, kMask, (size_t)tiles * R * c->n_pad * 2)) ||
-        (s = ensure(c, kMask1, (size_t)tiles * R * c->n_pad * 2)) ||
-        (s = ensure(c, kGemmPart, (size_t)tiles * std::max<int64_t>(1, ceil_div(c->d_pad, 32)) * R *
-                                      sizeof(float2))) ||
-        (s = ensure(c, kTileDone, (size_t)tiles * sizeof(unsigned))))
-        return s;
-    if ((s = refresh_maps(c, pair))) return s;
-    cudaError_t e;
-    GemmArgs g = gemm_args(c, info);
-    g.counts = counts;
-    g.rows_per_tile = (int)R;
-    g.tie_rel = cfg->tie_rel > 0 ? cfg->tie_rel : 1e-6;
+    const int64_t blk = block_tiles(cfg, c->n_pad, R) * (R - 1);
     for (int64_t off = 0; off < total; off += blk) {
-        const int64_t cnt = std::min<int64_t>(blk, total - off);
-        const int64_t nt = ceil_div(cnt, R - 1);
-        // mask slots alternate over all launches of the context: the generator of this
-        // block only waits for the mask-GEMM that last read its slot, so it can run
-        // concurrently with the previous block's (or previous test's) mask-GEMM and K1
-        const int slot = c->slot;
-        c->slot ^= 1;
-        PermArgs pa{};
-        pa.seed = cfg->seed;
-        pa.s = cfg->stream_id;
-        pa.b_begin = cfg->b_begin + (uint64_t)off;
-        pa.count = cnt;
-        pa.N = c->n_x + c->n_y;
-        pa.n_x = c->n_x;
-        pa.n_pad = c->n_pad;
-        pa.out = c->buf[slot ? kMask1 : kMask];
-        pa.out_kind = kMaskBf16Row;
-        pa.rows_per_tile = (int)R;
-        pa.ntiles = (int)nt;
-        {
-            static const char* cap = getenv("HAP_K2_MAX_CTAS");  // scheduling experiments
-            pa.max_ctas_per_sm = cap ? atoi(cap) : 0;
-        }
-        pa.span = next_span(c, HAP_PHASE_PERMGEN);
-        // K2 on the side stream; a slot is rewritten only after the K3 that read it
-        cudaStream_t gs = c->serial ? st : c->side;
-        e = (c->used[slot] && !c->serial) ? cudaStreamWaitEvent(gs, c->ev_free[slot], 0) : cudaSuccess;
-        if (e == cudaSuccess) {
-            PhaseScope ps(c, HAP_PHASE_PERMGEN, 1, gs);
-            e = launch_perm(pa, c->sm_count, gs);
-        }
-        if (e == cudaSuccess) e = cudaEventRecord(c->ev_ready[slot], gs);
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, c->ev_ready[slot], 0);  // join
-        if (e != cudaSuccess) return cuda_fail(c, e, "perm generator");
-        g.count = (int)cnt;
-        g.ntiles = (int)nt;
-        g.npairs = npairs;
-        if ((s = get_schedule(c, nt, npairs, st, g))) return s;
-        g.stats = stats ? stats + 3 * off : nullptr;
-        g.span = next_span(c, HAP_PHASE_MASKGEMM);
-        {
-            PhaseScope ps(c, HAP_PHASE_MASKGEMM, 1, st);
-            e = launch_maskgemm(&c->tmA[slot], &c->tmBhi, &c->tmBlo, g, pair, c->sm_count, st);
-        }
-        if (e == cudaSuccess) e = cudaEventRecord(c->ev_free[slot], st);
-        if (e != cudaSuccess) return cuda_fail(c, e, "mask-GEMM");
-        c->used[slot] = true;
+        const WaveTest t{c, info, cfg, counts, stats ? stats + 3 * off : nullptr,
+                         cfg->b_begin + (uint64_t)off, std::min<int64_t>(blk, total - off)};
+        if ((s = run_wave(c, 1, &t, pair, st))) return s;
     }
     c->last_stream = st;
     return HAP_OK;
@@ -627,6 +707,8 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
     if (P < 0 || !X_packed || !Y_packed || !cu_nx || !cu_ny || !cfg || !infos || !counts)
         return fail(c, HAP_E_INVALID_ARG, "null pointer / negative P");
     if (pair_sel && n_sel < 0) return fail(c, HAP_E_INVALID_ARG, "n_sel < 0");
+    hap_status s = check_cfg(c, cfg);
+    if (s) return s;
     if (!is_device_ptr(X_packed) || !is_device_ptr(Y_packed))
         return fail(c, HAP_E_INVALID_ARG, "X_packed / Y_packed must be device memory");
     const int64_t n = pair_sel ? n_sel : P;
@@ -642,35 +724,64 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
     cudaSetDevice(c->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     for (int k = 0; k < 2; ++k) {
-        if (!c->sub[k]) {
-            hap_status s = hap_create(c->device, &c->sub[k]);
-            if (s) return fail(c, s, "sub-context");
-            c->sub[k]->prof = c->prof;
-            c->sub[k]->serial = c->serial;
-        }
+        for (int j = 0; j < kMaxWave; ++j)
+            if (!c->sub[k][j]) {
+                s = hap_create(c->device, &c->sub[k][j]);
+                if (s) return fail(c, s, "sub-context");
+                hap_profile(c->sub[k][j], c->serial ? 2 : c->prof ? 1 : 0);
+                if (c->spans) hap_profile_spans(c->sub[k][j], 1);
+            }
         if (!c->sub_stream[k] &&
             (cudaStreamCreateWithFlags(&c->sub_stream[k], cudaStreamNonBlocking) != cudaSuccess ||
              cudaEventCreateWithFlags(&c->ev_sub[k], cudaEventDisableTiming) != cudaSuccess))
             return fail(c, HAP_E_CUDA, "batch streams");
     }
+    const int pair = cfg->pair_mode ? cfg->pair_mode : 2;
+    const int64_t R = (int64_t)kTileM * pair;
+    const int64_t B = (int64_t)(cfg->b_end - cfg->b_begin);
+    // wave size: tests whose whole b-range is one block may be grouped (HAP_WAVE; default
+    // 1: measured on B200, grouping independent C2/C4 tests does not beat two lanes of
+    // single tests because the lane's K1 launches then serialise); others run alone with
+    // their blocks in sequence
+    static const char* wv = getenv("HAP_WAVE");
+    const int wave_max = std::max(1, std::min(kMaxWave, wv ? atoi(wv) : 1));
     // fork: the two lanes start after the work already on the caller's stream
     cudaError_t e = cudaEventRecord(c->ev_fork, st);
     for (int k = 0; k < 2 && e == cudaSuccess; ++k) e = cudaStreamWaitEvent(c->sub_stream[k], c->ev_fork, 0);
     if (e != cudaSuccess) return cuda_fail(c, e, "batch fork");
-    hap_status s = HAP_OK;
-    for (int64_t i = 0; i < n && !s; ++i) {
-        const int64_t p = pair_sel ? pair_sel[i] : i;
-        const int k = (int)(i & 1);  // consecutive pairs alternate between the two lanes
-        hap_ctx w = c->sub[k];
-        const int64_t nx = cu_nx[p + 1] - cu_nx[p], ny = cu_ny[p + 1] - cu_ny[p];
-        s = hap_align(w, X_packed + cu_nx[p] * d, nx, Y_packed + cu_ny[p] * d, ny, d, mode, infos + p,
-                      c->sub_stream[k]);
-        if (!s) {
-            hap_perm_cfg pc = *cfg;
-            pc.stream_id = cfg->stream_id + (uint32_t)p;
-            s = hap_permtest(w, infos + p, &pc, counts + p, nullptr, c->sub_stream[k]);
+    std::vector<hap_perm_cfg> pcs((size_t)n);
+    int64_t i = 0, wave = 0;
+    while (i < n && !s) {
+        const int k = (int)(wave & 1);  // consecutive waves alternate between the two lanes
+        cudaStream_t ls = c->sub_stream[k];
+        WaveTest T[kMaxWave];
+        int G = 0;
+        while (i < n && G < wave_max) {
+            const int64_t p = pair_sel ? pair_sel[i] : i;
+            const int64_t nx = cu_nx[p + 1] - cu_nx[p], ny = cu_ny[p + 1] - cu_ny[p];
+            const bool one_block = ceil_div(std::max<int64_t>(B, 1), R - 1) <= block_tiles(cfg, round_up(nx + ny, kKBlock), R);
+            if (G > 0 && !one_block) break;  // a multi-block test starts its own wave
+            hap_ctx w = c->sub[k][G];
+            s = hap_align(w, X_packed + cu_nx[p] * d, nx, Y_packed + cu_ny[p] * d, ny, d, mode, infos + p, ls);
+            if (s) {
+                c->err = "pair " + std::to_string(p) + ": " + w->err;
+                break;
+            }
+            pcs[i] = *cfg;
+            pcs[i].stream_id = cfg->stream_id + (uint32_t)p;
+            T[G] = WaveTest{w, infos + p, &pcs[i], counts + p, nullptr, cfg->b_begin, B};
+            ++G;
+            ++i;
+            if (!one_block) break;
         }
-        if (s) c->err = "pair " + std::to_string(p) + ": " + w->err;
+        if (s || G == 0) break;
+        if (G == 1 && ceil_div(std::max<int64_t>(B, 1), R - 1) > block_tiles(cfg, T[0].w->n_pad, R)) {
+            s = hap_permtest(T[0].w, T[0].info, T[0].cfg, T[0].counts, nullptr, ls);  // blocks
+        } else if (B > 0) {
+            s = run_wave(T[0].w, G, T, pair, ls);
+        }
+        if (s) c->err = "wave " + std::to_string(wave) + ": " + T[0].w->err;
+        ++wave;
     }
     // join: the caller's stream waits for both lanes (also on error, to keep ordering sane)
     for (int k = 0; k < 2; ++k) {
@@ -690,11 +801,12 @@ hap_status hap_profile_spans(hap_ctx c, int enable) {
         if (s) return s;
     }
     c->spans = enable != 0;
-    for (hap_ctx w : c->sub)
-        if (w) {
-            hap_status s = hap_profile_spans(w, enable);
-            if (s) return s;
-        }
+    for (auto& lane : c->sub)
+        for (hap_ctx w : lane)
+            if (w) {
+                hap_status s = hap_profile_spans(w, enable);
+                if (s) return s;
+            }
     return HAP_OK;
 }
 
@@ -703,11 +815,15 @@ hap_status hap_profile_spans_read(hap_ctx c, double* out, int64_t max_n, int64_t
     cudaSetDevice(c->device);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return cuda_fail(c, e, "span read");
-    hap_ctx lanes[3] = {c, c->sub[0], c->sub[1]};
+    std::vector<std::pair<hap_ctx, int>> lanes = {{c, 0}};
+    for (int k = 0; k < 2; ++k)
+        for (hap_ctx w : c->sub[k])
+            if (w) lanes.push_back({w, k + 1});
     struct Rec { int code; unsigned long long a, b; };
     std::vector<Rec> recs;
-    for (int lane = 0; lane < 3; ++lane) {
-        hap_ctx w = lanes[lane];
+    for (auto& lw : lanes) {
+        hap_ctx w = lw.first;
+        const int lane = lw.second;
         if (!w || !w->spans || w->span_phase.empty()) continue;
         std::vector<unsigned long long> h(2 * w->span_phase.size());
         e = cudaMemcpy(h.data(), w->buf[kSpans], h.size() * 8, cudaMemcpyDeviceToHost);
@@ -738,8 +854,9 @@ hap_status hap_profile(hap_ctx c, int enable) {
     c->prof = enable != 0;
     c->serial = enable >= 2;
     c->stamp_k1 = enable >= 3;
-    for (hap_ctx w : c->sub)
-        if (w) hap_profile(w, enable);
+    for (auto& lane : c->sub)
+        for (hap_ctx w : lane)
+            if (w) hap_profile(w, enable);
     return HAP_OK;
 }
 
@@ -788,8 +905,9 @@ hap_status hap_profile_read(hap_ctx c, double* ms, int64_t* launches, int reset)
     c->marks.clear();
     double sub_ms[HAP_NUM_PHASES] = {}, sub_sum_ms[HAP_NUM_PHASES] = {};
     int64_t sub_n[HAP_NUM_PHASES] = {}, sub_sum_n[HAP_NUM_PHASES] = {};
-    for (hap_ctx w : c->sub)
-        if (w) {
+    for (auto& lane : c->sub)
+        for (hap_ctx w : lane) {
+            if (!w) continue;
             hap_profile_read(w, sub_ms, sub_n, reset);
             for (int p = 0; p < HAP_NUM_PHASES; ++p) {
                 sub_sum_ms[p] += sub_ms[p];
@@ -810,16 +928,19 @@ hap_status hap_profile_read(hap_ctx c, double* ms, int64_t* launches, int reset)
 hap_status hap_profile_timeline(hap_ctx c, double* out, int64_t max_n, int64_t* n) {
     if (!c || !n) return HAP_E_INVALID_ARG;
     cudaSetDevice(c->device);
-    // lane 0 = this context, lanes 1, 2 = the batch sub-contexts; one common time base
-    hap_ctx lanes[3] = {c, c->sub[0], c->sub[1]};
+    // lane 0 = this context, lanes 1, 2 = the batch lanes' sub-contexts; one time base
+    std::vector<std::pair<hap_ctx, int>> lanes = {{c, 0}};
+    for (int k = 0; k < 2; ++k)
+        for (hap_ctx w : c->sub[k])
+            if (w) lanes.push_back({w, k + 1});
     cudaEvent_t t0 = nullptr;
-    for (hap_ctx w : lanes)
-        if (w && !w->marks.empty() && !t0) t0 = w->marks.front().a;
+    for (auto& lw : lanes)
+        if (!lw.first->marks.empty() && !t0) t0 = lw.first->marks.front().a;
     int64_t k = 0;
     double tmin = 0.0;
-    for (int lane = 0; lane < 3; ++lane) {
-        hap_ctx w = lanes[lane];
-        if (!w) continue;
+    for (auto& lw : lanes) {
+        hap_ctx w = lw.first;
+        const int lane = lw.second;
         for (auto& m : w->marks) {
             float ta = 0.f, tb = 0.f;
             cudaError_t e = cudaEventSynchronize(m.b);
@@ -858,17 +979,19 @@ hap_status hap_perm_sets(hap_ctx c, uint64_t seed, uint32_t stream_id, uint64_t 
     if (b_begin + (uint64_t)count > (1ull << 32)) return fail(c, HAP_E_INVALID_ARG, "b >= 2^32");
     cudaSetDevice(c->device);
     PermArgs pa{};
-    pa.seed = seed;
-    pa.s = stream_id;
-    pa.b_begin = b_begin;
-    pa.count = count;
-    pa.N = N;
-    pa.n_x = n_x;
-    pa.n_pad = round_up(N, kKBlock);
-    pa.out = out;
+    pa.G = 1;
+    pa.t[0].seed = seed;
+    pa.t[0].s = stream_id;
+    pa.t[0].b_begin = b_begin;
+    pa.t[0].count = count;
+    pa.t[0].N = N;
+    pa.t[0].n_x = n_x;
+    pa.t[0].n_pad = round_up(N, kKBlock);
+    pa.t[0].out = out;
+    pa.t[0].ntiles = 0;
     pa.out_kind = kMaskU8Set;
     pa.rows_per_tile = 0;
-    pa.ntiles = 0;
+    perm_items(pa);
     cudaError_t e = launch_perm(pa, c->sm_count, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(c, e, "perm generator");
     return HAP_OK;

@@ -55,50 +55,71 @@ AlignGeom align_geometry(int64_t d);
 cudaError_t launch_align(const AlignArgs& a, int grid, cudaStream_t st);
 constexpr int kAlignLaunches = 1;  // kernels issued by launch_align
 
+// A WAVE is up to kMaxWave independent tests (each aligned in its own workspace) whose
+// generator rows go through ONE K2 launch and whose tiles go through ONE K3 launch: the
+// (test, tile, column) pieces of several tests balance over the CTA pairs far better than
+// one test's.
+constexpr int kMaxWave = 4;
+
 // ---- K2: PERM-SPEC v1 generator (k_perm.cu) ----------------------------------------
 enum MaskOut { kMaskBf16Row = 0, kMaskU8Set = 1 };
-struct PermArgs {
+struct PermTest {
     uint64_t seed;
-    uint32_t s;
+    uint32_t s;              // generator stream id
     uint64_t b_begin;
-    int64_t count;
+    int64_t count;           // permutations b_begin .. b_begin + count
     int64_t N, n_x, n_pad;
     void* out;               // bf16 rows (tile layout) or uint8 [count][N]
+    int ntiles;              // bf16 mode: tiles (each also gets its observed-split row 0)
+};
+struct PermArgs {
+    int G;                   // tests in this launch
+    PermTest t[kMaxWave];
+    int64_t item_off[kMaxWave + 1];  // warp items of test g: [item_off[g], item_off[g+1])
     int out_kind;            // MaskOut
     int rows_per_tile;       // bf16 mode: R; perm p -> row (p/(R-1))*R + 1 + p%(R-1),
                              // row t*R = observed split {0..n_x-1} for t < ntiles
-    int ntiles;
     int max_ctas_per_sm;     // 0 = occupancy limit
     unsigned long long* span;  // optional {first CTA entry, last CTA exit} globaltimer
 };
+// fills item_off from the tests (count + ntiles rows each in bf16 mode)
+void perm_items(PermArgs& a);
 cudaError_t launch_perm(const PermArgs& a, int sm_count, cudaStream_t st);
 
 // ---- K3: tcgen05 mask-GEMM + statistic epilogue (k_maskgemm.cu) --------------------
-struct GemmArgs {
-    int n_pad, d_pad, n_x, n_y, d;
-    int count;               // valid permutations in this launch
-    int ntiles;              // tiles of rows_per_tile mask rows (row 0 = observed split)
-    int npairs;              // CTA pairs (grid / pair_mode)
-    const int4* pieces;      // {tile, col0, width, slot} in (tile, col0) order
-    const int* piece_off;    // [npairs + 1] piece range of each pair
-    const int* tile_npieces; // [ntiles] pieces (= partial slots) per tile
-    int max_slots;           // partial slots per tile (stride)
-    int rows_per_tile;       // 128 * pair_mode
-    double tie_rel;
+struct GemmTest {
+    int n_pad, n_x, n_y;
+    int count;               // valid permutations of this test in the launch
+    int tile0;               // first wave tile of this test (its tiles are contiguous)
     hap_align_info* info;
     hap_counts* counts;
     double* stats;           // optional, [count][3]
     const float2* ab;        // [d_pad] {2a, 2b}
     const double* sconst;    // {sum a^2, sum b^2}
+};
+struct GemmArgs {
+    int d_pad, d;            // shared by the tests of a wave
+    int G;
+    GemmTest t[kMaxWave];
+    int ntiles;              // wave tiles of rows_per_tile mask rows (row 0 = observed split)
+    int npairs;              // CTA pairs (grid / pair_mode)
+    const int4* pieces;      // {wave tile, col0, width, slot} in (tile, col0) order
+    const int* piece_off;    // [npairs + 1] piece range of each pair
+    const int* tile_npieces; // [ntiles] pieces (= partial slots) per tile
+    int max_slots;           // partial slots per tile (stride)
+    int rows_per_tile;       // 128 * pair_mode
+    double tie_rel;
     float2* part;            // [ntiles][max_slots][rows_per_tile] piece partials {s1, s2}
     unsigned* tile_done;     // [ntiles] arrival tickets (zero between launches)
     int exp;                 // timing experiments only (HAP_K3_EXPERIMENT), 0 in production
     long long* stamps;       // exp bit 16: [grid][8 units][8 events] globaltimer
     unsigned long long* span;  // optional {first CTA entry, last CTA exit} globaltimer
 };
+// TMA descriptors of the wave's tests: mask (A), Zt hi / lo planes (B)
+struct GemmMaps {
+    CUtensorMap a[kMaxWave], bhi[kMaxWave], blo[kMaxWave];
+};
 int maskgemm_b_rows(int pair_mode);  // B tile rows per CTA (TMA box)
-cudaError_t launch_maskgemm(const CUtensorMap* tmA, const CUtensorMap* tmBhi,
-                            const CUtensorMap* tmBlo, const GemmArgs& g, int pair_mode, int sm_count,
-                            cudaStream_t st);
+cudaError_t launch_maskgemm(const GemmMaps& maps, const GemmArgs& g, int pair_mode, cudaStream_t st);
 
 }  // namespace hap

@@ -48,7 +48,7 @@ struct Cfg {
     static constexpr int kBRows = kChunkN / kPair;   // B rows (d-columns) held per CTA
     static constexpr int kStageB = kBRows * 128;     // one plane
     static constexpr int kStageBytes = kStageA + 2 * kStageB;
-    static constexpr size_t kSmem = (size_t)kStages * kStageBytes + 1024 + 256;
+    static constexpr size_t kSmem = (size_t)kStages * kStageBytes + 1024 + 512;
 };
 
 
@@ -78,10 +78,10 @@ __device__ __forceinline__ double kappa_hat(double r, double d) {
 
 // statistic of a tile row from its accumulated sums S1 = |sigma1|^2, S2 = |sigma2|^2;
 // T = L(r2) - L(r1) = log(q(r2)/q(r1)): one log (q = 0 gives the +-inf / both-zero cases)
-__device__ __forceinline__ RowStat row_stat(const GemmArgs& g, double S1, double S2) {
+__device__ __forceinline__ RowStat row_stat(const GemmArgs& g, const GemmTest& T, double S1, double S2) {
     RowStat s;
-    s.r1 = sqrt(fmax(S1, 0.0)) / (double)g.n_x;
-    s.r2 = sqrt(fmax(S2, 0.0)) / (double)g.n_y;
+    s.r1 = sqrt(fmax(S1, 0.0)) / (double)T.n_x;
+    s.r2 = sqrt(fmax(S2, 0.0)) / (double)T.n_y;
     const double q1 = kappa_hat(s.r1, (double)g.d), q2 = kappa_hat(s.r2, (double)g.d);
     s.T = (q1 == 0.0 && q2 == 0.0) ? 0.0 : (q1 == 0.0 ? INFINITY : log(q2 / q1));
     return s;
@@ -91,8 +91,8 @@ __device__ __forceinline__ RowStat row_stat(const GemmArgs& g, double S1, double
 // all threads: same partials, same order) and its own permutation rows etid, etid + 128.
 // All partial loads of the three rows are issued together (one L2 round trip per 8 pieces);
 // the piece partials are summed in ascending slot order (deterministic).
-__device__ void finalize_tile(const GemmArgs& g, int tile, int np, int etid, unsigned* s_cnt,
-                              double S1c, double S2c, double tau) {
+__device__ void finalize_tile(const GemmArgs& g, const GemmTest& T, int tile, int lt, int np, int etid,
+                              unsigned* s_cnt, double S1c, double S2c, double tau) {
     const int R = g.rows_per_tile;
     if (etid < 3) s_cnt[etid] = 0u;
     constexpr int kRows = 3;  // row 0, etid, etid + 128 (R <= 256)
@@ -120,11 +120,11 @@ __device__ void finalize_tile(const GemmArgs& g, int tile, int np, int etid, uns
                 S2[k] += (double)v[k][c].y;
             }
     }
-    const RowStat o = row_stat(g, S1[0], S2[0]);
-    if (tile == 0 && etid == 0) {
-        g.info->gemm_r_x = o.r1;
-        g.info->gemm_r_y = o.r2;
-        g.info->gemm_t_obs = o.T;
+    const RowStat o = row_stat(g, T, S1[0], S2[0]);
+    if (lt == 0 && etid == 0) {
+        T.info->gemm_r_x = o.r1;
+        T.info->gemm_r_y = o.r2;
+        T.info->gemm_t_obs = o.T;
     }
     const double t_obs = o.T;
     const int lane = etid & 31;
@@ -132,14 +132,14 @@ __device__ void finalize_tile(const GemmArgs& g, int tile, int np, int etid, uns
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
         const int row = rows[1 + j];
-        const int perm = tile * (R - 1) + row - 1;
-        const bool valid = row >= 1 && row < R && perm < g.count;
-        const RowStat st = row_stat(g, S1[1 + j], S2[1 + j]);
-        const double T = st.T;
-        const bool ge = valid && (T >= t_obs);
-        const bool ab = valid && (fabs(T) >= fabs(t_obs));
-        const bool fl = valid && (T == t_obs || fabs(T - t_obs) <= tau || fabs(T) == fabs(t_obs) ||
-                                  fabs(fabs(T) - fabs(t_obs)) <= tau);
+        const int perm = lt * (R - 1) + row - 1;
+        const bool valid = row >= 1 && row < R && perm < T.count;
+        const RowStat st = row_stat(g, T, S1[1 + j], S2[1 + j]);
+        const double Tb = st.T;
+        const bool ge = valid && (Tb >= t_obs);
+        const bool ab = valid && (fabs(Tb) >= fabs(t_obs));
+        const bool fl = valid && (Tb == t_obs || fabs(Tb - t_obs) <= tau || fabs(Tb) == fabs(t_obs) ||
+                                  fabs(fabs(Tb) - fabs(t_obs)) <= tau);
         const uint32_t bge = __ballot_sync(0xffffffffu, ge);
         const uint32_t bab = __ballot_sync(0xffffffffu, ab);
         const uint32_t bfl = __ballot_sync(0xffffffffu, fl);
@@ -148,26 +148,35 @@ __device__ void finalize_tile(const GemmArgs& g, int tile, int np, int etid, uns
             if (bab) atomicAdd(s_cnt + 1, (unsigned)__popc(bab));
             if (bfl) atomicAdd(s_cnt + 2, (unsigned)__popc(bfl));
         }
-        if (g.stats && valid) {
-            double* out = g.stats + 3 * (int64_t)perm;
+        if (T.stats && valid) {
+            double* out = T.stats + 3 * (int64_t)perm;
             out[0] = st.r1;
             out[1] = st.r2;
-            out[2] = T;
+            out[2] = Tb;
         }
     }
     named_bar_sync(1, 128);
     if (etid < 3 && s_cnt[etid])
-        atomicAdd(reinterpret_cast<unsigned long long*>(g.counts) + etid, (unsigned long long)s_cnt[etid]);
+        atomicAdd(reinterpret_cast<unsigned long long*>(T.counts) + etid, (unsigned long long)s_cnt[etid]);
     if (etid == 0) g.tile_done[tile] = 0;  // ready for the next launch
+}
+
+// test of a wave tile (the tests' tiles are contiguous, in test order)
+__device__ __forceinline__ int test_of(const GemmArgs& g, int tile) {
+    int ti = 0;
+    while (ti + 1 < g.G && tile >= g.t[ti + 1].tile0) ++ti;
+    return ti;
+}
+// a test whose data failed (ZeroVector, DegenerateMean) is skipped by every role alike
+__device__ __forceinline__ bool test_failed(const GemmTest& T) {
+    return *reinterpret_cast<const volatile int*>(&T.info->status) != HAP_OK;
 }
 
 template <int kPair>
 __global__ void __maxnreg__(168)
-    k3_maskgemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBhi,
-                const __grid_constant__ CUtensorMap tmBlo, GemmArgs g) {
+    k3_maskgemm(const __grid_constant__ GemmMaps maps, const GemmArgs g) {
     using C = Cfg<kPair>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    if (g.info->status != HAP_OK) return;  // deferred data error: whole test is a no-op
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
@@ -177,6 +186,7 @@ __global__ void __maxnreg__(168)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
     int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
     unsigned* s_cnt = tmem_slot + 4;  // [3] per-tile counts of the finalize
+    double* s_tc = reinterpret_cast<double*>(tmem_slot + 8);  // [kMaxWave][3] S1c, S2c, tau
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) K3_STAMP(7, 0);  // kernel entry
@@ -184,7 +194,6 @@ __global__ void __maxnreg__(168)
     const uint32_t rank = kPair == 2 ? cluster_ctarank() : 0u;
     const bool leader = rank == 0;
     const int pair_id = blockIdx.x / kPair;
-    const int nkb = g.n_pad / kKBlock;
     const int R = g.rows_per_tile;
     // this pair's pieces: a contiguous, equal-width range of the (tile, column) space
     const int pc_begin = g.piece_off[pair_id], pc_end = g.piece_off[pair_id + 1];
@@ -199,9 +208,17 @@ __global__ void __maxnreg__(168)
             mbar_init(&tempty[a], 4 * kPair);  // one arrival per epilogue warp of the pair
         }
         fence_barrier_init();
-        tma_prefetch_desc(&tmA);
-        tma_prefetch_desc(&tmBhi);
-        tma_prefetch_desc(&tmBlo);
+        for (int ti = 0; ti < g.G; ++ti) {
+            tma_prefetch_desc(&maps.a[ti]);
+            tma_prefetch_desc(&maps.bhi[ti]);
+            tma_prefetch_desc(&maps.blo[ti]);
+        }
+    }
+    if (threadIdx.x >= 64 && threadIdx.x < 64 + g.G) {  // finalize constants per test
+        const GemmTest& T = g.t[threadIdx.x - 64];
+        s_tc[3 * (threadIdx.x - 64) + 0] = T.sconst[0];
+        s_tc[3 * (threadIdx.x - 64) + 1] = T.sconst[1];
+        s_tc[3 * (threadIdx.x - 64) + 2] = g.tie_rel * (fabs(T.info->logk_x) + fabs(T.info->logk_y));
     }
     if (warp == 1) {
         if constexpr (kPair == 2) tmem_alloc_pair<kTmemCols>(tmem_slot);
@@ -220,9 +237,15 @@ __global__ void __maxnreg__(168)
             int stage = 0;
             uint32_t phase = 0;
             for (int pc = pc_begin; pc < pc_end; ++pc) {
-                const int4 pd = g.pieces[pc];  // {tile, col0, width, slot}
+                const int4 pd = g.pieces[pc];  // {wave tile, col0, width, slot}
                 const int tile = pd.x, width = pd.z;
-                const int arow = tile * R + (int)rank * kTileM;
+                const int ti = test_of(g, tile);
+                if (test_failed(g.t[ti])) continue;
+                const int nkb = g.t[ti].n_pad / kKBlock;
+                const CUtensorMap* tmA = &maps.a[ti];
+                const CUtensorMap* tmBhi = &maps.bhi[ti];
+                const CUtensorMap* tmBlo = &maps.blo[ti];
+                const int arow = (tile - g.t[ti].tile0) * R + (int)rank * kTileM;
                 const int brow = pd.y + (int)rank * (width / kPair);
                 const int ui = pc - pc_begin;
                 for (int kb = 0; kb < nkb; ++kb) {
@@ -236,15 +259,15 @@ __global__ void __maxnreg__(168)
                                                ((g.exp & 2) ? C::kStageB : 0);
                         if (leader) mbar_arrive_expect_tx(&full[stage], 2u * bytes);
                         const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
-                        if (!(g.exp & 1)) tma_load_2d_pair(&tmA, fb, sA, kb * kKBlock, arow);
-                        tma_load_2d_pair(&tmBhi, fb, sA + kStageA, kb * kKBlock, brow);
+                        if (!(g.exp & 1)) tma_load_2d_pair(tmA, fb, sA, kb * kKBlock, arow);
+                        tma_load_2d_pair(tmBhi, fb, sA + kStageA, kb * kKBlock, brow);
                         if (!(g.exp & 2))
-                            tma_load_2d_pair(&tmBlo, fb, sA + kStageA + C::kStageB, kb * kKBlock, brow);
+                            tma_load_2d_pair(tmBlo, fb, sA + kStageA + C::kStageB, kb * kKBlock, brow);
                     } else {
                         mbar_arrive_expect_tx(&full[stage], (uint32_t)C::kStageBytes);
-                        tma_load_2d(&tmA, &full[stage], sA, kb * kKBlock, arow);
-                        tma_load_2d(&tmBhi, &full[stage], sA + kStageA, kb * kKBlock, brow);
-                        tma_load_2d(&tmBlo, &full[stage], sA + kStageA + C::kStageB, kb * kKBlock,
+                        tma_load_2d(tmA, &full[stage], sA, kb * kKBlock, arow);
+                        tma_load_2d(tmBhi, &full[stage], sA + kStageA, kb * kKBlock, brow);
+                        tma_load_2d(tmBlo, &full[stage], sA + kStageA + C::kStageB, kb * kKBlock,
                                     brow);
                     }
                     if (++stage == C::kStages) { stage = 0; phase ^= 1u; }
@@ -257,8 +280,11 @@ __global__ void __maxnreg__(168)
             int stage = 0;
             uint32_t phase = 0;
             int i = 0;
-            for (int pc = pc_begin; pc < pc_end; ++pc, ++i) {
+            for (int pc = pc_begin; pc < pc_end; ++pc) {
                 const int width = g.pieces[pc].z;
+                const int ti = test_of(g, g.pieces[pc].x);
+                if (test_failed(g.t[ti])) continue;
+                const int nkb = g.t[ti].n_pad / kKBlock;
                 const uint32_t idesc = idesc_bf16_f32(kTileM * kPair, (uint32_t)width);
                 const int a = i & 1;
                 mbar_wait(&tempty[a], (((uint32_t)i >> 1) & 1u) ^ 1u);
@@ -290,6 +316,7 @@ __global__ void __maxnreg__(168)
                 if constexpr (kPair == 2) umma_commit_pair(&tfull[a], 0x3);
                 else umma_commit(&tfull[a]);
                 K3_STAMP(i, 3);
+                ++i;
             }
         }
     } else {
@@ -302,13 +329,13 @@ __global__ void __maxnreg__(168)
             tempty_c[0] = mapa_shared(smem_u32(&tempty[0]), 0);
             tempty_c[1] = mapa_shared(smem_u32(&tempty[1]), 0);
         }
-        // launch constants for the finalize, loaded while the first piece runs
-        const double S1c = g.sconst[0], S2c = g.sconst[1];
-        const double tau = g.tie_rel * (fabs(g.info->logk_x) + fabs(g.info->logk_y));
         int i = 0;
-        for (int pc = pc_begin; pc < pc_end; ++pc, ++i) {
+        for (int pc = pc_begin; pc < pc_end; ++pc) {
             const int4 pd = g.pieces[pc];
             const int tile = pd.x, width = pd.z;
+            const int ti = test_of(g, tile);
+            const GemmTest& T = g.t[ti];
+            if (test_failed(T)) continue;
             const int np_tile = g.tile_npieces[tile];
             const int a = i & 1;
             mbar_wait(&tfull[a], ((uint32_t)i >> 1) & 1u);
@@ -316,7 +343,7 @@ __global__ void __maxnreg__(168)
             if (etid == 0) K3_STAMP(i, 4);
             // sigma1 = a + acc, sigma2 = b - acc:  |sigma1|^2 - |a|^2 = sum acc (acc + 2a), ...
             float s1 = 0.f, s2 = 0.f;
-            const float4* abp = reinterpret_cast<const float4*>(g.ab + pd.y);
+            const float4* abp = reinterpret_cast<const float4*>(T.ab + pd.y);
             const uint32_t tbase = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(a * kChunkN);
             const int nblk = (g.exp & 8) ? 0 : width / 32;
             for (int cb = 0; cb < nblk; cb += 2) {  // two 32-column loads in flight per wait
@@ -356,10 +383,12 @@ __global__ void __maxnreg__(168)
             if (*s_last) {
                 __threadfence();
                 if (etid == 0) K3_STAMP(i, 6);
-                finalize_tile(g, tile, np_tile, etid, s_cnt, S1c, S2c, tau);
+                finalize_tile(g, T, tile, tile - T.tile0, np_tile, etid, s_cnt, s_tc[3 * ti],
+                              s_tc[3 * ti + 1], s_tc[3 * ti + 2]);
                 if (etid == 0) K3_STAMP(i, 7);
             }
             named_bar_sync(1, 128);
+            ++i;
         }
     }
     tc_fence_before();
@@ -375,8 +404,7 @@ __global__ void __maxnreg__(168)
 }
 
 template <int kPair>
-cudaError_t launch_impl(const CUtensorMap* tmA, const CUtensorMap* tmBhi, const CUtensorMap* tmBlo,
-                        const GemmArgs& g, int sm_count, cudaStream_t st) {
+cudaError_t launch_impl(const GemmMaps& maps, const GemmArgs& g, cudaStream_t st) {
     using C = Cfg<kPair>;
     static bool configured = false;
     if (!configured) {
@@ -385,10 +413,8 @@ cudaError_t launch_impl(const CUtensorMap* tmA, const CUtensorMap* tmBhi, const 
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    const int npairs = g.npairs;
-    (void)sm_count;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((unsigned)(npairs * kPair));
+    cfg.gridDim = dim3((unsigned)(g.npairs * kPair));
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = C::kSmem;
     cfg.stream = st;
@@ -399,19 +425,16 @@ cudaError_t launch_impl(const CUtensorMap* tmA, const CUtensorMap* tmBhi, const 
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k3_maskgemm<kPair>, *tmA, *tmBhi, *tmBlo, g);
+    return cudaLaunchKernelEx(&cfg, k3_maskgemm<kPair>, maps, g);
 }
 
 }  // namespace
 
 int maskgemm_b_rows(int pair_mode) { return kChunkN / pair_mode; }
 
-cudaError_t launch_maskgemm(const CUtensorMap* tmA, const CUtensorMap* tmBhi,
-                            const CUtensorMap* tmBlo, const GemmArgs& g, int pair_mode, int sm_count,
-                            cudaStream_t st) {
+cudaError_t launch_maskgemm(const GemmMaps& maps, const GemmArgs& g, int pair_mode, cudaStream_t st) {
     if (g.ntiles <= 0) return cudaSuccess;
-    return pair_mode == 2 ? launch_impl<2>(tmA, tmBhi, tmBlo, g, sm_count, st)
-                          : launch_impl<1>(tmA, tmBhi, tmBlo, g, sm_count, st);
+    return pair_mode == 2 ? launch_impl<2>(maps, g, st) : launch_impl<1>(maps, g, st);
 }
 
 }  // namespace hap

@@ -53,29 +53,33 @@ __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy(PermArgs a, int lt
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     uint16_t* LT = reinterpret_cast<uint16_t*>(smem) + (size_t)w * (lt_pitch + 128);
     uint16_t* stage = LT + lt_pitch;
-    const uint32_t N = (uint32_t)a.N, nx = (uint32_t)a.n_x, s = a.s;
-    const uint32_t key0 = (uint32_t)(a.seed & 0xFFFFFFFFu), key1 = (uint32_t)(a.seed >> 32);
     const int nw = (int)(blockDim.x >> 5);
     const int64_t wstride = (int64_t)gridDim.x * nw;
-    const int64_t items = a.count + (a.out_kind == kMaskBf16Row ? a.ntiles : 0);
+    const int64_t items = a.item_off[a.G];
     if (l == 0) span_enter(a.span);
     for (int64_t pi = (int64_t)blockIdx.x * nw + w; pi < items; pi += wstride) {
-        if (pi >= a.count) {  // observed split: row 0 of tile (pi - count)
-            const int64_t t = pi - a.count;
-            uint4* row = reinterpret_cast<uint4*>(static_cast<uint16_t*>(a.out) +
-                                                  t * a.rows_per_tile * a.n_pad);
-            for (int64_t v8 = l; v8 < a.n_pad / 8; v8 += 32) {
+        int ti = 0;  // test of this item (the tests' items are contiguous, in test order)
+        while (ti + 1 < a.G && pi >= a.item_off[ti + 1]) ++ti;
+        const PermTest& T = a.t[ti];
+        const int64_t li = pi - a.item_off[ti];
+        const uint32_t N = (uint32_t)T.N, nx = (uint32_t)T.n_x, s = T.s;
+        const uint32_t key0 = (uint32_t)(T.seed & 0xFFFFFFFFu), key1 = (uint32_t)(T.seed >> 32);
+        if (li >= T.count) {  // observed split: row 0 of tile (li - count)
+            const int64_t t = li - T.count;
+            uint4* row = reinterpret_cast<uint4*>(static_cast<uint16_t*>(T.out) +
+                                                  t * a.rows_per_tile * T.n_pad);
+            for (int64_t v8 = l; v8 < T.n_pad / 8; v8 += 32) {
                 uint32_t wds[4];
 #pragma unroll
                 for (int e2 = 0; e2 < 4; ++e2) {
                     const int64_t v = 8 * v8 + 2 * e2;
-                    wds[e2] = (v < a.n_x ? 0x3F80u : 0u) | ((v + 1 < a.n_x ? 0x3F80u : 0u) << 16);
+                    wds[e2] = (v < T.n_x ? 0x3F80u : 0u) | ((v + 1 < T.n_x ? 0x3F80u : 0u) << 16);
                 }
                 row[v8] = make_uint4(wds[0], wds[1], wds[2], wds[3]);
             }
             continue;
         }
-        const uint32_t b = (uint32_t)(a.b_begin + (uint64_t)pi);
+        const uint32_t b = (uint32_t)(T.b_begin + (uint64_t)li);
         uint4* LT4 = reinterpret_cast<uint4*>(LT);
         for (int q = l; q < lt_pitch / 8; q += 32) LT4[q] = make_uint4(0, 0, 0, 0);
         __syncwarp();
@@ -146,10 +150,10 @@ __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy(PermArgs a, int lt
         // ---- phase C: exact 0/1 row
         if (a.out_kind == kMaskBf16Row) {
             const int64_t R1 = a.rows_per_tile - 1;
-            const int64_t orow = (pi / R1) * a.rows_per_tile + 1 + pi % R1;
-            uint4* row = reinterpret_cast<uint4*>(static_cast<uint16_t*>(a.out) + orow * a.n_pad);
+            const int64_t orow = (li / R1) * a.rows_per_tile + 1 + li % R1;
+            uint4* row = reinterpret_cast<uint4*>(static_cast<uint16_t*>(T.out) + orow * T.n_pad);
             const uint4* L4 = reinterpret_cast<const uint4*>(LT);
-            for (int64_t v8 = l; v8 < a.n_pad / 8; v8 += 32) {
+            for (int64_t v8 = l; v8 < T.n_pad / 8; v8 += 32) {
                 const uint4 q = L4[v8];
                 const uint32_t w[4] = {q.x, q.y, q.z, q.w};
                 uint32_t o[4];
@@ -177,7 +181,7 @@ __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy(PermArgs a, int lt
                 row[v8] = make_uint4(o[0], o[1], o[2], o[3]);
             }
         } else {
-            uint8_t* row = static_cast<uint8_t*>(a.out) + pi * a.N;
+            uint8_t* row = static_cast<uint8_t*>(T.out) + li * T.N;
             for (uint32_t v = l; v < N; v += 32) {
                 const uint16_t t = LT[v];
                 row[v] = (v < nx) ? (t != kExiled) : (t != 0);
@@ -196,14 +200,14 @@ __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy(PermArgs a, int lt
 // walks the chains lane-balanced.  Same result bits as k2_perm_fy (tests).
 constexpr uint32_t kExiled32 = 0xFFFFFFFFu;
 
-__device__ __forceinline__ void emit_row_u32(const PermArgs& a, const uint32_t* LT, int64_t pi,
-                                             uint32_t nx, int l) {
+__device__ __forceinline__ void emit_row_u32(const PermArgs& a, const PermTest& T, const uint32_t* LT,
+                                             int64_t li, uint32_t nx, int l) {
     const int64_t R1 = a.rows_per_tile - 1;
-    const int64_t orow = (pi / R1) * a.rows_per_tile + 1 + pi % R1;
-    uint4* row = reinterpret_cast<uint4*>(static_cast<uint16_t*>(a.out) + orow * a.n_pad);
+    const int64_t orow = (li / R1) * a.rows_per_tile + 1 + li % R1;
+    uint4* row = reinterpret_cast<uint4*>(static_cast<uint16_t*>(T.out) + orow * T.n_pad);
     uint4* L4 = reinterpret_cast<uint4*>(const_cast<uint32_t*>(LT));
     const uint4 z = make_uint4(0, 0, 0, 0);
-    for (int v8 = l; v8 < (int)(a.n_pad >> 3); v8 += 32) {
+    for (int v8 = l; v8 < (int)(T.n_pad >> 3); v8 += 32) {
         const uint4 q0 = L4[2 * v8], q1 = L4[2 * v8 + 1];
         L4[2 * v8] = z;  // leave the table zeroed for the next permutation
         L4[2 * v8 + 1] = z;
@@ -229,11 +233,9 @@ __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy32(PermArgs a, int 
     uint32_t* LT = reinterpret_cast<uint32_t*>(smem + (size_t)w * ((size_t)lt_pitch * 5u + 160u));
     uint32_t* sink = LT + lt_pitch + l;  // per-lane target of the atomics of no-op steps
     uint16_t* starts = reinterpret_cast<uint16_t*>(LT + lt_pitch + 32);
-    const uint32_t N = (uint32_t)a.N, nx = (uint32_t)a.n_x, s = a.s;
-    const uint32_t key0 = (uint32_t)(a.seed & 0xFFFFFFFFu), key1 = (uint32_t)(a.seed >> 32);
     const int nw = (int)(blockDim.x >> 5);
     const int64_t wstride = (int64_t)gridDim.x * nw;
-    const int64_t items = a.count + (a.out_kind == kMaskBf16Row ? a.ntiles : 0);
+    const int64_t items = a.item_off[a.G];
     if (l == 0) span_enter(a.span);
     {
         uint4* L4 = reinterpret_cast<uint4*>(LT);
@@ -241,22 +243,28 @@ __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy32(PermArgs a, int 
     }
     __syncwarp();
     for (int64_t pi = (int64_t)blockIdx.x * nw + w; pi < items; pi += wstride) {
-        if (pi >= a.count) {  // observed split: row 0 of tile (pi - count)
-            const int64_t t = pi - a.count;
-            uint4* row = reinterpret_cast<uint4*>(static_cast<uint16_t*>(a.out) +
-                                                  t * a.rows_per_tile * a.n_pad);
-            for (int64_t v8 = l; v8 < a.n_pad / 8; v8 += 32) {
+        int ti = 0;  // test of this item (the tests' items are contiguous, in test order)
+        while (ti + 1 < a.G && pi >= a.item_off[ti + 1]) ++ti;
+        const PermTest& T = a.t[ti];
+        const int64_t li = pi - a.item_off[ti];
+        const uint32_t N = (uint32_t)T.N, nx = (uint32_t)T.n_x, s = T.s;
+        const uint32_t key0 = (uint32_t)(T.seed & 0xFFFFFFFFu), key1 = (uint32_t)(T.seed >> 32);
+        if (li >= T.count) {  // observed split: row 0 of tile (li - count)
+            const int64_t t = li - T.count;
+            uint4* row = reinterpret_cast<uint4*>(static_cast<uint16_t*>(T.out) +
+                                                  t * a.rows_per_tile * T.n_pad);
+            for (int64_t v8 = l; v8 < T.n_pad / 8; v8 += 32) {
                 uint32_t wds[4];
 #pragma unroll
                 for (int e2 = 0; e2 < 4; ++e2) {
                     const int64_t v = 8 * v8 + 2 * e2;
-                    wds[e2] = (v < a.n_x ? 0x3F80u : 0u) | ((v + 1 < a.n_x ? 0x3F80u : 0u) << 16);
+                    wds[e2] = (v < T.n_x ? 0x3F80u : 0u) | ((v + 1 < T.n_x ? 0x3F80u : 0u) << 16);
                 }
                 row[v8] = make_uint4(wds[0], wds[1], wds[2], wds[3]);
             }
             continue;
         }
-        const uint32_t b = (uint32_t)(a.b_begin + (uint64_t)pi);
+        const uint32_t b = (uint32_t)(T.b_begin + (uint64_t)li);
         // ---- phase A: draws + last-writer scatter (atomicMax = largest step wins)
         for (uint32_t k0 = 4u * (uint32_t)l; k0 < nx; k0 += 128u) {
             const u32x4 wd = philox4x32_10(u32x4{k0 >> 2, b, s, 0u}, key0, key1);
@@ -329,9 +337,9 @@ __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy32(PermArgs a, int 
         __syncwarp();
         // ---- phase C: exact 0/1 row (re-zeroes the table)
         if (a.out_kind == kMaskBf16Row) {
-            emit_row_u32(a, LT, pi, nx, l);
+            emit_row_u32(a, T, LT, li, nx, l);
         } else {
-            uint8_t* row = static_cast<uint8_t*>(a.out) + pi * a.N;
+            uint8_t* row = static_cast<uint8_t*>(T.out) + li * T.N;
             for (uint32_t v = l; v < N; v += 32) {
                 const uint32_t t = LT[v];
                 LT[v] = 0u;
@@ -345,9 +353,18 @@ __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy32(PermArgs a, int 
 
 }  // namespace
 
+void perm_items(PermArgs& a) {
+    a.item_off[0] = 0;
+    for (int g = 0; g < a.G; ++g)
+        a.item_off[g + 1] = a.item_off[g] + a.t[g].count + (a.out_kind == kMaskBf16Row ? a.t[g].ntiles : 0);
+}
+
 cudaError_t launch_perm(const PermArgs& a, int sm_count, cudaStream_t st) {
-    if (a.count <= 0) return cudaSuccess;
-    const int lt_pitch = (int)round_up(a.N, 64);  // entries, 128-byte multiple
+    const int64_t items = a.item_off[a.G];
+    if (items <= 0) return cudaSuccess;
+    int64_t maxN = 0;
+    for (int g = 0; g < a.G; ++g) maxN = std::max<int64_t>(maxN, a.t[g].N);
+    const int lt_pitch = (int)round_up(maxN, 64);  // entries, 128-byte multiple; >= every n_pad
     // wide (uint32) table + start list when 4 warps fit in the budget, else uint16 table
     const bool wide = (size_t)lt_pitch * 5u + 160u <= (200u * 1024u) / 4u;
     const size_t per_warp = wide ? (size_t)lt_pitch * 5u + 160u : (size_t)(lt_pitch + 128) * sizeof(uint16_t);
@@ -363,7 +380,7 @@ cudaError_t launch_perm(const PermArgs& a, int sm_count, cudaStream_t st) {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nw * 32, smem);
     per_sm = std::max(1, std::min(per_sm, a.max_ctas_per_sm > 0 ? a.max_ctas_per_sm : per_sm));
-    const int64_t need = ceil_div(a.count + (a.out_kind == kMaskBf16Row ? a.ntiles : 0), nw);
+    const int64_t need = ceil_div(items, nw);
     const int grid = (int)std::min<int64_t>(need, (int64_t)sm_count * per_sm);
     if (wide)
         k2_perm_fy32<<<grid, nw * 32, smem, st>>>(a, lt_pitch);

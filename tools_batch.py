@@ -12,7 +12,8 @@ import paper_2605_08048_b200 as hap
 
 P = int(sys.argv[1]) if len(sys.argv) > 1 else 24
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
-Xp, cnx, Yp, cny = HI.varlen_batch([1000] * P, d=768)
+sizes = [1000] * P if os.environ.get("HAP_SIZES", "c2") == "c2" else HI.c4_sizes(10000)[:P]
+Xp, cnx, Yp, cny = HI.varlen_batch(sizes, d=768)
 X, Y = torch.from_numpy(Xp).cuda(), torch.from_numpy(Yp).cuda()
 ctx = hap.Context(0)
 B = 10000
@@ -32,7 +33,8 @@ for _ in range(reps):
 e1.record()
 e1.synchronize()
 ms = e0.elapsed_time(e1) / reps
-print(f"batch P={P}: {ms * 1e3 / P:.1f} us/test, {P * B / ms * 1e3:.3e} perms/s")
+print(f"batch P={P}: {ms * 1e3 / P:.1f} us/test, {P * B / ms * 1e3:.3e} perms/s, "
+      f"{P / ms * 1e3:.0f} tests/s, mean n {np.mean(sizes):.0f}")
 
 for level in (1, 2):
     hap.hap_profile(ctx.h, level)
