@@ -86,11 +86,19 @@ typedef struct {
     uint32_t stream_id; /* s: third Philox counter word (pair id by default) */
     uint32_t block;     /* B0 permutations per generator/GEMM block; perf only, 0 = auto */
     int32_t pair_mode;  /* K3 CTA grouping: 0 = auto (2), 1 = cta_group::1, 2 = cta_group::2 */
-    int32_t reserved0;
+    int32_t wave;       /* hap_permtest_batch: tests per generator/GEMM launch, 1..4; perf only;
+                         * 0 = auto (1, or 4 with HAP_FLAG_SHARED_MASK) */
     double tie_rel;     /* tie band tau = tie_rel * (|logk_x| + |logk_y|) (R8); <= 0 -> 1e-6 */
-    uint32_t flags;     /* reserved, 0 */
+    uint32_t flags;     /* HAP_FLAG_* */
     uint32_t reserved;
 } hap_perm_cfg;
+
+/* hap_permtest_batch only: every pair uses the SAME permutations, generator stream
+ * s = cfg->stream_id (SPEC.md "shared mode").  Consecutive selected pairs
+ * with equal (n_x, n_y) then share one generated mask block per launch: the generator runs
+ * once per wave instead of once per pair.  Each pair is still an exact permutation test;
+ * the tests are no longer independent of each other. */
+#define HAP_FLAG_SHARED_MASK 1u
 
 /* Exceedance counters of one test, DEVICE memory, ADDED into (caller zeroes them), so
  * shards and resumed ranges compose by summation (Eq. pvalue). */
@@ -140,9 +148,11 @@ HAP_API hap_status hap_permtest(hap_ctx ctx, hap_align_info* info, const hap_per
 /* ---- many word pairs ------------------------------------------------------------ */
 /* Varlen batch of P independent tests (configs 4/5): pair p has X rows
  * X_packed[cu_nx[p] .. cu_nx[p+1]) and Y rows Y_packed[cu_ny[p] .. cu_ny[p+1]).
- * Consecutive selected pairs alternate between two internal lanes (own workspaces and
- * streams, forked from and joined back to `stream`), so one pair's alignment and mask
- * generation overlap the previous pair's mask-GEMM.  Shape errors of any selected pair
+ * Consecutive selected pairs are grouped into waves of cfg->wave tests (see hap_perm_cfg)
+ * that share one generator and one mask-GEMM launch; waves alternate between two internal
+ * lanes (own workspaces and streams, forked from and joined back to `stream`), so one
+ * wave's alignment and mask generation overlap the previous wave's mask-GEMM.  Pair p uses
+ * generator stream cfg->stream_id + p (cfg->stream_id for all with HAP_FLAG_SHARED_MASK).  Shape errors of any selected pair
  * are returned before anything is enqueued.
  *   X_packed, Y_packed [device]; cu_nx, cu_ny [host] int64[P+1] prefix offsets.
  *   pair_sel [host] optional list of the pairs this call handles (NULL = all P); the

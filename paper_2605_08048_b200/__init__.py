@@ -45,7 +45,7 @@ class hap_perm_cfg(ctypes.Structure):
     _fields_ = [("seed", ctypes.c_uint64), ("B", ctypes.c_uint64), ("b_begin", ctypes.c_uint64),
                 ("b_end", ctypes.c_uint64), ("stream_id", ctypes.c_uint32),
                 ("block", ctypes.c_uint32), ("pair_mode", ctypes.c_int32),
-                ("reserved0", ctypes.c_int32), ("tie_rel", ctypes.c_double),
+                ("wave", ctypes.c_int32), ("tie_rel", ctypes.c_double),
                 ("flags", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
 
 
@@ -155,11 +155,15 @@ def hap_align(ctx, X, Y, mode: int, info, stream=None) -> None:
                                 _stream(stream)))
 
 
+HAP_FLAG_SHARED_MASK = 1
+
+
 def make_cfg(seed: int, B: int, b_begin: int = 0, b_end: int | None = None, stream_id: int = 0,
-             block: int = 0, tie_rel: float = 1e-6, pair_mode: int = 0) -> hap_perm_cfg:
+             block: int = 0, tie_rel: float = 1e-6, pair_mode: int = 0, wave: int = 0,
+             flags: int = 0) -> hap_perm_cfg:
     return hap_perm_cfg(seed=seed, B=B, b_begin=b_begin, b_end=B if b_end is None else b_end,
-                        stream_id=stream_id, block=block, pair_mode=pair_mode, reserved0=0,
-                        tie_rel=tie_rel, flags=0, reserved=0)
+                        stream_id=stream_id, block=block, pair_mode=pair_mode, wave=wave,
+                        tie_rel=tie_rel, flags=flags, reserved=0)
 
 
 def hap_permtest(ctx, info, cfg: hap_perm_cfg, counts, stats=None, stream=None) -> None:
@@ -316,15 +320,18 @@ class Context:
 
     def permtest_batch(self, X_packed, cu_nx, Y_packed, cu_ny, B: int, seed: int,
                        stream_id: int = 0, mode: int = 0, tie_rel: float = 1e-6,
-                       pair_sel=None, pair_mode: int = 0, sync: bool = True):
-        """P independent tests of a varlen batch (hap_permtest_batch); pair p draws its
-        permutations from generator stream stream_id + p.  Returns one dict per pair
-        (None for pairs outside pair_sel); a pair whose data failed carries its status."""
+                       pair_sel=None, pair_mode: int = 0, sync: bool = True, wave: int = 0,
+                       shared: bool = False):
+        """P tests of a varlen batch (hap_permtest_batch); pair p draws its permutations
+        from generator stream stream_id + p (shared=True: every pair uses stream_id, one mask
+        block per wave of equal-size pairs).  Returns one dict per pair (None for pairs
+        outside pair_sel); a pair whose data failed carries its status."""
         torch = self.torch
         P = len(cu_nx) - 1
         infos = torch.zeros((P, INFO_BYTES), dtype=torch.uint8, device=self.device)
         counts = torch.zeros((P, COUNTS_WORDS), dtype=torch.int64, device=self.device)
-        cfg = make_cfg(seed, B, 0, B, stream_id, 0, tie_rel, pair_mode)
+        cfg = make_cfg(seed, B, 0, B, stream_id, 0, tie_rel, pair_mode, wave,
+                       HAP_FLAG_SHARED_MASK if shared else 0)
         hap_permtest_batch(self.h, X_packed, cu_nx, Y_packed, cu_ny, mode, cfg, infos, counts,
                            pair_sel)
         if not sync:

@@ -566,7 +566,8 @@ struct WaveTest {
 // wave buffers (piece partials, tile tickets, schedule) and the generator side stream; each
 // test's masks go to the next mask slot of its own workspace, which K2 rewrites only after
 // the K3 that last read it (event), so K2 can overlap earlier work of other streams.
-hap_status run_wave(hap_ctx owner, int G, const WaveTest* T, int pair, cudaStream_t st) {
+hap_status run_wave(hap_ctx owner, int G, const WaveTest* T, int pair, cudaStream_t st,
+                    bool shared = false) {
     const int64_t R = (int64_t)kTileM * pair;  // mask rows per tile; row 0 = observed split
     const int npairs = owner->sm_count / pair;
     GemmArgs g = gemm_args(owner);
@@ -592,8 +593,9 @@ hap_status run_wave(hap_ctx owner, int G, const WaveTest* T, int pair, cudaStrea
         if ((s = ensure(w, kMask, (size_t)nt * R * w->n_pad * 2)) ||
             (s = ensure(w, kMask1, (size_t)nt * R * w->n_pad * 2)) || (s = refresh_maps(w, pair)))
             return s == HAP_OK ? s : fail(owner, s, w->err);
-        slots[k] = w->slot;
-        w->slot ^= 1;
+        // shared masks: every test reads test 0's block (same N, n_x, stream, b-range)
+        slots[k] = (shared && k > 0) ? slots[0] : w->slot;
+        if (!(shared && k > 0)) w->slot ^= 1;
         PermTest& pt = pa.t[k];
         pt.seed = T[k].cfg->seed;
         pt.s = T[k].cfg->stream_id;
@@ -615,11 +617,12 @@ hap_status run_wave(hap_ctx owner, int G, const WaveTest* T, int pair, cudaStrea
         gt.stats = T[k].stats;
         gt.ab = B<float2>(w, kAB);
         gt.sconst = B<double>(w, kSconst);
-        maps.a[k] = w->tmA[slots[k]];
+        maps.a[k] = shared ? T[0].w->tmA[slots[0]] : w->tmA[slots[k]];
         maps.bhi[k] = w->tmBhi;
         maps.blo[k] = w->tmBlo;
         tiles += nt;
     }
+    if (shared) pa.G = 1;  // one generated block serves the whole wave
     perm_items(pa);
     g.ntiles = (int)tiles;
     g.npairs = npairs;
@@ -632,7 +635,7 @@ hap_status run_wave(hap_ctx owner, int G, const WaveTest* T, int pair, cudaStrea
     // K2 on the side stream: each test's slot is rewritten only after the K3 that read it
     cudaStream_t gs = owner->serial ? st : owner->side;
     cudaError_t e = cudaSuccess;
-    for (int k = 0; k < G && e == cudaSuccess && !owner->serial; ++k)
+    for (int k = 0; k < pa.G && e == cudaSuccess && !owner->serial; ++k)
         if (T[k].w->used[slots[k]]) e = cudaStreamWaitEvent(gs, T[k].w->ev_free[slots[k]], 0);
     if (e == cudaSuccess) {
         pa.span = next_span(owner, HAP_PHASE_PERMGEN);
@@ -648,7 +651,7 @@ hap_status run_wave(hap_ctx owner, int G, const WaveTest* T, int pair, cudaStrea
         PhaseScope ps(owner, HAP_PHASE_MASKGEMM, 1, st);
         e = launch_maskgemm(maps, g, pair, st);
     }
-    for (int k = 0; k < G && e == cudaSuccess; ++k) {
+    for (int k = 0; k < pa.G && e == cudaSuccess; ++k) {
         e = cudaEventRecord(T[k].w->ev_free[slots[k]], st);
         T[k].w->used[slots[k]] = true;
     }
@@ -743,8 +746,10 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
     // 1: measured on B200, grouping independent C2/C4 tests does not beat two lanes of
     // single tests because the lane's K1 launches then serialise); others run alone with
     // their blocks in sequence
+    const bool shared = (cfg->flags & HAP_FLAG_SHARED_MASK) != 0;
     static const char* wv = getenv("HAP_WAVE");
-    const int wave_max = std::max(1, std::min(kMaxWave, wv ? atoi(wv) : 1));
+    const int wave_max = std::max(1, std::min(kMaxWave, cfg->wave > 0 ? cfg->wave
+                                                        : wv ? atoi(wv) : shared ? kMaxWave : 1));
     // fork: the two lanes start after the work already on the caller's stream
     cudaError_t e = cudaEventRecord(c->ev_fork, st);
     for (int k = 0; k < 2 && e == cudaSuccess; ++k) e = cudaStreamWaitEvent(c->sub_stream[k], c->ev_fork, 0);
@@ -761,6 +766,7 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
             const int64_t nx = cu_nx[p + 1] - cu_nx[p], ny = cu_ny[p + 1] - cu_ny[p];
             const bool one_block = ceil_div(std::max<int64_t>(B, 1), R - 1) <= block_tiles(cfg, round_up(nx + ny, kKBlock), R);
             if (G > 0 && !one_block) break;  // a multi-block test starts its own wave
+            if (G > 0 && shared && (nx != T[0].w->n_x || ny != T[0].w->n_y)) break;  // same masks
             hap_ctx w = c->sub[k][G];
             s = hap_align(w, X_packed + cu_nx[p] * d, nx, Y_packed + cu_ny[p] * d, ny, d, mode, infos + p, ls);
             if (s) {
@@ -768,7 +774,7 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
                 break;
             }
             pcs[i] = *cfg;
-            pcs[i].stream_id = cfg->stream_id + (uint32_t)p;
+            pcs[i].stream_id = shared ? cfg->stream_id : cfg->stream_id + (uint32_t)p;
             T[G] = WaveTest{w, infos + p, &pcs[i], counts + p, nullptr, cfg->b_begin, B};
             ++G;
             ++i;
@@ -778,7 +784,7 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
         if (G == 1 && ceil_div(std::max<int64_t>(B, 1), R - 1) > block_tiles(cfg, T[0].w->n_pad, R)) {
             s = hap_permtest(T[0].w, T[0].info, T[0].cfg, T[0].counts, nullptr, ls);  // blocks
         } else if (B > 0) {
-            s = run_wave(T[0].w, G, T, pair, ls);
+            s = run_wave(T[0].w, G, T, pair, ls, shared);
         }
         if (s) c->err = "wave " + std::to_string(wave) + ": " + T[0].w->err;
         ++wave;

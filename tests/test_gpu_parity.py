@@ -363,3 +363,39 @@ def test_gpu_batch_sharded_world_invariant(ctx):
     torch.cuda.synchronize()
     assert torch.equal(acc_c, c1)
     assert torch.equal(acc_i.view(torch.uint8), i1)
+
+
+@pytest.mark.parametrize("wave", [2, 3, 4])
+def test_batch_waves_are_bitwise_invariant(ctx, wave):
+    """Several tests per generator/GEMM launch (cfg.wave) give bitwise the same statistics
+    and counts as one test per launch (ragged sizes, several waves and a short last one)."""
+    sizes = [50, 300, 7, 129, 1000, 64, 2, 333, 90]
+    ny = [60, 250, 9, 128, 1000, 64, 3, 300, 91]
+    Xp, cnx, Yp, cny = HI.varlen_batch(sizes, d=96, ny_sizes=ny)
+    X, Y = _cuda(Xp), _cuda(Yp)
+    ref = ctx.permtest_batch(X, cnx, Y, cny, 900, SEED, stream_id=4, wave=1)
+    got = ctx.permtest_batch(X, cnx, Y, cny, 900, SEED, stream_id=4, wave=wave)
+    for p in range(len(sizes)):
+        for k in ("t_obs", "gemm_t_obs", "exceed_ge", "exceed_abs", "flagged"):
+            assert got[p][k] == ref[p][k], (wave, p, k)
+
+
+def test_batch_shared_mask(ctx, orc):
+    """HAP_FLAG_SHARED_MASK: every pair uses generator stream cfg.stream_id; equal-size pairs
+    share one generated block per wave; results equal the oracle (and the single-pair path)
+    run with that stream."""
+    sizes = [120, 120, 120, 120, 120, 64, 64, 120]
+    Xp, cnx, Yp, cny = HI.varlen_batch(sizes, d=128)
+    X, Y = _cuda(Xp), _cuda(Yp)
+    B, s0 = 1500, 21
+    res = ctx.permtest_batch(X, cnx, Y, cny, B, SEED, stream_id=s0, shared=True)
+    for p in range(len(sizes)):
+        Xq, Yq = Xp[cnx[p]:cnx[p + 1]], Yp[cny[p]:cny[p + 1]]
+        ref = orc.run_pair(Xq, Yq, B, SEED, s=s0)
+        Ls = abs(ref["L_x"]) + abs(ref["L_y"])
+        assert abs(res[p]["t_obs"] - ref["t_obs"]) <= 1e-10 * Ls
+        for k in ("exceed_ge", "exceed_abs"):
+            assert abs(res[p][k] - ref[k]) <= ref["flagged"], (p, k)
+        one = ctx.permtest_pair(_cuda(Xq), _cuda(Yq), B, SEED, stream_id=s0)
+        for k in ("gemm_t_obs", "exceed_ge", "exceed_abs", "flagged"):
+            assert one[k] == res[p][k], (p, k)

@@ -12,7 +12,9 @@ import paper_2605_08048_b200 as hap
 
 P = int(sys.argv[1]) if len(sys.argv) > 1 else 24
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
-sizes = [1000] * P if os.environ.get("HAP_SIZES", "c2") == "c2" else HI.c4_sizes(10000)[:P]
+kind = os.environ.get("HAP_SIZES", "c2")
+sizes = [1000] * P if kind == "c2" else [500] * P if kind == "c5" else HI.c4_sizes(10000)[:P]
+shared = os.environ.get("HAP_SHARED", "0") == "1"
 Xp, cnx, Yp, cny = HI.varlen_batch(sizes, d=768)
 X, Y = torch.from_numpy(Xp).cuda(), torch.from_numpy(Yp).cuda()
 ctx = hap.Context(0)
@@ -20,7 +22,7 @@ B = 10000
 
 
 def run():
-    return ctx.permtest_batch(X, cnx, Y, cny, B, HI.PERM_SEED, sync=False)
+    return ctx.permtest_batch(X, cnx, Y, cny, B, HI.PERM_SEED, sync=False, shared=shared)
 
 
 for _ in range(3):
