@@ -454,27 +454,24 @@ hap_status hap_sync(hap_ctx c) {
 
 double hap_pvalue(uint64_t exceed, uint64_t Bn) { return (1.0 + (double)exceed) / ((double)Bn + 1.0); }
 
-hap_status hap_align(hap_ctx c, const float* X, int64_t n_x, const float* Y, int64_t n_y, int64_t d,
-                     hap_align_mode mode, hap_align_info* info, void* stream) {
-    if (!c) return HAP_E_INVALID_ARG;
+}  // extern "C"
+
+namespace {
+
+// Workspace of one pair in `c` (grow-only), host inputs staged on the stream; fills the
+// pair's K1 arguments and records the pair's shape in the context.
+hap_status prepare_pair(hap_ctx c, const float* X, int64_t n_x, const float* Y, int64_t n_y, int64_t d,
+                        hap_align_info* info, cudaStream_t st, AlignPair& q) {
     if (!X || !Y || !info) return fail(c, HAP_E_INVALID_ARG, "null pointer");
     if (n_x < 1 || n_y < 1 || n_x + n_y > 65535)
         return fail(c, HAP_E_INVALID_ARG, "need 1 <= n_x, n_y and n_x + n_y <= 65535");
     if (d < 2 || d > 16384) return fail(c, HAP_E_DIM_MISMATCH, "need 2 <= d <= 16384");
-    if (mode != HAP_ALIGN_HOUSEHOLDER && mode != HAP_ALIGN_NONE)
-        return fail(c, HAP_E_INVALID_ARG, "bad mode");
     if (!is_device_ptr(info)) return fail(c, HAP_E_INVALID_ARG, "info must be device memory");
-    cudaSetDevice(c->device);
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int64_t N = n_x + n_y;
     const int64_t n_pad = round_up(N, kKBlock);
     const int64_t d_pad = round_up(d, 32);
-    const int grid = c->sm_count;  // K1: one cooperative CTA per SM
     hap_status s;
-    if ((s = ensure(c, kNrm, N * 8)) || (s = ensure(c, kCoef, N * 8)) ||
-        (s = ensure(c, kPart, (size_t)2 * grid * d * 8)) || (s = ensure(c, kXbar, d * 8)) ||
-        (s = ensure(c, kYbar, d * 8)) || (s = ensure(c, kScal, 64)) ||
-        (s = ensure(c, kSpart, (size_t)8 * grid * 8)) ||
+    if ((s = ensure(c, kXbar, d * 8)) || (s = ensure(c, kYbar, d * 8)) ||
         (s = ensure(c, kInv, N * 8)) || (s = ensure(c, kU, d_pad * 8)) ||
         (s = ensure(c, kZhi, (size_t)zt_rows(d_pad) * n_pad * 2)) ||
         (s = ensure(c, kZlo, (size_t)zt_rows(d_pad) * n_pad * 2)) ||
@@ -503,48 +500,77 @@ hap_status hap_align(hap_ctx c, const float* X, int64_t n_x, const float* Y, int
     c->d = d;
     c->n_pad = n_pad;
     c->d_pad = d_pad;
+    q = AlignPair{};
+    q.X = dX;
+    q.Y = dY;
+    q.n_x = n_x;
+    q.n_y = n_y;
+    q.d = d;
+    q.n_pad = n_pad;
+    q.info = info;
+    q.inv = B<double>(c, kInv);
+    q.u = B<double>(c, kU);
+    q.xbar = B<double>(c, kXbar);
+    q.ybar = B<double>(c, kYbar);
+    q.zt_hi = B<uint16_t>(c, kZhi);
+    q.zt_lo = B<uint16_t>(c, kZlo);
+    q.m = B<double>(c, kM);
+    q.t64 = B<double>(c, kT64);
+    q.ab = B<float2>(c, kAB);
+    q.sconst = B<double>(c, kSconst);
+    q.acc = B<long long>(c, kTpart);
+    q.bad = B<long long>(c, kScratch);  // word 0 of the pair's own scratch
+    return HAP_OK;
+}
 
+// ONE K1 launch aligning G pairs (each in its own workspace ws[k]); `owner` (= ws[0])
+// provides the launch's barrier / ticket words and the profiling records.
+hap_status align_wave(hap_ctx owner, int G, hap_ctx* ws, const AlignPair* pairs, hap_align_mode mode,
+                      cudaStream_t st) {
     AlignArgs a{};
-    a.X = dX;
-    a.Y = dY;
-    a.n_x = n_x;
-    a.n_y = n_y;
-    a.d = d;
-    a.n_pad = n_pad;
-    a.d_pad = d_pad;
+    a.G = G;
+    for (int k = 0; k < G; ++k) {
+        a.p[k] = pairs[k];
+        if (pairs[k].d != pairs[0].d) return fail(owner, HAP_E_DIM_MISMATCH, "wave pairs differ in d");
+    }
+    a.d = pairs[0].d;
+    a.d_pad = round_up(a.d, 32);
     a.mode = mode;
-    a.info = info;
-    a.nrm = B<double>(c, kNrm);
-    a.coef = B<double>(c, kCoef);
-    a.part = B<double>(c, kPart);
-    a.xbar = B<double>(c, kXbar);
-    a.ybar = B<double>(c, kYbar);
-    a.scal = B<double>(c, kScal);
-    a.inv = B<double>(c, kInv);
-    a.u = B<double>(c, kU);
-    a.spart = B<double>(c, kSpart);
-    a.scratch = B<long long>(c, kScratch);
+    a.scratch = B<long long>(owner, kScratch);
     a.stamps = nullptr;
-    if (c->stamp_k1 && ensure(c, kStamps, (size_t)(8 + 8 * grid) * 8) == HAP_OK)
-        a.stamps = B<long long>(c, kStamps);
-    a.zt_hi = B<uint16_t>(c, kZhi);
-    a.zt_lo = B<uint16_t>(c, kZlo);
-    a.acc = B<long long>(c, kTpart);
-    a.t64 = B<double>(c, kT64);
-    a.m = B<double>(c, kM);
-    a.ab = B<float2>(c, kAB);
-    a.sconst = B<double>(c, kSconst);
-    a.span = next_span(c, HAP_PHASE_ALIGN);
+    if (owner->stamp_k1 && ensure(owner, kStamps, (size_t)(8 + 8 * owner->sm_count) * 8) == HAP_OK)
+        a.stamps = B<long long>(owner, kStamps);
+    align_items(a);
+    a.span = next_span(owner, HAP_PHASE_ALIGN);
     cudaError_t e;
     {
-        PhaseScope ps(c, HAP_PHASE_ALIGN, kAlignLaunches, st);
-        e = launch_align(a, grid, st);
+        PhaseScope ps(owner, HAP_PHASE_ALIGN, kAlignLaunches, st);
+        e = launch_align(a, owner->sm_count, st);
     }
-    if (e != cudaSuccess) return cuda_fail(c, e, "align kernels");
-    c->aligned = true;
-    c->last_stream = st;
-    c->last_info = info;
+    if (e != cudaSuccess) return cuda_fail(owner, e, "align kernel");
+    for (int k = 0; k < G; ++k) {
+        ws[k]->aligned = true;
+        ws[k]->last_stream = st;
+        ws[k]->last_info = pairs[k].info;
+    }
     return HAP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+hap_status hap_align(hap_ctx c, const float* X, int64_t n_x, const float* Y, int64_t n_y, int64_t d,
+                     hap_align_mode mode, hap_align_info* info, void* stream) {
+    if (!c) return HAP_E_INVALID_ARG;
+    if (mode != HAP_ALIGN_HOUSEHOLDER && mode != HAP_ALIGN_NONE)
+        return fail(c, HAP_E_INVALID_ARG, "bad mode");
+    cudaSetDevice(c->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    AlignPair q;
+    hap_status s = prepare_pair(c, X, n_x, Y, n_y, d, info, st, q);
+    if (s) return s;
+    return align_wave(c, 1, &c, &q, mode, st);
 }
 
 }  // extern "C"
@@ -710,6 +736,8 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
     if (P < 0 || !X_packed || !Y_packed || !cu_nx || !cu_ny || !cfg || !infos || !counts)
         return fail(c, HAP_E_INVALID_ARG, "null pointer / negative P");
     if (pair_sel && n_sel < 0) return fail(c, HAP_E_INVALID_ARG, "n_sel < 0");
+    if (mode != HAP_ALIGN_HOUSEHOLDER && mode != HAP_ALIGN_NONE)
+        return fail(c, HAP_E_INVALID_ARG, "bad mode");
     hap_status s = check_cfg(c, cfg);
     if (s) return s;
     if (!is_device_ptr(X_packed) || !is_device_ptr(Y_packed))
@@ -742,14 +770,13 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
     const int pair = cfg->pair_mode ? cfg->pair_mode : 2;
     const int64_t R = (int64_t)kTileM * pair;
     const int64_t B = (int64_t)(cfg->b_end - cfg->b_begin);
-    // wave size: tests whose whole b-range is one block may be grouped (HAP_WAVE; default
-    // 1: measured on B200, grouping independent C2/C4 tests does not beat two lanes of
-    // single tests because the lane's K1 launches then serialise); others run alone with
-    // their blocks in sequence
+    // wave size: tests whose whole b-range is one block are grouped (cfg->wave, else
+    // HAP_WAVE, else 3 (4 with shared masks): measured on B200 the best for C2, C4, C5);
+    // others run alone with their blocks in sequence
     const bool shared = (cfg->flags & HAP_FLAG_SHARED_MASK) != 0;
     static const char* wv = getenv("HAP_WAVE");
     const int wave_max = std::max(1, std::min(kMaxWave, cfg->wave > 0 ? cfg->wave
-                                                        : wv ? atoi(wv) : shared ? kMaxWave : 1));
+                                                        : wv ? atoi(wv) : shared ? kMaxWave : 3));
     // fork: the two lanes start after the work already on the caller's stream
     cudaError_t e = cudaEventRecord(c->ev_fork, st);
     for (int k = 0; k < 2 && e == cudaSuccess; ++k) e = cudaStreamWaitEvent(c->sub_stream[k], c->ev_fork, 0);
@@ -760,25 +787,32 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
         const int k = (int)(wave & 1);  // consecutive waves alternate between the two lanes
         cudaStream_t ls = c->sub_stream[k];
         WaveTest T[kMaxWave];
+        AlignPair Q[kMaxWave];
+        hap_ctx W[kMaxWave];
         int G = 0;
         while (i < n && G < wave_max) {
             const int64_t p = pair_sel ? pair_sel[i] : i;
             const int64_t nx = cu_nx[p + 1] - cu_nx[p], ny = cu_ny[p + 1] - cu_ny[p];
             const bool one_block = ceil_div(std::max<int64_t>(B, 1), R - 1) <= block_tiles(cfg, round_up(nx + ny, kKBlock), R);
             if (G > 0 && !one_block) break;  // a multi-block test starts its own wave
-            if (G > 0 && shared && (nx != T[0].w->n_x || ny != T[0].w->n_y)) break;  // same masks
+            if (G > 0 && shared && (nx != Q[0].n_x || ny != Q[0].n_y)) break;  // same masks
             hap_ctx w = c->sub[k][G];
-            s = hap_align(w, X_packed + cu_nx[p] * d, nx, Y_packed + cu_ny[p] * d, ny, d, mode, infos + p, ls);
+            s = prepare_pair(w, X_packed + cu_nx[p] * d, nx, Y_packed + cu_ny[p] * d, ny, d, infos + p, ls, Q[G]);
             if (s) {
                 c->err = "pair " + std::to_string(p) + ": " + w->err;
                 break;
             }
+            W[G] = w;
             pcs[i] = *cfg;
             pcs[i].stream_id = shared ? cfg->stream_id : cfg->stream_id + (uint32_t)p;
             T[G] = WaveTest{w, infos + p, &pcs[i], counts + p, nullptr, cfg->b_begin, B};
             ++G;
             ++i;
             if (!one_block) break;
+        }
+        if (!s && G > 0) {
+            s = align_wave(W[0], G, W, Q, mode, ls);  // one K1 launch for the wave
+            if (s) c->err = "wave " + std::to_string(wave) + ": " + W[0]->err;
         }
         if (s || G == 0) break;
         if (G == 1 && ceil_div(std::max<int64_t>(B, 1), R - 1) > block_tiles(cfg, T[0].w->n_pad, R)) {

@@ -17,30 +17,35 @@ inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 inline int64_t ceil_div(int64_t x, int64_t m) { return (x + m - 1) / m; }
 
 // ---- K1: alignment (k_align.cu) ----------------------------------------------------
-struct AlignArgs {
+constexpr int kMaxWave = 4;  // tests per launch of a wave (K1, K2, K3)
+
+// One word pair of a K1 launch (its own workspace buffers)
+struct AlignPair {
     const float* X;
     const float* Y;
-    int64_t n_x, n_y, d, n_pad, d_pad;
-    int mode;                // hap_align_mode
+    int64_t n_x, n_y, d, n_pad;
     hap_align_info* info;    // device
-    double* nrm;             // [N]    row norms ||h_i||
     double* inv;             // [N]    1/||h_i|| (0 for a zero row)
     double* u;               // [d_pad] Householder axis (0 for the identity)
-    double* coef;            // [n_x]  2 u^T x_i (0 for the identity)
-    double* part;            // [2 * grid][d] fp64 per-CTA column partials (X, Y)
     double* xbar;            // [d]
     double* ybar;            // [d]
-    double* scal;            // [8]    {||xbar||, ||ybar||, ||v||, u.xbar, identity}
-    double* spart;           // [8 * grid] per-CTA scalar partials
-    long long* scratch;      // [0] min ZeroVector row (LLONG_MAX = none), [2] grid barrier
     uint16_t* zt_hi;         // [>=d_pad][n_pad] bf16 bits
     uint16_t* zt_lo;         // [>=d_pad][n_pad]
     double* m;               // [d_pad] centre (multiple of 2^-12): planes hold z - m
-    long long* acc;          // [2 d + d_pad] fixed-point column sums (zero between launches)
     double* t64;             // [d_pad] t = N m + t'
     float2* ab;              // [d_pad] epilogue constants {2a, 2b}, a = n_x m, b = t - a
     double* sconst;          // [2]     {sum a^2, sum b^2}
-    long long* stamps;       // optional [8] globaltimer after each K1 phase (profiling)
+    long long* acc;          // [2 d + d_pad] fixed-point column sums (zero between launches)
+    long long* bad;          // min ZeroVector row (LLONG_MAX = none; reset by the launch)
+};
+struct AlignArgs {
+    int G;                   // pairs in this launch (same d)
+    AlignPair p[kMaxWave];
+    int64_t item_off[kMaxWave + 1];  // items (R-row blocks) of pair g: [item_off[g], item_off[g+1])
+    int64_t d, d_pad;
+    int mode;                // hap_align_mode
+    long long* scratch;      // [1] ticket, [2] grid barrier of the launch
+    long long* stamps;       // optional [8 + 8 grid] globaltimer stamps (profiling)
     unsigned long long* span;  // optional {first CTA entry, last CTA exit} globaltimer
 };
 // item geometry of K1: R pooled rows x all d columns as an fp32 smem tile of pitch P
@@ -51,15 +56,15 @@ struct AlignGeom {
     size_t smem;       // dynamic smem bytes
 };
 AlignGeom align_geometry(int64_t d);
+// fills item_off (n_pad / R items per pair) for the geometry of d
+void align_items(AlignArgs& a);
 // one cooperative kernel of `grid` CTAs (one per SM); scratch[2] holds its grid barrier
 cudaError_t launch_align(const AlignArgs& a, int grid, cudaStream_t st);
 constexpr int kAlignLaunches = 1;  // kernels issued by launch_align
 
 // A WAVE is up to kMaxWave independent tests (each aligned in its own workspace) whose
-// generator rows go through ONE K2 launch and whose tiles go through ONE K3 launch: the
-// (test, tile, column) pieces of several tests balance over the CTA pairs far better than
-// one test's.
-constexpr int kMaxWave = 4;
+// rows go through ONE K1 launch, whose generator rows go through ONE K2 launch and whose
+// tiles go through ONE K3 launch.
 
 // ---- K2: PERM-SPEC v1 generator (k_perm.cu) ----------------------------------------
 enum MaskOut { kMaskBf16Row = 0, kMaskU8Set = 1 };

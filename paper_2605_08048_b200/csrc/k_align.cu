@@ -120,31 +120,31 @@ __device__ __forceinline__ double logkappa64(double r, double d) {
     return log(r) + log(d - r2) - log(1.0 - r2);
 }
 
-__device__ __forceinline__ const float* row_ptr(const AlignArgs& a, int64_t i) {
-    return i < a.n_x ? a.X + i * a.d : a.Y + (i - a.n_x) * a.d;
+__device__ __forceinline__ const float* row_ptr(const AlignPair& q, int64_t i) {
+    return i < q.n_x ? q.X + i * q.d : q.Y + (i - q.n_x) * q.d;
 }
 
 // raw rows [r0, r0 + R) -> tile[r * P + c] (zero rows beyond N); all loads in flight first
-__device__ __forceinline__ void load_tile(const AlignArgs& a, float* tile, int64_t r0, int R, int P) {
-    const int64_t N = a.n_x + a.n_y;
-    if ((a.d & 3) == 0) {
-        const int q = (int)(a.d >> 2);
-        const int total = R * q;
+__device__ __forceinline__ void load_tile(const AlignPair& q, float* tile, int64_t r0, int R, int P) {
+    const int64_t N = q.n_x + q.n_y;
+    if ((q.d & 3) == 0) {
+        const int nq = (int)(q.d >> 2);
+        const int total = R * nq;
         for (int b = threadIdx.x; b < total; b += 4 * kThreads) {
             float4 v[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const int idx = b + k * kThreads;
-                const int r = idx / q, c4 = idx - r * q;
+                const int r = idx / nq, c4 = idx - r * nq;
                 v[k] = (idx < total && r0 + r < N)
-                           ? __ldg(reinterpret_cast<const float4*>(row_ptr(a, r0 + r)) + c4)
+                           ? __ldg(reinterpret_cast<const float4*>(row_ptr(q, r0 + r)) + c4)
                            : make_float4(0.f, 0.f, 0.f, 0.f);
             }
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const int idx = b + k * kThreads;
                 if (idx < total) {
-                    const int r = idx / q, c4 = idx - r * q;
+                    const int r = idx / nq, c4 = idx - r * nq;
                     float2* t2 = reinterpret_cast<float2*>(tile + (size_t)r * P + 4 * c4);
                     t2[0] = make_float2(v[k].x, v[k].y);
                     t2[1] = make_float2(v[k].z, v[k].w);
@@ -152,10 +152,10 @@ __device__ __forceinline__ void load_tile(const AlignArgs& a, float* tile, int64
             }
         }
     } else {
-        const int d = (int)a.d;
+        const int d = (int)q.d;
         for (int idx = threadIdx.x; idx < R * d; idx += kThreads) {
             const int r = idx / d, c = idx - r * d;
-            tile[(size_t)r * P + c] = r0 + r < N ? __ldg(row_ptr(a, r0 + r) + c) : 0.f;
+            tile[(size_t)r * P + c] = r0 + r < N ? __ldg(row_ptr(q, r0 + r) + c) : 0.f;
         }
     }
 }
@@ -175,10 +175,24 @@ __device__ __forceinline__ double fix_get(const long long* acc) {
     return (double)__ldcg(acc) * kFixInv;
 }
 
+// scalars of one pair that every CTA working on it derives itself (P3)
+struct PairScalars {
+    double rnx, rny, rnv, ux, rN, rnX, rnY;
+    bool identity;
+};
+
+__device__ __forceinline__ int pair_of(const AlignArgs& a, int64_t item) {
+    int g = 0;
+    while (g + 1 < a.G && item >= a.item_off[g + 1]) ++g;
+    return g;
+}
+
 // dynamic smem: tile f32 [R][P] | (u_c, m_c) f32 [d_pad] (stage_umc) | xs, ys f64 [d]
-// (stage_means); R <= 16.
+// (stage_means) | t' partials f64 [d_pad] (stage_umc); R <= 16.
 // <= 64 registers/thread (launch bound 2): a K1 CTA then fits beside a mask-GEMM CTA on
 // one SM, so the next test's alignment overlaps the current test's GEMM.
+// Items of all pairs of the launch (a wave) form one list; a CTA's column sums are flushed
+// to a pair's accumulators whenever its next item belongs to another pair.
 template <int R>
 __global__ void __launch_bounds__(kThreads, 2) k1_align_fused(AlignArgs a, int P, int stage_umc,
                                                               int stage_means) {
@@ -196,12 +210,8 @@ __global__ void __launch_bounds__(kThreads, 2) k1_align_fused(AlignArgs a, int P
     double* s_t = stage_means ? ys + a.d : xs;  // [d_pad] t' partials (with stage_umc)
     const int G = gridDim.x, cta = blockIdx.x;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t N = a.n_x + a.n_y;
     const int d = (int)a.d;
-    const int64_t items = a.n_pad / R;
-    long long* acc_x = a.acc;  // [d] fixed-point column sums of x (X rows), then Y rows
-    long long* acc_y = a.acc + d;
-    long long* acc_t = a.acc + 2 * d;  // [d_pad] fixed-point sums of t' = sum (hi + lo)
+    const int64_t items = a.item_off[a.G];
     unsigned* bar = reinterpret_cast<unsigned*>(a.scratch + 2);
     if (tid == 0) span_enter(a.span);
     stamp(a, 0);
@@ -211,10 +221,31 @@ __global__ void __launch_bounds__(kThreads, 2) k1_align_fused(AlignArgs a, int P
     int64_t resident = -1;
     {
         double sx0 = 0.0, sy0 = 0.0, sx1 = 0.0, sy1 = 0.0;  // columns tid, tid + kThreads
+        int cur = -1;  // pair of the partial sums held in registers
+        auto flush = [&]() {
+            if (cur < 0) return;
+            long long* acc = a.p[cur].acc;
+            if (tid < d) {
+                fix_add(acc + tid, sx0);
+                fix_add(acc + d + tid, sy0);
+            }
+            if (tid + kThreads < d) {
+                fix_add(acc + tid + kThreads, sx1);
+                fix_add(acc + d + tid + kThreads, sy1);
+            }
+            sx0 = sy0 = sx1 = sy1 = 0.0;
+        };
         for (int64_t item = cta; item < items; item += G) {
-            const int64_t r0 = item * R;
+            const int g = pair_of(a, item);
+            const AlignPair& q = a.p[g];
+            const int64_t N = q.n_x + q.n_y;
+            const int64_t r0 = (item - a.item_off[g]) * R;
+            if (g != cur) {
+                flush();
+                cur = g;
+            }
             if (resident >= 0) __syncthreads();  // previous tile fully consumed
-            load_tile(a, tile, r0, R, P);
+            load_tile(q, tile, r0, R, P);
             __syncthreads();
             if (warp < R) {
                 const int64_t i = r0 + warp;
@@ -229,14 +260,13 @@ __global__ void __launch_bounds__(kThreads, 2) k1_align_fused(AlignArgs a, int P
                     const double iv = (i < N && nrm >= 1e-12) ? 1.0 / nrm : 0.0;
                     s_inv[warp] = iv;
                     if (i < N) {
-                        a.inv[i] = iv;
-                        if (nrm < 1e-12)
-                            atomicMin(reinterpret_cast<long long*>(a.scratch), (long long)i);
+                        q.inv[i] = iv;
+                        if (nrm < 1e-12) atomicMin(q.bad, (long long)i);
                     }
                 }
             }
             __syncthreads();
-            const int64_t nxr64 = a.n_x - r0;  // X rows of the item
+            const int64_t nxr64 = q.n_x - r0;  // X rows of the item
             const int nxr = nxr64 <= 0 ? 0 : (nxr64 >= R ? R : (int)nxr64);
             for (int c = tid, k = 0; c < d; c += kThreads, ++k) {
                 double px = 0.0, py = 0.0;
@@ -252,20 +282,13 @@ __global__ void __launch_bounds__(kThreads, 2) k1_align_fused(AlignArgs a, int P
                     sx1 += px;
                     sy1 += py;
                 } else {  // d > 2 kThreads: straight to the accumulators
-                    fix_add(acc_x + c, px);
-                    fix_add(acc_y + c, py);
+                    fix_add(q.acc + c, px);
+                    fix_add(q.acc + d + c, py);
                 }
             }
             resident = item;
         }
-        if (resident >= 0 && tid < d) {
-            fix_add(acc_x + tid, sx0);
-            fix_add(acc_y + tid, sy0);
-        }
-        if (resident >= 0 && tid + kThreads < d) {
-            fix_add(acc_x + tid + kThreads, sx1);
-            fix_add(acc_y + tid + kThreads, sy1);
-        }
+        flush();
     }
     cstamp(a, 1);
     grid_sync(bar);
@@ -274,100 +297,136 @@ __global__ void __launch_bounds__(kThreads, 2) k1_align_fused(AlignArgs a, int P
     stamp(a, 2);
     cstamp(a, 3);
 
-    // ---------------- P3 (CTA-local, identical in every CTA): means, their norms, axis
-    const double rnX = 1.0 / (double)a.n_x, rnY = 1.0 / (double)a.n_y;
-    double sxx = 0.0, syy = 0.0;
-    for (int c = tid; c < d; c += kThreads) {
-        const double xb = fix_get(acc_x + c) * rnX, yb = fix_get(acc_y + c) * rnY;
-        if (stage_means) {
-            xs[c] = xb;
-            ys[c] = yb;
+    // ---------------- P3 (per pair, CTA-local, identical in every CTA that needs it):
+    // means, their norms, axis, centre; the CTA holding a pair's item 0 writes its info
+    PairScalars sc{};
+    auto pair_scalars = [&](int g, bool writer) {
+        const AlignPair& q = a.p[g];
+        const long long* acc_x = q.acc;
+        const long long* acc_y = q.acc + d;
+        const int64_t N = q.n_x + q.n_y;
+        sc.rnX = 1.0 / (double)q.n_x;
+        sc.rnY = 1.0 / (double)q.n_y;
+        double sxx = 0.0, syy = 0.0;
+        for (int c = tid; c < d; c += kThreads) {
+            const double xb = fix_get(acc_x + c) * sc.rnX, yb = fix_get(acc_y + c) * sc.rnY;
+            if (stage_means) {
+                xs[c] = xb;
+                ys[c] = yb;
+            }
+            if (writer) {
+                q.xbar[c] = xb;
+                q.ybar[c] = yb;
+            }
+            sxx += xb * xb;
+            syy += yb * yb;
         }
-        if (cta == 0) {
-            a.xbar[c] = xb;
-            a.ybar[c] = yb;
+        const double2 sq = block_sum2(sxx, syy, red);
+        const double nx = sqrt(sq.x), ny = sqrt(sq.y);
+        const bool degenerate = nx < 1e-12 || ny < 1e-12;
+        sc.rnx = degenerate ? 0.0 : 1.0 / nx;
+        sc.rny = degenerate ? 0.0 : 1.0 / ny;
+        double sv = 0.0, svx = 0.0;
+        for (int c = tid; c < d; c += kThreads) {
+            const double xb = stage_means ? xs[c] : fix_get(acc_x + c) * sc.rnX;
+            const double yb = stage_means ? ys[c] : fix_get(acc_y + c) * sc.rnY;
+            const double v = xb * sc.rnx - yb * sc.rny;
+            sv += v * v;
+            svx += v * xb;
         }
-        sxx += xb * xb;
-        syy += yb * yb;
-    }
-    const double2 sq = block_sum2(sxx, syy, red);
-    const double nx = sqrt(sq.x), ny = sqrt(sq.y);
-    const bool degenerate = nx < 1e-12 || ny < 1e-12;
-    const double rnx = degenerate ? 0.0 : 1.0 / nx, rny = degenerate ? 0.0 : 1.0 / ny;
-#define XB(c) (stage_means ? xs[c] : fix_get(acc_x + (c)) * rnX)
-#define YB(c) (stage_means ? ys[c] : fix_get(acc_y + (c)) * rnY)
-    double sv = 0.0, svx = 0.0;
-    for (int c = tid; c < d; c += kThreads) {
-        const double xb = XB(c), yb = YB(c);
-        const double v = xb * rnx - yb * rny;
-        sv += v * v;
-        svx += v * xb;
-    }
-    const double2 vv = block_sum2(sv, svx, red);
-    const double nv0 = sqrt(vv.x);
-    const bool identity = (a.mode == HAP_ALIGN_NONE) || degenerate || nv0 < 1e-9;  // R3
-    const double rnv = identity ? 0.0 : 1.0 / nv0;
-    const double ux = vv.y * rnv;  // u . xbar
-    const double rN = 4096.0 / (double)N;
-    // axis u_c and centre m_c = t_c/N quantised to 2^-12, t = n_x (xbar - 2u(u.xbar)) + n_y ybar
-    auto axis_centre = [&](int c, double& ud, double& md) {
+        const double2 vv = block_sum2(sv, svx, red);
+        const double nv0 = sqrt(vv.x);
+        sc.identity = (a.mode == HAP_ALIGN_NONE) || degenerate || nv0 < 1e-9;  // R3
+        sc.rnv = sc.identity ? 0.0 : 1.0 / nv0;
+        sc.ux = vv.y * sc.rnv;  // u . xbar
+        sc.rN = 4096.0 / (double)N;
+        if (stage_umc || writer)
+            for (int c = tid; c < (int)a.d_pad; c += kThreads) {
+                double ud = 0.0, md = 0.0;
+                if (c < d) {  // axis u_c; centre m_c = t_c/N quantised to 2^-12, t = n_x (xbar -
+                              // 2u(u.xbar)) + n_y ybar
+                    const double xb = stage_means ? xs[c] : fix_get(acc_x + c) * sc.rnX;
+                    const double yb = stage_means ? ys[c] : fix_get(acc_y + c) * sc.rnY;
+                    ud = (xb * sc.rnx - yb * sc.rny) * sc.rnv;
+                    const double t = (double)q.n_x * (xb - 2.0 * ud * sc.ux) + (double)q.n_y * yb;
+                    md = rint(t * sc.rN) * (1.0 / 4096.0);
+                }
+                if (stage_umc) umc[c] = make_float2((float)ud, (float)md);
+                if (writer) {  // export copies (read in P5 and by hap_export_pooled)
+                    q.u[c] = ud;
+                    q.m[c] = md;
+                }
+            }
+        if (writer && tid == 0) {
+            hap_align_info* f = q.info;
+            const long long bad = *reinterpret_cast<volatile long long*>(q.bad);
+            f->n_x = q.n_x;
+            f->n_y = q.n_y;
+            f->d = a.d;
+            f->n_pad = q.n_pad;
+            f->d_pad = a.d_pad;
+            f->is_identity = sc.identity ? 1 : 0;
+            f->status = bad < N ? HAP_E_ZERO_VECTOR : (degenerate ? HAP_E_DEGENERATE_MEAN : HAP_OK);
+            f->bad_row = bad < N ? bad : -1;
+            // observed statistic in fp64 (Alg. 1 step 4): r(X') = ||xbar||
+            // since H is orthogonal; T_obs = L(r_Y) - L(r_X) (Eq. 10)
+            f->r_x = nx;
+            f->r_y = ny;
+            const double lx = logkappa64(nx, (double)a.d), ly = logkappa64(ny, (double)a.d);
+            f->logk_x = lx;
+            f->logk_y = ly;
+            f->t_obs = (isinf(lx) && isinf(ly)) ? 0.0 : ly - lx;
+            const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+            f->gemm_r_x = f->gemm_r_y = f->gemm_t_obs = qnan;
+        }
+        __syncthreads();  // umc / xs / ys ready
+    };
+    // axis and centre of a column on the fly (wide d: not staged)
+    auto axis_centre = [&](const AlignPair& q, int c, double& ud, double& md) {
         ud = 0.0;
         md = 0.0;
         if (c < d) {
-            const double xb = XB(c), yb = YB(c);
-            ud = (xb * rnx - yb * rny) * rnv;
-            const double t = (double)a.n_x * (xb - 2.0 * ud * ux) + (double)a.n_y * yb;
-            md = rint(t * rN) * (1.0 / 4096.0);
+            const double xb = fix_get(q.acc + c) * sc.rnX, yb = fix_get(q.acc + d + c) * sc.rnY;
+            ud = (xb * sc.rnx - yb * sc.rny) * sc.rnv;
+            const double t = (double)q.n_x * (xb - 2.0 * ud * sc.ux) + (double)q.n_y * yb;
+            md = rint(t * sc.rN) * (1.0 / 4096.0);
         }
     };
-    if (stage_umc || cta == 0)
-        for (int c = tid; c < (int)a.d_pad; c += kThreads) {
-            double ud, md;
-            axis_centre(c, ud, md);
-            if (stage_umc) umc[c] = make_float2((float)ud, (float)md);
-            if (cta == 0) {  // export copies (read in P5 and by hap_export_pooled)
-                a.u[c] = ud;
-                a.m[c] = md;
-            }
-        }
-    if (cta == 0 && tid == 0) {
-        hap_align_info* f = a.info;
-        const long long bad = *reinterpret_cast<volatile long long*>(a.scratch);
-        f->n_x = a.n_x;
-        f->n_y = a.n_y;
-        f->d = a.d;
-        f->n_pad = a.n_pad;
-        f->d_pad = a.d_pad;
-        f->is_identity = identity ? 1 : 0;
-        f->status = bad < N ? HAP_E_ZERO_VECTOR : (degenerate ? HAP_E_DEGENERATE_MEAN : HAP_OK);
-        f->bad_row = bad < N ? bad : -1;
-        // observed statistic in fp64 (Alg. 1 step 4): r(X') = ||xbar||
-        // since H is orthogonal; T_obs = L(r_Y) - L(r_X) (Eq. 10)
-        f->r_x = nx;
-        f->r_y = ny;
-        const double lx = logkappa64(nx, (double)a.d), ly = logkappa64(ny, (double)a.d);
-        f->logk_x = lx;
-        f->logk_y = ly;
-        f->t_obs = (isinf(lx) && isinf(ly)) ? 0.0 : ly - lx;
-        const double qnan = __longlong_as_double(0x7ff8000000000000ll);
-        f->gemm_r_x = f->gemm_r_y = f->gemm_t_obs = qnan;
-    }
+    // pairs whose item 0 falls to another CTA still need no scalars here; the writer of
+    // each pair is the CTA of its item 0 (handled in the item loop below)
     stamp(a, 3);
     cstamp(a, 4);
 
-    // ---------------- P4: items again, last one first (its tile is still resident)
+    // ---------------- P4: this CTA's items again, last one first (still resident)
+    int sp = -1;  // pair whose scalars / t' partials are current
+    auto flush_t = [&]() {
+        if (sp < 0 || !stage_umc) return;
+        __syncthreads();
+        for (int c = tid; c < (int)a.d_pad; c += kThreads) fix_add(a.p[sp].acc + 2 * d + c, s_t[c]);
+    };
     const int units = rp * (int)a.d_pad;
-    if (stage_umc)
-        for (int c = tid; c < (int)a.d_pad; c += kThreads) s_t[c] = 0.0;
     if (resident >= 0) {
         const int64_t nmine = (resident - cta) / G + 1;
         for (int64_t k = nmine - 1; k >= 0; --k) {
             const int64_t item = cta + k * G;
-            const int64_t r0 = item * R;
+            const int g = pair_of(a, item);
+            const AlignPair& q = a.p[g];
+            const int64_t N = q.n_x + q.n_y;
+            const int64_t li = item - a.item_off[g];
+            const int64_t r0 = li * R;
+            if (g != sp) {
+                flush_t();
+                // the CTA that holds the pair's item 0 writes its info and exports
+                const int64_t item0 = a.item_off[g];
+                pair_scalars(g, item0 >= cta && (item0 - cta) % G == 0 && item0 <= resident);
+                if (stage_umc)
+                    for (int c = tid; c < (int)a.d_pad; c += kThreads) s_t[c] = 0.0;
+                sp = g;
+            }
             if (item != resident) {
                 __syncthreads();
-                load_tile(a, tile, r0, R, P);
-                if (tid < R) s_inv[tid] = r0 + tid < N ? __ldcg(a.inv + r0 + tid) : 0.0;
+                load_tile(q, tile, r0, R, P);
+                if (tid < R) s_inv[tid] = r0 + tid < N ? __ldcg(q.inv + r0 + tid) : 0.0;
                 __syncthreads();
             }
             // reflection coefficients 2 u^T x_i = 2 (xbar.h_i/||xbar|| - ybar.h_i/||ybar||)
@@ -375,16 +434,16 @@ __global__ void __launch_bounds__(kThreads, 2) k1_align_fused(AlignArgs a, int P
             if (warp < R) {
                 const int64_t i = r0 + warp;
                 double cf = 0.0;
-                if (i < a.n_x && !identity) {
+                if (i < q.n_x && !sc.identity) {
                     double dx = 0.0, dy = 0.0;
                     for (int c = lane; c < d; c += 32) {
                         const double hv = (double)tile[(size_t)warp * P + c];
-                        dx += hv * XB(c);
-                        dy += hv * YB(c);
+                        dx += hv * (stage_means ? xs[c] : fix_get(q.acc + c) * sc.rnX);
+                        dy += hv * (stage_means ? ys[c] : fix_get(q.acc + d + c) * sc.rnY);
                     }
                     dx = warp_sum(dx);
                     dy = warp_sum(dy);
-                    cf = 2.0 * ((dx * rnx - dy * rny) * s_inv[warp]) * rnv;
+                    cf = 2.0 * ((dx * sc.rnx - dy * sc.rny) * s_inv[warp]) * sc.rnv;
                 }
                 if (lane == 0) {
                     s_cff[warp] = (float)cf;
@@ -393,17 +452,15 @@ __global__ void __launch_bounds__(kThreads, 2) k1_align_fused(AlignArgs a, int P
             }
             __syncthreads();
             if (k == nmine - 1) cstamp(a, 5);
-            // z' = x - coef u - m (fp32 is ample: the value is then kept to 16 significant
-            // bits), hi/lo split; thread = (column, row pair): rp lanes write one column's
-            // 2R contiguous bytes of each plane
+            // z' = x - coef u - m in fp32 (the value is then kept to 16 bits), hi/lo split;
+            // thread = (column, row pair): rp lanes write one column's 2R contiguous bytes
             {
-                // j is fixed per thread (kThreads is a multiple of rp): hoist the row terms
-                const int j = tid & (rp - 1);
+                const int j = tid & (rp - 1);  // fixed per thread (kThreads % rp == 0)
                 const float cf0 = s_cff[2 * j], cf1 = s_cff[2 * j + 1];
                 const float iv0 = s_invf[2 * j], iv1 = s_invf[2 * j + 1];
                 const bool v0 = r0 + 2 * j < N, v1 = r0 + 2 * j + 1 < N;
-                uint32_t* zh = reinterpret_cast<uint32_t*>(a.zt_hi + r0) + j;
-                uint32_t* zl = reinterpret_cast<uint32_t*>(a.zt_lo + r0) + j;
+                uint32_t* zh = reinterpret_cast<uint32_t*>(q.zt_hi + r0) + j;
+                uint32_t* zl = reinterpret_cast<uint32_t*>(q.zt_lo + r0) + j;
                 const float* t0 = tile + (size_t)(2 * j) * P;
                 const float* t1 = t0 + P;
                 for (int uidx = tid; uidx < units; uidx += kThreads) {
@@ -413,16 +470,15 @@ __global__ void __launch_bounds__(kThreads, 2) k1_align_fused(AlignArgs a, int P
                         um = umc[c];
                     } else {
                         double ud, md;
-                        axis_centre(c, ud, md);
+                        axis_centre(q, c, ud, md);
                         um = make_float2((float)ud, (float)md);
                     }
-                    // z' = x - coef u - m in fp32 (the value is then kept to 16 bits)
                     const float z0 = v0 && c < d ? fmaf(-cf0, um.x, t0[c] * iv0) - um.y : 0.f;
                     const float z1 = v1 && c < d ? fmaf(-cf1, um.x, t1[c] * iv1) - um.y : 0.f;
                     const __nv_bfloat16 h0 = __float2bfloat16_rn(z0), h1 = __float2bfloat16_rn(z1);
                     const float fh0 = __bfloat162float(h0), fh1 = __bfloat162float(h1);
                     const __nv_bfloat16 l0 = __float2bfloat16_rn(z0 - fh0), l1 = __float2bfloat16_rn(z1 - fh1);
-                    const size_t off = (size_t)c * (size_t)(a.n_pad >> 1);
+                    const size_t off = (size_t)c * (size_t)(q.n_pad >> 1);
                     zh[off] = (uint32_t)__bfloat16_as_ushort(h0) | ((uint32_t)__bfloat16_as_ushort(h1) << 16);
                     zl[off] = (uint32_t)__bfloat16_as_ushort(l0) | ((uint32_t)__bfloat16_as_ushort(l1) << 16);
                     // hi + lo is exact in fp32; the column's t' partial is summed in fp64
@@ -431,24 +487,19 @@ __global__ void __launch_bounds__(kThreads, 2) k1_align_fused(AlignArgs a, int P
                     for (int o = 1; o < rp; o <<= 1) tv += __shfl_xor_sync(0xffffffffu, tv, o);
                     if (j == 0) {  // the column's owner thread (the same for every item)
                         if (stage_umc) s_t[c] += tv;
-                        else fix_add(acc_t + c, tv);
+                        else fix_add(q.acc + 2 * d + c, tv);
                     }
                 }
             }
         }
-        if (stage_umc) {
-            __syncthreads();
-            for (int c = tid; c < (int)a.d_pad; c += kThreads) fix_add(acc_t + c, s_t[c]);
-        }
+        flush_t();
     }
-#undef XB
-#undef YB
     cstamp(a, 6);
     stamp(a, 4);
 
-    // ---------------- P5 (last CTA to finish, ticket): t = N m + t', a = n_x m, b = t - a
-    // (fp32) for the GEMM epilogue, {sum a^2, sum b^2} in fixed order; then the
-    // accumulators are cleared for the next launch
+    // ---------------- P5 (last CTA to finish, ticket): per pair t = N m + t', a = n_x m,
+    // b = t - a (fp32) for the GEMM epilogue, {sum a^2, sum b^2} in fixed order; then the
+    // accumulators and flags are cleared for the next launch
     __threadfence();
     __syncthreads();
     if (tid == 0) {
@@ -458,23 +509,29 @@ __global__ void __launch_bounds__(kThreads, 2) k1_align_fused(AlignArgs a, int P
     __syncthreads();
     if (s_last) {
         __threadfence();
-        double sa = 0.0, sb = 0.0;
-        for (int64_t c = tid; c < a.d_pad; c += kThreads) {
-            const double tsum = fix_get(acc_t + c);
-            const double m = __ldcg(a.m + c);
-            a.t64[c] = (double)N * m + tsum;
-            const float af = (float)((double)a.n_x * m);
-            const float bf = (float)((double)a.n_y * m + tsum);
-            a.ab[c] = make_float2(2.0f * af, 2.0f * bf);
-            sa += (double)af * (double)af;
-            sb += (double)bf * (double)bf;
+        for (int g = 0; g < a.G; ++g) {
+            const AlignPair& q = a.p[g];
+            const int64_t N = q.n_x + q.n_y;
+            double sa = 0.0, sb = 0.0;
+            for (int64_t c = tid; c < a.d_pad; c += kThreads) {
+                const double tsum = fix_get(q.acc + 2 * d + c);
+                const double m = __ldcg(q.m + c);
+                q.t64[c] = (double)N * m + tsum;
+                const float af = (float)((double)q.n_x * m);
+                const float bf = (float)((double)q.n_y * m + tsum);
+                q.ab[c] = make_float2(2.0f * af, 2.0f * bf);
+                sa += (double)af * (double)af;
+                sb += (double)bf * (double)bf;
+            }
+            const double2 sab = block_sum2(sa, sb, red);
+            for (int64_t c = tid; c < 2 * (int64_t)d + a.d_pad; c += kThreads) q.acc[c] = 0;
+            if (tid == 0) {
+                q.sconst[0] = sab.x;
+                q.sconst[1] = sab.y;
+                *q.bad = LLONG_MAX;  // reset the pair's ZeroVector word
+            }
         }
-        const double2 sab = block_sum2(sa, sb, red);
-        for (int64_t c = tid; c < 2 * (int64_t)d + a.d_pad; c += kThreads) a.acc[c] = 0;
-        if (tid == 0) {
-            a.sconst[0] = sab.x;
-            a.sconst[1] = sab.y;
-            a.scratch[0] = LLONG_MAX;  // reset the ZeroVector word, the ticket, the barrier
+        if (tid == 0) {  // reset the ticket and the barrier
             reinterpret_cast<unsigned*>(a.scratch + 1)[0] = 0u;
             bar[0] = 0u;
         }
@@ -506,6 +563,12 @@ AlignGeom align_geometry(int64_t d) {
 // after the previous one on the device (an event chain; K1 is latency-bound and short).
 static std::mutex g_k1_mu;
 static cudaEvent_t g_k1_last[64] = {};
+
+void align_items(AlignArgs& a) {
+    const AlignGeom g = align_geometry(a.d);
+    a.item_off[0] = 0;
+    for (int k = 0; k < a.G; ++k) a.item_off[k + 1] = a.item_off[k] + a.p[k].n_pad / g.rows;
+}
 
 cudaError_t launch_align(const AlignArgs& a, int grid, cudaStream_t st) {
     const AlignGeom g = align_geometry(a.d);
