@@ -2,9 +2,10 @@
 """bench.py — throughput of the Householder-aligned permutation test hot path on B200.
 
 A "step" is one whole word-pair test of BASELINE.json configs[1] (C2: n_x = n_y = 1000
-unit vectors, d = 768, B = 10^4 permutations): S1-S6 (hap_align: normalise, means,
-Householder reflect, pool/split, T_obs) + S7-S9 (hap_permtest: PERM-SPEC v1 masks,
-tcgen05 mask-GEMM, statistic, exceedance counts) on inputs resident in HBM.
+unit vectors, d = 768, B = 10^4 permutations): S1-S6 (alignment: normalise, means,
+Householder reflect, pool/split, T_obs) + S7-S9 (PERM-SPEC v1 masks, tcgen05 mask-GEMM,
+statistic, exceedance counts) on inputs resident in HBM, run through the public batch
+entry point hap_permtest_batch (independent generator stream per test).
 metric = permuted statistics / second (whole job, all ranks).
 
 Multi-GPU (torchrun): word pairs are sharded over ranks (weak scaling: every rank runs
@@ -191,39 +192,38 @@ def run_hap(args):
         if world > 1:
             dist.barrier()
 
+    # a rotating pool of distinct input pairs, packed as one varlen batch on the device
     pool_np = make_pool(args.pool, rank)
-    pool = [(torch.from_numpy(X).to(dev), torch.from_numpy(Y).to(dev)) for X, Y in pool_np]
-    in_bytes = sum(x.numel() * 4 + y.numel() * 4 for x, y in pool)
-    # consecutive tests are independent: a pipeline of `depth` contexts, each on its own
-    # stream, lets test k+1's alignment/generator overlap test k's mask-GEMM
-    depth = max(1, args.depth)
-    ctxs = [hap.Context(local) for _ in range(depth)]
-    streams = [torch.cuda.Stream(device=dev) for _ in range(depth)]
-    ctx = ctxs[0]
+    P = len(pool_np)
+    Xp = np.ascontiguousarray(np.concatenate([X for X, _ in pool_np]))
+    Yp = np.ascontiguousarray(np.concatenate([Y for _, Y in pool_np]))
+    cu_nx = np.arange(P + 1, dtype=np.int64) * N_X
+    cu_ny = np.arange(P + 1, dtype=np.int64) * N_Y
+    Xd, Yd = torch.from_numpy(Xp).to(dev), torch.from_numpy(Yp).to(dev)
+    in_bytes = (Xp.nbytes + Yp.nbytes)
+    ctx = hap.Context(local)
     st = torch.cuda.current_stream()
     K, W = args.steps, args.warmup
-    counts = torch.zeros((max(K, 1) * world, 3), dtype=torch.int64, device=dev)
-    cfgs = [hap.make_cfg(HI.PERM_SEED, B) for _ in range(depth)]
+    INFO = hap.INFO_BYTES
+    infos = torch.zeros((P, INFO), dtype=torch.uint8, device=dev)
+    counts = torch.zeros((max(K, 1), 3), dtype=torch.int64, device=dev)
+    pcounts = torch.zeros((P, 3), dtype=torch.int64, device=dev)
 
-    def step(k, slot=None):
-        X, Y = pool[k % len(pool)]
-        c, s_, cf = ctxs[k % depth], streams[k % depth], cfgs[k % depth]
-        hap.hap_align(c.h, X, Y, hap.HAP_ALIGN_HOUSEHOLDER, c.info, s_)
-        out = counts[slot] if slot is not None else c.counts
-        cf.stream_id = (rank * 1_000_003 + k) & 0xFFFFFFFF
-        hap.hap_permtest(c.h, c.info, cf, out, None, s_)
-
-    def fork():  # all pipeline streams start after the work already on `st`
-        ev = torch.cuda.Event()
-        ev.record(st)
-        for s_ in streams:
-            s_.wait_event(ev)
-
-    def join():  # `st` waits for every pipeline stream
-        for s_ in streams:
-            ev = torch.cuda.Event()
-            ev.record(s_)
-            st.wait_event(ev)
+    def run_tests(k0, n, out_counts=None, wave=0):
+        """tests k0 .. k0+n-1 (test k = pool pair k % P, generator stream rank*1e6 + k)
+        through hap_permtest_batch, one call per pass over the pool"""
+        k = k0
+        while k < k0 + n:
+            m = min(P - (k % P), k0 + n - k)  # pairs k % P .. k % P + m - 1 of the pool
+            sel = np.arange(k % P, k % P + m, dtype=np.int64)
+            base = (rank * 1_000_003 + k - k % P) & 0xFFFFFFFF
+            cfg = hap.make_cfg(HI.PERM_SEED, B, stream_id=base, wave=wave)
+            pcounts.zero_()
+            hap.hap_permtest_batch(ctx.h, Xd, cu_nx, Yd, cu_ny, hap.HAP_ALIGN_HOUSEHOLDER, cfg,
+                                   infos, pcounts, pair_sel=sel, stream=st)
+            if out_counts is not None:
+                out_counts[k - k0: k - k0 + m].copy_(pcounts[k % P: k % P + m])
+            k += m
 
     gpu_id = None
     try:
@@ -235,21 +235,15 @@ def run_hap(args):
     time.sleep(0.3)
 
     # ---------------- pass 1: the headline number (no instrumentation)
-    for k in range(W):
-        step(k)
+    run_tests(0, W)
     torch.cuda.synchronize()
-    for c in ctxs:
-        hap.hap_profile_read(c.h, reset=True)
-    counts.zero_()
+    hap.hap_profile_read(ctx.h, reset=True)
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     tw0 = time.time()
     e0.record(st)
-    fork()
-    for k in range(K):
-        step(k, slot=rank * K + k)
-    join()
+    run_tests(W, K, counts)
     if world > 1:
         dist.all_reduce(counts)  # the one combine of the integer counts
     e1.record(st)
@@ -257,10 +251,7 @@ def run_hap(args):
     tw1 = time.time()
     barrier()
     ms = e0.elapsed_time(e1)
-    launches = {}
-    for c in ctxs:
-        for kname, v in hap.hap_profile_read(c.h, reset=True)[1].items():
-            launches[kname] = launches.get(kname, 0) + v
+    launches = hap.hap_profile_read(ctx.h, reset=True)[1]
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -270,78 +261,91 @@ def run_hap(args):
     ms_per_step = ms / K
 
     # ---------------- pass 2: per-kernel device time (CUDA events on the launching stream)
-    Kp = min(K, 400)
-    hap.hap_profile(ctx.h, 2)  # serialised phases so the per-kernel times do not overlap
-    for k in range(Kp):
-        X, Y = pool[k % len(pool)]
-        hap.hap_align(ctx.h, X, Y, hap.HAP_ALIGN_HOUSEHOLDER, ctx.info, st)
-        cfgs[0].stream_id = k
-        hap.hap_permtest(ctx.h, ctx.info, cfgs[0], ctx.counts, None, st)
+    # one wave per call and a sync after it, so no other launch overlaps the timed ones
+    wave = 3
+    nw = max(1, min(K, 300) // wave)
+    hap.hap_profile(ctx.h, 2)
+    for i in range(nw):
+        run_tests(W + K + i * wave, wave, wave=wave)
+        torch.cuda.synchronize()
     phase_ms, phase_n = hap.hap_profile_read(ctx.h, reset=True)
-    hap.hap_profile(ctx.h, False)
+    hap.hap_profile(ctx.h, 0)
     peaks, peak_src = load_peaks()
     Nf = N_X + N_Y
-    gemm_flops = 2.0 * Nf * D * B * Kp  # algorithmic: the U = S X row per permutation
-    gemm_s = phase_ms["maskgemm"] / 1e3
+    n_k3 = max(1, phase_n["maskgemm"])
+    gemm_flops = 2.0 * Nf * D * B * wave  # algorithmic: the U = S X row per permutation
+    gemm_s = phase_ms["maskgemm"] / 1e3 / n_k3  # per launch
     achieved_tflops = gemm_flops / gemm_s / 1e12 if gemm_s > 0 else 0.0
     peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
     n_pad = -(-Nf // 64) * 64
-    issued_tflops = 4.0 * n_pad * D * B * Kp / gemm_s / 1e12 if gemm_s > 0 else 0.0
+    issued_tflops = 4.0 * n_pad * D * B * wave / gemm_s / 1e12 if gemm_s > 0 else 0.0
     traffic = None
     tf = os.path.join(ROOT, "profiles", "k3_traffic.json")
     if os.path.exists(tf):
         with open(tf) as f:
-            traffic = json.load(f).get("bytes_per_launch")
+            tj = json.load(f)
+        traffic = tj.get("bytes_per_launch")
     roofline = {"bound": "tensor", "achieved": achieved_tflops, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved_tflops / peak, "traffic": traffic,
-                "kernel": "k3_maskgemm (S8+S9)",
+                "kernel": f"k3_maskgemm (S8+S9), one launch = a wave of {wave} C2 tests",
                 "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside the step loop)",
                 "achieved_basis": "algorithmic 2*N*d FLOP per permutation (SURVEY.md 8d)",
-                "issued_tflops": issued_tflops,
-                "gemm_share_of_step": phase_ms["maskgemm"] / sum(phase_ms.values())}
-    phases_per_step = {k: v / Kp for k, v in phase_ms.items()}
+                "issued_tflops": issued_tflops, "k3_us_per_launch": gemm_s * 1e6,
+                "gemm_share_of_step": phase_ms["maskgemm"] / max(1e-9, sum(phase_ms.values()))}
+    phases_per_test = {k: v / (nw * wave) for k, v in phase_ms.items()}
 
-    # ---------------- pass 3: end to end through the public API with host buffers: every
-    # step copies its pair's X, Y from pinned host memory (hap_align stages host inputs on
-    # the stream) and reads its counts back into pinned host memory; the same two-context
-    # pipeline lets step k+1's copy overlap step k's kernels
-    Ke = min(K, 400)
-    pinned = [(torch.from_numpy(X).pin_memory(), torch.from_numpy(Y).pin_memory())
-              for X, Y in pool_np[: min(len(pool_np), 8)]]
+    # ---------------- pass 3: end to end through the public API from pinned host memory:
+    # every chunk of tests copies its packed X, Y host -> device (double-buffered, copy
+    # stream) and reads its counts back into pinned host memory; one sync at the end
+    Ke = min(K, 480)
+    Xh = torch.from_numpy(Xp).pin_memory()
+    Yh = torch.from_numpy(Yp).pin_memory()
+    bufs = [(torch.empty_like(Xd), torch.empty_like(Yd)) for _ in range(2)]
     host_counts = torch.zeros((Ke, 3), dtype=torch.int64).pin_memory()
-    dev_counts = torch.zeros((Ke, 3), dtype=torch.int64, device=dev)
+    dev_counts = torch.zeros((2, P, 3), dtype=torch.int64, device=dev)
+    cp = torch.cuda.Stream(device=dev)
+    ev_in = [torch.cuda.Event() for _ in range(2)]
+    ev_done = [torch.cuda.Event() for _ in range(2)]
 
-    def e2e_step(k):
-        Xh, Yh = pinned[k % len(pinned)]
-        c, s_, cf = ctxs[k % depth], streams[k % depth], cfgs[k % depth]
-        hap.hap_align(c.h, Xh, Yh, hap.HAP_ALIGN_HOUSEHOLDER, c.info, s_)  # H2D inside
-        cf.stream_id = (rank * 1_000_003 + k) & 0xFFFFFFFF
-        hap.hap_permtest(c.h, c.info, cf, dev_counts[k], None, s_)
-        with torch.cuda.stream(s_):
-            host_counts[k].copy_(dev_counts[k], non_blocking=True)  # D2H of the result
+    def e2e_chunk(c, k0, m):
+        Xb, Yb = bufs[c % 2]
+        with torch.cuda.stream(cp):  # H2D of this chunk's inputs (pinned)
+            cp.wait_event(ev_done[c % 2])  # the buffer's previous chunk is done with it
+            Xb[: m * N_X].copy_(Xh[: m * N_X], non_blocking=True)
+            Yb[: m * N_Y].copy_(Yh[: m * N_Y], non_blocking=True)
+            ev_in[c % 2].record(cp)
+        st.wait_event(ev_in[c % 2])
+        cfg = hap.make_cfg(HI.PERM_SEED, B, stream_id=(rank * 1_000_003 + k0) & 0xFFFFFFFF)
+        dc = dev_counts[c % 2]
+        dc.zero_()
+        hap.hap_permtest_batch(ctx.h, Xb, cu_nx[: m + 1], Yb, cu_ny[: m + 1],
+                               hap.HAP_ALIGN_HOUSEHOLDER, cfg, infos, dc, stream=st)
+        host_counts[k0: k0 + m].copy_(dc[:m], non_blocking=True)  # D2H of the results
+        ev_done[c % 2].record(st)
 
-    for k in range(min(4, Ke)):
-        e2e_step(k)
+    e2e_chunk(0, 0, min(P, Ke))
     torch.cuda.synchronize()
-    dev_counts.zero_()
     barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    fork()
-    for k in range(Ke):
-        e2e_step(k)
-    join()
+    k, c = 0, 0
+    while k < Ke:
+        m = min(P, Ke - k)
+        e2e_chunk(c, k, m)
+        k += m
+        c += 1
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
     if world > 1:
         t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    res = {"exceed_ge": int(host_counts[Ke - 1, 0]), "p_value": hap.hap_pvalue(int(host_counts[Ke - 1, 0]), B)}
+    last = int(host_counts[Ke - 1, 0])
     e2e = {"value": Ke * B * world / e2e_s, "unit": UNIT,
            "h2d_bytes_per_step": (N_X + N_Y) * D * 4, "d2h_bytes_per_step": 3 * 8,
            "steps": Ke, "timer": "host wall clock around the loop, synchronize on both sides",
-           "api": "hap_align(pinned host X, Y) + hap_permtest + counts D2H, 2 contexts/streams"}
+           "api": f"hap_permtest_batch on chunks of {P} tests copied H2D from pinned memory "
+                  "(double-buffered copy stream), counts copied D2H"}
 
     clocks.stop()
     clk = clocks.summary(tw0, tw1)
@@ -355,20 +359,20 @@ def run_hap(args):
                "data": "synthetic",
                "config": {"workload": WORKLOAD, "global_batch": world, "B": B, "n_x": N_X,
                           "n_y": N_Y, "d": D,
-                          "l2": f"rotating pool of {len(pool)} input pairs per rank "
+                          "l2": f"rotating pool of {P} input pairs per rank "
                                 f"({in_bytes / 1e6:.0f} MB > 126 MB L2)",
-                          "parallelism": f"pairs sharded over {world} rank(s); 1 test per "
-                                         "rank per step; counts combined by one all_reduce",
-                          "pipeline_depth": depth,
+                          "parallelism": f"tests sharded over {world} rank(s); each rank runs "
+                                         "its own tests; counts combined by one all_reduce",
+                          "api": "hap_permtest_batch (2 internal lanes, waves of 3 tests per "
+                                 "alignment / generator / mask-GEMM launch)",
                           "arith": "bf16 hi/lo split operands, fp32 TMEM accumulation, "
                                    "fp64 statistic"},
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
                "gpu_launches": int(sum(launches.values())),
-               "gpu_launches_by_phase": launches, "phase_ms_per_step": phases_per_step,
-               "last_test": {"exceed_ge": res["exceed_ge"], "p_value": res["p_value"]}}
+               "gpu_launches_by_phase": launches, "phase_ms_per_test": phases_per_test,
+               "last_test": {"exceed_ge": last, "p_value": hap.hap_pvalue(last, B)}}
         print(json.dumps(out), flush=True)
-    for c in ctxs:
-        c.close()
+    ctx.close()
     if world > 1:
         dist.destroy_process_group()
 
@@ -381,8 +385,6 @@ def main():
     ap.add_argument("--impl", default="hap", choices=["hap", "reference"])
     ap.add_argument("--pool", type=int, default=24, help="distinct input pairs per rank")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--depth", type=int, default=2,
-                    help="independent tests in flight (contexts/streams)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
