@@ -249,11 +249,21 @@ __global__ void __launch_bounds__(kThreads, 2) k1_align_fused(AlignArgs a, int P
             __syncthreads();
             if (warp < R) {
                 const int64_t i = r0 + warp;
-                double s = 0.0;
-                for (int c = lane; c < d; c += 32) {
-                    const double v = (double)tile[(size_t)warp * P + c];
-                    s += v * v;
+                double s4[4] = {0.0, 0.0, 0.0, 0.0};  // independent chains (latency)
+                const float* tr = tile + (size_t)warp * P;
+                int c = lane;
+                for (; c + 96 < d; c += 128) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const double v = (double)tr[c + 32 * u];
+                        s4[u] += v * v;
+                    }
                 }
+                for (; c < d; c += 32) {
+                    const double v = (double)tr[c];
+                    s4[0] += v * v;
+                }
+                double s = (s4[0] + s4[1]) + (s4[2] + s4[3]);
                 s = warp_sum(s);
                 if (lane == 0) {
                     const double nrm = sqrt(s);
@@ -269,12 +279,17 @@ __global__ void __launch_bounds__(kThreads, 2) k1_align_fused(AlignArgs a, int P
             const int64_t nxr64 = q.n_x - r0;  // X rows of the item
             const int nxr = nxr64 <= 0 ? 0 : (nxr64 >= R ? R : (int)nxr64);
             for (int c = tid, k = 0; c < d; c += kThreads, ++k) {
-                double px = 0.0, py = 0.0;
-                for (int r = 0; r < R; ++r) {
-                    const double v = (double)tile[(size_t)r * P + c] * s_inv[r];
-                    if (r < nxr) px += v;
-                    else py += v;
+                double px0 = 0.0, py0 = 0.0, px1 = 0.0, py1 = 0.0;  // two chains per group
+#pragma unroll
+                for (int r = 0; r < R; r += 2) {
+                    const double v0 = (double)tile[(size_t)r * P + c] * s_inv[r];
+                    const double v1 = (double)tile[(size_t)(r + 1) * P + c] * s_inv[r + 1];
+                    if (r < nxr) px0 += v0;
+                    else py0 += v0;
+                    if (r + 1 < nxr) px1 += v1;
+                    else py1 += v1;
                 }
+                const double px = px0 + px1, py = py0 + py1;
                 if (k == 0) {
                     sx0 += px;
                     sy0 += py;
@@ -481,7 +496,8 @@ __global__ void __launch_bounds__(kThreads, 2) k1_align_fused(AlignArgs a, int P
                     const size_t off = (size_t)c * (size_t)(q.n_pad >> 1);
                     zh[off] = (uint32_t)__bfloat16_as_ushort(h0) | ((uint32_t)__bfloat16_as_ushort(h1) << 16);
                     zl[off] = (uint32_t)__bfloat16_as_ushort(l0) | ((uint32_t)__bfloat16_as_ushort(l1) << 16);
-                    // hi + lo is exact in fp32; the column's t' partial is summed in fp64
+                    // hi + lo is exact in fp32; the column's t' partial is summed in fp64, so
+                    // t = N m + t' is the exact sum of the planes (up to the fixed point)
                     double tv = (double)(fh0 + __bfloat162float(l0)) + (double)(fh1 + __bfloat162float(l1));
 #pragma unroll
                     for (int o = 1; o < rp; o <<= 1) tv += __shfl_xor_sync(0xffffffffu, tv, o);
