@@ -260,7 +260,38 @@ hap_status get_schedule(hap_ctx c, const GemmArgs& w, int np, cudaStream_t st, G
         else lo = mid;
     }
     std::vector<int> off(np + 1, 0), npc(nt_all, 0), pcs;
-    fill(hi, &pcs, &off, &npc);
+    // EXPERIMENT: list schedule of the whole chunks in (test, tile, chunk) order, each to the
+    // least loaded pair (round-robin for equal costs: a tile's chunks run at the same time on
+    // neighbouring pairs).  It reads the masks from DRAM exactly once even from a cold L2,
+    // but measured 19 % slower than the contiguous balanced schedule (the default below).
+    std::vector<double> load(np, 0.0);
+    std::vector<std::vector<int>> per(np);
+    for (const Chunk& ch : chunks) {
+        int best = 0;
+        for (int p = 1; p < np; ++p)
+            if (load[p] < load[best]) best = p;
+        load[best] += cost(ch.width, ch.nkb);
+        per[best].push_back((int)(&ch - chunks.data()));
+    }
+    const double list_ms = *std::max_element(load.begin(), load.end());
+    static const char* rr = getenv("HAP_K3_ROUND_ROBIN");  // measured slower on B200 (kept
+    if (rr && atoi(rr) && list_ms <= 1.05 * hi) {           // for experiments only)
+        for (int p = 0; p < np; ++p) {
+            off[p] = (int)(pcs.size() / 4);
+            for (int ci : per[p]) {
+                const Chunk& ch = chunks[ci];
+                pcs.insert(pcs.end(), {(int)ch.tile, (int)ch.c0, (int)ch.width, 0});
+            }
+        }
+        // slots: index of the piece within its tile, in (tile, column) order
+        std::vector<std::pair<int64_t, int>> order;  // (tile * d_pad + c0, piece index)
+        for (size_t k = 0; k < pcs.size() / 4; ++k)
+            order.push_back({(int64_t)pcs[4 * k] * w.d_pad + pcs[4 * k + 1], (int)k});
+        std::sort(order.begin(), order.end());
+        for (auto& o : order) pcs[4 * o.second + 3] = npc[pcs[4 * o.second]]++;
+    } else {
+        fill(hi, &pcs, &off, &npc);
+    }
     off[np] = (int)(pcs.size() / 4);
     int max_slots = 1;
     for (int v : npc) max_slots = std::max(max_slots, v);
