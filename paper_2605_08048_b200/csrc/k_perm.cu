@@ -233,6 +233,7 @@ __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy32(PermArgs a, int 
     uint32_t* LT = reinterpret_cast<uint32_t*>(smem + (size_t)w * ((size_t)lt_pitch * 5u + 160u));
     uint32_t* sink = LT + lt_pitch + l;  // per-lane target of the atomics of no-op steps
     uint16_t* starts = reinterpret_cast<uint16_t*>(LT + lt_pitch + 32);
+    const uint32_t lane_lt = (1u << l) - 1u;
     const int nw = (int)(blockDim.x >> 5);
     const int64_t wstride = (int64_t)gridDim.x * nw;
     const int64_t items = a.item_off[a.G];
@@ -302,36 +303,36 @@ __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy32(PermArgs a, int 
                 q.y = p0 + 1 >= nx ? q.y : 0u;
                 q.z = p0 + 2 >= nx ? q.z : 0u;
             }
-            const uint32_t c = (q.x != 0u) + (q.y != 0u) + (q.z != 0u) + (q.w != 0u);
-            uint32_t incl = c;  // inclusive warp prefix sum of the counts
+            // four independent ballots (short dependency chains); list order is e-major
+            const uint32_t t[4] = {q.x, q.y, q.z, q.w};
+            uint32_t bal[4];
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-                if (l >= o) incl += v;
+            for (int e = 0; e < 4; ++e) bal[e] = __ballot_sync(0xffffffffu, t[e] != 0u);
+            uint32_t base = nst;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                if (t[e]) starts[base + __popc(bal[e] & lane_lt)] = (uint16_t)(t[e] - 1u);
+                base += __popc(bal[e]);
             }
-            uint32_t at = nst + incl - c;
-            if (q.x) starts[at++] = (uint16_t)(q.x - 1u);
-            if (q.y) starts[at++] = (uint16_t)(q.y - 1u);
-            if (q.z) starts[at++] = (uint16_t)(q.z - 1u);
-            if (q.w) starts[at] = (uint16_t)(q.w - 1u);
-            nst += __shfl_sync(0xffffffffu, incl, 31);
+            nst = base;
         }
         __syncwarp();
-        // ---- phase B2: walk each chain to its end (an unwritten low position) and exile it
+        // ---- phase B2: walk each chain to its end (an unwritten low position) and exile it;
+        // two cursors per lane (starts l, l+64, ... and l+32, l+96, ...) keep two table
+        // reads in flight (chains are disjoint, so the cursors never meet)
         {
-            uint32_t i = (uint32_t)l;
-            uint32_t cur = i < nst ? starts[i] : 0u;
-            while (__any_sync(0xffffffffu, i < nst)) {
-#pragma unroll
-                for (int rep = 0; rep < 2; ++rep) {
-                    const uint32_t t = LT[cur];  // inactive lanes re-read a harmless entry
-                    const bool end = (i < nst) & (t == 0u);
-                    if (end) LT[cur] = kExiled32;
-                    i += end ? 32u : 0u;
-                    const uint32_t nxt = starts[min(i, nst)];  // nst < lt_pitch/2: in bounds
-                    cur = end ? nxt : t - 1u;
-                    cur = i < nst ? cur : 0u;
-                }
+            uint32_t i0 = (uint32_t)l, i1 = (uint32_t)l + 32u;
+            uint32_t c0 = i0 < nst ? starts[i0] : 0u, c1 = i1 < nst ? starts[i1] : 0u;
+            while (__any_sync(0xffffffffu, (i0 < nst) | (i1 < nst))) {
+                const uint32_t t0 = LT[c0], t1 = LT[c1];  // inactive cursors re-read entry 0
+                const bool e0 = (i0 < nst) & (t0 == 0u), e1 = (i1 < nst) & (t1 == 0u);
+                if (e0) LT[c0] = kExiled32;
+                if (e1) LT[c1] = kExiled32;
+                i0 += e0 ? 64u : 0u;
+                i1 += e1 ? 64u : 0u;
+                const uint32_t n0 = starts[min(i0, nst)], n1 = starts[min(i1, nst)];  // in bounds
+                c0 = i0 < nst ? (e0 ? n0 : t0 - 1u) : 0u;
+                c1 = i1 < nst ? (e1 ? n1 : t1 - 1u) : 0u;
             }
         }
         __syncwarp();
