@@ -399,3 +399,30 @@ def test_batch_shared_mask(ctx, orc):
         one = ctx.permtest_pair(_cuda(Xq), _cuda(Yq), B, SEED, stream_id=s0)
         for k in ("gemm_t_obs", "exceed_ge", "exceed_abs", "flagged"):
             assert one[k] == res[p][k], (p, k)
+
+
+def test_batch_multiblock_and_errors_in_waves(hap, ctx, orc):
+    """A batch whose B needs several generator/GEMM blocks per test (cfg.block) and a data
+    error inside a wave: every good pair matches the oracle, the bad one only reports."""
+    import torch
+    sizes = [40, 33, 80, 20, 55, 61]
+    Xp, cnx, Yp, cny = HI.varlen_batch(sizes, d=64)
+    Xp[cnx[4] + 3] = 0.0                     # pair 4 (second of the second wave): ZeroVector
+    B, s0 = 700, 8
+    X, Y = _cuda(Xp), _cuda(Yp)
+    infos = torch.zeros((len(sizes), hap.INFO_BYTES), dtype=torch.uint8, device=X.device)
+    counts = torch.zeros((len(sizes), 3), dtype=torch.int64, device=X.device)
+    cfg = hap.make_cfg(SEED, B, 0, B, s0, block=200, wave=3)
+    hap.hap_permtest_batch(ctx.h, X, cnx, Y, cny, 0, cfg, infos, counts)
+    hap.hap_sync(ctx.h)
+    cts = counts.cpu().tolist()
+    raw = infos.cpu().numpy()
+    for p in range(len(sizes)):
+        info = hap.hap_align_info.from_buffer_copy(bytes(raw[p].tobytes()))
+        if p == 4:
+            assert info.status == 3 and cts[p] == [0, 0, 0]
+            continue
+        assert info.status == 0
+        ref = orc.run_pair(Xp[cnx[p]:cnx[p + 1]], Yp[cny[p]:cny[p + 1]], B, SEED, s=s0 + p)
+        for k, c in zip(("exceed_ge", "exceed_abs"), cts[p][:2]):
+            assert abs(c - ref[k]) <= ref["flagged"], (p, k)
