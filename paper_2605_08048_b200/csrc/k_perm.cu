@@ -303,15 +303,26 @@ __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy32(PermArgs a, int 
                 q.y = p0 + 1 >= nx ? q.y : 0u;
                 q.z = p0 + 2 >= nx ? q.z : 0u;
             }
-            // four independent ballots (short dependency chains); list order is e-major
+            // A chain that ends at its start (the start position k* was not written before
+            // step k*, ~70 % of them) is exiled right here; the others enter the list at
+            // their second node.  Four independent ballots; list order is e-major.
             const uint32_t t[4] = {q.x, q.y, q.z, q.w};
+            uint32_t nx2[4];
+            bool more[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const uint32_t u = t[e] ? LT[t[e] - 1u] : 0u;
+                more[e] = t[e] != 0u && u != 0u;
+                if (t[e] != 0u && u == 0u) LT[t[e] - 1u] = kExiled32;
+                nx2[e] = u - 1u;
+            }
             uint32_t bal[4];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) bal[e] = __ballot_sync(0xffffffffu, t[e] != 0u);
+            for (int e = 0; e < 4; ++e) bal[e] = __ballot_sync(0xffffffffu, more[e]);
             uint32_t base = nst;
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-                if (t[e]) starts[base + __popc(bal[e] & lane_lt)] = (uint16_t)(t[e] - 1u);
+                if (more[e]) starts[base + __popc(bal[e] & lane_lt)] = (uint16_t)nx2[e];
                 base += __popc(bal[e]);
             }
             nst = base;
