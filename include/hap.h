@@ -100,6 +100,14 @@ typedef struct {
  * the tests are no longer independent of each other. */
 #define HAP_FLAG_SHARED_MASK 1u
 
+/* hap_permtest only: EXHAUSTIVE enumeration.  b
+ * indexes the C(N, n_x) splits in colex order (b -> the combination {c_1 < .. < c_nx} with
+ * b = sum_i C(c_i, i)) instead of PERM-SPEC draws; seed and stream_id are ignored.  Needs
+ * C(N, n_x) < 2^32 (N <= 34) and b_end <= C(N, n_x).  Over [0, C(N, n_x)) the counts are
+ * those of the exact permutation distribution, the observed split included:
+ * p_exact = exceed_ge / C(N, n_x).  HAP_E_INVALID_ARG otherwise. */
+#define HAP_FLAG_EXHAUSTIVE 2u
+
 /* Exceedance counters of one test, DEVICE memory, ADDED into (caller zeroes them), so
  * shards and resumed ranges compose by summation (Eq. pvalue). */
 typedef struct {
@@ -219,6 +227,13 @@ HAP_API hap_status hap_profile_spans_read(hap_ctx ctx, double* out, int64_t max_
  * membership (1 = group 1), produced by the product's generator kernel. */
 HAP_API hap_status hap_perm_sets(hap_ctx ctx, uint64_t seed, uint32_t stream_id, uint64_t b_begin,
                          int64_t count, int64_t N, int64_t n_x, uint8_t* out, void* stream);
+/* Parity introspection of HAP_FLAG_EXHAUSTIVE: out [device] count*N uint8, row r = the
+ * indicator of combination b_begin + r of C(N, n_x) (colex unranking); N <= 64,
+ * b_begin + count <= C(N, n_x) < 2^32. */
+HAP_API hap_status hap_comb_sets(hap_ctx ctx, uint64_t b_begin, int64_t count, int64_t N, int64_t n_x,
+                                 uint8_t* out, void* stream);
+/* C(N, k) as uint64 (0 when it exceeds 2^64 - 1 or k > N). */
+HAP_API uint64_t hap_n_choose_k(int64_t N, int64_t k);
 /* Copy out the pooled workspace of the last hap_align: zhi, zlo [device] d_pad*n_pad
  * uint16, the transposed bf16 planes Zt of the CENTRED cloud (row c holds column c of
  * Z - 1 m^T over the n_pad pooled rows, zero padded), so z[i][c] ~ hi + lo + m[c];

@@ -88,6 +88,8 @@ def lib() -> ctypes.CDLL:
         "hap_profile": ([vp, i32], i32),
         "hap_profile_read": ([vp, P(f64), P(i64), i32], i32),
         "hap_profile_spans": ([vp, i32], i32),
+        "hap_comb_sets": ([vp, u64, i64, i64, i64, vp, vp], i32),
+        "hap_n_choose_k": ([i64, i64], u64),
         "hap_profile_spans_read": ([vp, P(f64), i64, P(i64)], i32),
         "hap_profile_timeline": ([vp, P(f64), i64, P(i64)], i32),
         "hap_profile_k1_phases": ([vp, P(f64)], i32),
@@ -156,6 +158,7 @@ def hap_align(ctx, X, Y, mode: int, info, stream=None) -> None:
 
 
 HAP_FLAG_SHARED_MASK = 1
+HAP_FLAG_EXHAUSTIVE = 2
 
 
 def make_cfg(seed: int, B: int, b_begin: int = 0, b_end: int | None = None, stream_id: int = 0,
@@ -200,6 +203,14 @@ def hap_perm_sets(ctx, seed: int, stream_id: int, b_begin: int, count: int, N: i
                   out, stream=None) -> None:
     _check(ctx, lib().hap_perm_sets(ctx, seed, stream_id, b_begin, count, N, n_x, _ptr(out),
                                     _stream(stream)))
+
+
+def hap_comb_sets(ctx, b_begin: int, count: int, N: int, n_x: int, out, stream=None) -> None:
+    _check(ctx, lib().hap_comb_sets(ctx, b_begin, count, N, n_x, _ptr(out), _stream(stream)))
+
+
+def hap_n_choose_k(N: int, k: int) -> int:
+    return int(lib().hap_n_choose_k(int(N), int(k)))
 
 
 def hap_export_pooled(ctx, zhi, zlo, t, m, stream=None) -> None:
@@ -291,15 +302,18 @@ class Context:
     def permtest_pair(self, X, Y, B: int, seed: int, stream_id: int = 0, mode: int = 0,
                       b_begin: int = 0, b_end: int | None = None, tie_rel: float = 1e-6,
                       block: int = 0, want_stats: bool = False, sync: bool = True,
-                      pair_mode: int = 0):
-        """One word-pair test end to end: hap_align + hap_permtest (+ p-value)."""
+                      pair_mode: int = 0, exhaustive: bool = False):
+        """One word-pair test end to end: hap_align + hap_permtest (+ p-value).  With
+        exhaustive=True the b range indexes all C(N, n_x) splits (pass B = C(N, n_x)) and
+        p_exact = exceed_ge / B is added."""
         torch = self.torch
         b_end = B if b_end is None else b_end
         self.counts.zero_()
         hap_align(self.h, X, Y, mode, self.info)
         stats = (torch.empty((b_end - b_begin, 3), dtype=torch.float64, device=self.device)
                  if want_stats else None)
-        cfg = make_cfg(seed, B, b_begin, b_end, stream_id, block, tie_rel, pair_mode)
+        cfg = make_cfg(seed, B, b_begin, b_end, stream_id, block, tie_rel, pair_mode,
+                       flags=HAP_FLAG_EXHAUSTIVE if exhaustive else 0)
         hap_permtest(self.h, self.info, cfg, self.counts, stats)
         if not sync:
             return None
@@ -314,6 +328,9 @@ class Context:
                    is_identity=bool(info.is_identity), exceed_ge=c[0], exceed_abs=c[1],
                    flagged=c[2], B=B, p_value=hap_pvalue(c[0], B),
                    p_two_sided=hap_pvalue(c[1], B))
+        if exhaustive:
+            out["p_exact"] = c[0] / B
+            out["p_exact_two_sided"] = c[1] / B
         if want_stats:
             out["stats"] = stats
         return out

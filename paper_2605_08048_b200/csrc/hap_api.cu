@@ -663,6 +663,7 @@ hap_status run_wave(hap_ctx owner, int G, const WaveTest* T, int pair, cudaStrea
         pt.n_pad = w->n_pad;
         pt.out = w->buf[slots[k] ? kMask1 : kMask];
         pt.ntiles = (int)nt;
+        pt.exhaustive = (T[k].cfg->flags & HAP_FLAG_EXHAUSTIVE) ? 1 : 0;
         GemmTest& gt = g.t[k];
         gt.n_pad = (int)w->n_pad;
         gt.n_x = (int)w->n_x;
@@ -744,6 +745,11 @@ hap_status hap_permtest(hap_ctx c, hap_align_info* info, const hap_perm_cfg* cfg
     if (s) return s;
     if (!is_device_ptr(counts) || (stats && !is_device_ptr(stats)))
         return fail(c, HAP_E_INVALID_ARG, "counts/stats must be device memory");
+    if (cfg->flags & HAP_FLAG_EXHAUSTIVE) {
+        const uint64_t total = hap_n_choose_k(c->n_x + c->n_y, c->n_x);
+        if (c->n_x + c->n_y > 64 || total == 0 || total >= (1ull << 32) || cfg->b_end > total)
+            return fail(c, HAP_E_INVALID_ARG, "exhaustive mode needs C(N, n_x) < 2^32 and b_end <= C(N, n_x)");
+    }
     cudaSetDevice(c->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int pair = cfg->pair_mode ? cfg->pair_mode : 2;
@@ -769,6 +775,8 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
     if (pair_sel && n_sel < 0) return fail(c, HAP_E_INVALID_ARG, "n_sel < 0");
     if (mode != HAP_ALIGN_HOUSEHOLDER && mode != HAP_ALIGN_NONE)
         return fail(c, HAP_E_INVALID_ARG, "bad mode");
+    if (cfg->flags & HAP_FLAG_EXHAUSTIVE)
+        return fail(c, HAP_E_INVALID_ARG, "exhaustive mode: use hap_permtest per pair");
     hap_status s = check_cfg(c, cfg);
     if (s) return s;
     if (!is_device_ptr(X_packed) || !is_device_ptr(Y_packed))
@@ -1065,6 +1073,41 @@ hap_status hap_perm_sets(hap_ctx c, uint64_t seed, uint32_t stream_id, uint64_t 
     perm_items(pa);
     cudaError_t e = launch_perm(pa, c->sm_count, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(c, e, "perm generator");
+    return HAP_OK;
+}
+
+uint64_t hap_n_choose_k(int64_t N, int64_t k) {
+    if (k < 0 || N < 0 || k > N) return 0;
+    if (k > N - k) k = N - k;
+    unsigned __int128 c = 1;
+    for (int64_t i = 1; i <= k; ++i) {
+        c = c * (unsigned __int128)(N - k + i) / (unsigned __int128)i;  // exact at every step
+        if (c > (unsigned __int128)UINT64_MAX) return 0;
+    }
+    return (uint64_t)c;
+}
+
+hap_status hap_comb_sets(hap_ctx c, uint64_t b_begin, int64_t count, int64_t N, int64_t n_x, uint8_t* out,
+                         void* stream) {
+    if (!c) return HAP_E_INVALID_ARG;
+    const uint64_t total = hap_n_choose_k(N, n_x);
+    if (!out || count < 0 || N < 1 || N > 64 || n_x < 0 || n_x > N || total == 0 ||
+        total >= (1ull << 32) || b_begin + (uint64_t)count > total)
+        return fail(c, HAP_E_INVALID_ARG, "bad comb_sets arguments");
+    cudaSetDevice(c->device);
+    PermArgs pa{};
+    pa.G = 1;
+    pa.t[0].b_begin = b_begin;
+    pa.t[0].count = count;
+    pa.t[0].N = N;
+    pa.t[0].n_x = n_x;
+    pa.t[0].n_pad = round_up(N, kKBlock);
+    pa.t[0].out = out;
+    pa.t[0].exhaustive = 1;
+    pa.out_kind = kMaskU8Set;
+    perm_items(pa);
+    cudaError_t e = launch_perm(pa, c->sm_count, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(c, e, "comb generator");
     return HAP_OK;
 }
 

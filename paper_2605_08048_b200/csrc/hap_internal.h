@@ -76,6 +76,7 @@ struct PermTest {
     int64_t N, n_x, n_pad;
     void* out;               // bf16 rows (tile layout) or uint8 [count][N]
     int ntiles;              // bf16 mode: tiles (each also gets its observed-split row 0)
+    int exhaustive;          // 1: b = colex rank of the combination (HAP_FLAG_EXHAUSTIVE)
 };
 struct PermArgs {
     int G;                   // tests in this launch

@@ -363,6 +363,74 @@ __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy32(PermArgs a, int 
     if (l == 0) span_exit(a.span);
 }
 
+// ---------------------------------------------------------------------------------------
+// Exhaustive mode (HAP_FLAG_EXHAUSTIVE): thread = one combination, b is
+// its colex rank: b = sum_{i=1..n_x} C(c_i, i) with c_1 < .. < c_nx, unranked greedily from
+// the largest element down with a shared binomial table.  N <= 64 (n_pad = 64).
+constexpr int kCombMaxN = 64;
+
+__global__ void __launch_bounds__(128) k2_comb_unrank(PermArgs a) {
+    constexpr int kK = kCombMaxN / 2 + 1;  // k <= 32 (the smaller side of the split)
+    __shared__ unsigned long long binom[kCombMaxN + 1][kK + 1];
+    if (threadIdx.x == 0) {  // Pascal's triangle, saturating (only values < 2^32 are used)
+        const unsigned long long sat = 1ull << 62;
+        for (int n = 0; n <= kCombMaxN; ++n)
+            for (int k = 0; k <= kK; ++k) {
+                unsigned long long c;
+                if (k == 0) c = 1;
+                else if (n == 0) c = 0;
+                else c = binom[n - 1][k - 1] + binom[n - 1][k];
+                binom[n][k] = c > sat ? sat : c;
+            }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) span_enter(a.span);
+    const int64_t items = a.item_off[a.G];
+    for (int64_t pi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; pi < items;
+         pi += (int64_t)gridDim.x * blockDim.x) {
+        int ti = 0;
+        while (ti + 1 < a.G && pi >= a.item_off[ti + 1]) ++ti;
+        const PermTest& T = a.t[ti];
+        const int64_t li = pi - a.item_off[ti];
+        const int N = (int)T.N, nx = (int)T.n_x;
+        const unsigned long long all = N >= 64 ? ~0ull : ((1ull << N) - 1ull);
+        unsigned long long sel = 0;  // bit c = element c in group 1
+        if (li >= T.count) {
+            sel = nx >= 64 ? ~0ull : ((1ull << nx) - 1ull);  // observed split {0..n_x-1}
+        } else {
+            // enumerate the smaller side (k = min(n_x, n_y)); complement when n_x > n_y
+            const int k = nx <= N - nx ? nx : N - nx;
+            unsigned long long r = T.b_begin + (uint64_t)li;
+            int c = N - 1;
+            for (int i = k; i >= 1; --i) {  // largest c with C(c, i) <= r
+                while (binom[c][i] > r) --c;
+                r -= binom[c][i];
+                sel |= 1ull << c;
+                --c;
+            }
+            if (k != nx) sel = ~sel & all;
+        }
+        if (a.out_kind == kMaskBf16Row) {
+            const int64_t R1 = a.rows_per_tile - 1;
+            const int64_t orow = li >= T.count ? (li - T.count) * a.rows_per_tile
+                                               : (li / R1) * a.rows_per_tile + 1 + li % R1;
+            uint4* row = reinterpret_cast<uint4*>(static_cast<uint16_t*>(T.out) + orow * T.n_pad);
+            for (int v8 = 0; v8 < (int)(T.n_pad >> 3); ++v8) {
+                const uint32_t byte = (uint32_t)(v8 < 8 ? (sel >> (8 * v8)) & 0xFFu : 0u);
+                uint32_t o[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    o[e] = (((byte >> (2 * e)) & 1u) | (((byte >> (2 * e + 1)) & 1u) << 16)) * 0x3F80u;
+                row[v8] = make_uint4(o[0], o[1], o[2], o[3]);
+            }
+        } else {
+            uint8_t* row = static_cast<uint8_t*>(T.out) + li * T.N;
+            for (int v = 0; v < N; ++v) row[v] = (uint8_t)((sel >> v) & 1ull);
+        }
+    }
+    if (threadIdx.x == 0) span_exit(a.span);
+}
+
 }  // namespace
 
 void perm_items(PermArgs& a) {
@@ -374,6 +442,11 @@ void perm_items(PermArgs& a) {
 cudaError_t launch_perm(const PermArgs& a, int sm_count, cudaStream_t st) {
     const int64_t items = a.item_off[a.G];
     if (items <= 0) return cudaSuccess;
+    if (a.t[0].exhaustive) {  // a wave is all-exhaustive or not at all
+        const int64_t grid = std::min<int64_t>(ceil_div(items, 128), (int64_t)sm_count * 8);
+        k2_comb_unrank<<<(int)grid, 128, 0, st>>>(a);
+        return cudaGetLastError();
+    }
     int64_t maxN = 0;
     for (int g = 0; g < a.G; ++g) maxN = std::max<int64_t>(maxN, a.t[g].N);
     const int lt_pitch = (int)round_up(maxN, 64);  // entries, 128-byte multiple; >= every n_pad

@@ -426,3 +426,90 @@ def test_batch_multiblock_and_errors_in_waves(hap, ctx, orc):
         ref = orc.run_pair(Xp[cnx[p]:cnx[p + 1]], Yp[cny[p]:cny[p + 1]], B, SEED, s=s0 + p)
         for k, c in zip(("exceed_ge", "exceed_abs"), cts[p][:2]):
             assert abs(c - ref[k]) <= ref["flagged"], (p, k)
+
+
+# ------------------------------------------------------------------ exhaustive (exact p)
+def _colex_unrank(r, N, k):
+    """Independent colex unranking (combinatorial number system), plain Python."""
+    out = []
+    c = N - 1
+    for i in range(k, 0, -1):
+        while math.comb(c, i) > r:
+            c -= 1
+        r -= math.comb(c, i)
+        out.append(c)
+        c -= 1
+    return sorted(out)
+
+
+@pytest.mark.parametrize("N,n_x", [(6, 3), (10, 4), (12, 9), (16, 1), (20, 10)])
+def test_comb_sets_enumerate_all_splits(hap, ctx, N, n_x):
+    """HAP_FLAG_EXHAUSTIVE generator: rank b -> b-th combination in colex order (the
+    complement of the n_y-subset when n_x > n_y): every split exactly once."""
+    import itertools
+    import torch
+    total = math.comb(N, n_x)
+    assert hap.hap_n_choose_k(N, n_x) == total
+    out = torch.zeros((total, N), dtype=torch.uint8, device="cuda")
+    hap.hap_comb_sets(ctx.h, 0, total, N, n_x, out)
+    got = out.cpu().numpy()
+    assert np.all(got.sum(1) == n_x)
+    seen = {tuple(np.flatnonzero(r)) for r in got}
+    assert seen == set(itertools.combinations(range(N), n_x))
+    k = min(n_x, N - n_x)
+    for b in range(0, total, max(1, total // 50)):
+        sub = _colex_unrank(b, N, k)
+        want = sub if k == n_x else sorted(set(range(N)) - set(sub))
+        assert list(np.flatnonzero(got[b])) == want, b
+
+
+def test_comb_sets_large_sampled(hap, ctx):
+    """C(34, 17) = 2.3e9 splits: sampled ranks near both ends and the middle."""
+    import torch
+    N, n_x = 34, 17
+    total = math.comb(N, n_x)
+    for b0 in (0, total // 2 - 3, total - 7):
+        out = torch.zeros((7, N), dtype=torch.uint8, device="cuda")
+        hap.hap_comb_sets(ctx.h, b0, 7, N, n_x, out)
+        for r, row in enumerate(out.cpu().numpy()):
+            assert list(np.flatnonzero(row)) == _colex_unrank(b0 + r, N, n_x)
+    with pytest.raises(hap.HapError):
+        hap.hap_comb_sets(ctx.h, total - 3, 7, N, n_x, torch.zeros((7, N), dtype=torch.uint8,
+                                                                   device="cuda"))
+
+
+def test_exhaustive_worked_example_exact(ctx):
+    """SURVEY worked example: the exact permutation distribution gives 12 of 70 splits with
+    T >= T_obs (tests/golden/worked_example.txt, computed independently) - the GPU path
+    must reproduce the integer exactly; two-sided 24 within the flagged true ties."""
+    from conftest import read_golden
+    rows = read_golden("worked_example.txt")
+    X = np.array([[float(v) for v in r.split()[1:]] for r in rows if r.startswith("X ")], np.float32)
+    Y = np.array([[float(v) for v in r.split()[1:]] for r in rows if r.startswith("Y ")], np.float32)
+    vals = {r.split()[0]: r.split()[1:] for r in rows}
+    total = int(vals["exhaustive_total"][0])
+    g = ctx.permtest_pair(_cuda(X), _cuda(Y), total, SEED, exhaustive=True)
+    assert g["exceed_ge"] == int(vals["exhaustive_ge"][0])
+    assert abs(g["exceed_abs"] - int(vals["exhaustive_abs"][0])) <= g["flagged"]
+    assert g["p_exact"] == 12 / 70
+
+
+@pytest.mark.parametrize("n_x,n_y,d", [(5, 6, 32), (9, 9, 100), (3, 12, 768)])
+def test_exhaustive_matches_oracle(ctx, orc, n_x, n_y, d):
+    """Exhaustive GPU counts vs the oracle's brute-force enumeration (orc_exhaustive)."""
+    X, Y = HI.make_pair(HI.PairSpec(n_x, n_y, d, HI.kappa_for(d), HI.kappa_for(d), 30.0, seed=5))
+    total = math.comb(n_x + n_y, n_x)
+    ref = orc.run_pair(X, Y, 10, SEED)
+    counts, tot = orc.exhaustive(ref["Z"], n_x, ref["t_obs"], ref["tau"])
+    assert tot == total
+    g = ctx.permtest_pair(_cuda(X), _cuda(Y), total, SEED, exhaustive=True)
+    fl = int(counts[2])
+    assert abs(g["exceed_ge"] - int(counts[0])) <= fl
+    assert abs(g["exceed_abs"] - int(counts[1])) <= fl
+    assert g["exceed_ge"] >= 1  # the observed split itself is enumerated
+
+
+def test_exhaustive_rejects_too_many_splits(hap, ctx):
+    X, Y = HI.make_pair(HI.PairSpec(20, 20, 16, 20.0, 20.0, 30.0, seed=5))
+    with pytest.raises(hap.HapError):
+        ctx.permtest_pair(_cuda(X), _cuda(Y), 1000, SEED, exhaustive=True)
