@@ -513,3 +513,20 @@ def test_exhaustive_rejects_too_many_splits(hap, ctx):
     X, Y = HI.make_pair(HI.PairSpec(20, 20, 16, 20.0, 20.0, 30.0, seed=5))
     with pytest.raises(hap.HapError):
         ctx.permtest_pair(_cuda(X), _cuda(Y), 1000, SEED, exhaustive=True)
+
+
+def test_gpu_type1_calibration_batch(ctx):
+    """C5 recipe at test size: equal-kappa clouds with
+    different mean directions.  Through hap_permtest_batch the aligned test rejects at the
+    nominal rate (within 3 SE); the naive test (no reflection) is reported alongside."""
+    R, B, alpha = 400, 999, 0.10
+    pairs = [HI.make_pair(HI.PairSpec(60, 60, 32, 50.0, 50.0, 60.0, seed=78), rep) for rep in range(R)]
+    Xp = np.concatenate([p[0] for p in pairs])
+    Yp = np.concatenate([p[1] for p in pairs])
+    cu = np.arange(R + 1, dtype=np.int64) * 60
+    rates = {}
+    for mode in (0, 1):
+        res = ctx.permtest_batch(_cuda(Xp), cu, _cuda(Yp), cu, B, SEED, stream_id=0, mode=mode)
+        rates[mode] = np.mean([r["p_value"] <= alpha for r in res])
+    se = math.sqrt(alpha * (1 - alpha) / R)
+    assert abs(rates[0] - alpha) <= 3 * se, rates
