@@ -291,41 +291,41 @@ __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy32(PermArgs a, int 
             }
         }
         __syncwarp();
-        // ---- phase B1: compact the chain starts LT[p]-1 of the written high positions
+        // ---- phase B1: chain starts LT[p]-1 of the written high positions, 8 per lane per
+        // pass.  A chain that ends at its start (position k* not written before step k*,
+        // ~70 % of them) is exiled right here; the others enter the list at their second
+        // node, at offsets from a warp prefix sum of the per-lane counts (4 ballots).
         uint32_t nst = 0;
-        for (uint32_t p0 = (nx & ~3u) + 4u * (uint32_t)l; __any_sync(0xffffffffu, p0 < N);
-             p0 += 128u) {
-            uint4 q = make_uint4(0, 0, 0, 0);
-            if (p0 < N) q = *reinterpret_cast<const uint4*>(LT + p0);
-            // positions below n_x only occur in the first chunk; beyond N the table is 0
-            if (p0 < nx) {
-                q.x = p0 >= nx ? q.x : 0u;
-                q.y = p0 + 1 >= nx ? q.y : 0u;
-                q.z = p0 + 2 >= nx ? q.z : 0u;
+        for (uint32_t p0 = (nx & ~7u) + 8u * (uint32_t)l; __any_sync(0xffffffffu, p0 < N);
+             p0 += 256u) {
+            uint4 q0 = make_uint4(0, 0, 0, 0), q1 = q0;
+            if (p0 < N) {  // beyond N the table is 0 (p0 + 7 < lt_pitch)
+                q0 = *reinterpret_cast<const uint4*>(LT + p0);
+                q1 = *reinterpret_cast<const uint4*>(LT + p0 + 4);
             }
-            // A chain that ends at its start (the start position k* was not written before
-            // step k*, ~70 % of them) is exiled right here; the others enter the list at
-            // their second node.  Four independent ballots; list order is e-major.
-            const uint32_t t[4] = {q.x, q.y, q.z, q.w};
-            uint32_t nx2[4];
-            bool more[4];
+            uint32_t t[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+            if (p0 < nx) {  // positions below n_x only occur in the first pass
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const uint32_t u = t[e] ? LT[t[e] - 1u] : 0u;
-                more[e] = t[e] != 0u && u != 0u;
-                if (t[e] != 0u && u == 0u) LT[t[e] - 1u] = kExiled32;
-                nx2[e] = u - 1u;
+                for (int e = 0; e < 8; ++e) t[e] = p0 + e >= nx ? t[e] : 0u;
             }
-            uint32_t bal[4];
+            uint32_t u[8];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) bal[e] = __ballot_sync(0xffffffffu, more[e]);
-            uint32_t base = nst;
+            for (int e = 0; e < 8; ++e) u[e] = t[e] ? LT[t[e] - 1u] : 0u;  // all in flight
+            uint32_t cnt = 0;
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                if (more[e]) starts[base + __popc(bal[e] & lane_lt)] = (uint16_t)nx2[e];
-                base += __popc(bal[e]);
+            for (int e = 0; e < 8; ++e) {
+                if (t[e] != 0u && u[e] == 0u) LT[t[e] - 1u] = kExiled32;
+                cnt += (t[e] != 0u && u[e] != 0u) ? 1u : 0u;
             }
-            nst = base;
+            uint32_t at = nst;  // + exclusive prefix of cnt over the lanes below
+#pragma unroll
+            for (int bit = 0; bit < 4; ++bit)
+                at += (uint32_t)__popc(__ballot_sync(0xffffffffu, (cnt >> bit) & 1u) & lane_lt) << bit;
+            const uint32_t tot = __reduce_add_sync(0xffffffffu, cnt);
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+                if (t[e] != 0u && u[e] != 0u) starts[at++] = (uint16_t)(u[e] - 1u);
+            nst += tot;
         }
         __syncwarp();
         // ---- phase B2: walk each chain to its end (an unwritten low position) and exile it;
