@@ -232,6 +232,9 @@ HAP_API hap_status hap_perm_sets(hap_ctx ctx, uint64_t seed, uint32_t stream_id,
  * b_begin + count <= C(N, n_x) < 2^32. */
 HAP_API hap_status hap_comb_sets(hap_ctx ctx, uint64_t b_begin, int64_t count, int64_t N, int64_t n_x,
                                  uint8_t* out, void* stream);
+/* Development aid (scheduling experiments only): enqueue a register-only Philox loop of
+ * `iters` rounds on ctas x threads threads, no shared memory. */
+HAP_API hap_status hap_debug_alu_burn(hap_ctx ctx, uint32_t iters, int ctas, int threads, void* stream);
 /* C(N, k) as uint64 (0 when it exceeds 2^64 - 1 or k > N). */
 HAP_API uint64_t hap_n_choose_k(int64_t N, int64_t k);
 /* Copy out the pooled workspace of the last hap_align: zhi, zlo [device] d_pad*n_pad

@@ -90,6 +90,7 @@ def lib() -> ctypes.CDLL:
         "hap_profile_spans": ([vp, i32], i32),
         "hap_comb_sets": ([vp, u64, i64, i64, i64, vp, vp], i32),
         "hap_n_choose_k": ([i64, i64], u64),
+        "hap_debug_alu_burn": ([vp, u32, i32, i32, vp], i32),
         "hap_profile_spans_read": ([vp, P(f64), i64, P(i64)], i32),
         "hap_profile_timeline": ([vp, P(f64), i64, P(i64)], i32),
         "hap_profile_k1_phases": ([vp, P(f64)], i32),

@@ -44,6 +44,7 @@ struct hap_ctx_s {
     hap_ctx sub[2][kMaxWave] = {};
     cudaStream_t sub_stream[2] = {nullptr, nullptr};
     cudaEvent_t ev_sub[2] = {nullptr, nullptr};
+    cudaEvent_t ev_k1[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};  // per workspace set
     // cached K3 schedules: key {d_pad, npairs, (ntiles, n_pad) per test} -> offset (ints)
     // in buf[kSched]; new ones are staged in pinned host memory and copied on the stream
     struct Sched { std::vector<int64_t> key; int64_t off; int max_slots; };
@@ -453,6 +454,8 @@ hap_status hap_destroy(hap_ctx c) {
             if (c->sub[i][k]) hap_destroy(c->sub[i][k]);
         if (c->sub_stream[i]) cudaStreamDestroy(c->sub_stream[i]);
         if (c->ev_sub[i]) cudaEventDestroy(c->ev_sub[i]);
+        if (c->ev_k1[i]) cudaEventDestroy(c->ev_k1[i]);
+        if (c->ev_done[i]) cudaEventDestroy(c->ev_done[i]);
     }
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     for (int i = 0; i < 2; ++i) {
@@ -624,7 +627,7 @@ struct WaveTest {
 // test's masks go to the next mask slot of its own workspace, which K2 rewrites only after
 // the K3 that last read it (event), so K2 can overlap earlier work of other streams.
 hap_status run_wave(hap_ctx owner, int G, const WaveTest* T, int pair, cudaStream_t st,
-                    bool shared = false) {
+                    bool shared = false, cudaStream_t light = nullptr) {
     const int64_t R = (int64_t)kTileM * pair;  // mask rows per tile; row 0 = observed split
     const int npairs = owner->sm_count / pair;
     GemmArgs g = gemm_args(owner);
@@ -690,19 +693,40 @@ hap_status run_wave(hap_ctx owner, int G, const WaveTest* T, int pair, cudaStrea
         return s;
     g.part = B<float2>(owner, kGemmPart);
     g.tile_done = B<unsigned>(owner, kTileDone);
-    // K2 on the side stream: each test's slot is rewritten only after the K3 that read it
-    cudaStream_t gs = owner->serial ? st : owner->side;
     cudaError_t e = cudaSuccess;
-    for (int k = 0; k < pa.G && e == cudaSuccess && !owner->serial; ++k)
-        if (T[k].w->used[slots[k]]) e = cudaStreamWaitEvent(gs, T[k].w->ev_free[slots[k]], 0);
-    if (e == cudaSuccess) {
-        pa.span = next_span(owner, HAP_PHASE_PERMGEN);
-        PhaseScope ps(owner, HAP_PHASE_PERMGEN, 1, gs);
-        e = launch_perm(pa, owner->sm_count, gs);
+    if (light && light != st && perm_can_split(pa)) {
+        // split generator: K2a (draws, register-only) on the light stream, where it runs
+        // beside the other wave's mask-GEMM for free; K2b (table, chains, rows) on `st`,
+        // i.e. never beside a mask-GEMM (both lean on shared-memory bandwidth)
+        for (int k = 0; k < pa.G && e == cudaSuccess; ++k)
+            if (T[k].w->used[slots[k]]) e = cudaStreamWaitEvent(light, T[k].w->ev_free[slots[k]], 0);
+        PermArgs d = pa;
+        d.split = 1;
+        if (e == cudaSuccess) e = launch_perm(d, owner->sm_count, light);
+        if (e == cudaSuccess) e = cudaEventRecord(owner->ev_ready[0], light);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, owner->ev_ready[0], 0);
+        if (e == cudaSuccess) {
+            pa.split = 2;
+            pa.span = next_span(owner, HAP_PHASE_PERMGEN);
+            PhaseScope ps(owner, HAP_PHASE_PERMGEN, 2, st);
+            e = launch_perm(pa, owner->sm_count, st);
+        }
+        if (e != cudaSuccess) return cuda_fail(owner, e, "perm generator");
+    } else {
+        // K2 on the side stream: each test's slot is rewritten only after the K3 that read it
+        // (on `st` itself when serialised or when the caller passed its light stream as st)
+        cudaStream_t gs = (owner->serial || light == st) ? st : owner->side;
+        for (int k = 0; k < pa.G && e == cudaSuccess && !owner->serial; ++k)
+            if (T[k].w->used[slots[k]]) e = cudaStreamWaitEvent(gs, T[k].w->ev_free[slots[k]], 0);
+        if (e == cudaSuccess) {
+            pa.span = next_span(owner, HAP_PHASE_PERMGEN);
+            PhaseScope ps(owner, HAP_PHASE_PERMGEN, 1, gs);
+            e = launch_perm(pa, owner->sm_count, gs);
+        }
+        if (e == cudaSuccess) e = cudaEventRecord(owner->ev_ready[0], gs);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, owner->ev_ready[0], 0);  // join
+        if (e != cudaSuccess) return cuda_fail(owner, e, "perm generator");
     }
-    if (e == cudaSuccess) e = cudaEventRecord(owner->ev_ready[0], gs);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, owner->ev_ready[0], 0);  // join
-    if (e != cudaSuccess) return cuda_fail(owner, e, "perm generator");
     if ((s = get_schedule(owner, g, npairs, st, g))) return s;
     {
         g.span = next_span(owner, HAP_PHASE_MASKGEMM);
@@ -857,7 +881,9 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
         if (G == 1 && ceil_div(std::max<int64_t>(B, 1), R - 1) > block_tiles(cfg, T[0].w->n_pad, R)) {
             s = hap_permtest(T[0].w, T[0].info, T[0].cfg, T[0].counts, nullptr, ls);  // blocks
         } else if (B > 0) {
-            s = run_wave(T[0].w, G, T, pair, ls, shared);
+            static const char* sp = getenv("HAP_BATCH_SPLIT");  // K2a on the side stream
+            const bool split = sp && atoi(sp) != 0;
+            s = run_wave(T[0].w, G, T, pair, ls, shared, split ? T[0].w->side : nullptr);
         }
         if (s) c->err = "wave " + std::to_string(wave) + ": " + T[0].w->err;
         ++wave;
@@ -1074,6 +1100,14 @@ hap_status hap_perm_sets(hap_ctx c, uint64_t seed, uint32_t stream_id, uint64_t 
     cudaError_t e = launch_perm(pa, c->sm_count, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(c, e, "perm generator");
     return HAP_OK;
+}
+
+hap_status hap_debug_alu_burn(hap_ctx c, uint32_t iters, int ctas, int threads, void* stream) {
+    if (!c) return HAP_E_INVALID_ARG;
+    if (ensure(c, kStamps, 64) != HAP_OK) return HAP_E_OOM;
+    cudaError_t e = launch_debug_alu_burn(iters, ctas, threads, B<uint32_t>(c, kStamps),
+                                          static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? HAP_OK : cuda_fail(c, e, "alu burn");
 }
 
 uint64_t hap_n_choose_k(int64_t N, int64_t k) {

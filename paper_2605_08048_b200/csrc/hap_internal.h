@@ -86,11 +86,16 @@ struct PermArgs {
     int rows_per_tile;       // bf16 mode: R; perm p -> row (p/(R-1))*R + 1 + p%(R-1),
                              // row t*R = observed split {0..n_x-1} for t < ntiles
     int max_ctas_per_sm;     // 0 = occupancy limit
+    int split;               // 0 = fused; 1 = K2a: draws staged in the rows (register-only);
+                             // 2 = K2b: table, chains and rows from the staged draws
     unsigned long long* span;  // optional {first CTA entry, last CTA exit} globaltimer
 };
 // fills item_off from the tests (count + ntiles rows each in bf16 mode)
 void perm_items(PermArgs& a);
+// whether a launch may be split into K2a + K2b (bf16 rows, wide table, not exhaustive)
+bool perm_can_split(const PermArgs& a);
 cudaError_t launch_perm(const PermArgs& a, int sm_count, cudaStream_t st);
+cudaError_t launch_debug_alu_burn(uint32_t iters, int ctas, int threads, uint32_t* sink, cudaStream_t st);
 
 // ---- K3: tcgen05 mask-GEMM + statistic epilogue (k_maskgemm.cu) --------------------
 struct GemmTest {

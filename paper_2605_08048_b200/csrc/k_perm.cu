@@ -200,6 +200,56 @@ __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy(PermArgs a, int lt
 // walks the chains lane-balanced.  Same result bits as k2_perm_fy (tests).
 constexpr uint32_t kExiled32 = 0xFFFFFFFFu;
 
+// targets j_k = k + U(N - k) of steps k0 .. k0+3 (one Philox block; Lemire, exact slow path)
+__device__ __forceinline__ void draw_targets(uint32_t k0, uint32_t nx, uint32_t N, uint32_t b,
+                                             uint32_t s, uint32_t key0, uint32_t key1, uint32_t j[4]) {
+    const u32x4 wd = philox4x32_10(u32x4{k0 >> 2, b, s, 0u}, key0, key1);
+    const uint32_t x[4] = {wd.x, wd.y, wd.z, wd.w};
+    bool slow = false;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {  // Lemire fast path; rejection needs lo < bound
+        const uint32_t k = k0 + e, bound = N - k;
+        const uint64_t m = (uint64_t)x[e] * bound;
+        slow |= (uint32_t)m < bound;
+        j[e] = k + (uint32_t)(m >> 32);
+    }
+    if (slow) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            if (k0 + e < nx) j[e] = fy_target(x[e], k0 + e, N, b, s, key0, key1);
+    }
+}
+
+// K2a (split generator): the draws only, register-resident, no shared memory, so it can
+// run beside the smem-bandwidth-bound mask-GEMM without slowing it (measured); the targets
+// (u16, n_x per permutation) are staged in the permutation's own mask row, which K2b reads
+// before overwriting it with the mask.
+__global__ void __launch_bounds__(128) k2_draws(PermArgs a) {
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const int nw = (int)(blockDim.x >> 5);
+    const int64_t items = a.item_off[a.G];
+    if (threadIdx.x == 0) span_enter(a.span);
+    for (int64_t pi = (int64_t)blockIdx.x * nw + w; pi < items; pi += (int64_t)gridDim.x * nw) {
+        int ti = 0;
+        while (ti + 1 < a.G && pi >= a.item_off[ti + 1]) ++ti;
+        const PermTest& T = a.t[ti];
+        const int64_t li = pi - a.item_off[ti];
+        if (li >= T.count) continue;  // observed-split rows: K2b
+        const uint32_t N = (uint32_t)T.N, nx = (uint32_t)T.n_x;
+        const uint32_t key0 = (uint32_t)(T.seed & 0xFFFFFFFFu), key1 = (uint32_t)(T.seed >> 32);
+        const uint32_t b = (uint32_t)(T.b_begin + (uint64_t)li);
+        const int64_t R1 = a.rows_per_tile - 1;
+        const int64_t orow = (li / R1) * a.rows_per_tile + 1 + li % R1;
+        uint16_t* jrow = static_cast<uint16_t*>(T.out) + orow * T.n_pad;
+        for (uint32_t k0 = 4u * (uint32_t)l; k0 < nx; k0 += 128u) {
+            uint32_t j[4];
+            draw_targets(k0, nx, N, b, T.s, key0, key1, j);
+            *reinterpret_cast<uint2*>(jrow + k0) = make_uint2(j[0] | (j[1] << 16), j[2] | (j[3] << 16));
+        }
+    }
+    if (threadIdx.x == 0) span_exit(a.span);
+}
+
 __device__ __forceinline__ void emit_row_u32(const PermArgs& a, const PermTest& T, const uint32_t* LT,
                                              int64_t li, uint32_t nx, int l) {
     const int64_t R1 = a.rows_per_tile - 1;
@@ -266,28 +316,40 @@ __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy32(PermArgs a, int 
             continue;
         }
         const uint32_t b = (uint32_t)(T.b_begin + (uint64_t)li);
-        // ---- phase A: draws + last-writer scatter (atomicMax = largest step wins)
-        for (uint32_t k0 = 4u * (uint32_t)l; k0 < nx; k0 += 128u) {
-            const u32x4 wd = philox4x32_10(u32x4{k0 >> 2, b, s, 0u}, key0, key1);
-            const uint32_t x[4] = {wd.x, wd.y, wd.z, wd.w};
-            uint32_t j[4];
-            bool slow = false;
+        const int64_t R1 = a.rows_per_tile - 1;
+        const int64_t orow = (li / R1) * a.rows_per_tile + 1 + li % R1;
+        const uint16_t* jrow = static_cast<const uint16_t*>(T.out) + orow * T.n_pad;
+        // ---- phase A: draws (or the targets K2a staged in this row) + last-writer scatter
+        // (atomicMax = largest step wins)
+        if (a.split == 2) {
+            for (uint32_t kc = 4u * (uint32_t)l; kc < nx; kc += 8u * 128u) {
+                uint2 jj[8];  // 8 blocks of 4 targets in flight (one L2 round trip)
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {  // Lemire fast path; rejection needs lo < bound
-                const uint32_t k = k0 + e, bound = N - k;
-                const uint64_t m = (uint64_t)x[e] * bound;
-                slow |= (uint32_t)m < bound;
-                j[e] = k + (uint32_t)(m >> 32);
+                for (int it = 0; it < 8; ++it) {
+                    const uint32_t k0 = kc + 128u * it;
+                    jj[it] = k0 < nx ? *reinterpret_cast<const uint2*>(jrow + k0) : make_uint2(0, 0);
+                }
+#pragma unroll
+                for (int it = 0; it < 8; ++it) {
+                    const uint32_t k0 = kc + 128u * it;
+                    const uint32_t j[4] = {jj[it].x & 0xFFFFu, jj[it].x >> 16, jj[it].y & 0xFFFFu,
+                                           jj[it].y >> 16};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const uint32_t k = k0 + e;
+                        atomicMax((k < nx && j[e] != k) ? LT + j[e] : sink, k + 1u);
+                    }
+                }
             }
-            if (slow) {
+        } else {
+            for (uint32_t k0 = 4u * (uint32_t)l; k0 < nx; k0 += 128u) {
+                uint32_t j[4];
+                draw_targets(k0, nx, N, b, s, key0, key1, j);
 #pragma unroll
-                for (int e = 0; e < 4; ++e)
-                    if (k0 + e < nx) j[e] = fy_target(x[e], k0 + e, N, b, s, key0, key1);
-            }
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {  // unconditional: no-op steps hit the lane's sink
-                const uint32_t k = k0 + e;
-                atomicMax((k < nx && j[e] != k) ? LT + j[e] : sink, k + 1u);
+                for (int e = 0; e < 4; ++e) {  // unconditional: no-op steps hit the lane's sink
+                    const uint32_t k = k0 + e;
+                    atomicMax((k < nx && j[e] != k) ? LT + j[e] : sink, k + 1u);
+                }
             }
         }
         __syncwarp();
@@ -431,7 +493,33 @@ __global__ void __launch_bounds__(128) k2_comb_unrank(PermArgs a) {
     if (threadIdx.x == 0) span_exit(a.span);
 }
 
+// Development aid (scheduling experiments): a register-only Philox loop, no shared memory.
+__global__ void k_debug_alu_burn(uint32_t iters, uint32_t* sink) {
+    u32x4 c{threadIdx.x, blockIdx.x, 0u, 0u};
+    for (uint32_t i = 0; i < iters; ++i) {
+        c = philox4x32_10(c, 0x12345678u, 0x9abcdef0u);
+        c.z = i;
+    }
+    if (c.x == 0x7fffffffu) sink[0] = c.y;  // keep the loop alive
+}
+
 }  // namespace
+
+cudaError_t launch_debug_alu_burn(uint32_t iters, int ctas, int threads, uint32_t* sink, cudaStream_t st) {
+    k_debug_alu_burn<<<ctas, threads, 0, st>>>(iters, sink);
+    return cudaGetLastError();
+}
+
+bool perm_can_split(const PermArgs& a) {
+    if (a.out_kind != kMaskBf16Row) return false;
+    int64_t maxN = 0;
+    for (int g = 0; g < a.G; ++g) {
+        if (a.t[g].exhaustive) return false;
+        maxN = std::max<int64_t>(maxN, a.t[g].N);
+    }
+    const int lt_pitch = (int)round_up(maxN, 64);
+    return (size_t)lt_pitch * 5u + 160u <= (200u * 1024u) / 4u;  // the wide table path
+}
 
 void perm_items(PermArgs& a) {
     a.item_off[0] = 0;
@@ -467,10 +555,14 @@ cudaError_t launch_perm(const PermArgs& a, int sm_count, cudaStream_t st) {
     per_sm = std::max(1, std::min(per_sm, a.max_ctas_per_sm > 0 ? a.max_ctas_per_sm : per_sm));
     const int64_t need = ceil_div(items, nw);
     const int grid = (int)std::min<int64_t>(need, (int64_t)sm_count * per_sm);
-    if (wide)
+    if (a.split == 1) {  // K2a: draws into the rows, register-only (wide path only)
+        const int64_t g2 = std::min<int64_t>(ceil_div(items, 4), (int64_t)sm_count * 4);
+        k2_draws<<<(int)g2, 128, 0, st>>>(a);
+    } else if (wide) {
         k2_perm_fy32<<<grid, nw * 32, smem, st>>>(a, lt_pitch);
-    else
+    } else {
         k2_perm_fy<<<grid, nw * 32, smem, st>>>(a, lt_pitch);
+    }
     return cudaGetLastError();
 }
 
