@@ -530,3 +530,22 @@ def test_gpu_type1_calibration_batch(ctx):
         rates[mode] = np.mean([r["p_value"] <= alpha for r in res])
     se = math.sqrt(alpha * (1 - alpha) / R)
     assert abs(rates[0] - alpha) <= 3 * se, rates
+
+
+@pytest.mark.parametrize("shared", [False, True])
+def test_config5_batch_full_size(ctx, orc, shared):
+    """C5 at full size (n = 500/500, d = 768, B = 10^4) through hap_permtest_batch in the
+    bench's launch configuration (waves of 3 / 4, two lanes): 4 replicates vs the oracle."""
+    pairs = [HI.config_pair("C5", rep) for rep in range(4)]
+    Xp = np.concatenate([p[0] for p in pairs])
+    Yp = np.concatenate([p[1] for p in pairs])
+    cu = np.arange(5, dtype=np.int64) * 500
+    B, s0 = 10000, 40
+    res = ctx.permtest_batch(_cuda(Xp), cu, _cuda(Yp), cu, B, SEED, stream_id=s0, shared=shared)
+    for p in range(4):
+        ref = orc.run_pair(pairs[p][0], pairs[p][1], B, SEED, s=s0 if shared else s0 + p)
+        Ls = abs(ref["L_x"]) + abs(ref["L_y"])
+        assert abs(res[p]["t_obs"] - ref["t_obs"]) <= 1e-10 * Ls
+        assert abs(res[p]["gemm_t_obs"] - ref["t_obs"]) <= 1e-5 * Ls
+        for k in ("exceed_ge", "exceed_abs"):
+            assert abs(res[p][k] - ref[k]) <= ref["flagged"], (p, k)
