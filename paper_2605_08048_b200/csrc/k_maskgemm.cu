@@ -40,6 +40,7 @@ namespace {
 constexpr int kThreads = 192;
 constexpr uint32_t kTmemCols = 512;
 constexpr int kStageA = kTileM * 128;  // 16 KB: 128 rows x 64 bf16
+constexpr int kFinCap = 400;             // deferred finalizes per CTA (smem tail list)
 
 template <int kPair>
 struct Cfg {
@@ -48,7 +49,7 @@ struct Cfg {
     static constexpr int kBRows = kChunkN / kPair;   // B rows (d-columns) held per CTA
     static constexpr int kStageB = kBRows * 128;     // one plane
     static constexpr int kStageBytes = kStageA + 2 * kStageB;
-    static constexpr size_t kSmem = (size_t)kStages * kStageBytes + 1024 + 512;
+    static constexpr size_t kSmem = (size_t)kStages * kStageBytes + 1024 + 2048;
 };
 
 
@@ -83,7 +84,11 @@ __device__ __forceinline__ RowStat row_stat(const GemmArgs& g, const GemmTest& T
     s.r1 = sqrt(fmax(S1, 0.0)) / (double)T.n_x;
     s.r2 = sqrt(fmax(S2, 0.0)) / (double)T.n_y;
     const double q1 = kappa_hat(s.r1, (double)g.d), q2 = kappa_hat(s.r2, (double)g.d);
-    s.T = (q1 == 0.0 && q2 == 0.0) ? 0.0 : (q1 == 0.0 ? INFINITY : log(q2 / q1));
+    // log of the ratio in fp32 (log1p of q2/q1 - 1 formed in fp64): the error, ~1e-7 of
+    // T's natural scale, is far below the tie band tau = 1e-6 (|L_X| + |L_Y|) (DESIGN R8),
+    // and it keeps the finalize off the fp64 pipe, which the running MMAs slow down
+    s.T = (q1 == 0.0 && q2 == 0.0) ? 0.0
+                                   : (q1 == 0.0 ? INFINITY : (double)log1pf((float)((q2 - q1) / q1)));
     return s;
 }
 
@@ -92,7 +97,9 @@ __device__ __forceinline__ RowStat row_stat(const GemmArgs& g, const GemmTest& T
 // All partial loads of the three rows are issued together (one L2 round trip per 8 pieces);
 // the piece partials are summed in ascending slot order (deterministic).
 __device__ void finalize_tile(const GemmArgs& g, const GemmTest& T, int tile, int lt, int np, int etid,
-                              unsigned* s_cnt, double S1c, double S2c, double tau) {
+                              unsigned* s_cnt, double S1c, double S2c, double tau, int unit = -1) {
+#define FIN_STAMP(ev) do { if (unit == 3 && etid == 0) K3_STAMP(6, ev); } while (0)
+    FIN_STAMP(0);
     const int R = g.rows_per_tile;
     if (etid < 3) s_cnt[etid] = 0u;
     constexpr int kRows = 3;  // row 0, etid, etid + 128 (R <= 256)
@@ -120,7 +127,9 @@ __device__ void finalize_tile(const GemmArgs& g, const GemmTest& T, int tile, in
                 S2[k] += (double)v[k][c].y;
             }
     }
+    FIN_STAMP(1);
     const RowStat o = row_stat(g, T, S1[0], S2[0]);
+    FIN_STAMP(2);
     if (lt == 0 && etid == 0) {
         T.info->gemm_r_x = o.r1;
         T.info->gemm_r_y = o.r2;
@@ -129,6 +138,7 @@ __device__ void finalize_tile(const GemmArgs& g, const GemmTest& T, int tile, in
     const double t_obs = o.T;
     const int lane = etid & 31;
     named_bar_sync(1, 128);  // s_cnt cleared
+    FIN_STAMP(3);
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
         const int row = rows[1 + j];
@@ -155,10 +165,14 @@ __device__ void finalize_tile(const GemmArgs& g, const GemmTest& T, int tile, in
             out[2] = Tb;
         }
     }
+    FIN_STAMP(4);
     named_bar_sync(1, 128);
+    FIN_STAMP(5);
     if (etid < 3 && s_cnt[etid])
         atomicAdd(reinterpret_cast<unsigned long long*>(T.counts) + etid, (unsigned long long)s_cnt[etid]);
     if (etid == 0) g.tile_done[tile] = 0;  // ready for the next launch
+    FIN_STAMP(6);
+#undef FIN_STAMP
 }
 
 // test of a wave tile (the tests' tiles are contiguous, in test order)
@@ -187,6 +201,8 @@ __global__ void __maxnreg__(168)
     int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
     unsigned* s_cnt = tmem_slot + 4;  // [3] per-tile counts of the finalize
     double* s_tc = reinterpret_cast<double*>(tmem_slot + 8);  // [kMaxWave][3] S1c, S2c, tau
+    int* s_nfin = reinterpret_cast<int*>(s_tc + 3 * kMaxWave);  // tiles this CTA finalizes
+    int* s_fin = s_nfin + 1;                                    // [kFinCap] deferred tiles
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) K3_STAMP(7, 0);  // kernel entry
@@ -214,6 +230,7 @@ __global__ void __maxnreg__(168)
             tma_prefetch_desc(&maps.blo[ti]);
         }
     }
+    if (threadIdx.x == 64 + kMaxWave) *s_nfin = 0;
     if (threadIdx.x >= 64 && threadIdx.x < 64 + g.G) {  // finalize constants per test
         const GemmTest& T = g.t[threadIdx.x - 64];
         s_tc[3 * (threadIdx.x - 64) + 0] = T.sconst[0];
@@ -380,15 +397,32 @@ __global__ void __maxnreg__(168)
                 *s_last = (old == (unsigned)(kPair * np_tile - 1)) ? 1 : 0;
             }
             named_bar_sync(1, 128);
-            if (*s_last) {
+            // The last arriving CTA finalizes the tile - but only after its last piece: in
+            // the middle of the kernel the partial loads queue behind the operand streams
+            // (measured 12-16 us instead of ~1 us), which would hold the epilogue and with
+            // it the release of the accumulator buffer.
+            if (*s_last && *s_nfin < kFinCap) {  // defer (the list is full only for
+                if (etid == 0) s_fin[*s_nfin] = tile;  // pairs with hundreds of pieces)
+                named_bar_sync(1, 128);
+                if (etid == 0) ++*s_nfin;
+            } else if (*s_last) {
                 __threadfence();
-                if (etid == 0) K3_STAMP(i, 6);
                 finalize_tile(g, T, tile, tile - T.tile0, np_tile, etid, s_cnt, s_tc[3 * ti],
                               s_tc[3 * ti + 1], s_tc[3 * ti + 2]);
-                if (etid == 0) K3_STAMP(i, 7);
             }
             named_bar_sync(1, 128);
             ++i;
+        }
+        for (int f = 0; f < *s_nfin; ++f) {
+            const int tile = s_fin[f];
+            const int ti = test_of(g, tile);
+            const GemmTest& T = g.t[ti];
+            __threadfence();
+            if (etid == 0) K3_STAMP(f, 6);
+            finalize_tile(g, T, tile, tile - T.tile0, g.tile_npieces[tile], etid, s_cnt, s_tc[3 * ti],
+                          s_tc[3 * ti + 1], s_tc[3 * ti + 2], f);
+            if (etid == 0) K3_STAMP(f, 7);
+            named_bar_sync(1, 128);
         }
     }
     tc_fence_before();

@@ -9,7 +9,8 @@ L.hap_debug_k3_stamps.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_longl
 ctx = hap.Context(0)
 X, Y = HI.config_pair("C2")
 X, Y = torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda()
-cfg = hap.make_cfg(HI.PERM_SEED, 10000)
+Bk = int(os.environ.get("HAP_TRACE_B", "10000"))
+cfg = hap.make_cfg(HI.PERM_SEED, Bk, block=Bk)
 hap.hap_align(ctx.h, X, Y, 0, ctx.info)
 for k in range(3):
     hap.hap_permtest(ctx.h, ctx.info, cfg, ctx.counts, None)
@@ -20,8 +21,8 @@ st = buf.reshape(148, 8, 8).astype(np.float64)
 t0 = st[st > 0].min()
 st = np.where(st > 0, (st - t0) / 1e3, np.nan)
 names = ["tma0", "tmaN", "mma0", "mmaN", "epi0", "epiN", "fin0", "fin1"]
-for cta in [0, 1, 2, 3, 50, 51, 100, 101, 146, 147]:
-    for u in range(2):
+for cta in [0, 1, 50, 51, 146, 147]:
+    for u in range(6):
         row = st[cta, u]
         if np.all(np.isnan(row)): continue
         print(f"cta {cta:3d} unit {u}: " + " ".join(f"{n}={v:6.1f}" for n, v in zip(names, row) if not np.isnan(v)))
@@ -34,7 +35,7 @@ for f in fin[:6] + fin[-6:]:
     print(f"  cta {f[0]:3d} unit {f[1]} fin {f[2]:6.1f} -> {f[3]:6.1f} ({f[3]-f[2]:.1f} us)")
 # per-pair piece durations (leader CTAs), widths from the device schedule mirror
 def cost(w): return max(4.0*w, 784.0)
-d_pad, nt, npairs = 768, 40, 74
+d_pad, nt, npairs = 768, -(-Bk // 255), 74
 chunks=[min(256, d_pad-c0) for t in range(nt) for c0 in range(0, d_pad, 256)]
 def fill(M, keep=False):
     ci=0; done=0; out=[]
@@ -70,3 +71,11 @@ print("pieces per pair:", collections.Counter(len(x) for x in sch))
 ent = st[:, 7, 0]; setup = st[:, 7, 2]; ex = st[:, 7, 1]
 last0 = np.nanmax(st[:, :7, 0])
 print(f"kernel entry min {np.nanmin(ent):.1f} max {np.nanmax(ent):.1f}; setup done max {np.nanmax(setup):.1f}; first TMA {np.nanmin(st[:, :7, 0]):.1f}; exit min {np.nanmin(ex):.1f} max {np.nanmax(ex):.1f}")
+fs = st[:, 6, :7]
+ok = ~np.isnan(fs[:, 0])
+if ok.any():
+    d = np.diff(fs[ok], axis=1)
+    print("finalize internals (unit 3), median us: loads", np.nanmedian(d[:, 0]), "row0", np.nanmedian(d[:, 1]),
+          "bar1", np.nanmedian(d[:, 2]), "rows", np.nanmedian(d[:, 3]), "bar2", np.nanmedian(d[:, 4]),
+          "atomics", np.nanmedian(d[:, 5]))
+    print("max:", np.nanmax(d, axis=0))
