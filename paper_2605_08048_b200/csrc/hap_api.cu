@@ -560,8 +560,13 @@ hap_status prepare_pair(hap_ctx c, const float* X, int64_t n_x, const float* Y, 
 // ONE K1 launch aligning G pairs (each in its own workspace ws[k]); `owner` (= ws[0])
 // provides the launch's barrier / ticket words and the profiling records.
 hap_status align_wave(hap_ctx owner, int G, hap_ctx* ws, const AlignPair* pairs, hap_align_mode mode,
-                      cudaStream_t st) {
+                      cudaStream_t st, const PermArgs* draws = nullptr) {
     AlignArgs a{};
+    if (draws) {
+        a.do_draws = 1;
+        a.draws = *draws;
+        a.draws.split = 1;
+    }
     a.G = G;
     for (int k = 0; k < G; ++k) {
         a.p[k] = pairs[k];
@@ -626,13 +631,22 @@ struct WaveTest {
 // wave buffers (piece partials, tile tickets, schedule) and the generator side stream; each
 // test's masks go to the next mask slot of its own workspace, which K2 rewrites only after
 // the K3 that last read it (event), so K2 can overlap earlier work of other streams.
-hap_status run_wave(hap_ctx owner, int G, const WaveTest* T, int pair, cudaStream_t st,
-                    bool shared = false, cudaStream_t light = nullptr) {
-    const int64_t R = (int64_t)kTileM * pair;  // mask rows per tile; row 0 = observed split
-    const int npairs = owner->sm_count / pair;
-    GemmArgs g = gemm_args(owner);
+// Arguments of a wave's K2 and K3 launches; picks (and toggles) each test's mask slot.
+struct WavePlan {
+    GemmArgs g;
     GemmMaps maps;
-    PermArgs pa{};
+    PermArgs pa;
+    int slots[kMaxWave];
+    int npairs;
+};
+
+hap_status plan_wave(hap_ctx owner, int G, const WaveTest* T, int pair, bool shared, WavePlan& P) {
+    const int64_t R = (int64_t)kTileM * pair;  // mask rows per tile; row 0 = observed split
+    P.npairs = owner->sm_count / pair;
+    P.g = gemm_args(owner);
+    P.pa = PermArgs{};
+    GemmArgs& g = P.g;
+    PermArgs& pa = P.pa;
     pa.G = G;
     pa.out_kind = kMaskBf16Row;
     pa.rows_per_tile = (int)R;
@@ -643,7 +657,6 @@ hap_status run_wave(hap_ctx owner, int G, const WaveTest* T, int pair, cudaStrea
     g.G = G;
     g.rows_per_tile = (int)R;
     g.tie_rel = T[0].cfg->tie_rel > 0 ? T[0].cfg->tie_rel : 1e-6;
-    int slots[kMaxWave];
     int64_t tiles = 0;
     hap_status s;
     for (int k = 0; k < G; ++k) {
@@ -654,7 +667,7 @@ hap_status run_wave(hap_ctx owner, int G, const WaveTest* T, int pair, cudaStrea
             (s = ensure(w, kMask1, (size_t)nt * R * w->n_pad * 2)) || (s = refresh_maps(w, pair)))
             return s == HAP_OK ? s : fail(owner, s, w->err);
         // shared masks: every test reads test 0's block (same N, n_x, stream, b-range)
-        slots[k] = (shared && k > 0) ? slots[0] : w->slot;
+        P.slots[k] = (shared && k > 0) ? P.slots[0] : w->slot;
         if (!(shared && k > 0)) w->slot ^= 1;
         PermTest& pt = pa.t[k];
         pt.seed = T[k].cfg->seed;
@@ -664,7 +677,7 @@ hap_status run_wave(hap_ctx owner, int G, const WaveTest* T, int pair, cudaStrea
         pt.N = w->n_x + w->n_y;
         pt.n_x = w->n_x;
         pt.n_pad = w->n_pad;
-        pt.out = w->buf[slots[k] ? kMask1 : kMask];
+        pt.out = w->buf[P.slots[k] ? kMask1 : kMask];
         pt.ntiles = (int)nt;
         pt.exhaustive = (T[k].cfg->flags & HAP_FLAG_EXHAUSTIVE) ? 1 : 0;
         GemmTest& gt = g.t[k];
@@ -678,23 +691,50 @@ hap_status run_wave(hap_ctx owner, int G, const WaveTest* T, int pair, cudaStrea
         gt.stats = T[k].stats;
         gt.ab = B<float2>(w, kAB);
         gt.sconst = B<double>(w, kSconst);
-        maps.a[k] = shared ? T[0].w->tmA[slots[0]] : w->tmA[slots[k]];
-        maps.bhi[k] = w->tmBhi;
-        maps.blo[k] = w->tmBlo;
+        P.maps.a[k] = shared ? T[0].w->tmA[P.slots[0]] : w->tmA[P.slots[k]];
+        P.maps.bhi[k] = w->tmBhi;
+        P.maps.blo[k] = w->tmBlo;
         tiles += nt;
     }
     if (shared) pa.G = 1;  // one generated block serves the whole wave
     perm_items(pa);
     g.ntiles = (int)tiles;
-    g.npairs = npairs;
+    g.npairs = P.npairs;
     if ((s = ensure(owner, kGemmPart, (size_t)tiles * std::max<int64_t>(1, ceil_div(owner->d_pad, 32)) * R *
                                           sizeof(float2))) ||
         (s = ensure(owner, kTileDone, (size_t)tiles * sizeof(unsigned))))
         return s;
     g.part = B<float2>(owner, kGemmPart);
     g.tile_done = B<unsigned>(owner, kTileDone);
+    return HAP_OK;
+}
+
+// K2 (fused, split over `light`, or - `staged` - only the table pass after K1 staged the
+// draws on `st`) and K3 of a planned wave.
+hap_status launch_wave(hap_ctx owner, const WaveTest* T, int pair, cudaStream_t st, WavePlan& P,
+                       cudaStream_t light = nullptr, bool staged = false) {
+    PermArgs& pa = P.pa;
+    GemmArgs& g = P.g;
+    const int* slots = P.slots;
+    hap_status s;
     cudaError_t e = cudaSuccess;
-    if (light && light != st && perm_can_split(pa)) {
+    if (staged) {
+        // K1 (on st) staged the draws: the table pass waits for it on the side stream
+        cudaStream_t gs = owner->serial ? st : owner->side;
+        if (gs != st) {
+            e = cudaEventRecord(owner->ev_ready[1], st);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(gs, owner->ev_ready[1], 0);
+        }
+        if (e == cudaSuccess) {
+            pa.split = 2;
+            pa.span = next_span(owner, HAP_PHASE_PERMGEN);
+            PhaseScope ps(owner, HAP_PHASE_PERMGEN, 1, gs);
+            e = launch_perm(pa, owner->sm_count, gs);
+        }
+        if (e == cudaSuccess && gs != st) e = cudaEventRecord(owner->ev_ready[0], gs);
+        if (e == cudaSuccess && gs != st) e = cudaStreamWaitEvent(st, owner->ev_ready[0], 0);
+        if (e != cudaSuccess) return cuda_fail(owner, e, "perm generator");
+    } else if (light && light != st && perm_can_split(pa)) {
         // split generator: K2a (draws, register-only) on the light stream, where it runs
         // beside the other wave's mask-GEMM for free; K2b (table, chains, rows) on `st`,
         // i.e. never beside a mask-GEMM (both lean on shared-memory bandwidth)
@@ -727,11 +767,11 @@ hap_status run_wave(hap_ctx owner, int G, const WaveTest* T, int pair, cudaStrea
         if (e == cudaSuccess) e = cudaStreamWaitEvent(st, owner->ev_ready[0], 0);  // join
         if (e != cudaSuccess) return cuda_fail(owner, e, "perm generator");
     }
-    if ((s = get_schedule(owner, g, npairs, st, g))) return s;
+    if ((s = get_schedule(owner, g, P.npairs, st, g))) return s;
     {
         g.span = next_span(owner, HAP_PHASE_MASKGEMM);
         PhaseScope ps(owner, HAP_PHASE_MASKGEMM, 1, st);
-        e = launch_maskgemm(maps, g, pair, st);
+        e = launch_maskgemm(P.maps, g, pair, st);
     }
     for (int k = 0; k < pa.G && e == cudaSuccess; ++k) {
         e = cudaEventRecord(T[k].w->ev_free[slots[k]], st);
@@ -739,6 +779,15 @@ hap_status run_wave(hap_ctx owner, int G, const WaveTest* T, int pair, cudaStrea
     }
     if (e != cudaSuccess) return cuda_fail(owner, e, "mask-GEMM");
     return HAP_OK;
+}
+
+
+hap_status run_wave(hap_ctx owner, int G, const WaveTest* T, int pair, cudaStream_t st,
+                    bool shared = false, cudaStream_t light = nullptr) {
+    WavePlan P;
+    hap_status s = plan_wave(owner, G, T, pair, shared, P);
+    if (s) return s;
+    return launch_wave(owner, T, pair, st, P, light);
 }
 
 hap_status check_cfg(hap_ctx c, const hap_perm_cfg* cfg) {
@@ -873,17 +922,28 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
             ++i;
             if (!one_block) break;
         }
+        const bool multi = G == 1 && ceil_div(std::max<int64_t>(B, 1), R - 1) > block_tiles(cfg, Q[0].n_pad, R);
+        WavePlan P;
+        bool staged = false;
+        if (!s && G > 0 && !multi && B > 0) {
+            s = plan_wave(W[0], G, T, pair, shared, P);
+            // EXPERIMENT (HAP_K1_DRAWS=1): the wave's generator draws ride in K1's idle issue
+            // slots and K2 keeps only its table pass; bit-exact, but the lane then runs
+            // K1 -> K2b -> K3 in series and measured 106 vs 85 us per C2 test, so off
+            static const char* kd = getenv("HAP_K1_DRAWS");
+            staged = !s && kd && atoi(kd) != 0 && perm_can_split(P.pa);
+        }
         if (!s && G > 0) {
-            s = align_wave(W[0], G, W, Q, mode, ls);  // one K1 launch for the wave
+            s = align_wave(W[0], G, W, Q, mode, ls, staged ? &P.pa : nullptr);  // one K1 launch
             if (s) c->err = "wave " + std::to_string(wave) + ": " + W[0]->err;
         }
         if (s || G == 0) break;
-        if (G == 1 && ceil_div(std::max<int64_t>(B, 1), R - 1) > block_tiles(cfg, T[0].w->n_pad, R)) {
+        if (multi) {
             s = hap_permtest(T[0].w, T[0].info, T[0].cfg, T[0].counts, nullptr, ls);  // blocks
         } else if (B > 0) {
             static const char* sp = getenv("HAP_BATCH_SPLIT");  // K2a on the side stream
             const bool split = sp && atoi(sp) != 0;
-            s = run_wave(T[0].w, G, T, pair, ls, shared, split ? T[0].w->side : nullptr);
+            s = launch_wave(T[0].w, T, pair, ls, P, split ? T[0].w->side : nullptr, staged);
         }
         if (s) c->err = "wave " + std::to_string(wave) + ": " + T[0].w->err;
         ++wave;

@@ -257,4 +257,47 @@ HAP_DEV uint32_t u32x4_get(const u32x4& v, uint32_t e) {
     return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
 }
 
+// ---- PERM-SPEC v1 draws (R6), shared by K2 and K1's staged-draw pass
+// U(N-k) for step k: Lemire on the main-stream word x; rejected words are replaced by
+// the side stream (counter (q', b, s, 1+k)) in order.
+HAP_DEV uint32_t fy_target(uint32_t x, uint32_t k, uint32_t N, uint32_t b,
+                                              uint32_t s, uint32_t k0, uint32_t k1) {
+    const uint32_t bound = N - k;
+    uint64_t m = (uint64_t)x * bound;
+    uint32_t lo = (uint32_t)m;
+    if (lo < bound) {
+        const uint32_t t = (0u - bound) % bound;
+        uint32_t side = 0;
+        while (lo < t) {
+            const u32x4 w = philox4x32_10(u32x4{side >> 2, b, s, 1u + k}, k0, k1);
+            x = u32x4_get(w, side & 3u);
+            ++side;
+            m = (uint64_t)x * bound;
+            lo = (uint32_t)m;
+        }
+    }
+    return k + (uint32_t)(m >> 32);
+}
+
+// targets j_k = k + U(N - k) of steps k0 .. k0+3 (one Philox block; Lemire, exact slow path)
+HAP_DEV void draw_targets(uint32_t k0, uint32_t nx, uint32_t N, uint32_t b,
+                                             uint32_t s, uint32_t key0, uint32_t key1, uint32_t j[4]) {
+    const u32x4 wd = philox4x32_10(u32x4{k0 >> 2, b, s, 0u}, key0, key1);
+    const uint32_t x[4] = {wd.x, wd.y, wd.z, wd.w};
+    bool slow = false;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {  // Lemire fast path; rejection needs lo < bound
+        const uint32_t k = k0 + e, bound = N - k;
+        const uint64_t m = (uint64_t)x[e] * bound;
+        slow |= (uint32_t)m < bound;
+        j[e] = k + (uint32_t)(m >> 32);
+    }
+    if (slow) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            if (k0 + e < nx) j[e] = fy_target(x[e], k0 + e, N, b, s, key0, key1);
+    }
+}
+
+
 }  // namespace hap

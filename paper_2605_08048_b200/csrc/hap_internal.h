@@ -16,51 +16,7 @@ constexpr int kChunkN = 256;    // d-columns per accumulator chunk (UMMA N <= 25
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 inline int64_t ceil_div(int64_t x, int64_t m) { return (x + m - 1) / m; }
 
-// ---- K1: alignment (k_align.cu) ----------------------------------------------------
 constexpr int kMaxWave = 4;  // tests per launch of a wave (K1, K2, K3)
-
-// One word pair of a K1 launch (its own workspace buffers)
-struct AlignPair {
-    const float* X;
-    const float* Y;
-    int64_t n_x, n_y, d, n_pad;
-    hap_align_info* info;    // device
-    double* inv;             // [N]    1/||h_i|| (0 for a zero row)
-    double* u;               // [d_pad] Householder axis (0 for the identity)
-    double* xbar;            // [d]
-    double* ybar;            // [d]
-    uint16_t* zt_hi;         // [>=d_pad][n_pad] bf16 bits
-    uint16_t* zt_lo;         // [>=d_pad][n_pad]
-    double* m;               // [d_pad] centre (multiple of 2^-12): planes hold z - m
-    double* t64;             // [d_pad] t = N m + t'
-    float2* ab;              // [d_pad] epilogue constants {2a, 2b}, a = n_x m, b = t - a
-    double* sconst;          // [2]     {sum a^2, sum b^2}
-    long long* acc;          // [2 d + d_pad] fixed-point column sums (zero between launches)
-    long long* bad;          // min ZeroVector row (LLONG_MAX = none; reset by the launch)
-};
-struct AlignArgs {
-    int G;                   // pairs in this launch (same d)
-    AlignPair p[kMaxWave];
-    int64_t item_off[kMaxWave + 1];  // items (R-row blocks) of pair g: [item_off[g], item_off[g+1])
-    int64_t d, d_pad;
-    int mode;                // hap_align_mode
-    long long* scratch;      // [1] ticket, [2] grid barrier of the launch
-    long long* stamps;       // optional [8 + 8 grid] globaltimer stamps (profiling)
-    unsigned long long* span;  // optional {first CTA entry, last CTA exit} globaltimer
-};
-// item geometry of K1: R pooled rows x all d columns as an fp32 smem tile of pitch P
-struct AlignGeom {
-    int rows, pitch;
-    bool stage_umc;    // per-column (u_c, m_c) staged in smem
-    bool stage_means;  // xbar, ybar also staged in smem
-    size_t smem;       // dynamic smem bytes
-};
-AlignGeom align_geometry(int64_t d);
-// fills item_off (n_pad / R items per pair) for the geometry of d
-void align_items(AlignArgs& a);
-// one cooperative kernel of `grid` CTAs (one per SM); scratch[2] holds its grid barrier
-cudaError_t launch_align(const AlignArgs& a, int grid, cudaStream_t st);
-constexpr int kAlignLaunches = 1;  // kernels issued by launch_align
 
 // A WAVE is up to kMaxWave independent tests (each aligned in its own workspace) whose
 // rows go through ONE K1 launch, whose generator rows go through ONE K2 launch and whose
@@ -96,6 +52,53 @@ void perm_items(PermArgs& a);
 bool perm_can_split(const PermArgs& a);
 cudaError_t launch_perm(const PermArgs& a, int sm_count, cudaStream_t st);
 cudaError_t launch_debug_alu_burn(uint32_t iters, int ctas, int threads, uint32_t* sink, cudaStream_t st);
+
+// ---- K1: alignment (k_align.cu) ----------------------------------------------------
+
+// One word pair of a K1 launch (its own workspace buffers)
+struct AlignPair {
+    const float* X;
+    const float* Y;
+    int64_t n_x, n_y, d, n_pad;
+    hap_align_info* info;    // device
+    double* inv;             // [N]    1/||h_i|| (0 for a zero row)
+    double* u;               // [d_pad] Householder axis (0 for the identity)
+    double* xbar;            // [d]
+    double* ybar;            // [d]
+    uint16_t* zt_hi;         // [>=d_pad][n_pad] bf16 bits
+    uint16_t* zt_lo;         // [>=d_pad][n_pad]
+    double* m;               // [d_pad] centre (multiple of 2^-12): planes hold z - m
+    double* t64;             // [d_pad] t = N m + t'
+    float2* ab;              // [d_pad] epilogue constants {2a, 2b}, a = n_x m, b = t - a
+    double* sconst;          // [2]     {sum a^2, sum b^2}
+    long long* acc;          // [2 d + d_pad] fixed-point column sums (zero between launches)
+    long long* bad;          // min ZeroVector row (LLONG_MAX = none; reset by the launch)
+};
+struct AlignArgs {
+    int G;                   // pairs in this launch (same d)
+    AlignPair p[kMaxWave];
+    int64_t item_off[kMaxWave + 1];  // items (R-row blocks) of pair g: [item_off[g], item_off[g+1])
+    int64_t d, d_pad;
+    int mode;                // hap_align_mode
+    long long* scratch;      // [1] ticket, [2] grid barrier of the launch
+    long long* stamps;       // optional [8 + 8 grid] globaltimer stamps (profiling)
+    unsigned long long* span;  // optional {first CTA entry, last CTA exit} globaltimer
+    int do_draws;            // 1: also stage the generator draws of `draws` (K2a's work)
+    PermArgs draws;          // split = 1 job, run in K1's idle issue slots
+};
+// item geometry of K1: R pooled rows x all d columns as an fp32 smem tile of pitch P
+struct AlignGeom {
+    int rows, pitch;
+    bool stage_umc;    // per-column (u_c, m_c) staged in smem
+    bool stage_means;  // xbar, ybar also staged in smem
+    size_t smem;       // dynamic smem bytes
+};
+AlignGeom align_geometry(int64_t d);
+// fills item_off (n_pad / R items per pair) for the geometry of d
+void align_items(AlignArgs& a);
+// one cooperative kernel of `grid` CTAs (one per SM); scratch[2] holds its grid barrier
+cudaError_t launch_align(const AlignArgs& a, int grid, cudaStream_t st);
+constexpr int kAlignLaunches = 1;  // kernels issued by launch_align
 
 // ---- K3: tcgen05 mask-GEMM + statistic epilogue (k_maskgemm.cu) --------------------
 struct GemmTest {

@@ -510,6 +510,31 @@ __global__ void __launch_bounds__(kThreads, 2) k1_align_fused(AlignArgs a, int P
         }
         flush_t();
     }
+    // ---------------- P4b (optional): the generator draws of the wave (K2a's work, see
+    // k_perm.cu k2_draws), staged in each permutation's mask row.  Register-only work in
+    // this latency-bound kernel's idle issue slots; K2b then skips the draws.
+    if (a.do_draws) {
+        const PermArgs& pd = a.draws;
+        const int64_t ditems = pd.item_off[pd.G];
+        for (int64_t pi = (int64_t)cta * kWarps + warp; pi < ditems; pi += (int64_t)G * kWarps) {
+            int ti = 0;
+            while (ti + 1 < pd.G && pi >= pd.item_off[ti + 1]) ++ti;
+            const PermTest& T = pd.t[ti];
+            const int64_t li = pi - pd.item_off[ti];
+            if (li >= T.count) continue;  // observed-split rows: K2b
+            const uint32_t Nn = (uint32_t)T.N, nxx = (uint32_t)T.n_x;
+            const uint32_t key0 = (uint32_t)(T.seed & 0xFFFFFFFFu), key1 = (uint32_t)(T.seed >> 32);
+            const uint32_t b = (uint32_t)(T.b_begin + (uint64_t)li);
+            const int64_t R1 = pd.rows_per_tile - 1;
+            const int64_t orow = (li / R1) * pd.rows_per_tile + 1 + li % R1;
+            uint16_t* jrow = static_cast<uint16_t*>(T.out) + orow * T.n_pad;
+            for (uint32_t k0 = 4u * (uint32_t)lane; k0 < nxx; k0 += 128u) {
+                uint32_t j[4];
+                draw_targets(k0, nxx, Nn, b, T.s, key0, key1, j);
+                *reinterpret_cast<uint2*>(jrow + k0) = make_uint2(j[0] | (j[1] << 16), j[2] | (j[3] << 16));
+            }
+        }
+    }
     cstamp(a, 6);
     stamp(a, 4);
 
