@@ -549,3 +549,42 @@ def test_config5_batch_full_size(ctx, orc, shared):
         assert abs(res[p]["gemm_t_obs"] - ref["t_obs"]) <= 1e-5 * Ls
         for k in ("exceed_ge", "exceed_abs"):
             assert abs(res[p][k] - ref[k]) <= ref["flagged"], (p, k)
+
+
+_VARIANT_SCRIPT = r"""
+import sys, json
+sys.path.insert(0, sys.argv[1])
+import numpy as np, torch
+import hap_inputs as HI
+import paper_2605_08048_b200 as hap
+ctx = hap.Context(0)
+sizes = [50, 300, 129, 1000, 64, 333]
+Xp, cnx, Yp, cny = HI.varlen_batch(sizes, d=96)
+res = ctx.permtest_batch(torch.from_numpy(Xp).cuda(), cnx, torch.from_numpy(Yp).cuda(), cny,
+                         1200, HI.PERM_SEED, stream_id=9)
+print(json.dumps([[r["exceed_ge"], r["exceed_abs"], r["flagged"], r["gemm_t_obs"]] for r in res]))
+"""
+
+
+@pytest.mark.parametrize("env", [{"HAP_K1_DRAWS": "1"}, {"HAP_BATCH_SPLIT": "1"},
+                                 {"HAP_WAVE": "1"}, {"HAP_K3_ROUND_ROBIN": "1"}])
+def test_experimental_paths_bitwise_equal(env):
+    """The experimental scheduling paths (draws staged by K1, split generator on the side
+    stream, one test per wave, round-robin K3 schedule) give bitwise the default results."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+    def run(extra):
+        e = dict(os.environ)
+        for k in ("HAP_K1_DRAWS", "HAP_BATCH_SPLIT", "HAP_WAVE", "HAP_K3_ROUND_ROBIN"):
+            e.pop(k, None)
+        e.update(extra)
+        out = subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT, root], env=e,
+                             capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0, out.stderr[-2000:]
+        return json.loads(out.stdout.strip().splitlines()[-1])
+
+    assert run(env) == run({})
