@@ -213,25 +213,26 @@ __device__ __forceinline__ void emit_row_u32(const PermArgs& a, const PermTest& 
                                              int64_t li, uint32_t nx, int l) {
     const int64_t R1 = a.rows_per_tile - 1;
     const int64_t orow = (li / R1) * a.rows_per_tile + 1 + li % R1;
-    uint4* row = reinterpret_cast<uint4*>(static_cast<uint16_t*>(T.out) + orow * T.n_pad);
+    // lane = 4 consecutive entries per step (contiguous 512 B per warp: conflict-free
+    // LDS/STS.128), 8-byte stores of 4 bf16 (256 B per warp)
+    uint2* row = reinterpret_cast<uint2*>(static_cast<uint16_t*>(T.out) + orow * T.n_pad);
     uint4* L4 = reinterpret_cast<uint4*>(const_cast<uint32_t*>(LT));
     const uint4 z = make_uint4(0, 0, 0, 0);
-    for (int v8 = l; v8 < (int)(T.n_pad >> 3); v8 += 32) {
-        const uint4 q0 = L4[2 * v8], q1 = L4[2 * v8 + 1];
-        L4[2 * v8] = z;  // leave the table zeroed for the next permutation
-        L4[2 * v8 + 1] = z;
-        const uint32_t t[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
-        const uint32_t v0 = 8u * (uint32_t)v8;
-        uint32_t o[4];
+    for (int v4 = l; v4 < (int)(T.n_pad >> 2); v4 += 32) {
+        const uint4 q = L4[v4];
+        L4[v4] = z;  // leave the table zeroed for the next permutation
+        const uint32_t t[4] = {q.x, q.y, q.z, q.w};
+        const uint32_t v0 = 4u * (uint32_t)v4;
+        uint32_t o[2];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
+        for (int e = 0; e < 2; ++e) {
             // low position: selected unless exiled (t + 1 != 0); high: iff written (t != 0)
             const uint32_t va = v0 + 2 * e, vb = va + 1;
             const bool sa = t[2 * e] + (va < nx ? 1u : 0u) != 0u;
             const bool sb = t[2 * e + 1] + (vb < nx ? 1u : 0u) != 0u;
             o[e] = (sa ? 0x3F80u : 0u) | (sb ? 0x3F800000u : 0u);
         }
-        row[v8] = make_uint4(o[0], o[1], o[2], o[3]);
+        row[v4] = make_uint2(o[0], o[1]);
     }
 }
 
@@ -317,17 +318,18 @@ __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy32(PermArgs a, int 
         // ~70 % of them) is exiled right here; the others enter the list at their second
         // node, at offsets from a warp prefix sum of the per-lane counts (4 ballots).
         uint32_t nst = 0;
-        for (uint32_t p0 = (nx & ~7u) + 8u * (uint32_t)l; __any_sync(0xffffffffu, p0 < N);
-             p0 += 256u) {
+        for (uint32_t base = nx & ~3u; __any_sync(0xffffffffu, base + 4u * (uint32_t)l < N);
+             base += 256u) {
+            // entries base + 4l .. +3 and base + 128 + 4l .. +3: each half is a contiguous
+            // 512 B per warp (conflict-free LDS.128); beyond N the table is 0
+            const uint32_t pa = base + 4u * (uint32_t)l, pb = pa + 128u;
             uint4 q0 = make_uint4(0, 0, 0, 0), q1 = q0;
-            if (p0 < N) {  // beyond N the table is 0 (p0 + 7 < lt_pitch)
-                q0 = *reinterpret_cast<const uint4*>(LT + p0);
-                q1 = *reinterpret_cast<const uint4*>(LT + p0 + 4);
-            }
+            if (pa < N) q0 = *reinterpret_cast<const uint4*>(LT + pa);
+            if (pb < N) q1 = *reinterpret_cast<const uint4*>(LT + pb);
             uint32_t t[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
-            if (p0 < nx) {  // positions below n_x only occur in the first pass
+            if (pa < nx) {  // positions below n_x only occur in the first pass (lane 0)
 #pragma unroll
-                for (int e = 0; e < 8; ++e) t[e] = p0 + e >= nx ? t[e] : 0u;
+                for (int e = 0; e < 4; ++e) t[e] = pa + e >= nx ? t[e] : 0u;
             }
             uint32_t u[8];
 #pragma unroll
