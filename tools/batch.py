@@ -1,9 +1,9 @@
 """Throughput and phase timeline of hap_permtest_batch on P C2-shaped pairs.
-usage: python tools_batch.py [P] [reps]"""
+usage: python tools/batch.py [P] [reps]"""
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
 

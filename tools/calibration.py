@@ -1,13 +1,13 @@
 """C5 (BASELINE.json configs[4]): Type-I calibration study on the GPU - R null replicates of
 vMF clouds with equal concentration and mean directions theta apart (n = 500/500, d = 768,
 B = 10^4), aligned vs naive, through hap_permtest_batch.  Prints one JSON line.
-usage: python tools_calibration.py [R] [chunk]"""
+usage: python tools/calibration.py [R] [chunk]"""
 import json
 import os
 import sys
 import time
 
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
 

@@ -1,11 +1,11 @@
 """Single-test throughput of a BASELINE config on one GPU (C1, C2, C3) through
 hap_align + hap_permtest: device time per test (CUDA events), perms/s, and the K3
-algorithmic TFLOP/s from a serialised profiling pass.  usage: python tools_config.py C3 [B]"""
+algorithmic TFLOP/s from a serialised profiling pass.  usage: python tools/config.py C3 [B]"""
 import json
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 
 import hap_inputs as HI

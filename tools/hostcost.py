@@ -1,6 +1,6 @@
 """Host submission cost vs GPU time per C2 test (is the loop launch-bound?)."""
 import sys, os, time
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import hap_inputs as HI
 import paper_2605_08048_b200 as hap

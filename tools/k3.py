@@ -1,6 +1,6 @@
 """K3 alone, back to back (serialised profiling: K2 on the caller stream, so K3 time is clean)."""
 import sys, os
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import hap_inputs as HI
 import paper_2605_08048_b200 as hap

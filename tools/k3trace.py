@@ -1,6 +1,6 @@
 import sys, os, ctypes
 os.environ["HAP_K3_EXPERIMENT"] = str(16 | int(sys.argv[1]) if len(sys.argv) > 1 else 16)
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import hap_inputs as HI
 import paper_2605_08048_b200 as hap

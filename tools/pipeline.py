@@ -1,7 +1,7 @@
 """Two contexts on two streams: consecutive independent tests overlap (K1/K2 of test k+1
 under K3 of test k)."""
 import sys, os, time
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import hap_inputs as HI
 import paper_2605_08048_b200 as hap

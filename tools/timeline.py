@@ -1,6 +1,6 @@
 """Phase timeline of consecutive C2 tests (profiling level 1: events, overlap kept)."""
 import sys, os, json
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import hap_inputs as HI
 import paper_2605_08048_b200 as hap
