@@ -588,3 +588,18 @@ def test_experimental_paths_bitwise_equal(env):
         return json.loads(out.stdout.strip().splitlines()[-1])
 
     assert run(env) == run({})
+
+
+def test_gpu_power_broader_x(ctx):
+    """NEXT-3: when X is genuinely broader (kappa_X < kappa_Y) the
+    aligned one-sided test keeps its power (rejects in most replicates), like the naive one."""
+    R, B = 60, 999
+    pairs = [HI.make_pair(HI.PairSpec(100, 100, 32, 25.0, 60.0, 45.0, seed=79), rep) for rep in range(R)]
+    Xp = np.concatenate([p[0] for p in pairs])
+    Yp = np.concatenate([p[1] for p in pairs])
+    cu = np.arange(R + 1, dtype=np.int64) * 100
+    power = {}
+    for mode in (0, 1):
+        res = ctx.permtest_batch(_cuda(Xp), cu, _cuda(Yp), cu, B, SEED, mode=mode)
+        power[mode] = np.mean([r["p_value"] <= 0.05 for r in res])
+    assert power[0] >= 0.9, power
