@@ -44,7 +44,6 @@ struct hap_ctx_s {
     hap_ctx sub[2][kMaxWave] = {};
     cudaStream_t sub_stream[2] = {nullptr, nullptr};
     cudaEvent_t ev_sub[2] = {nullptr, nullptr};
-    cudaEvent_t ev_k1[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};  // per workspace set
     // cached K3 schedules: key {d_pad, npairs, (ntiles, n_pad) per test} -> offset (ints)
     // in buf[kSched]; new ones are staged in pinned host memory and copied on the stream
     struct Sched { std::vector<int64_t> key; int64_t off; int max_slots; };
@@ -454,8 +453,6 @@ hap_status hap_destroy(hap_ctx c) {
             if (c->sub[i][k]) hap_destroy(c->sub[i][k]);
         if (c->sub_stream[i]) cudaStreamDestroy(c->sub_stream[i]);
         if (c->ev_sub[i]) cudaEventDestroy(c->ev_sub[i]);
-        if (c->ev_k1[i]) cudaEventDestroy(c->ev_k1[i]);
-        if (c->ev_done[i]) cudaEventDestroy(c->ev_done[i]);
     }
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     for (int i = 0; i < 2; ++i) {
