@@ -13,6 +13,8 @@ HEADERS = ["hap_device.cuh", "hap_internal.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden"]
+# experiments only (e.g. -DHAP_K3_STAGES=4); empty in normal builds
+FLAGS += os.environ.get("HAP_EXTRA_NVCC_FLAGS", "").split()
 
 
 def _stale() -> bool:

@@ -29,6 +29,8 @@
 #include <cfloat>
 #include <climits>
 #include <mutex>
+#include <cstdlib>
+#include <algorithm>
 
 #include "hap_device.cuh"
 #include "hap_internal.h"
@@ -586,15 +588,18 @@ __global__ void __launch_bounds__(kThreads, 2) k1_align_fused(AlignArgs a, int P
 }  // namespace
 
 AlignGeom align_geometry(int64_t d) {
+    // EXPERIMENT HAP_K1_SMEM_KB: cap K1's shared memory (so it fits beside a deeper K3 ring)
+    static const char* cap_env = getenv("HAP_K1_SMEM_KB");
+    const size_t cap = cap_env ? (size_t)atoi(cap_env) * 1024u : 220u * 1024u;
     AlignGeom g{};
     g.pitch = (int)(round_up(d, 16) + 2);  // = 2 (mod 16): conflict-free (column, row-pair) reads
     g.rows = kMaxItemRows;
-    while (g.rows > 2 && (size_t)g.rows * g.pitch * 4 + (size_t)8 * round_up(d, 32) > 200u * 1024u)
+    const size_t umc = (size_t)8 * round_up(d, 32), means = (size_t)16 * d;
+    while (g.rows > 2 && (size_t)g.rows * g.pitch * 4 + std::min<size_t>(2 * umc, cap / 2) > std::min<size_t>(cap, 200u * 1024u))
         g.rows >>= 1;
-    const size_t tile = (size_t)g.rows * g.pitch * 4, umc = (size_t)8 * round_up(d, 32),
-                 means = (size_t)16 * d;
-    g.stage_umc = tile + 2 * umc <= 220u * 1024u;
-    g.stage_means = g.stage_umc && tile + 2 * umc + means <= 220u * 1024u;
+    const size_t tile = (size_t)g.rows * g.pitch * 4;
+    g.stage_umc = tile + 2 * umc <= cap;
+    g.stage_means = g.stage_umc && tile + 2 * umc + means <= cap;
     g.smem = tile + (g.stage_umc ? 2 * umc : 0) + (g.stage_means ? means : 0);  // + t' partials
     return g;
 }

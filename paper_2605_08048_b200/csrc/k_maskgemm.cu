@@ -42,10 +42,13 @@ constexpr uint32_t kTmemCols = 512;
 constexpr int kStageA = kTileM * 128;  // 16 KB: 128 rows x 64 bf16
 constexpr int kFinCap = 400;             // deferred finalizes per CTA (smem tail list)
 
+#ifndef HAP_K3_STAGES
+#define HAP_K3_STAGES 3
+#endif
 template <int kPair>
 struct Cfg {
     // 3 x 48 KB leaves room for the generator (K2) CTAs to co-reside on every SM
-    static constexpr int kStages = kPair == 2 ? 3 : 2;
+    static constexpr int kStages = kPair == 2 ? HAP_K3_STAGES : 2;
     static constexpr int kBRows = kChunkN / kPair;   // B rows (d-columns) held per CTA
     static constexpr int kStageB = kBRows * 128;     // one plane
     static constexpr int kStageBytes = kStageA + 2 * kStageB;
