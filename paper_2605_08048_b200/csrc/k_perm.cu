@@ -18,6 +18,8 @@
 // emits the exact 0/1 mask row.  Bit-exact against oracle/orc_perm_set (tests).
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "hap_device.cuh"
 #include "hap_internal.h"
 
@@ -472,7 +474,8 @@ cudaError_t launch_debug_alu_burn(uint32_t iters, int ctas, int threads, uint32_
 }
 
 bool perm_can_split(const PermArgs& a) {
-    if (a.out_kind != kMaskBf16Row) return false;
+    static const char* nar = getenv("HAP_K2_NARROW");
+    if (a.out_kind != kMaskBf16Row || (nar && atoi(nar))) return false;
     int64_t maxN = 0;
     for (int g = 0; g < a.G; ++g) {
         if (a.t[g].exhaustive) return false;
@@ -500,7 +503,8 @@ cudaError_t launch_perm(const PermArgs& a, int sm_count, cudaStream_t st) {
     for (int g = 0; g < a.G; ++g) maxN = std::max<int64_t>(maxN, a.t[g].N);
     const int lt_pitch = (int)round_up(maxN, 64);  // entries, 128-byte multiple; >= every n_pad
     // wide (uint32) table + start list when 4 warps fit in the budget, else uint16 table
-    const bool wide = (size_t)lt_pitch * 5u + 160u <= (200u * 1024u) / 4u;
+    static const char* nar = getenv("HAP_K2_NARROW");  // EXPERIMENT: force the u16 table
+    const bool wide = (size_t)lt_pitch * 5u + 160u <= (200u * 1024u) / 4u && !(nar && atoi(nar));
     const size_t per_warp = wide ? (size_t)lt_pitch * 5u + 160u : (size_t)(lt_pitch + 128) * sizeof(uint16_t);
     const int nw = (int)std::max<size_t>(1, std::min<size_t>(kPermWarps, (200u * 1024u) / per_warp));
     const size_t smem = (size_t)nw * per_warp;
