@@ -603,3 +603,23 @@ def test_gpu_power_broader_x(ctx):
         res = ctx.permtest_batch(_cuda(Xp), cu, _cuda(Yp), cu, B, SEED, mode=mode)
         power[mode] = np.mean([r["p_value"] <= 0.05 for r in res])
     assert power[0] >= 0.9, power
+
+
+def test_config2_batch_full_size_bench_launch(ctx, orc):
+    """C2 at full size in exactly the bench's launch configuration: one wave of 3 tests
+    through hap_permtest_batch (generator streams as bench.py assigns them), every test's
+    observed statistic, same-path T_obs and counts vs the oracle."""
+    pairs = [HI.make_pair(HI.PairSpec(1000, 1000, 768, HI.kappa_for(768), HI.kappa_for(768), 30.0,
+                                      seed=1002), rep=i) for i in range(3)]
+    Xp = np.concatenate([p[0] for p in pairs])
+    Yp = np.concatenate([p[1] for p in pairs])
+    cu = np.arange(4, dtype=np.int64) * 1000
+    B, s0 = 10000, 1_000_003
+    res = ctx.permtest_batch(_cuda(Xp), cu, _cuda(Yp), cu, B, SEED, stream_id=s0, wave=3)
+    for p in range(3):
+        ref = orc.run_pair(pairs[p][0], pairs[p][1], B, SEED, s=s0 + p)
+        Ls = abs(ref["L_x"]) + abs(ref["L_y"])
+        assert abs(res[p]["t_obs"] - ref["t_obs"]) <= 1e-10 * Ls
+        assert abs(res[p]["gemm_t_obs"] - ref["t_obs"]) <= 1e-5 * Ls
+        for k in ("exceed_ge", "exceed_abs"):
+            assert abs(res[p][k] - ref[k]) <= ref["flagged"], (p, k)
