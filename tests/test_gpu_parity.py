@@ -674,3 +674,29 @@ def test_fuzz_batches_vs_oracle(ctx, orc, seed):
         assert abs(res[p]["t_obs"] - ref["t_obs"]) <= 1e-10 * Ls, p
         for k in ("exceed_ge", "exceed_abs"):
             assert abs(res[p][k] - ref[k]) <= ref["flagged"], (p, k, res[p][k], ref[k])
+
+
+def test_batch_argument_errors(hap, ctx):
+    """Synchronous argument errors of hap_permtest_batch (nothing enqueued)."""
+    import torch
+    sizes = [10, 12]
+    Xp, cnx, Yp, cny = HI.varlen_batch(sizes, d=16)
+    X, Y = _cuda(Xp), _cuda(Yp)
+    infos = torch.zeros((2, hap.INFO_BYTES), dtype=torch.uint8, device="cuda")
+    counts = torch.zeros((2, 3), dtype=torch.int64, device="cuda")
+    ok = hap.make_cfg(SEED, 100)
+    with pytest.raises(hap.HapError):  # exhaustive mode is per pair only
+        hap.hap_permtest_batch(ctx.h, X, cnx, Y, cny, 0, hap.make_cfg(SEED, 100, flags=hap.HAP_FLAG_EXHAUSTIVE),
+                               infos, counts)
+    with pytest.raises(hap.HapError):  # bad alignment mode
+        hap.hap_permtest_batch(ctx.h, X, cnx, Y, cny, 7, ok, infos, counts)
+    with pytest.raises(hap.HapError):  # pair_sel out of range
+        hap.hap_permtest_batch(ctx.h, X, cnx, Y, cny, 0, ok, infos, counts, pair_sel=[0, 5])
+    with pytest.raises(hap.HapError):  # host inputs are not accepted by the batch
+        hap.hap_permtest_batch(ctx.h, torch.from_numpy(Xp), cnx, torch.from_numpy(Yp), cny, 0, ok,
+                               infos, counts)
+    with pytest.raises(hap.HapError):  # b_end beyond 2^32
+        hap.hap_permtest_batch(ctx.h, X, cnx, Y, cny, 0, hap.make_cfg(SEED, 1 << 33), infos, counts)
+    hap.hap_permtest_batch(ctx.h, X, cnx, Y, cny, 0, ok, infos, counts)  # still usable
+    hap.hap_sync(ctx.h)
+    assert int(counts.sum()) > 0
