@@ -190,6 +190,17 @@ GemmArgs gemm_args(hap_ctx c) {
 // (K3 piece durations on B200: 15.7 us for widths 32..128, 20.5 us for 256).
 constexpr double kPieceFloor = 4.0 * 196.0;
 
+constexpr int64_t kSchedInts = 1 << 20;  // 4 MB schedule ring (device + pinned host staging)
+
+hap_status reserve_schedule(hap_ctx c) {
+    if (c->sched_host) return HAP_OK;
+    hap_status s = ensure(c, kSched, (size_t)kSchedInts * sizeof(int));
+    if (s) return s;
+    if (cudaMallocHost(&c->sched_host, (size_t)kSchedInts * sizeof(int)) != cudaSuccess)
+        return fail(c, HAP_E_OOM, "pinned schedule staging");
+    return HAP_OK;
+}
+
 hap_status get_schedule(hap_ctx c, const GemmArgs& w, int np, cudaStream_t st, GemmArgs& g) {
     std::vector<int64_t> key = {w.d_pad, np};
     for (int k = 0; k < w.G; ++k) {
@@ -300,14 +311,8 @@ hap_status get_schedule(hap_ctx c, const GemmArgs& w, int np, cudaStream_t st, G
     std::copy(npc.begin(), npc.end(), blob.begin() + (np + 1));
     blob.insert(blob.end(), pcs.begin(), pcs.end());
     const int64_t need = (int64_t)blob.size();
-    constexpr int64_t kSchedInts = 1 << 20;  // 4 MB ring (device + pinned host staging)
     if (need > kSchedInts) return fail(c, HAP_E_INVALID_ARG, "K3 schedule too large");
-    if (!c->sched_host) {
-        hap_status s = ensure(c, kSched, (size_t)kSchedInts * sizeof(int));
-        if (s) return s;
-        if (cudaMallocHost(&c->sched_host, (size_t)kSchedInts * sizeof(int)) != cudaSuccess)
-            return fail(c, HAP_E_OOM, "pinned schedule staging");
-    }
+    if (hap_status s = reserve_schedule(c)) return s;
     if (c->sched_used + need > kSchedInts) {  // wrap: the ring's old copies must have run
         if (c->last_stream) cudaStreamSynchronize(c->last_stream);
         cudaStreamSynchronize(st);
@@ -491,6 +496,29 @@ namespace {
 
 // Workspace of one pair in `c` (grow-only), host inputs staged on the stream; fills the
 // pair's K1 arguments and records the pair's shape in the context.
+// Grow-only workspace for pairs of up to N pooled rows in d dimensions and waves of up to
+// `tiles` mask tiles of R rows (owner buffers included): allocating (and zeroing) buffers
+// synchronises, so the batch reserves every workspace before its first launch.
+hap_status reserve_pair(hap_ctx c, int64_t N, int64_t d, int64_t tiles, int64_t R) {
+    const int64_t n_pad = round_up(N, kKBlock), d_pad = round_up(d, 32);
+    hap_status s;
+    if ((s = ensure(c, kXbar, d * 8)) || (s = ensure(c, kYbar, d * 8)) ||
+        (s = ensure(c, kInv, N * 8)) || (s = ensure(c, kU, d_pad * 8)) ||
+        (s = ensure(c, kZhi, (size_t)zt_rows(d_pad) * n_pad * 2)) ||
+        (s = ensure(c, kZlo, (size_t)zt_rows(d_pad) * n_pad * 2)) ||
+        (s = ensure(c, kTpart, (size_t)(2 * d + d_pad) * 8)) ||
+        (s = ensure(c, kT64, d_pad * 8)) || (s = ensure(c, kAB, d_pad * 8)) ||
+        (s = ensure(c, kM, d_pad * 8)) || (s = ensure(c, kSconst, 16)) ||
+        (s = ensure(c, kMask, (size_t)std::max<int64_t>(2, tiles) * R * n_pad * 2)) ||
+        (s = ensure(c, kMask1, (size_t)std::max<int64_t>(2, tiles) * R * n_pad * 2)) ||
+        (s = ensure(c, kGemmPart, (size_t)kMaxWave * tiles * std::max<int64_t>(1, ceil_div(d_pad, 32)) * R *
+                                      sizeof(float2))) ||
+        (s = ensure(c, kTileDone, (size_t)kMaxWave * tiles * sizeof(unsigned))) ||
+        (s = reserve_schedule(c)))
+        return s;
+    return HAP_OK;
+}
+
 hap_status prepare_pair(hap_ctx c, const float* X, int64_t n_x, const float* Y, int64_t n_y, int64_t d,
                         hap_align_info* info, cudaStream_t st, AlignPair& q) {
     if (!X || !Y || !info) return fail(c, HAP_E_INVALID_ARG, "null pointer");
@@ -886,6 +914,21 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
     static const char* wv = getenv("HAP_WAVE");
     const int wave_max = std::max(1, std::min(kMaxWave, cfg->wave > 0 ? cfg->wave
                                                         : wv ? atoi(wv) : shared ? kMaxWave : 3));
+    {  // reserve every workspace the waves can use before the first launch
+        int64_t maxN = 0;
+        for (int64_t i = 0; i < n; ++i) {
+            const int64_t p = pair_sel ? pair_sel[i] : i;
+            maxN = std::max<int64_t>(maxN, (cu_nx[p + 1] - cu_nx[p]) + (cu_ny[p + 1] - cu_ny[p]));
+        }
+        if (maxN > 0) {
+            const int64_t n_pad = round_up(maxN, kKBlock);
+            const int64_t tiles = std::min(std::max<int64_t>(1, ceil_div(std::max<int64_t>(B, 1), R - 1)),
+                                           block_tiles(cfg, n_pad, R));
+            for (int k = 0; k < 2 && !s; ++k)
+                for (int j = 0; j < wave_max && !s; ++j) s = reserve_pair(c->sub[k][j], maxN, d, tiles, R);
+            if (s) return fail(c, s, "batch workspace");
+        }
+    }
     // fork: the two lanes start after the work already on the caller's stream
     cudaError_t e = cudaEventRecord(c->ev_fork, st);
     for (int k = 0; k < 2 && e == cudaSuccess; ++k) e = cudaStreamWaitEvent(c->sub_stream[k], c->ev_fork, 0);
