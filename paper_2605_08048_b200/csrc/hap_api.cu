@@ -44,6 +44,13 @@ struct hap_ctx_s {
     hap_ctx sub[2][kMaxWave] = {};
     cudaStream_t sub_stream[2] = {nullptr, nullptr};
     cudaEvent_t ev_sub[2] = {nullptr, nullptr};
+    // host inputs: per lane a copy stream that stages a wave's rows as soon as the lane's
+    // previous K1 (the last reader of the staging buffers) is done
+    // (two staging buffers per workspace, alternating over the lane's waves)
+    cudaStream_t cp_stream[2] = {nullptr, nullptr};
+    cudaEvent_t ev_k1done[2][2] = {}, ev_copied[2] = {nullptr, nullptr};
+    bool k1_recorded[2][2] = {};
+    int lane_waves[2] = {0, 0};
     // cached K3 schedules: key {d_pad, npairs, (ntiles, n_pad) per test} -> offset (ints)
     // in buf[kSched]; new ones are staged in pinned host memory and copied on the stream
     struct Sched { std::vector<int64_t> key; int64_t off; int max_slots; };
@@ -69,7 +76,7 @@ namespace {
 enum Buf {
     kX = 0, kY, kNrm, kCoef, kPart, kXbar, kYbar, kU, kZhi, kZlo, kTpart, kT64, kAB, kMask,
     kM, kSconst, kGemmPart, kTileDone, kScal, kSpart, kScratch, kMask1, kInv, kStamps, kK3Stamps,
-    kSched, kSpans, kNumBufs
+    kSched, kSpans, kX2, kY2, kNumBufs
 };
 
 hap_status fail(hap_ctx c, hap_status s, const std::string& msg) {
@@ -458,6 +465,10 @@ hap_status hap_destroy(hap_ctx c) {
             if (c->sub[i][k]) hap_destroy(c->sub[i][k]);
         if (c->sub_stream[i]) cudaStreamDestroy(c->sub_stream[i]);
         if (c->ev_sub[i]) cudaEventDestroy(c->ev_sub[i]);
+        if (c->cp_stream[i]) cudaStreamDestroy(c->cp_stream[i]);
+        for (int b = 0; b < 2; ++b)
+            if (c->ev_k1done[i][b]) cudaEventDestroy(c->ev_k1done[i][b]);
+        if (c->ev_copied[i]) cudaEventDestroy(c->ev_copied[i]);
     }
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     for (int i = 0; i < 2; ++i) {
@@ -519,8 +530,11 @@ hap_status reserve_pair(hap_ctx c, int64_t N, int64_t d, int64_t tiles, int64_t 
     return HAP_OK;
 }
 
-hap_status prepare_pair(hap_ctx c, const float* X, int64_t n_x, const float* Y, int64_t n_y, int64_t d,
-                        hap_align_info* info, cudaStream_t st, AlignPair& q) {
+// host inputs are copied on `cp` (default: st)
+hap_status prepare_pair_cp(hap_ctx c, const float* X, int64_t n_x, const float* Y, int64_t n_y, int64_t d,
+                           hap_align_info* info, cudaStream_t st, AlignPair& q, cudaStream_t cp = nullptr,
+                           int buf = 0) {
+    const int bX = buf ? kX2 : kX, bY = buf ? kY2 : kY;
     if (!X || !Y || !info) return fail(c, HAP_E_INVALID_ARG, "null pointer");
     if (n_x < 1 || n_y < 1 || n_x + n_y > 65535)
         return fail(c, HAP_E_INVALID_ARG, "need 1 <= n_x, n_y and n_x + n_y <= 65535");
@@ -543,16 +557,16 @@ hap_status prepare_pair(hap_ctx c, const float* X, int64_t n_x, const float* Y, 
     const float* dX = X;
     const float* dY = Y;
     if (!is_device_ptr(X)) {
-        if ((s = ensure(c, kX, (size_t)n_x * d * 4))) return s;
-        cudaError_t e = cudaMemcpyAsync(c->buf[kX], X, (size_t)n_x * d * 4, cudaMemcpyHostToDevice, st);
+        if ((s = ensure(c, bX, (size_t)n_x * d * 4))) return s;
+        cudaError_t e = cudaMemcpyAsync(c->buf[bX], X, (size_t)n_x * d * 4, cudaMemcpyHostToDevice, cp ? cp : st);
         if (e != cudaSuccess) return cuda_fail(c, e, "H2D X");
-        dX = B<float>(c, kX);
+        dX = B<float>(c, bX);
     }
     if (!is_device_ptr(Y)) {
-        if ((s = ensure(c, kY, (size_t)n_y * d * 4))) return s;
-        cudaError_t e = cudaMemcpyAsync(c->buf[kY], Y, (size_t)n_y * d * 4, cudaMemcpyHostToDevice, st);
+        if ((s = ensure(c, bY, (size_t)n_y * d * 4))) return s;
+        cudaError_t e = cudaMemcpyAsync(c->buf[bY], Y, (size_t)n_y * d * 4, cudaMemcpyHostToDevice, cp ? cp : st);
         if (e != cudaSuccess) return cuda_fail(c, e, "H2D Y");
-        dY = B<float>(c, kY);
+        dY = B<float>(c, bY);
     }
     c->n_x = n_x;
     c->n_y = n_y;
@@ -582,6 +596,10 @@ hap_status prepare_pair(hap_ctx c, const float* X, int64_t n_x, const float* Y, 
     return HAP_OK;
 }
 
+hap_status prepare_pair(hap_ctx c, const float* X, int64_t n_x, const float* Y, int64_t n_y, int64_t d,
+                        hap_align_info* info, cudaStream_t st, AlignPair& q) {
+    return prepare_pair_cp(c, X, n_x, Y, n_y, d, info, st, q);
+}
 // ONE K1 launch aligning G pairs (each in its own workspace ws[k]); `owner` (= ws[0])
 // provides the launch's barrier / ticket words and the profiling records.
 hap_status align_wave(hap_ctx owner, int G, hap_ctx* ws, const AlignPair* pairs, hap_align_mode mode,
@@ -877,8 +895,11 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
         return fail(c, HAP_E_INVALID_ARG, "exhaustive mode: use hap_permtest per pair");
     hap_status s = check_cfg(c, cfg);
     if (s) return s;
-    if (!is_device_ptr(X_packed) || !is_device_ptr(Y_packed))
-        return fail(c, HAP_E_INVALID_ARG, "X_packed / Y_packed must be device memory");
+    // inputs in device memory, or both in host memory (pinned for overlap): each wave then
+    // copies its pairs' rows on its lane stream, overlapping the other lane's kernels
+    const bool host_in = !is_device_ptr(X_packed);
+    if (host_in != !is_device_ptr(Y_packed))
+        return fail(c, HAP_E_INVALID_ARG, "X_packed and Y_packed must both be device or both host memory");
     const int64_t n = pair_sel ? n_sel : P;
     // shape checks are synchronous: validate every selected pair before enqueuing anything
     for (int64_t i = 0; i < n; ++i) {
@@ -903,6 +924,14 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
             (cudaStreamCreateWithFlags(&c->sub_stream[k], cudaStreamNonBlocking) != cudaSuccess ||
              cudaEventCreateWithFlags(&c->ev_sub[k], cudaEventDisableTiming) != cudaSuccess))
             return fail(c, HAP_E_CUDA, "batch streams");
+        if (host_in && !c->cp_stream[k] &&
+            (cudaStreamCreateWithFlags(&c->cp_stream[k], cudaStreamNonBlocking) != cudaSuccess ||
+             cudaEventCreateWithFlags(&c->ev_k1done[k][0], cudaEventDisableTiming) != cudaSuccess ||
+             cudaEventCreateWithFlags(&c->ev_k1done[k][1], cudaEventDisableTiming) != cudaSuccess ||
+             cudaEventCreateWithFlags(&c->ev_copied[k], cudaEventDisableTiming) != cudaSuccess))
+            return fail(c, HAP_E_CUDA, "batch copy streams");
+        c->k1_recorded[k][0] = c->k1_recorded[k][1] = false;
+        c->lane_waves[k] = 0;
     }
     const int pair = cfg->pair_mode ? cfg->pair_mode : 2;
     const int64_t R = (int64_t)kTileM * pair;
@@ -915,23 +944,34 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
     const int wave_max = std::max(1, std::min(kMaxWave, cfg->wave > 0 ? cfg->wave
                                                         : wv ? atoi(wv) : shared ? kMaxWave : 3));
     {  // reserve every workspace the waves can use before the first launch
-        int64_t maxN = 0;
+        int64_t maxN = 0, maxnx = 0, maxny = 0;
         for (int64_t i = 0; i < n; ++i) {
             const int64_t p = pair_sel ? pair_sel[i] : i;
             maxN = std::max<int64_t>(maxN, (cu_nx[p + 1] - cu_nx[p]) + (cu_ny[p + 1] - cu_ny[p]));
+            maxnx = std::max<int64_t>(maxnx, cu_nx[p + 1] - cu_nx[p]);
+            maxny = std::max<int64_t>(maxny, cu_ny[p + 1] - cu_ny[p]);
         }
         if (maxN > 0) {
             const int64_t n_pad = round_up(maxN, kKBlock);
             const int64_t tiles = std::min(std::max<int64_t>(1, ceil_div(std::max<int64_t>(B, 1), R - 1)),
                                            block_tiles(cfg, n_pad, R));
             for (int k = 0; k < 2 && !s; ++k)
-                for (int j = 0; j < wave_max && !s; ++j) s = reserve_pair(c->sub[k][j], maxN, d, tiles, R);
+                for (int j = 0; j < wave_max && !s; ++j) {
+                    s = reserve_pair(c->sub[k][j], maxN, d, tiles, R);
+                    for (int b = 0; b < 2 && host_in; ++b) {
+                        if (!s) s = ensure(c->sub[k][j], b ? kX2 : kX, (size_t)maxnx * d * 4);
+                        if (!s) s = ensure(c->sub[k][j], b ? kY2 : kY, (size_t)maxny * d * 4);
+                    }
+                }
             if (s) return fail(c, s, "batch workspace");
         }
     }
     // fork: the two lanes start after the work already on the caller's stream
     cudaError_t e = cudaEventRecord(c->ev_fork, st);
-    for (int k = 0; k < 2 && e == cudaSuccess; ++k) e = cudaStreamWaitEvent(c->sub_stream[k], c->ev_fork, 0);
+    for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
+        e = cudaStreamWaitEvent(c->sub_stream[k], c->ev_fork, 0);
+        if (e == cudaSuccess && host_in) e = cudaStreamWaitEvent(c->cp_stream[k], c->ev_fork, 0);
+    }
     if (e != cudaSuccess) return cuda_fail(c, e, "batch fork");
     std::vector<hap_perm_cfg> pcs((size_t)n);
     int64_t i = 0, wave = 0;
@@ -949,7 +989,11 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
             if (G > 0 && !one_block) break;  // a multi-block test starts its own wave
             if (G > 0 && shared && (nx != Q[0].n_x || ny != Q[0].n_y)) break;  // same masks
             hap_ctx w = c->sub[k][G];
-            s = prepare_pair(w, X_packed + cu_nx[p] * d, nx, Y_packed + cu_ny[p] * d, ny, d, infos + p, ls, Q[G]);
+            const int sb = c->lane_waves[k] & 1;  // staging buffer of this wave
+            if (G == 0 && host_in && c->k1_recorded[k][sb])  // its last reader: the K1 two waves back
+                cudaStreamWaitEvent(c->cp_stream[k], c->ev_k1done[k][sb], 0);
+            s = prepare_pair_cp(w, X_packed + cu_nx[p] * d, nx, Y_packed + cu_ny[p] * d, ny, d, infos + p, ls,
+                                Q[G], host_in ? c->cp_stream[k] : nullptr, sb);
             if (s) {
                 c->err = "pair " + std::to_string(p) + ": " + w->err;
                 break;
@@ -973,10 +1017,20 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
             static const char* kd = getenv("HAP_K1_DRAWS");
             staged = !s && kd && atoi(kd) != 0 && perm_can_split(P.pa);
         }
+        if (!s && G > 0 && host_in) {  // K1 waits for the wave's rows
+            cudaEventRecord(c->ev_copied[k], c->cp_stream[k]);
+            cudaStreamWaitEvent(ls, c->ev_copied[k], 0);
+        }
         if (!s && G > 0) {
             s = align_wave(W[0], G, W, Q, mode, ls, staged ? &P.pa : nullptr);  // one K1 launch
             if (s) c->err = "wave " + std::to_string(wave) + ": " + W[0]->err;
         }
+        if (!s && G > 0 && host_in) {
+            const int sb = c->lane_waves[k] & 1;
+            cudaEventRecord(c->ev_k1done[k][sb], ls);
+            c->k1_recorded[k][sb] = true;
+        }
+        ++c->lane_waves[k];
         if (s || G == 0) break;
         if (multi) {
             s = hap_permtest(T[0].w, T[0].info, T[0].cfg, T[0].counts, nullptr, ls);  // blocks

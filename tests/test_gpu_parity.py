@@ -692,11 +692,25 @@ def test_batch_argument_errors(hap, ctx):
         hap.hap_permtest_batch(ctx.h, X, cnx, Y, cny, 7, ok, infos, counts)
     with pytest.raises(hap.HapError):  # pair_sel out of range
         hap.hap_permtest_batch(ctx.h, X, cnx, Y, cny, 0, ok, infos, counts, pair_sel=[0, 5])
-    with pytest.raises(hap.HapError):  # host inputs are not accepted by the batch
-        hap.hap_permtest_batch(ctx.h, torch.from_numpy(Xp), cnx, torch.from_numpy(Yp), cny, 0, ok,
-                               infos, counts)
+    with pytest.raises(hap.HapError):  # one input in host memory, the other on the device
+        hap.hap_permtest_batch(ctx.h, torch.from_numpy(Xp), cnx, Y, cny, 0, ok, infos, counts)
     with pytest.raises(hap.HapError):  # b_end beyond 2^32
         hap.hap_permtest_batch(ctx.h, X, cnx, Y, cny, 0, hap.make_cfg(SEED, 1 << 33), infos, counts)
     hap.hap_permtest_batch(ctx.h, X, cnx, Y, cny, 0, ok, infos, counts)  # still usable
     hap.hap_sync(ctx.h)
     assert int(counts.sum()) > 0
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+def test_batch_host_inputs_bitwise(ctx, pinned):
+    """hap_permtest_batch with X_packed / Y_packed in host memory (pinned or pageable): the
+    library copies each wave's rows itself; results are bitwise those of device inputs."""
+    import torch
+    sizes = [50, 300, 7, 129, 1000, 64, 2, 333]
+    Xp, cnx, Yp, cny = HI.varlen_batch(sizes, d=96)
+    Xh, Yh = torch.from_numpy(Xp), torch.from_numpy(Yp)
+    if pinned:
+        Xh, Yh = Xh.pin_memory(), Yh.pin_memory()
+    dev = ctx.permtest_batch(_cuda(Xp), cnx, _cuda(Yp), cny, 900, SEED, stream_id=5)
+    host = ctx.permtest_batch(Xh, cnx, Yh, cny, 900, SEED, stream_id=5)
+    assert host == dev
