@@ -930,8 +930,6 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
              cudaEventCreateWithFlags(&c->ev_k1done[k][1], cudaEventDisableTiming) != cudaSuccess ||
              cudaEventCreateWithFlags(&c->ev_copied[k], cudaEventDisableTiming) != cudaSuccess))
             return fail(c, HAP_E_CUDA, "batch copy streams");
-        c->k1_recorded[k][0] = c->k1_recorded[k][1] = false;
-        c->lane_waves[k] = 0;
     }
     const int pair = cfg->pair_mode ? cfg->pair_mode : 2;
     const int64_t R = (int64_t)kTileM * pair;
@@ -969,8 +967,9 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
     // fork: the two lanes start after the work already on the caller's stream
     cudaError_t e = cudaEventRecord(c->ev_fork, st);
     for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
+        // (the copy streams need no fork: their only hazard, the K1 that last read a staging
+        // buffer, is tracked across calls, so the next call's copies start at once)
         e = cudaStreamWaitEvent(c->sub_stream[k], c->ev_fork, 0);
-        if (e == cudaSuccess && host_in) e = cudaStreamWaitEvent(c->cp_stream[k], c->ev_fork, 0);
     }
     if (e != cudaSuccess) return cuda_fail(c, e, "batch fork");
     std::vector<hap_perm_cfg> pcs((size_t)n);
