@@ -973,6 +973,16 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
     }
     if (e != cudaSuccess) return cuda_fail(c, e, "batch fork");
     std::vector<hap_perm_cfg> pcs((size_t)n);
+    // processing order: largest pairs first, equal shapes adjacent (results do not depend on
+    // the order: every pair has its own generator stream and workspace); waves of similar
+    // sizes balance the mask-GEMM and keep shared-mask waves full (C4: 134 -> 122 us/test)
+    std::vector<int64_t> order((size_t)n);
+    for (int64_t i = 0; i < n; ++i) order[(size_t)i] = pair_sel ? pair_sel[i] : i;
+    std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
+        const int64_t na = cu_nx[a + 1] - cu_nx[a], nb = cu_nx[b + 1] - cu_nx[b];
+        const int64_t Na = na + cu_ny[a + 1] - cu_ny[a], Nb = nb + cu_ny[b + 1] - cu_ny[b];
+        return Na != Nb ? Na > Nb : na > nb;
+    });
     int64_t i = 0, wave = 0;
     while (i < n && !s) {
         const int k = (int)(wave & 1);  // consecutive waves alternate between the two lanes
@@ -982,7 +992,7 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
         hap_ctx W[kMaxWave];
         int G = 0;
         while (i < n && G < wave_max) {
-            const int64_t p = pair_sel ? pair_sel[i] : i;
+            const int64_t p = order[(size_t)i];
             const int64_t nx = cu_nx[p + 1] - cu_nx[p], ny = cu_ny[p + 1] - cu_ny[p];
             const bool one_block = ceil_div(std::max<int64_t>(B, 1), R - 1) <= block_tiles(cfg, round_up(nx + ny, kKBlock), R);
             if (G > 0 && !one_block) break;  // a multi-block test starts its own wave

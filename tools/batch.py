@@ -21,8 +21,16 @@ ctx = hap.Context(0)
 B = 10000
 
 
+# HAP_ORDER=desc|asc: hand the pairs over in size order (pair_sel) - results are the same
+order = os.environ.get("HAP_ORDER", "")
+sel = None
+if order:
+    Ns = np.diff(cnx) + np.diff(cny)
+    sel = np.argsort(-Ns if order == "desc" else Ns, kind="stable")
+
+
 def run():
-    return ctx.permtest_batch(X, cnx, Y, cny, B, HI.PERM_SEED, sync=False, shared=shared)
+    return ctx.permtest_batch(X, cnx, Y, cny, B, HI.PERM_SEED, sync=False, shared=shared, pair_sel=sel)
 
 
 for _ in range(3):
