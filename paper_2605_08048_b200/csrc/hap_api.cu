@@ -1138,6 +1138,7 @@ hap_status hap_debug_k3_stamps(hap_ctx c, long long* out, int64_t n) {
 }
 
 hap_status hap_debug_k1_stamps(hap_ctx c, long long* out, int64_t n) {
+    if (c && !c->buf[kStamps] && c->sub[0][0]) c = c->sub[0][0];  // a batch: lane 0's owner
     if (!c || !out || !c->buf[kStamps]) return HAP_E_INVALID_ARG;
     cudaDeviceSynchronize();
     const size_t bytes = std::min<size_t>((size_t)n * 8, (size_t)(8 + 8 * c->sm_count) * 8);
