@@ -189,6 +189,45 @@ __device__ __forceinline__ int pair_of(const AlignArgs& a, int64_t item) {
     return g;
 }
 
+// Items of CTA `cta` (of G): the CTAs are split among the pairs in proportion to their items
+// (at least one each) and a pair's items evenly among its CTAs, so a CTA works on ONE pair
+// (its scalars are formed once) and on contiguous items.  Every partial sum is flushed per
+// item, so the bits do not depend on this assignment (a pair alone or in any wave).
+__device__ __forceinline__ void cta_items(const AlignArgs& a, int cta, int G, int64_t& i0, int64_t& i1) {
+    const int64_t items = a.item_off[a.G];
+    int c0 = 0;
+    i0 = i1 = 0;
+    for (int g = 0; g < a.G; ++g) {
+        const int64_t ng = a.item_off[g + 1] - a.item_off[g];
+        int cg = g == a.G - 1 ? G - c0 : (int)((ng * (int64_t)G) / (items > 0 ? items : 1));
+        cg = cg < 1 ? 1 : cg;
+        const int rest = G - c0 - (a.G - 1 - g);  // leave one CTA for each later pair
+        cg = cg > rest ? rest : cg;
+        if (cta < c0 + cg) {
+            const int64_t j = cta - c0;
+            i0 = a.item_off[g] + (j * ng) / cg;
+            i1 = a.item_off[g] + ((j + 1) * ng) / cg;
+            return;
+        }
+        c0 += cg;
+    }
+}
+
+// W consecutive u32 words (W = R/2 <= 8) to a 4W-byte aligned address
+template <int W>
+__device__ __forceinline__ void store_words(uint32_t* dst, const uint32_t (&w)[W]) {
+    if constexpr (W == 8) {
+        reinterpret_cast<uint4*>(dst)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+        reinterpret_cast<uint4*>(dst)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+    } else if constexpr (W == 4) {
+        reinterpret_cast<uint4*>(dst)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+    } else if constexpr (W == 2) {
+        reinterpret_cast<uint2*>(dst)[0] = make_uint2(w[0], w[1]);
+    } else {
+        dst[0] = w[0];
+    }
+}
+
 // dynamic smem: tile f32 [R][P] | (u_c, m_c) f32 [d_pad] (stage_umc) | xs, ys f64 [d]
 // (stage_means) | t' partials f64 [d_pad] (stage_umc); R <= 16.
 // <= 64 registers/thread (launch bound 2): a K1 CTA then fits beside a mask-GEMM CTA on
@@ -198,8 +237,6 @@ __device__ __forceinline__ int pair_of(const AlignArgs& a, int64_t item) {
 template <int R>
 __global__ void __launch_bounds__(kThreads, 2) k1_align_fused(AlignArgs a, int P, int stage_umc,
                                                               int stage_means) {
-    constexpr int rp = R / 2;  // row pairs per column: rp consecutive lanes share a column
-    constexpr int lrp = rp >= 8 ? 3 : rp >= 4 ? 2 : rp >= 2 ? 1 : 0;
     extern __shared__ __align__(16) uint8_t k1_smem[];
     __shared__ double red[2 * kWarps + 2];
     __shared__ double s_inv[kMaxItemRows];
@@ -237,15 +274,15 @@ __global__ void __launch_bounds__(kThreads, 2) k1_align_fused(AlignArgs a, int P
             }
             sx0 = sy0 = sx1 = sy1 = 0.0;
         };
-        for (int64_t item = cta; item < items; item += G) {
+        int64_t i0, i1;
+        cta_items(a, cta, G, i0, i1);
+        for (int64_t item = i0; item < i1; ++item) {
             const int g = pair_of(a, item);
             const AlignPair& q = a.p[g];
             const int64_t N = q.n_x + q.n_y;
             const int64_t r0 = (item - a.item_off[g]) * R;
-            if (g != cur) {
-                flush();
-                cur = g;
-            }
+            flush();  // per item (see cta_items)
+            cur = g;
             if (resident >= 0) __syncthreads();  // previous tile fully consumed
             load_tile(q, tile, r0, R, P);
             __syncthreads();
@@ -421,24 +458,24 @@ __global__ void __launch_bounds__(kThreads, 2) k1_align_fused(AlignArgs a, int P
         __syncthreads();
         for (int c = tid; c < (int)a.d_pad; c += kThreads) fix_add(a.p[sp].acc + 2 * d + c, s_t[c]);
     };
-    const int units = rp * (int)a.d_pad;
     if (resident >= 0) {
-        const int64_t nmine = (resident - cta) / G + 1;
-        for (int64_t k = nmine - 1; k >= 0; --k) {
-            const int64_t item = cta + k * G;
+        int64_t i0, i1;
+        cta_items(a, cta, G, i0, i1);
+        for (int64_t item = i1 - 1; item >= i0; --item) {
             const int g = pair_of(a, item);
             const AlignPair& q = a.p[g];
             const int64_t N = q.n_x + q.n_y;
             const int64_t li = item - a.item_off[g];
             const int64_t r0 = li * R;
+            flush_t();  // per item (see cta_items)
             if (g != sp) {
-                flush_t();
                 // the CTA that holds the pair's item 0 writes its info and exports
-                const int64_t item0 = a.item_off[g];
-                pair_scalars(g, item0 >= cta && (item0 - cta) % G == 0 && item0 <= resident);
-                if (stage_umc)
-                    for (int c = tid; c < (int)a.d_pad; c += kThreads) s_t[c] = 0.0;
+                pair_scalars(g, i0 == a.item_off[g]);
                 sp = g;
+            }
+            if (stage_umc) {
+                __syncthreads();
+                for (int c = tid; c < (int)a.d_pad; c += kThreads) s_t[c] = 0.0;
             }
             if (item != resident) {
                 __syncthreads();
@@ -468,46 +505,41 @@ __global__ void __launch_bounds__(kThreads, 2) k1_align_fused(AlignArgs a, int P
                 }
             }
             __syncthreads();
-            if (k == nmine - 1) cstamp(a, 5);
+            if (item == i1 - 1) cstamp(a, 5);
             // z' = x - coef u - m in fp32 (the value is then kept to 16 bits), hi/lo split;
-            // thread = (column, row pair): rp lanes write one column's 2R contiguous bytes
-            {
-                const int j = tid & (rp - 1);  // fixed per thread (kThreads % rp == 0)
-                const float cf0 = s_cff[2 * j], cf1 = s_cff[2 * j + 1];
-                const float iv0 = s_invf[2 * j], iv1 = s_invf[2 * j + 1];
-                const bool v0 = r0 + 2 * j < N, v1 = r0 + 2 * j + 1 < N;
-                uint32_t* zh = reinterpret_cast<uint32_t*>(q.zt_hi + r0) + j;
-                uint32_t* zl = reinterpret_cast<uint32_t*>(q.zt_lo + r0) + j;
-                const float* t0 = tile + (size_t)(2 * j) * P;
-                const float* t1 = t0 + P;
-                for (int uidx = tid; uidx < units; uidx += kThreads) {
-                    const int c = uidx >> lrp;
-                    float2 um;  // (0, 0) for pad columns
-                    if (stage_umc) {
-                        um = umc[c];
-                    } else {
-                        double ud, md;
-                        axis_centre(q, c, ud, md);
-                        um = make_float2((float)ud, (float)md);
-                    }
-                    const float z0 = v0 && c < d ? fmaf(-cf0, um.x, t0[c] * iv0) - um.y : 0.f;
-                    const float z1 = v1 && c < d ? fmaf(-cf1, um.x, t1[c] * iv1) - um.y : 0.f;
+            // thread = column: the item's R rows of the column -> 2R contiguous bytes per plane
+            // (16-byte stores), and the column's t' partial summed in fp64 without any
+            // cross-lane reduction (hi + lo is exact in fp32 with <= 16 significant bits, so the
+            // fp64 sum of the R values is exact: t = N m + t' is the exact sum of the planes)
+            for (int c = tid; c < (int)a.d_pad; c += kThreads) {
+                float2 um;  // (0, 0) for pad columns
+                if (stage_umc) {
+                    um = umc[c];
+                } else {
+                    double ud, md;
+                    axis_centre(q, c, ud, md);
+                    um = make_float2((float)ud, (float)md);
+                }
+                uint32_t hw[R / 2], lw[R / 2];
+                double tv = 0.0;
+#pragma unroll
+                for (int r = 0; r < R; r += 2) {
+                    const bool v0 = r0 + r < N && c < d, v1 = r0 + r + 1 < N && c < d;
+                    const float z0 = v0 ? fmaf(-s_cff[r], um.x, tile[(size_t)r * P + c] * s_invf[r]) - um.y : 0.f;
+                    const float z1 =
+                        v1 ? fmaf(-s_cff[r + 1], um.x, tile[(size_t)(r + 1) * P + c] * s_invf[r + 1]) - um.y : 0.f;
                     const __nv_bfloat16 h0 = __float2bfloat16_rn(z0), h1 = __float2bfloat16_rn(z1);
                     const float fh0 = __bfloat162float(h0), fh1 = __bfloat162float(h1);
                     const __nv_bfloat16 l0 = __float2bfloat16_rn(z0 - fh0), l1 = __float2bfloat16_rn(z1 - fh1);
-                    const size_t off = (size_t)c * (size_t)(q.n_pad >> 1);
-                    zh[off] = (uint32_t)__bfloat16_as_ushort(h0) | ((uint32_t)__bfloat16_as_ushort(h1) << 16);
-                    zl[off] = (uint32_t)__bfloat16_as_ushort(l0) | ((uint32_t)__bfloat16_as_ushort(l1) << 16);
-                    // hi + lo is exact in fp32; the column's t' partial is summed in fp64, so
-                    // t = N m + t' is the exact sum of the planes (up to the fixed point)
-                    double tv = (double)(fh0 + __bfloat162float(l0)) + (double)(fh1 + __bfloat162float(l1));
-#pragma unroll
-                    for (int o = 1; o < rp; o <<= 1) tv += __shfl_xor_sync(0xffffffffu, tv, o);
-                    if (j == 0) {  // the column's owner thread (the same for every item)
-                        if (stage_umc) s_t[c] += tv;
-                        else fix_add(q.acc + 2 * d + c, tv);
-                    }
+                    hw[r / 2] = (uint32_t)__bfloat16_as_ushort(h0) | ((uint32_t)__bfloat16_as_ushort(h1) << 16);
+                    lw[r / 2] = (uint32_t)__bfloat16_as_ushort(l0) | ((uint32_t)__bfloat16_as_ushort(l1) << 16);
+                    tv += (double)(fh0 + __bfloat162float(l0)) + (double)(fh1 + __bfloat162float(l1));
                 }
+                const size_t off = ((size_t)c * (size_t)q.n_pad + (size_t)r0) >> 1;  // u32 words
+                store_words<R / 2>(reinterpret_cast<uint32_t*>(q.zt_hi) + off, hw);
+                store_words<R / 2>(reinterpret_cast<uint32_t*>(q.zt_lo) + off, lw);
+                if (stage_umc) s_t[c] += tv;  // the column's owner thread
+                else fix_add(q.acc + 2 * d + c, tv);
             }
         }
         flush_t();
