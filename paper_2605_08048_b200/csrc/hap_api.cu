@@ -180,8 +180,16 @@ GemmArgs gemm_args(hap_ctx c) {
     g.d_pad = (int)c->d_pad;
     g.d = (int)c->d;
     g.tie_rel = 1e-6;
-    const char* ex = getenv("HAP_K3_EXPERIMENT");
+    // HAP_K3_EXPERIMENT: development switches; bits 1, 2, 4, 8 skip work (timing only, the
+    // counts are then invalid), bit 16 records per-unit timestamps
+    static const char* ex = getenv("HAP_K3_EXPERIMENT");
     g.exp = ex ? atoi(ex) : 0;
+    static bool warned = false;
+    if ((g.exp & 15) && !warned) {
+        fprintf(stderr, "libhap: HAP_K3_EXPERIMENT=%d skips mask-GEMM work: timing only, results are invalid\n",
+                g.exp);
+        warned = true;
+    }
     g.stamps = nullptr;
     if ((g.exp & 16) && ensure(c, kK3Stamps, (size_t)c->sm_count * 64 * 8) == HAP_OK)
         g.stamps = B<long long>(c, kK3Stamps);
