@@ -714,3 +714,15 @@ def test_batch_host_inputs_bitwise(ctx, pinned):
     dev = ctx.permtest_batch(_cuda(Xp), cnx, _cuda(Yp), cny, 900, SEED, stream_id=5)
     host = ctx.permtest_batch(Xh, cnx, Yh, cny, 900, SEED, stream_id=5)
     assert host == dev
+
+
+def test_batch_order_independent(ctx):
+    """The batch processes pairs largest-first in waves; the results of every pair are the
+    same bits whatever order pair_sel lists them in (own generator stream and workspace)."""
+    sizes = [50, 300, 7, 129, 1000, 64, 2, 333, 129, 50]
+    Xp, cnx, Yp, cny = HI.varlen_batch(sizes, d=96)
+    X, Y = _cuda(Xp), _cuda(Yp)
+    a = ctx.permtest_batch(X, cnx, Y, cny, 800, SEED, stream_id=3)
+    perm = list(np.random.default_rng(1).permutation(len(sizes)))
+    b = ctx.permtest_batch(X, cnx, Y, cny, 800, SEED, stream_id=3, pair_sel=perm)
+    assert a == b
