@@ -163,8 +163,10 @@ HAP_API hap_status hap_permtest(hap_ctx ctx, hap_align_info* info, const hap_per
  * generator stream cfg->stream_id + p (cfg->stream_id for all with HAP_FLAG_SHARED_MASK).  Shape errors of any selected pair
  * are returned before anything is enqueued.
  *   X_packed, Y_packed [device, or both host]: host inputs (pinned for overlap) are copied
- *            per pair into the wave's workspaces on the lane streams, so the copies of one
- *            wave overlap the other lane's kernels (the end-to-end path of bench.py);
+ *            per pair into the wave's workspaces on internal copy streams, so the copies of
+ *            one wave overlap the other lane's kernels (the end-to-end path of bench.py); the
+ *            host buffers must stay valid and unchanged until the work enqueued on `stream`
+ *            has completed (the copies are asynchronous);
  *   cu_nx, cu_ny [host] int64[P+1] prefix offsets.
  *   pair_sel [host] optional list of the pairs this call handles (NULL = all P); the
  *            others' infos/counts are left untouched (used for multi-GPU sharding).
