@@ -15,7 +15,9 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libhap.so")
+# HAP_LIB_VARIANT (experiments only): load variants/libhap_<name>.so built with other flags
+LIB_PATH = (os.path.join(os.path.dirname(_PKG), "variants", f"libhap_{os.environ['HAP_LIB_VARIANT']}.so")
+            if os.environ.get("HAP_LIB_VARIANT") else os.path.join(_PKG, "libhap.so"))
 
 HAP_OK = 0
 STATUS_NAMES = {0: "OK", 1: "INVALID_ARG", 2: "DIM_MISMATCH", 3: "ZERO_VECTOR",
