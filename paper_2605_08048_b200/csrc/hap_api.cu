@@ -344,7 +344,10 @@ hap_status get_schedule(hap_ctx c, const GemmArgs& w, int np, cudaStream_t st, G
     return get_schedule(c, w, np, st, g);
 }
 
-constexpr int64_t kMaskBudget = 64ll << 20;  // bytes of bf16 mask per launch (L2-resident)
+// bytes of bf16 mask per launch: large enough that a C4-sized test (N = 10^4, B = 10^4)
+// is one block and joins a wave (C4 sample 121.9 -> 117.5 us/test vs 64 MB); K3 streams
+// the masks with TMA and is not DRAM-bound, so they need not stay in L2
+constexpr int64_t kMaskBudget = 256ll << 20;
 
 cudaEvent_t take_event(hap_ctx c) {
     if (!c->pool.empty()) {
@@ -851,7 +854,9 @@ hap_status check_cfg(hap_ctx c, const hap_perm_cfg* cfg) {
 // tiles of one launch for a test of n_pad pooled rows: the block's bf16 mask stays within
 // the L2-resident budget, or cfg->block permutations when set
 int64_t block_tiles(const hap_perm_cfg* cfg, int64_t n_pad, int64_t R) {
-    int64_t t = std::max<int64_t>(1, kMaskBudget / (R * n_pad * 2));
+    static const char* mb = getenv("HAP_MASK_BUDGET_MB");  // EXPERIMENT: block size
+    const int64_t budget = mb ? (int64_t)atoi(mb) << 20 : kMaskBudget;
+    int64_t t = std::max<int64_t>(1, budget / (R * n_pad * 2));
     if (cfg->block) t = std::max<int64_t>(1, ceil_div((int64_t)cfg->block, R - 1));
     return t;
 }
