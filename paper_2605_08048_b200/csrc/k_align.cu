@@ -38,7 +38,10 @@
 namespace hap {
 namespace {
 
-constexpr int kThreads = 512;
+#ifndef HAP_K1_THREADS
+#define HAP_K1_THREADS 512
+#endif
+constexpr int kThreads = HAP_K1_THREADS;  // 64 registers per thread: 2 (or 4) CTAs fit per SM
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxItemRows = 16;
 constexpr int kSpartStride = 8;  // doubles per CTA in spart: P5 [4,5]
@@ -235,7 +238,7 @@ __device__ __forceinline__ void store_words(uint32_t* dst, const uint32_t (&w)[W
 // Items of all pairs of the launch (a wave) form one list; a CTA's column sums are flushed
 // to a pair's accumulators whenever its next item belongs to another pair.
 template <int R>
-__global__ void __launch_bounds__(kThreads, 2) k1_align_fused(AlignArgs a, int P, int stage_umc,
+__global__ void __launch_bounds__(kThreads, 65536 / (kThreads * 64)) k1_align_fused(AlignArgs a, int P, int stage_umc,
                                                               int stage_means) {
     extern __shared__ __align__(16) uint8_t k1_smem[];
     __shared__ double red[2 * kWarps + 2];
@@ -286,10 +289,10 @@ __global__ void __launch_bounds__(kThreads, 2) k1_align_fused(AlignArgs a, int P
             if (resident >= 0) __syncthreads();  // previous tile fully consumed
             load_tile(q, tile, r0, R, P);
             __syncthreads();
-            if (warp < R) {
-                const int64_t i = r0 + warp;
+            for (int rw = warp; rw < R; rw += kWarps) {
+                const int64_t i = r0 + rw;
                 double s4[4] = {0.0, 0.0, 0.0, 0.0};  // independent chains (latency)
-                const float* tr = tile + (size_t)warp * P;
+                const float* tr = tile + (size_t)rw * P;
                 int c = lane;
                 for (; c + 96 < d; c += 128) {
 #pragma unroll
@@ -307,7 +310,7 @@ __global__ void __launch_bounds__(kThreads, 2) k1_align_fused(AlignArgs a, int P
                 if (lane == 0) {
                     const double nrm = sqrt(s);
                     const double iv = (i < N && nrm >= 1e-12) ? 1.0 / nrm : 0.0;
-                    s_inv[warp] = iv;
+                    s_inv[rw] = iv;
                     if (i < N) {
                         q.inv[i] = iv;
                         if (nrm < 1e-12) atomicMin(q.bad, (long long)i);
@@ -485,23 +488,23 @@ __global__ void __launch_bounds__(kThreads, 2) k1_align_fused(AlignArgs a, int P
             }
             // reflection coefficients 2 u^T x_i = 2 (xbar.h_i/||xbar|| - ybar.h_i/||ybar||)
             // / (||v|| ||h_i||) of the X rows (Y is not reflected)
-            if (warp < R) {
-                const int64_t i = r0 + warp;
+            for (int rw = warp; rw < R; rw += kWarps) {
+                const int64_t i = r0 + rw;
                 double cf = 0.0;
                 if (i < q.n_x && !sc.identity) {
                     double dx = 0.0, dy = 0.0;
                     for (int c = lane; c < d; c += 32) {
-                        const double hv = (double)tile[(size_t)warp * P + c];
+                        const double hv = (double)tile[(size_t)rw * P + c];
                         dx += hv * (stage_means ? xs[c] : fix_get(q.acc + c) * sc.rnX);
                         dy += hv * (stage_means ? ys[c] : fix_get(q.acc + d + c) * sc.rnY);
                     }
                     dx = warp_sum(dx);
                     dy = warp_sum(dy);
-                    cf = 2.0 * ((dx * sc.rnx - dy * sc.rny) * s_inv[warp]) * sc.rnv;
+                    cf = 2.0 * ((dx * sc.rnx - dy * sc.rny) * s_inv[rw]) * sc.rnv;
                 }
                 if (lane == 0) {
-                    s_cff[warp] = (float)cf;
-                    s_invf[warp] = (float)s_inv[warp];
+                    s_cff[rw] = (float)cf;
+                    s_invf[rw] = (float)s_inv[rw];
                 }
             }
             __syncthreads();
