@@ -1142,6 +1142,7 @@ hap_status hap_profile(hap_ctx c, int enable) {
 }
 
 hap_status hap_debug_k3_stamps(hap_ctx c, long long* out, int64_t n) {
+    if (c && !c->buf[kK3Stamps] && c->sub[0][0]) c = c->sub[0][0];  // a batch: lane 0's owner
     if (!c || !out || !c->buf[kK3Stamps]) return HAP_E_INVALID_ARG;
     cudaDeviceSynchronize();
     const size_t bytes = std::min<size_t>((size_t)n * 8, (size_t)c->sm_count * 64 * 8);
