@@ -190,6 +190,27 @@ HAP_DEV void mbar_arrive_cluster(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
                  : "memory");
 }
+// remote arrive with the default (release, CTA-scope) semantics, as CUTLASS's cluster
+// barriers use for peer-CTA signalling
+HAP_DEV void mbar_arrive_remote(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// arrive on a (possibly remote) mbarrier and expect `bytes` of transaction data, relaxed
+HAP_DEV void mbar_arrive_expect_tx_cluster_relaxed(uint32_t cluster_bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.relaxed.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(cluster_bar),
+                 "r"(bytes)
+                 : "memory");
+}
+// asynchronous store into a (possibly remote) CTA's shared memory; completes `bytes` on the
+// mbarrier at `cluster_bar` (same CTA as the destination) when the data has landed
+HAP_DEV void st_async_u32(uint32_t cluster_addr, uint32_t v, uint32_t cluster_bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.u32 [%0], %1, [%2];" ::"r"(cluster_addr),
+                 "r"(v), "r"(cluster_bar)
+                 : "memory");
+}
+HAP_DEV void st_shared_cluster_u32(uint32_t cluster_addr, uint32_t v) {
+    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(cluster_addr), "r"(v) : "memory");
+}
 // 2-SM TMA: data lands in this CTA's smem, completion bytes are counted on the mbarrier at
 // the shared::cluster address `bar_cluster` (the leader CTA's barrier).
 HAP_DEV void tma_load_2d_pair(const void* desc, uint32_t bar_cluster, void* smem_dst, int32_t c0,

@@ -41,6 +41,8 @@ constexpr int kThreads = 192;
 constexpr uint32_t kTmemCols = 512;
 constexpr int kStageA = kTileM * 128;  // 16 KB: 128 rows x 64 bf16
 constexpr int kFinCap = 400;             // deferred finalizes per CTA (smem tail list)
+constexpr int kQ = 6;                    // piece queue: the leader's producer publishes the
+                                         // pair's pieces to every role of both CTAs
 
 #ifndef HAP_K3_STAGES
 #define HAP_K3_STAGES 3
@@ -200,7 +202,10 @@ __global__ void __maxnreg__(168)
     uint64_t* empty = full + C::kStages;
     uint64_t* tfull = empty + C::kStages;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* qfull = tempty + 2;   // [kQ] piece index published (both CTAs)
+    uint64_t* qempty = qfull + kQ;  // [kQ] every consumer has read it (leader)
+    int* s_q = reinterpret_cast<int*>(qempty + kQ);  // [kQ] piece indices (-1: no more)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_q + kQ);
     int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
     unsigned* s_cnt = tmem_slot + 4;  // [3] per-tile counts of the finalize
     double* s_tc = reinterpret_cast<double*>(tmem_slot + 8);  // [kMaxWave][3] S1c, S2c, tau
@@ -214,8 +219,24 @@ __global__ void __maxnreg__(168)
     const bool leader = rank == 0;
     const int pair_id = blockIdx.x / kPair;
     const int R = g.rows_per_tile;
-    // this pair's pieces: a contiguous, equal-width range of the (tile, column) space
-    const int pc_begin = g.piece_off[pair_id], pc_end = g.piece_off[pair_id + 1];
+    // static schedule: this pair's pieces are a contiguous, equal-cost range of the (tile,
+    // column) space; dynamic: pairs claim the next piece from a global counter, so pairs
+    // that start late (their SM still busy with another lane's kernels) take fewer
+    const int pc_begin = g.dyn ? 0 : g.piece_off[pair_id], pc_end = g.dyn ? 0 : g.piece_off[pair_id + 1];
+    constexpr uint32_t kQConsumers = 1 + 4 * kPair + (kPair - 1);  // MMA, epilogue warps, peer TMA
+    // consumer side of the piece queue: the piece of position `cur` (-1 = no more)
+    auto q_take = [&](int cur) -> int {
+        mbar_wait(&qfull[cur % kQ], (uint32_t)(cur / kQ) & 1u);
+        return *reinterpret_cast<volatile int*>(&s_q[cur % kQ]);
+    };
+    auto q_release = [&](int cur) {  // one thread per consumer unit, after it read the slot
+        if constexpr (kPair == 2) {
+            if (leader) mbar_arrive(&qempty[cur % kQ]);
+            else mbar_arrive_remote(mapa_shared(smem_u32(&qempty[cur % kQ]), 0));
+        } else {
+            mbar_arrive(&qempty[cur % kQ]);
+        }
+    };
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < C::kStages; ++s) {
@@ -225,6 +246,10 @@ __global__ void __maxnreg__(168)
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
             mbar_init(&tempty[a], 4 * kPair);  // one arrival per epilogue warp of the pair
+        }
+        for (int s = 0; s < kQ; ++s) {
+            mbar_init(&qfull[s], 1);
+            mbar_init(&qempty[s], kQConsumers);
         }
         fence_barrier_init();
         for (int ti = 0; ti < g.G; ++ti) {
@@ -256,41 +281,79 @@ __global__ void __maxnreg__(168)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int pc = pc_begin; pc < pc_end; ++pc) {
+            // the leader claims a piece and publishes it (queue entry e) to both CTAs; entry
+            // cur + 1 is published while piece cur is still being loaded, so the claim's
+            // atomic and the cross-CTA publish stay off the stage ring's critical path
+            auto claim_publish = [&](int e) -> int {
+                int pc;
+                if (g.dyn) {
+                    pc = atomicAdd(g.claim, 1);
+                    pc = pc < g.npieces ? pc : -1;
+                } else {
+                    pc = pc_begin + e < pc_end ? pc_begin + e : -1;
+                }
+                const int slot = e % kQ;
+                mbar_wait(&qempty[slot], ((uint32_t)(e / kQ) & 1u) ^ 1u);
+                s_q[slot] = pc;
+                if constexpr (kPair == 2) {  // the peer's slot: an async store that completes its barrier
+                    const uint32_t rb = mapa_shared(smem_u32(&qfull[slot]), 1);
+                    mbar_arrive_expect_tx_cluster_relaxed(rb, 4u);
+                    st_async_u32(mapa_shared(smem_u32(&s_q[slot]), 1), (uint32_t)pc, rb);
+                }
+                mbar_arrive(&qfull[slot]);
+                return pc;
+            };
+            int pc_cur = leader ? claim_publish(0) : 0, pc_nxt = -2;  // -2: not yet published
+            for (int cur = 0;; ++cur) {
+                int pc;
+                if (leader) {
+                    pc = pc_cur;
+                } else {
+                    pc = q_take(cur);
+                    q_release(cur);
+                }
+                if (pc < 0) break;
                 const int4 pd = g.pieces[pc];  // {wave tile, col0, width, slot}
                 const int tile = pd.x, width = pd.z;
                 const int ti = test_of(g, tile);
-                if (test_failed(g.t[ti])) continue;
-                const int nkb = g.t[ti].n_pad / kKBlock;
-                const CUtensorMap* tmA = &maps.a[ti];
-                const CUtensorMap* tmBhi = &maps.bhi[ti];
-                const CUtensorMap* tmBlo = &maps.blo[ti];
-                const int arow = (tile - g.t[ti].tile0) * R + (int)rank * kTileM;
-                const int brow = pd.y + (int)rank * (width / kPair);
-                const int ui = pc - pc_begin;
-                for (int kb = 0; kb < nkb; ++kb) {
-                    mbar_wait(&empty[stage], phase ^ 1u);
-                    if (kb == 0) K3_STAMP(ui, 0);
-                    if (kb == nkb - 1) K3_STAMP(ui, 1);
-                    uint8_t* sA = smem + stage * C::kStageBytes;
-                    if constexpr (kPair == 2) {
-                        // EXPERIMENT (timing only): bit0 skips A loads, bit1 skips B lo loads
-                        const uint32_t bytes = (uint32_t)C::kStageBytes - ((g.exp & 1) ? kStageA : 0) -
-                                               ((g.exp & 2) ? C::kStageB : 0);
-                        if (leader) mbar_arrive_expect_tx(&full[stage], 2u * bytes);
-                        const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
-                        if (!(g.exp & 1)) tma_load_2d_pair(tmA, fb, sA, kb * kKBlock, arow);
-                        tma_load_2d_pair(tmBhi, fb, sA + kStageA, kb * kKBlock, brow);
-                        if (!(g.exp & 2))
-                            tma_load_2d_pair(tmBlo, fb, sA + kStageA + C::kStageB, kb * kKBlock, brow);
-                    } else {
-                        mbar_arrive_expect_tx(&full[stage], (uint32_t)C::kStageBytes);
-                        tma_load_2d(tmA, &full[stage], sA, kb * kKBlock, arow);
-                        tma_load_2d(tmBhi, &full[stage], sA + kStageA, kb * kKBlock, brow);
-                        tma_load_2d(tmBlo, &full[stage], sA + kStageA + C::kStageB, kb * kKBlock,
-                                    brow);
+                if (!test_failed(g.t[ti])) {
+                    const int nkb = g.t[ti].n_pad / kKBlock;
+                    const CUtensorMap* tmA = &maps.a[ti];
+                    const CUtensorMap* tmBhi = &maps.bhi[ti];
+                    const CUtensorMap* tmBlo = &maps.blo[ti];
+                    const int arow = (tile - g.t[ti].tile0) * R + (int)rank * kTileM;
+                    const int brow = pd.y + (int)rank * (width / kPair);
+                    const int ui = cur;
+                    for (int kb = 0; kb < nkb; ++kb) {
+                        mbar_wait(&empty[stage], phase ^ 1u);
+                        if (kb == 0) K3_STAMP(ui, 0);
+                        if (kb == nkb - 1) K3_STAMP(ui, 1);
+                        uint8_t* sA = smem + stage * C::kStageBytes;
+                        if constexpr (kPair == 2) {
+                            // EXPERIMENT (timing only): bit0 skips A loads, bit1 skips B lo loads
+                            const uint32_t bytes = (uint32_t)C::kStageBytes - ((g.exp & 1) ? kStageA : 0) -
+                                                   ((g.exp & 2) ? C::kStageB : 0);
+                            if (leader) mbar_arrive_expect_tx(&full[stage], 2u * bytes);
+                            const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
+                            if (!(g.exp & 1)) tma_load_2d_pair(tmA, fb, sA, kb * kKBlock, arow);
+                            tma_load_2d_pair(tmBhi, fb, sA + kStageA, kb * kKBlock, brow);
+                            if (!(g.exp & 2))
+                                tma_load_2d_pair(tmBlo, fb, sA + kStageA + C::kStageB, kb * kKBlock, brow);
+                        } else {
+                            mbar_arrive_expect_tx(&full[stage], (uint32_t)C::kStageBytes);
+                            tma_load_2d(tmA, &full[stage], sA, kb * kKBlock, arow);
+                            tma_load_2d(tmBhi, &full[stage], sA + kStageA, kb * kKBlock, brow);
+                            tma_load_2d(tmBlo, &full[stage], sA + kStageA + C::kStageB, kb * kKBlock,
+                                        brow);
+                        }
+                        if (++stage == C::kStages) { stage = 0; phase ^= 1u; }
+                        if (leader && kb == (nkb >> 1) && pc_nxt == -2) pc_nxt = claim_publish(cur + 1);
                     }
-                    if (++stage == C::kStages) { stage = 0; phase ^= 1u; }
+                }
+                if (leader) {
+                    if (pc_nxt == -2) pc_nxt = claim_publish(cur + 1);
+                    pc_cur = pc_nxt;
+                    pc_nxt = -2;
                 }
             }
         }
@@ -300,7 +363,10 @@ __global__ void __maxnreg__(168)
             int stage = 0;
             uint32_t phase = 0;
             int i = 0;
-            for (int pc = pc_begin; pc < pc_end; ++pc) {
+            for (int cur = 0;; ++cur) {
+                const int pc = q_take(cur);
+                q_release(cur);
+                if (pc < 0) break;
                 const int width = g.pieces[pc].z;
                 const int ti = test_of(g, g.pieces[pc].x);
                 if (test_failed(g.t[ti])) continue;
@@ -350,7 +416,11 @@ __global__ void __maxnreg__(168)
             tempty_c[1] = mapa_shared(smem_u32(&tempty[1]), 0);
         }
         int i = 0;
-        for (int pc = pc_begin; pc < pc_end; ++pc) {
+        for (int cur = 0;; ++cur) {
+            const int pc = q_take(cur);
+            __syncwarp();
+            if (lane == 0) q_release(cur);
+            if (pc < 0) break;
             const int4 pd = g.pieces[pc];
             const int tile = pd.x, width = pd.z;
             const int ti = test_of(g, tile);
@@ -431,6 +501,13 @@ __global__ void __maxnreg__(168)
     tc_fence_before();
     __syncthreads();
     if constexpr (kPair == 2) cluster_sync();
+    if (g.dyn && threadIdx.x == 0) {  // the last CTA out resets the claim counters
+        __threadfence();
+        if (atomicAdd(g.claim + 1, 1) == (int)gridDim.x - 1) {
+            g.claim[0] = 0;
+            g.claim[1] = 0;
+        }
+    }
     if (threadIdx.x == 0) K3_STAMP(7, 1);  // all roles done
     if (threadIdx.x == 0) span_exit(g.span);
     if (warp == 1) {

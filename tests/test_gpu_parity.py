@@ -567,10 +567,12 @@ print(json.dumps([[r["exceed_ge"], r["exceed_abs"], r["flagged"], r["gemm_t_obs"
 
 
 @pytest.mark.parametrize("env", [{"HAP_K1_DRAWS": "1"}, {"HAP_BATCH_SPLIT": "1"},
-                                 {"HAP_WAVE": "1"}, {"HAP_K3_ROUND_ROBIN": "1"}])
+                                 {"HAP_WAVE": "1"}, {"HAP_K3_DYNAMIC": "0"},
+                                 {"HAP_K3_DYNAMIC": "0", "HAP_K3_ROUND_ROBIN": "1"}])
 def test_experimental_paths_bitwise_equal(env):
-    """The experimental scheduling paths (draws staged by K1, split generator on the side
-    stream, one test per wave, round-robin K3 schedule) give bitwise the default results."""
+    """The alternative scheduling paths (draws staged by K1, split generator on the side
+    stream, one test per wave, the static K3 split, round-robin K3 schedule) give bitwise
+    the default results."""
     import json
     import os
     import subprocess
@@ -579,7 +581,7 @@ def test_experimental_paths_bitwise_equal(env):
 
     def run(extra):
         e = dict(os.environ)
-        for k in ("HAP_K1_DRAWS", "HAP_BATCH_SPLIT", "HAP_WAVE", "HAP_K3_ROUND_ROBIN"):
+        for k in ("HAP_K1_DRAWS", "HAP_BATCH_SPLIT", "HAP_WAVE", "HAP_K3_ROUND_ROBIN", "HAP_K3_DYNAMIC"):
             e.pop(k, None)
         e.update(extra)
         out = subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT, root], env=e,
