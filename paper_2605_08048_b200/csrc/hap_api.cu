@@ -282,8 +282,12 @@ hap_status get_schedule(hap_ctx c, const GemmArgs& w, int np, cudaStream_t st, G
     auto cost = [](int64_t wd, int64_t nkb) { return (double)nkb * std::max(4.0 * (double)wd, kPieceFloor); };
     if (w.dyn) {  // dynamic: every chunk is a piece, claimed in (test, tile, column) order
         std::vector<int> npc(nt_all, 0), pcs;
+        static const char* pw = getenv("HAP_K3_PIECE_COLS");  // EXPERIMENT: piece width
+        const int64_t pwidth = pw ? std::max<int64_t>(32, atoi(pw)) : kChunkN;
         for (const Chunk& ch : chunks)
-            pcs.insert(pcs.end(), {(int)ch.tile, (int)ch.c0, (int)ch.width, npc[ch.tile]++});
+            for (int64_t o = 0; o < ch.width; o += pwidth)
+                pcs.insert(pcs.end(), {(int)ch.tile, (int)(ch.c0 + o), (int)std::min<int64_t>(pwidth, ch.width - o),
+                                       npc[ch.tile]++});
         std::vector<int> blob(round_up(np + 1 + nt_all, 4), 0);
         std::copy(npc.begin(), npc.end(), blob.begin() + (np + 1));
         blob.insert(blob.end(), pcs.begin(), pcs.end());
@@ -783,7 +787,14 @@ hap_status plan_wave(hap_ctx owner, int G, const WaveTest* T, int pair, bool sha
     perm_items(pa);
     g.ntiles = (int)tiles;
     g.npairs = P.npairs;
-    g.npieces = (int)(tiles * ceil_div(owner->d_pad, kChunkN));  // dynamic mode: every chunk
+    {  // dynamic mode: every piece (a chunk, or HAP_K3_PIECE_COLS columns of it)
+        static const char* pw = getenv("HAP_K3_PIECE_COLS");
+        const int64_t pwidth = pw ? std::max<int64_t>(32, atoi(pw)) : kChunkN;
+        int64_t per_tile = 0;
+        for (int64_t c0 = 0; c0 < owner->d_pad; c0 += kChunkN)
+            per_tile += ceil_div(std::min<int64_t>(kChunkN, owner->d_pad - c0), pwidth);
+        g.npieces = (int)(tiles * per_tile);
+    }
     if ((s = ensure(owner, kGemmPart, (size_t)tiles * std::max<int64_t>(1, ceil_div(owner->d_pad, 32)) * R *
                                           sizeof(float2))) ||
         (s = ensure(owner, kTileDone, (size_t)tiles * sizeof(unsigned))))
