@@ -474,7 +474,10 @@ __global__ void __maxnreg__(168)
             // the middle of the kernel the partial loads queue behind the operand streams
             // (measured 12-16 us instead of ~1 us), which would hold the epilogue and with
             // it the release of the accumulator buffer.
-            if (*s_last && *s_nfin < kFinCap) {  // defer (the list is full only for
+#ifndef HAP_K3_INLINE_FIN
+#define HAP_K3_INLINE_FIN 0
+#endif
+            if (*s_last && !HAP_K3_INLINE_FIN && *s_nfin < kFinCap) {  // defer (the list is full only for
                 if (etid == 0) s_fin[*s_nfin] = tile;  // pairs with hundreds of pieces)
                 named_bar_sync(1, 128);
                 if (etid == 0) ++*s_nfin;
