@@ -678,7 +678,11 @@ cudaError_t launch_align(const AlignArgs& a, int grid, cudaStream_t st) {
     AlignArgs copy = a;
     int P = g.pitch, su = g.stage_umc ? 1 : 0, sm = g.stage_means ? 1 : 0;
     void* args[] = {&copy, &P, &su, &sm};
-    cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, g.smem, st);
+    // no more CTAs than items: small pairs (C1, the small tests of a C4 batch) then pay a
+    // grid barrier and a ticket over few CTAs
+    const int64_t items = a.item_off[a.G];
+    const int g_ctas = (int)std::max<int64_t>(1, std::min<int64_t>(grid, items));
+    cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(g_ctas), dim3(kThreads), args, g.smem, st);
     if (e != cudaSuccess) return e;
     return cudaEventRecord(last, st);
 }
