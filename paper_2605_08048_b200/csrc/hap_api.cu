@@ -794,6 +794,9 @@ hap_status plan_wave(hap_ctx owner, int G, const WaveTest* T, int pair, bool sha
         for (int64_t c0 = 0; c0 < owner->d_pad; c0 += kChunkN)
             per_tile += ceil_div(std::min<int64_t>(kChunkN, owner->d_pad - c0), pwidth);
         g.npieces = (int)(tiles * per_tile);
+        // dynamic claiming needs no fixed split: a small wave launches only as many CTA
+        // pairs as it has pieces (less setup and teardown for C1-sized tests)
+        if (g.dyn && g.npieces < P.npairs) P.npairs = g.npairs = std::max(1, g.npieces);
     }
     if ((s = ensure(owner, kGemmPart, (size_t)tiles * std::max<int64_t>(1, ceil_div(owner->d_pad, 32)) * R *
                                           sizeof(float2))) ||
