@@ -156,7 +156,8 @@ HAP_API hap_status hap_permtest(hap_ctx ctx, hap_align_info* info, const hap_per
 /* ---- many word pairs ------------------------------------------------------------ */
 /* Varlen batch of P independent tests (configs 4/5): pair p has X rows
  * X_packed[cu_nx[p] .. cu_nx[p+1]) and Y rows Y_packed[cu_ny[p] .. cu_ny[p+1]).
- * Consecutive selected pairs are grouped into waves of cfg->wave tests (see hap_perm_cfg)
+ * The selected pairs are processed largest first (equal shapes adjacent; the results do not
+ * depend on the order) and grouped into waves of cfg->wave tests (see hap_perm_cfg)
  * that share one generator and one mask-GEMM launch; waves alternate between two internal
  * lanes (own workspaces and streams, forked from and joined back to `stream`), so one
  * wave's alignment and mask generation overlap the previous wave's mask-GEMM.  Pair p uses
