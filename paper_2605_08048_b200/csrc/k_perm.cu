@@ -504,7 +504,15 @@ cudaError_t launch_perm(const PermArgs& a, int sm_count, cudaStream_t st) {
     const int lt_pitch = (int)round_up(maxN, 64);  // entries, 128-byte multiple; >= every n_pad
     // wide (uint32) table + start list when 4 warps fit in the budget, else uint16 table
     static const char* nar = getenv("HAP_K2_NARROW");  // EXPERIMENT: force the u16 table
-    const bool wide = (size_t)lt_pitch * 5u + 160u <= (200u * 1024u) / 4u && !(nar && atoi(nar));
+    // the u32 table + start list take 5 bytes per pooled row and warp: for large N the u16
+    // table doubles the warps per SM, which wins over the wide kernel's cheaper scatter
+    // (batches of equal pairs: N = 2400 wide 100.7 vs 103.6 us/test, N = 3000 125.5 vs 124.1,
+    // N = 4000 169.7 vs 164.9; C4 115.2 -> 110-112, C3 13.9 -> 13.7 ms); cut-over at
+    // HAP_K2_WIDE_MAX_N (default 2560 pooled rows)
+    static const char* wmax_env = getenv("HAP_K2_WIDE_MAX_N");
+    const int64_t wide_max_n = wmax_env ? atoll(wmax_env) : 2560;
+    const bool wide = (size_t)lt_pitch * 5u + 160u <= (200u * 1024u) / 4u && !(nar && atoi(nar)) &&
+                      maxN <= wide_max_n;
     const size_t per_warp = wide ? (size_t)lt_pitch * 5u + 160u : (size_t)(lt_pitch + 128) * sizeof(uint16_t);
     const int nw = (int)std::max<size_t>(1, std::min<size_t>(kPermWarps, (200u * 1024u) / per_warp));
     const size_t smem = (size_t)nw * per_warp;

@@ -13,7 +13,8 @@ import paper_2605_08048_b200 as hap
 P = int(sys.argv[1]) if len(sys.argv) > 1 else 24
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
 kind = os.environ.get("HAP_SIZES", "c2")
-sizes = [1000] * P if kind == "c2" else [500] * P if kind == "c5" else HI.c4_sizes(10000)[:P]
+sizes = ([1000] * P if kind == "c2" else [500] * P if kind == "c5" else
+         [int(kind[1:])] * P if kind.startswith("n") else HI.c4_sizes(10000)[:P])  # nNNN: n_x = n_y = NNN
 shared = os.environ.get("HAP_SHARED", "0") == "1"
 Xp, cnx, Yp, cny = HI.varlen_batch(sizes, d=768)
 X, Y = torch.from_numpy(Xp).cuda(), torch.from_numpy(Yp).cuda()
