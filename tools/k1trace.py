@@ -24,6 +24,7 @@ G = torch.cuda.get_device_properties(0).multi_processor_count
 buf = np.zeros(8 + 8 * G, dtype=np.int64)
 L.hap_debug_k1_stamps(ctx.h, buf.ctypes.data_as(ctypes.POINTER(ctypes.c_longlong)), buf.size)
 st = buf[8:].reshape(G, 8).astype(np.float64)
+st = st[st[:, 0] > 0]  # CTAs of this launch (the grid is no larger than the item count)
 t0 = st[:, 0].min()
 st = (st - t0) / 1e3
 names = ["entry", "P1done", "bar1", "P2done", "P3done", "P4coef", "P4done", "exit"]
