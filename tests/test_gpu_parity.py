@@ -728,3 +728,10 @@ def test_batch_order_independent(ctx):
     perm = list(np.random.default_rng(1).permutation(len(sizes)))
     b = ctx.permtest_batch(X, cnx, Y, cny, 800, SEED, stream_id=3, pair_sel=perm)
     assert a == b
+
+
+def test_max_pooled_size(ctx, orc):
+    """N = n_x + n_y = 65535 (the ABI maximum; u16 generator table, 65536-row mask tiles):
+    every statistic and count against the oracle."""
+    X, Y = HI.make_pair(HI.PairSpec(40000, 25535, 16, 20.0, 30.0, 40.0, seed=65535))
+    check_pair(ctx, orc, X, Y, 300, s=7)
