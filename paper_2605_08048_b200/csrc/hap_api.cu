@@ -16,6 +16,9 @@
 
 using namespace hap;
 
+// batch lanes: two by default (HAP_LANES: 1..kMaxLanes, experiments)
+constexpr int kMaxLanes = 3;
+
 struct hap_ctx_s {
     int device = 0;
     int sm_count = 0;
@@ -41,16 +44,16 @@ struct hap_ctx_s {
     bool used[2] = {false, false};
     // batch pipeline: two lanes (internal streams forked from / joined to the caller's
     // stream), each with kMaxWave sub-contexts (own workspaces + generator streams)
-    hap_ctx sub[2][kMaxWave] = {};
-    cudaStream_t sub_stream[2] = {nullptr, nullptr};
-    cudaEvent_t ev_sub[2] = {nullptr, nullptr};
+    hap_ctx sub[kMaxLanes][kMaxWave] = {};
+    cudaStream_t sub_stream[kMaxLanes] = {};
+    cudaEvent_t ev_sub[kMaxLanes] = {};
     // host inputs: per lane a copy stream that stages a wave's rows as soon as the lane's
     // previous K1 (the last reader of the staging buffers) is done
     // (two staging buffers per workspace, alternating over the lane's waves)
-    cudaStream_t cp_stream[2] = {nullptr, nullptr};
-    cudaEvent_t ev_k1done[2][2] = {}, ev_copied[2] = {nullptr, nullptr};
-    bool k1_recorded[2][2] = {};
-    int lane_waves[2] = {0, 0};
+    cudaStream_t cp_stream[kMaxLanes] = {};
+    cudaEvent_t ev_k1done[kMaxLanes][2] = {}, ev_copied[kMaxLanes] = {};
+    bool k1_recorded[kMaxLanes][2] = {};
+    int lane_waves[kMaxLanes] = {};
     // cached K3 schedules: key {d_pad, npairs, (ntiles, n_pad) per test} -> offset (ints)
     // in buf[kSched]; new ones are staged in pinned host memory and copied on the stream
     struct Sched { std::vector<int64_t> key; int64_t off; int max_slots; };
@@ -504,7 +507,7 @@ hap_status hap_destroy(hap_ctx c) {
         cudaStreamDestroy(c->side);
     }
     if (c->sched_host) cudaFreeHost(c->sched_host);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kMaxLanes; ++i) {
         for (int k = 0; k < kMaxWave; ++k)
             if (c->sub[i][k]) hap_destroy(c->sub[i][k]);
         if (c->sub_stream[i]) cudaStreamDestroy(c->sub_stream[i]);
@@ -969,7 +972,9 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
     if (d < 2 || d > 16384) return fail(c, HAP_E_DIM_MISMATCH, "need 2 <= d <= 16384");
     cudaSetDevice(c->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    for (int k = 0; k < 2; ++k) {
+    static const char* lanes_env = getenv("HAP_LANES");  // EXPERIMENT: number of lanes
+    const int nlanes = std::max(1, std::min(kMaxLanes, lanes_env ? atoi(lanes_env) : 2));
+    for (int k = 0; k < nlanes; ++k) {
         for (int j = 0; j < kMaxWave; ++j)
             if (!c->sub[k][j]) {
                 s = hap_create(c->device, &c->sub[k][j]);
@@ -1010,7 +1015,7 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
             const int64_t n_pad = round_up(maxN, kKBlock);
             const int64_t tiles = std::min(std::max<int64_t>(1, ceil_div(std::max<int64_t>(B, 1), R - 1)),
                                            block_tiles(cfg, n_pad, R));
-            for (int k = 0; k < 2 && !s; ++k)
+            for (int k = 0; k < nlanes && !s; ++k)
                 for (int j = 0; j < wave_max && !s; ++j) {
                     s = reserve_pair(c->sub[k][j], maxN, d, tiles, R);
                     for (int b = 0; b < 2 && host_in; ++b) {
@@ -1023,7 +1028,7 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
     }
     // fork: the two lanes start after the work already on the caller's stream
     cudaError_t e = cudaEventRecord(c->ev_fork, st);
-    for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
+    for (int k = 0; k < nlanes && e == cudaSuccess; ++k) {
         // (the copy streams need no fork: their only hazard, the K1 that last read a staging
         // buffer, is tracked across calls, so the next call's copies start at once)
         e = cudaStreamWaitEvent(c->sub_stream[k], c->ev_fork, 0);
@@ -1042,7 +1047,7 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
     });
     int64_t i = 0, wave = 0;
     while (i < n && !s) {
-        const int k = (int)(wave & 1);  // consecutive waves alternate between the two lanes
+        const int k = (int)(wave % nlanes);  // consecutive waves rotate over the lanes
         cudaStream_t ls = c->sub_stream[k];
         WaveTest T[kMaxWave];
         AlignPair Q[kMaxWave];
@@ -1109,7 +1114,7 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
         ++wave;
     }
     // join: the caller's stream waits for both lanes (also on error, to keep ordering sane)
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < nlanes; ++k) {
         if (cudaEventRecord(c->ev_sub[k], c->sub_stream[k]) == cudaSuccess)
             cudaStreamWaitEvent(st, c->ev_sub[k], 0);
     }
@@ -1141,7 +1146,7 @@ hap_status hap_profile_spans_read(hap_ctx c, double* out, int64_t max_n, int64_t
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return cuda_fail(c, e, "span read");
     std::vector<std::pair<hap_ctx, int>> lanes = {{c, 0}};
-    for (int k = 0; k < 2; ++k)
+    for (int k = 0; k < kMaxLanes; ++k)
         for (hap_ctx w : c->sub[k])
             if (w) lanes.push_back({w, k + 1});
     struct Rec { int code; unsigned long long a, b; };
@@ -1257,7 +1262,7 @@ hap_status hap_profile_timeline(hap_ctx c, double* out, int64_t max_n, int64_t* 
     cudaSetDevice(c->device);
     // lane 0 = this context, lanes 1, 2 = the batch lanes' sub-contexts; one time base
     std::vector<std::pair<hap_ctx, int>> lanes = {{c, 0}};
-    for (int k = 0; k < 2; ++k)
+    for (int k = 0; k < kMaxLanes; ++k)
         for (hap_ctx w : c->sub[k])
             if (w) lanes.push_back({w, k + 1});
     cudaEvent_t t0 = nullptr;
