@@ -191,8 +191,11 @@ __device__ __forceinline__ bool test_failed(const GemmTest& T) {
     return *reinterpret_cast<const volatile int*>(&T.info->status) != HAP_OK;
 }
 
+#ifndef HAP_K3_MAXNREG
+#define HAP_K3_MAXNREG 168
+#endif
 template <int kPair>
-__global__ void __maxnreg__(168)
+__global__ void __maxnreg__(HAP_K3_MAXNREG)
     k3_maskgemm(const __grid_constant__ GemmMaps maps, const GemmArgs g) {
     using C = Cfg<kPair>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
