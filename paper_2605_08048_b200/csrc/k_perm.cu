@@ -29,16 +29,23 @@ namespace {
 constexpr int kPermWarps = 1;
 constexpr uint16_t kExiled = 0xFFFF;
 
-__global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy(PermArgs a, int lt_pitch) {
+// kPW warps share one permutation's table (more warps per SM for the same shared memory);
+// warp w draws and scatters steps k0 + 128 w .. of each block of 128 kPW steps.
+template <int kPW>
+__device__ __forceinline__ void perm_sync() {
+    if constexpr (kPW == 1) __syncwarp(); else __syncthreads();
+}
+
+template <int kPW>
+__global__ void __launch_bounds__(kPW * 32) k2_perm_fy(PermArgs a, int lt_pitch) {
     extern __shared__ __align__(16) uint8_t smem[];
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    uint16_t* LT = reinterpret_cast<uint16_t*>(smem) + (size_t)w * (lt_pitch + 128);
-    uint16_t* stage = LT + lt_pitch;
-    const int nw = (int)(blockDim.x >> 5);
-    const int64_t wstride = (int64_t)gridDim.x * nw;
+    constexpr uint32_t kT = 32u * kPW;
+    const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
+    uint16_t* LT = reinterpret_cast<uint16_t*>(smem);
+    uint16_t* stage = LT + lt_pitch + 128 * w;
     const int64_t items = a.item_off[a.G];
-    if (l == 0) span_enter(a.span);
-    for (int64_t pi = (int64_t)blockIdx.x * nw + w; pi < items; pi += wstride) {
+    if (tid == 0) span_enter(a.span);
+    for (int64_t pi = blockIdx.x; pi < items; pi += gridDim.x) {
         int ti = 0;  // test of this item (the tests' items are contiguous, in test order)
         while (ti + 1 < a.G && pi >= a.item_off[ti + 1]) ++ti;
         const PermTest& T = a.t[ti];
@@ -49,7 +56,7 @@ __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy(PermArgs a, int lt
             const int64_t t = li - T.count;
             uint4* row = reinterpret_cast<uint4*>(static_cast<uint16_t*>(T.out) +
                                                   t * a.rows_per_tile * T.n_pad);
-            for (int64_t v8 = l; v8 < T.n_pad / 8; v8 += 32) {
+            for (int64_t v8 = tid; v8 < T.n_pad / 8; v8 += kT) {
                 uint32_t wds[4];
 #pragma unroll
                 for (int e2 = 0; e2 < 4; ++e2) {
@@ -62,10 +69,11 @@ __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy(PermArgs a, int lt
         }
         const uint32_t b = (uint32_t)(T.b_begin + (uint64_t)li);
         uint4* LT4 = reinterpret_cast<uint4*>(LT);
-        for (int q = l; q < lt_pitch / 8; q += 32) LT4[q] = make_uint4(0, 0, 0, 0);
-        __syncwarp();
-        // ---- phase A: draws + last-writer scatter, 128 steps per round
-        for (uint32_t k0 = 0; k0 < nx; k0 += 128) {
+        for (int q = tid; q < lt_pitch / 8; q += kT) LT4[q] = make_uint4(0, 0, 0, 0);
+        perm_sync<kPW>();
+        // ---- phase A: draws + last-writer scatter, 128 steps per warp and round
+        for (uint32_t k00 = 0; k00 < nx; k00 += 128u * kPW) {
+            const uint32_t k0 = k00 + 128u * (uint32_t)w;
             if (k0 + 4u * l < nx) {
                 const u32x4 wd = philox4x32_10(u32x4{(k0 >> 2) + (uint32_t)l, b, s, 0u}, key0, key1);
                 uint32_t j[4];
@@ -79,7 +87,8 @@ __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy(PermArgs a, int lt
             }
             __syncwarp();
             // scatter in 4 rounds of 32 consecutive steps (round r has larger k than r-1,
-            // so rounds resolve in step order); a collision inside a round is fixed below
+            // so rounds resolve in step order); a collision inside a round (or, kPW > 1,
+            // with another warp's steps) is fixed below
             uint32_t jr[4], kr[4];
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
@@ -91,13 +100,17 @@ __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy(PermArgs a, int lt
                 if (kr[r]) LT[j] = (uint16_t)kr[r];
                 __syncwarp();
             }
-            // last writer (largest k) must win: a step that lost a same-round collision to
-            // a smaller k rewrites; repeat until no step is short-changed (rarely > 1 pass)
+            // last writer (largest k) must win: a step that lost a collision to a smaller k
+            // rewrites; repeat until no step is short-changed (rarely > 1 pass)
             for (;;) {
+                if constexpr (kPW > 1) __syncthreads();
                 uint32_t lost = 0u;
 #pragma unroll
                 for (int r = 0; r < 4; ++r) lost |= (uint32_t)(LT[jr[r]] < kr[r]) << r;
-                if (!__any_sync(0xffffffffu, lost)) break;
+                bool again;
+                if constexpr (kPW == 1) again = __any_sync(0xffffffffu, lost);
+                else again = __syncthreads_or(lost != 0u);
+                if (!again) break;
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
                     if ((lost >> r) & 1u) LT[jr[r]] = (uint16_t)kr[r];
@@ -105,6 +118,7 @@ __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy(PermArgs a, int lt
                 }
             }
         }
+        if constexpr (kPW > 1) __syncthreads();
         // ---- phase B: each written high position exiles the end of its chain.  Per lane a
         // two-state machine (scan the lane's high positions / walk a chain), one LDS per
         // iteration, so lanes with short chains keep scanning while others walk.  In both
@@ -112,7 +126,7 @@ __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy(PermArgs a, int lt
         // are never marked, chain nodes never exiled, so one test serves both states.
         {
             const uint32_t Nm1 = N - 1u;
-            uint32_t pn = nx + l;          // next high position of this lane to scan
+            uint32_t pn = nx + (uint32_t)tid;  // next high position of this thread to scan
             uint32_t cur = min(pn, Nm1);   // LT index read this iteration
             uint32_t walking = 0u;
             while (__any_sync(0xffffffffu, pn < N)) {
@@ -121,20 +135,20 @@ __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy(PermArgs a, int lt
                     const uint32_t t = LT[cur];
                     const uint32_t stop = (t == 0u) | (t == (uint32_t)kExiled);
                     if (walking & stop & (pn < N)) LT[cur] = kExiled;  // chain end: exiled
-                    pn += stop ? 32u : 0u;
+                    pn += stop ? kT : 0u;
                     cur = stop ? min(pn, Nm1) : t - 1u;
                     walking = stop ^ 1u;
                 }
             }
         }
-        __syncwarp();
+        perm_sync<kPW>();
         // ---- phase C: exact 0/1 row
         if (a.out_kind == kMaskBf16Row) {
             const int64_t R1 = a.rows_per_tile - 1;
             const int64_t orow = (li / R1) * a.rows_per_tile + 1 + li % R1;
             uint4* row = reinterpret_cast<uint4*>(static_cast<uint16_t*>(T.out) + orow * T.n_pad);
             const uint4* L4 = reinterpret_cast<const uint4*>(LT);
-            for (int64_t v8 = l; v8 < T.n_pad / 8; v8 += 32) {
+            for (int64_t v8 = tid; v8 < T.n_pad / 8; v8 += kT) {
                 const uint4 q = L4[v8];
                 const uint32_t w[4] = {q.x, q.y, q.z, q.w};
                 uint32_t o[4];
@@ -163,14 +177,14 @@ __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy(PermArgs a, int lt
             }
         } else {
             uint8_t* row = static_cast<uint8_t*>(T.out) + li * T.N;
-            for (uint32_t v = l; v < N; v += 32) {
+            for (uint32_t v = tid; v < N; v += kT) {
                 const uint16_t t = LT[v];
                 row[v] = (v < nx) ? (t != kExiled) : (t != 0);
             }
         }
-        __syncwarp();
+        perm_sync<kPW>();
     }
-    if (l == 0) span_exit(a.span);
+    if (tid == 0) span_exit(a.span);
 }
 
 
@@ -513,20 +527,31 @@ cudaError_t launch_perm(const PermArgs& a, int sm_count, cudaStream_t st) {
     const int64_t wide_max_n = wmax_env ? atoll(wmax_env) : 2560;
     const bool wide = (size_t)lt_pitch * 5u + 160u <= (200u * 1024u) / 4u && !(nar && atoi(nar)) &&
                       maxN <= wide_max_n;
-    const size_t per_warp = wide ? (size_t)lt_pitch * 5u + 160u : (size_t)(lt_pitch + 128) * sizeof(uint16_t);
-    const int nw = (int)std::max<size_t>(1, std::min<size_t>(kPermWarps, (200u * 1024u) / per_warp));
-    const size_t smem = (size_t)nw * per_warp;
-    const void* fn = wide ? (const void*)k2_perm_fy32 : (const void*)k2_perm_fy;
-    static size_t configured[2] = {0, 0};
-    if (smem > 48 * 1024 && smem > configured[wide]) {
+    // narrow: kPW warps per permutation share its table, so latency-bound warps are not
+    // limited by tables per SM (N = 5000 / 10^4 pairs: 216 -> 206 / 499 -> 408 us per test
+    // with 2 / 4 warps); HAP_K2_PW = 1, 2 or 4 overrides
+    static const char* pw_env = getenv("HAP_K2_PW");
+    const int pw = pw_env ? std::max(1, std::min(4, atoi(pw_env))) : maxN >= 6144 ? 4 : 2;
+    const int kpw = pw >= 4 ? 4 : pw >= 2 ? 2 : 1;
+    const size_t per_warp = wide ? (size_t)lt_pitch * 5u + 160u
+                                 : (size_t)(lt_pitch + 128 * kpw) * sizeof(uint16_t);
+    const int nw = wide ? (int)std::max<size_t>(1, std::min<size_t>(kPermWarps, (200u * 1024u) / per_warp)) : kpw;
+    const size_t smem = wide ? (size_t)nw * per_warp : per_warp;
+    const void* fn = wide ? (const void*)k2_perm_fy32
+                     : kpw == 4 ? (const void*)k2_perm_fy<4>
+                     : kpw == 2 ? (const void*)k2_perm_fy<2>
+                                : (const void*)k2_perm_fy<1>;
+    const int fi = wide ? 0 : kpw;
+    static size_t configured[5] = {0, 0, 0, 0, 0};
+    if (smem > 48 * 1024 && smem > configured[fi]) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        configured[wide] = smem;
+        configured[fi] = smem;
     }
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nw * 32, smem);
     per_sm = std::max(1, std::min(per_sm, a.max_ctas_per_sm > 0 ? a.max_ctas_per_sm : per_sm));
-    const int64_t need = ceil_div(items, nw);
+    const int64_t need = wide ? ceil_div(items, nw) : items;  // narrow: one permutation per CTA
     const int grid = (int)std::min<int64_t>(need, (int64_t)sm_count * per_sm);
     if (a.split == 1) {  // K2a: draws into the rows, register-only (wide path only)
         const int64_t g2 = std::min<int64_t>(ceil_div(items, 4), (int64_t)sm_count * 4);
@@ -534,7 +559,9 @@ cudaError_t launch_perm(const PermArgs& a, int sm_count, cudaStream_t st) {
     } else if (wide) {
         k2_perm_fy32<<<grid, nw * 32, smem, st>>>(a, lt_pitch);
     } else {
-        k2_perm_fy<<<grid, nw * 32, smem, st>>>(a, lt_pitch);
+        if (kpw == 4) k2_perm_fy<4><<<grid, 128, smem, st>>>(a, lt_pitch);
+        else if (kpw == 2) k2_perm_fy<2><<<grid, 64, smem, st>>>(a, lt_pitch);
+        else k2_perm_fy<1><<<grid, 32, smem, st>>>(a, lt_pitch);
     }
     return cudaGetLastError();
 }

@@ -568,11 +568,14 @@ print(json.dumps([[r["exceed_ge"], r["exceed_abs"], r["flagged"], r["gemm_t_obs"
 
 @pytest.mark.parametrize("env", [{"HAP_K1_DRAWS": "1"}, {"HAP_BATCH_SPLIT": "1"},
                                  {"HAP_WAVE": "1"}, {"HAP_K3_DYNAMIC": "0"},
-                                 {"HAP_K3_DYNAMIC": "0", "HAP_K3_ROUND_ROBIN": "1"}])
+                                 {"HAP_K3_DYNAMIC": "0", "HAP_K3_ROUND_ROBIN": "1"},
+                                 {"HAP_K2_NARROW": "1", "HAP_K2_PW": "1"},
+                                 {"HAP_K2_NARROW": "1", "HAP_K2_PW": "2"},
+                                 {"HAP_K2_NARROW": "1", "HAP_K2_PW": "4"}])
 def test_experimental_paths_bitwise_equal(env):
     """The alternative scheduling paths (draws staged by K1, split generator on the side
-    stream, one test per wave, the static K3 split, round-robin K3 schedule) give bitwise
-    the default results."""
+    stream, one test per wave, the static K3 split, round-robin K3 schedule, the u16-table
+    generator with 1, 2 or 4 warps per permutation) give bitwise the default results."""
     import json
     import os
     import subprocess
@@ -581,7 +584,8 @@ def test_experimental_paths_bitwise_equal(env):
 
     def run(extra):
         e = dict(os.environ)
-        for k in ("HAP_K1_DRAWS", "HAP_BATCH_SPLIT", "HAP_WAVE", "HAP_K3_ROUND_ROBIN", "HAP_K3_DYNAMIC"):
+        for k in ("HAP_K1_DRAWS", "HAP_BATCH_SPLIT", "HAP_WAVE", "HAP_K3_ROUND_ROBIN", "HAP_K3_DYNAMIC",
+                  "HAP_K2_NARROW", "HAP_K2_PW"):
             e.pop(k, None)
         e.update(extra)
         out = subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT, root], env=e,
