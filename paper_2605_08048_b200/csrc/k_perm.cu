@@ -26,7 +26,6 @@
 namespace hap {
 namespace {
 
-constexpr int kPermWarps = 1;
 constexpr uint16_t kExiled = 0xFFFF;
 
 // kPW warps share one permutation's table (more warps per SM for the same shared memory);
@@ -226,7 +225,7 @@ __global__ void __launch_bounds__(128) k2_draws(PermArgs a) {
 }
 
 __device__ __forceinline__ void emit_row_u32(const PermArgs& a, const PermTest& T, const uint32_t* LT,
-                                             int64_t li, uint32_t nx, int l) {
+                                             int64_t li, uint32_t nx, int l, int nthreads) {
     const int64_t R1 = a.rows_per_tile - 1;
     const int64_t orow = (li / R1) * a.rows_per_tile + 1 + li % R1;
     // lane = 4 consecutive entries per step (contiguous 512 B per warp: conflict-free
@@ -234,7 +233,7 @@ __device__ __forceinline__ void emit_row_u32(const PermArgs& a, const PermTest& 
     uint2* row = reinterpret_cast<uint2*>(static_cast<uint16_t*>(T.out) + orow * T.n_pad);
     uint4* L4 = reinterpret_cast<uint4*>(const_cast<uint32_t*>(LT));
     const uint4 z = make_uint4(0, 0, 0, 0);
-    for (int v4 = l; v4 < (int)(T.n_pad >> 2); v4 += 32) {
+    for (int v4 = l; v4 < (int)(T.n_pad >> 2); v4 += nthreads) {
         const uint4 q = L4[v4];
         L4[v4] = z;  // leave the table zeroed for the next permutation
         const uint32_t t[4] = {q.x, q.y, q.z, q.w};
@@ -252,24 +251,27 @@ __device__ __forceinline__ void emit_row_u32(const PermArgs& a, const PermTest& 
     }
 }
 
-__global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy32(PermArgs a, int lt_pitch) {
+// kPW warps share one permutation's table (as k2_perm_fy): the atomics of phase A and the
+// mask emit split the steps / positions; each warp compacts and walks the chains of its own
+// high positions (chains are disjoint) in its own start list.
+template <int kPW>
+__global__ void __launch_bounds__(kPW * 32) k2_perm_fy32(PermArgs a, int lt_pitch) {
     extern __shared__ __align__(16) uint8_t smem[];
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    // per warp: LT u32[lt_pitch] | sink u32[32] | starts u16[lt_pitch / 2 + 16]
-    uint32_t* LT = reinterpret_cast<uint32_t*>(smem + (size_t)w * ((size_t)lt_pitch * 5u + 160u));
-    uint32_t* sink = LT + lt_pitch + l;  // per-lane target of the atomics of no-op steps
-    uint16_t* starts = reinterpret_cast<uint16_t*>(LT + lt_pitch + 32);
+    constexpr uint32_t kT = 32u * kPW;
+    const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
+    // per CTA: LT u32[lt_pitch] | sink u32[32 kPW] | kPW x starts u16[lt_pitch / 2 + 16]
+    uint32_t* LT = reinterpret_cast<uint32_t*>(smem);
+    uint32_t* sink = LT + lt_pitch + tid;  // per-thread target of the atomics of no-op steps
+    uint16_t* starts = reinterpret_cast<uint16_t*>(LT + lt_pitch + kT) + (size_t)w * (lt_pitch / 2 + 16);
     const uint32_t lane_lt = (1u << l) - 1u;
-    const int nw = (int)(blockDim.x >> 5);
-    const int64_t wstride = (int64_t)gridDim.x * nw;
     const int64_t items = a.item_off[a.G];
-    if (l == 0) span_enter(a.span);
+    if (tid == 0) span_enter(a.span);
     {
         uint4* L4 = reinterpret_cast<uint4*>(LT);
-        for (int q = l; q < lt_pitch / 4; q += 32) L4[q] = make_uint4(0, 0, 0, 0);
+        for (int q = tid; q < lt_pitch / 4; q += kT) L4[q] = make_uint4(0, 0, 0, 0);
     }
-    __syncwarp();
-    for (int64_t pi = (int64_t)blockIdx.x * nw + w; pi < items; pi += wstride) {
+    perm_sync<kPW>();
+    for (int64_t pi = blockIdx.x; pi < items; pi += gridDim.x) {
         int ti = 0;  // test of this item (the tests' items are contiguous, in test order)
         while (ti + 1 < a.G && pi >= a.item_off[ti + 1]) ++ti;
         const PermTest& T = a.t[ti];
@@ -280,7 +282,7 @@ __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy32(PermArgs a, int 
             const int64_t t = li - T.count;
             uint4* row = reinterpret_cast<uint4*>(static_cast<uint16_t*>(T.out) +
                                                   t * a.rows_per_tile * T.n_pad);
-            for (int64_t v8 = l; v8 < T.n_pad / 8; v8 += 32) {
+            for (int64_t v8 = tid; v8 < T.n_pad / 8; v8 += kT) {
                 uint32_t wds[4];
 #pragma unroll
                 for (int e2 = 0; e2 < 4; ++e2) {
@@ -298,16 +300,16 @@ __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy32(PermArgs a, int 
         // ---- phase A: draws (or the targets K2a staged in this row) + last-writer scatter
         // (atomicMax = largest step wins)
         if (a.split == 2) {
-            for (uint32_t kc = 4u * (uint32_t)l; kc < nx; kc += 8u * 128u) {
+            for (uint32_t kc = 4u * (uint32_t)tid; kc < nx; kc += 8u * 4u * kT) {
                 uint2 jj[8];  // 8 blocks of 4 targets in flight (one L2 round trip)
 #pragma unroll
                 for (int it = 0; it < 8; ++it) {
-                    const uint32_t k0 = kc + 128u * it;
+                    const uint32_t k0 = kc + 4u * kT * it;
                     jj[it] = k0 < nx ? *reinterpret_cast<const uint2*>(jrow + k0) : make_uint2(0, 0);
                 }
 #pragma unroll
                 for (int it = 0; it < 8; ++it) {
-                    const uint32_t k0 = kc + 128u * it;
+                    const uint32_t k0 = kc + 4u * kT * it;
                     const uint32_t j[4] = {jj[it].x & 0xFFFFu, jj[it].x >> 16, jj[it].y & 0xFFFFu,
                                            jj[it].y >> 16};
 #pragma unroll
@@ -318,7 +320,7 @@ __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy32(PermArgs a, int 
                 }
             }
         } else {
-            for (uint32_t k0 = 4u * (uint32_t)l; k0 < nx; k0 += 128u) {
+            for (uint32_t k0 = 4u * (uint32_t)tid; k0 < nx; k0 += 4u * kT) {
                 uint32_t j[4];
                 draw_targets(k0, nx, N, b, s, key0, key1, j);
 #pragma unroll
@@ -328,14 +330,14 @@ __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy32(PermArgs a, int 
                 }
             }
         }
-        __syncwarp();
+        perm_sync<kPW>();
         // ---- phase B1: chain starts LT[p]-1 of the written high positions, 8 per lane per
         // pass.  A chain that ends at its start (position k* not written before step k*,
         // ~70 % of them) is exiled right here; the others enter the list at their second
         // node, at offsets from a warp prefix sum of the per-lane counts (4 ballots).
         uint32_t nst = 0;
-        for (uint32_t base = nx & ~3u; __any_sync(0xffffffffu, base + 4u * (uint32_t)l < N);
-             base += 256u) {
+        for (uint32_t base = (nx & ~3u) + 256u * (uint32_t)w; __any_sync(0xffffffffu, base + 4u * (uint32_t)l < N);
+             base += 256u * kPW) {
             // entries base + 4l .. +3 and base + 128 + 4l .. +3: each half is a contiguous
             // 512 B per warp (conflict-free LDS.128); beyond N the table is 0
             const uint32_t pa = base + 4u * (uint32_t)l, pb = pa + 128u;
@@ -385,21 +387,21 @@ __global__ void __launch_bounds__(kPermWarps * 32) k2_perm_fy32(PermArgs a, int 
                 c1 = i1 < nst ? (e1 ? n1 : t1 - 1u) : 0u;
             }
         }
-        __syncwarp();
+        perm_sync<kPW>();
         // ---- phase C: exact 0/1 row (re-zeroes the table)
         if (a.out_kind == kMaskBf16Row) {
-            emit_row_u32(a, T, LT, li, nx, l);
+            emit_row_u32(a, T, LT, li, nx, tid, (int)kT);
         } else {
             uint8_t* row = static_cast<uint8_t*>(T.out) + li * T.N;
-            for (uint32_t v = l; v < N; v += 32) {
+            for (uint32_t v = tid; v < N; v += kT) {
                 const uint32_t t = LT[v];
                 LT[v] = 0u;
                 row[v] = (v < nx) ? (t != kExiled32) : (t != 0u);
             }
         }
-        __syncwarp();
+        perm_sync<kPW>();
     }
-    if (l == 0) span_exit(a.span);
+    if (tid == 0) span_exit(a.span);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -532,17 +534,22 @@ cudaError_t launch_perm(const PermArgs& a, int sm_count, cudaStream_t st) {
     // with 2 / 4 warps); HAP_K2_PW = 1, 2 or 4 overrides
     static const char* pw_env = getenv("HAP_K2_PW");
     const int pw = pw_env ? std::max(1, std::min(4, atoi(pw_env))) : maxN >= 6144 ? 4 : 2;
-    const int kpw = pw >= 4 ? 4 : pw >= 2 ? 2 : 1;
-    const size_t per_warp = wide ? (size_t)lt_pitch * 5u + 160u
-                                 : (size_t)(lt_pitch + 128 * kpw) * sizeof(uint16_t);
-    const int nw = wide ? (int)std::max<size_t>(1, std::min<size_t>(kPermWarps, (200u * 1024u) / per_warp)) : kpw;
-    const size_t smem = wide ? (size_t)nw * per_warp : per_warp;
-    const void* fn = wide ? (const void*)k2_perm_fy32
+    static const char* wpw_env = getenv("HAP_K2_WIDE_PW");  // the same for the u32 table
+    const int wpw = wpw_env ? std::max(1, std::min(4, atoi(wpw_env))) : 1;
+    const int kpw = wide ? (wpw >= 4 ? 4 : wpw >= 2 ? 2 : 1) : (pw >= 4 ? 4 : pw >= 2 ? 2 : 1);
+    // per CTA (one permutation at a time): u32 table + sinks + a start list per warp, or
+    // u16 table + a staging row per warp
+    const size_t smem = wide ? (size_t)lt_pitch * (4u + kpw) + 160u * kpw
+                             : (size_t)(lt_pitch + 128 * kpw) * sizeof(uint16_t);
+    const int nw = kpw;
+    const void* fn = wide ? (kpw == 4 ? (const void*)k2_perm_fy32<4>
+                             : kpw == 2 ? (const void*)k2_perm_fy32<2>
+                                        : (const void*)k2_perm_fy32<1>)
                      : kpw == 4 ? (const void*)k2_perm_fy<4>
                      : kpw == 2 ? (const void*)k2_perm_fy<2>
                                 : (const void*)k2_perm_fy<1>;
-    const int fi = wide ? 0 : kpw;
-    static size_t configured[5] = {0, 0, 0, 0, 0};
+    const int fi = (wide ? 5 : 0) + kpw;
+    static size_t configured[10] = {};
     if (smem > 48 * 1024 && smem > configured[fi]) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -551,13 +558,15 @@ cudaError_t launch_perm(const PermArgs& a, int sm_count, cudaStream_t st) {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nw * 32, smem);
     per_sm = std::max(1, std::min(per_sm, a.max_ctas_per_sm > 0 ? a.max_ctas_per_sm : per_sm));
-    const int64_t need = wide ? ceil_div(items, nw) : items;  // narrow: one permutation per CTA
+    const int64_t need = items;  // one permutation per CTA at a time
     const int grid = (int)std::min<int64_t>(need, (int64_t)sm_count * per_sm);
     if (a.split == 1) {  // K2a: draws into the rows, register-only (wide path only)
         const int64_t g2 = std::min<int64_t>(ceil_div(items, 4), (int64_t)sm_count * 4);
         k2_draws<<<(int)g2, 128, 0, st>>>(a);
     } else if (wide) {
-        k2_perm_fy32<<<grid, nw * 32, smem, st>>>(a, lt_pitch);
+        if (kpw == 4) k2_perm_fy32<4><<<grid, 128, smem, st>>>(a, lt_pitch);
+        else if (kpw == 2) k2_perm_fy32<2><<<grid, 64, smem, st>>>(a, lt_pitch);
+        else k2_perm_fy32<1><<<grid, 32, smem, st>>>(a, lt_pitch);
     } else {
         if (kpw == 4) k2_perm_fy<4><<<grid, 128, smem, st>>>(a, lt_pitch);
         else if (kpw == 2) k2_perm_fy<2><<<grid, 64, smem, st>>>(a, lt_pitch);
