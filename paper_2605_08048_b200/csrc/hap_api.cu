@@ -381,9 +381,12 @@ hap_status get_schedule(hap_ctx c, const GemmArgs& w, int np, cudaStream_t st, G
 }
 
 // bytes of bf16 mask per launch: large enough that a C4-sized test (N = 10^4, B = 10^4)
-// is one block and joins a wave (C4 sample 121.9 -> 117.5 us/test vs 64 MB); K3 streams
-// the masks with TMA and is not DRAM-bound, so they need not stay in L2
-constexpr int64_t kMaskBudget = 256ll << 20;
+// is one block and joins a wave (C4 sample 121.9 -> 117.5 us/test vs 64 MB), and that a
+// C3 block gives every K3 pair ~45 pieces, so the last-piece tail is short (C3 12.9 /
+// 12.5 / 12.4 / 12.45 ms per test at 256 / 512 / 1024 / 2048 MB); K3 streams the masks
+// with TMA and is not DRAM-bound, so they need not stay in L2.  A worker holds two such
+// blocks (2 GB) only when a test's masks are that large.
+constexpr int64_t kMaskBudget = 1024ll << 20;
 
 cudaEvent_t take_event(hap_ctx c) {
     if (!c->pool.empty()) {
