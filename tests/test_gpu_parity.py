@@ -573,7 +573,8 @@ print(json.dumps([[r["exceed_ge"], r["exceed_abs"], r["flagged"], r["gemm_t_obs"
                                  {"HAP_K2_NARROW": "1", "HAP_K2_PW": "2"},
                                  {"HAP_K2_NARROW": "1", "HAP_K2_PW": "4"},
                                  {"HAP_K2_WIDE_PW": "1"}, {"HAP_K2_WIDE_PW": "2"},
-                                 {"HAP_K2_WIDE_PW": "4"}])
+                                 {"HAP_K2_WIDE_PW": "4"}, {"HAP_K3_TILE_GROUP": "0"},
+                                 {"HAP_K3_TILE_GROUP": "3"}])
 def test_experimental_paths_bitwise_equal(env):
     """The alternative scheduling paths (draws staged by K1, split generator on the side
     stream, one test per wave, the static K3 split, round-robin K3 schedule, the u16-table
@@ -587,7 +588,7 @@ def test_experimental_paths_bitwise_equal(env):
     def run(extra):
         e = dict(os.environ)
         for k in ("HAP_K1_DRAWS", "HAP_BATCH_SPLIT", "HAP_WAVE", "HAP_K3_ROUND_ROBIN", "HAP_K3_DYNAMIC",
-                  "HAP_K2_NARROW", "HAP_K2_PW", "HAP_K2_WIDE_PW"):
+                  "HAP_K2_NARROW", "HAP_K2_PW", "HAP_K2_WIDE_PW", "HAP_K3_TILE_GROUP"):
             e.pop(k, None)
         e.update(extra)
         out = subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT, root], env=e,
