@@ -68,6 +68,20 @@ def raw_cloud(rng: np.random.Generator, mu: np.ndarray, kappa: float, n: int,
 KAPPA_R075 = {768: 1315.34, 4096: 7020.48, 32: 53.627}
 
 
+def mrl_vmf(d: int, kappa: float) -> float:
+    """E[MRL] of vMF(kappa) on S^{d-1}: A_d(kappa) = I_{d/2}(kappa) / I_{d/2-1}(kappa)."""
+    import scipy.special as sp
+    return float(sp.ive(d / 2.0, kappa) / sp.ive(d / 2.0 - 1.0, kappa))
+
+
+def kappa_for_r(d: int, r: float) -> float:
+    """kappa with A_d(kappa) = r (0.5 <= r < 1): the concentration of a cloud whose mean
+    resultant length is r (narrow words r ~ 0.96, near-duplicate clouds r -> 1)."""
+    import scipy.optimize as so
+    return float(so.brentq(lambda k: mrl_vmf(d, k) - r, d * r,
+                           2.0 * d / (1.0 - r) + 10.0, xtol=1e-9, rtol=1e-13))
+
+
 def kappa_for(d: int) -> float:
     if d in KAPPA_R075:
         return KAPPA_R075[d]
@@ -137,6 +151,22 @@ def c4_sizes(P: int, n_min: int = 50, n_max: int = 5000, seed: int = 1004) -> np
     """Log-uniform pair sizes n_p in [n_min, n_max] (Zipf-like frequencies)."""
     rng = np.random.default_rng(seed)
     return np.exp(rng.uniform(math.log(n_min), math.log(n_max), size=P)).astype(np.int64)
+
+
+def duplicated_pair(spec: PairSpec, rep: int = 0, n_distinct_x: int = 8, n_distinct_y: int = 8,
+                    frac: float = 0.5):
+    """make_pair, then a fraction `frac` of each cloud's rows replaced by exact copies of
+    that cloud's first n_distinct rows (identical contexts give identical embeddings)."""
+    X, Y = make_pair(spec, rep)
+    rng = np.random.default_rng([spec.seed, rep, 11])
+    for M, nd in ((X, n_distinct_x), (Y, n_distinct_y)):
+        n = M.shape[0]
+        nd = max(1, min(nd, n))
+        k = int(round(frac * (n - nd)))
+        rows = rng.choice(np.arange(nd, n), size=k, replace=False) if k > 0 else []
+        for i in rows:
+            M[i] = M[int(rng.integers(0, nd))]
+    return X, Y
 
 
 def dyadic_pair(rng: np.random.Generator, n_x: int, n_y: int, d: int, ks=(1, 4, 16)):

@@ -590,7 +590,7 @@ hap_status reserve_pair(hap_ctx c, int64_t N, int64_t d, int64_t tiles, int64_t 
         (s = ensure(c, kZlo, (size_t)zt_rows(d_pad) * n_pad * 2)) ||
         (s = ensure(c, kTpart, (size_t)(2 * d + d_pad) * 8)) ||
         (s = ensure(c, kT64, d_pad * 8)) || (s = ensure(c, kAB, d_pad * 8)) ||
-        (s = ensure(c, kM, d_pad * 8)) || (s = ensure(c, kSconst, 16)) ||
+        (s = ensure(c, kM, d_pad * 8)) || (s = ensure(c, kSconst, 32)) ||
         (s = ensure(c, kMask, (size_t)std::max<int64_t>(2, tiles) * R * n_pad * 2)) ||
         (s = ensure(c, kMask1, (size_t)std::max<int64_t>(2, tiles) * R * n_pad * 2)) ||
         (s = ensure(c, kGemmPart, (size_t)kMaxWave * tiles * std::max<int64_t>(1, ceil_div(d_pad, 32)) * R *
@@ -621,7 +621,7 @@ hap_status prepare_pair_cp(hap_ctx c, const float* X, int64_t n_x, const float* 
         (s = ensure(c, kZlo, (size_t)zt_rows(d_pad) * n_pad * 2)) ||
         (s = ensure(c, kTpart, (size_t)(2 * d + d_pad) * 8)) ||
         (s = ensure(c, kT64, d_pad * 8)) || (s = ensure(c, kAB, d_pad * 8)) ||
-        (s = ensure(c, kM, d_pad * 8)) || (s = ensure(c, kSconst, 16)) ||
+        (s = ensure(c, kM, d_pad * 8)) || (s = ensure(c, kSconst, 32)) ||
         (s = ensure(c, kMask, (size_t)2 * kTileM * n_pad * 2)))
         return s;
     // host inputs are staged into the context (copied on `stream`)

@@ -70,7 +70,7 @@ struct AlignPair {
     double* m;               // [d_pad] centre (multiple of 2^-12): planes hold z - m
     double* t64;             // [d_pad] t = N m + t'
     float2* ab;              // [d_pad] epilogue constants {2a, 2b}, a = n_x m, b = t - a
-    double* sconst;          // [2]     {sum a^2, sum b^2}
+    double* sconst;          // [3]     {sum a^2, sum b^2, eps_rep (R14)}
     long long* acc;          // [2 d + d_pad] fixed-point column sums (zero between launches)
     long long* bad;          // min ZeroVector row (LLONG_MAX = none; reset by the launch)
 };
@@ -109,7 +109,7 @@ struct GemmTest {
     hap_counts* counts;
     double* stats;           // optional, [count][3]
     const float2* ab;        // [d_pad] {2a, 2b}
-    const double* sconst;    // {sum a^2, sum b^2}
+    const double* sconst;    // {sum a^2, sum b^2, eps_rep}
 };
 struct GemmArgs {
     int d_pad, d;            // shared by the tests of a wave

@@ -590,10 +590,11 @@ __global__ void __launch_bounds__(kThreads, 65536 / (kThreads * 64)) k1_align_fu
         for (int g = 0; g < a.G; ++g) {
             const AlignPair& q = a.p[g];
             const int64_t N = q.n_x + q.n_y;
-            double sa = 0.0, sb = 0.0;
+            double sa = 0.0, sb = 0.0, sm = 0.0;
             for (int64_t c = tid; c < a.d_pad; c += kThreads) {
                 const double tsum = fix_get(q.acc + 2 * d + c);
                 const double m = __ldcg(q.m + c);
+                sm += m * m;
                 q.t64[c] = (double)N * m + tsum;
                 const float af = (float)((double)q.n_x * m);
                 const float bf = (float)((double)q.n_y * m + tsum);
@@ -602,10 +603,15 @@ __global__ void __launch_bounds__(kThreads, 65536 / (kThreads * 64)) k1_align_fu
                 sb += (double)bf * (double)bf;
             }
             const double2 sab = block_sum2(sa, sb, red);
+            const double smm = block_sum2(sm, 0.0, red).x;
             for (int64_t c = tid; c < 2 * (int64_t)d + a.d_pad; c += kThreads) q.acc[c] = 0;
             if (tid == 0) {
                 q.sconst[0] = sab.x;
                 q.sconst[1] = sab.y;
+                // representation-error scale of a pooled row (R14): the planes keep
+                // z' = z - m to 2^-17 relative (bf16 hi + lo) after an fp32 evaluation of z
+                // (2^-23 of |z| = 1); E||z'||^2 = 1 - ||m||^2
+                q.sconst[2] = 0x1p-17 * sqrt(fmax(1.0 - smm, 0.0)) + 0x1p-23;
                 *q.bad = LLONG_MAX;  // reset the pair's ZeroVector word
             }
         }

@@ -71,7 +71,7 @@ __device__ __forceinline__ long long gtimer() {
     } while (0)
 
 struct RowStat {
-    double r1, r2, T;
+    double r1, r2, T, e;  // e: error bound of T (R14)
 };
 
 // q(r) = kappa-hat(r) = r (d - r^2)/(1 - r^2) with r clamped (R1, R4); L = log q
@@ -82,18 +82,44 @@ __device__ __forceinline__ double kappa_hat(double r, double d) {
     return r * (d - r2) / (1.0 - r2);
 }
 
+// log(q2/q1) = L(r2) - L(r1): near 1 the ratio goes through log1p of q2/q1 - 1 (formed in
+// fp64) in fp32 - its error, ~1e-7 of T's natural scale, is far below the tie band, and it
+// keeps the finalize off the fp64 pipe, which the running MMAs slow down; a ratio far from
+// 1 (|T| > 0.4) takes the fp64 log (fp32 would round q2/q1 - 1 to -1 once |T| > 16)
+__device__ __forceinline__ double log_ratio(double q1, double q2) {
+    if (q1 == 0.0) return q2 == 0.0 ? 0.0 : INFINITY;  // r1 = 0: T = +inf; both 0: T := 0 (R4)
+    const double x = (q2 - q1) / q1;
+    return fabs(x) < 0.5 ? (double)log1pf((float)x) : log(q2 / q1);
+}
+
+// Half-width of the interval that holds L(r) of the exact statistic, given the GPU's
+// estimate r and its error bound delta (R14).  First order 2 delta |L'(r)| (twice
+// the linear term, L' = 1/r + 2r/(1 - r^2) - 2r/(d - r^2) <= 1/r + 2r/(1 - r^2)); near the
+// clamp the exact interval up to L(1 - 1e-9); groups of one are exact (delta = 0).
+__device__ __forceinline__ double l_width(double r, double delta, double d) {
+    if (delta == 0.0) return 0.0;
+    if (r <= 2.0 * delta) return INFINITY;
+    if (r + 2.0 * delta >= 1.0 - 1e-9)
+        return log(kappa_hat(1.0, d) / kappa_hat(r - 2.0 * delta, d));
+    return 2.0 * delta * (1.0 / r + 2.0 * r / (1.0 - r * r));
+}
+
 // statistic of a tile row from its accumulated sums S1 = |sigma1|^2, S2 = |sigma2|^2;
-// T = L(r2) - L(r1) = log(q(r2)/q(r1)): one log (q = 0 gives the +-inf / both-zero cases)
-__device__ __forceinline__ RowStat row_stat(const GemmArgs& g, const GemmTest& T, double S1, double S2) {
+// T = L(r2) - L(r1) = log(q(r2)/q(r1)); eps = the test's representation-error scale
+__device__ __forceinline__ RowStat row_stat(const GemmArgs& g, const GemmTest& T, double S1, double S2,
+                                            double eps) {
     RowStat s;
-    s.r1 = sqrt(fmax(S1, 0.0)) / (double)T.n_x;
-    s.r2 = sqrt(fmax(S2, 0.0)) / (double)T.n_y;
-    const double q1 = kappa_hat(s.r1, (double)g.d), q2 = kappa_hat(s.r2, (double)g.d);
-    // log of the ratio in fp32 (log1p of q2/q1 - 1 formed in fp64): the error, ~1e-7 of
-    // T's natural scale, is far below the tie band tau = 1e-6 (|L_X| + |L_Y|) (DESIGN R8),
-    // and it keeps the finalize off the fp64 pipe, which the running MMAs slow down
-    s.T = (q1 == 0.0 && q2 == 0.0) ? 0.0
-                                   : (q1 == 0.0 ? INFINITY : (double)log1pf((float)((q2 - q1) / q1)));
+    // a group of one unit vector has MRL exactly 1 (Eq. 8); the GEMM's
+    // 1 +- 1e-7 would fall on either side of the clamp at 1 - 1e-9 (R4)
+    s.r1 = T.n_x == 1 ? 1.0 : sqrt(fmax(S1, 0.0)) / (double)T.n_x;
+    s.r2 = T.n_y == 1 ? 1.0 : sqrt(fmax(S2, 0.0)) / (double)T.n_y;
+    const double d = (double)g.d;
+    s.T = log_ratio(kappa_hat(s.r1, d), kappa_hat(s.r2, d));
+    // |r_gpu - r| <= 8 eps / sqrt(n d) per group (R14: the row errors average over the n
+    // rows and the d coordinates; measured <= 1/4 of this bound at every tested shape)
+    const double k = 8.0 * eps * rsqrt(d);
+    s.e = l_width(s.r1, T.n_x == 1 ? 0.0 : k * rsqrt((double)T.n_x), d) +
+          l_width(s.r2, T.n_y == 1 ? 0.0 : k * rsqrt((double)T.n_y), d);
     return s;
 }
 
@@ -102,7 +128,7 @@ __device__ __forceinline__ RowStat row_stat(const GemmArgs& g, const GemmTest& T
 // All partial loads of the three rows are issued together (one L2 round trip per 8 pieces);
 // the piece partials are summed in ascending slot order (deterministic).
 __device__ void finalize_tile(const GemmArgs& g, const GemmTest& T, int tile, int lt, int np, int etid,
-                              unsigned* s_cnt, double S1c, double S2c, double tau, int unit = -1) {
+                              unsigned* s_cnt, double S1c, double S2c, double tau, double eps, int unit = -1) {
 #define FIN_STAMP(ev) do { if (unit == 3 && etid == 0) K3_STAMP(6, ev); } while (0)
     FIN_STAMP(0);
     const int R = g.rows_per_tile;
@@ -133,7 +159,7 @@ __device__ void finalize_tile(const GemmArgs& g, const GemmTest& T, int tile, in
             }
     }
     FIN_STAMP(1);
-    const RowStat o = row_stat(g, T, S1[0], S2[0]);
+    const RowStat o = row_stat(g, T, S1[0], S2[0], eps);
     FIN_STAMP(2);
     if (lt == 0 && etid == 0) {
         T.info->gemm_r_x = o.r1;
@@ -149,12 +175,15 @@ __device__ void finalize_tile(const GemmArgs& g, const GemmTest& T, int tile, in
         const int row = rows[1 + j];
         const int perm = lt * (R - 1) + row - 1;
         const bool valid = row >= 1 && row < R && perm < T.count;
-        const RowStat st = row_stat(g, T, S1[1 + j], S2[1 + j]);
+        const RowStat st = row_stat(g, T, S1[1 + j], S2[1 + j], eps);
         const double Tb = st.T;
         const bool ge = valid && (Tb >= t_obs);
         const bool ab = valid && (fabs(Tb) >= fabs(t_obs));
-        const bool fl = valid && (Tb == t_obs || fabs(Tb - t_obs) <= tau || fabs(Tb) == fabs(t_obs) ||
-                                  fabs(fabs(Tb) - fabs(t_obs)) <= tau);
+        // near-ties (R8), the band widened by both statistics' error bounds (R14): every
+        // permutation whose decision the kernel's precision cannot certify is flagged
+        const double band = tau + st.e + o.e;
+        const bool fl = valid && (Tb == t_obs || fabs(Tb - t_obs) <= band || fabs(Tb) == fabs(t_obs) ||
+                                  fabs(fabs(Tb) - fabs(t_obs)) <= band);
         const uint32_t bge = __ballot_sync(0xffffffffu, ge);
         const uint32_t bab = __ballot_sync(0xffffffffu, ab);
         const uint32_t bfl = __ballot_sync(0xffffffffu, fl);
@@ -211,8 +240,8 @@ __global__ void __maxnreg__(HAP_K3_MAXNREG)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_q + kQ);
     int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
     unsigned* s_cnt = tmem_slot + 4;  // [3] per-tile counts of the finalize
-    double* s_tc = reinterpret_cast<double*>(tmem_slot + 8);  // [kMaxWave][3] S1c, S2c, tau
-    int* s_nfin = reinterpret_cast<int*>(s_tc + 3 * kMaxWave);  // tiles this CTA finalizes
+    double* s_tc = reinterpret_cast<double*>(tmem_slot + 8);  // [kMaxWave][4] S1c, S2c, tau, eps
+    int* s_nfin = reinterpret_cast<int*>(s_tc + 4 * kMaxWave);  // tiles this CTA finalizes
     int* s_fin = s_nfin + 1;                                    // [kFinCap] deferred tiles
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -264,9 +293,10 @@ __global__ void __maxnreg__(HAP_K3_MAXNREG)
     if (threadIdx.x == 64 + kMaxWave) *s_nfin = 0;
     if (threadIdx.x >= 64 && threadIdx.x < 64 + g.G) {  // finalize constants per test
         const GemmTest& T = g.t[threadIdx.x - 64];
-        s_tc[3 * (threadIdx.x - 64) + 0] = T.sconst[0];
-        s_tc[3 * (threadIdx.x - 64) + 1] = T.sconst[1];
-        s_tc[3 * (threadIdx.x - 64) + 2] = g.tie_rel * (fabs(T.info->logk_x) + fabs(T.info->logk_y));
+        s_tc[4 * (threadIdx.x - 64) + 0] = T.sconst[0];
+        s_tc[4 * (threadIdx.x - 64) + 1] = T.sconst[1];
+        s_tc[4 * (threadIdx.x - 64) + 2] = g.tie_rel * (fabs(T.info->logk_x) + fabs(T.info->logk_y));
+        s_tc[4 * (threadIdx.x - 64) + 3] = T.sconst[2];
     }
     if (warp == 1) {
         if constexpr (kPair == 2) tmem_alloc_pair<kTmemCols>(tmem_slot);
@@ -486,8 +516,8 @@ __global__ void __maxnreg__(HAP_K3_MAXNREG)
                 if (etid == 0) ++*s_nfin;
             } else if (*s_last) {
                 __threadfence();
-                finalize_tile(g, T, tile, tile - T.tile0, np_tile, etid, s_cnt, s_tc[3 * ti],
-                              s_tc[3 * ti + 1], s_tc[3 * ti + 2]);
+                finalize_tile(g, T, tile, tile - T.tile0, np_tile, etid, s_cnt, s_tc[4 * ti],
+                              s_tc[4 * ti + 1], s_tc[4 * ti + 2], s_tc[4 * ti + 3]);
             }
             named_bar_sync(1, 128);
             ++i;
@@ -498,8 +528,8 @@ __global__ void __maxnreg__(HAP_K3_MAXNREG)
             const GemmTest& T = g.t[ti];
             __threadfence();
             if (etid == 0) K3_STAMP(f, 6);
-            finalize_tile(g, T, tile, tile - T.tile0, g.tile_npieces[tile], etid, s_cnt, s_tc[3 * ti],
-                          s_tc[3 * ti + 1], s_tc[3 * ti + 2], f);
+            finalize_tile(g, T, tile, tile - T.tile0, g.tile_npieces[tile], etid, s_cnt, s_tc[4 * ti],
+                          s_tc[4 * ti + 1], s_tc[4 * ti + 2], s_tc[4 * ti + 3], f);
             if (etid == 0) K3_STAMP(f, 7);
             named_bar_sync(1, 128);
         }

@@ -103,6 +103,24 @@ def test_perm_sets_golden(hap, ctx):
         assert np.nonzero(out.cpu().numpy()[0])[0].tolist() == [int(x) for x in rhs.split()]
 
 
+def test_perm_sets_side_stream_golden(hap, ctx):
+    """The product generator on the Lemire-rejection golden sets (independent pure-Python
+    generator, tests/golden/gen_permspec_rejections.py) at the pooled sizes it supports."""
+    import hashlib
+    import torch
+    from test_oracle import _rejection_rows
+    rows = [r for r in _rejection_rows() if r[3] <= 65535]
+    assert len(rows) >= 6
+    for seed, s, b, N, n, rej, kind, want in rows:
+        out = torch.empty((1, N), dtype=torch.uint8, device="cuda")
+        hap.hap_perm_sets(ctx.h, seed, s, b, 1, N, n, out)
+        members = np.nonzero(out.cpu().numpy()[0])[0].tolist()
+        if kind == "sha":
+            assert hashlib.sha256(" ".join(map(str, members)).encode()).hexdigest() == want, (s, b)
+        else:
+            assert members == [int(x) for x in want.split()], (s, b, N, n)
+
+
 # ------------------------------------------------------------------ K1 (pooled planes)
 @pytest.mark.parametrize("n_x,n_y,d,mode", [(64, 64, 768, 0), (37, 50, 100, 0), (1000, 1000, 768, 0),
                                             (300, 200, 64, 1), (5, 3, 3, 0)])
@@ -148,7 +166,8 @@ def test_config1_full(ctx, orc, pair_mode):
 
 @pytest.mark.parametrize("pair_mode", [1, 2])
 @pytest.mark.parametrize("n_x,n_y,d,B,block", [(37, 50, 100, 300, 128), (2, 70, 48, 257, 0),
-                                               (70, 2, 40, 129, 0), (200, 300, 300, 1000, 256),
+                                               (70, 2, 40, 129, 0), (1, 70, 48, 257, 0),
+                                               (70, 1, 40, 129, 0), (200, 300, 300, 1000, 256),
                                                (5, 3, 3, 200, 0), (64, 64, 544, 700, 300)])
 def test_ragged_shapes(ctx, orc, n_x, n_y, d, B, block, pair_mode):
     """Ragged N (not a multiple of 64), d not a multiple of 32 (last d-chunk narrower than
@@ -165,15 +184,116 @@ def test_wide_dimension(ctx, orc, d):
     check_pair(ctx, orc, X, Y, 300, s=3)
 
 
-def test_singleton_group(ctx, orc):
-    """n_x = 1: r1 = ||z_i|| = 1 for every split (L is clamped at r = 1 - 1e-9, R4, and
-    ill-conditioned there), so only the MRLs are compared."""
-    X, Y = HI.make_pair(HI.PairSpec(1, 70, 48, 30.0, 60.0, 40.0, seed=11))
-    g = ctx.permtest_pair(_cuda(X), _cuda(Y), 200, SEED, want_stats=True)
-    ref = orc.run_pair(X, Y, 200, SEED, want_stats=True)
+@pytest.mark.parametrize("n_x,n_y,d", [(1, 70, 48), (70, 1, 768), (1, 1, 8), (1, 300, 4096)])
+def test_singleton_group(ctx, orc, n_x, n_y, d):
+    """A group of one unit vector has MRL exactly 1 (Eq. 8), so its L sits at the clamp
+    r = 1 - 1e-9 (R4) for every split: full parity bars, and the single side's r is exactly 1
+    in every permutation (n_x = n_y = 1: T = 0 for every split, all ties, all counted)."""
+    X, Y = HI.make_pair(HI.PairSpec(n_x, n_y, d, 30.0 + d, 60.0 + d, 40.0, seed=11 + d))
+    g, ref = check_pair(ctx, orc, X, Y, 300)
     gs = g["stats"].cpu().numpy()
-    assert np.allclose(gs[:, 0], 1.0, rtol=1e-6)
-    assert np.allclose(gs[:, 1], ref["stats"][:, 1], rtol=1e-5)
+    if n_x == 1:
+        assert np.all(gs[:, 0] == 1.0)
+    if n_y == 1:
+        assert np.all(gs[:, 1] == 1.0)
+    if n_x == n_y == 1:
+        assert np.all(gs[:, 2] == 0.0) and g["exceed_ge"] == 300 == ref["exceed_ge"]
+
+
+def _eps_rep(hap, ctx, d):
+    """The test's representation-error scale as K1 forms it (R14), from the
+    exported centre m: 2^-17 sqrt(1 - ||m||^2) + 2^-23."""
+    import torch
+    d_pad = -(-d // 32) * 32
+    n_pad = int(hap.decode_info(ctx.info).n_pad)
+    zh = torch.empty((d_pad, n_pad), dtype=torch.int16, device="cuda")
+    t = torch.empty(d_pad, dtype=torch.float64, device="cuda")
+    m = torch.empty(d_pad, dtype=torch.float64, device="cuda")
+    hap.hap_export_pooled(ctx.h, zh, torch.empty_like(zh), t, m)
+    mm = m.cpu().numpy()
+    return 2.0 ** -17 * math.sqrt(max(1.0 - float(mm @ mm), 0.0)) + 2.0 ** -23
+
+
+def _l_width(r, n, eps, d):
+    """DESIGN.md R14 (mirror of k_maskgemm.cu l_width): half-width of the interval holding
+    L(r) given the GPU's r and |dr| <= 8 eps / sqrt(n d)."""
+    r = np.asarray(r, dtype=np.float64)
+    if n == 1:
+        return np.zeros_like(r)
+    delta = 8.0 * eps / math.sqrt(n * d)
+
+    def q(x):
+        x = np.minimum(x, 1 - 1e-9)
+        return x * (d - x * x) / (1 - x * x)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        near = r + 2 * delta >= 1 - 1e-9
+        w = np.where(near, np.log(q(np.ones_like(r)) / q(np.maximum(r - 2 * delta, 1e-300))),
+                     2 * delta * (1 / r + 2 * r / (1 - r * r)))
+    return np.where(r <= 2 * delta, np.inf, w)
+
+
+def check_certified(hap, ctx, orc, X, Y, B, s=0):
+    """R14 at any r: the GPU's error bound e_T covers its actual error on every permutation
+    (and on T_obs); every decision outside the widened band matches the oracle; the GPU
+    flags a superset of the oracle's near-ties, and the counts differ by at most those."""
+    g = ctx.permtest_pair(_cuda(X), _cuda(Y), B, SEED, stream_id=s, want_stats=True)
+    ref = orc.run_pair(X, Y, B, SEED, s=s, want_stats=True)
+    d, n_x, n_y = X.shape[1], X.shape[0], Y.shape[0]
+    eps = _eps_rep(hap, ctx, d)
+    gs, rs = g["stats"].cpu().numpy(), ref["stats"]
+    e = _l_width(gs[:, 0], n_x, eps, d) + _l_width(gs[:, 1], n_y, eps, d)
+    e_obs = float(_l_width(np.array([g["gemm_r_x"]]), n_x, eps, d)[0] +
+                  _l_width(np.array([g["gemm_r_y"]]), n_y, eps, d)[0])
+    assert abs(g["gemm_t_obs"] - ref["t_obs"]) <= e_obs + 1e-6 * (abs(ref["L_x"]) + abs(ref["L_y"]))
+    assert np.all(np.abs(gs[:, 2] - rs[:, 2]) <= e + 1e-7 * (abs(ref["L_x"]) + abs(ref["L_y"])))
+    band = ref["tau"] + e + e_obs
+    tg = g["gemm_t_obs"]
+    out = np.abs(gs[:, 2] - tg) > band
+    assert np.array_equal(gs[out, 2] >= tg, rs[out, 2] >= ref["t_obs"])
+    out2 = np.abs(np.abs(gs[:, 2]) - abs(tg)) > band
+    assert np.array_equal(np.abs(gs[out2, 2]) >= abs(tg), np.abs(rs[out2, 2]) >= abs(ref["t_obs"]))
+    assert g["flagged"] >= ref["flagged"]
+    for k in ("exceed_ge", "exceed_abs"):
+        assert abs(g[k] - ref[k]) <= g["flagged"], (k, g[k], ref[k], g["flagged"])
+    return g, ref
+
+
+@pytest.mark.parametrize("d", [768, 4096])
+@pytest.mark.parametrize("r", [0.96, 0.99, 0.999])
+@pytest.mark.parametrize("n_x,n_y", [(2, 70), (64, 64), (500, 500)])
+def test_narrow_clouds(ctx, orc, d, r, n_x, n_y):
+    """Narrow words (r ~ 0.96, Table 4 colitis) up to r = 0.999, where L is
+    ill-conditioned (dL/dr ~ 1/(1 - r), "drift near r ~ 1"): the full parity bars
+    (1e-5 Ls on T, decisions outside tau, counts within the oracle's flagged)."""
+    if d == 4096 and n_x == 500:
+        n_x = n_y = 300
+    k = HI.kappa_for_r(d, r)
+    X, Y = HI.make_pair(HI.PairSpec(n_x, n_y, d, k, k, 30.0, seed=int(r * 1e4) + d + n_x))
+    check_pair(ctx, orc, X, Y, 1500, s=6)
+
+
+@pytest.mark.parametrize("d,r,n_x,n_y", [(48, 0.9999, 2, 70), (768, 0.9999, 64, 64),
+                                         (768, 0.9999, 1000, 1000), (4096, 0.9999, 300, 300),
+                                         (768, 0.75, 1000, 1000), (48, 0.999, 2, 70)])
+def test_certified_band_near_unit_mrl(hap, ctx, orc, d, r, n_x, n_y):
+    """Beyond r = 0.999 the two-term bf16 path's T error exceeds the plain tie band; the
+    kernel's error bound (R14) widens the band so that every decision it does not flag is
+    still the oracle's (and the bound holds at ordinary r too)."""
+    k = HI.kappa_for_r(d, r)
+    X, Y = HI.make_pair(HI.PairSpec(n_x, n_y, d, k, k, 30.0, seed=int(r * 1e4) + d + n_x))
+    check_certified(hap, ctx, orc, X, Y, 2000, s=5)
+
+
+@pytest.mark.parametrize("d", [48, 768])
+@pytest.mark.parametrize("n_x,n_y,ndx,ndy", [(3, 40, 1, 8), (5, 5, 2, 2), (64, 64, 4, 16),
+                                             (300, 200, 8, 8), (12, 12, 1, 12)])
+def test_duplicated_rows(hap, ctx, orc, d, n_x, n_y, ndx, ndy):
+    """Clouds with duplicated rows (identical contexts give identical embeddings): 70 % of
+    each cloud's rows are copies of a few distinct ones, so some permuted groups - and with
+    n_distinct = 1 the observed X itself - consist of identical vectors (r = 1 exactly)."""
+    X, Y = HI.duplicated_pair(HI.PairSpec(n_x, n_y, d, HI.kappa_for(d), HI.kappa_for(d), 30.0,
+                                          seed=77 + n_x), n_distinct_x=ndx, n_distinct_y=ndy, frac=0.7)
+    check_certified(hap, ctx, orc, X, Y, 1500, s=4)
 
 
 def test_naive_mode(ctx, orc):
@@ -492,6 +612,24 @@ def test_exhaustive_worked_example_exact(ctx):
     assert g["exceed_ge"] == int(vals["exhaustive_ge"][0])
     assert abs(g["exceed_abs"] - int(vals["exhaustive_abs"][0])) <= g["flagged"]
     assert g["p_exact"] == 12 / 70
+
+
+def test_exhaustive_flagged_exact_ties(ctx, orc):
+    """The flagged counter on the tie-structured pool of tests/tiecase.py: over all C(10, 5)
+    splits exactly prod C(m_k, c_k) + prod C(m_k, m_k - c_k) = 72 are near-ties (pinned by
+    combinatorics in test_oracle.py::test_flagged_counter_exact_ties); the GPU flags the same
+    72 and its counts agree with the oracle's up to them."""
+    import tiecase
+    X, Y, order = tiecase.pool()
+    want = tiecase.expected_flagged(order)[0]
+    total = math.comb(10, 5)
+    g = ctx.permtest_pair(_cuda(X), _cuda(Y), total, SEED, mode=1, exhaustive=True)
+    assert g["flagged"] == want
+    ref = orc.run_pair(X, Y, 10, SEED, mode=1)
+    counts, _ = orc.exhaustive(ref["Z"], 5, ref["t_obs"], ref["tau"])
+    assert int(counts[2]) == want
+    for k, c in (("exceed_ge", counts[0]), ("exceed_abs", counts[1])):
+        assert abs(g[k] - int(c)) <= want
 
 
 @pytest.mark.parametrize("n_x,n_y,d", [(5, 6, 32), (9, 9, 100), (3, 12, 768)])

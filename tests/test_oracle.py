@@ -86,6 +86,40 @@ def test_permspec_lemire_rejection_path(orc):
     assert tot > 0
 
 
+def _rejection_rows():
+    """tests/golden/permspec_v1_rejections.txt (independent generator, see its header)."""
+    out = []
+    for row in read_golden("permspec_v1_rejections.txt"):
+        if " sha: " in row:
+            lhs, rhs = row.split(" sha: ")
+            kind = "sha"
+        else:
+            lhs, rhs = row.split(":")
+            kind = "set"
+        seed, s, b, N, n, rej = lhs.split()
+        out.append((int(seed, 16), int(s), int(b), int(N), int(n), int(rej), kind, rhs.strip()))
+    return out
+
+
+def test_permspec_side_stream_golden(orc):
+    """Sets decided by Lemire rejections (side stream (q', b, s, 1 + i), R6) and
+    the rejection counts, from an independent sparse Fisher-Yates + Philox in pure Python
+    (tests/golden/gen_permspec_rejections.py): a wrong side-stream counter word, word order
+    or threshold changes at least one of these sets."""
+    import hashlib
+    rows = _rejection_rows()
+    assert len(rows) >= 10 and all(r[5] >= 1 for r in rows)
+    for seed, s, b, N, n, rej, kind, want in rows:
+        g = orc.perm_set(seed, s, b, N, n)
+        members = np.nonzero(g)[0].tolist()
+        assert len(members) == n
+        if kind == "sha":
+            assert hashlib.sha256(" ".join(map(str, members)).encode()).hexdigest() == want
+        else:
+            assert members == [int(x) for x in want.split()], (s, b, N, n)
+        assert orc.perm_set_redraws(seed, s, b, N, n) == rej, (s, b, N, n)
+
+
 # ---------------------------------------------------------------- SPEC worked numbers
 def test_normalize_and_2d_axis(orc):
     """SPEC.md:48-50 (3,4)->(0.6,0.8); SPEC.md:68 axis (0.70711,-0.70711) and
@@ -301,6 +335,43 @@ def test_counts_accumulate_over_shards(orc):
              for b0, b1 in [(0, 100), (100, 350), (350, 600)]]
     for k in ("exceed_ge", "exceed_abs", "flagged"):
         assert full[k] == sum(p[k] for p in parts)
+
+
+def test_flagged_counter_exact_ties(orc):
+    """Pin of the `flagged` counter (R8) by combinatorics alone (tests/tiecase.py):
+    a pool of 4 distinct rows with multiplicities (3, 2, 2, 3); the splits that reproduce the
+    observed count vector tie T_obs and those with the mirrored vector tie -T_obs, so the
+    exhaustive enumeration flags exactly prod C(m_k, c_k) + prod C(m_k, m_k - c_k) splits.
+    Every other count vector is checked to lie far outside the tie band, so a flag that
+    misses a boundary, double counts, or uses the wrong tau changes the number."""
+    import tiecase
+    X, Y, order = tiecase.pool()
+    ref = orc.run_pair(X, Y, 10, SEED, mode=1)
+    want, c_obs, mirror = tiecase.expected_flagged(order)
+    # separation: every other count vector's T (one representative split each) is far
+    # from both boundaries, so the tie band cannot catch it
+    N = len(order)
+    for c, mult in tiecase.count_vectors():
+        if c in (c_obs, mirror):
+            continue
+        members, need = [], list(c)
+        for i in range(N):
+            if need[order[i]] > 0:
+                members.append(i)
+                need[order[i]] -= 1
+        g = np.zeros(N, np.uint8)
+        g[members] = 1
+        T = orc.group_stats(ref["Z"], 5, g)["T"]
+        assert abs(T - ref["t_obs"]) > 1e3 * ref["tau"] and abs(abs(T) - abs(ref["t_obs"])) > 1e3 * ref["tau"]
+    assert sum(m for _, m in tiecase.count_vectors()) == math.comb(N, 5)
+    counts, total = orc.exhaustive(ref["Z"], 5, ref["t_obs"], ref["tau"])
+    assert total == math.comb(N, 5)
+    assert int(counts[2]) == want, (int(counts[2]), want)
+    # and by Monte Carlo: flagged / B estimates want / C(N, n_x)
+    B = 20000
+    mc = orc.run_pair(X, Y, B, SEED, mode=1)
+    p = want / math.comb(N, 5)
+    assert abs(mc["flagged"] / B - p) < 5 * math.sqrt(p * (1 - p) / B)
 
 
 # ---------------------------------------------------------------- input generator
