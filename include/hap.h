@@ -19,6 +19,12 @@
  *    returned by hap_sync().  No C++ exception crosses the ABI.  hap_last_error() gives
  *    a message for the last non-OK status of a context.
  *  - A context is bound to one device and is not thread-safe; use one per host thread.
+ *  - The alignment kernel (hap_align and the batch's alignment waves) is a cooperative grid
+ *    with a software grid barrier; two such grids sharing a device could each hold part of
+ *    the SMs and wait for the other.  Every alignment launch of the PROCESS on a device is
+ *    therefore ordered after the previous one (an event chain across all contexts and
+ *    streams): a hap_align on one stream also waits for the alignments already issued on
+ *    other streams, and the calls cannot be captured into a CUDA graph.
  *  - Requires sm_100 (B200).  There is no CPU fallback: hap_create fails with
  *    HAP_E_UNSUPPORTED_ARCH elsewhere.
  */
@@ -182,6 +188,10 @@ HAP_API hap_status hap_permtest_batch(hap_ctx ctx, int64_t P, const float* X_pac
 
 /* p = (1 + c)/(B + 1)  (Eq. pvalue). */
 HAP_API double hap_pvalue(uint64_t exceed, uint64_t B);
+/* Exact p-value of an exhaustive enumeration (HAP_FLAG_EXHAUSTIVE over all `total` =
+ * C(N, n_x) splits, the observed one included): p = c / total.
+ * NaN when total = 0. */
+HAP_API double hap_p_exact(uint64_t exceed, uint64_t total);
 
 /* ---- live profiling (bench.py) ---------------------------------------------------- */
 /* Phases of the hot path, for per-kernel timing and launch counting. */
@@ -202,16 +212,6 @@ HAP_API hap_status hap_profile(hap_ctx ctx, int enable);
  * is enabled).  reset != 0 clears both. */
 HAP_API hap_status hap_profile_read(hap_ctx ctx, double* ms, int64_t* launches, int reset);
 
-/* enable >= 3: K1 records a timestamp after each of its 7 phases; this returns the phase
- * durations (us, [host] double[7]) of the last hap_align (synchronises the device). */
-HAP_API hap_status hap_profile_k1_phases(hap_ctx ctx, double* us);
-/* Development aid: with HAP_K3_EXPERIMENT bit 16 set in the environment, K3 records
- * globaltimer stamps [sm_count][8 units][8 events]; copies up to n int64 into out [host]. */
-HAP_API hap_status hap_debug_k3_stamps(hap_ctx ctx, long long* out, int64_t n);
-/* Debug (profiling level 3): raw K1 timestamps, [8] kernel phases of CTA 0 then [grid][8]
- * per-CTA events (entry, P1 done, barrier 1 passed, P2 done, P3 done, P4 coefficients done,
- * P4 done, exit); out holds n int64 (at most 8 + 8 * SM count are written). */
-HAP_API hap_status hap_debug_k1_stamps(hap_ctx ctx, long long* out, int64_t n);
 /* Timeline of the launches timed since the last read/reset (profiling on): out [host]
  * max_n * 3 doubles {phase, start_us, end_us} relative to the first recorded launch, in
  * record order; *n receives the count.  Consumes the records (like hap_profile_read). */
@@ -238,9 +238,6 @@ HAP_API hap_status hap_perm_sets(hap_ctx ctx, uint64_t seed, uint32_t stream_id,
  * b_begin + count <= C(N, n_x) < 2^32. */
 HAP_API hap_status hap_comb_sets(hap_ctx ctx, uint64_t b_begin, int64_t count, int64_t N, int64_t n_x,
                                  uint8_t* out, void* stream);
-/* Development aid (scheduling experiments only): enqueue a register-only Philox loop of
- * `iters` rounds on ctas x threads threads, no shared memory. */
-HAP_API hap_status hap_debug_alu_burn(hap_ctx ctx, uint32_t iters, int ctas, int threads, void* stream);
 /* C(N, k) as uint64 (0 when it exceeds 2^64 - 1 or k > N). */
 HAP_API uint64_t hap_n_choose_k(int64_t N, int64_t k);
 /* Copy out the pooled workspace of the last hap_align: zhi, zlo [device] d_pad*n_pad

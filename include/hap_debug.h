@@ -1,0 +1,32 @@
+/*
+ * hap_debug.h — development aids of libhap.so (profiling experiments, not part of the
+ * hot-path boundary of include/hap.h).  Same conventions as hap.h.
+ */
+#ifndef HAP_DEBUG_H
+#define HAP_DEBUG_H
+
+#include "hap.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* enable >= 3 in hap_profile: K1 records a timestamp after each of its phases; this returns
+ * the phase durations (us, [host] double[7]) of the last hap_align (synchronises). */
+HAP_API hap_status hap_profile_k1_phases(hap_ctx ctx, double* us);
+/* Development build only (-DHAP_EXPERIMENTS, HAP_K3_EXPERIMENT bit 16 in the environment):
+ * K3 globaltimer stamps [sm_count][8 units][8 events]; copies up to n int64 into out [host].
+ * HAP_E_INVALID_ARG when none were recorded. */
+HAP_API hap_status hap_debug_k3_stamps(hap_ctx ctx, long long* out, int64_t n);
+/* Profiling level 3: raw K1 timestamps, [8] kernel phases of CTA 0 then [grid][8] per-CTA
+ * events (entry, P1 done, barrier passed, -, P3 done, P4 coefficients done, P4 done, exit);
+ * out holds n int64 (at most 8 + 8 * SM count are written). */
+HAP_API hap_status hap_debug_k1_stamps(hap_ctx ctx, long long* out, int64_t n);
+/* Scheduling experiments: enqueue a register-only Philox loop of `iters` rounds on
+ * ctas x threads threads, no shared memory. */
+HAP_API hap_status hap_debug_alu_burn(hap_ctx ctx, uint32_t iters, int ctas, int threads, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HAP_DEBUG_H */

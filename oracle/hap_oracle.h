@@ -10,11 +10,14 @@
  * cites a line of the paper's LaTeX source, "SPEC.md:L" the third-party spec,
  * "SURVEY.md §8c" the PERM-SPEC v1 reading recorded in DESIGN.md.
  *
- * Pins (tests/test_oracle_*.py): Random123 KATs (philox), SURVEY golden sets
- * (perm_set), FY chi^2 uniformity, Householder identities + App. D closed form
- * (align), SPEC worked numbers + brute-force exhaustive enumeration (stats,
- * exhaustive), MC-vs-exhaustive within 3 SE (permtest).  No function is
- * "parity unpinned".
+ * Pins (tests/test_oracle.py): Random123 KATs (philox), SURVEY golden sets (perm_set,
+ * main stream) and sets decided by Lemire rejections from an independent pure-Python
+ * generator, with their rejection counts (perm_set side stream, the redraw count;
+ * tests/golden/gen_permspec_rejections.py), FY chi^2 uniformity, Householder identities +
+ * App. D closed form (align), SPEC worked numbers + brute-force exhaustive enumeration
+ * (stats, exhaustive), MC-vs-exhaustive within 3 SE (permtest), and the near-tie counter
+ * on a pool whose ties are fixed by combinatorics (tally's `flagged`, tests/tiecase.py).
+ * No function is "parity unpinned".
  */
 #ifndef HAP_ORACLE_H
 #define HAP_ORACLE_H

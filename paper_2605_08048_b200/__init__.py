@@ -85,6 +85,7 @@ def lib() -> ctypes.CDLL:
         "hap_permtest_batch": ([vp, i64, vp, P(i64), vp, P(i64), i64, i32, P(hap_perm_cfg),
                                 P(i64), i64, vp, vp, vp], i32),
         "hap_pvalue": ([u64, u64], f64),
+        "hap_p_exact": ([u64, u64], f64),
         "hap_perm_sets": ([vp, u64, u32, u64, i64, i64, i64, vp, vp], i32),
         "hap_export_pooled": ([vp, vp, vp, vp, vp, vp], i32),
         "hap_profile": ([vp, i32], i32),
@@ -96,6 +97,8 @@ def lib() -> ctypes.CDLL:
         "hap_profile_spans_read": ([vp, P(f64), i64, P(i64)], i32),
         "hap_profile_timeline": ([vp, P(f64), i64, P(i64)], i32),
         "hap_profile_k1_phases": ([vp, P(f64)], i32),
+        "hap_debug_k3_stamps": ([vp, vp, i64], i32),
+        "hap_debug_k1_stamps": ([vp, vp, i64], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -200,6 +203,10 @@ def hap_permtest_batch(ctx, X_packed, cu_nx, Y_packed, cu_ny, mode: int, cfg: ha
 
 def hap_pvalue(exceed: int, B: int) -> float:
     return lib().hap_pvalue(int(exceed), int(B))
+
+
+def hap_p_exact(exceed: int, total: int) -> float:
+    return lib().hap_p_exact(int(exceed), int(total))
 
 
 def hap_perm_sets(ctx, seed: int, stream_id: int, b_begin: int, count: int, N: int, n_x: int,
@@ -332,8 +339,8 @@ class Context:
                    flagged=c[2], B=B, p_value=hap_pvalue(c[0], B),
                    p_two_sided=hap_pvalue(c[1], B))
         if exhaustive:
-            out["p_exact"] = c[0] / B
-            out["p_exact_two_sided"] = c[1] / B
+            out["p_exact"] = hap_p_exact(c[0], B)
+            out["p_exact_two_sided"] = hap_p_exact(c[1], B)
         if want_stats:
             out["stats"] = stats
         return out
@@ -356,7 +363,9 @@ class Context:
                            pair_sel)
         if not sync:
             return infos, counts
-        hap_sync(self.h)
+        st = hap_sync(self.h)
+        if st != HAP_OK:  # an asynchronous CUDA error: no count can be trusted
+            raise HapError(st, hap_last_error(self.h))
         raw = infos.cpu().numpy()
         cts = counts.cpu().tolist()
         sel = set(range(P)) if pair_sel is None else set(int(p) for p in pair_sel)
@@ -367,8 +376,10 @@ class Context:
                 continue
             info = hap_align_info.from_buffer_copy(bytes(raw[p].tobytes()))
             c = cts[p]
+            ok = info.status == HAP_OK  # a pair whose data failed has no p-value
             out.append(dict(status=info.status, t_obs=info.t_obs, r_x=info.r_x, r_y=info.r_y,
                             gemm_t_obs=info.gemm_t_obs, is_identity=bool(info.is_identity),
                             exceed_ge=c[0], exceed_abs=c[1], flagged=c[2], B=B,
-                            p_value=hap_pvalue(c[0], B), p_two_sided=hap_pvalue(c[1], B)))
+                            p_value=hap_pvalue(c[0], B) if ok else None,
+                            p_two_sided=hap_pvalue(c[1], B) if ok else None))
         return out

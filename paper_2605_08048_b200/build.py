@@ -22,7 +22,7 @@ def _stale() -> bool:
         return True
     t = os.path.getmtime(LIB)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
-    deps.append(os.path.join(os.path.dirname(PKG), "include", "hap.h"))
+    deps += [os.path.join(os.path.dirname(PKG), "include", h) for h in ("hap.h", "hap_debug.h")]
     return any(os.path.getmtime(p) > t for p in deps)
 
 

@@ -108,7 +108,11 @@ hap_status ensure(hap_ctx c, int which, size_t bytes) {
         cudaGetLastError();
         return fail(c, HAP_E_OOM, std::string("cudaMalloc failed: ") + cudaGetErrorString(e));
     }
-    cudaMemset(c->buf[which], 0, alloc);
+    // zero it and wait: the consumers run on non-blocking streams (lanes, generator, copies),
+    // which the legacy-stream memset does not order (allocation is a slow path anyway)
+    e = cudaMemset(c->buf[which], 0, alloc);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return fail(c, HAP_E_CUDA, std::string("workspace zeroing: ") + cudaGetErrorString(e));
     c->cap[which] = alloc;
     return HAP_OK;
 }
@@ -178,13 +182,33 @@ hap_status refresh_maps(hap_ctx c, int pair_mode) {
     return HAP_OK;
 }
 
+// dynamic piece claiming (default): CTA pairs that start late beside the other lane's
+// kernels take fewer pieces (C2 bench +2.7 %, C4 +3.6 % vs the static split);
+// HAP_K3_DYNAMIC=0 restores the static balanced split (scheduling knob, same results)
+int k3_dynamic() {
+    static const char* dy = getenv("HAP_K3_DYNAMIC");
+    return dy ? atoi(dy) : 1;
+}
+// dynamic mode piece width (HAP_K3_PIECE_COLS, scheduling knob; 256 = one accumulator chunk)
+int64_t k3_piece_cols() {
+    static const char* pw = getenv("HAP_K3_PIECE_COLS");
+    return pw ? std::max<int64_t>(32, atoi(pw)) : kChunkN;
+}
+// partial slots per tile: one per piece (dynamic: d_pad / piece width; static: pieces are cut
+// at multiples of 32 columns)
+int64_t part_slots(hap_ctx, int64_t d_pad) {
+    return std::max<int64_t>(1, ceil_div(d_pad, k3_dynamic() ? k3_piece_cols() : 32));
+}
+
 GemmArgs gemm_args(hap_ctx c) {
     GemmArgs g{};
     g.d_pad = (int)c->d_pad;
     g.d = (int)c->d;
     g.tie_rel = 1e-6;
-    // HAP_K3_EXPERIMENT: development switches; bits 1, 2, 4, 8 skip work (timing only, the
-    // counts are then invalid), bit 16 records per-unit timestamps
+#ifdef HAP_EXPERIMENTS
+    // development build only (-DHAP_EXPERIMENTS): HAP_K3_EXPERIMENT bits 1, 2, 4, 8 skip
+    // mask-GEMM work (timing only, the counts are then invalid), bit 16 records per-unit
+    // timestamps; the release library has no such switch
     static const char* ex = getenv("HAP_K3_EXPERIMENT");
     g.exp = ex ? atoi(ex) : 0;
     static bool warned = false;
@@ -193,11 +217,10 @@ GemmArgs gemm_args(hap_ctx c) {
                 g.exp);
         warned = true;
     }
-    // dynamic piece claiming (default): CTA pairs that start late beside the other lane's
-    // kernels take fewer pieces (C2 bench +2.7 %, C4 +3.6 % vs the static split);
-    // HAP_K3_DYNAMIC=0 restores the static balanced split
-    static const char* dy = getenv("HAP_K3_DYNAMIC");
-    g.dyn = dy ? atoi(dy) : 1;
+#else
+    g.exp = 0;
+#endif
+    g.dyn = k3_dynamic();
     g.claim = nullptr;
     if (g.dyn && ensure(c, kClaim, 64) == HAP_OK) g.claim = B<int>(c, kClaim);
     if (!g.claim) g.dyn = 0;
@@ -285,8 +308,7 @@ hap_status get_schedule(hap_ctx c, const GemmArgs& w, int np, cudaStream_t st, G
     auto cost = [](int64_t wd, int64_t nkb) { return (double)nkb * std::max(4.0 * (double)wd, kPieceFloor); };
     if (w.dyn) {  // dynamic: every chunk is a piece, claimed in (test, tile, column) order
         std::vector<int> npc(nt_all, 0), pcs;
-        static const char* pw = getenv("HAP_K3_PIECE_COLS");  // EXPERIMENT: piece width
-        const int64_t pwidth = pw ? std::max<int64_t>(32, atoi(pw)) : kChunkN;
+        const int64_t pwidth = k3_piece_cols();
         for (const Chunk& ch : chunks)
             for (int64_t o = 0; o < ch.width; o += pwidth)
                 pcs.insert(pcs.end(), {(int)ch.tile, (int)(ch.c0 + o), (int)std::min<int64_t>(pwidth, ch.width - o),
@@ -408,6 +430,7 @@ hap_status get_schedule(hap_ctx c, const GemmArgs& w, int np, cudaStream_t st, G
 // with TMA and is not DRAM-bound, so they need not stay in L2.  A worker holds two such
 // blocks (2 GB) only when a test's masks are that large.
 constexpr int64_t kMaskBudget = 1024ll << 20;
+constexpr int64_t kMaxBlockTiles = 4096;
 
 cudaEvent_t take_event(hap_ctx c) {
     if (!c->pool.empty()) {
@@ -572,6 +595,10 @@ hap_status hap_sync(hap_ctx c) {
 
 double hap_pvalue(uint64_t exceed, uint64_t Bn) { return (1.0 + (double)exceed) / ((double)Bn + 1.0); }
 
+double hap_p_exact(uint64_t exceed, uint64_t total) {
+    return total ? (double)exceed / (double)total : __builtin_nan("");
+}
+
 }  // extern "C"
 
 namespace {
@@ -581,9 +608,13 @@ namespace {
 // Grow-only workspace for pairs of up to N pooled rows in d dimensions and waves of up to
 // `tiles` mask tiles of R rows (owner buffers included): allocating (and zeroing) buffers
 // synchronises, so the batch reserves every workspace before its first launch.
-hap_status reserve_pair(hap_ctx c, int64_t N, int64_t d, int64_t tiles, int64_t R) {
+hap_status reserve_pair(hap_ctx c, int64_t N, int64_t d, int64_t tiles, int64_t R, bool owner) {
     const int64_t n_pad = round_up(N, kKBlock), d_pad = round_up(d, 32);
     hap_status s;
+    if (owner &&  // only a wave's owner (its first workspace) holds the launch's piece partials
+        ((s = ensure(c, kGemmPart, (size_t)kMaxWave * tiles * part_slots(c, d_pad) * R * sizeof(float2))) ||
+         (s = ensure(c, kTileDone, (size_t)kMaxWave * tiles * sizeof(unsigned)))))
+        return s;
     if ((s = ensure(c, kXbar, d * 8)) || (s = ensure(c, kYbar, d * 8)) ||
         (s = ensure(c, kInv, N * 8)) || (s = ensure(c, kU, d_pad * 8)) ||
         (s = ensure(c, kZhi, (size_t)zt_rows(d_pad) * n_pad * 2)) ||
@@ -593,9 +624,6 @@ hap_status reserve_pair(hap_ctx c, int64_t N, int64_t d, int64_t tiles, int64_t 
         (s = ensure(c, kM, d_pad * 8)) || (s = ensure(c, kSconst, 32)) ||
         (s = ensure(c, kMask, (size_t)std::max<int64_t>(2, tiles) * R * n_pad * 2)) ||
         (s = ensure(c, kMask1, (size_t)std::max<int64_t>(2, tiles) * R * n_pad * 2)) ||
-        (s = ensure(c, kGemmPart, (size_t)kMaxWave * tiles * std::max<int64_t>(1, ceil_div(d_pad, 32)) * R *
-                                      sizeof(float2))) ||
-        (s = ensure(c, kTileDone, (size_t)kMaxWave * tiles * sizeof(unsigned))) ||
         (s = reserve_schedule(c)))
         return s;
     return HAP_OK;
@@ -815,8 +843,7 @@ hap_status plan_wave(hap_ctx owner, int G, const WaveTest* T, int pair, bool sha
     g.ntiles = (int)tiles;
     g.npairs = P.npairs;
     {  // dynamic mode: every piece (a chunk, or HAP_K3_PIECE_COLS columns of it)
-        static const char* pw = getenv("HAP_K3_PIECE_COLS");
-        const int64_t pwidth = pw ? std::max<int64_t>(32, atoi(pw)) : kChunkN;
+        const int64_t pwidth = k3_piece_cols();
         int64_t per_tile = 0;
         for (int64_t c0 = 0; c0 < owner->d_pad; c0 += kChunkN)
             per_tile += ceil_div(std::min<int64_t>(kChunkN, owner->d_pad - c0), pwidth);
@@ -825,8 +852,7 @@ hap_status plan_wave(hap_ctx owner, int G, const WaveTest* T, int pair, bool sha
         // pairs as it has pieces (less setup and teardown for C1-sized tests)
         if (g.dyn && g.npieces < P.npairs) P.npairs = g.npairs = std::max(1, g.npieces);
     }
-    if ((s = ensure(owner, kGemmPart, (size_t)tiles * std::max<int64_t>(1, ceil_div(owner->d_pad, 32)) * R *
-                                          sizeof(float2))) ||
+    if ((s = ensure(owner, kGemmPart, (size_t)tiles * part_slots(owner, owner->d_pad) * R * sizeof(float2))) ||
         (s = ensure(owner, kTileDone, (size_t)tiles * sizeof(unsigned))))
         return s;
     g.part = B<float2>(owner, kGemmPart);
@@ -927,7 +953,9 @@ hap_status check_cfg(hap_ctx c, const hap_perm_cfg* cfg) {
 int64_t block_tiles(const hap_perm_cfg* cfg, int64_t n_pad, int64_t R) {
     static const char* mb = getenv("HAP_MASK_BUDGET_MB");  // EXPERIMENT: block size
     const int64_t budget = mb ? (int64_t)atoi(mb) << 20 : kMaskBudget;
-    int64_t t = std::max<int64_t>(1, budget / (R * n_pad * 2));
+    // at most kMaxBlockTiles tiles (~10^6 permutations) per launch: small pools would
+    // otherwise fill the byte budget with tens of thousands of tiles per workspace
+    int64_t t = std::max<int64_t>(1, std::min<int64_t>(kMaxBlockTiles, budget / (R * n_pad * 2)));
     if (cfg->block) t = std::max<int64_t>(1, ceil_div((int64_t)cfg->block, R - 1));
     return t;
 }
@@ -986,9 +1014,12 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
         return fail(c, HAP_E_INVALID_ARG, "X_packed and Y_packed must both be device or both host memory");
     const int64_t n = pair_sel ? n_sel : P;
     // shape checks are synchronous: validate every selected pair before enqueuing anything
+    std::vector<char> seen(pair_sel ? (size_t)P : 0, 0);
     for (int64_t i = 0; i < n; ++i) {
         const int64_t p = pair_sel ? pair_sel[i] : i;
         if (p < 0 || p >= P) return fail(c, HAP_E_INVALID_ARG, "pair_sel out of range");
+        if (pair_sel && seen[(size_t)p]++)  // a repeated pair would add its counts twice
+            return fail(c, HAP_E_INVALID_ARG, "pair_sel lists pair " + std::to_string(p) + " twice");
         const int64_t nx = cu_nx[p + 1] - cu_nx[p], ny = cu_ny[p + 1] - cu_ny[p];
         if (nx < 1 || ny < 1 || nx + ny > 65535)
             return fail(c, HAP_E_INVALID_ARG, "pair " + std::to_string(p) + ": bad n_x / n_y");
@@ -1041,7 +1072,7 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
                                            block_tiles(cfg, n_pad, R));
             for (int k = 0; k < nlanes && !s; ++k)
                 for (int j = 0; j < wave_max && !s; ++j) {
-                    s = reserve_pair(c->sub[k][j], maxN, d, tiles, R);
+                    s = reserve_pair(c->sub[k][j], maxN, d, tiles, R, j == 0);
                     for (int b = 0; b < 2 && host_in; ++b) {
                         if (!s) s = ensure(c->sub[k][j], b ? kX2 : kX, (size_t)maxnx * d * 4);
                         if (!s) s = ensure(c->sub[k][j], b ? kY2 : kY, (size_t)maxny * d * 4);

@@ -6,6 +6,7 @@
 #include <cstdint>
 
 #include "../../include/hap.h"
+#include "../../include/hap_debug.h"
 
 namespace hap {
 

@@ -58,6 +58,14 @@ struct Cfg {
 };
 
 
+// timing-only switches exist only in the development build (-DHAP_EXPERIMENTS); in the
+// release library they are the constant 0 and the skipped-work paths are compiled out
+#ifdef HAP_EXPERIMENTS
+#define K3_EXP(g) ((g).exp)
+#else
+#define K3_EXP(g) 0
+#endif
+
 __device__ __forceinline__ long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -66,7 +74,7 @@ __device__ __forceinline__ long long gtimer() {
 // EXPERIMENT (exp bit 16): per (CTA, local unit i, event) timestamps
 #define K3_STAMP(i, ev)                                                                      \
     do {                                                                                     \
-        if ((g.exp & 16) && g.stamps && (i) < 8)                                             \
+        if ((K3_EXP(g) & 16) && g.stamps && (i) < 8)                                             \
             g.stamps[((size_t)blockIdx.x * 8 + (i)) * 8 + (ev)] = gtimer();                  \
     } while (0)
 
@@ -364,13 +372,13 @@ __global__ void __maxnreg__(HAP_K3_MAXNREG)
                         uint8_t* sA = smem + stage * C::kStageBytes;
                         if constexpr (kPair == 2) {
                             // EXPERIMENT (timing only): bit0 skips A loads, bit1 skips B lo loads
-                            const uint32_t bytes = (uint32_t)C::kStageBytes - ((g.exp & 1) ? kStageA : 0) -
-                                                   ((g.exp & 2) ? C::kStageB : 0);
+                            const uint32_t bytes = (uint32_t)C::kStageBytes - ((K3_EXP(g) & 1) ? kStageA : 0) -
+                                                   ((K3_EXP(g) & 2) ? C::kStageB : 0);
                             if (leader) mbar_arrive_expect_tx(&full[stage], 2u * bytes);
                             const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
-                            if (!(g.exp & 1)) tma_load_2d_pair(tmA, fb, sA, kb * kKBlock, arow);
+                            if (!(K3_EXP(g) & 1)) tma_load_2d_pair(tmA, fb, sA, kb * kKBlock, arow);
                             tma_load_2d_pair(tmBhi, fb, sA + kStageA, kb * kKBlock, brow);
-                            if (!(g.exp & 2))
+                            if (!(K3_EXP(g) & 2))
                                 tma_load_2d_pair(tmBlo, fb, sA + kStageA + C::kStageB, kb * kKBlock, brow);
                         } else {
                             mbar_arrive_expect_tx(&full[stage], (uint32_t)C::kStageBytes);
@@ -422,7 +430,7 @@ __global__ void __maxnreg__(HAP_K3_MAXNREG)
                         const uint64_t ld = smem_desc_k_sw128(lBase + 32u * k);
                         if constexpr (kPair == 2) {
                             umma_bf16_ss_pair(dtm, ad, hd, idesc, (kb | k) != 0 ? 1u : 0u);
-                            if (!(g.exp & 4)) umma_bf16_ss_pair(dtm, ad, ld, idesc, 1u);
+                            if (!(K3_EXP(g) & 4)) umma_bf16_ss_pair(dtm, ad, ld, idesc, 1u);
                         } else {
                             umma_bf16_ss(dtm, ad, hd, idesc, (kb | k) != 0 ? 1u : 0u);
                             umma_bf16_ss(dtm, ad, ld, idesc, 1u);
@@ -468,7 +476,7 @@ __global__ void __maxnreg__(HAP_K3_MAXNREG)
             float s1 = 0.f, s2 = 0.f;
             const float4* abp = reinterpret_cast<const float4*>(T.ab + pd.y);
             const uint32_t tbase = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(a * kChunkN);
-            const int nblk = (g.exp & 8) ? 0 : width / 32;
+            const int nblk = (K3_EXP(g) & 8) ? 0 : width / 32;
             for (int cb = 0; cb < nblk; cb += 2) {  // two 32-column loads in flight per wait
                 uint32_t r[2][32];
                 tmem_ld_32x32b_x32(tbase + (uint32_t)(32 * cb), r[0]);

@@ -10,6 +10,8 @@ import pytest
 from conftest import ROOT
 
 HEADER = os.path.join(ROOT, "include", "hap.h")
+HEADERS = sorted(os.path.join(ROOT, "include", f) for f in os.listdir(os.path.join(ROOT, "include"))
+                 if f.endswith(".h"))
 
 
 @pytest.fixture(scope="module")
@@ -21,7 +23,7 @@ def libhap():
 
 
 def declared_functions():
-    src = open(HEADER).read()
+    src = "\n".join(open(h).read() for h in HEADERS)
     return sorted(set(re.findall(r"^HAP_API\s+[\w\s\*]+?\b(hap_\w+)\s*\(", src, flags=re.M)))
 
 

@@ -451,7 +451,7 @@ def test_batch_pair_sel_and_data_errors(hap, ctx, orc):
     res = ctx.permtest_batch(_cuda(Xp), cnx, _cuda(Yp), cny, 300, SEED, stream_id=3,
                              pair_sel=sel)
     assert res[1] is None and res[3] is None
-    assert res[2]["status"] == 3 and res[2]["exceed_ge"] == 0
+    assert res[2]["status"] == 3 and res[2]["exceed_ge"] == 0 and res[2]["p_value"] is None
     _batch_vs_oracle(orc, res, Xp, cnx, Yp, cny, 300, 3, [4, 0])
     infos, counts = ctx.permtest_batch(_cuda(Xp), cnx, _cuda(Yp), cny, 300, SEED,
                                        pair_sel=sel, sync=False)
@@ -839,6 +839,8 @@ def test_batch_argument_errors(hap, ctx):
         hap.hap_permtest_batch(ctx.h, X, cnx, Y, cny, 7, ok, infos, counts)
     with pytest.raises(hap.HapError):  # pair_sel out of range
         hap.hap_permtest_batch(ctx.h, X, cnx, Y, cny, 0, ok, infos, counts, pair_sel=[0, 5])
+    with pytest.raises(hap.HapError):  # a pair listed twice would add its counts twice
+        hap.hap_permtest_batch(ctx.h, X, cnx, Y, cny, 0, ok, infos, counts, pair_sel=[1, 0, 1])
     with pytest.raises(hap.HapError):  # one input in host memory, the other on the device
         hap.hap_permtest_batch(ctx.h, torch.from_numpy(Xp), cnx, Y, cny, 0, ok, infos, counts)
     with pytest.raises(hap.HapError):  # b_end beyond 2^32

@@ -45,7 +45,7 @@ for c0 in range(0, R, chunk):
         e1.record()
         e1.synchronize()
         gpu_s += e0.elapsed_time(e1) / 1e3
-        pv[mode] += [(1 + int(c)) / (B + 1) for c in counts[:, 0].cpu().tolist()]
+        pv[mode] += [hap.hap_pvalue(int(c), B) for c in counts[:, 0].cpu().tolist()]
 out = {"workload": f"C5: {R} null replicates, n_x = n_y = {n}, d = {d}, B = {B}, "
                    f"kappa(r=0.75) both, mean directions {theta} deg apart"
                    + (", anisotropic noise (SURVEY App. B)" if aniso else ""),
