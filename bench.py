@@ -1,21 +1,28 @@
 #!/usr/bin/env python
 """bench.py — throughput of the Householder-aligned permutation test hot path on B200.
 
-A "step" is one whole word-pair test of BASELINE.json configs[1] (C2: n_x = n_y = 1000
-unit vectors, d = 768, B = 10^4 permutations): S1-S6 (alignment: normalise, means,
-Householder reflect, pool/split, T_obs) + S7-S9 (PERM-SPEC v1 masks, tcgen05 mask-GEMM,
-statistic, exceedance counts) on inputs resident in HBM, run through the public batch
-entry point hap_permtest_batch (independent generator stream per test).
-metric = permuted statistics / second (whole job, all ranks).
+Workloads (BASELINE.json configs; `--workload`, default c2):
+  c2  the headline: "permuted statistics/sec (N=2k, d=768)".  A STEP is one batch of
+      --tests-per-step (100) whole word-pair tests of configs[1] (n_x = n_y = 1000, d = 768,
+      B = 10^4 permutations each: 10^6 permuted statistics) through ONE call of the public
+      batch entry point hap_permtest_batch: S1-S6 (normalise, means, Householder reflect,
+      pool/split, T_obs) + S7-S9 (PERM-SPEC v1 masks, tcgen05 mask-GEMM, statistic,
+      exceedance counts), every test on its own generator stream.  Multi-GPU: every rank
+      runs its own tests (weak scaling).
+  c3  configs[2]: one LLM-sized pair (n = 5000/5000, d = 4096, B = 10^5) per step,
+      hap_align + hap_permtest; multi-GPU: the b-range is sharded (strong scaling).
+  c4  configs[3]: the thesaurus-scale batch, 10^4 pairs of log-uniform n in [50, 5000],
+      d = 768, B = 10^4 each, one hap_permtest_batch call per rank per step; multi-GPU:
+      pairs LPT-assigned over ranks (strong scaling).  Metric: word-pair tests/sec.
+  c5  configs[4]: the Type-I calibration workload, 10^3 null replicates x {aligned,
+      naive}, n = 500/500, d = 768, B = 10^4 (2000 tests per step).  Metric: tests/sec.
+Timing: CUDA events on the launching stream, barrier + synchronize on both sides, max
+over ranks; the integer counts are combined with ONE all_reduce inside the timed region.
+Inputs of every step are larger than the 126 MB L2 (stated in `config.l2`).
 
-Multi-GPU (torchrun): word pairs are sharded over ranks (weak scaling: every rank runs
-its own tests each step); the per-test integer counts are combined with one NCCL
-all_reduce at the end of the timed region.  Timing: CUDA events on the launching
-stream, barrier + synchronize on both sides, max over ranks.  L2: each step reads a
-different pair from a rotating pool of input pairs larger than the 126 MB L2.
-
---impl reference runs the fp64 CPU oracle (oracle/, the checker) on the same workload
-as the baseline arm (rank 0 only).
+--impl reference runs the fp64 CPU oracle (oracle/, the checker) on a bounded sample of
+the same workload (rank 0 only).  bench.py refuses to run with any HAP_* environment
+variable set (library experiment knobs), and says so on its JSON line.
 """
 from __future__ import annotations
 
@@ -36,13 +43,11 @@ import numpy as np  # noqa: E402
 
 import hap_inputs as HI  # noqa: E402
 
-METRIC = "permuted statistics/sec (N=2k, d=768)"
-UNIT = "perms/s"
-CFG = HI.CONFIGS["C2"]
-N_X, N_Y, D, B = CFG["n_x"], CFG["n_y"], CFG["d"], CFG["B"]
-WORKLOAD = (f"C2 (BASELINE.json configs[1]): single word-pair test n_x=n_y={N_X}, d={D}, "
-            f"B={B} permutations; BERT-base-shaped vMF clouds kappa=1315.34 (r~0.75), "
-            f"mean directions 30 deg apart, raw norms LogNormal(ln 20, 0.1)")
+UNIT_P = "perms/s"
+UNIT_T = "tests/s"
+TESTS_PER_STEP = 100
+RECIPE = ("vMF clouds (Wood sampler) with E[MRL]=0.75 (kappa=1315.34 at d=768, 7020.48 at "
+          "d=4096), mean directions 30 deg apart, raw norms LogNormal(ln 20, 0.1)")
 
 
 def load_peaks():
@@ -54,12 +59,22 @@ def load_peaks():
             "fallback (B200_PROFILING.md)"
 
 
-def make_pool(npairs: int, rank: int):
-    pairs = []
-    for i in range(npairs):
-        spec = HI.PairSpec(N_X, N_Y, D, HI.kappa_for(D), HI.kappa_for(D), 30.0, seed=1002)
-        pairs.append(HI.make_pair(spec, rep=1000 * rank + i))
-    return pairs
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def usable_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -102,66 +117,130 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self, t0: float, t1: float):
-        rows = [p for (t, p) in self.rows if t0 - 0.25 <= t <= t1 + 0.25] or \
+        rows = [p for (t, p) in self.rows if t0 - 0.15 <= t <= t1 + 0.15] or \
             [p for (_, p) in self.rows]
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         sm = [float(p[1]) for p in rows if p[1].replace(".", "").isdigit()]
         smax = [float(p[2]) for p in rows if p[2].replace(".", "").isdigit()]
+        pw = [float(p[3]) for p in rows if p[3].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for p in rows for i in range(4) if p[5 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(smax) if smax else None, "reasons": reasons,
-                "samples": len(rows)}
+                "power_w_max": max(pw) if pw else None, "samples": len(rows)}
 
 
-# ----------------------------------------------------------------------------- arms
+# ----------------------------------------------------------------------------- workloads
+def c2_pool(npairs: int, rank: int, n_x=1000, n_y=1000, d=768, seed=1002):
+    k = HI.kappa_for(d)
+    return [HI.make_pair(HI.PairSpec(n_x, n_y, d, k, k, 30.0, seed=seed), rep=1000 * rank + i)
+            for i in range(npairs)]
+
+
+def c4_sizes():
+    c = HI.CONFIGS["C4"]
+    n = HI.c4_sizes(c["P"], c["n_min"], c["n_max"])  # n_X = n_Y = n_p
+    return n
+
+
+WORKLOADS = {
+    "c2": dict(metric="permuted statistics/sec (N=2k, d=768)", unit=UNIT_P,
+               config="C2", scaling="weak"),
+    "c3": dict(metric="permuted statistics/sec (N=10k, d=4096)", unit=UNIT_P,
+               config="C3", scaling="strong"),
+    "c4": dict(metric="word-pair tests/sec (thesaurus-scale batch)", unit=UNIT_T,
+               config="C4", scaling="strong"),
+    "c5": dict(metric="word-pair tests/sec (Type-I calibration, aligned + naive)",
+               unit=UNIT_T, config="C5", scaling="strong"),
+}
+
+
+def workload_desc(name: str, T: int) -> str:
+    c = HI.CONFIGS[WORKLOADS[name]["config"]]
+    if name == "c2":
+        return (f"C2 (BASELINE.json configs[1]): {T} word-pair tests per step, each n_x=n_y="
+                f"{c['n_x']}, d={c['d']}, B={c['B']}; {RECIPE}")
+    if name == "c3":
+        return (f"C3 (configs[2]): one pair n_x=n_y={c['n_x']}, d={c['d']}, B={c['B']} per "
+                f"step, b-range sharded over ranks; {RECIPE}")
+    if name == "c4":
+        return (f"C4 (configs[3]): {c['P']} pairs, n_x=n_y=n_p log-uniform in "
+                f"[{c['n_min']}, {c['n_max']}] (seed 1004), d={c['d']}, B={c['B']} each, pairs "
+                f"LPT-sharded over ranks; {RECIPE}")
+    return (f"C5 (configs[4]): {c['R']} null replicates x (aligned, naive), n_x=n_y={c['n_x']}, "
+            f"d={c['d']}, B={c['B']}; {RECIPE}")
+
+
+# ----------------------------------------------------------------------------- reference arm
 def run_reference(args):
-    """The oracle as it stands, on the host cores, same metric/config; rank 0 only."""
+    """The oracle as it stands, on the host cores, same metric/unit/config; rank 0 only.
+    Each step is a bounded sample of the workload (align + T_obs + the first S
+    permutations of one test), sized so that the whole run takes ~BENCH_REF_BUDGET_S."""
     import oracle
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    cores = os.cpu_count() or 1
-    pool = make_pool(min(args.pool, 4), 0)
-    # calibrate so that W + K steps take about `budget` seconds in total
+    W = WORKLOADS[args.workload]
+    cfg = HI.CONFIGS[W["config"]]
+    cores = usable_cores()
+    if args.workload == "c3":
+        pool = [HI.config_pair("C3")]
+    elif args.workload == "c4":
+        sizes = c4_sizes()[:8]
+        pool = [HI.make_pair(HI.PairSpec(int(n), int(n), 768, HI.kappa_for(768),
+                                         HI.kappa_for(768), 30.0, seed=1004), rep=p)
+                for p, n in enumerate(sizes)]
+    elif args.workload == "c5":
+        pool = c2_pool(4, 0, 500, 500, 768, seed=1005)
+    else:
+        pool = c2_pool(4, 0)
+    B = cfg["B"]
     t0 = time.perf_counter()
-    oracle.run_pair(*pool[0], 64, HI.PERM_SEED, nthreads=cores)
+    oracle.run_pair(*pool[0], B, HI.PERM_SEED, b_begin=0, b_end=64, nthreads=cores)
     rate = 64 / max(time.perf_counter() - t0, 1e-3)
-    budget = float(os.environ.get("HAP_REF_BUDGET_S", "150"))
+    budget = float(os.environ.get("BENCH_REF_BUDGET_S", "150"))
     per_step = max(0.05, min(10.0, budget / max(1, args.steps + args.warmup)))
     S = int(max(cores, min(B, rate * per_step)))
-    total_perms, total_s = 0, 0.0
+    perms, secs, test_s = 0, 0.0, 0.0
     for k in range(args.warmup + args.steps):
         X, Y = pool[k % len(pool)]
         t0 = time.perf_counter()
         oracle.run_pair(X, Y, B, HI.PERM_SEED, s=k, b_begin=0, b_end=S, nthreads=cores)
         dt = time.perf_counter() - t0
         if k >= args.warmup:
-            total_perms += S
-            total_s += dt
-    value = total_perms / total_s
-    sample = (f"each step: oracle align + T_obs + b in [0,{S}) of the B={B} permutations "
-              f"(a bounded sample of the C2 test) on {cores} threads")
-    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            perms += S
+            secs += dt
+            test_s += dt * B / S  # one whole test, extrapolated from the sample
+    if W["unit"] == UNIT_P:
+        value = perms / secs
+        sample = (f"each step: oracle align + T_obs + b in [0,{S}) of one {W['config']} test "
+                  f"(B={B}) on {cores} threads")
+    else:
+        value = args.steps / test_s
+        sample = (f"each step: oracle align + T_obs + b in [0,{S}) of one {W['config']}-shaped "
+                  f"test, time per whole test extrapolated x{B / S:.1f}; {cores} threads")
+    out = {"metric": W["metric"], "value": value, "unit": W["unit"], "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup,
-           "ms_per_step": 1e3 * total_s / args.steps, "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True,
+           "scaling": W["scaling"], "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "impl": "reference",
-           "config": {"workload": WORKLOAD, "parallelism": "rank 0 only (host cores)"},
-           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                            "sample": sample},
-           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+           "config": {"workload": workload_desc(args.workload, args.tests_per_step),
+                      "parallelism": "rank 0 only (host cores)"},
+           "cpu_baseline": {"value": value, "unit": W["unit"], "cores": cores, "kind": "oracle",
+                            "sample": sample, "cpu": cpu_model()},
+           "e2e": {"value": value, "unit": W["unit"], "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
 
-def cpu_baseline(pool):
-    """The oracle (untuned) on this box's host cores: whole C2 tests (align + T_obs + all
-    B permutations) on successive pool pairs until ~HAP_CPU_BASELINE_S seconds have run."""
+def cpu_baseline(pool, B, budget_s=12.0):
+    """The oracle (untuned) on this box's host cores: whole tests (align + T_obs + all B
+    permutations) on successive pool pairs for ~budget_s seconds, plus the same oracle on
+    ONE thread over a bounded b-range of one test."""
     import oracle
-    cores = os.cpu_count() or 1
-    budget = float(os.environ.get("HAP_CPU_BASELINE_S", "12"))
+    cores = usable_cores()
+    budget = float(os.environ.get("BENCH_CPU_BASELINE_S", str(budget_s)))
     done, t0 = 0, time.perf_counter()
     while True:
         X, Y = pool[done % len(pool)]
@@ -170,217 +249,496 @@ def cpu_baseline(pool):
         dt = time.perf_counter() - t0
         if dt >= budget or done >= 200:
             break
-    return {"value": done * B / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{done} complete C2 tests (B={B} each) on {cores} threads in {dt:.1f} s"}
+    S1 = 200
+    X, Y = pool[0]
+    t1 = time.perf_counter()
+    oracle.run_pair(X, Y, B, HI.PERM_SEED, s=0, b_begin=0, b_end=S1, nthreads=1)
+    one = S1 / (time.perf_counter() - t1)
+    return {"value": done * B / dt, "unit": UNIT_P, "cores": cores, "kind": "oracle",
+            "cpu": cpu_model(), "value_1thread": one,
+            "sample": f"{done} complete tests (B={B} each) on {cores} threads in {dt:.1f} s; "
+                      f"1-thread rate: align + b in [0,{S1}) of one test"}
+
+
+# ----------------------------------------------------------------------------- GPU arm
+class Env:
+    def __init__(self):
+        import torch
+        import torch.distributed as dist
+        import paper_2605_08048_b200 as hap
+        self.torch, self.dist, self.hap = torch, dist, hap
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(self.local)
+        self.dev = torch.device("cuda", self.local)
+        if self.world > 1:
+            dist.init_process_group("nccl", device_id=self.dev)
+        self.ctx = hap.Context(self.local)
+        self.st = torch.cuda.current_stream()
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def max_over_ranks(self, v: float) -> float:
+        if self.world == 1:
+            return v
+        t = self.torch.tensor([v], dtype=self.torch.float64, device=self.dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def timed(self, fn, K):
+        """barrier + sync; events around K calls of fn(k) on the launching stream; max over
+        ranks.  Returns (ms, wall_t0, wall_t1)."""
+        torch = self.torch
+        self.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        tw0 = time.time()
+        e0.record(self.st)
+        for k in range(K):
+            fn(k)
+        e1.record(self.st)
+        e1.synchronize()
+        tw1 = time.time()
+        torch.cuda.synchronize()
+        self.barrier()
+        return self.max_over_ranks(e0.elapsed_time(e1)), tw0, tw1
+
+
+def kernel_profile(E, run_waves, n_tests, N, d, B, peaks, what):
+    """Per-kernel device time with CUDA events on each launch's own stream (hap_profile
+    level 2: phases serialised, one wave per call and a sync after it, so no other launch
+    overlaps a timed one): K3 (dominant, tensor-bound), K1 (HBM), K2 (integer ALU).
+    Normalised per test: `n_tests` tests of N pooled rows, d columns, B permutations."""
+    hap = E.hap
+    hap.hap_profile_read(E.ctx.h, reset=True)
+    hap.hap_profile(E.ctx.h, 2)
+    run_waves()
+    phase_ms, phase_n = hap.hap_profile_read(E.ctx.h, reset=True)
+    hap.hap_profile(E.ctx.h, 0)
+    n_pad = -(-N // 64) * 64
+    d_pad = -(-d // 32) * 32
+    k3_s = phase_ms["maskgemm"] / 1e3
+    flops = 2.0 * N * d * B * n_tests  # algorithmic: the U = S X row per permutation
+    ach = flops / k3_s / 1e12 if k3_s > 0 else 0.0
+    peak = peaks["bf16_tflops"]
+    k1_s = phase_ms["align"] / 1e3
+    k1_bytes = n_tests * (4.0 * N * d + 4.0 * n_pad * d_pad)  # read X,Y fp32; write hi,lo
+    k2_s = phase_ms["permgen"] / 1e3
+    k1_gbs = k1_bytes / k1_s / 1e9 if k1_s else 0.0
+    return {
+        "bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+        "frac": ach / peak, "kernel": f"k3_maskgemm (S8+S9); {what}",
+        "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst): K3 is timed one isolated "
+                       "launch at a time (CUDA events on its stream, a sync between launches)",
+        "achieved_basis": "algorithmic 2*N*d FLOP per permutation (SURVEY.md 8d) x the "
+                          "permutations of the timed launches / their summed duration",
+        "issued_tflops": 4.0 * n_pad * d_pad * B * n_tests / k3_s / 1e12 if k3_s else 0.0,
+        "k3_us_per_launch": phase_ms["maskgemm"] * 1e3 / max(1, phase_n["maskgemm"]),
+        "launches_timed": phase_n,
+        "k1_align": {"bound": "hbm", "unit": "GB/s", "achieved": k1_gbs,
+                     "peak": peaks["hbm_gbs"], "frac": k1_gbs / peaks["hbm_gbs"],
+                     "us_per_test": k1_s * 1e6 / n_tests,
+                     "basis": "read 4*N*d (fp32 X, Y) + write 4*n_pad*d_pad (bf16 hi, lo) "
+                              "bytes per test"},
+        "k2_permgen": {"bound": "alu", "unit": "perms/s",
+                       "achieved": n_tests * B / k2_s if k2_s else 0.0,
+                       "us_per_test": k2_s * 1e6 / n_tests},
+        "phase_ms": phase_ms,
+    }
+
+
+def in_step_spans(E, run_one_step, flops, peaks):
+    """K3 inside the real pipelined step: device-clock spans (first CTA entry -> last CTA
+    exit) of every mask-GEMM launch of one step; the step's algorithmic FLOP over the time
+    in which at least one K3 launch was running, as a fraction of the SUSTAINED peak."""
+    hap = E.hap
+    hap.hap_profile_spans(E.ctx.h, 1)
+    run_one_step()
+    E.torch.cuda.synchronize()
+    spans = hap.hap_profile_spans_read(E.ctx.h)
+    hap.hap_profile_spans(E.ctx.h, 0)
+    k3 = sorted((s, e) for (ph, s, e) in spans if ph.startswith("maskgemm") and e >= s)
+    if not k3:
+        return None
+    busy, cur_s, cur_e = 0.0, k3[0][0], k3[0][1]
+    for s, e in k3[1:]:
+        if s > cur_e:
+            busy += cur_e - cur_s
+            cur_s, cur_e = s, e
+        else:
+            cur_e = max(cur_e, e)
+    busy += cur_e - cur_s
+    allsp = [(s, e) for (_, s, e) in spans if e >= s]
+    step_us = max(e for _, e in allsp) - min(s for s, _ in allsp)
+    ach = flops / (busy * 1e-6) / 1e12
+    return {"k3_launches": len(k3), "k3_busy_us": busy, "step_us": step_us,
+            "k3_busy_share": busy / step_us, "achieved": ach,
+            "peak": peaks["bf16_tflops_sustained"],
+            "frac": ach / peaks["bf16_tflops_sustained"],
+            "basis": "one step with kernel spans on; algorithmic FLOP of the step / union of "
+                     "the K3 spans (K3 shares the SMs with the other lane's K1/K2)"}
+
+
+def run_c2(args, E, peaks):
+    torch, hap = E.torch, E.hap
+    T, K, W = args.tests_per_step, args.steps, args.warmup
+    cfg0 = HI.CONFIGS["C2"]
+    n_x, n_y, d, B = cfg0["n_x"], cfg0["n_y"], cfg0["d"], cfg0["B"]
+    N = n_x + n_y
+    pool = c2_pool(args.pool, E.rank)
+    P = len(pool)
+    Xp = np.ascontiguousarray(np.concatenate([pool[i % P][0] for i in range(T)]))
+    Yp = np.ascontiguousarray(np.concatenate([pool[i % P][1] for i in range(T)]))
+    Xd, Yd = torch.from_numpy(Xp).to(E.dev), torch.from_numpy(Yp).to(E.dev)
+    cu_nx = np.arange(T + 1, dtype=np.int64) * n_x
+    cu_ny = np.arange(T + 1, dtype=np.int64) * n_y
+    in_bytes = Xp.nbytes + Yp.nbytes
+    INFO = hap.INFO_BYTES
+    infos = torch.zeros((T, INFO), dtype=torch.uint8, device=E.dev)
+    # every rank writes ITS block of one [world, K, T, 3] buffer; one all_reduce combines
+    counts = torch.zeros((E.world, K, T, 3), dtype=torch.int64, device=E.dev)
+    scratch = torch.zeros((T, 3), dtype=torch.int64, device=E.dev)
+    base = (E.rank << 27) & 0xFFFFFFFF  # generator streams: rank, step, test
+
+    def step(k, out, X=Xd, Y=Yd, n=T, wave=0):
+        cfg = hap.make_cfg(HI.PERM_SEED, B, stream_id=(base + k * T) & 0xFFFFFFFF, wave=wave)
+        hap.hap_permtest_batch(E.ctx.h, X, cu_nx[: n + 1], Y, cu_ny[: n + 1],
+                               hap.HAP_ALIGN_HOUSEHOLDER, cfg, infos, out, stream=E.st)
+
+    for k in range(W):
+        step(K + k, scratch)
+    torch.cuda.synchronize()
+    hap.hap_profile_read(E.ctx.h, reset=True)
+
+    def timed_step(k):
+        step(k, counts[E.rank, k])
+        if k == K - 1 and E.world > 1:
+            E.dist.all_reduce(counts)  # the one combine of the integer counts
+
+    ms, tw0, tw1 = E.timed(timed_step, K)
+    launches = hap.hap_profile_read(E.ctx.h, reset=True)[1]
+    value = E.world * K * T * B / (ms / 1e3)
+
+    # per-kernel rooflines (isolated waves of 3 tests)
+    wave = 3
+    nw = max(4, min(40, K * T // wave // 4))
+
+    def waves():
+        for i in range(nw):
+            scratch.zero_()
+            step(2 * K + i, scratch, wave=wave, n=wave)
+            torch.cuda.synchronize()
+    roof = kernel_profile(E, waves, nw * wave, N, d, B, peaks,
+                          f"one launch = a wave of {wave} C2 tests")
+
+    def one_step():
+        scratch.zero_()
+        step(3 * K, scratch)
+    roof["in_step"] = in_step_spans(E, one_step, 2.0 * N * d * B * T, peaks)
+
+    # end to end through the C ABI with HOST inputs: each step's packed X, Y (pinned) are
+    # copied by the library per wave on its lane streams; the counts are copied D2H
+    Ke = min(K, args.e2e_steps)
+    Xh, Yh = torch.from_numpy(Xp).pin_memory(), torch.from_numpy(Yp).pin_memory()
+    hcounts = torch.zeros((Ke, T, 3), dtype=torch.int64).pin_memory()
+    dcounts = torch.zeros((2, T, 3), dtype=torch.int64, device=E.dev)
+
+    def e2e_step(k):
+        dc = dcounts[k % 2]
+        dc.zero_()
+        step(4 * K + k, dc, X=Xh, Y=Yh)
+        hcounts[k].copy_(dc, non_blocking=True)
+
+    e2e_step(0)
+    torch.cuda.synchronize()
+    E.barrier()
+    t0 = time.perf_counter()
+    for k in range(Ke):
+        e2e_step(k)
+    torch.cuda.synchronize()
+    e2e_s = E.max_over_ranks(time.perf_counter() - t0)
+    e2e = {"value": E.world * Ke * T * B / e2e_s, "unit": UNIT_P,
+           "h2d_bytes_per_step": in_bytes, "d2h_bytes_per_step": T * 3 * 8, "steps": Ke,
+           "timer": "host wall clock around the loop, synchronize on both sides",
+           "api": "hap_permtest_batch with the step's packed X, Y in pinned HOST memory (the "
+                  "library copies each wave's rows on its lane streams); counts copied D2H"}
+    cpu = None
+    if E.rank == 0 and E.world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(pool, B)
+    cfg_out = {"workload": workload_desc("c2", T), "tests_per_step": T, "B": B, "n_x": n_x,
+               "n_y": n_y, "d": d, "global_batch": E.world * T,
+               "l2": f"each step reads {in_bytes / 1e6:.0f} MB of input pairs ({P} distinct, "
+                     "repeated in HBM) > 126 MB L2; no flush",
+               "parallelism": f"dp{E.world}: each rank runs its own {T} tests per step; "
+                              "counts combined by one all_reduce",
+               "api": "hap_permtest_batch (2 internal lanes, waves of 3 tests per alignment / "
+                      "generator / mask-GEMM launch)",
+               "arith": "bf16 hi/lo split operands, fp32 TMEM accumulation, fp64 statistic"}
+    last = int(counts[E.rank, K - 1, T - 1, 0])
+    extra = {"last_test": {"exceed_ge": last, "p_value": hap.hap_pvalue(last, B)}}
+    return value, ms, tw0, tw1, launches, roof, e2e, cpu, cfg_out, extra
+
+
+def run_c3(args, E, peaks):
+    torch, hap = E.torch, E.hap
+    from paper_2605_08048_b200 import parallel
+    c = HI.CONFIGS["C3"]
+    n_x, n_y, d, B = c["n_x"], c["n_y"], c["d"], c["B"]
+    N = n_x + n_y
+    K, W = args.steps, args.warmup
+    pool = [HI.config_pair("C3", rep=r) for r in range(2)]
+    dev_pool = [(torch.from_numpy(X).to(E.dev), torch.from_numpy(Y).to(E.dev)) for X, Y in pool]
+    b0, b1 = parallel.shard_range(B, E.rank, E.world)
+    infos = torch.zeros((2, hap.INFO_BYTES), dtype=torch.uint8, device=E.dev)
+    counts = torch.zeros((K, 3), dtype=torch.int64, device=E.dev)
+    scratch = torch.zeros(3, dtype=torch.int64, device=E.dev)
+
+    def step(k, out, X=None, Y=None):
+        Xs, Ys = dev_pool[k % 2] if X is None else (X, Y)
+        info = infos[k % 2]
+        hap.hap_align(E.ctx.h, Xs, Ys, hap.HAP_ALIGN_HOUSEHOLDER, info, stream=E.st)
+        cfg = hap.make_cfg(HI.PERM_SEED, B, b0, b1, stream_id=k)
+        hap.hap_permtest(E.ctx.h, info, cfg, out, None, stream=E.st)
+
+    for k in range(W):
+        step(k, scratch)
+    torch.cuda.synchronize()
+    hap.hap_profile_read(E.ctx.h, reset=True)
+
+    def timed_step(k):
+        step(k, counts[k])
+        if E.world > 1:
+            E.dist.all_reduce(counts[k])  # one combine per test (b-range shards)
+
+    ms, tw0, tw1 = E.timed(timed_step, K)
+    launches = hap.hap_profile_read(E.ctx.h, reset=True)[1]
+    value = K * B / (ms / 1e3)
+
+    def waves():
+        for i in range(2):
+            scratch.zero_()
+            step(i, scratch)
+            torch.cuda.synchronize()
+    roof = kernel_profile(E, waves, 2, N, d, b1 - b0, peaks,
+                          f"one test = this rank's b-range [{b0},{b1}) in L2-sized blocks")
+    Ke = min(K, 4)
+    Xh, Yh = [torch.from_numpy(X).pin_memory() for X, _ in pool], \
+        [torch.from_numpy(Y).pin_memory() for _, Y in pool]
+    hcounts = torch.zeros((Ke, 3), dtype=torch.int64).pin_memory()
+    dcounts = torch.zeros((Ke, 3), dtype=torch.int64, device=E.dev)
+    torch.cuda.synchronize()
+    E.barrier()
+    t0 = time.perf_counter()
+    for k in range(Ke):
+        step(k, dcounts[k], Xh[k % 2], Yh[k % 2])
+        if E.world > 1:
+            E.dist.all_reduce(dcounts[k])
+        hcounts[k].copy_(dcounts[k], non_blocking=True)
+    torch.cuda.synchronize()
+    e2e_s = E.max_over_ranks(time.perf_counter() - t0)
+    e2e = {"value": Ke * B / e2e_s, "unit": UNIT_P,
+           "h2d_bytes_per_step": int(pool[0][0].nbytes + pool[0][1].nbytes),
+           "d2h_bytes_per_step": 24, "steps": Ke,
+           "timer": "host wall clock around the loop, synchronize on both sides",
+           "api": "hap_align (X, Y in pinned HOST memory) + hap_permtest, counts D2H"}
+    cfg_out = {"workload": workload_desc("c3", 1), "B": B, "n_x": n_x, "n_y": n_y, "d": d,
+               "global_batch": 1,
+               "l2": "two distinct 164 MB pairs alternate (> 126 MB L2); no flush",
+               "parallelism": f"b-range sharded over {E.world} rank(s); one all_reduce of "
+                              "the 3 counts per test"}
+    return value, ms, tw0, tw1, launches, roof, e2e, None, cfg_out, {}
+
+
+def c4_packed(E, sizes, Q=8):
+    """Device-resident packed C4 batch: pair p takes the first n_p rows of pool pair p % Q
+    (a vMF prefix is itself a vMF sample); each pair has its own generator stream."""
+    torch = E.torch
+    k = HI.kappa_for(768)
+    pool = [HI.make_pair(HI.PairSpec(5000, 5000, 768, k, k, 30.0, seed=1004), rep=q)
+            for q in range(Q)]
+    px = [torch.from_numpy(X).to(E.dev) for X, _ in pool]
+    py = [torch.from_numpy(Y).to(E.dev) for _, Y in pool]
+    tot = int(np.sum(sizes))
+    Xd = torch.empty((tot, 768), dtype=torch.float32, device=E.dev)
+    Yd = torch.empty((tot, 768), dtype=torch.float32, device=E.dev)
+    off = 0
+    for p, n in enumerate(sizes):
+        n = int(n)
+        Xd[off:off + n].copy_(px[p % Q][:n])
+        Yd[off:off + n].copy_(py[p % Q][:n])
+        off += n
+    cu = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    return Xd, cu, Yd, cu.copy(), pool
+
+
+def run_batch_workload(args, E, peaks, name):
+    """c4 / c5: one hap_permtest_batch call per rank per step over its LPT share."""
+    torch, hap = E.torch, E.hap
+    from paper_2605_08048_b200 import parallel
+    K, W = args.steps, args.warmup
+    if name == "c4":
+        c = HI.CONFIGS["C4"]
+        sizes = c4_sizes()
+        Xd, cnx, Yd, cny, pool = c4_packed(E, sizes)
+        modes = [hap.HAP_ALIGN_HOUSEHOLDER]
+        B = c["B"]
+        l2 = f"{Xd.numel() * 8 / 1e9:.1f} GB of packed inputs per step (> 126 MB L2)"
+    else:
+        c = HI.CONFIGS["C5"]
+        R = c["R"]
+        pool = c2_pool(args.pool, 0, c["n_x"], c["n_y"], c["d"], seed=1005)
+        sizes = np.full(R, c["n_x"], dtype=np.int64)
+        Xd = torch.from_numpy(np.concatenate([pool[i % len(pool)][0] for i in range(R)])).to(E.dev)
+        Yd = torch.from_numpy(np.concatenate([pool[i % len(pool)][1] for i in range(R)])).to(E.dev)
+        cnx = np.arange(R + 1, dtype=np.int64) * c["n_x"]
+        cny = np.arange(R + 1, dtype=np.int64) * c["n_y"]
+        modes = [hap.HAP_ALIGN_HOUSEHOLDER, hap.HAP_ALIGN_NONE]
+        B = c["B"]
+        l2 = f"{Xd.numel() * 8 / 1e6:.0f} MB of packed inputs per step (> 126 MB L2)"
+    P = len(sizes)
+    costs = (np.diff(cnx) + np.diff(cny)).tolist()
+    mine = parallel.lpt_assign(costs, E.world)[E.rank]
+    iw = hap.INFO_BYTES // 8
+    nm = len(modes)
+    buf = torch.zeros((K, nm, P, iw + 3), dtype=torch.int64, device=E.dev)
+    infos = torch.zeros((nm, P, hap.INFO_BYTES), dtype=torch.uint8, device=E.dev)
+    dcounts = torch.zeros((nm, P, 3), dtype=torch.int64, device=E.dev)
+
+    def step(k, sel=mine, X=Xd, Y=Yd):
+        for mi, mode in enumerate(modes):
+            cfg = hap.make_cfg(HI.PERM_SEED, B, stream_id=((k * nm + mi) * P) & 0xFFFFFFFF)
+            if sel:
+                hap.hap_permtest_batch(E.ctx.h, X, cnx, Y, cny, mode, cfg, infos[mi],
+                                       dcounts[mi], pair_sel=sel, stream=E.st)
+
+    for k in range(W):
+        step(K + k)
+    torch.cuda.synchronize()
+    hap.hap_profile_read(E.ctx.h, reset=True)
+
+    def timed_step(k):
+        dcounts.zero_()
+        step(k)
+        buf[k, :, :, :iw].copy_(infos.view(torch.int64).view(nm, P, iw))
+        buf[k, :, :, iw:].copy_(dcounts)
+        if k == K - 1 and E.world > 1:
+            # every row is written by exactly one rank (zero elsewhere): the sum is the union
+            E.dist.all_reduce(buf)
+
+    ms, tw0, tw1 = E.timed(timed_step, K)
+    launches = hap.hap_profile_read(E.ctx.h, reset=True)[1]
+    tests = K * P * nm
+    value = tests / (ms / 1e3)
+    perms = tests * B / (ms / 1e3)
+    # dominant kernel of the batch: profile waves of the largest pairs in isolation
+    order = sorted(range(P), key=lambda p: -costs[p])
+    big = order[:6]
+
+    def waves():
+        for i in range(2):
+            dcounts.zero_()
+            step(10 * K + i, sel=big[3 * i: 3 * i + 3])
+            torch.cuda.synchronize()
+    nb = int(sizes[big[0]])
+    roof = kernel_profile(E, waves, 6, 2 * nb, 768, B, peaks,
+                          f"isolated waves of the 3 largest pairs (n~{nb}) of the batch")
+    # e2e on a bounded slice from pinned host memory (whole batch would pin tens of GB)
+    Pe = min(P, 1000 if name == "c4" else P)
+    ne = int(cnx[Pe])
+    Xh = Xd[:ne].cpu().pin_memory()
+    Yh = Yd[:ne].cpu().pin_memory()
+    sel_e = [p for p in mine if p < Pe]
+    hc = torch.zeros((nm, P, 3), dtype=torch.int64).pin_memory()
+    torch.cuda.synchronize()
+    E.barrier()
+    t0 = time.perf_counter()
+    dcounts.zero_()
+    for mi, mode in enumerate(modes):
+        cfg = hap.make_cfg(HI.PERM_SEED, B, stream_id=(99 * P + mi) & 0xFFFFFFFF)
+        if sel_e:
+            hap.hap_permtest_batch(E.ctx.h, Xh, cnx[: Pe + 1], Yh, cny[: Pe + 1], mode, cfg,
+                                   infos[mi], dcounts[mi], pair_sel=sel_e, stream=E.st)
+    hc.copy_(dcounts, non_blocking=True)
+    torch.cuda.synchronize()
+    e2e_s = E.max_over_ranks(time.perf_counter() - t0)
+    e2e = {"value": Pe * nm / e2e_s, "unit": UNIT_T,
+           "h2d_bytes_per_step": int(Xh.numel() * 4 * 2 * nm),
+           "d2h_bytes_per_step": int(nm * P * 24), "steps": 1,
+           "sample": f"the first {Pe} pairs of the batch (one step), inputs in pinned HOST "
+                     "memory",
+           "timer": "host wall clock, synchronize on both sides"}
+    cfg_out = {"workload": workload_desc(name, 0), "pairs": P, "B": B, "d": 768,
+               "global_batch": P * nm, "l2": l2,
+               "parallelism": f"pairs LPT-assigned (cost n_x+n_y) over {E.world} rank(s), one "
+                              "hap_permtest_batch per rank; one all_reduce of int64[K, modes, "
+                              "P, info+3] rows (each written by one rank)",
+               "input_pool": (f"pair p = first n_p rows of pool pair p % 8 (8 distinct "
+                              "5000/5000 vMF pairs)") if name == "c4" else
+               f"{len(pool)} distinct pairs repeated"}
+    extra = {"perms_per_s": perms,
+             "mean_n": float(np.mean(sizes)),
+             "rank_share_pairs": len(mine)}
+    return value, ms, tw0, tw1, launches, roof, e2e, None, cfg_out, extra
 
 
 def run_hap(args):
-    import torch
-    import torch.distributed as dist
-
-    import paper_2605_08048_b200 as hap
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
-    # a rotating pool of distinct input pairs; the device batch repeats the pool so every
-    # test of the run has its own slot (generator stream base + slot: its own permutations)
-    # and the whole timed region is ONE hap_permtest_batch call (no drain between calls)
-    pool_np = make_pool(args.pool, rank)
-    P = len(pool_np)
-    K, W = args.steps, args.warmup
-    nwave_prof = max(1, min(K, 300) // 3)
-    V = W + K + 3 * nwave_prof  # virtual pairs: warm-up, timed, profiling pass
-    Xp = np.ascontiguousarray(np.concatenate([X for X, _ in pool_np]))
-    Yp = np.ascontiguousarray(np.concatenate([Y for _, Y in pool_np]))
-    Xpool, Ypool = torch.from_numpy(Xp).to(dev), torch.from_numpy(Yp).to(dev)
-    reps = -(-V // P)
-    Xd = Xpool.repeat(reps, 1)[: V * N_X].contiguous()
-    Yd = Ypool.repeat(reps, 1)[: V * N_Y].contiguous()
-    del Xpool, Ypool
-    cu_nx = np.arange(V + 1, dtype=np.int64) * N_X
-    cu_ny = np.arange(V + 1, dtype=np.int64) * N_Y
-    in_bytes = (Xp.nbytes + Yp.nbytes)
-    ctx = hap.Context(local)
-    st = torch.cuda.current_stream()
-    INFO = hap.INFO_BYTES
-    infos = torch.zeros((V, INFO), dtype=torch.uint8, device=dev)
-    counts = torch.zeros((max(K, 1), 3), dtype=torch.int64, device=dev)
-    vcounts = torch.zeros((V, 3), dtype=torch.int64, device=dev)
-    base_sid = (rank * 1_000_003) & 0xFFFFFFFF
-
-    def run_tests(k0, n, out_counts=None, wave=0):
-        """tests k0 .. k0+n-1 (virtual pair k = pool pair k % P, generator stream base + k)
-        in one hap_permtest_batch call"""
-        sel = np.arange(k0, k0 + n, dtype=np.int64)
-        cfg = hap.make_cfg(HI.PERM_SEED, B, stream_id=base_sid, wave=wave)
-        hap.hap_permtest_batch(ctx.h, Xd, cu_nx, Yd, cu_ny, hap.HAP_ALIGN_HOUSEHOLDER, cfg,
-                               infos, vcounts, pair_sel=sel, stream=st)
-        if out_counts is not None:
-            out_counts[:n].copy_(vcounts[k0:k0 + n])
-
+    peaks, peak_src = load_peaks()
+    E = Env()
     gpu_id = None
     try:
-        gpu_id = "GPU-" + str(torch.cuda.get_device_properties(local).uuid)
+        gpu_id = "GPU-" + str(E.torch.cuda.get_device_properties(E.local).uuid)
     except Exception:
         pass
     clocks = ClockSampler(gpu_id)
     clocks.start()
     time.sleep(0.3)
-
-    # ---------------- pass 1: the headline number (no instrumentation)
-    run_tests(0, W)
-    torch.cuda.synchronize()
-    vcounts.zero_()
-    hap.hap_profile_read(ctx.h, reset=True)
-    barrier()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    tw0 = time.time()
-    e0.record(st)
-    run_tests(W, K, counts)
-    if world > 1:
-        dist.all_reduce(counts)  # the one combine of the integer counts
-    e1.record(st)
-    e1.synchronize()
-    tw1 = time.time()
-    barrier()
-    ms = e0.elapsed_time(e1)
-    launches = hap.hap_profile_read(ctx.h, reset=True)[1]
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    total_perms = K * B * world
-    value = total_perms / (ms / 1e3)
-    ms_per_step = ms / K
-
-    # ---------------- pass 2: per-kernel device time (CUDA events on the launching stream)
-    # one wave per call and a sync after it, so no other launch overlaps the timed ones
-    wave = 3
-    nw = nwave_prof
-    hap.hap_profile(ctx.h, 2)
-    for i in range(nw):
-        run_tests(W + K + i * wave, wave, wave=wave)
-        torch.cuda.synchronize()
-    phase_ms, phase_n = hap.hap_profile_read(ctx.h, reset=True)
-    hap.hap_profile(ctx.h, 0)
-    peaks, peak_src = load_peaks()
-    Nf = N_X + N_Y
-    n_k3 = max(1, phase_n["maskgemm"])
-    gemm_flops = 2.0 * Nf * D * B * wave  # algorithmic: the U = S X row per permutation
-    gemm_s = phase_ms["maskgemm"] / 1e3 / n_k3  # per launch
-    achieved_tflops = gemm_flops / gemm_s / 1e12 if gemm_s > 0 else 0.0
-    peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
-    n_pad = -(-Nf // 64) * 64
-    issued_tflops = 4.0 * n_pad * D * B * wave / gemm_s / 1e12 if gemm_s > 0 else 0.0
-    traffic = None
-    tf = os.path.join(ROOT, "profiles", "k3_traffic.json")
-    if os.path.exists(tf):
-        with open(tf) as f:
-            tj = json.load(f)
-        traffic = tj.get("bytes_per_launch")
-    roofline = {"bound": "tensor", "achieved": achieved_tflops, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved_tflops / peak, "traffic": traffic,
-                "kernel": f"k3_maskgemm (S8+S9), one launch = a wave of {wave} C2 tests",
-                "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside the step loop)",
-                "achieved_basis": "algorithmic 2*N*d FLOP per permutation (SURVEY.md 8d)",
-                "issued_tflops": issued_tflops, "k3_us_per_launch": gemm_s * 1e6,
-                "gemm_share_of_step": phase_ms["maskgemm"] / max(1e-9, sum(phase_ms.values()))}
-    phases_per_test = {k: v / (nw * wave) for k, v in phase_ms.items()}
-
-    # ---------------- pass 3: end to end through the C ABI with HOST inputs: every chunk
-    # of tests passes the packed X, Y in pinned host memory to hap_permtest_batch, which
-    # copies each wave's rows on its lane streams (overlapping the other lane's kernels);
-    # the counts are read back into pinned host memory; one sync at the end
-    Ke = min(K, 480)
-    Xh = torch.from_numpy(Xp).pin_memory()
-    Yh = torch.from_numpy(Yp).pin_memory()
-    host_counts = torch.zeros((Ke, 3), dtype=torch.int64).pin_memory()
-    dev_counts = torch.zeros((2, P, 3), dtype=torch.int64, device=dev)
-
-    def e2e_chunk(c, k0, m):
-        cfg = hap.make_cfg(HI.PERM_SEED, B, stream_id=(rank * 1_000_003 + k0) & 0xFFFFFFFF)
-        dc = dev_counts[c % 2]
-        dc.zero_()
-        hap.hap_permtest_batch(ctx.h, Xh, cu_nx[: m + 1], Yh, cu_ny[: m + 1],
-                               hap.HAP_ALIGN_HOUSEHOLDER, cfg, infos, dc, stream=st)
-        host_counts[k0: k0 + m].copy_(dc[:m], non_blocking=True)  # D2H of the results
-
-    e2e_chunk(0, 0, min(P, Ke))
-    torch.cuda.synchronize()
-    barrier()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    k, c = 0, 0
-    while k < Ke:
-        m = min(P, Ke - k)
-        e2e_chunk(c, k, m)
-        k += m
-        c += 1
-    torch.cuda.synchronize()
-    e2e_s = time.perf_counter() - t0
-    if world > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    last = int(host_counts[Ke - 1, 0])
-    e2e = {"value": Ke * B * world / e2e_s, "unit": UNIT,
-           "h2d_bytes_per_step": (N_X + N_Y) * D * 4, "d2h_bytes_per_step": 3 * 8,
-           "steps": Ke, "timer": "host wall clock around the loop, synchronize on both sides",
-           "api": f"hap_permtest_batch on chunks of {P} tests with X, Y in pinned HOST memory "
-                  "(the library copies each wave's rows on its lane streams), counts copied D2H"}
-
+    fn = {"c2": run_c2, "c3": run_c3}.get(args.workload)
+    if fn is None:
+        res = run_batch_workload(args, E, peaks, args.workload)
+    else:
+        res = fn(args, E, peaks)
+    value, ms, tw0, tw1, launches, roof, e2e, cpu, cfg_out, extra = res
     clocks.stop()
     clk = clocks.summary(tw0, tw1)
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(pool_np)
-    if rank == 0:
-        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
-               "warmup": W, "ms_per_step": ms_per_step, "higher_is_better": True,
-               "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-               "data": "synthetic",
-               "config": {"workload": WORKLOAD, "global_batch": world, "B": B, "n_x": N_X,
-                          "n_y": N_Y, "d": D,
-                          "l2": f"rotating pool of {P} distinct input pairs per rank "
-                                f"({in_bytes / 1e6:.0f} MB > 126 MB L2), repeated in HBM so "
-                                f"each test has its own slot",
-                          "parallelism": f"tests sharded over {world} rank(s); each rank runs "
-                                         "its own tests; counts combined by one all_reduce",
-                          "api": "hap_permtest_batch (2 internal lanes, waves of 3 tests per "
-                                 "alignment / generator / mask-GEMM launch)",
-                          "arith": "bf16 hi/lo split operands, fp32 TMEM accumulation, "
-                                   "fp64 statistic"},
-               "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+    roof["peaks_source"] = peak_src
+    W = WORKLOADS[args.workload]
+    if E.rank == 0:
+        out = {"metric": W["metric"], "value": value, "unit": W["unit"], "n_gpus": E.world,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+               "higher_is_better": True, "scaling": W["scaling"], "vs_baseline": None,
+               "dtype": "bf16", "data": "synthetic", "config": cfg_out, "roofline": roof,
+               "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
                "gpu_launches": int(sum(launches.values())),
-               "gpu_launches_by_phase": launches, "phase_ms_per_test": phases_per_test,
-               "last_test": {"exceed_ge": last, "p_value": hap.hap_pvalue(last, B)}}
+               "gpu_launches_by_phase": launches, "env_knobs": "none (HAP_* refused)"}
+        out.update(extra)
         print(json.dumps(out), flush=True)
-    ctx.close()
-    if world > 1:
-        dist.destroy_process_group()
+    E.ctx.close()
+    if E.world > 1:
+        E.dist.destroy_process_group()
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=2000)
-    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="hap", choices=["hap", "reference"])
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--tests-per-step", type=int, default=TESTS_PER_STEP)
     ap.add_argument("--pool", type=int, default=24, help="distinct input pairs per rank")
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    knobs = sorted(k for k in os.environ if k.startswith("HAP_"))
+    if knobs:
+        print(json.dumps({"metric": WORKLOADS[args.workload]["metric"], "value": None,
+                          "refused": f"HAP_* experiment knobs set: {knobs}; bench.py measures "
+                                     "the library as built, unset them"}), flush=True)
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args)
     else:
