@@ -71,6 +71,35 @@ def batch_sharded(run_pair: Callable[[int], np.ndarray], sizes: Sequence[int], r
     return _allreduce_sum(buf, group, device).reshape(P, 3)
 
 
+def allreduce_device(t, group=None) -> None:
+    """In-place SUM all-reduce of a device tensor: NCCL reduces on the device; other
+    backends (gloo in the multi-process tests) go through a host copy."""
+    import torch.distributed as dist
+    if dist.get_backend(group) == "nccl":
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+        return
+    h = t.cpu()
+    dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+    t.copy_(h)
+
+
+def gpu_range_counts(ctx, X, Y, B: int, seed: int, rank: int, world: int, counts, info,
+                     stream_id: int = 0, mode: int = 0, group=None, stream=None,
+                     reduce: bool = True) -> None:
+    """Config C3 on the CUDA library, asynchronous: every rank aligns the same pair (the
+    K1 arithmetic is deterministic, so every rank builds bit-identical planes), counts its
+    b-range shard into `counts` (device int64[3], added into) and ONE all-reduce combines
+    the ranks.  Nothing synchronises the host."""
+    import paper_2605_08048_b200 as hap
+    b0, b1 = shard_range(B, rank, world)
+    hap.hap_align(ctx.h, X, Y, mode, info, stream=stream)
+    if b1 > b0:
+        cfg = hap.make_cfg(seed, B, b0, b1, stream_id)
+        hap.hap_permtest(ctx.h, info, cfg, counts, None, stream=stream)
+    if world > 1 and reduce:
+        allreduce_device(counts, group)
+
+
 def gpu_range_runner(ctx, X, Y, B: int, seed: int, stream_id: int = 0, mode: int = 0):
     """run_range for the CUDA library: align once, then count any b-range."""
     import paper_2605_08048_b200 as hap
@@ -121,6 +150,5 @@ def gpu_batch_sharded(ctx, X_packed, cu_nx, Y_packed, cu_ny, B: int, seed: int, 
         infos.copy_(inf_d.view(torch.int64))
         counts.copy_(cnt_d)
     if world > 1 and reduce:
-        import torch.distributed as dist
-        dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+        allreduce_device(buf, group)
     return buf[:, :iw].contiguous().view(torch.uint8), buf[:, iw:].contiguous()

@@ -399,3 +399,26 @@ def test_type1_aligned_calibrated(orc):
         rej += r["p_value"] <= alpha
     se = math.sqrt(alpha * (1 - alpha) / R)
     assert abs(rej / R - alpha) <= 3 * se
+
+
+def test_naive_inflates_type1_on_anisotropic_clouds(orc):
+    """The north star's calibration pin (§1 Fig. 1: a mean-direction
+    difference distorts the naive test's null; PAPER.md:445-448 anisotropy caveat; SURVEY.md
+    App. B, R15): under H0 (equal concentration) with mean directions 60 deg apart
+    and shared anisotropic noise (hap_inputs.anisotropic_pair), the two-sided rejection rate
+    of the naive test at alpha = 0.10 is inflated by > 2.5 SE while the aligned test stays
+    within 2 SE of alpha, on the same permutations (R = 600, n = 200/200, d = 768, B = 200).
+    Seeded, so the outcome is fixed; the GPU sweep at R = 1000, B = 10^4 is
+    profiles/r02_c5_sweep.json."""
+    R, n, d, B, alpha = 600, 200, 768, 200, 0.10
+    spec = HI.PairSpec(n, n, d, HI.kappa_for(d), HI.kappa_for(d), 60.0, seed=2005)
+    rej = {0: 0, 1: 0}
+    for rep in range(R):
+        X, Y = HI.anisotropic_pair(spec, rep)
+        for mode in (0, 1):
+            r = orc.run_pair(X, Y, B, SEED, s=rep, mode=mode, nthreads=8)
+            rej[mode] += orc.pvalue(r["exceed_abs"], B) <= alpha
+    se = math.sqrt(alpha * (1 - alpha) / R)
+    aligned, naive = rej[0] / R, rej[1] / R
+    assert abs(aligned - alpha) <= 2 * se, (aligned, naive)
+    assert naive - alpha >= 2.5 * se, (aligned, naive)
