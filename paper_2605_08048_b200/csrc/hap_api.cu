@@ -616,7 +616,8 @@ hap_status reserve_pair(hap_ctx c, int64_t N, int64_t d, int64_t tiles, int64_t 
          (s = ensure(c, kTileDone, (size_t)kMaxWave * tiles * sizeof(unsigned)))))
         return s;
     if ((s = ensure(c, kXbar, d * 8)) || (s = ensure(c, kYbar, d * 8)) ||
-        (s = ensure(c, kInv, N * 8)) || (s = ensure(c, kU, d_pad * 8)) ||
+        (s = ensure(c, kInv, N * 8)) || (s = ensure(c, kCoef, n_pad * 8)) ||
+        (s = ensure(c, kU, d_pad * 8)) ||
         (s = ensure(c, kZhi, (size_t)zt_rows(d_pad) * n_pad * 2)) ||
         (s = ensure(c, kZlo, (size_t)zt_rows(d_pad) * n_pad * 2)) ||
         (s = ensure(c, kTpart, (size_t)(2 * d + d_pad) * 8)) ||
@@ -644,7 +645,8 @@ hap_status prepare_pair_cp(hap_ctx c, const float* X, int64_t n_x, const float* 
     const int64_t d_pad = round_up(d, 32);
     hap_status s;
     if ((s = ensure(c, kXbar, d * 8)) || (s = ensure(c, kYbar, d * 8)) ||
-        (s = ensure(c, kInv, N * 8)) || (s = ensure(c, kU, d_pad * 8)) ||
+        (s = ensure(c, kInv, N * 8)) || (s = ensure(c, kCoef, n_pad * 8)) ||
+        (s = ensure(c, kU, d_pad * 8)) ||
         (s = ensure(c, kZhi, (size_t)zt_rows(d_pad) * n_pad * 2)) ||
         (s = ensure(c, kZlo, (size_t)zt_rows(d_pad) * n_pad * 2)) ||
         (s = ensure(c, kTpart, (size_t)(2 * d + d_pad) * 8)) ||
@@ -681,6 +683,7 @@ hap_status prepare_pair_cp(hap_ctx c, const float* X, int64_t n_x, const float* 
     q.n_pad = n_pad;
     q.info = info;
     q.inv = B<double>(c, kInv);
+    q.coef = B<float2>(c, kCoef);
     q.u = B<double>(c, kU);
     q.xbar = B<double>(c, kXbar);
     q.ybar = B<double>(c, kYbar);
@@ -725,7 +728,7 @@ hap_status align_wave(hap_ctx owner, int G, hap_ctx* ws, const AlignPair* pairs,
     a.span = next_span(owner, HAP_PHASE_ALIGN);
     cudaError_t e;
     {
-        PhaseScope ps(owner, HAP_PHASE_ALIGN, kAlignLaunches, st);
+        PhaseScope ps(owner, HAP_PHASE_ALIGN, align_launch_count(a), st);
         e = launch_align(a, owner->sm_count, st);
     }
     if (e != cudaSuccess) return cuda_fail(owner, e, "align kernel");
@@ -906,7 +909,7 @@ hap_status launch_wave(hap_ctx owner, const WaveTest* T, int pair, cudaStream_t 
     } else {
         // K2 on the side stream: each test's slot is rewritten only after the K3 that read it
         // (on `st` itself when serialised or when the caller passed its light stream as st)
-        cudaStream_t gs = (owner->serial || light == st) ? st : owner->side;
+        cudaStream_t gs = (owner->serial || (light && light == st)) ? st : owner->side;
         for (int k = 0; k < pa.G && e == cudaSuccess && !owner->serial; ++k)
             if (T[k].w->used[slots[k]]) e = cudaStreamWaitEvent(gs, T[k].w->ev_free[slots[k]], 0);
         if (e == cudaSuccess) {
@@ -1114,6 +1117,8 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
             const bool one_block = ceil_div(std::max<int64_t>(B, 1), R - 1) <= block_tiles(cfg, round_up(nx + ny, kKBlock), R);
             if (G > 0 && !one_block) break;  // a multi-block test starts its own wave
             if (G > 0 && shared && (nx != Q[0].n_x || ny != Q[0].n_y)) break;  // same masks
+            // one alignment path per wave (the path is a function of the pair's shape)
+            if (G > 0 && align_stream_pair(nx + ny, d) != align_stream_pair(Q[0].n_x + Q[0].n_y, d)) break;
             hap_ctx w = c->sub[k][G];
             const int sb = c->lane_waves[k] & 1;  // staging buffer of this wave
             if (G == 0 && host_in && c->k1_recorded[k][sb])  // its last reader: the K1 two waves back
@@ -1141,7 +1146,8 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
             // slots and K2 keeps only its table pass; bit-exact, but the lane then runs
             // K1 -> K2b -> K3 in series and measured 106 vs 85 us per C2 test, so off
             static const char* kd = getenv("HAP_K1_DRAWS");
-            staged = !s && kd && atoi(kd) != 0 && perm_can_split(P.pa);
+            staged = !s && kd && atoi(kd) != 0 && perm_can_split(P.pa) &&
+                     !align_stream_pair(Q[0].n_x + Q[0].n_y, d);
         }
         if (!s && G > 0 && host_in) {  // K1 waits for the wave's rows
             cudaEventRecord(c->ev_copied[k], c->cp_stream[k]);

@@ -63,6 +63,7 @@ struct AlignPair {
     int64_t n_x, n_y, d, n_pad;
     hap_align_info* info;    // device
     double* inv;             // [N]    1/||h_i|| (0 for a zero row)
+    float2* coef;            // [N]    {2 u.x_i, 1/||h_i||} (streaming path, K1s)
     double* u;               // [d_pad] Householder axis (0 for the identity)
     double* xbar;            // [d]
     double* ybar;            // [d]
@@ -97,9 +98,14 @@ struct AlignGeom {
 AlignGeom align_geometry(int64_t d);
 // fills item_off (n_pad / R items per pair) for the geometry of d
 void align_items(AlignArgs& a);
-// one cooperative kernel of `grid` CTAs (one per SM); scratch[2] holds its grid barrier
+// Large pairs (align_stream_pair: d % 4 == 0, d <= 4096, n_pad d >= 8 Mi elements; inputs
+// 16-byte aligned) take the streaming path K1s (three bandwidth kernels); the others ONE
+// cooperative kernel of `grid` CTAs (one per SM) whose scratch[2] holds its grid barrier.
+// A wave's pairs must all take the same path (the batch forms its waves so).
+bool align_stream_pair(int64_t N, int64_t d);
+bool align_uses_stream(const AlignArgs& a);
+int align_launch_count(const AlignArgs& a);  // kernels issued by launch_align
 cudaError_t launch_align(const AlignArgs& a, int grid, cudaStream_t st);
-constexpr int kAlignLaunches = 1;  // kernels issued by launch_align
 
 // ---- K3: tcgen05 mask-GEMM + statistic epilogue (k_maskgemm.cu) --------------------
 struct GemmTest {

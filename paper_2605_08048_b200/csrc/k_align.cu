@@ -76,6 +76,32 @@ __device__ double2 block_sum2(double v0, double v1, double* red) {
     return make_double2(red[2 * kWarps], red[2 * kWarps + 1]);
 }
 
+// the same for a block of NT threads (streaming kernels)
+template <int NT>
+__device__ double2 block_sum2_n(double v0, double v1, double* red) {
+    constexpr int W = NT / 32;
+    v0 = warp_sum(v0);
+    v1 = warp_sum(v1);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) {
+        red[w] = v0;
+        red[W + w] = v1;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s0 = 0.0, s1 = 0.0;
+        for (int i = 0; i < W; ++i) {
+            s0 += red[i];
+            s1 += red[W + i];
+        }
+        red[2 * W] = s0;
+        red[2 * W + 1] = s1;
+    }
+    __syncthreads();
+    return make_double2(red[2 * W], red[2 * W + 1]);
+}
+
 // sum over CTAs p of spart[p*kSpartStride + k], fixed order (same in every CTA)
 __device__ double cta_partials_sum(const double* spart, int k, double* red) {
     double v = 0.0;
@@ -228,6 +254,47 @@ __device__ __forceinline__ void store_words(uint32_t* dst, const uint32_t (&w)[W
         reinterpret_cast<uint2*>(dst)[0] = make_uint2(w[0], w[1]);
     } else {
         dst[0] = w[0];
+    }
+}
+
+// P5 (the last CTA of an alignment launch, by ticket): per pair t = N m + t', a = n_x m,
+// b = t - a (fp32) for the GEMM epilogue, {sum a^2, sum b^2} in fixed order; then the
+// accumulators and flags are cleared for the next launch.  Shared by the fused K1 and the
+// streaming K1s transform kernel.
+__device__ void finish_pairs(const AlignArgs& a, double* red) {
+    const int tid = threadIdx.x;
+    const int d = (int)a.d;
+    for (int g = 0; g < a.G; ++g) {
+        const AlignPair& q = a.p[g];
+        const int64_t N = q.n_x + q.n_y;
+        double sa = 0.0, sb = 0.0, sm = 0.0;
+        for (int64_t c = tid; c < a.d_pad; c += kThreads) {
+            const double tsum = fix_get(q.acc + 2 * d + c);
+            const double m = __ldcg(q.m + c);
+            sm += m * m;
+            q.t64[c] = (double)N * m + tsum;
+            const float af = (float)((double)q.n_x * m);
+            const float bf = (float)((double)q.n_y * m + tsum);
+            q.ab[c] = make_float2(2.0f * af, 2.0f * bf);
+            sa += (double)af * (double)af;
+            sb += (double)bf * (double)bf;
+        }
+        const double2 sab = block_sum2(sa, sb, red);
+        const double smm = block_sum2(sm, 0.0, red).x;
+        for (int64_t c = tid; c < 2 * (int64_t)d + a.d_pad; c += kThreads) q.acc[c] = 0;
+        if (tid == 0) {
+            q.sconst[0] = sab.x;
+            q.sconst[1] = sab.y;
+            // representation-error scale of a pooled row (R14): the planes keep
+            // z' = z - m to 2^-17 relative (bf16 hi + lo) after an fp32 evaluation of z
+            // (2^-23 of |z| = 1); E||z'||^2 = 1 - ||m||^2
+            q.sconst[2] = 0x1p-17 * sqrt(fmax(1.0 - smm, 0.0)) + 0x1p-23;
+            *q.bad = LLONG_MAX;  // reset the pair's ZeroVector word
+        }
+    }
+    if (tid == 0) {  // reset the ticket and the barrier
+        reinterpret_cast<unsigned*>(a.scratch + 1)[0] = 0u;
+        reinterpret_cast<unsigned*>(a.scratch + 2)[0] = 0u;
     }
 }
 
@@ -587,38 +654,7 @@ __global__ void __launch_bounds__(kThreads, 65536 / (kThreads * 64)) k1_align_fu
     __syncthreads();
     if (s_last) {
         __threadfence();
-        for (int g = 0; g < a.G; ++g) {
-            const AlignPair& q = a.p[g];
-            const int64_t N = q.n_x + q.n_y;
-            double sa = 0.0, sb = 0.0, sm = 0.0;
-            for (int64_t c = tid; c < a.d_pad; c += kThreads) {
-                const double tsum = fix_get(q.acc + 2 * d + c);
-                const double m = __ldcg(q.m + c);
-                sm += m * m;
-                q.t64[c] = (double)N * m + tsum;
-                const float af = (float)((double)q.n_x * m);
-                const float bf = (float)((double)q.n_y * m + tsum);
-                q.ab[c] = make_float2(2.0f * af, 2.0f * bf);
-                sa += (double)af * (double)af;
-                sb += (double)bf * (double)bf;
-            }
-            const double2 sab = block_sum2(sa, sb, red);
-            const double smm = block_sum2(sm, 0.0, red).x;
-            for (int64_t c = tid; c < 2 * (int64_t)d + a.d_pad; c += kThreads) q.acc[c] = 0;
-            if (tid == 0) {
-                q.sconst[0] = sab.x;
-                q.sconst[1] = sab.y;
-                // representation-error scale of a pooled row (R14): the planes keep
-                // z' = z - m to 2^-17 relative (bf16 hi + lo) after an fp32 evaluation of z
-                // (2^-23 of |z| = 1); E||z'||^2 = 1 - ||m||^2
-                q.sconst[2] = 0x1p-17 * sqrt(fmax(1.0 - smm, 0.0)) + 0x1p-23;
-                *q.bad = LLONG_MAX;  // reset the pair's ZeroVector word
-            }
-        }
-        if (tid == 0) {  // reset the ticket and the barrier
-            reinterpret_cast<unsigned*>(a.scratch + 1)[0] = 0u;
-            bar[0] = 0u;
-        }
+        finish_pairs(a, red);
     }
     stamp(a, 5);
     cstamp(a, 7);
@@ -626,6 +662,574 @@ __global__ void __launch_bounds__(kThreads, 65536 / (kThreads * 64)) k1_align_fu
     if (tid == 0) span_exit(a.span);
 }
 
+
+// ==========================================================================================
+// K1s — STREAMING alignment for large pairs (n_pad * d >= kStreamMinElems).
+// The fused kernel above is latency-shaped (one CTA per SM, a grid barrier, reloads); at
+// LLM sizes (C3: 164 MB of fp32 input) the alignment is a bandwidth problem, so it runs as
+// three bandwidth passes over HBM, each with many loads in flight:
+//   KS1 k1s_stats : items of R rows -> a 3-stage shared-memory ring filled by cp.async.bulk
+//                   (one bulk copy per row); row norms -> inv (ZeroVector check); fp64
+//                   column partials of x = h/||h|| per item, rounded per item to fixed point
+//                   and summed as int64 in registers (exact, order-free), one atomic per
+//                   column per CTA; the last CTA (ticket) forms every pair's means, axis,
+//                   centre and observed statistic (the P3 arithmetic of the fused kernel)
+//   KS2 k1s_coef  : reflection coefficients 2 u.x_i of the X rows (fp64 dot, 4 rows per
+//                   warp so each u load serves 4 rows); {coef, 1/||h||} per row
+//   KS3 k1s_xform : tiled transpose, 64 rows x 64 columns per tile: z' = x - coef u - m
+//                   (fp32, as the fused kernel), bf16 hi/lo split, 128-byte column runs per
+//                   plane; per-column t' partials per tile in fixed point; the last CTA
+//                   (ticket) runs P5 (finish_pairs).
+// Algorithmic bytes: read 4Nd (KS1) + 4 n_x d (KS2) + 4Nd (KS3), write 4 n_pad d_pad (KS3).
+// Deterministic: every cross-CTA sum is an integer sum of per-item / per-tile roundings and
+// the CTA -> work assignment depends only on the shapes.
+constexpr int kSStages = 3;
+constexpr int64_t kStreamMinElems = 8ll << 20;  // n_pad * d: 32 MB of fp32 input
+constexpr int kXfRows = 128, kXfCols = 64;  // KS3 tile: 128 rows x 64 columns
+
+__device__ __forceinline__ void bulk_load_row(float* dst, const float* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// expect_tx + arrive WITHOUT release semantics: a release arrive waits (MEMBAR) for the
+// issuing thread's earlier global stores and atomics, which stalled the whole CTA once per
+// item; the stage's readers are ordered before the refill by the __syncthreads before it
+__device__ __forceinline__ void mbar_arrive_expect_tx_relaxed(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+// P3 of one pair from its (complete) accumulators, written to global memory: xbar, ybar,
+// axis u, centre m, info (the arithmetic of the fused kernel's pair_scalars, writer case)
+template <int NT>
+__device__ void stream_pair_scalars(const AlignArgs& a, int g, double* red) {
+    const AlignPair& q = a.p[g];
+    const int tid = threadIdx.x;
+    const int d = (int)a.d;
+    const long long* acc_x = q.acc;
+    const long long* acc_y = q.acc + d;
+    const int64_t N = q.n_x + q.n_y;
+    const double rnX = 1.0 / (double)q.n_x, rnY = 1.0 / (double)q.n_y;
+    double sxx = 0.0, syy = 0.0;
+    for (int c = tid; c < d; c += NT) {
+        const double xb = fix_get(acc_x + c) * rnX, yb = fix_get(acc_y + c) * rnY;
+        q.xbar[c] = xb;
+        q.ybar[c] = yb;
+        sxx += xb * xb;
+        syy += yb * yb;
+    }
+    const double2 sq = block_sum2_n<NT>(sxx, syy, red);
+    const double nx = sqrt(sq.x), ny = sqrt(sq.y);
+    const bool degenerate = nx < 1e-12 || ny < 1e-12;
+    const double rnx = degenerate ? 0.0 : 1.0 / nx;
+    const double rny = degenerate ? 0.0 : 1.0 / ny;
+    double sv = 0.0, svx = 0.0;
+    for (int c = tid; c < d; c += NT) {
+        const double xb = fix_get(acc_x + c) * rnX, yb = fix_get(acc_y + c) * rnY;
+        const double v = xb * rnx - yb * rny;
+        sv += v * v;
+        svx += v * xb;
+    }
+    const double2 vv = block_sum2_n<NT>(sv, svx, red);
+    const double nv0 = sqrt(vv.x);
+    const bool identity = (a.mode == HAP_ALIGN_NONE) || degenerate || nv0 < 1e-9;  // R3
+    const double rnv = identity ? 0.0 : 1.0 / nv0;
+    const double ux = vv.y * rnv;
+    const double rN = 4096.0 / (double)N;
+    for (int c = tid; c < (int)a.d_pad; c += NT) {
+        double ud = 0.0, md = 0.0;
+        if (c < d) {
+            const double xb = fix_get(acc_x + c) * rnX, yb = fix_get(acc_y + c) * rnY;
+            ud = (xb * rnx - yb * rny) * rnv;
+            const double t = (double)q.n_x * (xb - 2.0 * ud * ux) + (double)q.n_y * yb;
+            md = rint(t * rN) * (1.0 / 4096.0);
+        }
+        q.u[c] = ud;
+        q.m[c] = md;
+    }
+    if (tid == 0) {
+        hap_align_info* f = q.info;
+        const long long bad = *reinterpret_cast<volatile long long*>(q.bad);
+        f->n_x = q.n_x;
+        f->n_y = q.n_y;
+        f->d = a.d;
+        f->n_pad = q.n_pad;
+        f->d_pad = a.d_pad;
+        f->is_identity = identity ? 1 : 0;
+        f->status = bad < N ? HAP_E_ZERO_VECTOR : (degenerate ? HAP_E_DEGENERATE_MEAN : HAP_OK);
+        f->bad_row = bad < N ? bad : -1;
+        f->r_x = nx;  // r(X') = ||xbar||
+        f->r_y = ny;
+        const double lx = logkappa64(nx, (double)a.d), ly = logkappa64(ny, (double)a.d);
+        f->logk_x = lx;
+        f->logk_y = ly;
+        f->t_obs = (isinf(lx) && isinf(ly)) ? 0.0 : ly - lx;  // Eq. 10
+        const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+        f->gemm_r_x = f->gemm_r_y = f->gemm_t_obs = qnan;
+    }
+    __syncthreads();
+}
+
+// KS1.  a.item_off: items of R rows (R = 8 / G4), ceil(N/R) per pair.  CTA c takes items
+// [I c / grid, I (c+1) / grid); 256 threads, two CTAs per SM.  Thread t owns the float4
+// column groups t + 256 k (k < G4) of every row of an item: it widens each fp32 value to
+// fp64 ONCE (registers), forms its partial squares per row (reduced in fixed order ->
+// 1/||h||) and then the item's column partials of x = h/||h||.  Column sums of pair g, side
+// X (0) / Y (1) are held as int64 in registers and flushed (one atomic per column) when the
+// (pair, side) changes.
+constexpr int kS1Threads = 256;
+template <int G4>
+__global__ void __launch_bounds__(kS1Threads, 2) k1s_stats(AlignArgs a) {
+    constexpr int R = 8 / G4;
+    constexpr int W = kS1Threads / 32;
+    extern __shared__ __align__(128) uint8_t ks_smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(ks_smem);
+    float* ring = reinterpret_cast<float*>(ks_smem + 128);
+    __shared__ double red[2 * W + 2];
+    __shared__ double s_part[W][R];
+    __shared__ double s_inv[R];
+    __shared__ int s_last;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int d = (int)a.d;
+    const int d4 = d >> 2;
+    const int64_t items = a.item_off[a.G];
+    const int64_t i0 = items * blockIdx.x / gridDim.x, i1 = items * (blockIdx.x + 1) / gridDim.x;
+    const size_t stage_floats = (size_t)R * d;
+    if (tid == 0) {
+        span_enter(a.span);
+        for (int k = 0; k < kSStages; ++k) mbar_init(&full[k], 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    auto issue = [&](int64_t item, int st) {  // one thread
+        const int g = pair_of(a, item);
+        const AlignPair& q = a.p[g];
+        const int64_t N = q.n_x + q.n_y;
+        const int64_t r0 = (item - a.item_off[g]) * R;
+        const int nr = (int)(N - r0 < R ? N - r0 : R);
+        mbar_arrive_expect_tx_relaxed(&full[st], (uint32_t)nr * (uint32_t)d * 4u);
+        for (int r = 0; r < nr; ++r)
+            bulk_load_row(ring + st * stage_floats + (size_t)r * d, row_ptr(q, r0 + r), (uint32_t)d * 4u, &full[st]);
+    };
+    if (tid == 0)
+        for (int k = 0; k < kSStages && i0 + k < i1; ++k) issue(i0 + k, k);
+    long long acc[G4][4];
+#pragma unroll
+    for (int k = 0; k < G4; ++k)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[k][e] = 0;
+    int cur = -1;  // 2 * pair + side of the register sums
+    auto flush = [&]() {
+        if (cur < 0) return;
+        long long* dst = a.p[cur >> 1].acc + (cur & 1) * d;
+#pragma unroll
+        for (int k = 0; k < G4; ++k) {
+            const int c4 = tid + k * kS1Threads;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                if (c4 < d4 && acc[k][e] != 0)
+                    atomicAdd(reinterpret_cast<unsigned long long*>(dst + 4 * c4 + e), (unsigned long long)acc[k][e]);
+                acc[k][e] = 0;
+            }
+        }
+    };
+    for (int64_t item = i0; item < i1; ++item) {
+        const int64_t k = item - i0;
+        const int st = (int)(k % kSStages);
+        const int g = pair_of(a, item);
+        const AlignPair& q = a.p[g];
+        const int64_t N = q.n_x + q.n_y;
+        const int64_t r0 = (item - a.item_off[g]) * R;
+        const int nr = (int)(N - r0 < R ? N - r0 : R);
+        const float4* tile = reinterpret_cast<const float4*>(ring + st * stage_floats);
+        mbar_wait(&full[st], (uint32_t)((k / kSStages) & 1));
+        double v[R][G4][4];
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int kk = 0; kk < G4; ++kk) {
+                const int c4 = tid + kk * kS1Threads;
+                float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (r < nr && c4 < d4) f = tile[(size_t)r * d4 + c4];
+                v[r][kk][0] = (double)f.x;
+                v[r][kk][1] = (double)f.y;
+                v[r][kk][2] = (double)f.z;
+                v[r][kk][3] = (double)f.w;
+            }
+        __syncthreads();  // the stage is in registers: refill it
+        if (tid == 0 && item + kSStages < i1) issue(item + kSStages, st);
+        // row norms: per-thread partial squares, warp tree, then the warps in order
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            double sq0 = 0.0, sq1 = 0.0;
+#pragma unroll
+            for (int kk = 0; kk < G4; ++kk) {
+                sq0 += v[r][kk][0] * v[r][kk][0] + v[r][kk][1] * v[r][kk][1];
+                sq1 += v[r][kk][2] * v[r][kk][2] + v[r][kk][3] * v[r][kk][3];
+            }
+            const double sq = warp_sum(sq0 + sq1);
+            if (lane == 0) s_part[warp][r] = sq;
+        }
+        __syncthreads();
+        if (tid < nr) {
+            double ss = 0.0;
+#pragma unroll
+            for (int w = 0; w < W; ++w) ss += s_part[w][tid];
+            const double nrm = sqrt(ss);
+            const double iv = nrm >= 1e-12 ? 1.0 / nrm : 0.0;
+            s_inv[tid] = iv;
+            q.inv[r0 + tid] = iv;
+            if (nrm < 1e-12) atomicMin(q.bad, (long long)(r0 + tid));
+        }
+        __syncthreads();
+        double iv[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) iv[r] = r < nr ? s_inv[r] : 0.0;
+        const int64_t nxr64 = q.n_x - r0;
+        const int nxr = nxr64 <= 0 ? 0 : (nxr64 >= nr ? nr : (int)nxr64);
+        if (nxr == 0 || nxr == nr) {  // the whole item on one side (all but <= 1 item per pair)
+            const int code = 2 * g + (nxr == 0 ? 1 : 0);
+            if (code != cur) {
+                flush();
+                cur = code;
+            }
+#pragma unroll
+            for (int kk = 0; kk < G4; ++kk)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    double p0 = 0.0, p1 = 0.0;
+#pragma unroll
+                    for (int r = 0; r < R; r += 2) {
+                        p0 += v[r][kk][e] * iv[r];
+                        if (r + 1 < R) p1 += v[r + 1][kk][e] * iv[r + 1];
+                    }
+                    acc[kk][e] += __double2ll_rn((p0 + p1) * kFixScale);
+                }
+        } else {
+#pragma unroll
+            for (int side = 0; side < 2; ++side) {
+                const int lo = side ? nxr : 0, hi = side ? nr : nxr;
+                const int code = 2 * g + side;
+                if (code != cur) {
+                    flush();
+                    cur = code;
+                }
+#pragma unroll
+                for (int kk = 0; kk < G4; ++kk)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        double p = 0.0;
+#pragma unroll
+                        for (int r = 0; r < R; ++r)
+                            if (r >= lo && r < hi) p += v[r][kk][e] * iv[r];
+                        acc[kk][e] += __double2ll_rn(p * kFixScale);
+                    }
+            }
+        }
+    }
+    flush();
+    // the last CTA forms every pair's means, axis, centre and observed statistic
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(reinterpret_cast<unsigned*>(a.scratch + 3), 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
+        for (int g = 0; g < a.G; ++g) stream_pair_scalars<kS1Threads>(a, g, red);
+        if (tid == 0) reinterpret_cast<unsigned*>(a.scratch + 3)[0] = 0u;
+    }
+    __syncthreads();
+    if (tid == 0) span_exit(a.span);
+}
+
+// KS2: {2 u.x_i, 1/||h_i||} per pooled row (Y rows and identity pairs: coefficient 0).  The
+// CTAs are split among the pairs in proportion to their X rows; a warp takes one X row
+// (fp64 dot with u staged in shared memory) with 8 column steps of 16 bytes in flight per
+// lane, so an SM has ~30 rows streaming at once.
+__global__ void __launch_bounds__(256) k1s_coef(AlignArgs a, int ctas_per_pair0, int ctas_per_pair1,
+                                                int ctas_per_pair2, int ctas_per_pair3) {
+    extern __shared__ __align__(16) uint8_t kc_smem[];
+    double* su = reinterpret_cast<double*>(kc_smem);  // [d_pad]
+    const int cpp[4] = {ctas_per_pair0, ctas_per_pair1, ctas_per_pair2, ctas_per_pair3};
+    int g = 0, c0 = 0;
+    while (g < a.G - 1 && (int)blockIdx.x >= c0 + cpp[g]) c0 += cpp[g++];
+    const int nct = cpp[g], cta = blockIdx.x - c0;
+    const AlignPair& q = a.p[g];
+    const int d = (int)a.d;
+    const int64_t N = q.n_x + q.n_y;
+    if (threadIdx.x == 0) span_enter(a.span);
+    const bool identity = q.info->is_identity != 0;
+    // rows without a reflection: {0, 1/||h||}
+    for (int64_t i = (int64_t)cta * blockDim.x + threadIdx.x; i < N; i += (int64_t)nct * blockDim.x)
+        if (identity || i >= q.n_x) q.coef[i] = make_float2(0.f, (float)__ldcg(q.inv + i));
+    if (!identity) {
+        for (int c = threadIdx.x; c < (int)a.d_pad; c += blockDim.x) su[c] = q.u[c];
+        __syncthreads();
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+        const int n4 = d / 4;
+        const double2* su2 = reinterpret_cast<const double2*>(su);
+        for (int64_t i = (int64_t)cta * nw + warp; i < q.n_x; i += (int64_t)nct * nw) {
+            const float4* rp = reinterpret_cast<const float4*>(q.X + i * d);
+            double dot0 = 0.0, dot1 = 0.0;
+            for (int c4b = 0; c4b < n4; c4b += 32 * 8) {
+                float4 h[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int c4 = c4b + 32 * u + lane;
+                    h[u] = c4 < n4 ? __ldcs(rp + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int c4 = c4b + 32 * u + lane;
+                    if (c4 < n4) {
+                        const double2 ua = su2[2 * c4], ub = su2[2 * c4 + 1];
+                        dot0 += (double)h[u].x * ua.x + (double)h[u].y * ua.y;
+                        dot1 += (double)h[u].z * ub.x + (double)h[u].w * ub.y;
+                    }
+                }
+            }
+            const double dot = warp_sum(dot0 + dot1);
+            if (lane == 0) {
+                const double iv = __ldcg(q.inv + i);
+                q.coef[i] = make_float2((float)(2.0 * dot * iv), (float)iv);
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) span_exit(a.span);
+}
+
+// KS3: tiles (pair, column strip of 64, row block of 128) in that order; CTA c takes tiles
+// [T c / grid, T (c+1) / grid).  The raw fp32 tiles stream into a 3-stage shared-memory
+// ring with cp.async (two tiles in flight per CTA); 512 threads.  Transform thread = (row
+// pair 2p, 2p + 1; columns 4 q .. 4 q + 3) x 2 row pairs: z' = x - coef u - m (fp32), bf16
+// hi/lo, each column's two rows packed into one 32-bit word of a TRANSPOSED staging tile
+// [column][row]; writing thread = (column, 16 rows): two 16-byte shared loads per plane and
+// two 16-byte global stores (8 threads cover a column's 256-byte run per plane).  t' per
+// column and tile in fp64 (exact: hi + lo has <= 16 significant bits), rounded per tile to
+// fixed point, summed as int64 over the CTA's tiles of one strip, one atomic per column per
+// strip run.
+constexpr int kXfStages = 3;
+constexpr int kXfTP = kXfRows + 2;  // u16 pitch of the transposed staging (65 words)
+constexpr size_t kXfSmem = (size_t)kXfStages * kXfRows * kXfCols * 4 + (size_t)kXfStages * kXfRows * 8 +
+                           2 * (size_t)kXfCols * kXfTP * 2;
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// the fields of one pair that KS3 touches per tile, cached in registers
+struct XfPair {
+    const float* X;
+    const float* Y;
+    const float2* coef;
+    uint16_t* zhi;
+    uint16_t* zlo;
+    long long* tacc;
+    int n_x, N, n_pad, rtiles;
+};
+
+__global__ void __launch_bounds__(kThreads, 1) k1s_xform(AlignArgs a, int64_t tile_off1, int64_t tile_off2,
+                                                         int64_t tile_off3, int64_t tiles_total) {
+    extern __shared__ __align__(16) uint8_t xf_smem[];
+    float* raw = reinterpret_cast<float*>(xf_smem);  // [kXfStages][128][64]
+    float2* rcoef = reinterpret_cast<float2*>(raw + kXfStages * kXfRows * kXfCols);  // [kXfStages][128]
+    uint16_t* sh_hi = reinterpret_cast<uint16_t*>(rcoef + kXfStages * kXfRows);  // [64][kXfTP]
+    uint16_t* sh_lo = sh_hi + kXfCols * kXfTP;
+    __shared__ double red[2 * kWarps + 2];
+    __shared__ int s_last;
+    const int tid = threadIdx.x;
+    const int d = (int)a.d, d_pad = (int)a.d_pad;
+    const int64_t t0 = tiles_total * blockIdx.x / gridDim.x, t1 = tiles_total * (blockIdx.x + 1) / gridDim.x;
+    if (tid == 0) span_enter(a.span);
+    // copy role: rows lr + 32 k (k < 4), columns 4 lc4 .. 4 lc4 + 3
+    const int lc4 = tid & 15, lr = tid >> 4;
+    // transform role: row pairs (2 tp, 2 tp + 1) and (64 + 2 tp, 65 + 2 tp), columns 4 tq ..
+    const int tq = tid & 15, tp = tid >> 4;
+    // write role: column wc, rows 8 wg .. 8 wg + 7 and 64 + 8 wg .. 64 + 8 wg + 7
+    const int wg = tid & 7, wc = tid >> 3;
+    const int strips = (d_pad + kXfCols - 1) / kXfCols;
+    auto pair_fields = [&](int g) {
+        const AlignPair& q = a.p[g];
+        XfPair P;
+        P.X = q.X;
+        P.Y = q.Y;
+        P.coef = q.coef;
+        P.zhi = q.zt_hi;
+        P.zlo = q.zt_lo;
+        P.tacc = q.acc + 2 * d;
+        P.n_x = (int)q.n_x;
+        P.N = (int)(q.n_x + q.n_y);
+        P.n_pad = (int)q.n_pad;
+        P.rtiles = (int)((q.n_pad + kXfRows - 1) / kXfRows);
+        return P;
+    };
+    struct TileAt {
+        int g, strip, rt;
+    };
+    auto locate = [&](int64_t t) {  // once per CTA (offsets of absent pairs are tiles_total)
+        TileAt L;
+        L.g = (t >= tile_off1) + (t >= tile_off2) + (t >= tile_off3);
+        const int64_t lt = t - (L.g == 0 ? 0 : L.g == 1 ? tile_off1 : L.g == 2 ? tile_off2 : tile_off3);
+        const int64_t rtiles = (a.p[L.g].n_pad + kXfRows - 1) / kXfRows;
+        L.strip = (int)(lt / rtiles);
+        L.rt = (int)(lt % rtiles);
+        return L;
+    };
+    TileAt Ld = locate(t0);  // the loader's position and its pair
+    XfPair Pl = pair_fields(Ld.g);
+    auto load = [&](int64_t t, int slot) {  // this thread's 4 pieces of tile t (+ coefficients)
+        if (t < t1) {
+            const int r0 = Ld.rt * kXfRows, c = Ld.strip * kXfCols + 4 * lc4;
+            float* dst = raw + (size_t)slot * kXfRows * kXfCols + 4 * lc4;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int i = r0 + lr + 32 * k;
+                if (i < Pl.N && c < d) {
+                    const float* src = i < Pl.n_x ? Pl.X + (size_t)i * d : Pl.Y + (size_t)(i - Pl.n_x) * d;
+                    cp_async16(dst + (lr + 32 * k) * kXfCols, src + c);
+                }
+            }
+            if (tid < kXfRows / 2 && r0 + 2 * tid < Pl.n_pad)  // {coef, 1/||h||} of the rows (n_pad long)
+                cp_async16(rcoef + slot * kXfRows + 2 * tid, Pl.coef + r0 + 2 * tid);
+            if (++Ld.rt == Pl.rtiles) {  // advance
+                Ld.rt = 0;
+                if (++Ld.strip == strips) {
+                    Ld.strip = 0;
+                    if (++Ld.g < a.G) Pl = pair_fields(Ld.g);
+                }
+            }
+        }
+        cp_async_commit();
+    };
+#pragma unroll
+    for (int k = 0; k < kXfStages - 1; ++k) load(t0 + k, k);
+    long long tacc = 0;  // fixed-point t' of column wc of the current strip (wg == 0 lanes)
+    TileAt L = locate(t0);
+    XfPair P = pair_fields(L.g);
+    int cur_g = -1, cur_strip = -1;
+    float4 u4 = make_float4(0.f, 0.f, 0.f, 0.f), m4 = u4;
+    auto flush = [&]() {
+        const int c = cur_strip * kXfCols + wc;
+        if (cur_g >= 0 && wg == 0 && c < d_pad && tacc != 0)
+            atomicAdd(reinterpret_cast<unsigned long long*>(P.tacc + c), (unsigned long long)tacc);
+        tacc = 0;
+    };
+    int slot = 0;
+    for (int64_t t = t0; t < t1; ++t) {
+        if (L.g != cur_g || L.strip != cur_strip) {
+            flush();
+            if (L.g != cur_g) P = pair_fields(L.g);
+            cur_g = L.g;
+            cur_strip = L.strip;
+            const AlignPair& q = a.p[L.g];
+            float uu[4], mm[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int c = L.strip * kXfCols + 4 * tq + k;
+                uu[k] = c < d ? (float)__ldcg(q.u + c) : 0.f;
+                mm[k] = c < d ? (float)__ldcg(q.m + c) : 0.f;
+            }
+            u4 = make_float4(uu[0], uu[1], uu[2], uu[3]);
+            m4 = make_float4(mm[0], mm[1], mm[2], mm[3]);
+        }
+        const int r0 = L.rt * kXfRows, cb = L.strip * kXfCols;
+        cp_async_wait<kXfStages - 2>();  // this thread's pieces of tile t have landed
+        __syncthreads();                 // ... and every thread's (rows, coefficients)
+        const float* rt_raw = raw + (size_t)slot * kXfRows * kXfCols;
+        const bool cvalid = cb + 4 * tq < d;
+#pragma unroll
+        for (int hp = 0; hp < 2; ++hp) {  // row pairs (2 tp, 2 tp + 1) + 64 hp
+            const int ra = 64 * hp + 2 * tp;
+            float z[2][4];
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const int rr = ra + k;
+                if (r0 + rr < P.N && cvalid) {
+                    const float4 h = *reinterpret_cast<const float4*>(rt_raw + rr * kXfCols + 4 * tq);
+                    const float2 cv = rcoef[slot * kXfRows + rr];  // {coef, 1/||h||}
+                    z[k][0] = fmaf(-cv.x, u4.x, h.x * cv.y) - m4.x;
+                    z[k][1] = fmaf(-cv.x, u4.y, h.y * cv.y) - m4.y;
+                    z[k][2] = fmaf(-cv.x, u4.z, h.z * cv.y) - m4.z;
+                    z[k][3] = fmaf(-cv.x, u4.w, h.w * cv.y) - m4.w;
+                } else {
+                    z[k][0] = z[k][1] = z[k][2] = z[k][3] = 0.f;
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {  // column 4 tq + e: rows ra, ra + 1 in one word
+                const __nv_bfloat162 hh = __floats2bfloat162_rn(z[0][e], z[1][e]);
+                const float2 hf = __bfloat1622float2(hh);
+                const __nv_bfloat162 ll = __floats2bfloat162_rn(z[0][e] - hf.x, z[1][e] - hf.y);
+                const int w = (4 * tq + e) * (kXfTP / 2) + (ra >> 1);
+                reinterpret_cast<uint32_t*>(sh_hi)[w] = *reinterpret_cast<const uint32_t*>(&hh);
+                reinterpret_cast<uint32_t*>(sh_lo)[w] = *reinterpret_cast<const uint32_t*>(&ll);
+            }
+        }
+        __syncthreads();  // planes staged (transposed); the ring slot of tile t is free
+        load(t + kXfStages - 1, slot == 0 ? kXfStages - 1 : slot - 1);
+        {
+            const int col = cb + wc;
+            double tv = 0.0;
+#pragma unroll
+            for (int hb = 0; hb < 2; ++hb) {
+                const int rb = 64 * hb + 8 * wg;
+                if (r0 + rb < P.n_pad) {  // (the last row block of a pair may be half: n_pad % 128 = 64)
+                    // 8 rows = 16 bytes per plane; the staging rows are 4-byte aligned (65-word
+                    // pitch), so two 8-byte loads
+                    const uint32_t* hs = reinterpret_cast<const uint32_t*>(sh_hi) + wc * (kXfTP / 2) + (rb >> 1);
+                    const uint32_t* ls = reinterpret_cast<const uint32_t*>(sh_lo) + wc * (kXfTP / 2) + (rb >> 1);
+                    const uint4 hv = make_uint4(hs[0], hs[1], hs[2], hs[3]);
+                    const uint4 lv = make_uint4(ls[0], ls[1], ls[2], ls[3]);
+                    const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w}, lw[4] = {lv.x, lv.y, lv.z, lv.w};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        tv += (double)(__uint_as_float(hw[j] << 16) + __uint_as_float(lw[j] << 16));
+                        tv += (double)(__uint_as_float(hw[j] & 0xFFFF0000u) + __uint_as_float(lw[j] & 0xFFFF0000u));
+                    }
+                    if (col < d_pad) {
+                        const size_t off = (size_t)col * (size_t)P.n_pad + (size_t)(r0 + rb);  // u16 elements
+                        *reinterpret_cast<uint4*>(P.zhi + off) = hv;
+                        *reinterpret_cast<uint4*>(P.zlo + off) = lv;
+                    }
+                }
+            }
+            // fixed-order sum of the column's 8 row groups (adjacent lanes)
+            tv += __shfl_xor_sync(0xffffffffu, tv, 1);
+            tv += __shfl_xor_sync(0xffffffffu, tv, 2);
+            tv += __shfl_xor_sync(0xffffffffu, tv, 4);
+            tacc += __double2ll_rn(tv * kFixScale);
+        }
+        __syncthreads();  // the plane staging is free
+        slot = slot + 1 == kXfStages ? 0 : slot + 1;
+        if (++L.rt == P.rtiles) {
+            L.rt = 0;
+            if (++L.strip == strips) {
+                L.strip = 0;
+                ++L.g;
+            }
+        }
+    }
+    cp_async_wait<0>();
+    flush();
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(reinterpret_cast<unsigned*>(a.scratch + 1), 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
+        finish_pairs(a, red);
+    }
+    __syncthreads();
+    if (tid == 0) span_exit(a.span);
+}
 }  // namespace
 
 AlignGeom align_geometry(int64_t d) {
@@ -645,6 +1249,88 @@ AlignGeom align_geometry(int64_t d) {
     return g;
 }
 
+
+// ---- K1s host side -------------------------------------------------------------------
+// every pipeline kernel asks for the whole unified L1/shared array as shared memory, so the
+// SM's carveout leaves room for the other lane's / next block's CTAs (see k_maskgemm.cu)
+static cudaError_t max_carveout(const void* fn) {
+    return cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+}
+bool align_stream_pair(int64_t N, int64_t d) {
+    return d % 4 == 0 && d <= 4096 && round_up(N, kKBlock) * d >= kStreamMinElems;
+}
+
+bool align_uses_stream(const AlignArgs& a) {
+    if (a.do_draws || a.stamps) return false;  // experiments / K1 phase stamps: fused kernel only
+    for (int g = 0; g < a.G; ++g) {
+        const AlignPair& q = a.p[g];
+        if (!align_stream_pair(q.n_x + q.n_y, a.d)) return false;
+        if ((reinterpret_cast<uintptr_t>(q.X) | reinterpret_cast<uintptr_t>(q.Y)) & 15u) return false;
+    }
+    return true;
+}
+
+int align_launch_count(const AlignArgs& a) { return align_uses_stream(a) ? 3 : 1; }
+
+static cudaError_t launch_align_stream(AlignArgs a, int sm_count, cudaStream_t st) {
+    const int d = (int)a.d;
+    const int g4 = (int)ceil_div(d / 4, kS1Threads);  // float4 column groups per thread
+    const int G4t = g4 <= 1 ? 1 : g4 <= 2 ? 2 : 4;     // template instance
+    const int R = 8 / G4t;                              // rows per item (= the kernel's)
+    a.item_off[0] = 0;
+    for (int g = 0; g < a.G; ++g) a.item_off[g + 1] = a.item_off[g] + ceil_div(a.p[g].n_x + a.p[g].n_y, R);
+    const int64_t items = a.item_off[a.G];
+    const size_t smem1 = 128 + (size_t)kSStages * R * d * 4;
+    const void* fn = G4t == 1 ? (const void*)k1s_stats<1>
+                     : G4t == 2 ? (const void*)k1s_stats<2>
+                                : (const void*)k1s_stats<4>;
+    static size_t configured[3] = {0, 0, 0};
+    const int fi = G4t == 1 ? 0 : G4t == 2 ? 1 : 2;
+    cudaError_t e;
+    if (smem1 > configured[fi]) {
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
+        if (e == cudaSuccess) e = max_carveout(fn);
+        if (e != cudaSuccess) return e;
+        configured[fi] = smem1;
+    }
+    {
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(items, 2ll * sm_count));
+        void* args[] = {&a};
+        e = cudaLaunchKernel(fn, dim3(grid), dim3(kS1Threads), args, smem1, st);
+        if (e != cudaSuccess) return e;
+    }
+    {  // KS2: CTAs in proportion to the pairs' rows, ~4 per SM in total
+        int cpp[kMaxWave] = {0, 0, 0, 0}, total = 0;
+        for (int g = 0; g < a.G; ++g) {  // one warp per X row (8 warps per CTA)
+            cpp[g] = (int)std::max<int64_t>(1, ceil_div(a.p[g].n_x, 8));
+            total += cpp[g];
+        }
+        const size_t smem2 = (size_t)a.d_pad * 8;
+        k1s_coef<<<total, 256, smem2, st>>>(a, cpp[0], cpp[1], cpp[2], cpp[3]);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    {  // KS3
+        const int64_t strips = ceil_div(a.d_pad, kXfCols);
+        int64_t off[kMaxWave + 1] = {0, 0, 0, 0, 0};
+        for (int g = 0; g < a.G; ++g) off[g + 1] = off[g] + strips * ceil_div(a.p[g].n_pad, kXfRows);
+        for (int g = a.G + 1; g <= kMaxWave; ++g) off[g] = off[a.G];
+        const int64_t total = off[a.G];
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(total, sm_count));
+        static bool xf_configured = false;
+        if (!xf_configured) {
+            e = cudaFuncSetAttribute(k1s_xform, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kXfSmem);
+            if (e == cudaSuccess) e = max_carveout((const void*)k1s_xform);
+            if (e == cudaSuccess) e = max_carveout((const void*)k1s_coef);
+            if (e != cudaSuccess) return e;
+            xf_configured = true;
+        }
+        k1s_xform<<<grid, kThreads, kXfSmem, st>>>(a, off[1], off[2], off[3], total);
+        e = cudaGetLastError();
+    }
+    return e;
+}
+
 // Cooperative grids of different streams could each be partly resident and wait for each
 // other's SMs at their grid barriers; every K1 launch of the process is therefore ordered
 // after the previous one on the device (an event chain; K1 is latency-bound and short).
@@ -658,6 +1344,7 @@ void align_items(AlignArgs& a) {
 }
 
 cudaError_t launch_align(const AlignArgs& a, int grid, cudaStream_t st) {
+    if (align_uses_stream(a)) return launch_align_stream(a, grid, st);
     const AlignGeom g = align_geometry(a.d);
     int dev = 0;
     cudaGetDevice(&dev);
@@ -676,8 +1363,11 @@ cudaError_t launch_align(const AlignArgs& a, int grid, cudaStream_t st) {
                                    : (const void*)k1_align_fused<2>;
     static size_t configured[5] = {0, 0, 0, 0, 0};
     const int fi = g.rows == 16 ? 4 : g.rows == 8 ? 3 : g.rows == 4 ? 2 : 1;
-    if (g.smem > 48 * 1024 && g.smem > configured[fi]) {
-        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
+    if (g.smem > configured[fi]) {
+        cudaError_t e = g.smem > 48 * 1024
+                            ? cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem)
+                            : cudaSuccess;
+        if (e == cudaSuccess) e = max_carveout(fn);
         if (e != cudaSuccess) return e;
         configured[fi] = g.smem;
     }

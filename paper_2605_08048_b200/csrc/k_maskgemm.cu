@@ -568,6 +568,12 @@ cudaError_t launch_impl(const GemmMaps& maps, const GemmArgs& g, cudaStream_t st
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(k3_maskgemm<kPair>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem);
+        // the whole unified L1/shared array as shared memory: with the default (smallest
+        // sufficient) carveout an SM running a mask-GEMM CTA has no room left for the
+        // generator / alignment CTAs of the next block, which then wait for it to finish
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k3_maskgemm<kPair>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     cudaSharedmemCarveoutMaxShared);
         if (e != cudaSuccess) return e;
         configured = true;
     }

@@ -555,6 +555,13 @@ cudaError_t launch_perm(const PermArgs& a, int sm_count, cudaStream_t st) {
         if (e != cudaSuccess) return e;
         configured[fi] = smem;
     }
+    static bool carve[10] = {};
+    if (!carve[fi]) {  // max shared carveout, so generator CTAs fit beside a mask-GEMM CTA
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                             cudaSharedmemCarveoutMaxShared);
+        if (e != cudaSuccess) return e;
+        carve[fi] = true;
+    }
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nw * 32, smem);
     per_sm = std::max(1, std::min(per_sm, a.max_ctas_per_sm > 0 ? a.max_ctas_per_sm : per_sm));
