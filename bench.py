@@ -496,12 +496,12 @@ def run_c3(args, E, peaks):
     counts = torch.zeros((K, 3), dtype=torch.int64, device=E.dev)
     scratch = torch.zeros(3, dtype=torch.int64, device=E.dev)
 
-    def step(k, out, X=None, Y=None):
+    def step(k, out, X=None, Y=None, combine=False):
+        """align (every rank: the same deterministic planes) + this rank's b-range; with
+        combine, one all-reduce of the 3 counts (parallel.gpu_range_counts)"""
         Xs, Ys = dev_pool[k % 2] if X is None else (X, Y)
-        info = infos[k % 2]
-        hap.hap_align(E.ctx.h, Xs, Ys, hap.HAP_ALIGN_HOUSEHOLDER, info, stream=E.st)
-        cfg = hap.make_cfg(HI.PERM_SEED, B, b0, b1, stream_id=k)
-        hap.hap_permtest(E.ctx.h, info, cfg, out, None, stream=E.st)
+        parallel.gpu_range_counts(E.ctx, Xs, Ys, B, HI.PERM_SEED, E.rank, E.world, out,
+                                  infos[k % 2], stream_id=k, stream=E.st, reduce=combine)
 
     for k in range(W):
         step(k, scratch)
@@ -509,9 +509,7 @@ def run_c3(args, E, peaks):
     hap.hap_profile_read(E.ctx.h, reset=True)
 
     def timed_step(k):
-        step(k, counts[k])
-        if E.world > 1:
-            E.dist.all_reduce(counts[k])  # one combine per test (b-range shards)
+        step(k, counts[k], combine=True)
 
     ms, tw0, tw1 = E.timed(timed_step, K)
     launches = hap.hap_profile_read(E.ctx.h, reset=True)[1]
@@ -533,9 +531,7 @@ def run_c3(args, E, peaks):
     E.barrier()
     t0 = time.perf_counter()
     for k in range(Ke):
-        step(k, dcounts[k], Xh[k % 2], Yh[k % 2])
-        if E.world > 1:
-            E.dist.all_reduce(dcounts[k])
+        step(k, dcounts[k], Xh[k % 2], Yh[k % 2], combine=True)
         hcounts[k].copy_(dcounts[k], non_blocking=True)
     torch.cuda.synchronize()
     e2e_s = E.max_over_ranks(time.perf_counter() - t0)
@@ -603,7 +599,6 @@ def run_batch_workload(args, E, peaks, name):
     mine = parallel.lpt_assign(costs, E.world)[E.rank]
     iw = hap.INFO_BYTES // 8
     nm = len(modes)
-    buf = torch.zeros((K, nm, P, iw + 3), dtype=torch.int64, device=E.dev)
     infos = torch.zeros((nm, P, hap.INFO_BYTES), dtype=torch.uint8, device=E.dev)
     dcounts = torch.zeros((nm, P, 3), dtype=torch.int64, device=E.dev)
 
@@ -619,14 +614,15 @@ def run_batch_workload(args, E, peaks, name):
     torch.cuda.synchronize()
     hap.hap_profile_read(E.ctx.h, reset=True)
 
+    results = []
+
     def timed_step(k):
-        dcounts.zero_()
-        step(k)
-        buf[k, :, :, :iw].copy_(infos.view(torch.int64).view(nm, P, iw))
-        buf[k, :, :, iw:].copy_(dcounts)
-        if k == K - 1 and E.world > 1:
-            # every row is written by exactly one rank (zero elsewhere): the sum is the union
-            E.dist.all_reduce(buf)
+        # parallel.gpu_batch_sharded: this rank's LPT share in ONE hap_permtest_batch call,
+        # then one all-reduce of int64[P, info + 3] rows (each written by exactly one rank)
+        for mi, mode in enumerate(modes):
+            results.append(parallel.gpu_batch_sharded(
+                E.ctx, Xd, cnx, Yd, cny, B, HI.PERM_SEED, E.rank, E.world,
+                stream_id=((k * nm + mi) * P) & 0xFFFFFFFF, mode=mode))
 
     ms, tw0, tw1 = E.timed(timed_step, K)
     launches = hap.hap_profile_read(E.ctx.h, reset=True)[1]
@@ -673,8 +669,9 @@ def run_batch_workload(args, E, peaks, name):
     cfg_out = {"workload": workload_desc(name, 0), "pairs": P, "B": B, "d": 768,
                "global_batch": P * nm, "l2": l2,
                "parallelism": f"pairs LPT-assigned (cost n_x+n_y) over {E.world} rank(s), one "
-                              "hap_permtest_batch per rank; one all_reduce of int64[K, modes, "
-                              "P, info+3] rows (each written by one rank)",
+                              "hap_permtest_batch per rank and mode per step, then one "
+                              "all_reduce of int64[P, info+3] rows (each written by one rank): "
+                              "parallel.gpu_batch_sharded",
                "input_pool": (f"pair p = first n_p rows of pool pair p % 8 (8 distinct "
                               "5000/5000 vMF pairs)") if name == "c4" else
                f"{len(pool)} distinct pairs repeated"}

@@ -40,6 +40,11 @@ struct hap_ctx_s {
     // the mask slot it overwrites; K3 joins it with an event wait
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_ready[2] = {}, ev_free[2] = {};
+    // hap_permtest's mask-GEMM stream (highest priority): when a mask-GEMM ends, the next
+    // block's mask-GEMM and the generator of the block after it become ready together, and
+    // the block scheduler must place the GEMM's CTAs first
+    cudaStream_t hi = nullptr;
+    cudaEvent_t ev_hi[2] = {};
     int slot = 0;
     bool used[2] = {false, false};
     // batch pipeline: two lanes (internal streams forked from / joined to the caller's
@@ -565,6 +570,9 @@ hap_status hap_destroy(hap_ctx c) {
         if (c->ev_copied[i]) cudaEventDestroy(c->ev_copied[i]);
     }
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->hi) cudaStreamDestroy(c->hi);
+    for (auto e : c->ev_hi)
+        if (e) cudaEventDestroy(e);
     for (int i = 0; i < 2; ++i) {
         if (c->ev_ready[i]) cudaEventDestroy(c->ev_ready[i]);
         if (c->ev_free[i]) cudaEventDestroy(c->ev_free[i]);
@@ -986,11 +994,46 @@ hap_status hap_permtest(hap_ctx c, hap_align_info* info, const hap_perm_cfg* cfg
     const int pair = cfg->pair_mode ? cfg->pair_mode : 2;
     const int64_t R = (int64_t)kTileM * pair;
     const int64_t total = (int64_t)(cfg->b_end - cfg->b_begin);
-    const int64_t blk = block_tiles(cfg, c->n_pad, R) * (R - 1);
-    for (int64_t off = 0; off < total; off += blk) {
+    const int64_t max_tiles = block_tiles(cfg, c->n_pad, R);
+    const int64_t total_tiles = ceil_div(std::max<int64_t>(total, 1), R - 1);
+    // Block schedule: the generator of block i+1 runs beside the mask-GEMM of block i (side
+    // stream, two mask slots), but block 0's generator and the alignment have nothing to hide
+    // behind.  A long test therefore starts with a small block and grows it geometrically
+    // (x1.75: the generator, slowed ~2x beside a mask-GEMM, still finishes within the
+    // previous block's GEMM) up to the L2-sized maximum; an explicit cfg->block is kept as
+    // given.  Results do not depend on the blocking (PERM-SPEC v1 is addressed by b).
+    int64_t tiles = max_tiles;
+    const bool grow = !cfg->block && total_tiles >= 16;
+    if (grow) tiles = std::min<int64_t>(max_tiles, std::max<int64_t>(4, total_tiles / 12));
+    // the blocks' mask-GEMMs run on the context's high-priority stream, forked from and
+    // joined back to `st`
+    cudaStream_t ks = st;
+    if (total_tiles > tiles) {
+        if (!c->hi) {
+            int lo_p = 0, hi_p = 0;
+            cudaDeviceGetStreamPriorityRange(&lo_p, &hi_p);
+            if (cudaStreamCreateWithPriority(&c->hi, cudaStreamNonBlocking, hi_p) != cudaSuccess ||
+                cudaEventCreateWithFlags(&c->ev_hi[0], cudaEventDisableTiming) != cudaSuccess ||
+                cudaEventCreateWithFlags(&c->ev_hi[1], cudaEventDisableTiming) != cudaSuccess)
+                return fail(c, HAP_E_CUDA, "mask-GEMM stream");
+        }
+        cudaError_t e = cudaEventRecord(c->ev_hi[0], st);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(c->hi, c->ev_hi[0], 0);
+        if (e != cudaSuccess) return cuda_fail(c, e, "fork");
+        ks = c->hi;
+    }
+    for (int64_t off = 0; off < total;) {
+        const int64_t blk = tiles * (R - 1);
         const WaveTest t{c, info, cfg, counts, stats ? stats + 3 * off : nullptr,
                          cfg->b_begin + (uint64_t)off, std::min<int64_t>(blk, total - off)};
-        if ((s = run_wave(c, 1, &t, pair, st))) return s;
+        if ((s = run_wave(c, 1, &t, pair, ks))) return s;
+        off += blk;
+        if (grow) tiles = std::min<int64_t>(max_tiles, (tiles * 7 + 3) / 4);
+    }
+    if (ks != st) {
+        cudaError_t e = cudaEventRecord(c->ev_hi[1], ks);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, c->ev_hi[1], 0);
+        if (e != cudaSuccess) return cuda_fail(c, e, "join");
     }
     c->last_stream = st;
     return HAP_OK;
