@@ -114,6 +114,20 @@ typedef struct {
  * p_exact = exceed_ge / C(N, n_x).  HAP_E_INVALID_ARG otherwise. */
 #define HAP_FLAG_EXHAUSTIVE 2u
 
+/* K3 arithmetic:
+ * the statistic needs only S1 = ||sigma1||^2 and S2 = ||sigma2||^2 of the group sums, and
+ * with the centred pooled rows z'_i, ||sum_{i in G_b} z'_i||^2 = m_b^T (Z' Z'^T) m_b is a
+ * quadratic form in the N x N Gram matrix.  The GRAM form multiplies the mask block by
+ * Z' Z'^T (bf16 hi/lo of fp64-combined sums, N_pad x N_pad) instead of Z' (N_pad x d_pad):
+ * 4 N_pad^2 instead of 4 N_pad d_pad issued tensor FLOP per permutation, for N << d.
+ * By default hap_permtest / hap_permtest_batch choose it per test from (n_pad, d_pad,
+ * cfg->B) when it saves time (never for 2 n_pad > d_pad); HAP_FLAG_GRAM forces it
+ * (needs n_pad <= 4096), HAP_FLAG_NO_GRAM forbids it.  Both forms meet the same parity
+ * bar; their statistics differ in rounding only, so flag a test consistently over its
+ * shards (the automatic choice uses cfg->B, the whole test's permutation count). */
+#define HAP_FLAG_GRAM 4u
+#define HAP_FLAG_NO_GRAM 8u
+
 /* Exceedance counters of one test, DEVICE memory, ADDED into (caller zeroes them), so
  * shards and resumed ranges compose by summation (Eq. pvalue). */
 typedef struct {

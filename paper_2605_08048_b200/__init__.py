@@ -165,6 +165,13 @@ def hap_align(ctx, X, Y, mode: int, info, stream=None) -> None:
 
 HAP_FLAG_SHARED_MASK = 1
 HAP_FLAG_EXHAUSTIVE = 2
+HAP_FLAG_GRAM = 4
+HAP_FLAG_NO_GRAM = 8
+
+
+def gram_flags(gram) -> int:
+    """None: the library chooses the K3 form; True: Gram form; False: plane form."""
+    return 0 if gram is None else (HAP_FLAG_GRAM if gram else HAP_FLAG_NO_GRAM)
 
 
 def make_cfg(seed: int, B: int, b_begin: int = 0, b_end: int | None = None, stream_id: int = 0,
@@ -312,7 +319,7 @@ class Context:
     def permtest_pair(self, X, Y, B: int, seed: int, stream_id: int = 0, mode: int = 0,
                       b_begin: int = 0, b_end: int | None = None, tie_rel: float = 1e-6,
                       block: int = 0, want_stats: bool = False, sync: bool = True,
-                      pair_mode: int = 0, exhaustive: bool = False):
+                      pair_mode: int = 0, exhaustive: bool = False, gram=None):
         """One word-pair test end to end: hap_align + hap_permtest (+ p-value).  With
         exhaustive=True the b range indexes all C(N, n_x) splits (pass B = C(N, n_x)) and
         p_exact = exceed_ge / B is added."""
@@ -323,7 +330,7 @@ class Context:
         stats = (torch.empty((b_end - b_begin, 3), dtype=torch.float64, device=self.device)
                  if want_stats else None)
         cfg = make_cfg(seed, B, b_begin, b_end, stream_id, block, tie_rel, pair_mode,
-                       flags=HAP_FLAG_EXHAUSTIVE if exhaustive else 0)
+                       flags=(HAP_FLAG_EXHAUSTIVE if exhaustive else 0) | gram_flags(gram))
         hap_permtest(self.h, self.info, cfg, self.counts, stats)
         if not sync:
             return None
@@ -348,7 +355,7 @@ class Context:
     def permtest_batch(self, X_packed, cu_nx, Y_packed, cu_ny, B: int, seed: int,
                        stream_id: int = 0, mode: int = 0, tie_rel: float = 1e-6,
                        pair_sel=None, pair_mode: int = 0, sync: bool = True, wave: int = 0,
-                       shared: bool = False):
+                       shared: bool = False, gram=None):
         """P tests of a varlen batch (hap_permtest_batch); pair p draws its permutations
         from generator stream stream_id + p (shared=True: every pair uses stream_id, one mask
         block per wave of equal-size pairs).  Returns one dict per pair (None for pairs
@@ -358,7 +365,7 @@ class Context:
         infos = torch.zeros((P, INFO_BYTES), dtype=torch.uint8, device=self.device)
         counts = torch.zeros((P, COUNTS_WORDS), dtype=torch.int64, device=self.device)
         cfg = make_cfg(seed, B, 0, B, stream_id, 0, tie_rel, pair_mode, wave,
-                       HAP_FLAG_SHARED_MASK if shared else 0)
+                       (HAP_FLAG_SHARED_MASK if shared else 0) | gram_flags(gram))
         hap_permtest_batch(self.h, X_packed, cu_nx, Y_packed, cu_ny, mode, cfg, infos, counts,
                            pair_sel)
         if not sync:

@@ -8,7 +8,7 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libhap.so")
-SOURCES = ["hap_api.cu", "k_align.cu", "k_perm.cu", "k_maskgemm.cu"]
+SOURCES = ["hap_api.cu", "k_align.cu", "k_perm.cu", "k_maskgemm.cu", "k_gram.cu"]
 HEADERS = ["hap_device.cuh", "hap_internal.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -26,13 +26,17 @@ struct hap_ctx_s {
     cudaStream_t last_stream = nullptr;
     const hap_align_info* last_info = nullptr;
     // ---- workspace (grow-only)
-    void* buf[32] = {};
-    size_t cap[32] = {};
+    void* buf[40] = {};
+    size_t cap[40] = {};
     // ---- state of the last successful hap_align
     bool aligned = false;
+    bool gram_ok = false;  // the Gram planes of the current alignment are built (k_gram.cu)
     int64_t n_x = 0, n_y = 0, d = 0, n_pad = 0, d_pad = 0;
     // ---- TMA descriptors (valid for the current buffers/shape); tmA per mask slot
     CUtensorMap tmA[2]{}, tmBhi{}, tmBlo{};
+    CUtensorMap tmGhi{}, tmGlo{};  // Gram planes (B operand of the Gram form)
+    const void* tmg_key[2] = {};
+    int64_t tmg_shape[2] = {};
     const void* tm_key[4] = {};
     int64_t tm_shape[5] = {};
     // ---- generator side stream: K2 only depends on (seed, s, b, N, n_x), so it runs on
@@ -84,7 +88,7 @@ namespace {
 enum Buf {
     kX = 0, kY, kNrm, kCoef, kPart, kXbar, kYbar, kU, kZhi, kZlo, kTpart, kT64, kAB, kMask,
     kM, kSconst, kGemmPart, kTileDone, kScal, kSpart, kScratch, kMask1, kInv, kStamps, kK3Stamps,
-    kSched, kSpans, kX2, kY2, kClaim, kNumBufs
+    kSched, kSpans, kX2, kY2, kClaim, kGhi, kGlo, kGab, kMbits, kMbits1, kNumBufs
 };
 
 hap_status fail(hap_ctx c, hap_status s, const std::string& msg) {
@@ -187,6 +191,33 @@ hap_status refresh_maps(hap_ctx c, int pair_mode) {
     return HAP_OK;
 }
 
+// ---- Gram form (k_gram.cu) -----------
+// The mask-GEMM multiplies the masks by the N_pad x N_pad Gram matrix of the centred cloud
+// instead of the N_pad x d_pad planes.  Forced by HAP_FLAG_GRAM (n_pad <= kGramMaxNpad),
+// refused by HAP_FLAG_NO_GRAM; otherwise chosen when the tensor time it saves (4 n_pad
+// (d_pad - n_pad) FLOP per permutation at ~1.3 PFLOP/s) exceeds twice its set-up (the Gram
+// kernel, ~n_pad^2 d_pad / 10^7 us, plus ~10 us).  The choice depends only on the test's
+// shape, cfg->B (the whole test, not this call's shard) and the flags, so every shard of a
+// test takes the same form.
+constexpr int64_t kGramMaxNpad = 4096;
+
+bool use_gram(hap_ctx w, const hap_perm_cfg* cfg) {
+    if (cfg->flags & HAP_FLAG_NO_GRAM) return false;
+    if (cfg->flags & HAP_FLAG_EXHAUSTIVE) return false;
+    if (cfg->flags & HAP_FLAG_GRAM) return w->n_pad <= kGramMaxNpad;
+    if (2 * w->n_pad > w->d_pad) return false;
+    const double B = (double)(cfg->B ? cfg->B : cfg->b_end - cfg->b_begin);
+    const double np = (double)w->n_pad, dp = (double)w->d_pad;
+    const double save_us = B * 4.0 * np * (dp - np) / 1.3e9;
+    const double cost_us = 10.0 + np * np * dp / 1e7;
+    return save_us > 2.0 * cost_us;
+}
+
+// Gram planes of `w` (buffers and TMA descriptors; plan time) and their contents for the
+// current alignment (built once per hap_align, on the wave's stream after the alignment)
+hap_status ensure_gram(hap_ctx w, int pair_mode);
+hap_status build_gram(hap_ctx w, cudaStream_t st);
+
 // dynamic piece claiming (default): CTA pairs that start late beside the other lane's
 // kernels take fewer pieces (C2 bench +2.7 %, C4 +3.6 % vs the static split);
 // HAP_K3_DYNAMIC=0 restores the static balanced split (scheduling knob, same results)
@@ -285,6 +316,7 @@ hap_status get_schedule(hap_ctx c, const GemmArgs& w, int np, cudaStream_t st, G
         const int64_t nt = (k + 1 < w.G ? w.t[k + 1].tile0 : w.ntiles) - w.t[k].tile0;
         key.push_back(nt);
         key.push_back(w.t[k].n_pad);
+        key.push_back(w.t[k].ncols);
     }
     const int64_t nt_all = w.ntiles;
     for (auto& e : c->sched)
@@ -306,8 +338,8 @@ hap_status get_schedule(hap_ctx c, const GemmArgs& w, int np, cudaStream_t st, G
     for (int k = 0; k < w.G; ++k) {
         const int64_t nt = (k + 1 < w.G ? w.t[k + 1].tile0 : w.ntiles) - w.t[k].tile0;
         for (int64_t t = 0; t < nt; ++t)
-            for (int64_t c0 = 0; c0 < w.d_pad; c0 += kChunkN)
-                chunks.push_back({std::min<int64_t>(kChunkN, w.d_pad - c0), w.t[k].n_pad / kKBlock,
+            for (int64_t c0 = 0; c0 < w.t[k].ncols; c0 += kChunkN)
+                chunks.push_back({std::min<int64_t>(kChunkN, w.t[k].ncols - c0), w.t[k].n_pad / kKBlock,
                                   w.t[k].tile0 + t, c0});
     }
     auto cost = [](int64_t wd, int64_t nkb) { return (double)nkb * std::max(4.0 * (double)wd, kPieceFloor); };
@@ -411,7 +443,7 @@ hap_status get_schedule(hap_ctx c, const GemmArgs& w, int np, cudaStream_t st, G
         // slots: index of the piece within its tile, in (tile, column) order
         std::vector<std::pair<int64_t, int>> order;  // (tile * d_pad + c0, piece index)
         for (size_t k = 0; k < pcs.size() / 4; ++k)
-            order.push_back({(int64_t)pcs[4 * k] * w.d_pad + pcs[4 * k + 1], (int)k});
+            order.push_back({(int64_t)pcs[4 * k] * 65536 + pcs[4 * k + 1], (int)k});
         std::sort(order.begin(), order.end());
         for (auto& o : order) pcs[4 * o.second + 3] = npc[pcs[4 * o.second]]++;
     } else {
@@ -616,6 +648,49 @@ namespace {
 // Grow-only workspace for pairs of up to N pooled rows in d dimensions and waves of up to
 // `tiles` mask tiles of R rows (owner buffers included): allocating (and zeroing) buffers
 // synchronises, so the batch reserves every workspace before its first launch.
+hap_status ensure_gram(hap_ctx w, int pair_mode) {
+    const int64_t n_pad = w->n_pad, rows = zt_rows(n_pad);
+    hap_status s;
+    if ((s = ensure(w, kGhi, (size_t)rows * n_pad * 2)) || (s = ensure(w, kGlo, (size_t)rows * n_pad * 2)) ||
+        (s = ensure(w, kGab, (size_t)n_pad * 8)))
+        return s;
+    const void* keys[2] = {w->buf[kGhi], w->buf[kGlo]};
+    const int64_t shape[2] = {n_pad, pair_mode};
+    if (!std::equal(keys, keys + 2, w->tmg_key) || !std::equal(shape, shape + 2, w->tmg_shape)) {
+        const uint32_t box_b = (uint32_t)maskgemm_b_rows(pair_mode);
+        if (!make_map(&w->tmGhi, w->buf[kGhi], (uint64_t)n_pad, (uint64_t)rows, box_b) ||
+            !make_map(&w->tmGlo, w->buf[kGlo], (uint64_t)n_pad, (uint64_t)rows, box_b))
+            return fail(w, HAP_E_CUDA, "cuTensorMapEncodeTiled failed (Gram planes)");
+        std::copy(keys, keys + 2, w->tmg_key);
+        std::copy(shape, shape + 2, w->tmg_shape);
+    }
+    return HAP_OK;
+}
+
+hap_status build_gram(hap_ctx w, cudaStream_t st) {
+    const int64_t n_pad = w->n_pad;
+    if (!w->gram_ok) {
+        GramArgs ga{};
+        ga.zt_hi = B<uint16_t>(w, kZhi);
+        ga.zt_lo = B<uint16_t>(w, kZlo);
+        ga.ab = B<float2>(w, kAB);
+        ga.n_pad = (int)n_pad;
+        ga.d_pad = (int)w->d_pad;
+        ga.g_hi = B<uint16_t>(w, kGhi);
+        ga.g_lo = B<uint16_t>(w, kGlo);
+        ga.gab = B<float2>(w, kGab);
+        ga.span = next_span(w, HAP_PHASE_ALIGN);
+        cudaError_t e;
+        {
+            PhaseScope ps(w, HAP_PHASE_ALIGN, 1, st);
+            e = launch_gram(ga, st);
+        }
+        if (e != cudaSuccess) return cuda_fail(w, e, "Gram kernel");
+        w->gram_ok = true;
+    }
+    return HAP_OK;
+}
+
 hap_status reserve_pair(hap_ctx c, int64_t N, int64_t d, int64_t tiles, int64_t R, bool owner) {
     const int64_t n_pad = round_up(N, kKBlock), d_pad = round_up(d, 32);
     hap_status s;
@@ -742,6 +817,7 @@ hap_status align_wave(hap_ctx owner, int G, hap_ctx* ws, const AlignPair* pairs,
     if (e != cudaSuccess) return cuda_fail(owner, e, "align kernel");
     for (int k = 0; k < G; ++k) {
         ws[k]->aligned = true;
+        ws[k]->gram_ok = false;
         ws[k]->last_stream = st;
         ws[k]->last_info = pairs[k].info;
     }
@@ -810,7 +886,7 @@ hap_status plan_wave(hap_ctx owner, int G, const WaveTest* T, int pair, bool sha
     g.G = G;
     g.rows_per_tile = (int)R;
     g.tie_rel = T[0].cfg->tie_rel > 0 ? T[0].cfg->tie_rel : 1e-6;
-    int64_t tiles = 0;
+    int64_t tiles = 0, max_cols = 0;
     hap_status s;
     for (int k = 0; k < G; ++k) {
         hap_ctx w = T[k].w;
@@ -834,6 +910,17 @@ hap_status plan_wave(hap_ctx owner, int G, const WaveTest* T, int pair, bool sha
         pt.ntiles = (int)nt;
         pt.exhaustive = (T[k].cfg->flags & HAP_FLAG_EXHAUSTIVE) ? 1 : 0;
         GemmTest& gt = g.t[k];
+        gt.gram = use_gram(w, T[k].cfg) ? 1 : 0;
+        gt.ncols = gt.gram ? (int)w->n_pad : (int)w->d_pad;
+        gt.mbits = nullptr;
+        if (gt.gram) {
+            // the mask owner's bit rows (test 0's with shared masks), packed after K2
+            hap_ctx mo = (shared && k > 0) ? T[0].w : w;
+            const int mb = P.slots[k] ? kMbits1 : kMbits;
+            if ((s = ensure(mo, mb, (size_t)nt * R * (mo->n_pad / 8))) || (s = ensure_gram(w, pair)))
+                return s == HAP_OK ? s : fail(owner, s, w->err + mo->err);
+            gt.mbits = B<uint32_t>(mo, mb);
+        }
         gt.n_pad = (int)w->n_pad;
         gt.n_x = (int)w->n_x;
         gt.n_y = (int)w->n_y;
@@ -842,11 +929,12 @@ hap_status plan_wave(hap_ctx owner, int G, const WaveTest* T, int pair, bool sha
         gt.info = T[k].info;
         gt.counts = T[k].counts;
         gt.stats = T[k].stats;
-        gt.ab = B<float2>(w, kAB);
+        gt.ab = B<float2>(w, gt.gram ? kGab : kAB);
         gt.sconst = B<double>(w, kSconst);
         P.maps.a[k] = shared ? T[0].w->tmA[P.slots[0]] : w->tmA[P.slots[k]];
-        P.maps.bhi[k] = w->tmBhi;
-        P.maps.blo[k] = w->tmBlo;
+        P.maps.bhi[k] = gt.gram ? w->tmGhi : w->tmBhi;
+        P.maps.blo[k] = gt.gram ? w->tmGlo : w->tmBlo;
+        max_cols = std::max<int64_t>(max_cols, gt.ncols);
         tiles += nt;
     }
     if (shared) pa.G = 1;  // one generated block serves the whole wave
@@ -855,15 +943,19 @@ hap_status plan_wave(hap_ctx owner, int G, const WaveTest* T, int pair, bool sha
     g.npairs = P.npairs;
     {  // dynamic mode: every piece (a chunk, or HAP_K3_PIECE_COLS columns of it)
         const int64_t pwidth = k3_piece_cols();
-        int64_t per_tile = 0;
-        for (int64_t c0 = 0; c0 < owner->d_pad; c0 += kChunkN)
-            per_tile += ceil_div(std::min<int64_t>(kChunkN, owner->d_pad - c0), pwidth);
-        g.npieces = (int)(tiles * per_tile);
+        int64_t np_all = 0;
+        for (int k = 0; k < G; ++k) {
+            int64_t per_tile = 0;
+            for (int64_t c0 = 0; c0 < g.t[k].ncols; c0 += kChunkN)
+                per_tile += ceil_div(std::min<int64_t>(kChunkN, g.t[k].ncols - c0), pwidth);
+            np_all += (int64_t)pa.t[k].ntiles * per_tile;
+        }
+        g.npieces = (int)np_all;
         // dynamic claiming needs no fixed split: a small wave launches only as many CTA
         // pairs as it has pieces (less setup and teardown for C1-sized tests)
         if (g.dyn && g.npieces < P.npairs) P.npairs = g.npairs = std::max(1, g.npieces);
     }
-    if ((s = ensure(owner, kGemmPart, (size_t)tiles * part_slots(owner, owner->d_pad) * R * sizeof(float2))) ||
+    if ((s = ensure(owner, kGemmPart, (size_t)tiles * part_slots(owner, max_cols) * R * sizeof(float2))) ||
         (s = ensure(owner, kTileDone, (size_t)tiles * sizeof(unsigned))))
         return s;
     g.part = B<float2>(owner, kGemmPart);
@@ -929,6 +1021,15 @@ hap_status launch_wave(hap_ctx owner, const WaveTest* T, int pair, cudaStream_t 
         if (e == cudaSuccess) e = cudaStreamWaitEvent(st, owner->ev_ready[0], 0);  // join
         if (e != cudaSuccess) return cuda_fail(owner, e, "perm generator");
     }
+    for (int k = 0; k < g.G; ++k)  // Gram form: G' of each test's current alignment
+        if (g.t[k].gram && (s = build_gram(T[k].w, st))) return fail(owner, s, T[k].w->err);
+    for (int k = 0; k < pa.G && e == cudaSuccess; ++k) {  // Gram form: bit rows of the masks
+        if (!g.t[k].gram) continue;
+        PhaseScope ps(owner, HAP_PHASE_PERMGEN, 1, st);
+        e = launch_pack_bits(static_cast<const uint16_t*>(pa.t[k].out), const_cast<uint32_t*>(g.t[k].mbits),
+                             (int64_t)pa.t[k].ntiles * P.g.rows_per_tile, (int)pa.t[k].n_pad, owner->sm_count, st);
+    }
+    if (e != cudaSuccess) return cuda_fail(owner, e, "mask bits");
     if ((s = get_schedule(owner, g, P.npairs, st, g))) return s;
     {
         g.span = next_span(owner, HAP_PHASE_MASKGEMM);
@@ -1083,8 +1184,15 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
                 hap_profile(c->sub[k][j], c->serial ? 2 : c->prof ? 1 : 0);
                 if (c->spans) hap_profile_spans(c->sub[k][j], 1);
             }
+        // lane streams (alignment + mask-GEMM) at the highest priority, the generator side
+        // streams at the default (lowest): pending alignment / mask-GEMM CTAs are placed before
+        // the generator's (HAP_LANE_PRIO=0: all at the default, experiments)
+        static const char* lp = getenv("HAP_LANE_PRIO");
+        int prio_lo = 0, prio_hi = 0;
+        cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+        const int lane_prio = (lp && atoi(lp) == 0) ? prio_lo : prio_hi;
         if (!c->sub_stream[k] &&
-            (cudaStreamCreateWithFlags(&c->sub_stream[k], cudaStreamNonBlocking) != cudaSuccess ||
+            (cudaStreamCreateWithPriority(&c->sub_stream[k], cudaStreamNonBlocking, lane_prio) != cudaSuccess ||
              cudaEventCreateWithFlags(&c->ev_sub[k], cudaEventDisableTiming) != cudaSuccess))
             return fail(c, HAP_E_CUDA, "batch streams");
         if (host_in && !c->cp_stream[k] &&
@@ -1161,7 +1269,7 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
             if (G > 0 && !one_block) break;  // a multi-block test starts its own wave
             if (G > 0 && shared && (nx != Q[0].n_x || ny != Q[0].n_y)) break;  // same masks
             // one alignment path per wave (the path is a function of the pair's shape)
-            if (G > 0 && align_stream_pair(nx + ny, d) != align_stream_pair(Q[0].n_x + Q[0].n_y, d)) break;
+            if (G > 0 && align_path(nx + ny, d) != align_path(Q[0].n_x + Q[0].n_y, d)) break;
             hap_ctx w = c->sub[k][G];
             const int sb = c->lane_waves[k] & 1;  // staging buffer of this wave
             if (G == 0 && host_in && c->k1_recorded[k][sb])  // its last reader: the K1 two waves back
@@ -1190,7 +1298,7 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
             // K1 -> K2b -> K3 in series and measured 106 vs 85 us per C2 test, so off
             static const char* kd = getenv("HAP_K1_DRAWS");
             staged = !s && kd && atoi(kd) != 0 && perm_can_split(P.pa) &&
-                     !align_stream_pair(Q[0].n_x + Q[0].n_y, d);
+                     align_path(Q[0].n_x + Q[0].n_y, d) == kAlignFused;
         }
         if (!s && G > 0 && host_in) {  // K1 waits for the wave's rows
             cudaEventRecord(c->ev_copied[k], c->cp_stream[k]);

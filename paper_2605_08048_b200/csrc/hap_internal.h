@@ -98,11 +98,17 @@ struct AlignGeom {
 AlignGeom align_geometry(int64_t d);
 // fills item_off (n_pad / R items per pair) for the geometry of d
 void align_items(AlignArgs& a);
-// Large pairs (align_stream_pair: d % 4 == 0, d <= 4096, n_pad d >= 8 Mi elements; inputs
-// 16-byte aligned) take the streaming path K1s (three bandwidth kernels); the others ONE
-// cooperative kernel of `grid` CTAs (one per SM) whose scratch[2] holds its grid barrier.
-// A wave's pairs must all take the same path (the batch forms its waves so).
-bool align_stream_pair(int64_t N, int64_t d);
+// Alignment path of a pair, a function of its shape only (so a pair gets the same bits
+// alone, in any batch wave and on every rank; a wave's pairs all take one path):
+//   kAlignRing  d % 4 == 0, d <= 4096, n_pad d >= 8 Mi elements: K1s, three bandwidth
+//               kernels with shared-memory rings (LLM-sized clouds, C3);
+//   kAlignLean  the same constraints below 8 Mi elements: K1s-lean, the same three passes
+//               with register-prefetched loads and < 18 KB of shared memory per CTA, so
+//               they run beside a mask-GEMM CTA (C1, C2, C4, C5);
+//   kAlignFused otherwise (d % 4 != 0 or d > 4096; also inputs not 16-byte aligned): ONE
+//               cooperative kernel of `grid` CTAs whose scratch[2] holds its grid barrier.
+enum { kAlignFused = 0, kAlignLean = 1, kAlignRing = 2 };
+int align_path(int64_t N, int64_t d);
 bool align_uses_stream(const AlignArgs& a);
 int align_launch_count(const AlignArgs& a);  // kernels issued by launch_align
 cudaError_t launch_align(const AlignArgs& a, int grid, cudaStream_t st);
@@ -110,6 +116,9 @@ cudaError_t launch_align(const AlignArgs& a, int grid, cudaStream_t st);
 // ---- K3: tcgen05 mask-GEMM + statistic epilogue (k_maskgemm.cu) --------------------
 struct GemmTest {
     int n_pad, n_x, n_y;
+    int ncols;               // GEMM output columns: d_pad (planes) or n_pad (Gram form)
+    int gram;                // 1: B = the Gram planes G' (k_gram.cu), epilogue reads mbits
+    const uint32_t* mbits;   // Gram form: the launch's mask rows, one bit per pooled row
     int count;               // valid permutations of this test in the launch
     int tile0;               // first wave tile of this test (its tiles are contiguous)
     hap_align_info* info;
@@ -139,6 +148,22 @@ struct GemmArgs {
     long long* stamps;       // exp bit 16: [grid][8 units][8 events] globaltimer
     unsigned long long* span;  // optional {first CTA entry, last CTA exit} globaltimer
 };
+// ---- Gram form (k_gram.cu) -----------------------------------
+struct GramArgs {
+    const uint16_t* zt_hi;   // [d_pad][n_pad] planes of hap_align
+    const uint16_t* zt_lo;
+    const float2* ab;        // [d_pad] {2a, 2b} of the plane epilogue
+    int n_pad, d_pad;
+    uint16_t* g_hi;          // [n_pad][n_pad] bf16 hi / lo of G' = Z' Z'^T
+    uint16_t* g_lo;
+    float2* gab;             // [n_pad] {2 a.z'_j, 2 b.z'_j}
+    unsigned long long* span;
+};
+cudaError_t launch_gram(const GramArgs& g, cudaStream_t st);
+// bf16 mask rows [rows][n_pad] -> bits [rows][n_pad / 32] (bit j % 32 of word j / 32)
+cudaError_t launch_pack_bits(const uint16_t* mask, uint32_t* bits, int64_t rows, int n_pad, int sm_count,
+                             cudaStream_t st);
+
 // TMA descriptors of the wave's tests: mask (A), Zt hi / lo planes (B)
 struct GemmMaps {
     CUtensorMap a[kMaxWave], bhi[kMaxWave], blo[kMaxWave];

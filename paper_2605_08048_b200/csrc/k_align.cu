@@ -261,6 +261,7 @@ __device__ __forceinline__ void store_words(uint32_t* dst, const uint32_t (&w)[W
 // b = t - a (fp32) for the GEMM epilogue, {sum a^2, sum b^2} in fixed order; then the
 // accumulators and flags are cleared for the next launch.  Shared by the fused K1 and the
 // streaming K1s transform kernel.
+template <int NT = kThreads>
 __device__ void finish_pairs(const AlignArgs& a, double* red) {
     const int tid = threadIdx.x;
     const int d = (int)a.d;
@@ -268,7 +269,7 @@ __device__ void finish_pairs(const AlignArgs& a, double* red) {
         const AlignPair& q = a.p[g];
         const int64_t N = q.n_x + q.n_y;
         double sa = 0.0, sb = 0.0, sm = 0.0;
-        for (int64_t c = tid; c < a.d_pad; c += kThreads) {
+        for (int64_t c = tid; c < a.d_pad; c += NT) {
             const double tsum = fix_get(q.acc + 2 * d + c);
             const double m = __ldcg(q.m + c);
             sm += m * m;
@@ -279,9 +280,9 @@ __device__ void finish_pairs(const AlignArgs& a, double* red) {
             sa += (double)af * (double)af;
             sb += (double)bf * (double)bf;
         }
-        const double2 sab = block_sum2(sa, sb, red);
-        const double smm = block_sum2(sm, 0.0, red).x;
-        for (int64_t c = tid; c < 2 * (int64_t)d + a.d_pad; c += kThreads) q.acc[c] = 0;
+        const double2 sab = block_sum2_n<NT>(sa, sb, red);
+        const double smm = block_sum2_n<NT>(sm, 0.0, red).x;
+        for (int64_t c = tid; c < 2 * (int64_t)d + a.d_pad; c += NT) q.acc[c] = 0;
         if (tid == 0) {
             q.sconst[0] = sab.x;
             q.sconst[1] = sab.y;
@@ -684,7 +685,10 @@ __global__ void __launch_bounds__(kThreads, 65536 / (kThreads * 64)) k1_align_fu
 // Deterministic: every cross-CTA sum is an integer sum of per-item / per-tile roundings and
 // the CTA -> work assignment depends only on the shapes.
 constexpr int kSStages = 3;
-constexpr int64_t kStreamMinElems = 8ll << 20;  // n_pad * d: 32 MB of fp32 input
+#ifndef HAP_K1S_MIN_ELEMS
+#define HAP_K1S_MIN_ELEMS (8ll << 20)
+#endif
+constexpr int64_t kStreamMinElems = HAP_K1S_MIN_ELEMS;  // n_pad * d: 32 MB of fp32 input
 constexpr int kXfRows = 128, kXfCols = 64;  // KS3 tile: 128 rows x 64 columns
 
 __device__ __forceinline__ void bulk_load_row(float* dst, const float* src, uint32_t bytes, uint64_t* bar) {
@@ -781,11 +785,17 @@ __device__ void stream_pair_scalars(const AlignArgs& a, int g, double* red) {
 // 1/||h||) and then the item's column partials of x = h/||h||.  Column sums of pair g, side
 // X (0) / Y (1) are held as int64 in registers and flushed (one atomic per column) when the
 // (pair, side) changes.
+// kRing = false (K1s-lean, pairs below kStreamMinElems): no shared-memory ring; every
+// thread loads its own float4 groups of the item's rows straight into registers and the
+// NEXT item's rows are in flight while the current one is reduced - the same arithmetic in
+// the same order (identical bits), < 1 KB of shared memory, so the CTAs fit beside a
+// mask-GEMM CTA and generator CTAs on one SM.
 constexpr int kS1Threads = 256;
-template <int G4>
-__global__ void __launch_bounds__(kS1Threads, 2) k1s_stats(AlignArgs a) {
+constexpr int kS1LeanThreads = 128;  // lean: one warp per SM sub-partition (registers beside K3)
+template <int G4, bool kRing = true, int NT = kS1Threads>
+__global__ void __launch_bounds__(NT, 512 / NT) k1s_stats(AlignArgs a) {
     constexpr int R = 8 / G4;
-    constexpr int W = kS1Threads / 32;
+    constexpr int W = NT / 32;
     extern __shared__ __align__(128) uint8_t ks_smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(ks_smem);
     float* ring = reinterpret_cast<float*>(ks_smem + 128);
@@ -801,10 +811,30 @@ __global__ void __launch_bounds__(kS1Threads, 2) k1s_stats(AlignArgs a) {
     const size_t stage_floats = (size_t)R * d;
     if (tid == 0) {
         span_enter(a.span);
-        for (int k = 0; k < kSStages; ++k) mbar_init(&full[k], 1);
-        fence_barrier_init();
+        if constexpr (kRing) {
+            for (int k = 0; k < kSStages; ++k) mbar_init(&full[k], 1);
+            fence_barrier_init();
+        }
     }
     __syncthreads();
+    // lean mode: this thread's float4 groups of an item's rows, straight from global memory
+    auto load_regs = [&](int64_t item, float4 (&f)[R][G4]) {
+        const int g = pair_of(a, item);
+        const AlignPair& q = a.p[g];
+        const int64_t N = q.n_x + q.n_y;
+        const int64_t r0 = (item - a.item_off[g]) * R;
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int kk = 0; kk < G4; ++kk) {
+                const int c4 = tid + kk * NT;
+                f[r][kk] = (r0 + r < N && c4 < d4) ? __ldcs(reinterpret_cast<const float4*>(row_ptr(q, r0 + r)) + c4)
+                                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+    };
+    float4 nxt[R][G4];
+    if constexpr (!kRing)
+        if (i0 < i1) load_regs(i0, nxt);
     auto issue = [&](int64_t item, int st) {  // one thread
         const int g = pair_of(a, item);
         const AlignPair& q = a.p[g];
@@ -815,8 +845,9 @@ __global__ void __launch_bounds__(kS1Threads, 2) k1s_stats(AlignArgs a) {
         for (int r = 0; r < nr; ++r)
             bulk_load_row(ring + st * stage_floats + (size_t)r * d, row_ptr(q, r0 + r), (uint32_t)d * 4u, &full[st]);
     };
-    if (tid == 0)
-        for (int k = 0; k < kSStages && i0 + k < i1; ++k) issue(i0 + k, k);
+    if constexpr (kRing)
+        if (tid == 0)
+            for (int k = 0; k < kSStages && i0 + k < i1; ++k) issue(i0 + k, k);
     long long acc[G4][4];
 #pragma unroll
     for (int k = 0; k < G4; ++k)
@@ -828,7 +859,7 @@ __global__ void __launch_bounds__(kS1Threads, 2) k1s_stats(AlignArgs a) {
         long long* dst = a.p[cur >> 1].acc + (cur & 1) * d;
 #pragma unroll
         for (int k = 0; k < G4; ++k) {
-            const int c4 = tid + k * kS1Threads;
+            const int c4 = tid + k * NT;
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 if (c4 < d4 && acc[k][e] != 0)
@@ -845,23 +876,36 @@ __global__ void __launch_bounds__(kS1Threads, 2) k1s_stats(AlignArgs a) {
         const int64_t N = q.n_x + q.n_y;
         const int64_t r0 = (item - a.item_off[g]) * R;
         const int nr = (int)(N - r0 < R ? N - r0 : R);
-        const float4* tile = reinterpret_cast<const float4*>(ring + st * stage_floats);
-        mbar_wait(&full[st], (uint32_t)((k / kSStages) & 1));
         double v[R][G4][4];
+        if constexpr (kRing) {
+            const float4* tile = reinterpret_cast<const float4*>(ring + st * stage_floats);
+            mbar_wait(&full[st], (uint32_t)((k / kSStages) & 1));
 #pragma unroll
-        for (int r = 0; r < R; ++r)
+            for (int r = 0; r < R; ++r)
 #pragma unroll
-            for (int kk = 0; kk < G4; ++kk) {
-                const int c4 = tid + kk * kS1Threads;
-                float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (r < nr && c4 < d4) f = tile[(size_t)r * d4 + c4];
-                v[r][kk][0] = (double)f.x;
-                v[r][kk][1] = (double)f.y;
-                v[r][kk][2] = (double)f.z;
-                v[r][kk][3] = (double)f.w;
-            }
-        __syncthreads();  // the stage is in registers: refill it
-        if (tid == 0 && item + kSStages < i1) issue(item + kSStages, st);
+                for (int kk = 0; kk < G4; ++kk) {
+                    const int c4 = tid + kk * NT;
+                    float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (r < nr && c4 < d4) f = tile[(size_t)r * d4 + c4];
+                    v[r][kk][0] = (double)f.x;
+                    v[r][kk][1] = (double)f.y;
+                    v[r][kk][2] = (double)f.z;
+                    v[r][kk][3] = (double)f.w;
+                }
+            __syncthreads();  // the stage is in registers: refill it
+            if (tid == 0 && item + kSStages < i1) issue(item + kSStages, st);
+        } else {
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+#pragma unroll
+                for (int kk = 0; kk < G4; ++kk) {
+                    v[r][kk][0] = (double)nxt[r][kk].x;
+                    v[r][kk][1] = (double)nxt[r][kk].y;
+                    v[r][kk][2] = (double)nxt[r][kk].z;
+                    v[r][kk][3] = (double)nxt[r][kk].w;
+                }
+            if (item + 1 < i1) load_regs(item + 1, nxt);  // in flight during this item
+        }
         // row norms: per-thread partial squares, warp tree, then the warps in order
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -939,7 +983,7 @@ __global__ void __launch_bounds__(kS1Threads, 2) k1s_stats(AlignArgs a) {
     __syncthreads();
     if (s_last) {
         __threadfence();
-        for (int g = 0; g < a.G; ++g) stream_pair_scalars<kS1Threads>(a, g, red);
+        for (int g = 0; g < a.G; ++g) stream_pair_scalars<NT>(a, g, red);
         if (tid == 0) reinterpret_cast<unsigned*>(a.scratch + 3)[0] = 0u;
     }
     __syncthreads();
@@ -1230,6 +1274,186 @@ __global__ void __launch_bounds__(kThreads, 1) k1s_xform(AlignArgs a, int64_t ti
     __syncthreads();
     if (tid == 0) span_exit(a.span);
 }
+
+// KS3-lean (pairs below kStreamMinElems): tiles of 64 rows x 64 columns in the same (pair,
+// strip, row block) order, 128 threads (one warp per SM sub-partition, so the CTA's
+// registers fit beside a mask-GEMM CTA's), NO raw-tile ring: thread (row pair p, column
+// group q) loads rows 2p + 16k, 2p + 1 + 16k (k < 4) x columns 4q..4q+3 (float4, 256
+// coalesced bytes per row) and their {coef, 1/||h||} straight into registers, the next
+// tile's in flight while the current one is transformed; z' = x - coef u - m (fp32, the
+// arithmetic of KS3), bf16 hi/lo, two rows per 32-bit word into a TRANSPOSED staging tile
+// [column][row] (17 KB for both planes); write thread = (column, 32 rows): 64 contiguous
+// bytes per plane.  t' per column and tile in fp64, rounded per tile to fixed point,
+// summed as int64 per strip run; the last CTA (ticket) runs P5.
+constexpr int kXlRows = 64;
+constexpr int kXlThreads = 128;
+constexpr int kXlTW = kXlRows / 2 + 1;  // u32 words per staging column (33: conflict-free reads)
+
+__global__ void __launch_bounds__(kXlThreads, 4) k1s_xform_lean(AlignArgs a, int64_t tile_off1, int64_t tile_off2,
+                                                               int64_t tile_off3, int64_t tiles_total) {
+    __shared__ uint32_t sh_hi[kXfCols * kXlTW];
+    __shared__ uint32_t sh_lo[kXfCols * kXlTW];
+    __shared__ double red[2 * (kXlThreads / 32) + 2];
+    __shared__ int s_last;
+    const int tid = threadIdx.x;
+    const int d = (int)a.d, d_pad = (int)a.d_pad;
+    const int64_t t0 = tiles_total * blockIdx.x / gridDim.x, t1 = tiles_total * (blockIdx.x + 1) / gridDim.x;
+    if (tid == 0) span_enter(a.span);
+    const int q = tid & 15, p = tid >> 4;     // transform role: column group, row pair (0..7)
+    const int wg = tid & 1, wc = tid >> 1;    // write role: 32-row half, column
+    const int strips = (d_pad + kXfCols - 1) / kXfCols;
+    struct TileAt {
+        int g, strip, rt;
+    };
+    auto locate = [&](int64_t t) {
+        TileAt L;
+        L.g = (t >= tile_off1) + (t >= tile_off2) + (t >= tile_off3);
+        const int64_t lt = t - (L.g == 0 ? 0 : L.g == 1 ? tile_off1 : L.g == 2 ? tile_off2 : tile_off3);
+        const int64_t rtiles = (a.p[L.g].n_pad + kXlRows - 1) / kXlRows;
+        L.strip = (int)(lt / rtiles);
+        L.rt = (int)(lt % rtiles);
+        return L;
+    };
+    auto advance = [&](TileAt& L) {
+        const int64_t rtiles = (a.p[L.g].n_pad + kXlRows - 1) / kXlRows;
+        if (++L.rt == rtiles) {
+            L.rt = 0;
+            if (++L.strip == strips) {
+                L.strip = 0;
+                ++L.g;
+            }
+        }
+    };
+    // row k (k < 8) of this thread: pair block k / 2, row 2p + (k & 1) + 16 (k / 2)
+    auto row_of = [&](int k) { return 2 * p + (k & 1) + 16 * (k >> 1); };
+    auto load = [&](const TileAt& L, float4 (&h)[8], float2 (&cv)[8]) {
+        const AlignPair& qp = a.p[L.g];
+        const int N = (int)(qp.n_x + qp.n_y);
+        const int r0 = L.rt * kXlRows, c = L.strip * kXfCols + 4 * q;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int i = r0 + row_of(k);
+            h[k] = (i < N && c < d) ? __ldcs(reinterpret_cast<const float4*>(row_ptr(qp, i) + c))
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+            cv[k] = i < N ? __ldcg(qp.coef + i) : make_float2(0.f, 0.f);
+        }
+    };
+    float4 hn[8];
+    float2 cn[8];
+    TileAt Ld = locate(t0);
+    if (t0 < t1) load(Ld, hn, cn);
+    TileAt L = Ld;
+    long long tacc = 0;  // fixed-point t' of column wc of the current strip (wg == 0 lanes)
+    int cur_g = -1, cur_strip = -1;
+    float4 u4 = make_float4(0.f, 0.f, 0.f, 0.f), m4 = u4;
+    auto flush = [&]() {
+        const int c = cur_strip * kXfCols + wc;
+        if (cur_g >= 0 && wg == 0 && c < d_pad && tacc != 0)
+            atomicAdd(reinterpret_cast<unsigned long long*>(a.p[cur_g].acc + 2 * d + c), (unsigned long long)tacc);
+        tacc = 0;
+    };
+    for (int64_t t = t0; t < t1; ++t) {
+        float4 h[8];
+        float2 cv[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            h[k] = hn[k];
+            cv[k] = cn[k];
+        }
+        if (t + 1 < t1) {  // the next tile's rows in flight during this one
+            advance(Ld);
+            load(Ld, hn, cn);
+        }
+        if (L.g != cur_g || L.strip != cur_strip) {
+            flush();
+            cur_g = L.g;
+            cur_strip = L.strip;
+            const AlignPair& qp = a.p[L.g];
+            float uu[4], mm[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int c = L.strip * kXfCols + 4 * q + k;
+                uu[k] = c < d ? (float)__ldcg(qp.u + c) : 0.f;
+                mm[k] = c < d ? (float)__ldcg(qp.m + c) : 0.f;
+            }
+            u4 = make_float4(uu[0], uu[1], uu[2], uu[3]);
+            m4 = make_float4(mm[0], mm[1], mm[2], mm[3]);
+        }
+        const AlignPair& qp = a.p[L.g];
+        const int N = (int)(qp.n_x + qp.n_y), n_pad = (int)qp.n_pad;
+        const int r0 = L.rt * kXlRows, cb = L.strip * kXfCols;
+        const bool cvalid = cb + 4 * q < d;
+#pragma unroll
+        for (int hp = 0; hp < 4; ++hp) {  // row pair (2p, 2p+1) + 16 hp
+            float z[2][4];
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const int kk = 2 * hp + k;
+                if (r0 + row_of(kk) < N && cvalid) {
+                    z[k][0] = fmaf(-cv[kk].x, u4.x, h[kk].x * cv[kk].y) - m4.x;
+                    z[k][1] = fmaf(-cv[kk].x, u4.y, h[kk].y * cv[kk].y) - m4.y;
+                    z[k][2] = fmaf(-cv[kk].x, u4.z, h[kk].z * cv[kk].y) - m4.z;
+                    z[k][3] = fmaf(-cv[kk].x, u4.w, h[kk].w * cv[kk].y) - m4.w;
+                } else {
+                    z[k][0] = z[k][1] = z[k][2] = z[k][3] = 0.f;
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {  // column 4q + e: rows 2p + 16hp, +1 in one word
+                const __nv_bfloat162 hh = __floats2bfloat162_rn(z[0][e], z[1][e]);
+                const float2 hf = __bfloat1622float2(hh);
+                const __nv_bfloat162 ll = __floats2bfloat162_rn(z[0][e] - hf.x, z[1][e] - hf.y);
+                const int w = (4 * q + e) * kXlTW + p + 8 * hp;
+                sh_hi[w] = *reinterpret_cast<const uint32_t*>(&hh);
+                sh_lo[w] = *reinterpret_cast<const uint32_t*>(&ll);
+            }
+        }
+        __syncthreads();  // planes staged (transposed)
+        {
+            const int col = cb + wc;
+            const int rb = 32 * wg;
+            double tv = 0.0;
+            if (r0 + rb < n_pad) {
+                uint32_t hw[16], lw[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    hw[j] = sh_hi[wc * kXlTW + (rb >> 1) + j];
+                    lw[j] = sh_lo[wc * kXlTW + (rb >> 1) + j];
+                }
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    tv += (double)(__uint_as_float(hw[j] << 16) + __uint_as_float(lw[j] << 16));
+                    tv += (double)(__uint_as_float(hw[j] & 0xFFFF0000u) + __uint_as_float(lw[j] & 0xFFFF0000u));
+                }
+                if (col < d_pad) {
+                    const size_t off = (size_t)col * (size_t)n_pad + (size_t)(r0 + rb);  // u16 elements
+                    uint4* dh = reinterpret_cast<uint4*>(qp.zt_hi + off);
+                    uint4* dl = reinterpret_cast<uint4*>(qp.zt_lo + off);
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) {
+                        dh[v] = make_uint4(hw[4 * v], hw[4 * v + 1], hw[4 * v + 2], hw[4 * v + 3]);
+                        dl[v] = make_uint4(lw[4 * v], lw[4 * v + 1], lw[4 * v + 2], lw[4 * v + 3]);
+                    }
+                }
+            }
+            tv += __shfl_xor_sync(0xffffffffu, tv, 1);  // the column's two halves, fixed order
+            tacc += __double2ll_rn(tv * kFixScale);
+        }
+        __syncthreads();  // the staging is free
+        advance(L);
+    }
+    flush();
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(reinterpret_cast<unsigned*>(a.scratch + 1), 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
+        finish_pairs<kXlThreads>(a, red);
+    }
+    __syncthreads();
+    if (tid == 0) span_exit(a.span);
+}
 }  // namespace
 
 AlignGeom align_geometry(int64_t d) {
@@ -1256,15 +1480,16 @@ AlignGeom align_geometry(int64_t d) {
 static cudaError_t max_carveout(const void* fn) {
     return cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
 }
-bool align_stream_pair(int64_t N, int64_t d) {
-    return d % 4 == 0 && d <= 4096 && round_up(N, kKBlock) * d >= kStreamMinElems;
+int align_path(int64_t N, int64_t d) {
+    if (d % 4 != 0 || d > 4096) return kAlignFused;
+    return round_up(N, kKBlock) * d >= kStreamMinElems ? kAlignRing : kAlignLean;
 }
 
 bool align_uses_stream(const AlignArgs& a) {
     if (a.do_draws || a.stamps) return false;  // experiments / K1 phase stamps: fused kernel only
     for (int g = 0; g < a.G; ++g) {
         const AlignPair& q = a.p[g];
-        if (!align_stream_pair(q.n_x + q.n_y, a.d)) return false;
+        if (align_path(q.n_x + q.n_y, a.d) == kAlignFused) return false;
         if ((reinterpret_cast<uintptr_t>(q.X) | reinterpret_cast<uintptr_t>(q.Y)) & 15u) return false;
     }
     return true;
@@ -1274,29 +1499,36 @@ int align_launch_count(const AlignArgs& a) { return align_uses_stream(a) ? 3 : 1
 
 static cudaError_t launch_align_stream(AlignArgs a, int sm_count, cudaStream_t st) {
     const int d = (int)a.d;
-    const int g4 = (int)ceil_div(d / 4, kS1Threads);  // float4 column groups per thread
-    const int G4t = g4 <= 1 ? 1 : g4 <= 2 ? 2 : 4;     // template instance
+    // every pair of a launch takes the same variant (the callers form waves so)
+    const bool lean = align_path(a.p[0].n_x + a.p[0].n_y, a.d) == kAlignLean;
+    const int nt1 = lean ? kS1LeanThreads : kS1Threads;
+    const int g4 = (int)ceil_div(d / 4, nt1);           // float4 column groups per thread
+    const int G4t = g4 <= 1 ? 1 : g4 <= 2 ? 2 : g4 <= 4 ? 4 : 8;  // template instance
     const int R = 8 / G4t;                              // rows per item (= the kernel's)
     a.item_off[0] = 0;
     for (int g = 0; g < a.G; ++g) a.item_off[g + 1] = a.item_off[g] + ceil_div(a.p[g].n_x + a.p[g].n_y, R);
     const int64_t items = a.item_off[a.G];
-    const size_t smem1 = 128 + (size_t)kSStages * R * d * 4;
-    const void* fn = G4t == 1 ? (const void*)k1s_stats<1>
-                     : G4t == 2 ? (const void*)k1s_stats<2>
-                                : (const void*)k1s_stats<4>;
-    static size_t configured[3] = {0, 0, 0};
-    const int fi = G4t == 1 ? 0 : G4t == 2 ? 1 : 2;
+    const size_t smem1 = lean ? 0 : 128 + (size_t)kSStages * R * d * 4;
+    const void* fn = lean ? (G4t == 1   ? (const void*)k1s_stats<1, false, kS1LeanThreads>
+                             : G4t == 2 ? (const void*)k1s_stats<2, false, kS1LeanThreads>
+                             : G4t == 4 ? (const void*)k1s_stats<4, false, kS1LeanThreads>
+                                        : (const void*)k1s_stats<8, false, kS1LeanThreads>)
+                          : (G4t == 1 ? (const void*)k1s_stats<1>
+                             : G4t == 2 ? (const void*)k1s_stats<2>
+                                        : (const void*)k1s_stats<4>);
+    static size_t configured[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // dynamic smem configured + 1
+    const int fi = (G4t == 1 ? 0 : G4t == 2 ? 1 : G4t == 4 ? 2 : 3) + (lean ? 4 : 0);
     cudaError_t e;
-    if (smem1 > configured[fi]) {
+    if (smem1 + 1 > configured[fi]) {
         e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
         if (e == cudaSuccess) e = max_carveout(fn);
         if (e != cudaSuccess) return e;
-        configured[fi] = smem1;
+        configured[fi] = smem1 + 1;
     }
     {
-        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(items, 2ll * sm_count));
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(items, (lean ? 4ll : 2ll) * sm_count));
         void* args[] = {&a};
-        e = cudaLaunchKernel(fn, dim3(grid), dim3(kS1Threads), args, smem1, st);
+        e = cudaLaunchKernel(fn, dim3(grid), dim3(nt1), args, smem1, st);
         if (e != cudaSuccess) return e;
     }
     {  // KS2: CTAs in proportion to the pairs' rows, ~4 per SM in total
@@ -1309,6 +1541,23 @@ static cudaError_t launch_align_stream(AlignArgs a, int sm_count, cudaStream_t s
         k1s_coef<<<total, 256, smem2, st>>>(a, cpp[0], cpp[1], cpp[2], cpp[3]);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
+    }
+    if (lean) {  // KS3-lean: 64-row tiles, two CTAs per SM at most
+        const int64_t strips = ceil_div(a.d_pad, kXfCols);
+        int64_t off[kMaxWave + 1] = {0, 0, 0, 0, 0};
+        for (int g = 0; g < a.G; ++g) off[g + 1] = off[g] + strips * ceil_div(a.p[g].n_pad, kXlRows);
+        for (int g = a.G + 1; g <= kMaxWave; ++g) off[g] = off[a.G];
+        const int64_t total = off[a.G];
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(total, 4ll * sm_count));
+        static bool xl_configured = false;
+        if (!xl_configured) {
+            e = max_carveout((const void*)k1s_xform_lean);
+            if (e == cudaSuccess) e = max_carveout((const void*)k1s_coef);
+            if (e != cudaSuccess) return e;
+            xl_configured = true;
+        }
+        k1s_xform_lean<<<grid, kXlThreads, 0, st>>>(a, off[1], off[2], off[3], total);
+        return cudaGetLastError();
     }
     {  // KS3
         const int64_t strips = ceil_div(a.d_pad, kXfCols);

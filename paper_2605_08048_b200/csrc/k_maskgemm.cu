@@ -112,6 +112,17 @@ __device__ __forceinline__ double l_width(double r, double delta, double d) {
     return 2.0 * delta * (1.0 / r + 2.0 * r / (1.0 - r * r));
 }
 
+// Gram form (k_gram.cu): error of r from the form's own roundings, on top of the planes'
+// representation error that both forms share (R14).  |acc|^2 = sum_{j,k} G'_jk carries the
+// bf16 hi/lo rounding of the n^2 entries (2^-17 relative, independent signs: ~ sqrt of the
+// sum of squares, entries <= |z'|^2 <= 4, off-diagonal ones ~ 1/sqrt(d) of that) and the
+// fp32 accumulation of each U_bj over n terms (2^-24 per add); 8x margin as in R14;
+// dr = dS / (2 n^2 r).
+__device__ __forceinline__ double gram_delta(double n, double d, double r) {
+    const double dS = 8.0 * 4.0 * sqrt(1.0 + n / d) * (0x1p-17 * sqrt(n) + 0x1p-22 * n);
+    return dS / (2.0 * n * n * fmax(r, 1e-6));
+}
+
 // statistic of a tile row from its accumulated sums S1 = |sigma1|^2, S2 = |sigma2|^2;
 // T = L(r2) - L(r1) = log(q(r2)/q(r1)); eps = the test's representation-error scale
 __device__ __forceinline__ RowStat row_stat(const GemmArgs& g, const GemmTest& T, double S1, double S2,
@@ -126,8 +137,12 @@ __device__ __forceinline__ RowStat row_stat(const GemmArgs& g, const GemmTest& T
     // |r_gpu - r| <= 8 eps / sqrt(n d) per group (R14: the row errors average over the n
     // rows and the d coordinates; measured <= 1/4 of this bound at every tested shape)
     const double k = 8.0 * eps * rsqrt(d);
-    s.e = l_width(s.r1, T.n_x == 1 ? 0.0 : k * rsqrt((double)T.n_x), d) +
-          l_width(s.r2, T.n_y == 1 ? 0.0 : k * rsqrt((double)T.n_y), d);
+    double d1 = k * rsqrt((double)T.n_x), d2 = k * rsqrt((double)T.n_y);
+    if (T.gram) {  // + the Gram form's own rounding
+        d1 += gram_delta((double)T.n_x, d, s.r1);
+        d2 += gram_delta((double)T.n_y, d, s.r2);
+    }
+    s.e = l_width(s.r1, T.n_x == 1 ? 0.0 : d1, d) + l_width(s.r2, T.n_y == 1 ? 0.0 : d2, d);
     return s;
 }
 
@@ -469,6 +484,15 @@ __global__ void __maxnreg__(HAP_K3_MAXNREG)
             if (test_failed(T)) continue;
             const int np_tile = g.tile_npieces[tile];
             const int a = i & 1;
+            // Gram form: this row's mask bits for the piece's columns, loaded before the
+            // accumulator wait (width <= 256: at most 8 words)
+            uint32_t mw[8];
+            if (T.gram) {
+                const uint32_t* mb =
+                    T.mbits + (size_t)((tile - T.tile0) * R + trow) * (size_t)(T.n_pad >> 5) + (pd.y >> 5);
+#pragma unroll
+                for (int w = 0; w < 8; ++w) mw[w] = w < (width >> 5) ? __ldcg(mb + w) : 0u;
+            }
             mbar_wait(&tfull[a], ((uint32_t)i >> 1) & 1u);
             tc_fence_after();
             if (etid == 0) K3_STAMP(i, 4);
@@ -477,7 +501,33 @@ __global__ void __maxnreg__(HAP_K3_MAXNREG)
             const float4* abp = reinterpret_cast<const float4*>(T.ab + pd.y);
             const uint32_t tbase = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(a * kChunkN);
             const int nblk = (K3_EXP(g) & 8) ? 0 : width / 32;
-            for (int cb = 0; cb < nblk; cb += 2) {  // two 32-column loads in flight per wait
+            if (T.gram) {
+                // s1 = sum_j m_bj (U_bj + 2 alpha_j), s2 = sum_j m_bj (U_bj - 2 beta_j)
+#pragma unroll
+                for (int cb = 0; cb < 8; cb += 2) {
+                    if (cb >= nblk) break;
+                    uint32_t r[2][32];
+                    tmem_ld_32x32b_x32(tbase + (uint32_t)(32 * cb), r[0]);
+                    if (cb + 1 < nblk) tmem_ld_32x32b_x32(tbase + (uint32_t)(32 * cb + 32), r[1]);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        if (cb + h >= nblk) break;
+                        const uint32_t bits = mw[cb + h];
+#pragma unroll
+                        for (int j2 = 0; j2 < 16; ++j2) {
+                            const float4 k4 = __ldg(abp + (cb + h) * 16 + j2);  // {2al, 2be} x 2 columns
+                            const float x0 = __uint_as_float(r[h][2 * j2]), x1 = __uint_as_float(r[h][2 * j2 + 1]);
+                            const bool m0 = (bits >> (2 * j2)) & 1u, m1 = (bits >> (2 * j2 + 1)) & 1u;
+                            s1 += m0 ? x0 + k4.x : 0.f;
+                            s2 += m0 ? x0 - k4.y : 0.f;
+                            s1 += m1 ? x1 + k4.z : 0.f;
+                            s2 += m1 ? x1 - k4.w : 0.f;
+                        }
+                    }
+                }
+            }
+            for (int cb = 0; cb < (T.gram ? 0 : nblk); cb += 2) {  // two 32-column loads in flight per wait
                 uint32_t r[2][32];
                 tmem_ld_32x32b_x32(tbase + (uint32_t)(32 * cb), r[0]);
                 if (cb + 1 < nblk) tmem_ld_32x32b_x32(tbase + (uint32_t)(32 * cb + 32), r[1]);

@@ -41,11 +41,13 @@ def _cuda(a):
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
 
 
-def check_pair(ctx, orc, X, Y, B, s=0, mode=0, block=0, b_begin=0, b_end=None, pair_mode=0):
-    """Run both sides with stats; assert the parity bars; return (gpu, ref)."""
+def check_pair(ctx, orc, X, Y, B, s=0, mode=0, block=0, b_begin=0, b_end=None, pair_mode=0, gram=None):
+    """Run both sides with stats; assert the parity bars; return (gpu, ref).  gram: K3 form
+    (None = the library's choice, True = Gram form, False = plane form)."""
     b_end = B if b_end is None else b_end
     g = ctx.permtest_pair(_cuda(X), _cuda(Y), B, SEED, stream_id=s, mode=mode, block=block,
-                          b_begin=b_begin, b_end=b_end, want_stats=True, pair_mode=pair_mode)
+                          b_begin=b_begin, b_end=b_end, want_stats=True, pair_mode=pair_mode,
+                          gram=gram)
     ref = orc.run_pair(X, Y, B, SEED, s=s, mode=mode, b_begin=b_begin, b_end=b_end,
                        want_stats=True)
     Ls = abs(ref["L_x"]) + abs(ref["L_y"])
