@@ -88,7 +88,7 @@ namespace {
 enum Buf {
     kX = 0, kY, kNrm, kCoef, kPart, kXbar, kYbar, kU, kZhi, kZlo, kTpart, kT64, kAB, kMask,
     kM, kSconst, kGemmPart, kTileDone, kScal, kSpart, kScratch, kMask1, kInv, kStamps, kK3Stamps,
-    kSched, kSpans, kX2, kY2, kClaim, kGhi, kGlo, kGab, kMbits, kMbits1, kNumBufs
+    kSched, kSpans, kX2, kY2, kClaim, kGhi, kGlo, kGab, kMbits, kMbits1, kGacc, kNumBufs
 };
 
 hap_status fail(hap_ctx c, hap_status s, const std::string& msg) {
@@ -652,7 +652,8 @@ hap_status ensure_gram(hap_ctx w, int pair_mode) {
     const int64_t n_pad = w->n_pad, rows = zt_rows(n_pad);
     hap_status s;
     if ((s = ensure(w, kGhi, (size_t)rows * n_pad * 2)) || (s = ensure(w, kGlo, (size_t)rows * n_pad * 2)) ||
-        (s = ensure(w, kGab, (size_t)n_pad * 8)))
+        (s = ensure(w, kGab, (size_t)n_pad * 8)) ||
+        (s = ensure(w, kGacc, (size_t)n_pad * n_pad * 8 + (size_t)n_pad * 16)))
         return s;
     const void* keys[2] = {w->buf[kGhi], w->buf[kGlo]};
     const int64_t shape[2] = {n_pad, pair_mode};
@@ -679,11 +680,13 @@ hap_status build_gram(hap_ctx w, cudaStream_t st) {
         ga.g_hi = B<uint16_t>(w, kGhi);
         ga.g_lo = B<uint16_t>(w, kGlo);
         ga.gab = B<float2>(w, kGab);
+        ga.gacc = B<long long>(w, kGacc);
+        ga.gabacc = ga.gacc + n_pad * n_pad;
         ga.span = next_span(w, HAP_PHASE_ALIGN);
         cudaError_t e;
         {
-            PhaseScope ps(w, HAP_PHASE_ALIGN, 1, st);
-            e = launch_gram(ga, st);
+            PhaseScope ps(w, HAP_PHASE_ALIGN, 2, st);
+            e = launch_gram(ga, w->sm_count, st);
         }
         if (e != cudaSuccess) return cuda_fail(w, e, "Gram kernel");
         w->gram_ok = true;

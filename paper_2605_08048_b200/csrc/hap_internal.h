@@ -157,9 +157,11 @@ struct GramArgs {
     uint16_t* g_hi;          // [n_pad][n_pad] bf16 hi / lo of G' = Z' Z'^T
     uint16_t* g_lo;
     float2* gab;             // [n_pad] {2 a.z'_j, 2 b.z'_j}
+    long long* gacc;         // [n_pad][n_pad] fixed-point accumulators (zero between uses)
+    long long* gabacc;       // [n_pad][2]
     unsigned long long* span;
 };
-cudaError_t launch_gram(const GramArgs& g, cudaStream_t st);
+cudaError_t launch_gram(const GramArgs& g, int sm_count, cudaStream_t st);
 // bf16 mask rows [rows][n_pad] -> bits [rows][n_pad / 32] (bit j % 32 of word j / 32)
 cudaError_t launch_pack_bits(const uint16_t* mask, uint32_t* bits, int64_t rows, int n_pad, int sm_count,
                              cudaStream_t st);

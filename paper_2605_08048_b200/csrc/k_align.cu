@@ -262,16 +262,28 @@ __device__ __forceinline__ void store_words(uint32_t* dst, const uint32_t (&w)[W
 // accumulators and flags are cleared for the next launch.  Shared by the fused K1 and the
 // streaming K1s transform kernel.
 template <int NT = kThreads>
-__device__ void finish_pairs(const AlignArgs& a, double* red) {
+__device__ void finish_pair(const AlignArgs& a, int g, double* red) {
     const int tid = threadIdx.x;
     const int d = (int)a.d;
-    for (int g = 0; g < a.G; ++g) {
+    {
         const AlignPair& q = a.p[g];
         const int64_t N = q.n_x + q.n_y;
         double sa = 0.0, sb = 0.0, sm = 0.0;
-        for (int64_t c = tid; c < a.d_pad; c += NT) {
-            const double tsum = fix_get(q.acc + 2 * d + c);
-            const double m = __ldcg(q.m + c);
+        constexpr int kC = 8;  // loads of kC columns in flight per thread (ascending c)
+        for (int64_t c0 = tid; c0 < a.d_pad; c0 += kC * NT) {
+          double ts[kC], ms[kC];
+#pragma unroll
+          for (int u = 0; u < kC; ++u) {
+            const int64_t c = c0 + u * NT;
+            ts[u] = c < a.d_pad ? fix_get(q.acc + 2 * d + c) : 0.0;
+            ms[u] = c < a.d_pad ? __ldcg(q.m + c) : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < kC; ++u) {
+            const int64_t c = c0 + u * NT;
+            if (c >= a.d_pad) break;
+            const double tsum = ts[u];
+            const double m = ms[u];
             sm += m * m;
             q.t64[c] = (double)N * m + tsum;
             const float af = (float)((double)q.n_x * m);
@@ -279,6 +291,7 @@ __device__ void finish_pairs(const AlignArgs& a, double* red) {
             q.ab[c] = make_float2(2.0f * af, 2.0f * bf);
             sa += (double)af * (double)af;
             sb += (double)bf * (double)bf;
+          }
         }
         const double2 sab = block_sum2_n<NT>(sa, sb, red);
         const double smm = block_sum2_n<NT>(sm, 0.0, red).x;
@@ -293,10 +306,33 @@ __device__ void finish_pairs(const AlignArgs& a, double* red) {
             *q.bad = LLONG_MAX;  // reset the pair's ZeroVector word
         }
     }
-    if (tid == 0) {  // reset the ticket and the barrier
+}
+template <int NT = kThreads>
+__device__ void finish_pairs(const AlignArgs& a, double* red) {
+    for (int g = 0; g < a.G; ++g) finish_pair<NT>(a, g, red);
+    if (threadIdx.x == 0) {  // reset the ticket and the barrier
         reinterpret_cast<unsigned*>(a.scratch + 1)[0] = 0u;
         reinterpret_cast<unsigned*>(a.scratch + 2)[0] = 0u;
     }
+}
+
+// Per-pair completion tickets of the streaming kernels (K1s): the CTA that completes a
+// pair's last work unit runs that pair's scalar pass, so the pairs of a wave finish in
+// parallel on different CTAs instead of in series on the launch's last one.  Word 4 (KS1
+// items) / 5 (KS3 tiles) of the pair's own scratch; reset by the finishing CTA.
+__device__ __forceinline__ bool pair_ticket(const AlignPair& q, int word, unsigned units, unsigned total, int* s_flag) {
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned* t = reinterpret_cast<unsigned*>(q.bad + word);
+        const unsigned old = atomicAdd(t, units);
+        *s_flag = old + units == total;
+        if (old + units == total) *t = 0u;
+    }
+    __syncthreads();
+    const bool last = *s_flag != 0;
+    if (last) __threadfence();
+    return last;
 }
 
 // dynamic smem: tile f32 [R][P] | (u_c, m_c) f32 [d_pad] (stage_umc) | xs, ys f64 [d]
@@ -868,10 +904,24 @@ __global__ void __launch_bounds__(NT, 512 / NT) k1s_stats(AlignArgs a) {
             }
         }
     };
+    // a pair's P3 runs on the CTA that completes its last item (per-pair ticket)
+    int pg = i0 < i1 ? pair_of(a, i0) : 0;
+    unsigned pcnt = 0;
+    auto pair_done = [&]() {
+        flush();
+        const unsigned total = (unsigned)(a.item_off[pg + 1] - a.item_off[pg]);
+        if (pair_ticket(a.p[pg], 4, pcnt, total, &s_last)) stream_pair_scalars<NT>(a, pg, red);
+        pcnt = 0;
+    };
     for (int64_t item = i0; item < i1; ++item) {
         const int64_t k = item - i0;
         const int st = (int)(k % kSStages);
         const int g = pair_of(a, item);
+        if (g != pg) {
+            pair_done();
+            pg = g;
+        }
+        ++pcnt;
         const AlignPair& q = a.p[g];
         const int64_t N = q.n_x + q.n_y;
         const int64_t r0 = (item - a.item_off[g]) * R;
@@ -975,18 +1025,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k1s_stats(AlignArgs a) {
             }
         }
     }
-    flush();
-    // the last CTA forms every pair's means, axis, centre and observed statistic
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) s_last = atomicAdd(reinterpret_cast<unsigned*>(a.scratch + 3), 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (s_last) {
-        __threadfence();
-        for (int g = 0; g < a.G; ++g) stream_pair_scalars<NT>(a, g, red);
-        if (tid == 0) reinterpret_cast<unsigned*>(a.scratch + 3)[0] = 0u;
-    }
-    __syncthreads();
+    if (i0 < i1) pair_done();  // (a CTA without items takes part in no ticket)
     if (tid == 0) span_exit(a.span);
 }
 
@@ -1167,7 +1206,22 @@ __global__ void __launch_bounds__(kThreads, 1) k1s_xform(AlignArgs a, int64_t ti
         tacc = 0;
     };
     int slot = 0;
+    // a pair's P5 runs on the CTA that completes its last tile (per-pair ticket)
+    int pg = L.g;
+    unsigned pcnt = 0;
+    auto pair_done = [&]() {
+        flush();
+        cur_g = -1;  // (flushed)
+        const unsigned total = (unsigned)(strips * ((a.p[pg].n_pad + kXfRows - 1) / kXfRows));
+        if (pair_ticket(a.p[pg], 5, pcnt, total, &s_last)) finish_pair(a, pg, red);
+        pcnt = 0;
+    };
     for (int64_t t = t0; t < t1; ++t) {
+        if (L.g != pg) {
+            pair_done();
+            pg = L.g;
+        }
+        ++pcnt;
         if (L.g != cur_g || L.strip != cur_strip) {
             flush();
             if (L.g != cur_g) P = pair_fields(L.g);
@@ -1262,16 +1316,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1s_xform(AlignArgs a, int64_t ti
         }
     }
     cp_async_wait<0>();
-    flush();
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) s_last = atomicAdd(reinterpret_cast<unsigned*>(a.scratch + 1), 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (s_last) {
-        __threadfence();
-        finish_pairs(a, red);
-    }
-    __syncthreads();
+    if (t0 < t1) pair_done();
     if (tid == 0) span_exit(a.span);
 }
 
@@ -1352,7 +1397,22 @@ __global__ void __launch_bounds__(kXlThreads, 4) k1s_xform_lean(AlignArgs a, int
             atomicAdd(reinterpret_cast<unsigned long long*>(a.p[cur_g].acc + 2 * d + c), (unsigned long long)tacc);
         tacc = 0;
     };
+    // a pair's P5 runs on the CTA that completes its last tile (per-pair ticket)
+    int pg = L.g;
+    unsigned pcnt = 0;
+    auto pair_done = [&]() {
+        flush();
+        cur_g = -1;  // (flushed)
+        const unsigned total = (unsigned)(strips * ((a.p[pg].n_pad + kXlRows - 1) / kXlRows));
+        if (pair_ticket(a.p[pg], 5, pcnt, total, &s_last)) finish_pair<kXlThreads>(a, pg, red);
+        pcnt = 0;
+    };
     for (int64_t t = t0; t < t1; ++t) {
+        if (L.g != pg) {
+            pair_done();
+            pg = L.g;
+        }
+        ++pcnt;
         float4 h[8];
         float2 cv[8];
 #pragma unroll
@@ -1442,16 +1502,7 @@ __global__ void __launch_bounds__(kXlThreads, 4) k1s_xform_lean(AlignArgs a, int
         __syncthreads();  // the staging is free
         advance(L);
     }
-    flush();
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) s_last = atomicAdd(reinterpret_cast<unsigned*>(a.scratch + 1), 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (s_last) {
-        __threadfence();
-        finish_pairs<kXlThreads>(a, red);
-    }
-    __syncthreads();
+    if (t0 < t1) pair_done();
     if (tid == 0) span_exit(a.span);
 }
 }  // namespace

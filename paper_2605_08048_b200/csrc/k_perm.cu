@@ -239,13 +239,19 @@ __device__ __forceinline__ void emit_row_u32(const PermArgs& a, const PermTest& 
         const uint32_t t[4] = {q.x, q.y, q.z, q.w};
         const uint32_t v0 = 4u * (uint32_t)v4;
         uint32_t o[2];
+        // low position: selected unless exiled (t + 1 != 0); high: iff written (t != 0)
+        if (v0 + 4u <= nx || v0 >= nx) {  // all four on one side of n_x (all but one group)
+            const uint32_t k = v0 < nx ? 1u : 0u;
+            o[0] = (t[0] + k ? 0x3F80u : 0u) | (t[1] + k ? 0x3F800000u : 0u);
+            o[1] = (t[2] + k ? 0x3F80u : 0u) | (t[3] + k ? 0x3F800000u : 0u);
+        } else {
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            // low position: selected unless exiled (t + 1 != 0); high: iff written (t != 0)
-            const uint32_t va = v0 + 2 * e, vb = va + 1;
-            const bool sa = t[2 * e] + (va < nx ? 1u : 0u) != 0u;
-            const bool sb = t[2 * e + 1] + (vb < nx ? 1u : 0u) != 0u;
-            o[e] = (sa ? 0x3F80u : 0u) | (sb ? 0x3F800000u : 0u);
+            for (int e = 0; e < 2; ++e) {
+                const uint32_t va = v0 + 2 * e, vb = va + 1;
+                const bool sa = t[2 * e] + (va < nx ? 1u : 0u) != 0u;
+                const bool sb = t[2 * e + 1] + (vb < nx ? 1u : 0u) != 0u;
+                o[e] = (sa ? 0x3F80u : 0u) | (sb ? 0x3F800000u : 0u);
+            }
         }
         row[v4] = make_uint2(o[0], o[1]);
     }
