@@ -22,6 +22,14 @@ HAP_API hap_status hap_debug_k3_stamps(hap_ctx ctx, long long* out, int64_t n);
  * events (entry, P1 done, barrier passed, -, P3 done, P4 coefficients done, P4 done, exit);
  * out holds n int64 (at most 8 + 8 * SM count are written). */
 HAP_API hap_status hap_debug_k1_stamps(hap_ctx ctx, long long* out, int64_t n);
+/* Checked build only (libhap_checked.so, -DHAP_DEVICE_CHECKS):
+ * synchronises the device, then writes to *word [host] the first failed device-side bounds /
+ * invariant check since the last call ({translation unit << 32 | source line}: 1 k_align.cu,
+ * 2 k_perm.cu, 3 k_maskgemm.cu, 4 k_gram.cu; 0 = none) and clears it; it also verifies
+ * the guard bytes (0xA5) past the requested size of every workspace buffer of ctx and its
+ * batch sub-contexts and returns HAP_E_CUDA (message: the buffer) if one was overwritten.
+ * The release library writes 0 and returns HAP_E_INVALID_ARG (no checks compiled in). */
+HAP_API hap_status hap_debug_check_status(hap_ctx ctx, uint64_t* word);
 /* Scheduling experiments: enqueue a register-only Philox loop of `iters` rounds on
  * ctas x threads threads, no shared memory. */
 HAP_API hap_status hap_debug_alu_burn(hap_ctx ctx, uint32_t iters, int ctas, int threads, void* stream);

@@ -16,8 +16,11 @@ import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 # HAP_LIB_VARIANT (experiments only): load variants/libhap_<name>.so built with other flags
+# HAP_LIB=checked: the device-checked build (tests only)
 LIB_PATH = (os.path.join(os.path.dirname(_PKG), "variants", f"libhap_{os.environ['HAP_LIB_VARIANT']}.so")
-            if os.environ.get("HAP_LIB_VARIANT") else os.path.join(_PKG, "libhap.so"))
+            if os.environ.get("HAP_LIB_VARIANT") else
+            os.path.join(_PKG, "libhap_checked.so") if os.environ.get("HAP_LIB") == "checked"
+            else os.path.join(_PKG, "libhap.so"))
 
 HAP_OK = 0
 STATUS_NAMES = {0: "OK", 1: "INVALID_ARG", 2: "DIM_MISMATCH", 3: "ZERO_VECTOR",
@@ -99,6 +102,7 @@ def lib() -> ctypes.CDLL:
         "hap_profile_k1_phases": ([vp, P(f64)], i32),
         "hap_debug_k3_stamps": ([vp, vp, i64], i32),
         "hap_debug_k1_stamps": ([vp, vp, i64], i32),
+        "hap_debug_check_status": ([vp, P(u64)], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -390,3 +394,10 @@ class Context:
                             p_value=hap_pvalue(c[0], B) if ok else None,
                             p_two_sided=hap_pvalue(c[1], B) if ok else None))
         return out
+
+
+def hap_debug_check_status(ctx):
+    """Checked build: (status, first failed device check word); see include/hap_debug.h."""
+    w = ctypes.c_uint64(0)
+    st = lib().hap_debug_check_status(ctx, ctypes.byref(w))
+    return st, int(w.value)

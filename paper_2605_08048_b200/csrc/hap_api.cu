@@ -28,6 +28,7 @@ struct hap_ctx_s {
     // ---- workspace (grow-only)
     void* buf[40] = {};
     size_t cap[40] = {};
+    size_t req[40] = {};  // checked build: bytes requested (guard bytes beyond, up to cap)
     // ---- state of the last successful hap_align
     bool aligned = false;
     bool gram_ok = false;  // the Gram planes of the current alignment are built (k_gram.cu)
@@ -103,7 +104,12 @@ hap_status cuda_fail(hap_ctx c, cudaError_t e, const char* what) {
 // grow-only device buffer
 hap_status ensure(hap_ctx c, int which, size_t bytes) {
     bytes = std::max<size_t>(bytes, 256);
-    if (c->cap[which] >= bytes) return HAP_OK;
+    if (c->cap[which] >= bytes) {
+#ifdef HAP_DEVICE_CHECKS
+        c->req[which] = std::max(c->req[which], bytes);  // the guard starts past the largest request
+#endif
+        return HAP_OK;
+    }
     if (c->buf[which]) {
         if (c->last_stream) cudaStreamSynchronize(c->last_stream);
         if (c->side) cudaStreamSynchronize(c->side);
@@ -120,6 +126,12 @@ hap_status ensure(hap_ctx c, int which, size_t bytes) {
     // zero it and wait: the consumers run on non-blocking streams (lanes, generator, copies),
     // which the legacy-stream memset does not order (allocation is a slow path anyway)
     e = cudaMemset(c->buf[which], 0, alloc);
+#ifdef HAP_DEVICE_CHECKS
+    // guard bytes past the request: a kernel that writes beyond what its buffer was sized
+    // for is reported by hap_debug_check_status
+    if (e == cudaSuccess) e = cudaMemset(static_cast<char*>(c->buf[which]) + bytes, 0xA5, alloc - bytes);
+    c->req[which] = bytes;
+#endif
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return fail(c, HAP_E_CUDA, std::string("workspace zeroing: ") + cudaGetErrorString(e));
     c->cap[which] = alloc;
@@ -1542,6 +1554,39 @@ hap_status hap_perm_sets(hap_ctx c, uint64_t seed, uint32_t stream_id, uint64_t 
     cudaError_t e = launch_perm(pa, c->sm_count, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(c, e, "perm generator");
     return HAP_OK;
+}
+
+hap_status hap_debug_check_status(hap_ctx c, uint64_t* word) {
+    if (!c || !word) return HAP_E_INVALID_ARG;
+    *word = 0;
+#ifdef HAP_DEVICE_CHECKS
+    cudaSetDevice(c->device);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(c, e, "check sync");
+    const unsigned long long w[4] = {check_word_align(), check_word_perm(), check_word_gemm(), check_word_gram()};
+    for (unsigned long long v : w)
+        if (v && !*word) *word = v;
+    std::vector<hap_ctx> all = {c};
+    for (auto& lane : c->sub)
+        for (hap_ctx s : lane)
+            if (s) all.push_back(s);
+    std::vector<unsigned char> tail;
+    for (hap_ctx s : all)
+        for (int b = 0; b < kNumBufs; ++b) {
+            if (!s->buf[b] || s->cap[b] <= s->req[b]) continue;
+            tail.resize(s->cap[b] - s->req[b]);
+            if (cudaMemcpy(tail.data(), static_cast<char*>(s->buf[b]) + s->req[b], tail.size(),
+                           cudaMemcpyDeviceToHost) != cudaSuccess)
+                return fail(c, HAP_E_CUDA, "guard readback");
+            for (unsigned char x : tail)
+                if (x != 0xA5)
+                    return fail(c, HAP_E_CUDA, "guard bytes of workspace buffer " + std::to_string(b) +
+                                                   " overwritten");
+        }
+    return HAP_OK;
+#else
+    return fail(c, HAP_E_INVALID_ARG, "release library: no device checks compiled in");
+#endif
 }
 
 hap_status hap_debug_alu_burn(hap_ctx c, uint32_t iters, int ctas, int threads, void* stream) {

@@ -27,6 +27,34 @@ HAP_DEV void span_exit(unsigned long long* span) {
     if (span) atomicMax(span + 1, global_ns());
 }
 
+// ---- device checks (the checked build, -DHAP_DEVICE_CHECKS: libhap_checked.so).  A
+// failed HAP_CHECK records {translation unit, source line} of the FIRST failure in a
+// per-translation-unit word (read and cleared by hap_debug_check_status) and execution
+// continues; the release library compiles every check out.  The stand-in for
+// compute-sanitizer, which this GPU pool refuses.
+#ifdef HAP_DEVICE_CHECKS
+static __device__ unsigned long long g_hap_check = 0ull;
+#define HAP_CHECK(cond)                                                                         \
+    do {                                                                                       \
+        if (!(cond))                                                                           \
+            atomicCAS(&g_hap_check, 0ull, ((unsigned long long)HAP_CHECK_TU << 32) | __LINE__); \
+    } while (0)
+// host side: read and clear this translation unit's word
+#define HAP_CHECK_ACCESSOR(fn)                                                   \
+    unsigned long long fn() {                                                   \
+        unsigned long long v = 0ull, z = 0ull;                                   \
+        cudaMemcpyFromSymbol(&v, g_hap_check, sizeof v);                        \
+        cudaMemcpyToSymbol(g_hap_check, &z, sizeof z);                          \
+        return v;                                                               \
+    }
+#else
+#define HAP_CHECK(cond) \
+    do {                \
+    } while (0)
+#define HAP_CHECK_ACCESSOR(fn) \
+    unsigned long long fn() { return 0ull; }
+#endif
+
 HAP_DEV uint32_t lane_id() { return threadIdx.x & 31u; }
 HAP_DEV uint32_t warp_id() { return __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0); }
 HAP_DEV bool elect_one() {
@@ -274,6 +302,31 @@ HAP_DEV u32x4 philox4x32_10(u32x4 c, uint32_t k0, uint32_t k1) {
     }
     return c;
 }
+// the ten round keys of a (seed) key, computed once per permutation instead of once per
+// block (2 adds per round otherwise)
+struct PhiloxKeys {
+    uint32_t a[10], b[10];
+};
+HAP_DEV PhiloxKeys philox_keys(uint32_t k0, uint32_t k1) {
+    PhiloxKeys K;
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        K.a[r] = k0;
+        K.b[r] = k1;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    return K;
+}
+HAP_DEV u32x4 philox4x32_10(u32x4 c, const PhiloxKeys& K) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+        const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+        c = u32x4{hi1 ^ c.y ^ K.a[r], lo1, hi0 ^ c.w ^ K.b[r], lo0};
+    }
+    return c;
+}
 HAP_DEV uint32_t u32x4_get(const u32x4& v, uint32_t e) {
     return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
 }
@@ -302,8 +355,10 @@ HAP_DEV uint32_t fy_target(uint32_t x, uint32_t k, uint32_t N, uint32_t b,
 
 // targets j_k = k + U(N - k) of steps k0 .. k0+3 (one Philox block; Lemire, exact slow path)
 HAP_DEV void draw_targets(uint32_t k0, uint32_t nx, uint32_t N, uint32_t b,
-                                             uint32_t s, uint32_t key0, uint32_t key1, uint32_t j[4]) {
-    const u32x4 wd = philox4x32_10(u32x4{k0 >> 2, b, s, 0u}, key0, key1);
+                                             uint32_t s, uint32_t key0, uint32_t key1, uint32_t j[4],
+                                             const PhiloxKeys* K = nullptr) {
+    const u32x4 wd = K ? philox4x32_10(u32x4{k0 >> 2, b, s, 0u}, *K)
+                       : philox4x32_10(u32x4{k0 >> 2, b, s, 0u}, key0, key1);
     const uint32_t x[4] = {wd.x, wd.y, wd.z, wd.w};
     bool slow = false;
 #pragma unroll

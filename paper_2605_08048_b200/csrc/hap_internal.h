@@ -10,6 +10,13 @@
 
 namespace hap {
 
+// checked build (-DHAP_DEVICE_CHECKS): first failed device check per translation unit,
+// {unit << 32 | line}, 0 = none; read and cleared (0 in the release library)
+unsigned long long check_word_align();
+unsigned long long check_word_perm();
+unsigned long long check_word_gemm();
+unsigned long long check_word_gram();
+
 constexpr int kKBlock = 64;     // GEMM K-block: 64 bf16 = one 128-byte swizzle atom
 constexpr int kTileM = 128;     // permutations per CTA tile (TMEM lanes)
 constexpr int kChunkN = 256;    // d-columns per accumulator chunk (UMMA N <= 256)

@@ -32,6 +32,7 @@
 #include <cstdlib>
 #include <algorithm>
 
+#define HAP_CHECK_TU 1
 #include "hap_device.cuh"
 #include "hap_internal.h"
 
@@ -814,6 +815,98 @@ __device__ void stream_pair_scalars(const AlignArgs& a, int g, double* red) {
     __syncthreads();
 }
 
+// P3 with every column's accumulators loaded ONCE into registers (kC >= d / NT columns per
+// thread, all loads in flight together): one L2 round trip instead of three passes of
+// dependent loads (the warp-per-row KS1 calls it after its main loop, when registers are
+// free).  Same arithmetic and per-thread order as stream_pair_scalars.
+template <int NT, int kC>
+__device__ void stream_pair_scalars_cached(const AlignArgs& a, int g, double* red) {
+    const AlignPair& q = a.p[g];
+    const int tid = threadIdx.x;
+    const int d = (int)a.d;
+    const long long* acc_x = q.acc;
+    const long long* acc_y = q.acc + d;
+    const int64_t N = q.n_x + q.n_y;
+    const double rnX = 1.0 / (double)q.n_x, rnY = 1.0 / (double)q.n_y;
+    double xb[kC], yb[kC];
+#pragma unroll
+    for (int u = 0; u < kC; ++u) {
+        const int c = tid + u * NT;
+        xb[u] = c < d ? fix_get(acc_x + c) * rnX : 0.0;
+        yb[u] = c < d ? fix_get(acc_y + c) * rnY : 0.0;
+    }
+    double sxx = 0.0, syy = 0.0;
+#pragma unroll
+    for (int u = 0; u < kC; ++u) {
+        const int c = tid + u * NT;
+        if (c < d) {
+            q.xbar[c] = xb[u];
+            q.ybar[c] = yb[u];
+            sxx += xb[u] * xb[u];
+            syy += yb[u] * yb[u];
+        }
+    }
+    const double2 sq = block_sum2_n<NT>(sxx, syy, red);
+    const double nx = sqrt(sq.x), ny = sqrt(sq.y);
+    const bool degenerate = nx < 1e-12 || ny < 1e-12;
+    const double rnx = degenerate ? 0.0 : 1.0 / nx;
+    const double rny = degenerate ? 0.0 : 1.0 / ny;
+    double sv = 0.0, svx = 0.0;
+#pragma unroll
+    for (int u = 0; u < kC; ++u) {
+        if (tid + u * NT < d) {
+            const double v = xb[u] * rnx - yb[u] * rny;
+            sv += v * v;
+            svx += v * xb[u];
+        }
+    }
+    const double2 vv = block_sum2_n<NT>(sv, svx, red);
+    const double nv0 = sqrt(vv.x);
+    const bool identity = (a.mode == HAP_ALIGN_NONE) || degenerate || nv0 < 1e-9;  // R3
+    const double rnv = identity ? 0.0 : 1.0 / nv0;
+    const double ux = vv.y * rnv;
+    const double rN = 4096.0 / (double)N;
+#pragma unroll
+    for (int u = 0; u < kC; ++u) {
+        const int c = tid + u * NT;
+        double ud = 0.0, md = 0.0;
+        if (c < d) {
+            ud = (xb[u] * rnx - yb[u] * rny) * rnv;
+            const double t = (double)q.n_x * (xb[u] - 2.0 * ud * ux) + (double)q.n_y * yb[u];
+            md = rint(t * rN) * (1.0 / 4096.0);
+        }
+        if (c < (int)a.d_pad) {
+            q.u[c] = ud;
+            q.m[c] = md;
+        }
+    }
+    for (int c = tid + kC * NT; c < (int)a.d_pad; c += NT) {  // padding columns beyond kC NT
+        q.u[c] = 0.0;
+        q.m[c] = 0.0;
+    }
+    if (tid == 0) {
+        hap_align_info* f = q.info;
+        const long long bad = *reinterpret_cast<volatile long long*>(q.bad);
+        f->n_x = q.n_x;
+        f->n_y = q.n_y;
+        f->d = a.d;
+        f->n_pad = q.n_pad;
+        f->d_pad = a.d_pad;
+        f->is_identity = identity ? 1 : 0;
+        f->status = bad < N ? HAP_E_ZERO_VECTOR : (degenerate ? HAP_E_DEGENERATE_MEAN : HAP_OK);
+        f->bad_row = bad < N ? bad : -1;
+        f->r_x = nx;  // r(X') = ||xbar||
+        f->r_y = ny;
+        const double lx = logkappa64(nx, (double)a.d), ly = logkappa64(ny, (double)a.d);
+        f->logk_x = lx;
+        f->logk_y = ly;
+        f->t_obs = (isinf(lx) && isinf(ly)) ? 0.0 : ly - lx;  // Eq. 10
+        const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+        f->gemm_r_x = f->gemm_r_y = f->gemm_t_obs = qnan;
+    }
+    __syncthreads();
+}
+
 // KS1.  a.item_off: items of R rows (R = 8 / G4), ceil(N/R) per pair.  CTA c takes items
 // [I c / grid, I (c+1) / grid); 256 threads, two CTAs per SM.  Thread t owns the float4
 // column groups t + 256 k (k < G4) of every row of an item: it widens each fp32 value to
@@ -925,6 +1018,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k1s_stats(AlignArgs a) {
         const AlignPair& q = a.p[g];
         const int64_t N = q.n_x + q.n_y;
         const int64_t r0 = (item - a.item_off[g]) * R;
+        HAP_CHECK(g < a.G && r0 >= 0 && r0 < N && item < a.item_off[a.G]);
         const int nr = (int)(N - r0 < R ? N - r0 : R);
         double v[R][G4][4];
         if constexpr (kRing) {
@@ -1026,6 +1120,112 @@ __global__ void __launch_bounds__(NT, 512 / NT) k1s_stats(AlignArgs a) {
         }
     }
     if (i0 < i1) pair_done();  // (a CTA without items takes part in no ticket)
+    if (tid == 0) span_exit(a.span);
+}
+
+// KS1-lean for d <= 1024 (C1, C2, C4, C5): WARP per row, no block-wide barrier per item.
+// A CTA takes a contiguous run of ONE pair's items (cta_items) of 8 rows; its 4 warps take
+// the items in turn.  A warp streams an item's rows (lane = float4 column groups l + 32 k,
+// the next row in flight), forms the row norm with a butterfly (identical bits in every
+// lane) -> 1/||h|| (ZeroVector check), and adds x = h/||h|| into fp64 register partials of
+// its columns; each (item, side) segment is rounded to fixed point and added into the CTA's
+// int64 shared-memory column sums (exact, order-free), flushed once per CTA.  Bits depend on
+// the pair's shape only (rounding per item), not on the grid.  The per-pair ticket runs P3.
+constexpr int kSWRows = 8;
+template <int G>
+__global__ void __launch_bounds__(kS1LeanThreads, 4) k1s_stats_warp(AlignArgs a) {
+    constexpr int W = kS1LeanThreads / 32;
+    extern __shared__ __align__(16) long long sw_acc[];  // [2][d] X / Y column sums
+    __shared__ double red[2 * W + 2];
+    __shared__ int s_last;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int d = (int)a.d, d4 = d >> 2;
+    if (tid == 0) span_enter(a.span);
+    int64_t i0, i1;
+    cta_items(a, blockIdx.x, gridDim.x, i0, i1);
+    if (i0 >= i1) {
+        if (tid == 0) span_exit(a.span);
+        return;
+    }
+    const int g = pair_of(a, i0);
+    const AlignPair& q = a.p[g];
+    const int64_t N = q.n_x + q.n_y;
+    for (int c = tid; c < 2 * d; c += kS1LeanThreads) sw_acc[c] = 0;
+    __syncthreads();
+    auto load_row = [&](int64_t i, float4 (&f)[G]) {
+        const float4* rp = reinterpret_cast<const float4*>(row_ptr(q, i));
+#pragma unroll
+        for (int k = 0; k < G; ++k) {
+            const int c4 = lane + 32 * k;
+            f[k] = c4 < d4 ? __ldcs(rp + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    };
+    for (int64_t item = i0 + warp; item < i1; item += W) {
+        const int64_t r0 = (item - a.item_off[g]) * kSWRows;
+        const int nr = (int)(N - r0 < kSWRows ? N - r0 : kSWRows);
+        HAP_CHECK(r0 >= 0 && nr >= 1);
+        double p[G][4];
+#pragma unroll
+        for (int k = 0; k < G; ++k) p[k][0] = p[k][1] = p[k][2] = p[k][3] = 0.0;
+        int side = r0 < q.n_x ? 0 : 1;
+        auto flush = [&]() {  // this (item, side) segment -> fixed point -> CTA sums
+            long long* dst = sw_acc + side * d;
+#pragma unroll
+            for (int k = 0; k < G; ++k) {
+                const int c4 = lane + 32 * k;
+                if (c4 < d4)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const long long v = __double2ll_rn(p[k][e] * kFixScale);
+                        if (v) atomicAdd(reinterpret_cast<unsigned long long*>(dst + 4 * c4 + e), (unsigned long long)v);
+                        p[k][e] = 0.0;
+                    }
+            }
+        };
+        float4 nxt[G];
+        load_row(r0, nxt);
+        for (int r = 0; r < nr; ++r) {
+            float4 cur[G];
+#pragma unroll
+            for (int k = 0; k < G; ++k) cur[k] = nxt[k];
+            if (r + 1 < nr) load_row(r0 + r + 1, nxt);
+            const int rs = r0 + r < q.n_x ? 0 : 1;
+            if (rs != side) {
+                flush();
+                side = rs;
+            }
+            double sq0 = 0.0, sq1 = 0.0;
+#pragma unroll
+            for (int k = 0; k < G; ++k) {
+                const double x0 = cur[k].x, x1 = cur[k].y, x2 = cur[k].z, x3 = cur[k].w;
+                sq0 += x0 * x0 + x1 * x1;
+                sq1 += x2 * x2 + x3 * x3;
+            }
+            const double ss = warp_sum(sq0 + sq1);
+            const double nrm = sqrt(ss);
+            const double iv = nrm >= 1e-12 ? 1.0 / nrm : 0.0;
+            if (lane == 0) {
+                q.inv[r0 + r] = iv;
+                if (nrm < 1e-12) atomicMin(q.bad, (long long)(r0 + r));
+            }
+#pragma unroll
+            for (int k = 0; k < G; ++k) {
+                p[k][0] += (double)cur[k].x * iv;
+                p[k][1] += (double)cur[k].y * iv;
+                p[k][2] += (double)cur[k].z * iv;
+                p[k][3] += (double)cur[k].w * iv;
+            }
+        }
+        flush();
+    }
+    __syncthreads();
+    for (int c = tid; c < 2 * d; c += kS1LeanThreads) {
+        const long long v = sw_acc[c];
+        if (v) atomicAdd(reinterpret_cast<unsigned long long*>(q.acc + c), (unsigned long long)v);
+    }
+    const unsigned total = (unsigned)(a.item_off[g + 1] - a.item_off[g]);
+    if (pair_ticket(q, 4, (unsigned)(i1 - i0), total, &s_last))
+        stream_pair_scalars_cached<kS1LeanThreads, (32 * G + kS1LeanThreads - 1) / kS1LeanThreads * 4>(a, g, red);
     if (tid == 0) span_exit(a.span);
 }
 
@@ -1442,6 +1642,7 @@ __global__ void __launch_bounds__(kXlThreads, 4) k1s_xform_lean(AlignArgs a, int
         const AlignPair& qp = a.p[L.g];
         const int N = (int)(qp.n_x + qp.n_y), n_pad = (int)qp.n_pad;
         const int r0 = L.rt * kXlRows, cb = L.strip * kXfCols;
+        HAP_CHECK(L.g < a.G && r0 < n_pad && cb < d_pad && N <= n_pad);
         const bool cvalid = cb + 4 * q < d;
 #pragma unroll
         for (int hp = 0; hp < 4; ++hp) {  // row pair (2p, 2p+1) + 16 hp
@@ -1548,10 +1749,37 @@ bool align_uses_stream(const AlignArgs& a) {
 
 int align_launch_count(const AlignArgs& a) { return align_uses_stream(a) ? 3 : 1; }
 
+static cudaError_t launch_align_ks23(AlignArgs a, int sm_count, cudaStream_t st, bool lean);
+
 static cudaError_t launch_align_stream(AlignArgs a, int sm_count, cudaStream_t st) {
     const int d = (int)a.d;
     // every pair of a launch takes the same variant (the callers form waves so)
     const bool lean = align_path(a.p[0].n_x + a.p[0].n_y, a.d) == kAlignLean;
+    cudaError_t e;
+    if (lean && d <= 1024) {  // KS1 warp-per-row variant (items of 8 rows)
+        a.item_off[0] = 0;
+        for (int g = 0; g < a.G; ++g)
+            a.item_off[g + 1] = a.item_off[g] + ceil_div(a.p[g].n_x + a.p[g].n_y, kSWRows);
+        const int G = (int)ceil_div(d, 128);
+        const void* fw[8] = {(const void*)k1s_stats_warp<1>, (const void*)k1s_stats_warp<2>,
+                             (const void*)k1s_stats_warp<3>, (const void*)k1s_stats_warp<4>,
+                             (const void*)k1s_stats_warp<5>, (const void*)k1s_stats_warp<6>,
+                             (const void*)k1s_stats_warp<7>, (const void*)k1s_stats_warp<8>};
+        const void* fn = fw[G - 1];
+        static bool sw_configured[8] = {};
+        if (!sw_configured[G - 1]) {
+            e = max_carveout(fn);
+            if (e != cudaSuccess) return e;
+            sw_configured[G - 1] = true;
+        }
+        const int64_t items = a.item_off[a.G];
+        // ~4 items per CTA (one per warp), at least one CTA per pair
+        const int grid = (int)std::max<int64_t>(a.G, std::min<int64_t>(ceil_div(items, 4), 4ll * sm_count));
+        void* args[] = {&a};
+        e = cudaLaunchKernel(fn, dim3(grid), dim3(kS1LeanThreads), args, (size_t)2 * d * 8, st);
+        if (e != cudaSuccess) return e;
+        return launch_align_ks23(a, sm_count, st, lean);
+    }
     const int nt1 = lean ? kS1LeanThreads : kS1Threads;
     const int g4 = (int)ceil_div(d / 4, nt1);           // float4 column groups per thread
     const int G4t = g4 <= 1 ? 1 : g4 <= 2 ? 2 : g4 <= 4 ? 4 : 8;  // template instance
@@ -1569,7 +1797,6 @@ static cudaError_t launch_align_stream(AlignArgs a, int sm_count, cudaStream_t s
                                         : (const void*)k1s_stats<4>);
     static size_t configured[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // dynamic smem configured + 1
     const int fi = (G4t == 1 ? 0 : G4t == 2 ? 1 : G4t == 4 ? 2 : 3) + (lean ? 4 : 0);
-    cudaError_t e;
     if (smem1 + 1 > configured[fi]) {
         e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
         if (e == cudaSuccess) e = max_carveout(fn);
@@ -1582,6 +1809,11 @@ static cudaError_t launch_align_stream(AlignArgs a, int sm_count, cudaStream_t s
         e = cudaLaunchKernel(fn, dim3(grid), dim3(nt1), args, smem1, st);
         if (e != cudaSuccess) return e;
     }
+    return launch_align_ks23(a, sm_count, st, lean);
+}
+
+static cudaError_t launch_align_ks23(AlignArgs a, int sm_count, cudaStream_t st, bool lean) {
+    cudaError_t e;
     {  // KS2: CTAs in proportion to the pairs' rows, ~4 per SM in total
         int cpp[kMaxWave] = {0, 0, 0, 0}, total = 0;
         for (int g = 0; g < a.G; ++g) {  // one warp per X row (8 warps per CTA)
@@ -1682,5 +1914,7 @@ cudaError_t launch_align(const AlignArgs& a, int grid, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     return cudaEventRecord(last, st);
 }
+
+HAP_CHECK_ACCESSOR(check_word_align)
 
 }  // namespace hap

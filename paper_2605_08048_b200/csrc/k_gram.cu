@@ -29,6 +29,7 @@
 
 #include <algorithm>
 
+#define HAP_CHECK_TU 4
 #include "hap_device.cuh"
 #include "hap_internal.h"
 
@@ -62,6 +63,7 @@ __global__ void __launch_bounds__(kGThreads) k1g_gram(GramArgs g) {
     const int kb = jb + rem;
     const int j0 = jb * kGT, k0 = kb * kGT;
     const bool diag = jb == kb;
+    HAP_CHECK(kb < T && k0 + kGT <= g.n_pad && split * kGSplit < g.d_pad);
     if (tid == 0 && blockIdx.x == 0 && split == 0) span_enter(g.span);
     const int ty = tid >> 4, tx = tid & 15;  // outputs (j0 + 4 ty + u, k0 + 4 tx + v)
     // staging role: column cc = tid / 8, rows 8 (tid % 8) .. + 7 (one 16-byte load per plane)
@@ -223,5 +225,7 @@ cudaError_t launch_pack_bits(const uint16_t* mask, uint32_t* bits, int64_t rows,
     k2_pack_bits<<<grid, 256, 0, st>>>(mask, bits, rows, n_pad);
     return cudaGetLastError();
 }
+
+HAP_CHECK_ACCESSOR(check_word_gram)
 
 }  // namespace hap

@@ -31,6 +31,7 @@
 // statistics and counts.
 #include <cmath>
 
+#define HAP_CHECK_TU 3
 #include "hap_device.cuh"
 #include "hap_internal.h"
 
@@ -372,6 +373,10 @@ __global__ void __maxnreg__(HAP_K3_MAXNREG)
                 const int4 pd = g.pieces[pc];  // {wave tile, col0, width, slot}
                 const int tile = pd.x, width = pd.z;
                 const int ti = test_of(g, tile);
+                HAP_CHECK(tile >= 0 && tile < g.ntiles && pd.w >= 0 && pd.w < g.max_slots);
+                HAP_CHECK(width > 0 && width <= kChunkN && width % 32 == 0 && pd.y % 32 == 0 &&
+                          pd.y + width <= g.t[ti].ncols);
+                HAP_CHECK(pd.w < g.tile_npieces[tile]);
                 if (!test_failed(g.t[ti])) {
                     const int nkb = g.t[ti].n_pad / kKBlock;
                     const CUtensorMap* tmA = &maps.a[ti];
@@ -483,6 +488,9 @@ __global__ void __maxnreg__(HAP_K3_MAXNREG)
             const GemmTest& T = g.t[ti];
             if (test_failed(T)) continue;
             const int np_tile = g.tile_npieces[tile];
+            HAP_CHECK(np_tile >= 1 && np_tile <= g.max_slots && trow < R);
+            HAP_CHECK(!T.gram || (T.mbits != nullptr &&
+                                  tile - T.tile0 < (ti + 1 < g.G ? g.t[ti + 1].tile0 : g.ntiles) - T.tile0));
             const int a = i & 1;
             // Gram form: this row's mask bits for the piece's columns, loaded before the
             // accumulator wait (width <= 256: at most 8 words)
@@ -650,5 +658,7 @@ cudaError_t launch_maskgemm(const GemmMaps& maps, const GemmArgs& g, int pair_mo
     if (g.ntiles <= 0) return cudaSuccess;
     return pair_mode == 2 ? launch_impl<2>(maps, g, st) : launch_impl<1>(maps, g, st);
 }
+
+HAP_CHECK_ACCESSOR(check_word_gemm)
 
 }  // namespace hap

@@ -20,6 +20,7 @@
 
 #include <cstdlib>
 
+#define HAP_CHECK_TU 2
 #include "hap_device.cuh"
 #include "hap_internal.h"
 
@@ -228,6 +229,7 @@ __device__ __forceinline__ void emit_row_u32(const PermArgs& a, const PermTest& 
                                              int64_t li, uint32_t nx, int l, int nthreads) {
     const int64_t R1 = a.rows_per_tile - 1;
     const int64_t orow = (li / R1) * a.rows_per_tile + 1 + li % R1;
+    HAP_CHECK(orow < (int64_t)T.ntiles * a.rows_per_tile && (T.n_pad & 3) == 0);
     // lane = 4 consecutive entries per step (contiguous 512 B per warp: conflict-free
     // LDS/STS.128), 8-byte stores of 4 bf16 (256 B per warp)
     uint2* row = reinterpret_cast<uint2*>(static_cast<uint16_t*>(T.out) + orow * T.n_pad);
@@ -326,12 +328,14 @@ __global__ void __launch_bounds__(kPW * 32) k2_perm_fy32(PermArgs a, int lt_pitc
                 }
             }
         } else {
+            const PhiloxKeys K = philox_keys(key0, key1);
             for (uint32_t k0 = 4u * (uint32_t)tid; k0 < nx; k0 += 4u * kT) {
                 uint32_t j[4];
-                draw_targets(k0, nx, N, b, s, key0, key1, j);
+                draw_targets(k0, nx, N, b, s, key0, key1, j, &K);
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {  // unconditional: no-op steps hit the lane's sink
                     const uint32_t k = k0 + e;
+                    HAP_CHECK(k >= nx || (j[e] >= k && j[e] < N));
                     atomicMax((k < nx && j[e] != k) ? LT + j[e] : sink, k + 1u);
                 }
             }
@@ -369,6 +373,7 @@ __global__ void __launch_bounds__(kPW * 32) k2_perm_fy32(PermArgs a, int lt_pitc
             for (int bit = 0; bit < 4; ++bit)
                 at += (uint32_t)__popc(__ballot_sync(0xffffffffu, (cnt >> bit) & 1u) & lane_lt) << bit;
             const uint32_t tot = __reduce_add_sync(0xffffffffu, cnt);
+            HAP_CHECK(at + 8u <= (uint32_t)(lt_pitch / 2 + 16));
 #pragma unroll
             for (int e = 0; e < 8; ++e)
                 if (t[e] != 0u && u[e] != 0u) starts[at++] = (uint16_t)(u[e] - 1u);
@@ -587,5 +592,7 @@ cudaError_t launch_perm(const PermArgs& a, int sm_count, cudaStream_t st) {
     }
     return cudaGetLastError();
 }
+
+HAP_CHECK_ACCESSOR(check_word_perm)
 
 }  // namespace hap

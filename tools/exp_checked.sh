@@ -1,0 +1,6 @@
+O=gpurun_out
+python -c "import __graft_entry__ as g; g.build()"
+timeout 900 python -m pytest tests/test_gpu_checked.py tests/test_gpu_gram.py -x -q > $O/e10_gt.log 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q > $O/e10_gtall.log 2>&1
+echo "c2: $(python tools/batch.py 48 5 2>&1 | head -1)" >> $O/e10_batch.log
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/e10_launch.csv python tools/batch.py 6 1 > /dev/null 2>&1
