@@ -1124,14 +1124,14 @@ __global__ void __launch_bounds__(NT, 512 / NT) k1s_stats(AlignArgs a) {
 }
 
 // KS1-lean for d <= 1024 (C1, C2, C4, C5): WARP per row, no block-wide barrier per item.
-// A CTA takes a contiguous run of ONE pair's items (cta_items) of 8 rows; its 4 warps take
+// A CTA takes a contiguous run of ONE pair's items (cta_items) of kSWRows = 4 rows; its 4 warps take
 // the items in turn.  A warp streams an item's rows (lane = float4 column groups l + 32 k,
 // the next row in flight), forms the row norm with a butterfly (identical bits in every
 // lane) -> 1/||h|| (ZeroVector check), and adds x = h/||h|| into fp64 register partials of
 // its columns; each (item, side) segment is rounded to fixed point and added into the CTA's
 // int64 shared-memory column sums (exact, order-free), flushed once per CTA.  Bits depend on
 // the pair's shape only (rounding per item), not on the grid.  The per-pair ticket runs P3.
-constexpr int kSWRows = 8;
+constexpr int kSWRows = 4;
 template <int G>
 __global__ void __launch_bounds__(kS1LeanThreads, 4) k1s_stats_warp(AlignArgs a) {
     constexpr int W = kS1LeanThreads / 32;
