@@ -156,7 +156,11 @@ HAP_API const char* hap_last_error(hap_ctx ctx);
  * hi = bf16(z), lo = bf16(z - hi) (PAPER.md:258 precision note; R9), the total
  * t = 1^T Z (Eq. gemm) and the observed statistic r_x, r_y, logk_x,
  * logk_y, t_obs in fp64 (Alg. 1 step 4).
- * Constraints: 1 <= n_x, n_y; n_x + n_y <= 65535; 2 <= d <= 16384. */
+ * Constraints: 1 <= n_x, n_y; n_x + n_y <= 65535; 2 <= d <= 16384.
+ * Kernels: pairs with d % 4 == 0, d <= 4096 and 16-byte aligned X, Y take the streaming
+ * alignment (K1s: three bandwidth kernels); the others one cooperative kernel, and those
+ * cooperative launches are ordered one after the other on a device across all contexts and
+ * streams (an event chain; concurrent cooperative grids could wait on each other's SMs). */
 HAP_API hap_status hap_align(hap_ctx ctx, const float* X, int64_t n_x, const float* Y, int64_t n_y,
                      int64_t d, hap_align_mode mode, hap_align_info* info, void* stream);
 

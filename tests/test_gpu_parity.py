@@ -126,6 +126,10 @@ def test_perm_sets_side_stream_golden(hap, ctx):
 # ------------------------------------------------------------------ K1 (pooled planes)
 @pytest.mark.parametrize("n_x,n_y,d,mode", [(64, 64, 768, 0), (37, 50, 100, 0), (1000, 1000, 768, 0),
                                             (300, 200, 64, 1), (5, 3, 3, 0),
+                                            # fused cooperative K1 (d % 4 != 0), lean K1s with
+                                            # d > 1024 (block variant), warp variant at d = 1024
+                                            (40, 50, 770, 0), (300, 200, 766, 1), (100, 120, 1028, 0),
+                                            (2000, 1000, 2048, 0), (129, 3, 1024, 0),
                                             # streaming K1s path (n_pad d >= 8 Mi): R = 4 / 8
                                             # row items, an item straddling X | Y, naive mode
                                             (1024, 1024, 4096, 0), (3001, 1500, 2048, 0),
