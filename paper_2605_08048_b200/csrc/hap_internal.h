@@ -19,7 +19,10 @@ unsigned long long check_word_gram();
 
 constexpr int kKBlock = 64;     // GEMM K-block: 64 bf16 = one 128-byte swizzle atom
 constexpr int kTileM = 128;     // permutations per CTA tile (TMEM lanes)
-constexpr int kChunkN = 256;    // d-columns per accumulator chunk (UMMA N <= 256)
+#ifndef HAP_CHUNK_N
+#define HAP_CHUNK_N 256
+#endif
+constexpr int kChunkN = HAP_CHUNK_N;  // d-columns per accumulator chunk (UMMA N <= 256, % 32 == 0)
 
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 inline int64_t ceil_div(int64_t x, int64_t m) { return (x + m - 1) / m; }

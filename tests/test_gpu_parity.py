@@ -840,29 +840,30 @@ def test_config2_batch_full_size_bench_launch(ctx, orc):
             assert abs(res[p][k] - ref[k]) <= ref["flagged"], (p, k)
 
 
-def _fuzz_cases(n=14, seed=20261018):
+def _fuzz_cases(n=18, seed=20261018):
     rng = np.random.default_rng(seed)
     out = []
     for i in range(n):
         nx = int(rng.integers(2, 300))
         ny = int(rng.integers(2, 300))
-        d = int(rng.choice([2, 3, 17, 31, 64, 100, 257, 768]))
+        d = int(rng.choice([2, 3, 17, 31, 64, 100, 257, 768, 1024, 1540]))
         B = int(rng.integers(1, 1500))
         out.append((i, nx, ny, d, B, int(rng.integers(0, 2)), int(rng.choice([1, 2])),
-                    int(rng.choice([0, 97]))))
+                    int(rng.choice([0, 97])), [None, True, False][int(rng.integers(0, 3))]))
     return out
 
 
 @pytest.mark.parametrize("case", _fuzz_cases(), ids=lambda c: f"fuzz{c[0]}")
 def test_fuzz_shapes_vs_oracle(ctx, orc, case):
     """Seeded random shapes (tiny d, ragged n, odd B, both alignment modes, both K3 modes,
-    forced multi-block): full parity bars against the oracle."""
-    i, nx, ny, d, B, mode, pair_mode, block = case
+    forced multi-block, the Gram / plane / automatic K3 form): full parity bars against the
+    oracle."""
+    i, nx, ny, d, B, mode, pair_mode, block, gram = case
     X, Y = HI.make_pair(HI.PairSpec(nx, ny, d, 8.0 + d, 8.0 + d, 40.0, seed=900 + i))
-    check_pair(ctx, orc, X, Y, B, s=i, mode=mode, block=block, pair_mode=pair_mode)
+    check_pair(ctx, orc, X, Y, B, s=i, mode=mode, block=block, pair_mode=pair_mode, gram=gram)
 
 
-@pytest.mark.parametrize("seed", [1, 2, 3, 4])
+@pytest.mark.parametrize("seed", [1, 2, 3, 4, 5, 6])
 def test_fuzz_batches_vs_oracle(ctx, orc, seed):
     """Seeded random varlen batches: random pair counts and sizes, wave size, alignment
     mode and shared / independent masks, every pair against the oracle."""
@@ -880,8 +881,9 @@ def test_fuzz_batches_vs_oracle(ctx, orc, seed):
     Xp, cnx, Yp, cny = HI.varlen_batch(sx, d=d, ny_sizes=sy, seed=3000 + seed)
     B, s0 = int(rng.integers(50, 900)), int(rng.integers(0, 1000))
     wave, mode = int(rng.integers(1, 5)), int(rng.integers(0, 2))
+    gram = bool(rng.integers(0, 2))
     res = ctx.permtest_batch(_cuda(Xp), cnx, _cuda(Yp), cny, B, SEED, stream_id=s0, mode=mode,
-                             wave=wave, shared=shared)
+                             wave=wave, shared=shared, gram=gram)
     for p in range(P):
         ref = orc.run_pair(Xp[cnx[p]:cnx[p + 1]], Yp[cny[p]:cny[p + 1]], B, SEED,
                            s=s0 if shared else s0 + p, mode=mode)
