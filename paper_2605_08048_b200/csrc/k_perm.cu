@@ -194,7 +194,6 @@ __global__ void __launch_bounds__(kPW * 32) k2_perm_fy(PermArgs a, int lt_pitch)
 // compacts the chain starts of the written high positions into a per-warp list, then
 // walks the chains lane-balanced.  Same result bits as k2_perm_fy (tests).
 constexpr uint32_t kExiled32 = 0xFFFFFFFFu;
-constexpr uint32_t kChainMark = 1u << 30;  // kMark: a chain start still to walk (entries <= 2^16)
 
 // K2a (split generator): the draws only, register-resident, no shared memory, so it can
 // run beside the smem-bandwidth-bound mask-GEMM without slowing it (measured); the targets
@@ -263,11 +262,7 @@ __device__ __forceinline__ void emit_row_u32(const PermArgs& a, const PermTest& 
 // kPW warps share one permutation's table (as k2_perm_fy): the atomics of phase A and the
 // mask emit split the steps / positions; each warp compacts and walks the chains of its own
 // high positions (chains are disjoint) in its own start list.
-// kMark (large N, K2): instead of compacting the chain starts into per-warp lists,
-// phase B1 marks them in place (bit 30 of the entry) and phase B2 scans the low positions
-// for marks and walks each chain from there - no start lists, so a u32 table shared by 2-4
-// warps fits where the lists did not.
-template <int kPW, bool kMark = false>
+template <int kPW>
 __global__ void __launch_bounds__(kPW * 32) k2_perm_fy32(PermArgs a, int lt_pitch) {
     extern __shared__ __align__(16) uint8_t smem[];
     constexpr uint32_t kT = 32u * kPW;
@@ -346,56 +341,6 @@ __global__ void __launch_bounds__(kPW * 32) k2_perm_fy32(PermArgs a, int lt_pitc
             }
         }
         perm_sync<kPW>();
-        if constexpr (kMark) {
-        // ---- phase B1 (marks): for every written high position p the chain start
-        // k* = LT[p] - 1 is exiled at once when position k* was never written (the chain ends
-        // there), else marked as a chain still to walk; one select + one store per entry
-        for (uint32_t base = (nx & ~3u) + 256u * (uint32_t)w; __any_sync(0xffffffffu, base + 4u * (uint32_t)l < N);
-             base += 256u * kPW) {
-            const uint32_t pa = base + 4u * (uint32_t)l, pb = pa + 128u;
-            uint4 q0 = make_uint4(0, 0, 0, 0), q1 = q0;
-            if (pa < N) q0 = *reinterpret_cast<const uint4*>(LT + pa);
-            if (pb < N) q1 = *reinterpret_cast<const uint4*>(LT + pb);
-            uint32_t t[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
-            if (pa < nx) {  // positions below n_x only occur in the first pass (lane 0)
-#pragma unroll
-                for (int e = 0; e < 4; ++e) t[e] = pa + e >= nx ? t[e] : 0u;
-            }
-            uint32_t u[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) u[e] = t[e] ? LT[t[e] - 1u] : 0u;  // all in flight
-#pragma unroll
-            for (int e = 0; e < 8; ++e)
-                if (t[e]) LT[t[e] - 1u] = u[e] ? (u[e] | kChainMark) : kExiled32;
-        }
-        perm_sync<kPW>();
-        // ---- phase B2 (marks): each marked low position starts a chain (chain starts are
-        // never inner nodes: a step writes one position); walk it to its unwritten end, exile
-        for (uint32_t base = 256u * (uint32_t)w; __any_sync(0xffffffffu, base + 4u * (uint32_t)l < nx);
-             base += 256u * kPW) {
-            const uint32_t pa = base + 4u * (uint32_t)l, pb = pa + 128u;
-            uint4 q0 = make_uint4(0, 0, 0, 0), q1 = q0;
-            if (pa < nx) q0 = *reinterpret_cast<const uint4*>(LT + pa);
-            if (pb < nx) q1 = *reinterpret_cast<const uint4*>(LT + pb);
-            const uint32_t t[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const uint32_t pos = (e < 4 ? pa : pb) + (uint32_t)(e & 3);
-                if (pos < nx && t[e] != kExiled32 && (t[e] & kChainMark)) {
-                    uint32_t c = (t[e] & ~kChainMark) - 1u;
-                    for (;;) {
-                        const uint32_t v = LT[c];
-                        if (v == 0u) {
-                            LT[c] = kExiled32;
-                            break;
-                        }
-                        c = v - 1u;
-                    }
-                }
-            }
-        }
-        perm_sync<kPW>();
-        } else {
         // ---- phase B1: chain starts LT[p]-1 of the written high positions, 8 per lane per
         // pass.  A chain that ends at its start (position k* not written before step k*,
         // ~70 % of them) is exiled right here; the others enter the list at their second
@@ -454,7 +399,6 @@ __global__ void __launch_bounds__(kPW * 32) k2_perm_fy32(PermArgs a, int lt_pitc
             }
         }
         perm_sync<kPW>();
-        }
         // ---- phase C: exact 0/1 row (re-zeroes the table)
         if (a.out_kind == kMaskBf16Row) {
             emit_row_u32(a, T, LT, li, nx, tid, (int)kT);
@@ -594,14 +538,8 @@ cudaError_t launch_perm(const PermArgs& a, int sm_count, cudaStream_t st) {
     // HAP_K2_WIDE_MAX_N (default 2560 pooled rows)
     static const char* wmax_env = getenv("HAP_K2_WIDE_MAX_N");
     const int64_t wide_max_n = wmax_env ? atoll(wmax_env) : 2560;
-    const bool wide0 = (size_t)lt_pitch * 5u + 160u <= (200u * 1024u) / 4u && !(nar && atoi(nar)) &&
+    const bool wide = (size_t)lt_pitch * 5u + 160u <= (200u * 1024u) / 4u && !(nar && atoi(nar)) &&
                       maxN <= wide_max_n;
-    // beyond the cut-over: the u32 table with in-place chain marks shared by 2-4 warps
-    // (HAP_K2_MARK=0: the u16 table as before)
-    static const char* mk = getenv("HAP_K2_MARK");
-    const bool mark = !wide0 && !(nar && atoi(nar)) && !(mk && atoi(mk) == 0) &&
-                      (size_t)lt_pitch * 4u + 512u <= 96u * 1024u;
-    const bool wide = wide0 || mark;
     // narrow: kPW warps per permutation share its table, so latency-bound warps are not
     // limited by tables per SM (N = 5000 / 10^4 pairs: 216 -> 206 / 499 -> 408 us per test
     // with 2 / 4 warps); HAP_K2_PW = 1, 2 or 4 overrides
@@ -609,31 +547,26 @@ cudaError_t launch_perm(const PermArgs& a, int sm_count, cudaStream_t st) {
     const int pw = pw_env ? std::max(1, std::min(4, atoi(pw_env))) : maxN >= 6144 ? 4 : 2;
     static const char* wpw_env = getenv("HAP_K2_WIDE_PW");  // the same for the u32 table
     const int wpw = wpw_env ? std::max(1, std::min(4, atoi(wpw_env))) : 1;
-    const int kpw = mark ? (pw >= 4 ? 4 : pw >= 2 ? 2 : 1)
-                    : wide ? (wpw >= 4 ? 4 : wpw >= 2 ? 2 : 1) : (pw >= 4 ? 4 : pw >= 2 ? 2 : 1);
+    const int kpw = wide ? (wpw >= 4 ? 4 : wpw >= 2 ? 2 : 1) : (pw >= 4 ? 4 : pw >= 2 ? 2 : 1);
     // per CTA (one permutation at a time): u32 table + sinks + a start list per warp, or
     // u16 table + a staging row per warp
-    const size_t smem = mark ? (size_t)lt_pitch * 4u + 128u * kpw
-                        : wide ? (size_t)lt_pitch * (4u + kpw) + 160u * kpw
-                               : (size_t)(lt_pitch + 128 * kpw) * sizeof(uint16_t);
+    const size_t smem = wide ? (size_t)lt_pitch * (4u + kpw) + 160u * kpw
+                             : (size_t)(lt_pitch + 128 * kpw) * sizeof(uint16_t);
     const int nw = kpw;
-    const void* fn = mark ? (kpw == 4 ? (const void*)k2_perm_fy32<4, true>
-                             : kpw == 2 ? (const void*)k2_perm_fy32<2, true>
-                                        : (const void*)k2_perm_fy32<1, true>)
-                     : wide ? (kpw == 4 ? (const void*)k2_perm_fy32<4>
+    const void* fn = wide ? (kpw == 4 ? (const void*)k2_perm_fy32<4>
                              : kpw == 2 ? (const void*)k2_perm_fy32<2>
                                         : (const void*)k2_perm_fy32<1>)
                      : kpw == 4 ? (const void*)k2_perm_fy<4>
                      : kpw == 2 ? (const void*)k2_perm_fy<2>
                                 : (const void*)k2_perm_fy<1>;
-    const int fi = (mark ? 10 : wide ? 5 : 0) + kpw;
-    static size_t configured[15] = {};
+    const int fi = (wide ? 5 : 0) + kpw;
+    static size_t configured[10] = {};
     if (smem > 48 * 1024 && smem > configured[fi]) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         configured[fi] = smem;
     }
-    static bool carve[15] = {};
+    static bool carve[10] = {};
     if (!carve[fi]) {  // max shared carveout, so generator CTAs fit beside a mask-GEMM CTA
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
                                              cudaSharedmemCarveoutMaxShared);
@@ -648,10 +581,6 @@ cudaError_t launch_perm(const PermArgs& a, int sm_count, cudaStream_t st) {
     if (a.split == 1) {  // K2a: draws into the rows, register-only (wide path only)
         const int64_t g2 = std::min<int64_t>(ceil_div(items, 4), (int64_t)sm_count * 4);
         k2_draws<<<(int)g2, 128, 0, st>>>(a);
-    } else if (mark) {
-        if (kpw == 4) k2_perm_fy32<4, true><<<grid, 128, smem, st>>>(a, lt_pitch);
-        else if (kpw == 2) k2_perm_fy32<2, true><<<grid, 64, smem, st>>>(a, lt_pitch);
-        else k2_perm_fy32<1, true><<<grid, 32, smem, st>>>(a, lt_pitch);
     } else if (wide) {
         if (kpw == 4) k2_perm_fy32<4><<<grid, 128, smem, st>>>(a, lt_pitch);
         else if (kpw == 2) k2_perm_fy32<2><<<grid, 64, smem, st>>>(a, lt_pitch);
