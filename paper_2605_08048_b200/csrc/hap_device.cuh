@@ -55,6 +55,12 @@ static __device__ unsigned long long g_hap_check = 0ull;
     unsigned long long fn() { return 0ull; }
 #endif
 
+// programmatic dependent launch: a kernel launched with programmatic stream serialization
+// may start while its predecessor finishes; griddepcontrol.wait blocks until the predecessor
+// grid has completed and its memory is visible (a no-op without the launch attribute)
+HAP_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+HAP_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 HAP_DEV uint32_t lane_id() { return threadIdx.x & 31u; }
 HAP_DEV uint32_t warp_id() { return __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0); }
 HAP_DEV bool elect_one() {

@@ -31,6 +31,7 @@
 #include <mutex>
 #include <cstdlib>
 #include <algorithm>
+#include <utility>
 
 #define HAP_CHECK_TU 1
 #include "hap_device.cuh"
@@ -1119,6 +1120,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k1s_stats(AlignArgs a) {
             }
         }
     }
+    pdl_trigger();  // the coefficient pass may launch (it waits for this grid to complete)
     if (i0 < i1) pair_done();  // (a CTA without items takes part in no ticket)
     if (tid == 0) span_exit(a.span);
 }
@@ -1218,6 +1220,7 @@ __global__ void __launch_bounds__(kS1LeanThreads, 4) k1s_stats_warp(AlignArgs a)
         }
         flush();
     }
+    pdl_trigger();
     __syncthreads();
     for (int c = tid; c < 2 * d; c += kS1LeanThreads) {
         const long long v = sw_acc[c];
@@ -1235,6 +1238,7 @@ __global__ void __launch_bounds__(kS1LeanThreads, 4) k1s_stats_warp(AlignArgs a)
 // lane, so an SM has ~30 rows streaming at once.
 __global__ void __launch_bounds__(256) k1s_coef(AlignArgs a, int ctas_per_pair0, int ctas_per_pair1,
                                                 int ctas_per_pair2, int ctas_per_pair3) {
+    pdl_wait();  // KS1 (P3: u, inv) complete and visible
     extern __shared__ __align__(16) uint8_t kc_smem[];
     double* su = reinterpret_cast<double*>(kc_smem);  // [d_pad]
     const int cpp[4] = {ctas_per_pair0, ctas_per_pair1, ctas_per_pair2, ctas_per_pair3};
@@ -1282,6 +1286,7 @@ __global__ void __launch_bounds__(256) k1s_coef(AlignArgs a, int ctas_per_pair0,
             }
         }
     }
+    pdl_trigger();
     __syncthreads();
     if (threadIdx.x == 0) span_exit(a.span);
 }
@@ -1321,6 +1326,7 @@ struct XfPair {
 
 __global__ void __launch_bounds__(kThreads, 1) k1s_xform(AlignArgs a, int64_t tile_off1, int64_t tile_off2,
                                                          int64_t tile_off3, int64_t tiles_total) {
+    pdl_wait();  // KS2 (coefficients) complete and visible
     extern __shared__ __align__(16) uint8_t xf_smem[];
     float* raw = reinterpret_cast<float*>(xf_smem);  // [kXfStages][128][64]
     float2* rcoef = reinterpret_cast<float2*>(raw + kXfStages * kXfRows * kXfCols);  // [kXfStages][128]
@@ -1536,6 +1542,7 @@ constexpr int kXlTW = kXlRows / 2 + 1;  // u32 words per staging column (33: con
 
 __global__ void __launch_bounds__(kXlThreads, 4) k1s_xform_lean(AlignArgs a, int64_t tile_off1, int64_t tile_off2,
                                                                int64_t tile_off3, int64_t tiles_total) {
+    pdl_wait();  // KS2 (coefficients) complete and visible
     __shared__ uint32_t sh_hi[kXfCols * kXlTW];
     __shared__ uint32_t sh_lo[kXfCols * kXlTW];
     __shared__ double red[2 * (kXlThreads / 32) + 2];
@@ -1751,6 +1758,26 @@ int align_launch_count(const AlignArgs& a) { return align_uses_stream(a) ? 3 : 1
 
 static cudaError_t launch_align_ks23(AlignArgs a, int sm_count, cudaStream_t st, bool lean);
 
+// launch with programmatic stream serialization: the kernel may start while the previous
+// kernel on `st` finishes (its griddepcontrol.wait orders the reads); HAP_PDL=0 turns it off
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*fn)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+    static const char* env = getenv("HAP_PDL");
+    static const bool on = !(env && atoi(env) == 0);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = on ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, fn, std::forward<Args>(args)...);
+}
+
 static cudaError_t launch_align_stream(AlignArgs a, int sm_count, cudaStream_t st) {
     const int d = (int)a.d;
     // every pair of a launch takes the same variant (the callers form waves so)
@@ -1821,8 +1848,7 @@ static cudaError_t launch_align_ks23(AlignArgs a, int sm_count, cudaStream_t st,
             total += cpp[g];
         }
         const size_t smem2 = (size_t)a.d_pad * 8;
-        k1s_coef<<<total, 256, smem2, st>>>(a, cpp[0], cpp[1], cpp[2], cpp[3]);
-        e = cudaGetLastError();
+        e = launch_pdl(k1s_coef, dim3(total), dim3(256), smem2, st, a, cpp[0], cpp[1], cpp[2], cpp[3]);
         if (e != cudaSuccess) return e;
     }
     if (lean) {  // KS3-lean: 64-row tiles, two CTAs per SM at most
@@ -1839,8 +1865,7 @@ static cudaError_t launch_align_ks23(AlignArgs a, int sm_count, cudaStream_t st,
             if (e != cudaSuccess) return e;
             xl_configured = true;
         }
-        k1s_xform_lean<<<grid, kXlThreads, 0, st>>>(a, off[1], off[2], off[3], total);
-        return cudaGetLastError();
+        return launch_pdl(k1s_xform_lean, dim3(grid), dim3(kXlThreads), 0, st, a, off[1], off[2], off[3], total);
     }
     {  // KS3
         const int64_t strips = ceil_div(a.d_pad, kXfCols);
@@ -1857,8 +1882,7 @@ static cudaError_t launch_align_ks23(AlignArgs a, int sm_count, cudaStream_t st,
             if (e != cudaSuccess) return e;
             xf_configured = true;
         }
-        k1s_xform<<<grid, kThreads, kXfSmem, st>>>(a, off[1], off[2], off[3], total);
-        e = cudaGetLastError();
+        e = launch_pdl(k1s_xform, dim3(grid), dim3(kThreads), kXfSmem, st, a, off[1], off[2], off[3], total);
     }
     return e;
 }
