@@ -654,8 +654,10 @@ def run_batch_workload(args, E, peaks, name):
             step(10 * K + i, sel=big[3 * i: 3 * i + 3])
             torch.cuda.synchronize()
     nb = int(sizes[big[0]])
-    roof = kernel_profile(E, waves, 6, 2 * nb, 768, B, peaks,
-                          f"isolated waves of the 3 largest pairs (n~{nb}) of the batch")
+    # (step() runs every mode, so the two isolated calls hold 6 tests per mode)
+    roof = kernel_profile(E, waves, 6 * nm, 2 * nb, 768, B, peaks,
+                          f"isolated waves of the 3 largest pairs (n~{nb}) of the batch, "
+                          f"{nm} mode(s)")
     # e2e on a bounded slice from pinned host memory (whole batch would pin tens of GB)
     Pe = min(P, 1000 if name == "c4" else P)
     ne = int(cnx[Pe])
