@@ -95,22 +95,28 @@ __device__ __forceinline__ double kappa_hat(double r, double d) {
 // fp64) in fp32 - its error, ~1e-7 of T's natural scale, is far below the tie band, and it
 // keeps the finalize off the fp64 pipe, which the running MMAs slow down; a ratio far from
 // 1 (|T| > 0.4) takes the fp64 log (fp32 would round q2/q1 - 1 to -1 once |T| > 16)
+// the rare far-from-1 ratio: an out-of-line fp64 log, so the common path does not evaluate
+// it under a predicate
+__device__ __noinline__ double log_far(double q1, double q2) { return log(q2 / q1); }
 __device__ __forceinline__ double log_ratio(double q1, double q2) {
     if (q1 == 0.0) return q2 == 0.0 ? 0.0 : INFINITY;  // r1 = 0: T = +inf; both 0: T := 0 (R4)
     const double x = (q2 - q1) / q1;
-    return fabs(x) < 0.5 ? (double)log1pf((float)x) : log(q2 / q1);
+    if (fabs(x) < 0.5) return (double)log1pf((float)x);
+    return log_far(q1, q2);
 }
 
 // Half-width of the interval that holds L(r) of the exact statistic, given the GPU's
-// estimate r and its error bound delta (R14).  First order 2 delta |L'(r)| (twice
-// the linear term, L' = 1/r + 2r/(1 - r^2) - 2r/(d - r^2) <= 1/r + 2r/(1 - r^2)); near the
-// clamp the exact interval up to L(1 - 1e-9); groups of one are exact (delta = 0).
-__device__ __forceinline__ double l_width(double r, double delta, double d) {
-    if (delta == 0.0) return 0.0;
-    if (r <= 2.0 * delta) return INFINITY;
-    if (r + 2.0 * delta >= 1.0 - 1e-9)
-        return log(kappa_hat(1.0, d) / kappa_hat(r - 2.0 * delta, d));
-    return 2.0 * delta * (1.0 / r + 2.0 * r / (1.0 - r * r));
+// estimate r and its error bound delta (R14): 2 delta |L'(r)| (twice the linear
+// term, L' = 1/r + 2r/(1 - r^2) - 2r/(d - r^2) <= 1/r + 2r/(1 - r^2)), formed in fp32 with a
+// 1 % allowance; unbounded (every decision flagged) when the interval reaches r = 0 or the
+// clamp at 1 - 1e-9; groups of one are exact (delta = 0).  Branch-free: the finalize runs
+// beside the MMAs, and a data-dependent branch to an exact near-clamp interval cost ~6 % of
+// the mask-GEMM (profiles/r02_experiments/e31_eb.log).
+__device__ __forceinline__ double l_width(double r, float delta) {
+    const float rf = (float)r;
+    const float w = 2.02f * delta * (__frcp_rn(rf) + 2.f * rf * __frcp_rn(1.f - rf * rf));
+    const bool unbounded = r <= 2.0 * (double)delta || r + 2.0 * (double)delta >= 1.0 - 1e-9;
+    return delta == 0.f ? 0.0 : (unbounded ? (double)INFINITY : (double)w);
 }
 
 // Gram form (k_gram.cu): error of r from the form's own roundings, on top of the planes'
@@ -119,9 +125,9 @@ __device__ __forceinline__ double l_width(double r, double delta, double d) {
 // sum of squares, entries <= |z'|^2 <= 4, off-diagonal ones ~ 1/sqrt(d) of that) and the
 // fp32 accumulation of each U_bj over n terms (2^-24 per add); 8x margin as in R14;
 // dr = dS / (2 n^2 r).
-__device__ __forceinline__ double gram_delta(double n, double d, double r) {
-    const double dS = 8.0 * 4.0 * sqrt(1.0 + n / d) * (0x1p-17 * sqrt(n) + 0x1p-22 * n);
-    return dS / (2.0 * n * n * fmax(r, 1e-6));
+__device__ __forceinline__ float gram_delta(float n, float d, double r) {
+    const float dS = 8.f * 4.f * sqrtf(1.f + n / d) * (0x1p-17f * sqrtf(n) + 0x1p-22f * n);
+    return 1.01f * dS / (2.f * n * n * fmaxf((float)r, 1e-6f));
 }
 
 // statistic of a tile row from its accumulated sums S1 = |sigma1|^2, S2 = |sigma2|^2;
@@ -137,13 +143,13 @@ __device__ __forceinline__ RowStat row_stat(const GemmArgs& g, const GemmTest& T
     s.T = log_ratio(kappa_hat(s.r1, d), kappa_hat(s.r2, d));
     // |r_gpu - r| <= 8 eps / sqrt(n d) per group (R14: the row errors average over the n
     // rows and the d coordinates; measured <= 1/4 of this bound at every tested shape)
-    const double k = 8.0 * eps * rsqrt(d);
-    double d1 = k * rsqrt((double)T.n_x), d2 = k * rsqrt((double)T.n_y);
+    const float k = 1.01f * 8.f * (float)eps * rsqrtf((float)d);
+    float d1 = k * rsqrtf((float)T.n_x), d2 = k * rsqrtf((float)T.n_y);
     if (T.gram) {  // + the Gram form's own rounding
-        d1 += gram_delta((double)T.n_x, d, s.r1);
-        d2 += gram_delta((double)T.n_y, d, s.r2);
+        d1 += gram_delta((float)T.n_x, (float)d, s.r1);
+        d2 += gram_delta((float)T.n_y, (float)d, s.r2);
     }
-    s.e = l_width(s.r1, T.n_x == 1 ? 0.0 : d1, d) + l_width(s.r2, T.n_y == 1 ? 0.0 : d2, d);
+    s.e = l_width(s.r1, T.n_x == 1 ? 0.f : d1) + l_width(s.r2, T.n_y == 1 ? 0.f : d2);
     return s;
 }
 
