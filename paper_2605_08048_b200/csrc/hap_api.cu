@@ -89,7 +89,7 @@ namespace {
 enum Buf {
     kX = 0, kY, kNrm, kCoef, kPart, kXbar, kYbar, kU, kZhi, kZlo, kTpart, kT64, kAB, kMask,
     kM, kSconst, kGemmPart, kTileDone, kScal, kSpart, kScratch, kMask1, kInv, kStamps, kK3Stamps,
-    kSched, kSpans, kX2, kY2, kClaim, kGhi, kGlo, kGab, kMbits, kMbits1, kGacc, kNumBufs
+    kSched, kSpans, kX2, kY2, kClaim, kGhi, kGlo, kGab, kMbits, kMbits1, kGacc, kFinQ, kNumBufs
 };
 
 hap_status fail(hap_ctx c, hap_status s, const std::string& msg) {
@@ -971,8 +971,10 @@ hap_status plan_wave(hap_ctx owner, int G, const WaveTest* T, int pair, bool sha
         if (g.dyn && g.npieces < P.npairs) P.npairs = g.npairs = std::max(1, g.npieces);
     }
     if ((s = ensure(owner, kGemmPart, (size_t)tiles * part_slots(owner, max_cols) * R * sizeof(float2))) ||
-        (s = ensure(owner, kTileDone, (size_t)tiles * sizeof(unsigned))))
+        (s = ensure(owner, kTileDone, (size_t)tiles * sizeof(unsigned))) ||
+        (s = ensure(owner, kFinQ, (size_t)(4 + tiles) * sizeof(int))))
         return s;
+    g.fq = B<int>(owner, kFinQ);
     g.part = B<float2>(owner, kGemmPart);
     g.tile_done = B<unsigned>(owner, kTileDone);
     return HAP_OK;

@@ -154,6 +154,7 @@ struct GemmArgs {
     int dyn;                 // 1: CTA pairs claim pieces from a global counter (dynamic)
     int npieces;             // pieces in the launch (dynamic mode: every kChunkN chunk)
     int* claim;              // [2] claim / exit counters (zero between launches)
+    int* fq;                 // [4 + ntiles] finalize queue (zero between launches)
     int exp;                 // timing experiments only (HAP_K3_EXPERIMENT), 0 in production
     long long* stamps;       // exp bit 16: [grid][8 units][8 events] globaltimer
     unsigned long long* span;  // optional {first CTA entry, last CTA exit} globaltimer

@@ -41,7 +41,6 @@ namespace {
 constexpr int kThreads = 192;
 constexpr uint32_t kTmemCols = 512;
 constexpr int kStageA = kTileM * 128;  // 16 KB: 128 rows x 64 bf16
-constexpr int kFinCap = 400;             // deferred finalizes per CTA (smem tail list)
 constexpr int kQ = 6;                    // piece queue: the leader's producer publishes the
                                          // pair's pieces to every role of both CTAs
 
@@ -239,6 +238,14 @@ __device__ void finalize_tile(const GemmArgs& g, const GemmTest& T, int tile, in
 #undef FIN_STAMP
 }
 
+// finalize queue (GemmArgs::fq): [0] pop counter, [1] push counter, [2] exit counter,
+// [4 + k] the k-th published entry: tile + 1, or -(tile + 1) for a failed test's tile
+__device__ __forceinline__ void fq_push(const GemmArgs& g, int v) {
+    __threadfence();  // the tile's partials (all pieces, fenced before their tickets) first
+    const int pos = atomicAdd(g.fq + 1, 1);
+    atomicExch(g.fq + 4 + pos, v);
+}
+
 // test of a wave tile (the tests' tiles are contiguous, in test order)
 __device__ __forceinline__ int test_of(const GemmArgs& g, int tile) {
     int ti = 0;
@@ -271,8 +278,6 @@ __global__ void __maxnreg__(HAP_K3_MAXNREG)
     int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
     unsigned* s_cnt = tmem_slot + 4;  // [3] per-tile counts of the finalize
     double* s_tc = reinterpret_cast<double*>(tmem_slot + 8);  // [kMaxWave][4] S1c, S2c, tau, eps
-    int* s_nfin = reinterpret_cast<int*>(s_tc + 4 * kMaxWave);  // tiles this CTA finalizes
-    int* s_fin = s_nfin + 1;                                    // [kFinCap] deferred tiles
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) K3_STAMP(7, 0);  // kernel entry
@@ -320,7 +325,6 @@ __global__ void __maxnreg__(HAP_K3_MAXNREG)
             tma_prefetch_desc(&maps.blo[ti]);
         }
     }
-    if (threadIdx.x == 64 + kMaxWave) *s_nfin = 0;
     if (threadIdx.x >= 64 && threadIdx.x < 64 + g.G) {  // finalize constants per test
         const GemmTest& T = g.t[threadIdx.x - 64];
         s_tc[4 * (threadIdx.x - 64) + 0] = T.sconst[0];
@@ -492,7 +496,19 @@ __global__ void __maxnreg__(HAP_K3_MAXNREG)
             const int tile = pd.x, width = pd.z;
             const int ti = test_of(g, tile);
             const GemmTest& T = g.t[ti];
-            if (test_failed(T)) continue;
+            if (test_failed(T)) {
+                // no MMA ran for it; the tile still takes part in the finalize queue (as a
+                // skip entry) so that every queue position is filled exactly once
+                named_bar_sync(1, 128);
+                if (etid == 0) {
+                    const unsigned old = atomicAdd(g.tile_done + tile, 1u);
+                    if (old == (unsigned)(kPair * g.tile_npieces[tile] - 1)) {
+                        g.tile_done[tile] = 0;
+                        fq_push(g, -(tile + 1));
+                    }
+                }
+                continue;
+            }
             const int np_tile = g.tile_npieces[tile];
             HAP_CHECK(np_tile >= 1 && np_tile <= g.max_slots && trow < R);
             HAP_CHECK(!T.gram || (T.mbits != nullptr &&
@@ -575,45 +591,59 @@ __global__ void __maxnreg__(HAP_K3_MAXNREG)
                 *s_last = (old == (unsigned)(kPair * np_tile - 1)) ? 1 : 0;
             }
             named_bar_sync(1, 128);
-            // The last arriving CTA finalizes the tile - but only after its last piece: in
-            // the middle of the kernel the partial loads queue behind the operand streams
-            // (measured 12-16 us instead of ~1 us), which would hold the epilogue and with
-            // it the release of the accumulator buffer.
-#ifndef HAP_K3_INLINE_FIN
-#define HAP_K3_INLINE_FIN 0
-#endif
-            if (*s_last && !HAP_K3_INLINE_FIN && *s_nfin < kFinCap) {  // defer (the list is full only for
-                if (etid == 0) s_fin[*s_nfin] = tile;  // pairs with hundreds of pieces)
-                named_bar_sync(1, 128);
-                if (etid == 0) ++*s_nfin;
-            } else if (*s_last) {
-                __threadfence();
-                finalize_tile(g, T, tile, tile - T.tile0, np_tile, etid, s_cnt, s_tc[4 * ti],
-                              s_tc[4 * ti + 1], s_tc[4 * ti + 2], s_tc[4 * ti + 3]);
-            }
+            // The last arriving CTA publishes the tile in the launch's finalize queue; the
+            // finalizes run after the CTAs' pieces (mid-kernel the partial loads queue behind
+            // the operand streams: 12-16 us instead of ~1 us), taken from the queue by
+            // whichever CTAs are done, so the tail is shared by all of them instead of each
+            // CTA finalizing the tiles it happened to complete (up to ~3 x 5 us).
+            if (*s_last && etid == 0) fq_push(g, tile + 1);
             named_bar_sync(1, 128);
             ++i;
         }
-        for (int f = 0; f < *s_nfin; ++f) {
-            const int tile = s_fin[f];
+        for (int f = 0;; ++f) {
+            if (etid == 0) {
+                const int pos = atomicAdd(g.fq, 1);
+                int v = 0;
+                if (pos < g.ntiles) {
+                    volatile int* slot = g.fq + 4 + pos;
+                    for (uint32_t spins = 0; (v = *slot) == 0; ++spins) {
+                        __nanosleep(64);
+                        if (spins > (1u << 27)) __trap();  // never wait forever
+                    }
+                    *slot = 0;  // ready for the next launch
+                    __threadfence();
+                }
+                *s_last = v;  // 0: queue drained
+            }
+            named_bar_sync(1, 128);
+            const int v = *s_last;
+            named_bar_sync(1, 128);
+            if (v == 0) break;
+            if (v < 0) continue;  // a failed test's tile: nothing to count
+            const int tile = v - 1;
             const int ti = test_of(g, tile);
             const GemmTest& T = g.t[ti];
             __threadfence();
-            if (etid == 0) K3_STAMP(f, 6);
+            if (etid == 0) K3_STAMP(f & 7, 6);
             finalize_tile(g, T, tile, tile - T.tile0, g.tile_npieces[tile], etid, s_cnt, s_tc[4 * ti],
                           s_tc[4 * ti + 1], s_tc[4 * ti + 2], s_tc[4 * ti + 3], f);
-            if (etid == 0) K3_STAMP(f, 7);
+            if (etid == 0) K3_STAMP(f & 7, 7);
             named_bar_sync(1, 128);
         }
     }
     tc_fence_before();
     __syncthreads();
     if constexpr (kPair == 2) cluster_sync();
-    if (g.dyn && threadIdx.x == 0) {  // the last CTA out resets the claim counters
+    if (threadIdx.x == 0) {  // the last CTA out resets the claim and finalize-queue counters
         __threadfence();
-        if (atomicAdd(g.claim + 1, 1) == (int)gridDim.x - 1) {
-            g.claim[0] = 0;
-            g.claim[1] = 0;
+        if (atomicAdd(g.fq + 2, 1) == (int)gridDim.x - 1) {
+            if (g.dyn) {
+                g.claim[0] = 0;
+                g.claim[1] = 0;
+            }
+            g.fq[0] = 0;
+            g.fq[1] = 0;
+            g.fq[2] = 0;
         }
     }
     if (threadIdx.x == 0) K3_STAMP(7, 1);  // all roles done
