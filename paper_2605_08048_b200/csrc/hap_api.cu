@@ -820,7 +820,7 @@ hap_status align_wave(hap_ctx owner, int G, hap_ctx* ws, const AlignPair* pairs,
     a.mode = mode;
     a.scratch = B<long long>(owner, kScratch);
     a.stamps = nullptr;
-    if (owner->stamp_k1 && ensure(owner, kStamps, (size_t)(8 + 8 * owner->sm_count) * 8) == HAP_OK)
+    if (owner->stamp_k1 && ensure(owner, kStamps, (size_t)(8 + 8 * 4 * owner->sm_count) * 8) == HAP_OK)
         a.stamps = B<long long>(owner, kStamps);
     align_items(a);
     a.span = next_span(owner, HAP_PHASE_ALIGN);
@@ -1433,7 +1433,7 @@ hap_status hap_debug_k1_stamps(hap_ctx c, long long* out, int64_t n) {
     if (c && !c->buf[kStamps] && c->sub[0][0]) c = c->sub[0][0];  // a batch: lane 0's owner
     if (!c || !out || !c->buf[kStamps]) return HAP_E_INVALID_ARG;
     cudaDeviceSynchronize();
-    const size_t bytes = std::min<size_t>((size_t)n * 8, (size_t)(8 + 8 * c->sm_count) * 8);
+    const size_t bytes = std::min<size_t>((size_t)n * 8, c->cap[kStamps]);
     if (cudaMemcpy(out, c->buf[kStamps], bytes, cudaMemcpyDeviceToHost) != cudaSuccess)
         return HAP_E_CUDA;
     return HAP_OK;

@@ -129,6 +129,13 @@ __device__ __forceinline__ void cstamp(const AlignArgs& a, int k) {
     }
 }
 
+// development build only: KS1 per-CTA phase stamps (stamps[8 + 8 cta + k], grid <= 4 SMs)
+#ifdef HAP_EXPERIMENTS
+#define KS1_STAMP(k) cstamp(a, k)
+#else
+#define KS1_STAMP(k) do { } while (0)
+#endif
+
 // Software grid barrier (all CTAs are co-resident: cooperative launch): one release-add
 // per CTA on a counter that only grows within a launch, then acquire-polling until every
 // CTA has arrived.  The counter is cleared for the next launch by the last CTA of P5 (all
@@ -318,10 +325,10 @@ __device__ void finish_pairs(const AlignArgs& a, double* red) {
     }
 }
 
-// Per-pair completion tickets of the streaming kernels (K1s): the CTA that completes a
-// pair's last work unit runs that pair's scalar pass, so the pairs of a wave finish in
-// parallel on different CTAs instead of in series on the launch's last one.  Word 4 (KS1
-// items) / 5 (KS3 tiles) of the pair's own scratch; reset by the finishing CTA.
+// Per-pair completion tickets of the streaming kernels: the CTA that completes a pair's last
+// work unit runs that pair's scalar pass, so the pairs of a wave finish in parallel on
+// different CTAs instead of in series on the launch's last one.  Word 4 (warp-per-row KS1
+// items: P3) / 5 (KS3 tiles: P5) of the pair's own scratch; reset by the finishing CTA.
 __device__ __forceinline__ bool pair_ticket(const AlignPair& q, int word, unsigned units, unsigned total, int* s_flag) {
     __threadfence();
     __syncthreads();
@@ -745,81 +752,12 @@ __device__ __forceinline__ void mbar_arrive_expect_tx_relaxed(uint64_t* bar, uin
                  : "memory");
 }
 
-// P3 of one pair from its (complete) accumulators, written to global memory: xbar, ybar,
-// axis u, centre m, info (the arithmetic of the fused kernel's pair_scalars, writer case)
-template <int NT>
-__device__ void stream_pair_scalars(const AlignArgs& a, int g, double* red) {
-    const AlignPair& q = a.p[g];
-    const int tid = threadIdx.x;
-    const int d = (int)a.d;
-    const long long* acc_x = q.acc;
-    const long long* acc_y = q.acc + d;
-    const int64_t N = q.n_x + q.n_y;
-    const double rnX = 1.0 / (double)q.n_x, rnY = 1.0 / (double)q.n_y;
-    double sxx = 0.0, syy = 0.0;
-    for (int c = tid; c < d; c += NT) {
-        const double xb = fix_get(acc_x + c) * rnX, yb = fix_get(acc_y + c) * rnY;
-        q.xbar[c] = xb;
-        q.ybar[c] = yb;
-        sxx += xb * xb;
-        syy += yb * yb;
-    }
-    const double2 sq = block_sum2_n<NT>(sxx, syy, red);
-    const double nx = sqrt(sq.x), ny = sqrt(sq.y);
-    const bool degenerate = nx < 1e-12 || ny < 1e-12;
-    const double rnx = degenerate ? 0.0 : 1.0 / nx;
-    const double rny = degenerate ? 0.0 : 1.0 / ny;
-    double sv = 0.0, svx = 0.0;
-    for (int c = tid; c < d; c += NT) {
-        const double xb = fix_get(acc_x + c) * rnX, yb = fix_get(acc_y + c) * rnY;
-        const double v = xb * rnx - yb * rny;
-        sv += v * v;
-        svx += v * xb;
-    }
-    const double2 vv = block_sum2_n<NT>(sv, svx, red);
-    const double nv0 = sqrt(vv.x);
-    const bool identity = (a.mode == HAP_ALIGN_NONE) || degenerate || nv0 < 1e-9;  // R3
-    const double rnv = identity ? 0.0 : 1.0 / nv0;
-    const double ux = vv.y * rnv;
-    const double rN = 4096.0 / (double)N;
-    for (int c = tid; c < (int)a.d_pad; c += NT) {
-        double ud = 0.0, md = 0.0;
-        if (c < d) {
-            const double xb = fix_get(acc_x + c) * rnX, yb = fix_get(acc_y + c) * rnY;
-            ud = (xb * rnx - yb * rny) * rnv;
-            const double t = (double)q.n_x * (xb - 2.0 * ud * ux) + (double)q.n_y * yb;
-            md = rint(t * rN) * (1.0 / 4096.0);
-        }
-        q.u[c] = ud;
-        q.m[c] = md;
-    }
-    if (tid == 0) {
-        hap_align_info* f = q.info;
-        const long long bad = *reinterpret_cast<volatile long long*>(q.bad);
-        f->n_x = q.n_x;
-        f->n_y = q.n_y;
-        f->d = a.d;
-        f->n_pad = q.n_pad;
-        f->d_pad = a.d_pad;
-        f->is_identity = identity ? 1 : 0;
-        f->status = bad < N ? HAP_E_ZERO_VECTOR : (degenerate ? HAP_E_DEGENERATE_MEAN : HAP_OK);
-        f->bad_row = bad < N ? bad : -1;
-        f->r_x = nx;  // r(X') = ||xbar||
-        f->r_y = ny;
-        const double lx = logkappa64(nx, (double)a.d), ly = logkappa64(ny, (double)a.d);
-        f->logk_x = lx;
-        f->logk_y = ly;
-        f->t_obs = (isinf(lx) && isinf(ly)) ? 0.0 : ly - lx;  // Eq. 10
-        const double qnan = __longlong_as_double(0x7ff8000000000000ll);
-        f->gemm_r_x = f->gemm_r_y = f->gemm_t_obs = qnan;
-    }
-    __syncthreads();
-}
-
-// P3 with every column's accumulators loaded ONCE into registers (kC >= d / NT columns per
-// thread, all loads in flight together): one L2 round trip instead of three passes of
-// dependent loads (the warp-per-row KS1 calls it after its main loop, when registers are
-// free).  Same arithmetic and per-thread order as stream_pair_scalars.
+// P3 of one pair from its (complete) accumulators, written to global memory (xbar, ybar, axis
+// u, centre m, info), with every column's accumulators loaded ONCE into registers (kC >= d /
+// NT columns per thread, all loads in flight together: one L2 round trip).  The warp-per-row
+// KS1 (d <= 1024) runs it on the CTA that completes the pair's last item (per-pair ticket,
+// word 4 of the pair's scratch), after its main loop, when registers are free; for d > 1024
+// every KS2 CTA derives P3 itself (k1s_coef<true>) instead of one CTA holding up the pass.
 template <int NT, int kC>
 __device__ void stream_pair_scalars_cached(const AlignArgs& a, int g, double* red) {
     const AlignPair& q = a.p[g];
@@ -929,16 +867,14 @@ __global__ void __launch_bounds__(NT, 512 / NT) k1s_stats(AlignArgs a) {
     extern __shared__ __align__(128) uint8_t ks_smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(ks_smem);
     float* ring = reinterpret_cast<float*>(ks_smem + 128);
-    __shared__ double red[2 * W + 2];
-    __shared__ double s_part[W][R];
-    __shared__ double s_inv[R];
-    __shared__ int s_last;
+    __shared__ double s_part[2][W][R];  // by item parity: one barrier per item
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int d = (int)a.d;
     const int d4 = d >> 2;
     const int64_t items = a.item_off[a.G];
     const int64_t i0 = items * blockIdx.x / gridDim.x, i1 = items * (blockIdx.x + 1) / gridDim.x;
     const size_t stage_floats = (size_t)R * d;
+    KS1_STAMP(0);
     if (tid == 0) {
         span_enter(a.span);
         if constexpr (kRing) {
@@ -998,24 +934,12 @@ __global__ void __launch_bounds__(NT, 512 / NT) k1s_stats(AlignArgs a) {
             }
         }
     };
-    // a pair's P3 runs on the CTA that completes its last item (per-pair ticket)
-    int pg = i0 < i1 ? pair_of(a, i0) : 0;
-    unsigned pcnt = 0;
-    auto pair_done = [&]() {
-        flush();
-        const unsigned total = (unsigned)(a.item_off[pg + 1] - a.item_off[pg]);
-        if (pair_ticket(a.p[pg], 4, pcnt, total, &s_last)) stream_pair_scalars<NT>(a, pg, red);
-        pcnt = 0;
-    };
+    // (the pairs' scalars P3 are derived by every KS2 CTA from the complete column sums, so
+    // no CTA here waits for the others: a CTA issues its last atomics and exits)
     for (int64_t item = i0; item < i1; ++item) {
         const int64_t k = item - i0;
         const int st = (int)(k % kSStages);
         const int g = pair_of(a, item);
-        if (g != pg) {
-            pair_done();
-            pg = g;
-        }
-        ++pcnt;
         const AlignPair& q = a.p[g];
         const int64_t N = q.n_x + q.n_y;
         const int64_t r0 = (item - a.item_off[g]) * R;
@@ -1025,6 +949,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k1s_stats(AlignArgs a) {
         if constexpr (kRing) {
             const float4* tile = reinterpret_cast<const float4*>(ring + st * stage_floats);
             mbar_wait(&full[st], (uint32_t)((k / kSStages) & 1));
+            if (k == 0) KS1_STAMP(1);
 #pragma unroll
             for (int r = 0; r < R; ++r)
 #pragma unroll
@@ -1037,8 +962,6 @@ __global__ void __launch_bounds__(NT, 512 / NT) k1s_stats(AlignArgs a) {
                     v[r][kk][2] = (double)f.z;
                     v[r][kk][3] = (double)f.w;
                 }
-            __syncthreads();  // the stage is in registers: refill it
-            if (tid == 0 && item + kSStages < i1) issue(item + kSStages, st);
         } else {
 #pragma unroll
             for (int r = 0; r < R; ++r)
@@ -1051,7 +974,13 @@ __global__ void __launch_bounds__(NT, 512 / NT) k1s_stats(AlignArgs a) {
                 }
             if (item + 1 < i1) load_regs(item + 1, nxt);  // in flight during this item
         }
-        // row norms: per-thread partial squares, warp tree, then the warps in order
+        // row norms: per-thread partial squares, warp tree, then the warps in order.  ONE
+        // barrier per item: it also frees the ring stage (every thread holds the item in
+        // registers), and every warp forms the rows' 1/||h|| itself (lane r: row r, the same
+        // fixed-order sum in every warp), so no second barrier hands them out; s_part is
+        // double-buffered by item parity (a warp reaches item k + 2 only after every warp
+        // has passed item k + 1's barrier, i.e. finished reading item k's partials).
+        double (*sp)[R] = s_part[k & 1];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             double sq0 = 0.0, sq1 = 0.0;
@@ -1061,23 +990,26 @@ __global__ void __launch_bounds__(NT, 512 / NT) k1s_stats(AlignArgs a) {
                 sq1 += v[r][kk][2] * v[r][kk][2] + v[r][kk][3] * v[r][kk][3];
             }
             const double sq = warp_sum(sq0 + sq1);
-            if (lane == 0) s_part[warp][r] = sq;
+            if (lane == 0) sp[warp][r] = sq;
         }
         __syncthreads();
-        if (tid < nr) {
+        if constexpr (kRing)
+            if (tid == 0 && item + kSStages < i1) issue(item + kSStages, st);
+        double my_iv = 0.0;
+        if (lane < nr) {
             double ss = 0.0;
 #pragma unroll
-            for (int w = 0; w < W; ++w) ss += s_part[w][tid];
+            for (int w = 0; w < W; ++w) ss += sp[w][lane];
             const double nrm = sqrt(ss);
-            const double iv = nrm >= 1e-12 ? 1.0 / nrm : 0.0;
-            s_inv[tid] = iv;
-            q.inv[r0 + tid] = iv;
-            if (nrm < 1e-12) atomicMin(q.bad, (long long)(r0 + tid));
+            my_iv = nrm >= 1e-12 ? 1.0 / nrm : 0.0;
+            if (warp == 0) {
+                q.inv[r0 + lane] = my_iv;
+                if (nrm < 1e-12) atomicMin(q.bad, (long long)(r0 + lane));
+            }
         }
-        __syncthreads();
         double iv[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r) iv[r] = r < nr ? s_inv[r] : 0.0;
+        for (int r = 0; r < R; ++r) iv[r] = __shfl_sync(0xffffffffu, my_iv, r);  // 0 beyond nr
         const int64_t nxr64 = q.n_x - r0;
         const int nxr = nxr64 <= 0 ? 0 : (nxr64 >= nr ? nr : (int)nxr64);
         if (nxr == 0 || nxr == nr) {  // the whole item on one side (all but <= 1 item per pair)
@@ -1120,8 +1052,10 @@ __global__ void __launch_bounds__(NT, 512 / NT) k1s_stats(AlignArgs a) {
             }
         }
     }
+    KS1_STAMP(2);
     pdl_trigger();  // the coefficient pass may launch (it waits for this grid to complete)
-    if (i0 < i1) pair_done();  // (a CTA without items takes part in no ticket)
+    flush();
+    KS1_STAMP(4);
     if (tid == 0) span_exit(a.span);
 }
 
@@ -1233,44 +1167,160 @@ __global__ void __launch_bounds__(kS1LeanThreads, 4) k1s_stats_warp(AlignArgs a)
 }
 
 // KS2: {2 u.x_i, 1/||h_i||} per pooled row (Y rows and identity pairs: coefficient 0).  The
-// CTAs are split among the pairs in proportion to their X rows; a warp takes one X row
-// (fp64 dot with u staged in shared memory) with 8 column steps of 16 bytes in flight per
-// lane, so an SM has ~30 rows streaming at once.
-__global__ void __launch_bounds__(256) k1s_coef(AlignArgs a, int ctas_per_pair0, int ctas_per_pair1,
-                                                int ctas_per_pair2, int ctas_per_pair3) {
-    pdl_wait();  // KS1 (P3: u, inv) complete and visible
+// CTAs (no more than fit on the GPU at once, so there is no second wave) are split among the
+// pairs in proportion to their X rows; a warp takes X rows in turn (fp64 dot with u staged in
+// shared memory, lane = columns l, l + 32, ... in that order) with 16 column steps of 16
+// bytes in flight per lane (a d = 4096 row in two round trips).
+constexpr int kCoefInFlight = 16;
+constexpr int kCoefThreads = 256;
+template <bool kP3>
+__global__ void __launch_bounds__(kCoefThreads) k1s_coef(AlignArgs a, int ctas_per_pair0, int ctas_per_pair1,
+                                                         int ctas_per_pair2, int ctas_per_pair3) {
+    if constexpr (kP3) {  // the X rows are inputs, not KS1 results: toward L2 while KS1 finishes
+        const int cpp[4] = {ctas_per_pair0, ctas_per_pair1, ctas_per_pair2, ctas_per_pair3};
+        int g = 0, c0 = 0;
+        while (g < a.G - 1 && (int)blockIdx.x >= c0 + cpp[g]) c0 += cpp[g++];
+        const AlignPair& q = a.p[g];
+        const int nw = blockDim.x >> 5;
+        if ((threadIdx.x & 31) == 0)
+            for (int64_t i = (int64_t)(blockIdx.x - c0) * nw + (threadIdx.x >> 5); i < q.n_x; i += (int64_t)cpp[g] * nw)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(q.X + i * a.d), "r"((uint32_t)a.d * 4u)
+                             : "memory");
+    }
+    pdl_wait();  // KS1 (column sums, 1/||h||, ZeroVector rows) complete and visible
     extern __shared__ __align__(16) uint8_t kc_smem[];
-    double* su = reinterpret_cast<double*>(kc_smem);  // [d_pad]
+    double* su = reinterpret_cast<double*>(kc_smem);  // [d_pad] axis u
+    double* sxb = su + a.d_pad;                         // [d_pad] xbar (kP3 only)
+    double* syb = sxb + a.d_pad;                        // [d_pad] ybar
+    __shared__ double red[2 * (kCoefThreads / 32) + 2];
     const int cpp[4] = {ctas_per_pair0, ctas_per_pair1, ctas_per_pair2, ctas_per_pair3};
     int g = 0, c0 = 0;
     while (g < a.G - 1 && (int)blockIdx.x >= c0 + cpp[g]) c0 += cpp[g++];
     const int nct = cpp[g], cta = blockIdx.x - c0;
     const AlignPair& q = a.p[g];
-    const int d = (int)a.d;
+    const int d = (int)a.d, tid = threadIdx.x;
     const int64_t N = q.n_x + q.n_y;
-    if (threadIdx.x == 0) span_enter(a.span);
-    const bool identity = q.info->is_identity != 0;
-    // rows without a reflection: {0, 1/||h||}
-    for (int64_t i = (int64_t)cta * blockDim.x + threadIdx.x; i < N; i += (int64_t)nct * blockDim.x)
+    if (tid == 0) span_enter(a.span);
+    bool identity;
+    if constexpr (kP3) {
+        // ---- P3, derived by EVERY CTA of the pair from the complete column sums (all loads in
+        // flight together: one L2 round trip; identical arithmetic and order in every CTA, so
+        // every CTA holds the same bits): xbar, ybar (Eq. 8 means), r, the axis u and centre m
+        // (Eq. householder_fast), the observed statistic; CTA 0 of the pair publishes u, m and
+        // the pair's info for KS3, K3 and the host.  (d <= 4096 on this path: kPC columns per
+        // thread cover it.)
+        // (xbar, ybar of this thread's own columns are kept in shared memory: no barrier needed
+        // between the passes, registers stay free for the coefficient loop)
+        constexpr int kPC = 4096 / kCoefThreads;
+        const double rnX = 1.0 / (double)q.n_x, rnY = 1.0 / (double)q.n_y;
+        double sxx = 0.0, syy = 0.0;
+        {
+            long long ax[kPC], ay[kPC];
+    #pragma unroll
+            for (int u = 0; u < kPC; ++u) {
+                const int c = tid + u * kCoefThreads;
+                ax[u] = c < d ? __ldcg(q.acc + c) : 0;
+                ay[u] = c < d ? __ldcg(q.acc + d + c) : 0;
+            }
+    #pragma unroll
+            for (int u = 0; u < kPC; ++u) {
+                const int c = tid + u * kCoefThreads;
+                const double xb = (double)ax[u] * kFixInv * rnX, yb = (double)ay[u] * kFixInv * rnY;
+                sxx += xb * xb;
+                syy += yb * yb;
+                if (c < (int)a.d_pad) {
+                    sxb[c] = xb;
+                    syb[c] = yb;
+                }
+            }
+        }
+        const double2 sq = block_sum2_n<kCoefThreads>(sxx, syy, red);
+        const double nx = sqrt(sq.x), ny = sqrt(sq.y);
+        const bool degenerate = nx < 1e-12 || ny < 1e-12;
+        const double rnx = degenerate ? 0.0 : 1.0 / nx;
+        const double rny = degenerate ? 0.0 : 1.0 / ny;
+        double sv = 0.0, svx = 0.0;
+    #pragma unroll
+        for (int u = 0; u < kPC; ++u) {
+            const int c = tid + u * kCoefThreads;
+            if (c < d) {
+                const double v = sxb[c] * rnx - syb[c] * rny;
+                sv += v * v;
+                svx += v * sxb[c];
+            }
+        }
+        const double2 vv = block_sum2_n<kCoefThreads>(sv, svx, red);
+        const double nv0 = sqrt(vv.x);
+        const bool identity_ = (a.mode == HAP_ALIGN_NONE) || degenerate || nv0 < 1e-9;  // R3
+        const double rnv = identity_ ? 0.0 : 1.0 / nv0;
+        const double ux = vv.y * rnv;
+        const double rN = 4096.0 / (double)N;
+    #pragma unroll
+        for (int u = 0; u < kPC; ++u) {
+            const int c = tid + u * kCoefThreads;
+            double ud = 0.0, md = 0.0;
+            if (c < d) {
+                const double xb = sxb[c], yb = syb[c];
+                ud = (xb * rnx - yb * rny) * rnv;
+                const double t = (double)q.n_x * (xb - 2.0 * ud * ux) + (double)q.n_y * yb;
+                md = rint(t * rN) * (1.0 / 4096.0);
+            }
+            if (c < (int)a.d_pad) {
+                su[c] = ud;
+                if (cta == 0) {
+                    q.u[c] = ud;
+                    q.m[c] = md;
+                }
+            }
+        }
+        if (cta == 0 && tid == 0) {
+            hap_align_info* f = q.info;
+            const long long bad = __ldcg(q.bad);
+            f->n_x = q.n_x;
+            f->n_y = q.n_y;
+            f->d = a.d;
+            f->n_pad = q.n_pad;
+            f->d_pad = a.d_pad;
+            f->is_identity = identity_ ? 1 : 0;
+            f->status = bad < N ? HAP_E_ZERO_VECTOR : (degenerate ? HAP_E_DEGENERATE_MEAN : HAP_OK);
+            f->bad_row = bad < N ? bad : -1;
+            f->r_x = nx;  // r(X') = ||xbar||
+            f->r_y = ny;
+            const double lx = logkappa64(nx, (double)a.d), ly = logkappa64(ny, (double)a.d);
+            f->logk_x = lx;
+            f->logk_y = ly;
+            f->t_obs = (isinf(lx) && isinf(ly)) ? 0.0 : ly - lx;  // Eq. 10
+            const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+            f->gemm_r_x = f->gemm_r_y = f->gemm_t_obs = qnan;
+        }
+        identity = identity_;
+    } else {  // P3 ran in KS1 (warp-per-row variant, d <= 1024): stage u
+        identity = q.info->is_identity != 0;
+        for (int c = tid; c < (int)a.d_pad; c += kCoefThreads) su[c] = q.u[c];
+    }
+    __syncthreads();  // su complete
+    // ---- S4 coefficients: rows without a reflection {0, 1/||h||}
+    for (int64_t i = (int64_t)cta * blockDim.x + tid; i < N; i += (int64_t)nct * blockDim.x)
         if (identity || i >= q.n_x) q.coef[i] = make_float2(0.f, (float)__ldcg(q.inv + i));
     if (!identity) {
-        for (int c = threadIdx.x; c < (int)a.d_pad; c += blockDim.x) su[c] = q.u[c];
-        __syncthreads();
-        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+        const int warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
         const int n4 = d / 4;
         const double2* su2 = reinterpret_cast<const double2*>(su);
         for (int64_t i = (int64_t)cta * nw + warp; i < q.n_x; i += (int64_t)nct * nw) {
             const float4* rp = reinterpret_cast<const float4*>(q.X + i * d);
             double dot0 = 0.0, dot1 = 0.0;
-            for (int c4b = 0; c4b < n4; c4b += 32 * 8) {
-                float4 h[8];
+            // (d <= 1024: 8 steps cover a row, and fewer registers leave room beside K3)
+            constexpr int kIF = kP3 ? kCoefInFlight : 8;
+#pragma unroll 1
+            for (int c4b = 0; c4b < n4; c4b += 32 * kIF) {
+                float4 h[kIF];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
+                for (int u = 0; u < kIF; ++u) {
                     const int c4 = c4b + 32 * u + lane;
                     h[u] = c4 < n4 ? __ldcs(rp + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
+                for (int u = 0; u < kIF; ++u) {
                     const int c4 = c4b + 32 * u + lane;
                     if (c4 < n4) {
                         const double2 ua = su2[2 * c4], ub = su2[2 * c4 + 1];
@@ -1288,7 +1338,7 @@ __global__ void __launch_bounds__(256) k1s_coef(AlignArgs a, int ctas_per_pair0,
     }
     pdl_trigger();
     __syncthreads();
-    if (threadIdx.x == 0) span_exit(a.span);
+    if (tid == 0) span_exit(a.span);
 }
 
 // KS3: tiles (pair, column strip of 64, row block of 128) in that order; CTA c takes tiles
@@ -1327,6 +1377,7 @@ struct XfPair {
 __global__ void __launch_bounds__(kThreads, 1) k1s_xform(AlignArgs a, int64_t tile_off1, int64_t tile_off2,
                                                          int64_t tile_off3, int64_t tiles_total) {
     pdl_wait();  // KS2 (coefficients) complete and visible
+    KS1_STAMP(7);
     extern __shared__ __align__(16) uint8_t xf_smem[];
     float* raw = reinterpret_cast<float*>(xf_smem);  // [kXfStages][128][64]
     float2* rcoef = reinterpret_cast<float2*>(raw + kXfStages * kXfRows * kXfCols);  // [kXfStages][128]
@@ -1419,7 +1470,10 @@ __global__ void __launch_bounds__(kThreads, 1) k1s_xform(AlignArgs a, int64_t ti
         flush();
         cur_g = -1;  // (flushed)
         const unsigned total = (unsigned)(strips * ((a.p[pg].n_pad + kXfRows - 1) / kXfRows));
-        if (pair_ticket(a.p[pg], 5, pcnt, total, &s_last)) finish_pair(a, pg, red);
+        if (pair_ticket(a.p[pg], 5, pcnt, total, &s_last)) {
+            finish_pair(a, pg, red);
+            KS1_STAMP(6);
+        }
         pcnt = 0;
     };
     for (int64_t t = t0; t < t1; ++t) {
@@ -1522,7 +1576,9 @@ __global__ void __launch_bounds__(kThreads, 1) k1s_xform(AlignArgs a, int64_t ti
         }
     }
     cp_async_wait<0>();
+    KS1_STAMP(3);
     if (t0 < t1) pair_done();
+    KS1_STAMP(5);
     if (tid == 0) span_exit(a.span);
 }
 
@@ -1543,6 +1599,7 @@ constexpr int kXlTW = kXlRows / 2 + 1;  // u32 words per staging column (33: con
 __global__ void __launch_bounds__(kXlThreads, 4) k1s_xform_lean(AlignArgs a, int64_t tile_off1, int64_t tile_off2,
                                                                int64_t tile_off3, int64_t tiles_total) {
     pdl_wait();  // KS2 (coefficients) complete and visible
+    KS1_STAMP(7);
     __shared__ uint32_t sh_hi[kXfCols * kXlTW];
     __shared__ uint32_t sh_lo[kXfCols * kXlTW];
     __shared__ double red[2 * (kXlThreads / 32) + 2];
@@ -1745,7 +1802,11 @@ int align_path(int64_t N, int64_t d) {
 }
 
 bool align_uses_stream(const AlignArgs& a) {
+#ifdef HAP_EXPERIMENTS
+    if (a.do_draws) return false;  // development build: KS1 writes per-CTA stamps (ks1_stamp)
+#else
     if (a.do_draws || a.stamps) return false;  // experiments / K1 phase stamps: fused kernel only
+#endif
     for (int g = 0; g < a.G; ++g) {
         const AlignPair& q = a.p[g];
         if (align_path(q.n_x + q.n_y, a.d) == kAlignFused) return false;
@@ -1841,14 +1902,43 @@ static cudaError_t launch_align_stream(AlignArgs a, int sm_count, cudaStream_t s
 
 static cudaError_t launch_align_ks23(AlignArgs a, int sm_count, cudaStream_t st, bool lean) {
     cudaError_t e;
-    {  // KS2: CTAs in proportion to the pairs' rows, ~4 per SM in total
+    // KS2 derives P3 itself unless KS1 was the warp-per-row variant (lean, d <= 1024), whose
+    // ticketed P3 is a single short round trip (and whose waves run beside the mask-GEMM)
+    const bool p3 = !(lean && a.d <= 1024);
+    {  // KS2: CTAs in proportion to the pairs' X rows (kP3: at most what is resident at once)
+        const size_t smem2 = (size_t)a.d_pad * 8 * (p3 ? 3 : 1);  // u (+ xbar, ybar)
         int cpp[kMaxWave] = {0, 0, 0, 0}, total = 0;
-        for (int g = 0; g < a.G; ++g) {  // one warp per X row (8 warps per CTA)
-            cpp[g] = (int)std::max<int64_t>(1, ceil_div(a.p[g].n_x, 8));
-            total += cpp[g];
+        if (p3) {
+            static int per_sm[2] = {0, 0};  // resident CTAs per SM for d_pad <= / > 2048
+            const int big = a.d_pad > 2048;
+            if (per_sm[big] == 0) {
+                e = cudaFuncSetAttribute(k1s_coef<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 8 * 3);
+                if (e == cudaSuccess) e = max_carveout((const void*)k1s_coef<true>);
+                if (e == cudaSuccess)
+                    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[big], k1s_coef<true>, kCoefThreads,
+                                                                      (big ? 4096 : 2048) * 8 * 3);
+                if (e != cudaSuccess) return e;
+                per_sm[big] = std::max(per_sm[big], 1);
+            }
+            const int64_t cap = (int64_t)per_sm[big] * sm_count;
+            int64_t rows = 0;
+            for (int g = 0; g < a.G; ++g) rows += a.p[g].n_x;
+            for (int g = 0; g < a.G; ++g) {  // one warp per X row at a time (8 warps per CTA)
+                const int64_t want = ceil_div(a.p[g].n_x, 8);
+                const int64_t share = rows > 0 ? ceil_div(cap * a.p[g].n_x, rows) : 1;
+                cpp[g] = (int)std::max<int64_t>(1, std::min(want, share));
+                total += cpp[g];
+            }
+            e = launch_pdl(k1s_coef<true>, dim3(total), dim3(kCoefThreads), smem2, st, a, cpp[0], cpp[1], cpp[2],
+                           cpp[3]);
+        } else {
+            for (int g = 0; g < a.G; ++g) {  // one warp per X row (8 warps per CTA)
+                cpp[g] = (int)std::max<int64_t>(1, ceil_div(a.p[g].n_x, 8));
+                total += cpp[g];
+            }
+            e = launch_pdl(k1s_coef<false>, dim3(total), dim3(kCoefThreads), smem2, st, a, cpp[0], cpp[1], cpp[2],
+                           cpp[3]);
         }
-        const size_t smem2 = (size_t)a.d_pad * 8;
-        e = launch_pdl(k1s_coef, dim3(total), dim3(256), smem2, st, a, cpp[0], cpp[1], cpp[2], cpp[3]);
         if (e != cudaSuccess) return e;
     }
     if (lean) {  // KS3-lean: 64-row tiles, two CTAs per SM at most
@@ -1861,7 +1951,7 @@ static cudaError_t launch_align_ks23(AlignArgs a, int sm_count, cudaStream_t st,
         static bool xl_configured = false;
         if (!xl_configured) {
             e = max_carveout((const void*)k1s_xform_lean);
-            if (e == cudaSuccess) e = max_carveout((const void*)k1s_coef);
+            if (e == cudaSuccess) e = max_carveout((const void*)k1s_coef<false>);
             if (e != cudaSuccess) return e;
             xl_configured = true;
         }
@@ -1878,7 +1968,6 @@ static cudaError_t launch_align_ks23(AlignArgs a, int sm_count, cudaStream_t st,
         if (!xf_configured) {
             e = cudaFuncSetAttribute(k1s_xform, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kXfSmem);
             if (e == cudaSuccess) e = max_carveout((const void*)k1s_xform);
-            if (e == cudaSuccess) e = max_carveout((const void*)k1s_coef);
             if (e != cudaSuccess) return e;
             xf_configured = true;
         }
