@@ -46,7 +46,6 @@ namespace {
 constexpr int kThreads = HAP_K1_THREADS;  // 64 registers per thread: 2 (or 4) CTAs fit per SM
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxItemRows = 16;
-constexpr int kSpartStride = 8;  // doubles per CTA in spart: P5 [4,5]
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -104,13 +103,6 @@ __device__ double2 block_sum2_n(double v0, double v1, double* red) {
     return make_double2(red[2 * W], red[2 * W + 1]);
 }
 
-// sum over CTAs p of spart[p*kSpartStride + k], fixed order (same in every CTA)
-__device__ double cta_partials_sum(const double* spart, int k, double* red) {
-    double v = 0.0;
-    for (int p = threadIdx.x; p < (int)gridDim.x; p += kThreads)
-        v += __ldcg(spart + (size_t)p * kSpartStride + k);
-    return block_sum2(v, 0.0, red).x;
-}
 
 __device__ __forceinline__ void stamp(const AlignArgs& a, int k) {
     if (a.stamps && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -366,7 +358,6 @@ __global__ void __launch_bounds__(kThreads, 65536 / (kThreads * 64)) k1_align_fu
     const int G = gridDim.x, cta = blockIdx.x;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int d = (int)a.d;
-    const int64_t items = a.item_off[a.G];
     unsigned* bar = reinterpret_cast<unsigned*>(a.scratch + 2);
     if (tid == 0) span_enter(a.span);
     stamp(a, 0);
