@@ -30,6 +30,10 @@ HAP_API hap_status hap_debug_k1_stamps(hap_ctx ctx, long long* out, int64_t n);
  * batch sub-contexts and returns HAP_E_CUDA (message: the buffer) if one was overwritten.
  * The release library writes 0 and returns HAP_E_INVALID_ARG (no checks compiled in). */
 HAP_API hap_status hap_debug_check_status(hap_ctx ctx, uint64_t* word);
+/* K3 form of the last test hap_permtest planned on ctx (host value, no sync): *gram = 1 for
+ * the Gram form, 0 for the plane form, -1 before any test; the
+ * parity tests use it to mirror the kernel's error bound (R14). */
+HAP_API hap_status hap_debug_last_form(hap_ctx ctx, int32_t* gram);
 /* Scheduling experiments: enqueue a register-only Philox loop of `iters` rounds on
  * ctas x threads threads, no shared memory. */
 HAP_API hap_status hap_debug_alu_burn(hap_ctx ctx, uint32_t iters, int ctas, int threads, void* stream);

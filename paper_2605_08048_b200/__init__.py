@@ -103,6 +103,7 @@ def lib() -> ctypes.CDLL:
         "hap_debug_k3_stamps": ([vp, vp, i64], i32),
         "hap_debug_k1_stamps": ([vp, vp, i64], i32),
         "hap_debug_check_status": ([vp, P(u64)], i32),
+        "hap_debug_last_form": ([vp, P(ctypes.c_int32)], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -394,6 +395,13 @@ class Context:
                             p_value=hap_pvalue(c[0], B) if ok else None,
                             p_two_sided=hap_pvalue(c[1], B) if ok else None))
         return out
+
+
+def hap_debug_last_form(ctx):
+    """K3 form of the last test planned on ctx: 1 Gram, 0 planes, -1 none (include/hap_debug.h)."""
+    g = ctypes.c_int32(-1)
+    st = lib().hap_debug_last_form(ctx, ctypes.byref(g))
+    return int(g.value) if st == 0 else -1
 
 
 def hap_debug_check_status(ctx):

@@ -32,6 +32,7 @@ struct hap_ctx_s {
     // ---- state of the last successful hap_align
     bool aligned = false;
     bool gram_ok = false;  // the Gram planes of the current alignment are built (k_gram.cu)
+    int last_gram = -1;    // K3 form of the last test planned on this context (1 = Gram)
     int64_t n_x = 0, n_y = 0, d = 0, n_pad = 0, d_pad = 0;
     // ---- TMA descriptors (valid for the current buffers/shape); tmA per mask slot
     CUtensorMap tmA[2]{}, tmBhi{}, tmBlo{};
@@ -926,6 +927,7 @@ hap_status plan_wave(hap_ctx owner, int G, const WaveTest* T, int pair, bool sha
         pt.exhaustive = (T[k].cfg->flags & HAP_FLAG_EXHAUSTIVE) ? 1 : 0;
         GemmTest& gt = g.t[k];
         gt.gram = use_gram(w, T[k].cfg) ? 1 : 0;
+        w->last_gram = gt.gram;
         gt.ncols = gt.gram ? (int)w->n_pad : (int)w->d_pad;
         gt.mbits = nullptr;
         if (gt.gram) {
@@ -1555,6 +1557,12 @@ hap_status hap_perm_sets(hap_ctx c, uint64_t seed, uint32_t stream_id, uint64_t 
     perm_items(pa);
     cudaError_t e = launch_perm(pa, c->sm_count, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(c, e, "perm generator");
+    return HAP_OK;
+}
+
+hap_status hap_debug_last_form(hap_ctx c, int32_t* gram) {
+    if (!c || !gram) return HAP_E_INVALID_ARG;
+    *gram = c->last_gram;
     return HAP_OK;
 }
 

@@ -119,14 +119,16 @@ __device__ __forceinline__ double l_width(double r, float delta) {
 }
 
 // Gram form (k_gram.cu): error of r from the form's own roundings, on top of the planes'
-// representation error that both forms share (R14).  |acc|^2 = sum_{j,k} G'_jk carries the
-// bf16 hi/lo rounding of the n^2 entries (2^-17 relative, independent signs: ~ sqrt of the
-// sum of squares, entries <= |z'|^2 <= 4, off-diagonal ones ~ 1/sqrt(d) of that) and the
-// fp32 accumulation of each U_bj over n terms (2^-24 per add); 8x margin as in R14;
-// dr = dS / (2 n^2 r).
-__device__ __forceinline__ float gram_delta(float n, float d, double r) {
-    const float dS = 8.f * 4.f * sqrtf(1.f + n / d) * (0x1p-17f * sqrtf(n) + 0x1p-22f * n);
-    return 1.01f * dS / (2.f * n * n * fmaxf((float)r, 1e-6f));
+// representation error that both forms share (R14).  Both S1 and S2 are sums over the MASKED
+// group's entries (S_g = S_gc + sum_j m_bj (U_bj +- 2 alpha/beta_j), U_bj = sum_k m_bk G'_jk),
+// so both carry the error of n^2 Gram entries with n = n_x, the mask's group: the bf16 hi/lo
+// rounding (2^-17 relative, independent signs: ~ sqrt of the sum of squares, entries <=
+// |z'|^2 <= 4, off-diagonal ones ~ 1/sqrt(d) of that) and the fp32 accumulation of each U_bj
+// over n terms (2^-24 per add); 8x margin as in R14; dr_g = dS / (2 n_g^2 r_g) (the complement
+// group's r inherits the masked group's dS: a small Y next to a large X is wide).
+__device__ __forceinline__ float gram_delta(float n_mask, float n_g, float d, double r) {
+    const float dS = 8.f * 4.f * sqrtf(1.f + n_mask / d) * (0x1p-17f * sqrtf(n_mask) + 0x1p-22f * n_mask);
+    return 1.01f * dS / (2.f * n_g * n_g * fmaxf((float)r, 1e-6f));
 }
 
 // statistic of a tile row from its accumulated sums S1 = |sigma1|^2, S2 = |sigma2|^2;
@@ -145,8 +147,16 @@ __device__ __forceinline__ RowStat row_stat(const GemmArgs& g, const GemmTest& T
     const float k = 1.01f * 8.f * (float)eps * rsqrtf((float)d);
     float d1 = k * rsqrtf((float)T.n_x), d2 = k * rsqrtf((float)T.n_y);
     if (T.gram) {  // + the Gram form's own rounding
-        d1 += gram_delta((float)T.n_x, (float)d, s.r1);
-        d2 += gram_delta((float)T.n_y, (float)d, s.r2);
+        d1 += gram_delta((float)T.n_x, (float)T.n_x, (float)d, s.r1);
+        d2 += gram_delta((float)T.n_x, (float)T.n_y, (float)d, s.r2);
+    } else {
+        // + the fp32 accumulation of the masked sums (R14b): sigma1 = a + acc and, through
+        // the complement, sigma2 = b - acc carry the accumulator's rounding over the n_x
+        // masked rows (2 n_x / 16 MMA steps, |acc_c| ~ sqrt(n_x / d)): 8x margin ->
+        // |dr_g| <= 2^-22 n_x / (sqrt(d) n_g), which matters for a small group beside a large one
+        const float ka = 1.01f * 0x1p-22f * (float)T.n_x * rsqrtf((float)d);
+        d1 += ka / (float)T.n_x;
+        d2 += ka / (float)T.n_y;
     }
     s.e = l_width(s.r1, T.n_x == 1 ? 0.f : d1) + l_width(s.r2, T.n_y == 1 ? 0.f : d2);
     return s;

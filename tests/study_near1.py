@@ -5,7 +5,9 @@ the same seeded inputs; prints one JSON line with the largest |dr| of the permut
 the largest |dT| relative to the tie band scale (|L_X| + |L_Y|), the decisions that differ
 outside the oracle's tie band, and the largest representation error max_i ||z~_i - z_i||
 of the pooled planes (hap_export_pooled vs the oracle's aligned cloud).
-Usage (B200): python tools/near1.py [--out gpurun_out/near1.jsonl]
+Usage (B200): python tests/study_near1.py [--out gpurun_out/near1.jsonl]
+(A test-side study: it calls oracle/, which only tests/, smoke() and bench.py's cpu_baseline
+may touch, so it lives here rather than in tools/; pytest does not collect it.)
 """
 from __future__ import annotations
 

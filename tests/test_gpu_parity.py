@@ -7,6 +7,7 @@ on the same seeded inputs.  Bars:
     |c_gpu - c_oracle| <= flagged (tie band tau = 1e-6 (|L_X| + |L_Y|), R8).
 """
 import math
+import os
 
 import numpy as np
 import pytest
@@ -226,13 +227,20 @@ def _eps_rep(hap, ctx, d):
     return 2.0 ** -17 * math.sqrt(max(1.0 - float(mm @ mm), 0.0)) + 2.0 ** -23
 
 
-def _l_width(r, n, eps, d):
-    """DESIGN.md R14 (mirror of k_maskgemm.cu l_width): half-width of the interval holding
-    L(r) given the GPU's r and |dr| <= 8 eps / sqrt(n d)."""
+def _l_width(r, n, eps, d, n_mask=None, gram=False):
+    """DESIGN.md R14 (mirror of k_maskgemm.cu row_stat / l_width): half-width of the interval
+    holding L(r) given the GPU's r and |dr| <= 8 eps / sqrt(n d) (+ R14b: the accumulation
+    over the masked group's n_mask rows, or the Gram form's dS of n_mask^2 entries)."""
     r = np.asarray(r, dtype=np.float64)
     if n == 1:
         return np.zeros_like(r)
+    n_mask = n if n_mask is None else n_mask
     delta = 8.0 * eps / math.sqrt(n * d)
+    if gram:
+        dS = 8.0 * 4.0 * math.sqrt(1.0 + n_mask / d) * (2.0 ** -17 * math.sqrt(n_mask) + 2.0 ** -22 * n_mask)
+        delta = delta + dS / (2.0 * n * n * np.maximum(r, 1e-6))
+    else:
+        delta = delta + 2.0 ** -22 * n_mask / (math.sqrt(d) * n)
 
     def q(x):
         x = np.minimum(x, 1 - 1e-9)
@@ -244,18 +252,20 @@ def _l_width(r, n, eps, d):
     return np.where(r <= 2 * delta, np.inf, w)
 
 
-def check_certified(hap, ctx, orc, X, Y, B, s=0):
+def check_certified(hap, ctx, orc, X, Y, B, s=0, mode=0, block=0, pair_mode=0, gram=None):
     """R14 at any r: the GPU's error bound e_T covers its actual error on every permutation
     (and on T_obs); every decision outside the widened band matches the oracle; the GPU
     flags a superset of the oracle's near-ties, and the counts differ by at most those."""
-    g = ctx.permtest_pair(_cuda(X), _cuda(Y), B, SEED, stream_id=s, want_stats=True)
-    ref = orc.run_pair(X, Y, B, SEED, s=s, want_stats=True)
+    g = ctx.permtest_pair(_cuda(X), _cuda(Y), B, SEED, stream_id=s, want_stats=True, mode=mode,
+                          block=block, pair_mode=pair_mode, gram=gram)
+    ref = orc.run_pair(X, Y, B, SEED, s=s, want_stats=True, mode=mode)
     d, n_x, n_y = X.shape[1], X.shape[0], Y.shape[0]
     eps = _eps_rep(hap, ctx, d)
     gs, rs = g["stats"].cpu().numpy(), ref["stats"]
-    e = _l_width(gs[:, 0], n_x, eps, d) + _l_width(gs[:, 1], n_y, eps, d)
-    e_obs = float(_l_width(np.array([g["gemm_r_x"]]), n_x, eps, d)[0] +
-                  _l_width(np.array([g["gemm_r_y"]]), n_y, eps, d)[0])
+    gf = hap.hap_debug_last_form(ctx.h) == 1
+    e = _l_width(gs[:, 0], n_x, eps, d, n_x, gf) + _l_width(gs[:, 1], n_y, eps, d, n_x, gf)
+    e_obs = float(_l_width(np.array([g["gemm_r_x"]]), n_x, eps, d, n_x, gf)[0] +
+                  _l_width(np.array([g["gemm_r_y"]]), n_y, eps, d, n_x, gf)[0])
     assert abs(g["gemm_t_obs"] - ref["t_obs"]) <= e_obs + 1e-6 * (abs(ref["L_x"]) + abs(ref["L_y"]))
     assert np.all(np.abs(gs[:, 2] - rs[:, 2]) <= e + 1e-7 * (abs(ref["L_x"]) + abs(ref["L_y"])))
     band = ref["tau"] + e + e_obs
@@ -861,6 +871,47 @@ def test_fuzz_shapes_vs_oracle(ctx, orc, case):
     i, nx, ny, d, B, mode, pair_mode, block, gram = case
     X, Y = HI.make_pair(HI.PairSpec(nx, ny, d, 8.0 + d, 8.0 + d, 40.0, seed=900 + i))
     check_pair(ctx, orc, X, Y, B, s=i, mode=mode, block=block, pair_mode=pair_mode, gram=gram)
+
+
+def _campaign_cases(seed=20261019):
+    """Wider seeded shapes than _fuzz_cases: log-uniform group sizes 1..1500 (singletons
+    included), d up to 4096 (the streaming ring K1 path once n_pad d >= 8 Mi), B scaled so the
+    oracle stays within seconds.  FUZZ_CASES (default 6) sets the count: the suite runs 6; a
+    campaign run (profiles/r02_fuzz_campaign.log) runs 120."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(int(os.environ.get("FUZZ_CASES", "6"))):
+        nx = int(np.exp(rng.uniform(0.0, np.log(1500))))
+        ny = int(np.exp(rng.uniform(0.0, np.log(1500))))
+        if rng.uniform() < 0.15:  # ring-path sizes (n_pad d >= 8 Mi at d = 4096)
+            nx, ny = int(rng.integers(1000, 1400)), int(rng.integers(1000, 1400))
+            d = 4096
+        else:
+            d = int(rng.choice([2, 3, 17, 31, 64, 100, 257, 768, 1024, 1540, 2048, 4096]))
+        B = int(max(1, min(int(rng.integers(1, 2500)), 3e9 // max(1, (nx + ny) * d))))
+        out.append((i, nx, ny, d, B, int(rng.integers(0, 2)), int(rng.choice([1, 2])),
+                    int(rng.choice([0, 97])), [None, True, False][int(rng.integers(0, 3))]))
+    return out
+
+
+@pytest.mark.parametrize("case", _campaign_cases(),
+                         ids=lambda c: f"c{c[0]}_n{c[1]}x{c[2]}_d{c[3]}_B{c[4]}")
+def test_fuzz_campaign_vs_oracle(hap, ctx, orc, case):
+    """Seeded wide random shapes against the oracle.  Every case must meet the certified bar
+    (R14: the kernel's own error bound covers its error on every permutation, every decision
+    outside the widened band is the oracle's, counts within the GPU's flagged); the plain 1e-5
+    bars of check_pair are reported per case (they fail where a tiny group's sums come from
+    the complement t - sigma of a large one, or where d <= 3 makes L(r) ill-conditioned:
+    DESIGN.md §4)."""
+    i, nx, ny, d, B, mode, pair_mode, block, gram = case
+    X, Y = HI.make_pair(HI.PairSpec(nx, ny, d, 8.0 + d, 8.0 + d, 40.0, seed=5000 + i))
+    check_certified(hap, ctx, orc, X, Y, B, s=100 + i, mode=mode, block=block, pair_mode=pair_mode,
+                    gram=gram)
+    try:
+        check_pair(ctx, orc, X, Y, B, s=100 + i, mode=mode, block=block, pair_mode=pair_mode, gram=gram)
+        print(f"PLAIN-BARS ok   case {i} n {nx}x{ny} d {d}")
+    except AssertionError:
+        print(f"PLAIN-BARS miss case {i} n {nx}x{ny} d {d} (certified bar met)")
 
 
 @pytest.mark.parametrize("seed", [1, 2, 3, 4, 5, 6])
