@@ -347,7 +347,34 @@ def kernel_profile(E, run_waves, n_tests, N, d, B, peaks, what):
                        "achieved": n_tests * B / k2_s if k2_s else 0.0,
                        "us_per_test": k2_s * 1e6 / n_tests},
         "phase_ms": phase_ms,
+        "traffic": None,
+        "traffic_basis": "no ncu --set full capture of this workload's K3 launch is committed "
+                         "(profiles/r02_ncu_full_k3_k2_raw.csv is a C2 wave)",
     }
+
+
+NCU_FULL = os.path.join(ROOT, "profiles", "r02_ncu_full_k3_k2_raw.csv")
+
+
+def ncu_traffic(kernel="k3_maskgemm"):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one launch of `kernel` from the
+    committed `ncu --set full` capture (a C2 batch wave of 3 tests: the launch shape the C2
+    bench times), in bytes; None if the capture is absent."""
+    import csv
+    try:
+        rows = list(csv.reader(open(NCU_FULL)))
+    except OSError:
+        return None
+    hdr, units = rows[0], rows[1]
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    for r in rows[2:]:
+        if kernel in r[hdr.index("Kernel Name")]:
+            tot = 0.0
+            for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                i = hdr.index(k)
+                tot += float(r[i].replace(",", "")) * scale.get(units[i], 1.0)
+            return tot
+    return None
 
 
 def in_step_spans(E, run_one_step, flops, peaks):
@@ -434,6 +461,13 @@ def run_c2(args, E, peaks):
             torch.cuda.synchronize()
     roof = kernel_profile(E, waves, nw * wave, N, d, B, peaks,
                           f"one launch = a wave of {wave} C2 tests")
+    n_pad, d_pad = -(-N // 64) * 64, -(-d // 32) * 32
+    tiles = -(-B // 127)  # 127 permutation rows + the observed row per 128-row tile
+    roof["traffic"] = ncu_traffic()
+    roof["traffic_basis"] = ("dram__bytes_read.sum + dram__bytes_write.sum of one K3 launch "
+                             "(a wave of 3 C2 tests) from profiles/r02_ncu_full_k3_k2_raw.csv "
+                             "(ncu --set full)")
+    roof["operand_bytes_per_launch"] = wave * (tiles * 128 * n_pad * 2 + 2 * d_pad * n_pad * 2)
 
     def one_step():
         scratch.zero_()
