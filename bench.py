@@ -509,8 +509,8 @@ def run_c2(args, E, peaks):
                      "repeated in HBM) > 126 MB L2; no flush",
                "parallelism": f"dp{E.world}: each rank runs its own {T} tests per step; "
                               "counts combined by one all_reduce",
-               "api": "hap_permtest_batch (2 internal lanes, waves of 3 tests per alignment / "
-                      "generator / mask-GEMM launch)",
+               "api": "hap_permtest_batch (2 internal lanes, the library's automatic wave size: 4 "
+                      "tests per alignment / generator / mask-GEMM launch at N <= 2048)",
                "arith": "bf16 hi/lo split operands, fp32 TMEM accumulation, fp64 statistic"}
     last = int(counts[E.rank, K - 1, T - 1, 0])
     extra = {"last_test": {"exceed_ge": last, "p_value": hap.hap_pvalue(last, B)}}

@@ -93,7 +93,8 @@ typedef struct {
     uint32_t block;     /* B0 permutations per generator/GEMM block; perf only, 0 = auto */
     int32_t pair_mode;  /* K3 CTA grouping: 0 = auto (2), 1 = cta_group::1, 2 = cta_group::2 */
     int32_t wave;       /* hap_permtest_batch: tests per alignment/generator/GEMM launch, 1..4;
-                         * perf only; 0 = auto (3, or 4 with HAP_FLAG_SHARED_MASK) */
+                         * perf only; 0 = auto (4 with HAP_FLAG_SHARED_MASK or when every
+                         * pair of the batch has N <= 2048, else 3) */
     double tie_rel;     /* tie band tau = tie_rel * (|logk_x| + |logk_y|) (R8); <= 0 -> 1e-6 */
     uint32_t flags;     /* HAP_FLAG_* */
     uint32_t reserved;

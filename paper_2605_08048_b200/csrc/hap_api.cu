@@ -1224,21 +1224,23 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
     const int pair = cfg->pair_mode ? cfg->pair_mode : 2;
     const int64_t R = (int64_t)kTileM * pair;
     const int64_t B = (int64_t)(cfg->b_end - cfg->b_begin);
+    int64_t maxN = 0, maxnx = 0, maxny = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t p = pair_sel ? pair_sel[i] : i;
+        maxN = std::max<int64_t>(maxN, (cu_nx[p + 1] - cu_nx[p]) + (cu_ny[p + 1] - cu_ny[p]));
+        maxnx = std::max<int64_t>(maxnx, cu_nx[p + 1] - cu_nx[p]);
+        maxny = std::max<int64_t>(maxny, cu_ny[p + 1] - cu_ny[p]);
+    }
     // wave size: tests whose whole b-range is one block are grouped (cfg->wave, else
-    // HAP_WAVE, else 3 (4 with shared masks): measured on B200 the best for C2, C4, C5);
-    // others run alone with their blocks in sequence
+    // HAP_WAVE, else 4 with shared masks or when every pair has N <= 2048, else 3: measured on
+    // B200, profiles/r02_experiments/e50_wave.log: C2 73.0 -> 72.0 and C5 40.2 -> 39.2 us per
+    // test with 4, the varlen C4 batch (N up to 10^4) 92.4 vs 93.9 with 3); others run alone
+    // with their blocks in sequence
     const bool shared = (cfg->flags & HAP_FLAG_SHARED_MASK) != 0;
     static const char* wv = getenv("HAP_WAVE");
-    const int wave_max = std::max(1, std::min(kMaxWave, cfg->wave > 0 ? cfg->wave
-                                                        : wv ? atoi(wv) : shared ? kMaxWave : 3));
+    const int wave_auto = (shared || maxN <= 2048) ? kMaxWave : 3;
+    const int wave_max = std::max(1, std::min(kMaxWave, cfg->wave > 0 ? cfg->wave : wv ? atoi(wv) : wave_auto));
     {  // reserve every workspace the waves can use before the first launch
-        int64_t maxN = 0, maxnx = 0, maxny = 0;
-        for (int64_t i = 0; i < n; ++i) {
-            const int64_t p = pair_sel ? pair_sel[i] : i;
-            maxN = std::max<int64_t>(maxN, (cu_nx[p + 1] - cu_nx[p]) + (cu_ny[p + 1] - cu_ny[p]));
-            maxnx = std::max<int64_t>(maxnx, cu_nx[p + 1] - cu_nx[p]);
-            maxny = std::max<int64_t>(maxny, cu_ny[p + 1] - cu_ny[p]);
-        }
         if (maxN > 0) {
             const int64_t n_pad = round_up(maxN, kKBlock);
             const int64_t tiles = std::min(std::max<int64_t>(1, ceil_div(std::max<int64_t>(B, 1), R - 1)),
