@@ -1248,9 +1248,10 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
             for (int k = 0; k < nlanes && !s; ++k)
                 for (int j = 0; j < wave_max && !s; ++j) {
                     s = reserve_pair(c->sub[k][j], maxN, d, tiles, R, j == 0);
-                    for (int b = 0; b < 2 && host_in; ++b) {
-                        if (!s) s = ensure(c->sub[k][j], b ? kX2 : kX, (size_t)maxnx * d * 4);
-                        if (!s) s = ensure(c->sub[k][j], b ? kY2 : kY, (size_t)maxny * d * 4);
+                    for (int b = 0; b < 2 && host_in; ++b) {  // (the owner's: a whole wave's rows)
+                        const int64_t f = j == 0 ? wave_max : 1;
+                        if (!s) s = ensure(c->sub[k][j], b ? kX2 : kX, (size_t)f * maxnx * d * 4);
+                        if (!s) s = ensure(c->sub[k][j], b ? kY2 : kY, (size_t)f * maxny * d * 4);
                     }
                 }
             if (s) return fail(c, s, "batch workspace");
@@ -1282,21 +1283,61 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
         WaveTest T[kMaxWave];
         AlignPair Q[kMaxWave];
         hap_ctx W[kMaxWave];
-        int G = 0;
-        while (i < n && G < wave_max) {
-            const int64_t p = order[(size_t)i];
+        // the wave's pairs (decided on their shapes before anything is enqueued)
+        int64_t mem[kMaxWave];
+        int Gm = 0;
+        for (int64_t j = i; j < n && Gm < wave_max;) {
+            const int64_t p = order[(size_t)j];
             const int64_t nx = cu_nx[p + 1] - cu_nx[p], ny = cu_ny[p + 1] - cu_ny[p];
             const bool one_block = ceil_div(std::max<int64_t>(B, 1), R - 1) <= block_tiles(cfg, round_up(nx + ny, kKBlock), R);
-            if (G > 0 && !one_block) break;  // a multi-block test starts its own wave
-            if (G > 0 && shared && (nx != Q[0].n_x || ny != Q[0].n_y)) break;  // same masks
-            // one alignment path per wave (the path is a function of the pair's shape)
-            if (G > 0 && align_path(nx + ny, d) != align_path(Q[0].n_x + Q[0].n_y, d)) break;
+            if (Gm > 0) {
+                const int64_t p0 = mem[0], nx0 = cu_nx[p0 + 1] - cu_nx[p0], ny0 = cu_ny[p0 + 1] - cu_ny[p0];
+                if (!one_block) break;  // a multi-block test starts its own wave
+                if (shared && (nx != nx0 || ny != ny0)) break;  // same masks
+                // one alignment path per wave (the path is a function of the pair's shape)
+                if (align_path(nx + ny, d) != align_path(nx0 + ny0, d)) break;
+            }
+            mem[Gm++] = p;
+            ++j;
+            if (!one_block) break;
+        }
+        const int sb = c->lane_waves[k] & 1;  // staging buffers of this wave
+        if (host_in && Gm > 0 && c->k1_recorded[k][sb])  // their last reader: the K1 two waves back
+            cudaStreamWaitEvent(c->cp_stream[k], c->ev_k1done[k][sb], 0);
+        // host inputs of consecutive packed pairs: ONE copy of the wave's X rows and one of its
+        // Y rows into the wave owner's staging buffers (a copy per pair paid ~5 us of DMA set-up
+        // per 3 MB at C2, ~9 % of the H2D time); the pairs then read their rows from there
+        const float* dXw = nullptr;
+        const float* dYw = nullptr;
+        if (host_in && Gm > 1) {
+            bool contiguous = true;
+            for (int j = 1; j < Gm; ++j) contiguous &= mem[j] == mem[j - 1] + 1;
+            if (contiguous) {
+                hap_ctx w0 = c->sub[k][0];
+                const int bX = sb ? kX2 : kX, bY = sb ? kY2 : kY;
+                const int64_t rx = cu_nx[mem[Gm - 1] + 1] - cu_nx[mem[0]], ry = cu_ny[mem[Gm - 1] + 1] - cu_ny[mem[0]];
+                if (!(s = ensure(w0, bX, (size_t)rx * d * 4)) && !(s = ensure(w0, bY, (size_t)ry * d * 4))) {
+                    cudaError_t e2 = cudaMemcpyAsync(w0->buf[bX], X_packed + cu_nx[mem[0]] * d, (size_t)rx * d * 4,
+                                                     cudaMemcpyHostToDevice, c->cp_stream[k]);
+                    if (e2 == cudaSuccess)
+                        e2 = cudaMemcpyAsync(w0->buf[bY], Y_packed + cu_ny[mem[0]] * d, (size_t)ry * d * 4,
+                                             cudaMemcpyHostToDevice, c->cp_stream[k]);
+                    if (e2 != cudaSuccess) s = cuda_fail(c, e2, "H2D wave rows");
+                    dXw = static_cast<const float*>(w0->buf[bX]);
+                    dYw = static_cast<const float*>(w0->buf[bY]);
+                }
+                if (s) break;
+            }
+        }
+        int G = 0;
+        for (; G < Gm; ++G) {
+            const int64_t p = mem[G];
+            const int64_t nx = cu_nx[p + 1] - cu_nx[p], ny = cu_ny[p + 1] - cu_ny[p];
             hap_ctx w = c->sub[k][G];
-            const int sb = c->lane_waves[k] & 1;  // staging buffer of this wave
-            if (G == 0 && host_in && c->k1_recorded[k][sb])  // its last reader: the K1 two waves back
-                cudaStreamWaitEvent(c->cp_stream[k], c->ev_k1done[k][sb], 0);
-            s = prepare_pair_cp(w, X_packed + cu_nx[p] * d, nx, Y_packed + cu_ny[p] * d, ny, d, infos + p, ls,
-                                Q[G], host_in ? c->cp_stream[k] : nullptr, sb);
+            const float* Xp = dXw ? dXw + (cu_nx[p] - cu_nx[mem[0]]) * d : X_packed + cu_nx[p] * d;
+            const float* Yp = dYw ? dYw + (cu_ny[p] - cu_ny[mem[0]]) * d : Y_packed + cu_ny[p] * d;
+            s = prepare_pair_cp(w, Xp, nx, Yp, ny, d, infos + p, ls, Q[G],
+                                host_in && !dXw ? c->cp_stream[k] : nullptr, sb);
             if (s) {
                 c->err = "pair " + std::to_string(p) + ": " + w->err;
                 break;
@@ -1305,9 +1346,7 @@ hap_status hap_permtest_batch(hap_ctx c, int64_t P, const float* X_packed, const
             pcs[i] = *cfg;
             pcs[i].stream_id = shared ? cfg->stream_id : cfg->stream_id + (uint32_t)p;
             T[G] = WaveTest{w, infos + p, &pcs[i], counts + p, nullptr, cfg->b_begin, B};
-            ++G;
             ++i;
-            if (!one_block) break;
         }
         const bool multi = G == 1 && ceil_div(std::max<int64_t>(B, 1), R - 1) > block_tiles(cfg, Q[0].n_pad, R);
         WavePlan P;
