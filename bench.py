@@ -699,23 +699,28 @@ def run_batch_workload(args, E, peaks, name):
     Yh = Yd[:ne].cpu().pin_memory()
     sel_e = [p for p in mine if p < Pe]
     hc = torch.zeros((nm, P, 3), dtype=torch.int64).pin_memory()
+
+    def e2e_pass():
+        dcounts.zero_()
+        for mi, mode in enumerate(modes):
+            cfg = hap.make_cfg(HI.PERM_SEED, B, stream_id=(99 * P + mi) & 0xFFFFFFFF)
+            if sel_e:
+                hap.hap_permtest_batch(E.ctx.h, Xh, cnx[: Pe + 1], Yh, cny[: Pe + 1], mode, cfg,
+                                       infos[mi], dcounts[mi], pair_sel=sel_e, stream=E.st)
+        hc.copy_(dcounts, non_blocking=True)
+
+    e2e_pass()  # warm-up: the host-input path's staging buffers and copy streams
     torch.cuda.synchronize()
     E.barrier()
     t0 = time.perf_counter()
-    dcounts.zero_()
-    for mi, mode in enumerate(modes):
-        cfg = hap.make_cfg(HI.PERM_SEED, B, stream_id=(99 * P + mi) & 0xFFFFFFFF)
-        if sel_e:
-            hap.hap_permtest_batch(E.ctx.h, Xh, cnx[: Pe + 1], Yh, cny[: Pe + 1], mode, cfg,
-                                   infos[mi], dcounts[mi], pair_sel=sel_e, stream=E.st)
-    hc.copy_(dcounts, non_blocking=True)
+    e2e_pass()
     torch.cuda.synchronize()
     e2e_s = E.max_over_ranks(time.perf_counter() - t0)
     e2e = {"value": Pe * nm / e2e_s, "unit": UNIT_T,
            "h2d_bytes_per_step": int(Xh.numel() * 4 * 2 * nm),
            "d2h_bytes_per_step": int(nm * P * 24), "steps": 1,
-           "sample": f"the first {Pe} pairs of the batch (one step), inputs in pinned HOST "
-                     "memory",
+           "sample": f"the first {Pe} pairs of the batch (one step after one untimed warm-up "
+                     "pass), inputs in pinned HOST memory",
            "timer": "host wall clock, synchronize on both sides"}
     cfg_out = {"workload": workload_desc(name, 0), "pairs": P, "B": B, "d": 768,
                "global_batch": P * nm, "l2": l2,
