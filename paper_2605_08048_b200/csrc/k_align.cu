@@ -1160,9 +1160,10 @@ __global__ void __launch_bounds__(kS1LeanThreads, 4) k1s_stats_warp(AlignArgs a)
 // KS2: {2 u.x_i, 1/||h_i||} per pooled row (Y rows and identity pairs: coefficient 0).  The
 // CTAs (no more than fit on the GPU at once, so there is no second wave) are split among the
 // pairs in proportion to their X rows; a warp takes X rows in turn (fp64 dot with u staged in
-// shared memory, lane = columns l, l + 32, ... in that order) with 16 column steps of 16
-// bytes in flight per lane (a d = 4096 row in two round trips).
-constexpr int kCoefInFlight = 16;
+// shared memory, lane = columns l, l + 32, ... in that order) with 8 column steps of 16 bytes
+// in flight per lane; 64 registers and (kP3) 2 d_pad doubles of shared memory, u written over
+// xbar, let 3 CTAs share an SM (KS2 36.7 -> 33 us at C3 against 16 steps and 3 d_pad).
+constexpr int kCoefInFlight = 8;
 constexpr int kCoefThreads = 256;
 template <bool kP3>
 __global__ void __launch_bounds__(kCoefThreads) k1s_coef(AlignArgs a, int ctas_per_pair0, int ctas_per_pair1,
@@ -1181,8 +1182,9 @@ __global__ void __launch_bounds__(kCoefThreads) k1s_coef(AlignArgs a, int ctas_p
     pdl_wait();  // KS1 (column sums, 1/||h||, ZeroVector rows) complete and visible
     extern __shared__ __align__(16) uint8_t kc_smem[];
     double* su = reinterpret_cast<double*>(kc_smem);  // [d_pad] axis u
-    double* sxb = su + a.d_pad;                         // [d_pad] xbar (kP3 only)
-    double* syb = sxb + a.d_pad;                        // [d_pad] ybar
+    double* sxb = su;                                   // [d_pad] xbar (kP3 only; the axis u
+                                                        // overwrites it column by column)
+    double* syb = su + a.d_pad;                         // [d_pad] ybar
     __shared__ double red[2 * (kCoefThreads / 32) + 2];
     const int cpp[4] = {ctas_per_pair0, ctas_per_pair1, ctas_per_pair2, ctas_per_pair3};
     int g = 0, c0 = 0;
@@ -1897,17 +1899,17 @@ static cudaError_t launch_align_ks23(AlignArgs a, int sm_count, cudaStream_t st,
     // ticketed P3 is a single short round trip (and whose waves run beside the mask-GEMM)
     const bool p3 = !(lean && a.d <= 1024);
     {  // KS2: CTAs in proportion to the pairs' X rows (kP3: at most what is resident at once)
-        const size_t smem2 = (size_t)a.d_pad * 8 * (p3 ? 3 : 1);  // u (+ xbar, ybar)
+        const size_t smem2 = (size_t)a.d_pad * 8 * (p3 ? 2 : 1);  // u (= xbar) (+ ybar)
         int cpp[kMaxWave] = {0, 0, 0, 0}, total = 0;
         if (p3) {
             static int per_sm[2] = {0, 0};  // resident CTAs per SM for d_pad <= / > 2048
             const int big = a.d_pad > 2048;
             if (per_sm[big] == 0) {
-                e = cudaFuncSetAttribute(k1s_coef<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 8 * 3);
+                e = cudaFuncSetAttribute(k1s_coef<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 8 * 2);
                 if (e == cudaSuccess) e = max_carveout((const void*)k1s_coef<true>);
                 if (e == cudaSuccess)
                     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[big], k1s_coef<true>, kCoefThreads,
-                                                                      (big ? 4096 : 2048) * 8 * 3);
+                                                                      (big ? 4096 : 2048) * 8 * 2);
                 if (e != cudaSuccess) return e;
                 per_sm[big] = std::max(per_sm[big], 1);
             }
