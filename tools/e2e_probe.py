@@ -8,6 +8,7 @@ import sys
 import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
 import torch
 
 import hap_inputs as HI
@@ -37,4 +38,23 @@ Yd = [y.cuda() for y in Yh]
 torch.cuda.synchronize()
 out["c3_h2d_ms_2pairs"] = (time.perf_counter() - t0) * 1e3
 out["pinned"] = [bool(x.is_pinned()) for x in Xh + Yh]
+# C2 batch: 100 tests (n = 1000 + 1000, d = 768) per call from pinned host memory, 1 warm-up
+# call then 5 timed calls enqueued back to back
+pairs = [HI.config_pair("C2", rep=r) for r in range(4)]
+T = 100
+Xp = np.concatenate([pairs[i % 4][0] for i in range(T)])
+Yp = np.concatenate([pairs[i % 4][1] for i in range(T)])
+cu = np.arange(T + 1, dtype=np.int64) * pairs[0][0].shape[0]
+Xh2, Yh2 = torch.from_numpy(Xp).pin_memory(), torch.from_numpy(Yp).pin_memory()
+infos2 = torch.zeros((T, hap.INFO_BYTES), dtype=torch.uint8, device="cuda")
+cnt2 = torch.zeros((T, 3), dtype=torch.int64, device="cuda")
+Bc2 = 10000
+for k in range(6):
+    if k == 1:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+    cfg = hap.make_cfg(HI.PERM_SEED, Bc2, stream_id=k * T)
+    hap.hap_permtest_batch(ctx.h, Xh2, cu, Yh2, cu, 0, cfg, infos2, cnt2)
+torch.cuda.synchronize()
+out["c2_e2e_perms_per_s"] = 5 * T * Bc2 / (time.perf_counter() - t0)
 print(json.dumps(out), flush=True)
